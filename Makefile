@@ -1,0 +1,36 @@
+# Builds the sm_100a kernel layer + C++ host engine into one in-tree shared
+# library (paper_2110_03888_b200/libp2r.so) and the reference oracle.
+NVCC    ?= nvcc
+CXX     ?= g++
+ARCH    := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall \
+           -Iinclude -Ipaper_2110_03888_b200/csrc --expt-relaxed-constexpr
+PKG     := paper_2110_03888_b200
+CSRC    := $(PKG)/csrc
+BUILD   := build
+CU_SRCS := $(wildcard $(CSRC)/*.cu)
+CPP_SRCS:= $(wildcard $(CSRC)/engine/*.cpp)
+CU_OBJS := $(patsubst $(CSRC)/%.cu,$(BUILD)/%.o,$(CU_SRCS))
+CPP_OBJS:= $(patsubst $(CSRC)/engine/%.cpp,$(BUILD)/engine/%.o,$(CPP_SRCS))
+LIB     := $(PKG)/libp2r.so
+
+all: $(LIB)
+
+$(BUILD)/%.o: $(CSRC)/%.cu $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h) include/p2r_cuda.h
+	@mkdir -p $(dir $@)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(BUILD)/engine/%.o: $(CSRC)/engine/%.cpp $(wildcard include/p2r/*.hpp) $(wildcard include/*.h)
+	@mkdir -p $(dir $@)
+	$(CXX) -std=c++20 -O2 -fPIC -Wall -Iinclude -I/usr/local/cuda/include -c $< -o $@
+
+$(LIB): $(CU_OBJS) $(CPP_OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $^ -cudart static
+
+oracle:
+	bash oracle/build_ref.sh
+
+clean:
+	rm -rf $(BUILD) $(LIB)
+
+.PHONY: all clean oracle

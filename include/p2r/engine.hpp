@@ -1,0 +1,237 @@
+// C++ host engine: the reference's layer/step API (model.hpp, optim.hpp,
+// tensor.hpp of /root/reference/proj/core) re-implemented over the sm_100a
+// kernel layer (p2r_cuda.h). Same class / method names and error behaviour;
+// tensors live on the device.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <functional>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace p2r {
+
+// ---------------------------------------------------------------- configs
+struct MoEConfig {  // model.hpp:13-22
+  int n_experts = 0;
+  int n_prototypes = 1;
+  int n_shards = 1;
+  float capacity_factor = 1.25f;
+  bool enabled() const { return n_experts > 0; }
+  int group_size() const { return n_experts / n_prototypes; }
+  void validate() const;
+};
+
+struct ModelConfig {  // model.hpp:27-41
+  int d_model = 128;
+  int d_ff = 512;
+  int n_layers_graph = 8;
+  int n_layers_params = 8;
+  int n_heads = 4;
+  int vocab_size = 260;
+  int seq_len = 64;
+  MoEConfig moe;
+  bool shared() const { return n_layers_params == 1 && n_layers_graph > 1; }
+  void validate() const;
+  ModelConfig as_shared() const;
+  ModelConfig as_unshared() const;
+};
+
+struct ParamCounts {
+  std::int64_t embedding_params = 0;
+  std::int64_t per_layer_params = 0;
+  std::int64_t total_params = 0;
+};
+ParamCounts count_params(const ModelConfig& config);
+
+enum class AttentionMode { Causal, Full };
+
+// Reference-compatible per-tensor init (model.cpp:11-36).
+std::uint64_t init_mix_seed(std::uint64_t seed, const std::string& name);
+void init_normal_host(float* out, std::size_t n, std::uint64_t seed, const std::string& name,
+                      float stddev = 0.02f);
+
+// ---------------------------------------------------------------- device memory
+struct DevBuf {
+  void* p = nullptr;
+  std::size_t bytes = 0;
+  DevBuf() = default;
+  explicit DevBuf(std::size_t n);
+  ~DevBuf();
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept;
+  template <typename T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+// Device activation handle (fp32, row-major [rows, cols]); `grad` is the
+// gradient buffer the backward closures read/write.
+struct Tensor {
+  int rows = 0, cols = 0;
+  float* data = nullptr;
+  float* grad = nullptr;
+  void* grad16 = nullptr;  // bf16 shadow of grad (GEMM operand)
+  bool defined() const { return data != nullptr; }
+};
+
+// tensor.hpp:70-82: closures replayed once in reverse order.
+class GradTape {
+ public:
+  void record(std::function<void()> fn) { entries_.push_back(std::move(fn)); }
+  void backward() {
+    for (auto it = entries_.rbegin(); it != entries_.rend(); ++it) (*it)();
+  }
+  // The fused cross-entropy already produced dlogits for dL = 1, which is
+  // exactly what backward_scalar seeds (tensor.cpp:110-114).
+  void backward_scalar(Tensor& /*loss*/) { backward(); }
+  void clear() { entries_.clear(); }
+  std::size_t size() const { return entries_.size(); }
+
+ private:
+  std::vector<std::function<void()>> entries_;
+};
+
+// One parameter as the reference names it, viewed inside a granule buffer.
+struct ParamView {
+  std::string name;
+  int granule;        // -1 = embeddings granule, else owned layer index
+  long long off;      // element offset in the granule
+  int rows, cols, ld; // 2-D view (vectors: rows = 1)
+  std::vector<int> shape;
+};
+
+// Element layout of one granule (a layer, or the embeddings) — all of its
+// parameters contiguous so delink / offload / AdamW move it as one block.
+struct GranuleLayout {
+  struct Seg {
+    long long off, len;
+    bool decay;
+  };
+  std::vector<Seg> segs;
+  long long numel = 0;
+  // layer roles
+  long long ln1_g = 0, ln1_b = 0, wqkv = 0, wo = 0, ln2_g = 0, ln2_b = 0;
+  long long w1 = 0, b1 = 0, w2 = 0, b2 = 0, gate = 0;
+  // embedding roles
+  long long tok = 0, pos = 0, fin_g = 0, fin_b = 0;
+  long long add(long long n, bool decay);
+};
+
+struct Acts;  // per-shape activation / workspace buffers
+
+class Model {
+ public:
+  Model(ModelConfig config, std::uint64_t seed);
+  ~Model();
+  Model(const Model&) = delete;
+  Model& operator=(const Model&) = delete;
+
+  const ModelConfig& config() const { return cfg_; }
+  int n_graph_layers() const { return cfg_.n_layers_graph; }
+  int n_owned_layers() const { return n_owned_; }
+  int owned_index_of_graph_layer(int g) const { return cfg_.shared() || n_owned_ == 1 ? 0 : g; }
+
+  // segmented API (model.hpp:101-106); token / target / mask pointers are device arrays
+  Tensor embed_forward(GradTape* tape, const int* d_tokens, int batch, int seq);
+  Tensor block_forward(GradTape* tape, int graph_layer, const Tensor& x, int batch,
+                       AttentionMode mode);
+  Tensor head_forward(GradTape* tape, const Tensor& x);
+  // fused softmax_cross_entropy(mask, denom) (tensor.cpp:670-723); returns a
+  // 1-element device tensor
+  Tensor softmax_cross_entropy(GradTape* tape, const Tensor& logits, const int* d_targets,
+                               const std::uint8_t* d_mask, double denom);
+
+  // whole micro-step (controller CS-1)
+  void train_step_device(const int* d_tokens, const int* d_targets, const std::uint8_t* d_mask,
+                         int batch, int seq, double denom, AttentionMode mode, bool zero,
+                         float* loss_dev);
+  float train_step_host(const int* tokens, const int* targets, const std::uint8_t* mask,
+                        int batch, int seq, double denom, AttentionMode mode, bool zero);
+  void forward_host(const int* tokens, int batch, int seq, AttentionMode mode, float* logits_out);
+
+  void zero_grads();
+  void flush_shared_layer_grads() {}  // accumulated in place by the dW epilogues
+  std::int64_t scratch_grad_bytes() const { return 0; }
+  std::int64_t grad_bytes() const;
+
+  // parameters (for_each_param order)
+  const std::vector<ParamView>& params() const { return views_; }
+  void get_param(int i, float* host) const;
+  void set_param(int i, const float* host);
+  void get_grad(int i, float* host) const;
+  void get_moment(int i, int which, float* host) const;
+
+  // optimizer state (AdamW moments live beside the parameters, same layout)
+  void adamw_attach(float b1, float b2, float eps, float wd);
+  void adamw_step(float lr);
+  std::int64_t step_count() const { return step_count_; }
+  void set_step_count(std::int64_t t) { step_count_ = t; }
+  std::int64_t state_bytes() const;
+  bool has_optimizer() const { return has_opt_; }
+
+  std::unique_ptr<Model> delinked() const;
+
+  cudaStream_t stream() const { return stream_; }
+  void routing_host(int g, int* selected, std::uint8_t* survived, int* raw_load, int* capacity,
+                    int* dropped) const;
+
+ private:
+  struct NoInit {};
+  Model(ModelConfig config, NoInit);
+  void build_layout();
+  void allocate();
+  void init_params(std::uint64_t seed);
+  void refresh_bf16();
+  void ensure_acts(int batch, int seq);
+  float* lp(int owned, long long off) const;
+  float* lg(int owned, long long off) const;
+  void* lp16(int owned, long long off) const;
+  const float* ep(long long off) const { return emb_p_.as<float>() + off; }
+  float* eg(long long off) const { return emb_g_.as<float>() + off; }
+  void* ep16(long long off) const { return emb_p16_.as<std::uint16_t>() + off; }
+  void block_backward(int g, AttentionMode mode);
+  void gemm(int m, int n, int k, const void* a, int lda, bool a_mn, const void* b, int ldb,
+            bool b_mn, int epi, void* c, int ldc, void* c2 = nullptr, int ldc2 = 0,
+            const float* bias = nullptr, const void* aux = nullptr, int ldaux = 0,
+            int group_mode = 0, int groups = 0, int seg_rows = 0, const int* counts = nullptr,
+            int split_k = 1);
+
+  ModelConfig cfg_;
+  int n_owned_ = 0;
+  GranuleLayout layer_, emb_;
+  long long layer_stride_ = 0;  // elements between owned layer granules (aligned)
+  std::vector<ParamView> views_;
+  DevBuf emb_p_, emb_g_, emb_p16_, emb_m_, emb_v_;
+  DevBuf lay_p_, lay_g_, lay_p16_, lay_m_, lay_v_;
+  bool has_opt_ = false;
+  float b1_ = 0.9f, b2_ = 0.999f, eps_ = 1e-8f, wd_ = 0.01f;
+  std::int64_t step_count_ = 0;
+  cudaStream_t stream_ = nullptr;
+  std::unique_ptr<Acts> acts_;
+  DevBuf splitk_ws_;
+  DevBuf dev_in_;   // tokens / targets / mask staging
+  void* pinned_ = nullptr;
+  std::size_t pinned_bytes_ = 0;
+};
+
+// moe_dispatch on host logits via the routing kernel (bit-exact, model.cpp:294-332)
+struct HostRouting {
+  std::vector<int> selected;
+  std::vector<std::uint8_t> survived;
+  std::vector<int> raw_load, offsets, rows, slots;
+  int capacity = 0, dropped = 0;
+};
+HostRouting moe_dispatch_host(const float* logits, int T, const MoEConfig& moe);
+
+float lr_at(float peak, double warmup_ratio, std::int64_t total, std::int64_t step);
+
+void cuda_check(cudaError_t e, const char* what);
+void p2r_check(int status, const char* what);
+
+}  // namespace p2r

@@ -34,6 +34,8 @@ typedef enum {
   P2R_ENCCL = 6
 } p2r_status;
 
+#define P2R_MAX_ADAM_SEGS 16
+
 const char* p2r_last_error(void);
 const char* p2r_version(void);
 /* Number of p2r kernels launched by this process so far (all entry points). */
@@ -87,6 +89,95 @@ p2r_status p2r_gemm(const p2r_gemm_args* args, void* stream);
 size_t p2r_gemm_workspace_bytes(const p2r_gemm_args* args);
 /* Supply caller-owned scratch (device) the library may use for split-K. */
 p2r_status p2r_set_workspace(void* ptr, size_t bytes);
+
+/* ------------------------------------------------------------------------ */
+/* Fused attention (replaces masked_attention + split/merge_heads,           */
+/* tensor.cpp:400-545). qkv: bf16 [B*S, 3d] (q | k | v, heads contiguous);   */
+/* o: bf16 [B*S, d]; lse: fp32 [B, H, S]. hd = d/H in {64, 128}.             */
+/* ------------------------------------------------------------------------ */
+p2r_status p2r_attention_fwd(const void* qkv, void* o, float* lse, int B, int H, int S, int d,
+                             int causal, void* stream);
+/* dsum_ws: fp32 [B, H, S] scratch. dqkv: bf16 [B*S, 3d] (overwritten). */
+p2r_status p2r_attention_bwd(const void* qkv, const void* o, const float* lse, const void* dout,
+                             float* dsum_ws, void* dqkv, int B, int H, int S, int d, int causal,
+                             void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* LayerNorm (tensor.cpp:265-336). d in {128,256,512,1024,2048}.             */
+/* ------------------------------------------------------------------------ */
+p2r_status p2r_layernorm_fwd(const float* x, const float* gain, const float* bias, int rows, int d,
+                             float eps, void* y_bf16, float* y_f32, float* mean, float* rstd,
+                             void* stream);
+size_t p2r_layernorm_bwd_workspace(int rows, int d);
+/* dx = resid + LN'(dy); ggain/gbias (+=) may be NULL. */
+p2r_status p2r_layernorm_bwd(const float* dy, const float* x, const float* mean, const float* rstd,
+                             const float* gain, const float* resid, int rows, int d, float* dx,
+                             void* dx_bf16, float* ggain, float* gbias, float* partial_ws,
+                             void* stream);
+
+/* Embeddings (embedding_lookup x2 + add, model.cpp:229-241; tensor.cpp:338-368). */
+p2r_status p2r_embed_fwd(const int* ids, const float* tok, const float* pos, int T, int S, int d,
+                         float* x, void* stream);
+p2r_status p2r_embed_bwd(const int* ids, const float* dx, int B, int S, int d, int V, float* dtok,
+                         float* dpos, void* stream);
+
+/* Softmax cross-entropy fwd+bwd (tensor.cpp:670-723). logits fp32 [rows][ld];
+ * dlogits bf16 [rows][ldg] = (p - onehot) * loss_grad / denom, zero on masked
+ * rows and pad columns; *loss (device) = sum(-log p_t) / denom. */
+size_t p2r_cross_entropy_workspace(int rows);
+p2r_status p2r_cross_entropy(const float* logits, int rows, int V, int ld, const int* targets,
+                             const uint8_t* mask, double denom, float loss_grad,
+                             void* dlogits_bf16, int ldg, float* loss, double* loss_sum,
+                             double* partial_ws, void* stream);
+
+/* AdamW over one granule (optim.cpp:41-63), bit-exact given equal grads.
+ * Segments give (offset, length, decay) inside the granule; bc1/bc2 are the
+ * host-computed float bias corrections 1 - powf(beta, t). */
+p2r_status p2r_adamw_step(float* p, const float* g, float* m, float* v, void* p_bf16,
+                          const long long* seg_off, const long long* seg_len,
+                          const int* seg_decay, int nseg, float b1, float b2, float eps, float wd,
+                          float lr, float bc1, float bc2, void* stream);
+p2r_status p2r_cast_bf16(const float* src, void* dst, long long n, void* stream);
+
+/* Delink broadcast (model.cpp:358-377): dst + l*dst_stride_bytes = src, l < L. */
+p2r_status p2r_delink_broadcast(const void* src, void* dst, size_t bytes, size_t dst_stride_bytes,
+                                int L, void* stream);
+
+/* Bias gradient column sums (add_bias backward, tensor.cpp:227-231). */
+size_t p2r_colsum_workspace(int rows, int n, int groups);
+p2r_status p2r_bias_grad(const void* x, int dtype, int ld, int rows, int n, int groups,
+                         int seg_rows, const int* counts, float* out, long long out_group_stride,
+                         float* ws, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* MoE (model.cpp:248-332; tensor.cpp:370-398, 547-664).                     */
+/* ------------------------------------------------------------------------ */
+int p2r_moe_capacity(float capacity_factor, int n_tokens, int n_experts, int n_prototypes);
+p2r_status p2r_moe_gate_logits(const float* b, const float* gate, int T, int d, int E,
+                               float* logits, void* stream);
+/* Bit-exact moe_dispatch. pos[t*k+g] = slot row inside the expert segment or -1
+ * (dropped); rows_pad/slots_pad: [E*seg_rows] token / group of each admitted
+ * row (expert-major, token order); counts[e] = admitted rows. */
+p2r_status p2r_moe_route(const float* logits, int T, int E, int k, int capacity, int seg_rows,
+                         int* selected, uint8_t* survived, int* pos, int* raw_load, int* counts,
+                         int* rows_pad, int* slots_pad, int* dropped, void* stream);
+p2r_status p2r_moe_combine_weights(const float* logits, int T, int E, int k, const int* selected,
+                                   const uint8_t* survived, float* w, void* stream);
+p2r_status p2r_moe_dispatch(const void* src, int src_dtype, int d, int E, int seg_rows,
+                            const int* rows_pad, const int* slots_pad, const int* counts,
+                            const float* w, int k, void* xe_bf16, void* stream);
+p2r_status p2r_moe_combine(const float* ye, int T, int d, int k, int seg_rows, const int* selected,
+                           const int* pos, const float* w, const float* resid, float* out,
+                           void* stream);
+p2r_status p2r_moe_combine_bwd_weights(const float* dout, const float* ye, int T, int d, int k,
+                                       int seg_rows, const int* selected, const int* pos,
+                                       float* dw, void* stream);
+p2r_status p2r_moe_gate_bwd(const float* b, const float* w, const float* gw, int T, int d, int E,
+                            int k, const int* selected, const uint8_t* survived, float* glogits,
+                            float* dgate, void* stream);
+p2r_status p2r_moe_dispatch_bwd(const float* dxe, int T, int d, int k, int seg_rows,
+                                const int* selected, const int* pos, const float* glogits,
+                                const float* gate, int E, float* db, int accumulate, void* stream);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,103 @@
+/*
+ * p2r_engine.h — C-ABI of the step-level host engine (C++ above the kernel
+ * layer of p2r_cuda.h). This is the drop-in boundary a non-C++ caller binds
+ * (ctypes / cgo / JNI): it exposes exactly the reference's Model / AdamW /
+ * delink / routing surface (/root/reference/proj/core/include/p2r/model.hpp,
+ * optim.hpp) with host buffers in and out, plus a device-pointer fast path.
+ *
+ * Parameter names and order follow Model::for_each_param (model.cpp:188-198):
+ * "embed.tok", "embed.pos", "final_norm.gain", "final_norm.bias",
+ * "layer.<i>.ln1.gain", ..., "layer.<i>.moe.expert.<e>.b2".
+ */
+#ifndef P2R_ENGINE_H_
+#define P2R_ENGINE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "p2r_cuda.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ModelConfig + MoEConfig (model.hpp:13-41), same field meaning and defaults. */
+typedef struct {
+  int d_model, d_ff, n_layers_graph, n_layers_params, n_heads, vocab_size, seq_len;
+  int n_experts, n_prototypes, n_shards;
+  float capacity_factor;
+} p2r_model_config;
+
+typedef struct p2r_model p2r_model;
+
+/* count_params (model.cpp:73-89): out3 = {embedding, per_layer, total}. */
+p2r_status p2r_count_params(const p2r_model_config* cfg, int64_t* out3);
+/* Model(config, seed) (model.cpp:123-179): identical std::mt19937_64 /
+ * std::normal_distribution<float>(0, 0.02) init per named tensor. */
+p2r_status p2r_model_create(const p2r_model_config* cfg, uint64_t seed, p2r_model** out);
+p2r_status p2r_model_destroy(p2r_model* m);
+int p2r_model_num_params(const p2r_model* m);
+p2r_status p2r_model_param_info(const p2r_model* m, int i, char* name128, int* ndim, int* shape4,
+                                int64_t* numel);
+/* Host <-> device copies of one named parameter / its gradient. */
+p2r_status p2r_model_get_param(const p2r_model* m, int i, float* host_out);
+p2r_status p2r_model_set_param(p2r_model* m, int i, const float* host_in);
+p2r_status p2r_model_get_grad(const p2r_model* m, int i, float* host_out);
+
+/* Model::forward (model.cpp:287-292): logits [batch*seq, vocab] to host. */
+p2r_status p2r_model_forward(p2r_model* m, const int* tokens, int batch, int seq, int causal,
+                             float* logits_out);
+
+/* One micro-step of the absent controller (CS-1):
+ * zero_grads (if zero) -> embed -> L blocks -> head -> masked CE(denom) ->
+ * backward with shared-layer grads accumulated in place. tokens/targets/mask
+ * are HOST arrays (copied in on the model's stream); *loss_out is the loss.
+ * Error behaviour matches the reference (out-of-range ids / targets ->
+ * P2R_ERANGE with the reference's message). */
+p2r_status p2r_model_train_step(p2r_model* m, const int* tokens, const int* targets,
+                                const uint8_t* mask, int batch, int seq, double denom, int causal,
+                                int zero, float* loss_out);
+/* Same, inputs already resident on the device; the loss stays on the device
+ * (loss_dev, may be NULL) so steps can be enqueued / graph-captured. */
+p2r_status p2r_model_train_step_device(p2r_model* m, const int* d_tokens, const int* d_targets,
+                                       const uint8_t* d_mask, int batch, int seq, double denom,
+                                       int causal, int zero, float* loss_dev);
+
+/* AdamW (optim.hpp:29-54). */
+p2r_status p2r_model_adamw_attach(p2r_model* m, float b1, float b2, float eps, float wd);
+p2r_status p2r_model_adamw_step(p2r_model* m, float lr);
+int64_t p2r_model_adamw_step_count(const p2r_model* m);
+p2r_status p2r_model_adamw_set_step_count(p2r_model* m, int64_t t);
+/* which: 0 = m, 1 = v */
+p2r_status p2r_model_get_moment(const p2r_model* m, int i, int which, float* host_out);
+int64_t p2r_model_state_bytes(const p2r_model* m);
+/* Gradient bytes held on the device (one layer in Pseudo mode: no scratch copy). */
+int64_t p2r_model_grad_bytes(const p2r_model* m);
+int64_t p2r_model_scratch_grad_bytes(const p2r_model* m);
+
+/* Model::delinked (model.cpp:358-377) + optimizer-moment copy (SPEC.md:279,
+ * :312) as one device broadcast; logic error on a non-shared model. */
+p2r_status p2r_model_delinked(const p2r_model* m, p2r_model** out);
+
+/* Raw device stream the model enqueues on (cudaStream_t). */
+void* p2r_model_stream(p2r_model* m);
+/* Last routing of graph layer g (MoE): host copies of moe_dispatch outputs. */
+p2r_status p2r_model_routing(const p2r_model* m, int g, int* selected, uint8_t* survived,
+                             int* raw_load, int* capacity, int* dropped);
+
+/* moe_dispatch (model.cpp:294-332) on host logits [T, E]: same outputs as the
+ * reference's Routing, expert_rows/slots flattened CSR (offsets[E+1]). */
+p2r_status p2r_moe_dispatch_host(const float* logits, int T, int E, int k, float cf, int* selected,
+                                 uint8_t* survived, int* raw_load, int* offsets, int* rows,
+                                 int* slots, int* capacity, int* dropped);
+
+/* init_normal (model.cpp:28-36) on the host: the exact values Model() uploads. */
+void p2r_init_normal_host(uint64_t seed, const char* name, int64_t n, float* out);
+
+/* LrSchedule::cosine(peak, warmup_ratio, total).at(step) (optim.cpp:8-24). */
+float p2r_lr_at(float peak, double warmup_ratio, int64_t total, int64_t step);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* P2R_ENGINE_H_ */

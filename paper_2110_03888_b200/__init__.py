@@ -1,0 +1,13 @@
+"""B200-native (sm_100a) training-step hot path of arXiv 2110.03888 (Pseudo-to-Real).
+
+The product is libp2r.so: hand-written tcgen05/TMA GEMMs, fused attention,
+LayerNorm / CE / AdamW / delink / MoE routing kernels and a C++ host engine
+that keeps the reference's Model / AdamW / moe_dispatch API. This package is
+a thin ctypes mirror of that API (see model.py); it never computes on the CPU.
+"""
+from ._lib import (P2RError, P2RInvalidArgument, P2RLogicError, P2ROutOfRange, launch_count,
+                   lib)
+from .model import Config, Model, Routing, count_params, lr_at, moe_dispatch
+
+__all__ = ["Config", "Model", "Routing", "count_params", "lr_at", "moe_dispatch", "lib",
+           "launch_count", "P2RError", "P2RInvalidArgument", "P2ROutOfRange", "P2RLogicError"]

@@ -1,0 +1,196 @@
+// extern "C" wrappers of the host engine (include/p2r_engine.h). No exception
+// crosses this boundary: each maps to a p2r_status with the reference's message.
+#include <cstring>
+#include <memory>
+#include <new>
+
+#include "../p2r_internal.h"
+#include "p2r/engine.hpp"
+#include "p2r_engine.h"
+
+struct p2r_model {
+  std::unique_ptr<p2r::Model> m;
+};
+
+namespace {
+
+p2r::ModelConfig to_cfg(const p2r_model_config* c) {
+  p2r::ModelConfig m;
+  m.d_model = c->d_model;
+  m.d_ff = c->d_ff;
+  m.n_layers_graph = c->n_layers_graph;
+  m.n_layers_params = c->n_layers_params;
+  m.n_heads = c->n_heads;
+  m.vocab_size = c->vocab_size;
+  m.seq_len = c->seq_len;
+  m.moe.n_experts = c->n_experts;
+  m.moe.n_prototypes = c->n_prototypes;
+  m.moe.n_shards = c->n_shards;
+  m.moe.capacity_factor = c->capacity_factor;
+  return m;
+}
+
+template <typename F>
+p2r_status guard(F&& f) {
+  try {
+    f();
+    return P2R_OK;
+  } catch (const std::invalid_argument& e) {
+    return p2r::set_error(P2R_EINVAL, e.what());
+  } catch (const std::out_of_range& e) {
+    return p2r::set_error(P2R_ERANGE, e.what());
+  } catch (const std::logic_error& e) {
+    return p2r::set_error(P2R_ELOGIC, e.what());
+  } catch (const std::bad_alloc&) {
+    return p2r::set_error(P2R_ERUNTIME, "out of memory");
+  } catch (const std::exception& e) {
+    return p2r::set_error(P2R_ERUNTIME, e.what());
+  }
+}
+
+p2r::AttentionMode mode_of(int causal) { return causal ? p2r::AttentionMode::Causal : p2r::AttentionMode::Full; }
+
+}  // namespace
+
+extern "C" {
+
+p2r_status p2r_count_params(const p2r_model_config* cfg, int64_t* out3) {
+  return guard([&] {
+    p2r::ParamCounts p = p2r::count_params(to_cfg(cfg));
+    out3[0] = p.embedding_params;
+    out3[1] = p.per_layer_params;
+    out3[2] = p.total_params;
+  });
+}
+
+p2r_status p2r_model_create(const p2r_model_config* cfg, uint64_t seed, p2r_model** out) {
+  return guard([&] {
+    auto h = std::make_unique<p2r_model>();
+    h->m = std::make_unique<p2r::Model>(to_cfg(cfg), seed);
+    *out = h.release();
+  });
+}
+
+p2r_status p2r_model_destroy(p2r_model* m) {
+  delete m;
+  return P2R_OK;
+}
+
+int p2r_model_num_params(const p2r_model* m) { return static_cast<int>(m->m->params().size()); }
+
+p2r_status p2r_model_param_info(const p2r_model* m, int i, char* name128, int* ndim, int* shape4,
+                                int64_t* numel) {
+  return guard([&] {
+    const p2r::ParamView& v = m->m->params().at(static_cast<std::size_t>(i));
+    std::strncpy(name128, v.name.c_str(), 127);
+    name128[127] = 0;
+    *ndim = static_cast<int>(v.shape.size());
+    int64_t n = 1;
+    for (std::size_t d = 0; d < v.shape.size() && d < 4; ++d) {
+      shape4[d] = v.shape[d];
+      n *= v.shape[d];
+    }
+    *numel = n;
+  });
+}
+
+p2r_status p2r_model_get_param(const p2r_model* m, int i, float* host_out) {
+  return guard([&] { m->m->get_param(i, host_out); });
+}
+p2r_status p2r_model_set_param(p2r_model* m, int i, const float* host_in) {
+  return guard([&] { m->m->set_param(i, host_in); });
+}
+p2r_status p2r_model_get_grad(const p2r_model* m, int i, float* host_out) {
+  return guard([&] { m->m->get_grad(i, host_out); });
+}
+
+p2r_status p2r_model_forward(p2r_model* m, const int* tokens, int batch, int seq, int causal, float* logits_out) {
+  return guard([&] { m->m->forward_host(tokens, batch, seq, mode_of(causal), logits_out); });
+}
+
+p2r_status p2r_model_train_step(p2r_model* m, const int* tokens, const int* targets, const uint8_t* mask,
+                                int batch, int seq, double denom, int causal, int zero, float* loss_out) {
+  return guard([&] {
+    const float l = m->m->train_step_host(tokens, targets, mask, batch, seq, denom, mode_of(causal), zero != 0);
+    if (loss_out) *loss_out = l;
+  });
+}
+
+p2r_status p2r_model_train_step_device(p2r_model* m, const int* d_tokens, const int* d_targets,
+                                       const uint8_t* d_mask, int batch, int seq, double denom, int causal,
+                                       int zero, float* loss_dev) {
+  return guard([&] {
+    if (denom <= 0.0) throw std::invalid_argument("softmax_cross_entropy: denominator must be > 0");
+    m->m->train_step_device(d_tokens, d_targets, d_mask, batch, seq, denom, mode_of(causal), zero != 0, loss_dev);
+  });
+}
+
+p2r_status p2r_model_adamw_attach(p2r_model* m, float b1, float b2, float eps, float wd) {
+  return guard([&] { m->m->adamw_attach(b1, b2, eps, wd); });
+}
+p2r_status p2r_model_adamw_step(p2r_model* m, float lr) {
+  return guard([&] { m->m->adamw_step(lr); });
+}
+int64_t p2r_model_adamw_step_count(const p2r_model* m) { return m->m->step_count(); }
+p2r_status p2r_model_adamw_set_step_count(p2r_model* m, int64_t t) {
+  m->m->set_step_count(t);
+  return P2R_OK;
+}
+p2r_status p2r_model_get_moment(const p2r_model* m, int i, int which, float* host_out) {
+  return guard([&] { m->m->get_moment(i, which, host_out); });
+}
+int64_t p2r_model_state_bytes(const p2r_model* m) { return m->m->state_bytes(); }
+int64_t p2r_model_grad_bytes(const p2r_model* m) { return m->m->grad_bytes(); }
+int64_t p2r_model_scratch_grad_bytes(const p2r_model* m) { return m->m->scratch_grad_bytes(); }
+
+p2r_status p2r_model_delinked(const p2r_model* m, p2r_model** out) {
+  return guard([&] {
+    auto h = std::make_unique<p2r_model>();
+    h->m = m->m->delinked();
+    *out = h.release();
+  });
+}
+
+void* p2r_model_stream(p2r_model* m) { return m->m->stream(); }
+
+p2r_status p2r_model_routing(const p2r_model* m, int g, int* selected, uint8_t* survived, int* raw_load,
+                             int* capacity, int* dropped) {
+  return guard([&] { m->m->routing_host(g, selected, survived, raw_load, capacity, dropped); });
+}
+
+p2r_status p2r_moe_dispatch_host(const float* logits, int T, int E, int k, float cf, int* selected,
+                                 uint8_t* survived, int* raw_load, int* offsets, int* rows, int* slots,
+                                 int* capacity, int* dropped) {
+  return guard([&] {
+    p2r::MoEConfig moe;
+    moe.n_experts = E;
+    moe.n_prototypes = k;
+    moe.capacity_factor = cf;
+    p2r::HostRouting r = p2r::moe_dispatch_host(logits, T, moe);
+    std::memcpy(selected, r.selected.data(), r.selected.size() * 4);
+    std::memcpy(survived, r.survived.data(), r.survived.size());
+    std::memcpy(raw_load, r.raw_load.data(), r.raw_load.size() * 4);
+    std::memcpy(offsets, r.offsets.data(), r.offsets.size() * 4);
+    if (!r.rows.empty()) {
+      std::memcpy(rows, r.rows.data(), r.rows.size() * 4);
+      std::memcpy(slots, r.slots.data(), r.slots.size() * 4);
+    }
+    *capacity = r.capacity;
+    *dropped = r.dropped;
+  });
+}
+
+void p2r_init_normal_host(uint64_t seed, const char* name, int64_t n, float* out) {
+  p2r::init_normal_host(out, static_cast<std::size_t>(n), seed, name);
+}
+
+float p2r_lr_at(float peak, double warmup_ratio, int64_t total, int64_t step) {
+  try {
+    return p2r::lr_at(peak, warmup_ratio, total, step);
+  } catch (const std::exception& e) {
+    p2r::set_error(P2R_EINVAL, e.what());
+    return -1.0f;
+  }
+}
+
+}  // extern "C"

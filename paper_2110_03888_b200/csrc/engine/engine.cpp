@@ -1,0 +1,903 @@
+// Host engine: Model / GradTape / AdamW / delink over the sm_100a kernel layer.
+//
+// Mirrors /root/reference/proj/core/src/model.cpp and optim.cpp (and the
+// absent controller's per-micro-batch step) with identical
+// names, parameter naming/order, init RNG and error messages. Differences are
+// the B200 design: parameters of a layer live in one contiguous granule
+// (fp32 master + grad + AdamW m/v + a bf16 shadow for the tensor cores),
+// Q/K/V are stored fused as one [d, 3d] matrix (views keep the reference
+// names), shared-layer gradients are accumulated in place by the dW GEMM
+// epilogues (no scratch buffer + flush), and the forward/backward of a block
+// is a handful of fused kernels instead of ~40 primitive closures.
+#include "p2r/engine.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <random>
+#include <string>
+
+#include "p2r_cuda.h"
+
+namespace p2r {
+
+// ---------------------------------------------------------------- errors
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void p2r_check(int st, const char* what) {
+  if (st == P2R_OK) return;
+  const std::string msg = p2r_last_error();
+  switch (st) {
+    case P2R_EINVAL: throw std::invalid_argument(msg);
+    case P2R_ERANGE: throw std::out_of_range(msg);
+    case P2R_ELOGIC: throw std::logic_error(msg);
+    default: throw std::runtime_error(std::string(what) + ": " + msg);
+  }
+}
+
+// ---------------------------------------------------------------- DevBuf
+DevBuf::DevBuf(std::size_t n) : bytes(n) {
+  if (n) cuda_check(cudaMalloc(&p, n), "cudaMalloc");
+}
+DevBuf::~DevBuf() {
+  if (p) cudaFree(p);
+}
+DevBuf& DevBuf::operator=(DevBuf&& o) noexcept {
+  if (this != &o) {
+    if (p) cudaFree(p);
+    p = o.p;
+    bytes = o.bytes;
+    o.p = nullptr;
+    o.bytes = 0;
+  }
+  return *this;
+}
+
+// ---------------------------------------------------------------- configs (model.cpp:40-89)
+void MoEConfig::validate() const {
+  if (!enabled()) return;
+  if (n_prototypes <= 0 || n_experts % n_prototypes != 0)
+    throw std::invalid_argument("moe config: n_experts must be divisible by n_prototypes");
+  if (n_shards <= 0 || n_experts % n_shards != 0)
+    throw std::invalid_argument("moe config: n_experts must be divisible by n_shards");
+  if (!(capacity_factor > 0.0f))
+    throw std::invalid_argument("moe config: capacity_factor must be positive");
+}
+
+void ModelConfig::validate() const {
+  if (d_model <= 0 || d_ff <= 0 || n_layers_graph <= 0 || n_heads <= 0 || vocab_size <= 0 ||
+      seq_len <= 0)
+    throw std::invalid_argument("model config: dimensions must be positive");
+  if (d_model % n_heads != 0)
+    throw std::invalid_argument("model config: d_model must be divisible by n_heads");
+  if (n_layers_params != 1 && n_layers_params != n_layers_graph)
+    throw std::invalid_argument("model config: n_layers_params must be 1 or n_layers_graph");
+  moe.validate();
+}
+
+ModelConfig ModelConfig::as_shared() const {
+  ModelConfig c = *this;
+  c.n_layers_params = 1;
+  return c;
+}
+ModelConfig ModelConfig::as_unshared() const {
+  ModelConfig c = *this;
+  c.n_layers_params = c.n_layers_graph;
+  return c;
+}
+
+ParamCounts count_params(const ModelConfig& config) {
+  config.validate();
+  const std::int64_t d = config.d_model, dff = config.d_ff;
+  ParamCounts out;
+  out.embedding_params = static_cast<std::int64_t>(config.vocab_size) * d +
+                         static_cast<std::int64_t>(config.seq_len) * d + 2 * d;
+  std::int64_t layer = 4 * d * d + 4 * d;
+  const std::int64_t ffn = d * dff + dff + dff * d + d;
+  if (config.moe.enabled())
+    layer += d * config.moe.n_experts + static_cast<std::int64_t>(config.moe.n_experts) * ffn;
+  else
+    layer += ffn;
+  out.per_layer_params = layer;
+  out.total_params = out.embedding_params + config.n_layers_params * layer;
+  return out;
+}
+
+// ---------------------------------------------------------------- init (model.cpp:11-36)
+namespace {
+std::uint64_t fnv1a(const std::string& s) {
+  std::uint64_t h = 1469598103934665603ull;
+  for (char c : s) {
+    h ^= static_cast<unsigned char>(c);
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+}  // namespace
+
+std::uint64_t init_mix_seed(std::uint64_t seed, const std::string& name) {
+  std::uint64_t z = seed ^ fnv1a(name);
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+void init_normal_host(float* out, std::size_t n, std::uint64_t seed, const std::string& name,
+                      float stddev) {
+  std::mt19937_64 rng(init_mix_seed(seed, name));
+  std::normal_distribution<float> dist(0.0f, stddev);
+  for (std::size_t i = 0; i < n; ++i) out[i] = dist(rng);
+}
+
+float lr_at(float peak, double warmup_ratio, std::int64_t total, std::int64_t step) {
+  // LrSchedule::cosine + at (optim.cpp:8-24)
+  if (total <= 0) throw std::invalid_argument("lr schedule: total_steps must be positive");
+  const std::int64_t warm = std::max<std::int64_t>(
+      1, static_cast<std::int64_t>(std::llround(warmup_ratio * static_cast<double>(total))));
+  if (step < warm) return peak * static_cast<float>(step) / static_cast<float>(warm);
+  const double span = static_cast<double>(std::max<std::int64_t>(1, total - warm));
+  const double t = std::min(1.0, static_cast<double>(step - warm) / span);
+  return static_cast<float>(peak * 0.5 * (1.0 + std::cos(t * 3.14159265358979323846)));
+}
+
+// ---------------------------------------------------------------- layout
+long long GranuleLayout::add(long long n, bool decay) {
+  const long long off = numel;
+  segs.push_back({off, n, decay});
+  numel += (n + 63) / 64 * 64;  // 256-byte aligned segments (TMA needs 16 B)
+  return off;
+}
+
+// ---------------------------------------------------------------- activations
+struct LayerActs {
+  DevBuf xout, a16, mean1, rstd1, qkv16, o16, lse, x1, b16, mean2, rstd2;
+  DevBuf hpre16, g16;                                                 // dense FFN
+  DevBuf b32, logits, sel, surv, pos, w, raw, counts, rows_pad, slots_pad, dropped;  // MoE
+  DevBuf xe16, hpre_e16, ge16, ye32;
+  int capacity = 0;
+};
+
+struct Acts {
+  int B = 0, S = 0, T = 0, seg = 0, cap = 0, vld = 0;
+  DevBuf x0;
+  std::vector<LayerActs> L;
+  DevBuf h16, meanf, rstdf, logits32, dlogits16, loss, loss_sum, ce_ws, dh32;
+  DevBuf dres, dres16, tmp32, dx1, dx1_16, do16, dqkv16, dh16, dye16, dxe32, dw, glogits, dsum;
+  DevBuf ln_ws, colsum_ws;
+  DevBuf tokens, targets, mask;
+};
+
+// ---------------------------------------------------------------- Model
+Model::Model(ModelConfig config, std::uint64_t seed) : cfg_(std::move(config)) {
+  cfg_.validate();
+  build_layout();
+  allocate();
+  init_params(seed);
+}
+
+Model::Model(ModelConfig config, NoInit) : cfg_(std::move(config)) {
+  cfg_.validate();
+  build_layout();
+  allocate();
+}
+
+Model::~Model() {
+  if (pinned_) cudaFreeHost(pinned_);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+void Model::build_layout() {
+  const int d = cfg_.d_model, dff = cfg_.d_ff, V = cfg_.vocab_size, S = cfg_.seq_len;
+  const int E = cfg_.moe.n_experts;
+  n_owned_ = cfg_.n_layers_params;
+  // embeddings granule (for_each_param order: tok, pos, final gain, final bias)
+  emb_ = GranuleLayout{};
+  emb_.tok = emb_.add(1LL * V * d, true);
+  emb_.pos = emb_.add(1LL * S * d, true);
+  emb_.fin_g = emb_.add(d, false);
+  emb_.fin_b = emb_.add(d, false);
+  // layer granule
+  layer_ = GranuleLayout{};
+  layer_.ln1_g = layer_.add(d, false);
+  layer_.ln1_b = layer_.add(d, false);
+  layer_.wqkv = layer_.add(3LL * d * d, true);  // [d, 3d] = wq | wk | wv
+  layer_.wo = layer_.add(1LL * d * d, true);
+  layer_.ln2_g = layer_.add(d, false);
+  layer_.ln2_b = layer_.add(d, false);
+  if (cfg_.moe.enabled()) {
+    layer_.gate = layer_.add(1LL * d * E, true);
+    layer_.w1 = layer_.add(1LL * E * d * dff, true);  // [E, d, dff]
+    layer_.b1 = layer_.add(1LL * E * dff, false);     // [E, dff]
+    layer_.w2 = layer_.add(1LL * E * dff * d, true);  // [E, dff, d]
+    layer_.b2 = layer_.add(1LL * E * d, false);       // [E, d]
+  } else {
+    layer_.w1 = layer_.add(1LL * d * dff, true);
+    layer_.b1 = layer_.add(dff, false);
+    layer_.w2 = layer_.add(1LL * dff * d, true);
+    layer_.b2 = layer_.add(d, false);
+  }
+  layer_stride_ = (layer_.numel + 63) / 64 * 64;
+
+  // reference-named views, Model::for_each_param order (model.cpp:188-198)
+  views_.clear();
+  views_.push_back({"embed.tok", -1, emb_.tok, V, d, d, {V, d}});
+  views_.push_back({"embed.pos", -1, emb_.pos, S, d, d, {S, d}});
+  views_.push_back({"final_norm.gain", -1, emb_.fin_g, 1, d, d, {d}});
+  views_.push_back({"final_norm.bias", -1, emb_.fin_b, 1, d, d, {d}});
+  for (int i = 0; i < n_owned_; ++i) {
+    const std::string pre = "layer." + std::to_string(i) + ".";
+    views_.push_back({pre + "ln1.gain", i, layer_.ln1_g, 1, d, d, {d}});
+    views_.push_back({pre + "ln1.bias", i, layer_.ln1_b, 1, d, d, {d}});
+    views_.push_back({pre + "attn.wq", i, layer_.wqkv, d, d, 3 * d, {d, d}});
+    views_.push_back({pre + "attn.wk", i, layer_.wqkv + d, d, d, 3 * d, {d, d}});
+    views_.push_back({pre + "attn.wv", i, layer_.wqkv + 2LL * d, d, d, 3 * d, {d, d}});
+    views_.push_back({pre + "attn.wo", i, layer_.wo, d, d, d, {d, d}});
+    views_.push_back({pre + "ln2.gain", i, layer_.ln2_g, 1, d, d, {d}});
+    views_.push_back({pre + "ln2.bias", i, layer_.ln2_b, 1, d, d, {d}});
+    if (!cfg_.moe.enabled()) {
+      views_.push_back({pre + "ffn.w1", i, layer_.w1, d, dff, dff, {d, dff}});
+      views_.push_back({pre + "ffn.b1", i, layer_.b1, 1, dff, dff, {dff}});
+      views_.push_back({pre + "ffn.w2", i, layer_.w2, dff, d, d, {dff, d}});
+      views_.push_back({pre + "ffn.b2", i, layer_.b2, 1, d, d, {d}});
+    } else {
+      views_.push_back({pre + "moe.gate", i, layer_.gate, d, E, E, {d, E}});
+      for (int e = 0; e < E; ++e) {
+        const std::string ep = pre + "moe.expert." + std::to_string(e) + ".";
+        views_.push_back({ep + "w1", i, layer_.w1 + 1LL * e * d * dff, d, dff, dff, {d, dff}});
+        views_.push_back({ep + "b1", i, layer_.b1 + 1LL * e * dff, 1, dff, dff, {dff}});
+        views_.push_back({ep + "w2", i, layer_.w2 + 1LL * e * dff * d, dff, d, d, {dff, d}});
+        views_.push_back({ep + "b2", i, layer_.b2 + 1LL * e * d, 1, d, d, {d}});
+      }
+    }
+  }
+}
+
+void Model::allocate() {
+  cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
+  const std::size_t eb = static_cast<std::size_t>(emb_.numel);
+  const std::size_t lb = static_cast<std::size_t>(layer_stride_) * n_owned_;
+  emb_p_ = DevBuf(eb * 4);
+  emb_g_ = DevBuf(eb * 4);
+  emb_p16_ = DevBuf(eb * 2);
+  lay_p_ = DevBuf(lb * 4);
+  lay_g_ = DevBuf(lb * 4);
+  lay_p16_ = DevBuf(lb * 2);
+  cuda_check(cudaMemsetAsync(emb_p_.p, 0, eb * 4, stream_), "memset");
+  cuda_check(cudaMemsetAsync(emb_g_.p, 0, eb * 4, stream_), "memset");
+  cuda_check(cudaMemsetAsync(lay_p_.p, 0, lb * 4, stream_), "memset");
+  cuda_check(cudaMemsetAsync(lay_g_.p, 0, lb * 4, stream_), "memset");
+}
+
+float* Model::lp(int o, long long off) const { return lay_p_.as<float>() + o * layer_stride_ + off; }
+float* Model::lg(int o, long long off) const { return lay_g_.as<float>() + o * layer_stride_ + off; }
+void* Model::lp16(int o, long long off) const {
+  return lay_p16_.as<std::uint16_t>() + o * layer_stride_ + off;
+}
+
+void Model::init_params(std::uint64_t seed) {
+  // model.cpp:128-164: gains 1, biases 0, matrices N(0, 0.02) per named tensor
+  std::vector<float> host;
+  for (int i = 0; i < static_cast<int>(views_.size()); ++i) {
+    const ParamView& v = views_[i];
+    const std::size_t n = static_cast<std::size_t>(v.rows) * v.cols;
+    host.assign(n, 0.0f);
+    const std::string& nm = v.name;
+    auto ends_with = [&](const char* suf) {
+      const std::size_t L = std::strlen(suf);
+      return nm.size() >= L && nm.compare(nm.size() - L, L, suf) == 0;
+    };
+    if (ends_with(".gain")) {
+      std::fill(host.begin(), host.end(), 1.0f);
+    } else if (ends_with(".bias") || ends_with(".b1") || ends_with(".b2")) {
+      // zeros
+    } else {
+      init_normal_host(host.data(), n, seed, nm);
+    }
+    set_param(i, host.data());
+  }
+  refresh_bf16();
+}
+
+void Model::refresh_bf16() {
+  p2r_check(p2r_cast_bf16(emb_p_.as<float>(), emb_p16_.p, emb_.numel, stream_), "cast");
+  p2r_check(p2r_cast_bf16(lay_p_.as<float>(), lay_p16_.p, layer_stride_ * n_owned_, stream_), "cast");
+}
+
+void Model::get_param(int i, float* host) const {
+  const ParamView& v = views_.at(static_cast<std::size_t>(i));
+  const float* base = v.granule < 0 ? ep(v.off) : lp(v.granule, v.off);
+  cuda_check(cudaMemcpy2DAsync(host, static_cast<std::size_t>(v.cols) * 4, base,
+                               static_cast<std::size_t>(v.ld) * 4, static_cast<std::size_t>(v.cols) * 4,
+                               v.rows, cudaMemcpyDeviceToHost, stream_),
+             "get_param");
+  cuda_check(cudaStreamSynchronize(stream_), "sync");
+}
+
+void Model::set_param(int i, const float* host) {
+  const ParamView& v = views_.at(static_cast<std::size_t>(i));
+  float* base = v.granule < 0 ? const_cast<float*>(ep(v.off)) : lp(v.granule, v.off);
+  cuda_check(cudaMemcpy2DAsync(base, static_cast<std::size_t>(v.ld) * 4, host,
+                               static_cast<std::size_t>(v.cols) * 4, static_cast<std::size_t>(v.cols) * 4,
+                               v.rows, cudaMemcpyHostToDevice, stream_),
+             "set_param");
+  cuda_check(cudaStreamSynchronize(stream_), "sync");
+  // keep the bf16 shadow in step with the master copy
+  if (v.granule < 0)
+    p2r_check(p2r_cast_bf16(emb_p_.as<float>(), emb_p16_.p, emb_.numel, stream_), "cast");
+  else
+    p2r_check(p2r_cast_bf16(lp(v.granule, 0), lp16(v.granule, 0), layer_stride_, stream_), "cast");
+}
+
+void Model::get_grad(int i, float* host) const {
+  const ParamView& v = views_.at(static_cast<std::size_t>(i));
+  const float* base = v.granule < 0 ? emb_g_.as<float>() + v.off : lg(v.granule, v.off);
+  cuda_check(cudaMemcpy2DAsync(host, static_cast<std::size_t>(v.cols) * 4, base,
+                               static_cast<std::size_t>(v.ld) * 4, static_cast<std::size_t>(v.cols) * 4,
+                               v.rows, cudaMemcpyDeviceToHost, stream_),
+             "get_grad");
+  cuda_check(cudaStreamSynchronize(stream_), "sync");
+}
+
+void Model::get_moment(int i, int which, float* host) const {
+  if (!has_opt_) throw std::logic_error("adamw: optimizer not attached");
+  const ParamView& v = views_.at(static_cast<std::size_t>(i));
+  const DevBuf& eb = which ? emb_v_ : emb_m_;
+  const DevBuf& lb = which ? lay_v_ : lay_m_;
+  const float* base = v.granule < 0 ? eb.as<float>() + v.off : lb.as<float>() + v.granule * layer_stride_ + v.off;
+  cuda_check(cudaMemcpy2DAsync(host, static_cast<std::size_t>(v.cols) * 4, base,
+                               static_cast<std::size_t>(v.ld) * 4, static_cast<std::size_t>(v.cols) * 4,
+                               v.rows, cudaMemcpyDeviceToHost, stream_),
+             "get_moment");
+  cuda_check(cudaStreamSynchronize(stream_), "sync");
+}
+
+std::int64_t Model::grad_bytes() const {
+  return (emb_.numel + layer_stride_ * n_owned_) * 4;
+}
+
+void Model::zero_grads() {
+  cuda_check(cudaMemsetAsync(emb_g_.p, 0, emb_g_.bytes, stream_), "zero grads");
+  cuda_check(cudaMemsetAsync(lay_g_.p, 0, lay_g_.bytes, stream_), "zero grads");
+}
+
+// ---------------------------------------------------------------- activations
+void Model::ensure_acts(int B, int S) {
+  const int T = B * S;
+  if (acts_ && acts_->B == B && acts_->S == S) return;
+  acts_.reset();
+  auto A = std::make_unique<Acts>();
+  const int d = cfg_.d_model, dff = cfg_.d_ff, H = cfg_.n_heads, V = cfg_.vocab_size;
+  const int E = cfg_.moe.n_experts, k = cfg_.moe.n_prototypes;
+  A->B = B;
+  A->S = S;
+  A->T = T;
+  A->vld = (V + 7) / 8 * 8;
+  const std::size_t Td = static_cast<std::size_t>(T) * d;
+  if (cfg_.moe.enabled()) {
+    A->cap = p2r_moe_capacity(cfg_.moe.capacity_factor, T, E, k);
+    const int rows = std::min(A->cap, T);
+    A->seg = std::max(128, (rows + 127) / 128 * 128);
+  }
+  const std::size_t ES = static_cast<std::size_t>(E) * A->seg;
+  A->x0 = DevBuf(Td * 4);
+  A->L.resize(static_cast<std::size_t>(cfg_.n_layers_graph));
+  for (auto& l : A->L) {
+    l.xout = DevBuf(Td * 4);
+    l.a16 = DevBuf(Td * 2);
+    l.mean1 = DevBuf(T * 4);
+    l.rstd1 = DevBuf(T * 4);
+    l.qkv16 = DevBuf(Td * 3 * 2);
+    l.o16 = DevBuf(Td * 2);
+    l.lse = DevBuf(static_cast<std::size_t>(T) * H * 4);
+    l.x1 = DevBuf(Td * 4);
+    l.b16 = DevBuf(Td * 2);
+    l.mean2 = DevBuf(T * 4);
+    l.rstd2 = DevBuf(T * 4);
+    if (!cfg_.moe.enabled()) {
+      l.hpre16 = DevBuf(static_cast<std::size_t>(T) * dff * 2);
+      l.g16 = DevBuf(static_cast<std::size_t>(T) * dff * 2);
+    } else {
+      l.capacity = A->cap;
+      l.b32 = DevBuf(Td * 4);
+      l.logits = DevBuf(static_cast<std::size_t>(T) * E * 4);
+      l.sel = DevBuf(static_cast<std::size_t>(T) * k * 4);
+      l.surv = DevBuf(static_cast<std::size_t>(T) * k);
+      l.pos = DevBuf(static_cast<std::size_t>(T) * k * 4);
+      l.w = DevBuf(static_cast<std::size_t>(T) * k * 4);
+      l.raw = DevBuf(static_cast<std::size_t>(E) * 4);
+      l.counts = DevBuf(static_cast<std::size_t>(E) * 4);
+      l.rows_pad = DevBuf(ES * 4);
+      l.slots_pad = DevBuf(ES * 4);
+      l.dropped = DevBuf(4);
+      l.xe16 = DevBuf(ES * d * 2);
+      l.hpre_e16 = DevBuf(ES * dff * 2);
+      l.ge16 = DevBuf(ES * dff * 2);
+      l.ye32 = DevBuf(ES * d * 4);
+    }
+  }
+  A->h16 = DevBuf(Td * 2);
+  A->meanf = DevBuf(T * 4);
+  A->rstdf = DevBuf(T * 4);
+  A->logits32 = DevBuf(static_cast<std::size_t>(T) * A->vld * 4);
+  A->dlogits16 = DevBuf(static_cast<std::size_t>(T) * A->vld * 2);
+  A->loss = DevBuf(4);
+  A->loss_sum = DevBuf(8);
+  A->ce_ws = DevBuf(p2r_cross_entropy_workspace(T));
+  A->dh32 = DevBuf(Td * 4);
+  A->dres = DevBuf(Td * 4);
+  A->dres16 = DevBuf(Td * 2);
+  A->tmp32 = DevBuf(Td * 4);
+  A->dx1 = DevBuf(Td * 4);
+  A->dx1_16 = DevBuf(Td * 2);
+  A->do16 = DevBuf(Td * 2);
+  A->dqkv16 = DevBuf(Td * 3 * 2);
+  A->dsum = DevBuf(static_cast<std::size_t>(T) * H * 4);
+  if (!cfg_.moe.enabled()) {
+    A->dh16 = DevBuf(static_cast<std::size_t>(T) * dff * 2);
+  } else {
+    A->dh16 = DevBuf(ES * dff * 2);
+    A->dye16 = DevBuf(ES * d * 2);
+    A->dxe32 = DevBuf(ES * d * 4);
+    A->dw = DevBuf(static_cast<std::size_t>(T) * k * 4);
+    A->glogits = DevBuf(static_cast<std::size_t>(T) * E * 4);
+  }
+  A->ln_ws = DevBuf(p2r_layernorm_bwd_workspace(T, d));
+  const int bias_n = std::max(dff, d);
+  A->colsum_ws = DevBuf(p2r_colsum_workspace(std::max(T, A->seg), bias_n, std::max(1, E)));
+  A->tokens = DevBuf(static_cast<std::size_t>(T) * 4);
+  A->targets = DevBuf(static_cast<std::size_t>(T) * 4);
+  A->mask = DevBuf(static_cast<std::size_t>(T));
+  acts_ = std::move(A);
+  const std::size_t pin = static_cast<std::size_t>(T) * 9 + 64;
+  if (pinned_bytes_ < pin) {
+    if (pinned_) cudaFreeHost(pinned_);
+    cuda_check(cudaMallocHost(&pinned_, pin), "pinned staging");
+    pinned_bytes_ = pin;
+  }
+}
+
+void Model::gemm(int m, int n, int k, const void* a, int lda, bool a_mn, const void* b, int ldb,
+                 bool b_mn, int epi, void* c, int ldc, void* c2, int ldc2, const float* bias,
+                 const void* aux, int ldaux, int group_mode, int groups, int seg_rows,
+                 const int* counts, int split_k) {
+  p2r_gemm_args g{};
+  g.m = m;
+  g.n = n;
+  g.k = k;
+  g.a = a;
+  g.lda = lda;
+  g.a_mn_major = a_mn;
+  g.b = b;
+  g.ldb = ldb;
+  g.b_mn_major = b_mn;
+  g.epi = epi;
+  g.c = c;
+  g.ldc = ldc;
+  g.c2 = c2;
+  g.ldc2 = ldc2;
+  g.bias = bias;
+  g.aux = aux;
+  g.ldaux = ldaux;
+  g.group_mode = group_mode;
+  g.groups = groups;
+  g.seg_rows = seg_rows;
+  g.counts = counts;
+  g.split_k = split_k;
+  if (split_k > 1) {
+    const std::size_t need = p2r_gemm_workspace_bytes(&g);
+    if (splitk_ws_.bytes < need) splitk_ws_ = DevBuf(need);
+    p2r_set_workspace(splitk_ws_.p, splitk_ws_.bytes);
+  }
+  p2r_check(p2r_gemm(&g, stream_), "gemm");
+}
+
+namespace {
+// split-K only when the output tile count leaves most SMs idle
+int pick_split(int m, int n, int k) {
+  const int bn = n <= 128 ? 128 : 256;
+  const int tiles = ((m + 127) / 128) * ((n + bn - 1) / bn);
+  if (tiles >= 74) return 1;
+  int s = 148 / std::max(1, tiles);
+  s = std::min(s, std::max(1, k / 1024));
+  return std::max(1, std::min(s, 4));
+}
+}  // namespace
+
+// ---------------------------------------------------------------- forward pieces
+Tensor Model::embed_forward(GradTape* tape, const int* d_tokens, int batch, int seq) {
+  if (batch <= 0) throw std::invalid_argument("forward: token count must be a multiple of batch");
+  if (seq > cfg_.seq_len) throw std::invalid_argument("forward: sequence longer than configured seq_len");
+  ensure_acts(batch, seq);
+  Acts& A = *acts_;
+  const int d = cfg_.d_model;
+  p2r_check(p2r_embed_fwd(d_tokens, ep(emb_.tok), ep(emb_.pos), A.T, seq, d, A.x0.as<float>(), stream_), "embed");
+  if (tape) {
+    tape->record([this, d_tokens, batch, seq]() {
+      Acts& A2 = *acts_;
+      p2r_check(p2r_embed_bwd(d_tokens, A2.dres.as<float>(), batch, seq, cfg_.d_model, cfg_.vocab_size,
+                              eg(emb_.tok), eg(emb_.pos), stream_),
+                "embed bwd");
+    });
+  }
+  return Tensor{A.T, d, A.x0.as<float>(), A.dres.as<float>(), A.dres16.p};
+}
+
+Tensor Model::block_forward(GradTape* tape, int g, const Tensor& x, int batch, AttentionMode mode) {
+  if (g < 0 || g >= cfg_.n_layers_graph) throw std::out_of_range("model: graph layer index out of range");
+  Acts& A = *acts_;
+  if (x.rows != A.T || batch != A.B) throw std::invalid_argument("block_forward: batch does not match embed_forward");
+  LayerActs& L = A.L[static_cast<std::size_t>(g)];
+  const int o = owned_index_of_graph_layer(g);
+  const int T = A.T, d = cfg_.d_model, dff = cfg_.d_ff, H = cfg_.n_heads;
+  const int causal = mode == AttentionMode::Causal ? 1 : 0;
+  // a = LN1(x)
+  p2r_check(p2r_layernorm_fwd(x.data, lp(o, layer_.ln1_g), lp(o, layer_.ln1_b), T, d, 1e-5f, L.a16.p, nullptr,
+                              L.mean1.as<float>(), L.rstd1.as<float>(), stream_),
+            "ln1");
+  // qkv = a . [wq|wk|wv]  (B = fused [d, 3d] bf16, N-major)
+  gemm(T, 3 * d, d, L.a16.p, d, false, lp16(o, layer_.wqkv), 3 * d, true, P2R_EPI_BF16, L.qkv16.p, 3 * d);
+  p2r_check(p2r_attention_fwd(L.qkv16.p, L.o16.p, L.lse.as<float>(), A.B, H, A.S, d, causal, stream_), "attn");
+  // x1 = x + o . wo
+  gemm(T, d, d, L.o16.p, d, false, lp16(o, layer_.wo), d, true, P2R_EPI_F32, L.x1.p, d, nullptr, 0, nullptr,
+       x.data, d);
+  // b = LN2(x1)
+  const bool moe = cfg_.moe.enabled();
+  p2r_check(p2r_layernorm_fwd(L.x1.as<float>(), lp(o, layer_.ln2_g), lp(o, layer_.ln2_b), T, d, 1e-5f, L.b16.p,
+                              moe ? L.b32.as<float>() : nullptr, L.mean2.as<float>(), L.rstd2.as<float>(), stream_),
+            "ln2");
+  if (!moe) {
+    gemm(T, dff, d, L.b16.p, d, false, lp16(o, layer_.w1), dff, true, P2R_EPI_BIAS_GELU, L.g16.p, dff, L.hpre16.p,
+         dff, lp(o, layer_.b1));
+    gemm(T, d, dff, L.g16.p, dff, false, lp16(o, layer_.w2), d, true, P2R_EPI_F32, L.xout.p, d, nullptr, 0,
+         lp(o, layer_.b2), L.x1.p, d);
+  } else {
+    const int E = cfg_.moe.n_experts, k = cfg_.moe.n_prototypes, seg = A.seg;
+    p2r_check(p2r_moe_gate_logits(L.b32.as<float>(), lp(o, layer_.gate), T, d, E, L.logits.as<float>(), stream_),
+              "gate");
+    p2r_check(p2r_moe_route(L.logits.as<float>(), T, E, k, A.cap, seg, L.sel.as<int>(), L.surv.as<std::uint8_t>(),
+                            L.pos.as<int>(), L.raw.as<int>(), L.counts.as<int>(), L.rows_pad.as<int>(),
+                            L.slots_pad.as<int>(), L.dropped.as<int>(), stream_),
+              "route");
+    p2r_check(p2r_moe_combine_weights(L.logits.as<float>(), T, E, k, L.sel.as<int>(), L.surv.as<std::uint8_t>(),
+                                      L.w.as<float>(), stream_),
+              "combine weights");
+    p2r_check(p2r_moe_dispatch(L.b16.p, 1, d, E, seg, L.rows_pad.as<int>(), L.slots_pad.as<int>(),
+                               L.counts.as<int>(), nullptr, k, L.xe16.p, stream_),
+              "dispatch");
+    gemm(E * seg, dff, d, L.xe16.p, d, false, lp16(o, layer_.w1), dff, true, P2R_EPI_BIAS_GELU, L.ge16.p, dff,
+         L.hpre_e16.p, dff, lp(o, layer_.b1), nullptr, 0, P2R_GROUP_M, E, seg, L.counts.as<int>());
+    gemm(E * seg, d, dff, L.ge16.p, dff, false, lp16(o, layer_.w2), d, true, P2R_EPI_F32, L.ye32.p, d, nullptr, 0,
+         lp(o, layer_.b2), nullptr, 0, P2R_GROUP_M, E, seg, L.counts.as<int>());
+    p2r_check(p2r_moe_combine(L.ye32.as<float>(), T, d, k, seg, L.sel.as<int>(), L.pos.as<int>(), L.w.as<float>(),
+                              L.x1.as<float>(), L.xout.as<float>(), stream_),
+              "combine");
+  }
+  if (tape) tape->record([this, g, mode]() { block_backward(g, mode); });
+  return Tensor{T, d, L.xout.as<float>(), A.dres.as<float>(), A.dres16.p};
+}
+
+// Backward of graph layer g. On entry A.dres/dres16 hold dL/d(block output);
+// on exit they hold dL/d(block input). Parameter grads of the owned layer are
+// accumulated in place (beta = 1), so in Pseudo mode the L graph layers sum
+// into one buffer in reverse layer order exactly like the reference's
+// per-layer flush (model.cpp:210-221).
+void Model::block_backward(int g, AttentionMode mode) {
+  Acts& A = *acts_;
+  LayerActs& L = A.L[static_cast<std::size_t>(g)];
+  const int o = owned_index_of_graph_layer(g);
+  const int T = A.T, d = cfg_.d_model, dff = cfg_.d_ff, H = cfg_.n_heads;
+  const int causal = mode == AttentionMode::Causal ? 1 : 0;
+  const float* xin = g == 0 ? A.x0.as<float>() : A.L[static_cast<std::size_t>(g - 1)].xout.as<float>();
+  float* dy = A.dres.as<float>();
+  void* dy16 = A.dres16.p;
+  if (!cfg_.moe.enabled()) {
+    // FFN2: dW2 += g^T dy ; db2 += colsum(dy) ; dh = (dy W2^T) * gelu'(hpre)
+    gemm(dff, d, T, L.g16.p, dff, true, dy16, d, true, P2R_EPI_ACC_F32, lg(o, layer_.w2), d, nullptr, 0, nullptr,
+         nullptr, 0, 0, 0, 0, nullptr, pick_split(dff, d, T));
+    p2r_check(p2r_bias_grad(dy, 0, d, T, d, 1, 0, nullptr, lg(o, layer_.b2), 0, A.colsum_ws.as<float>(), stream_),
+              "db2");
+    gemm(T, dff, d, dy16, d, false, lp16(o, layer_.w2), d, false, P2R_EPI_DGELU, A.dh16.p, dff, nullptr, 0, nullptr,
+         L.hpre16.p, dff);
+    // FFN1: dW1 += b^T dh ; db1 += colsum(dh) ; db = dh W1^T
+    gemm(d, dff, T, L.b16.p, d, true, A.dh16.p, dff, true, P2R_EPI_ACC_F32, lg(o, layer_.w1), dff, nullptr, 0,
+         nullptr, nullptr, 0, 0, 0, 0, nullptr, pick_split(d, dff, T));
+    p2r_check(p2r_bias_grad(A.dh16.p, 1, dff, T, dff, 1, 0, nullptr, lg(o, layer_.b1), 0, A.colsum_ws.as<float>(),
+                            stream_),
+              "db1");
+    gemm(T, d, dff, A.dh16.p, dff, false, lp16(o, layer_.w1), dff, false, P2R_EPI_F32, A.tmp32.p, d);
+  } else {
+    const int E = cfg_.moe.n_experts, k = cfg_.moe.n_prototypes, seg = A.seg;
+    const int* cnt = L.counts.as<int>();
+    // combine backward: dw = <dy, ye>, dye = w * dy (expert-major, bf16)
+    p2r_check(p2r_moe_combine_bwd_weights(dy, L.ye32.as<float>(), T, d, k, seg, L.sel.as<int>(), L.pos.as<int>(),
+                                          A.dw.as<float>(), stream_),
+              "combine bwd");
+    p2r_check(p2r_moe_dispatch(dy, 0, d, E, seg, L.rows_pad.as<int>(), L.slots_pad.as<int>(), cnt, L.w.as<float>(),
+                               k, A.dye16.p, stream_),
+              "dispatch dy");
+    gemm(dff, d, seg, L.ge16.p, dff, true, A.dye16.p, d, true, P2R_EPI_ACC_F32, lg(o, layer_.w2), d, nullptr, 0,
+         nullptr, nullptr, 0, P2R_GROUP_K, E, seg, cnt);
+    p2r_check(p2r_bias_grad(A.dye16.p, 1, d, E * seg, d, E, seg, cnt, lg(o, layer_.b2), d, A.colsum_ws.as<float>(),
+                            stream_),
+              "db2");
+    gemm(E * seg, dff, d, A.dye16.p, d, false, lp16(o, layer_.w2), d, false, P2R_EPI_DGELU, A.dh16.p, dff, nullptr,
+         0, nullptr, L.hpre_e16.p, dff, P2R_GROUP_M, E, seg, cnt);
+    gemm(d, dff, seg, L.xe16.p, d, true, A.dh16.p, dff, true, P2R_EPI_ACC_F32, lg(o, layer_.w1), dff, nullptr, 0,
+         nullptr, nullptr, 0, P2R_GROUP_K, E, seg, cnt);
+    p2r_check(p2r_bias_grad(A.dh16.p, 1, dff, E * seg, dff, E, seg, cnt, lg(o, layer_.b1), dff,
+                            A.colsum_ws.as<float>(), stream_),
+              "db1");
+    gemm(E * seg, d, dff, A.dh16.p, dff, false, lp16(o, layer_.w1), dff, false, P2R_EPI_F32, A.dxe32.p, d, nullptr,
+         0, nullptr, nullptr, 0, P2R_GROUP_M, E, seg, cnt);
+    const float* glog = nullptr;
+    if (k > 1) {  // top-1 => combine weights are exactly 1 and the gate gradient is exactly 0
+      p2r_check(p2r_moe_gate_bwd(L.b32.as<float>(), L.w.as<float>(), A.dw.as<float>(), T, d, E, k, L.sel.as<int>(),
+                                 L.surv.as<std::uint8_t>(), A.glogits.as<float>(), lg(o, layer_.gate), stream_),
+                "gate bwd");
+      glog = A.glogits.as<float>();
+    }
+    p2r_check(p2r_moe_dispatch_bwd(A.dxe32.as<float>(), T, d, k, seg, L.sel.as<int>(), L.pos.as<int>(), glog,
+                                   lp(o, layer_.gate), E, A.tmp32.as<float>(), 0, stream_),
+              "dispatch bwd");
+  }
+  // LN2 backward: dx1 = dy + LN2'(db)
+  p2r_check(p2r_layernorm_bwd(A.tmp32.as<float>(), L.x1.as<float>(), L.mean2.as<float>(), L.rstd2.as<float>(),
+                              lp(o, layer_.ln2_g), dy, T, d, A.dx1.as<float>(), A.dx1_16.p, lg(o, layer_.ln2_g),
+                              lg(o, layer_.ln2_b), A.ln_ws.as<float>(), stream_),
+            "ln2 bwd");
+  // O projection: dWo += o^T dx1 ; do = dx1 Wo^T
+  gemm(d, d, T, L.o16.p, d, true, A.dx1_16.p, d, true, P2R_EPI_ACC_F32, lg(o, layer_.wo), d, nullptr, 0, nullptr,
+       nullptr, 0, 0, 0, 0, nullptr, pick_split(d, d, T));
+  gemm(T, d, d, A.dx1_16.p, d, false, lp16(o, layer_.wo), d, false, P2R_EPI_BF16, A.do16.p, d);
+  p2r_check(p2r_attention_bwd(L.qkv16.p, L.o16.p, L.lse.as<float>(), A.do16.p, A.dsum.as<float>(), A.dqkv16.p, A.B,
+                              H, A.S, d, causal, stream_),
+            "attn bwd");
+  // QKV: dWqkv += a^T dqkv ; da = dqkv Wqkv^T
+  gemm(d, 3 * d, T, L.a16.p, d, true, A.dqkv16.p, 3 * d, true, P2R_EPI_ACC_F32, lg(o, layer_.wqkv), 3 * d, nullptr,
+       0, nullptr, nullptr, 0, 0, 0, 0, nullptr, pick_split(d, 3 * d, T));
+  gemm(T, d, 3 * d, A.dqkv16.p, 3 * d, false, lp16(o, layer_.wqkv), 3 * d, false, P2R_EPI_F32, A.tmp32.p, d);
+  // LN1 backward: dx = dx1 + LN1'(da)
+  p2r_check(p2r_layernorm_bwd(A.tmp32.as<float>(), xin, L.mean1.as<float>(), L.rstd1.as<float>(), lp(o, layer_.ln1_g),
+                              A.dx1.as<float>(), T, d, dy, dy16, lg(o, layer_.ln1_g), lg(o, layer_.ln1_b),
+                              A.ln_ws.as<float>(), stream_),
+            "ln1 bwd");
+}
+
+Tensor Model::head_forward(GradTape* tape, const Tensor& x) {
+  Acts& A = *acts_;
+  const int T = A.T, d = cfg_.d_model, V = cfg_.vocab_size;
+  p2r_check(p2r_layernorm_fwd(x.data, ep(emb_.fin_g), ep(emb_.fin_b), T, d, 1e-5f, A.h16.p, nullptr,
+                              A.meanf.as<float>(), A.rstdf.as<float>(), stream_),
+            "final ln");
+  // logits = h . tok^T  (tied head, matmul_nt)
+  gemm(T, V, d, A.h16.p, d, false, ep16(emb_.tok), d, false, P2R_EPI_F32, A.logits32.p, A.vld);
+  if (tape) {
+    const float* xin = x.data;
+    tape->record([this, xin]() {
+      Acts& A2 = *acts_;
+      const int T2 = A2.T, d2 = cfg_.d_model, V2 = cfg_.vocab_size;
+      // dtok += dlogits^T h ; dh = dlogits . tok
+      gemm(V2, d2, T2, A2.dlogits16.p, A2.vld, true, A2.h16.p, d2, true, P2R_EPI_ACC_F32, eg(emb_.tok), d2, nullptr,
+           0, nullptr, nullptr, 0, 0, 0, 0, nullptr, pick_split(V2, d2, T2));
+      gemm(T2, d2, V2, A2.dlogits16.p, A2.vld, false, ep16(emb_.tok), d2, true, P2R_EPI_F32, A2.dh32.p, d2);
+      p2r_check(p2r_layernorm_bwd(A2.dh32.as<float>(), xin, A2.meanf.as<float>(), A2.rstdf.as<float>(),
+                                  ep(emb_.fin_g), nullptr, T2, d2, A2.dres.as<float>(), A2.dres16.p, eg(emb_.fin_g),
+                                  eg(emb_.fin_b), A2.ln_ws.as<float>(), stream_),
+                "final ln bwd");
+    });
+  }
+  return Tensor{T, V, A.logits32.as<float>(), nullptr, nullptr};
+}
+
+Tensor Model::softmax_cross_entropy(GradTape* /*tape*/, const Tensor& logits, const int* d_targets,
+                                    const std::uint8_t* d_mask, double denom) {
+  if (denom <= 0.0) throw std::invalid_argument("softmax_cross_entropy: denominator must be > 0");
+  Acts& A = *acts_;
+  p2r_check(p2r_cross_entropy(logits.data, A.T, cfg_.vocab_size, A.vld, d_targets, d_mask, denom, 1.0f,
+                              A.dlogits16.p, A.vld, A.loss.as<float>(), A.loss_sum.as<double>(),
+                              A.ce_ws.as<double>(), stream_),
+            "cross entropy");
+  return Tensor{1, 1, A.loss.as<float>(), nullptr, nullptr};
+}
+
+void Model::train_step_device(const int* d_tokens, const int* d_targets, const std::uint8_t* d_mask, int batch,
+                              int seq, double denom, AttentionMode mode, bool zero, float* loss_dev) {
+  if (zero) zero_grads();
+  GradTape tape;
+  Tensor x = embed_forward(&tape, d_tokens, batch, seq);
+  for (int g = 0; g < cfg_.n_layers_graph; ++g) x = block_forward(&tape, g, x, batch, mode);
+  Tensor logits = head_forward(&tape, x);
+  Tensor loss = softmax_cross_entropy(&tape, logits, d_targets, d_mask, denom);
+  tape.backward_scalar(loss);
+  flush_shared_layer_grads();
+  if (loss_dev && loss_dev != loss.data)
+    cuda_check(cudaMemcpyAsync(loss_dev, loss.data, 4, cudaMemcpyDeviceToDevice, stream_), "loss copy");
+}
+
+namespace {
+void validate_ids(const int* ids, std::size_t n, int V, const char* msg) {
+  for (std::size_t i = 0; i < n; ++i)
+    if (ids[i] < 0 || ids[i] >= V) throw std::out_of_range(msg);
+}
+}  // namespace
+
+float Model::train_step_host(const int* tokens, const int* targets, const std::uint8_t* mask, int batch, int seq,
+                             double denom, AttentionMode mode, bool zero) {
+  if (batch <= 0 || seq <= 0) throw std::invalid_argument("forward: token count must be a multiple of batch");
+  if (seq > cfg_.seq_len) throw std::invalid_argument("forward: sequence longer than configured seq_len");
+  if (denom <= 0.0) throw std::invalid_argument("softmax_cross_entropy: denominator must be > 0");
+  const std::size_t T = static_cast<std::size_t>(batch) * seq;
+  validate_ids(tokens, T, cfg_.vocab_size, "embedding_lookup: id out of range");
+  for (std::size_t i = 0; i < T; ++i)
+    if ((mask == nullptr || mask[i] != 0) && (targets[i] < 0 || targets[i] >= cfg_.vocab_size))
+      throw std::out_of_range("softmax_cross_entropy: target out of range");
+  ensure_acts(batch, seq);
+  Acts& A = *acts_;
+  char* pin = static_cast<char*>(pinned_);
+  std::memcpy(pin, tokens, T * 4);
+  std::memcpy(pin + T * 4, targets, T * 4);
+  if (mask) std::memcpy(pin + T * 8, mask, T);
+  cuda_check(cudaMemcpyAsync(A.tokens.p, pin, T * 4, cudaMemcpyHostToDevice, stream_), "h2d");
+  cuda_check(cudaMemcpyAsync(A.targets.p, pin + T * 4, T * 4, cudaMemcpyHostToDevice, stream_), "h2d");
+  if (mask) cuda_check(cudaMemcpyAsync(A.mask.p, pin + T * 8, T, cudaMemcpyHostToDevice, stream_), "h2d");
+  train_step_device(A.tokens.as<int>(), A.targets.as<int>(), mask ? A.mask.as<std::uint8_t>() : nullptr, batch, seq,
+                    denom, mode, zero, nullptr);
+  float* lh = reinterpret_cast<float*>(pin + T * 9 + (64 - (T * 9) % 64) % 64);
+  if (reinterpret_cast<char*>(lh) + 4 > pin + pinned_bytes_) lh = reinterpret_cast<float*>(pin);
+  cuda_check(cudaMemcpyAsync(lh, A.loss.p, 4, cudaMemcpyDeviceToHost, stream_), "d2h loss");
+  cuda_check(cudaStreamSynchronize(stream_), "step sync");
+  return *lh;
+}
+
+void Model::forward_host(const int* tokens, int batch, int seq, AttentionMode mode, float* logits_out) {
+  if (batch <= 0 || seq <= 0) throw std::invalid_argument("forward: token count must be a multiple of batch");
+  if (seq > cfg_.seq_len) throw std::invalid_argument("forward: sequence longer than configured seq_len");
+  const std::size_t T = static_cast<std::size_t>(batch) * seq;
+  validate_ids(tokens, T, cfg_.vocab_size, "embedding_lookup: id out of range");
+  ensure_acts(batch, seq);
+  Acts& A = *acts_;
+  cuda_check(cudaMemcpyAsync(A.tokens.p, tokens, T * 4, cudaMemcpyHostToDevice, stream_), "h2d");
+  Tensor x = embed_forward(nullptr, A.tokens.as<int>(), batch, seq);
+  for (int g = 0; g < cfg_.n_layers_graph; ++g) x = block_forward(nullptr, g, x, batch, mode);
+  Tensor logits = head_forward(nullptr, x);
+  cuda_check(cudaMemcpy2DAsync(logits_out, static_cast<std::size_t>(cfg_.vocab_size) * 4, logits.data,
+                               static_cast<std::size_t>(A.vld) * 4, static_cast<std::size_t>(cfg_.vocab_size) * 4, T,
+                               cudaMemcpyDeviceToHost, stream_),
+             "d2h logits");
+  cuda_check(cudaStreamSynchronize(stream_), "forward sync");
+}
+
+void Model::routing_host(int g, int* selected, std::uint8_t* survived, int* raw_load, int* capacity,
+                         int* dropped) const {
+  if (!cfg_.moe.enabled()) throw std::logic_error("routing: dense model");
+  if (!acts_) throw std::logic_error("routing: no forward pass yet");
+  const LayerActs& L = acts_->L.at(static_cast<std::size_t>(g));
+  const std::size_t Tk = static_cast<std::size_t>(acts_->T) * cfg_.moe.n_prototypes;
+  cuda_check(cudaMemcpyAsync(selected, L.sel.p, Tk * 4, cudaMemcpyDeviceToHost, stream_), "d2h");
+  cuda_check(cudaMemcpyAsync(survived, L.surv.p, Tk, cudaMemcpyDeviceToHost, stream_), "d2h");
+  cuda_check(cudaMemcpyAsync(raw_load, L.raw.p, cfg_.moe.n_experts * 4, cudaMemcpyDeviceToHost, stream_), "d2h");
+  cuda_check(cudaMemcpyAsync(dropped, L.dropped.p, 4, cudaMemcpyDeviceToHost, stream_), "d2h");
+  cuda_check(cudaStreamSynchronize(stream_), "sync");
+  *capacity = L.capacity;
+}
+
+// ---------------------------------------------------------------- AdamW (optim.cpp:28-70)
+void Model::adamw_attach(float b1, float b2, float eps, float wd) {
+  b1_ = b1;
+  b2_ = b2;
+  eps_ = eps;
+  wd_ = wd;
+  if (!has_opt_) {
+    emb_m_ = DevBuf(emb_p_.bytes);
+    emb_v_ = DevBuf(emb_p_.bytes);
+    lay_m_ = DevBuf(lay_p_.bytes);
+    lay_v_ = DevBuf(lay_p_.bytes);
+    cuda_check(cudaMemsetAsync(emb_m_.p, 0, emb_m_.bytes, stream_), "memset");
+    cuda_check(cudaMemsetAsync(emb_v_.p, 0, emb_v_.bytes, stream_), "memset");
+    cuda_check(cudaMemsetAsync(lay_m_.p, 0, lay_m_.bytes, stream_), "memset");
+    cuda_check(cudaMemsetAsync(lay_v_.p, 0, lay_v_.bytes, stream_), "memset");
+    has_opt_ = true;
+  }
+}
+
+void Model::adamw_step(float lr) {
+  if (!has_opt_) throw std::logic_error("adamw: unregistered parameter embed.tok");
+  ++step_count_;
+  const float bc1 = 1.0f - std::pow(b1_, static_cast<float>(step_count_));
+  const float bc2 = 1.0f - std::pow(b2_, static_cast<float>(step_count_));
+  auto run = [&](const GranuleLayout& lay, float* p, float* g, float* m, float* v, void* p16) {
+    std::vector<long long> off, len;
+    std::vector<int> dec;
+    for (const auto& s : lay.segs) {
+      off.push_back(s.off);
+      len.push_back(s.len);
+      dec.push_back(s.decay ? 1 : 0);
+    }
+    p2r_check(p2r_adamw_step(p, g, m, v, p16, off.data(), len.data(), dec.data(), static_cast<int>(off.size()), b1_,
+                             b2_, eps_, wd_, lr, bc1, bc2, stream_),
+              "adamw");
+  };
+  run(emb_, emb_p_.as<float>(), emb_g_.as<float>(), emb_m_.as<float>(), emb_v_.as<float>(), emb_p16_.p);
+  for (int i = 0; i < n_owned_; ++i)
+    run(layer_, lp(i, 0), lg(i, 0), lay_m_.as<float>() + i * layer_stride_, lay_v_.as<float>() + i * layer_stride_,
+        lp16(i, 0));
+}
+
+std::int64_t Model::state_bytes() const {
+  if (!has_opt_) return 0;
+  // two fp32 moments per parameter element (optim.cpp:65-70)
+  return 2 * 4 * (count_params(cfg_).total_params);
+}
+
+// ---------------------------------------------------------------- delink (model.cpp:358-377)
+std::unique_ptr<Model> Model::delinked() const {
+  if (cfg_.n_layers_params != 1) throw std::logic_error("delinked: model is not in shared-parameter mode");
+  std::unique_ptr<Model> real(new Model(cfg_.as_unshared(), NoInit{}));
+  cudaStream_t s = real->stream_;
+  cuda_check(cudaStreamSynchronize(stream_), "sync");
+  // embeddings + final norm: direct copies
+  cuda_check(cudaMemcpyAsync(real->emb_p_.p, emb_p_.p, emb_p_.bytes, cudaMemcpyDeviceToDevice, s), "delink emb");
+  cuda_check(cudaMemcpyAsync(real->emb_p16_.p, emb_p16_.p, emb_p16_.bytes, cudaMemcpyDeviceToDevice, s), "delink emb");
+  const int L = real->n_owned_;
+  const std::size_t g4 = static_cast<std::size_t>(layer_stride_) * 4, g2 = static_cast<std::size_t>(layer_stride_) * 2;
+  // shared layer -> L layers: master + bf16 shadow (+ moments), one read, L writes
+  p2r_check(p2r_delink_broadcast(lay_p_.p, real->lay_p_.p, g4, g4, L, s), "delink");
+  p2r_check(p2r_delink_broadcast(lay_p16_.p, real->lay_p16_.p, g2, g2, L, s), "delink");
+  if (has_opt_) {
+    real->adamw_attach(b1_, b2_, eps_, wd_);
+    real->step_count_ = step_count_;
+    cuda_check(cudaMemcpyAsync(real->emb_m_.p, emb_m_.p, emb_m_.bytes, cudaMemcpyDeviceToDevice, s), "delink m");
+    cuda_check(cudaMemcpyAsync(real->emb_v_.p, emb_v_.p, emb_v_.bytes, cudaMemcpyDeviceToDevice, s), "delink v");
+    p2r_check(p2r_delink_broadcast(lay_m_.p, real->lay_m_.p, g4, g4, L, s), "delink m");
+    p2r_check(p2r_delink_broadcast(lay_v_.p, real->lay_v_.p, g4, g4, L, s), "delink v");
+  }
+  cuda_check(cudaStreamSynchronize(s), "delink sync");
+  return real;
+}
+
+// ---------------------------------------------------------------- host routing
+HostRouting moe_dispatch_host(const float* logits, int T, const MoEConfig& moe) {
+  moe.validate();
+  if (!moe.enabled()) throw std::invalid_argument("moe_dispatch: moe disabled");
+  const int E = moe.n_experts, k = moe.n_prototypes;
+  HostRouting r;
+  r.capacity = p2r_moe_capacity(moe.capacity_factor, T, E, k);
+  const int seg = std::max(1, std::min(std::max(r.capacity, 0), T));
+  cudaStream_t s = nullptr;
+  const std::size_t Tk = static_cast<std::size_t>(T) * k;
+  DevBuf dl(static_cast<std::size_t>(T) * E * 4 + 4), dsel(Tk * 4 + 4), dsur(Tk + 4), dpos(Tk * 4 + 4), draw(E * 4),
+      dcnt(E * 4), drows(static_cast<std::size_t>(E) * seg * 4), dslots(static_cast<std::size_t>(E) * seg * 4),
+      ddrop(4);
+  if (T > 0) cuda_check(cudaMemcpy(dl.p, logits, static_cast<std::size_t>(T) * E * 4, cudaMemcpyHostToDevice), "h2d");
+  p2r_check(p2r_moe_route(dl.as<float>(), T, E, k, r.capacity, seg, dsel.as<int>(), dsur.as<std::uint8_t>(),
+                          dpos.as<int>(), draw.as<int>(), dcnt.as<int>(), drows.as<int>(), dslots.as<int>(),
+                          ddrop.as<int>(), s),
+            "route");
+  cuda_check(cudaDeviceSynchronize(), "route sync");
+  r.selected.resize(Tk);
+  r.survived.resize(Tk);
+  r.raw_load.resize(static_cast<std::size_t>(E));
+  std::vector<int> cnt(static_cast<std::size_t>(E)), rows(static_cast<std::size_t>(E) * seg),
+      slots(static_cast<std::size_t>(E) * seg);
+  cuda_check(cudaMemcpy(r.selected.data(), dsel.p, Tk * 4, cudaMemcpyDeviceToHost), "d2h");
+  cuda_check(cudaMemcpy(r.survived.data(), dsur.p, Tk, cudaMemcpyDeviceToHost), "d2h");
+  cuda_check(cudaMemcpy(r.raw_load.data(), draw.p, E * 4, cudaMemcpyDeviceToHost), "d2h");
+  cuda_check(cudaMemcpy(cnt.data(), dcnt.p, E * 4, cudaMemcpyDeviceToHost), "d2h");
+  cuda_check(cudaMemcpy(rows.data(), drows.p, rows.size() * 4, cudaMemcpyDeviceToHost), "d2h");
+  cuda_check(cudaMemcpy(slots.data(), dslots.p, slots.size() * 4, cudaMemcpyDeviceToHost), "d2h");
+  cuda_check(cudaMemcpy(&r.dropped, ddrop.p, 4, cudaMemcpyDeviceToHost), "d2h");
+  r.offsets.assign(static_cast<std::size_t>(E) + 1, 0);
+  for (int e = 0; e < E; ++e) {
+    r.offsets[static_cast<std::size_t>(e) + 1] = r.offsets[static_cast<std::size_t>(e)] + cnt[static_cast<std::size_t>(e)];
+    for (int i = 0; i < cnt[static_cast<std::size_t>(e)]; ++i) {
+      r.rows.push_back(rows[static_cast<std::size_t>(e) * seg + i]);
+      r.slots.push_back(slots[static_cast<std::size_t>(e) * seg + i]);
+    }
+  }
+  return r;
+}
+
+}  // namespace p2r

@@ -75,7 +75,7 @@ P2R_DEVICE Tile get_tile(const GemmParams& p, int t, int BN) {
     T.valid = T.m_blk * BM < cnt;
     T.a_row = T.g * p.seg_rows + T.m_blk * BM;
     T.b_row = T.g * p.n + T.n_blk * BN;
-    T.kbase = 0;
+    T.kbase = T.g * p.k;  // MN-major B: stacked [groups*k, n]
     T.kb0 = 0;
     T.kb1 = p.num_k_blk;
   } else if (p.group_mode == P2R_GROUP_K) {
@@ -544,8 +544,10 @@ extern "C" p2r_status p2r_gemm(const p2r_gemm_args* a, void* stream) {
   if (a->group_mode != P2R_GROUP_NONE && (a->counts == nullptr || a->groups <= 0 ||
                                           a->seg_rows <= 0 || (a->seg_rows % BM) != 0))
     return set_error(P2R_EINVAL, "gemm: grouped GEMM needs counts and seg_rows % 128 == 0");
-  if (a->group_mode == P2R_GROUP_M && (a->a_mn_major || a->b_mn_major))
-    return set_error(P2R_EINVAL, "gemm: GROUP_M needs K-major operands");
+  if (a->group_mode == P2R_GROUP_M && a->a_mn_major)
+    return set_error(P2R_EINVAL, "gemm: GROUP_M needs a K-major A");
+  if (a->group_mode == P2R_GROUP_M && a->b_mn_major && (a->k % BK) != 0)
+    return set_error(P2R_EINVAL, "gemm: GROUP_M with MN-major B needs k % 64 == 0");
   if (a->group_mode == P2R_GROUP_K && !(a->a_mn_major && a->b_mn_major))
     return set_error(P2R_EINVAL, "gemm: GROUP_K needs MN-major operands");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -599,7 +601,8 @@ extern "C" p2r_status p2r_gemm(const p2r_gemm_args* a, void* stream) {
   const long long b_rows_k = a->group_mode == P2R_GROUP_M ? 1LL * a->groups * a->n : a->n;
   bool ok = a->a_mn_major ? make_map(&ta, a->a, a_rows_mn, a->m, a->lda, 64, 64)
                           : make_map(&ta, a->a, a_rows_k, a->k, a->lda, 64, BM);
-  ok = ok && (a->b_mn_major ? make_map(&tb, a->b, a_rows_mn, a->n, a->ldb, 64, 64)
+  const long long b_rows_mn = a->group_mode == P2R_GROUP_M ? 1LL * a->groups * a->k : a_rows_mn;
+  ok = ok && (a->b_mn_major ? make_map(&tb, a->b, b_rows_mn, a->n, a->ldb, 64, 64)
                             : make_map(&tb, a->b, b_rows_k, a->k, a->ldb, 64, BN));
   if (!ok) return set_error(P2R_ECUDA, "gemm: cuTensorMapEncodeTiled failed");
 

@@ -1,0 +1,269 @@
+"""Python mirror of the reference's Model / AdamW / moe_dispatch surface
+(/root/reference/proj/core/include/p2r/model.hpp, optim.hpp) over the C-ABI in
+include/p2r_engine.h. Method names match oracle/ref.RefModel so parity tests
+read the same against either side. All compute runs in libp2r.so (sm_100a);
+there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, lib
+
+vp, ip, fp, i64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_float, ctypes.c_int64
+
+
+class ModelConfigC(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int) for n in (
+        "d_model", "d_ff", "n_layers_graph", "n_layers_params", "n_heads", "vocab_size",
+        "seq_len", "n_experts", "n_prototypes", "n_shards")] + [("capacity_factor", ctypes.c_float)]
+
+
+_lib._EXTRA_SIGNATURES.update({
+    "p2r_count_params": [ctypes.POINTER(ModelConfigC), vp],
+    "p2r_model_create": [ctypes.POINTER(ModelConfigC), ctypes.c_uint64, ctypes.POINTER(vp)],
+    "p2r_model_destroy": [vp],
+    "p2r_model_param_info": [vp, ip, ctypes.c_char_p, ctypes.POINTER(ip), vp, ctypes.POINTER(i64)],
+    "p2r_model_get_param": [vp, ip, vp],
+    "p2r_model_set_param": [vp, ip, vp],
+    "p2r_model_get_grad": [vp, ip, vp],
+    "p2r_model_forward": [vp, vp, ip, ip, ip, vp],
+    "p2r_model_train_step": [vp, vp, vp, vp, ip, ip, ctypes.c_double, ip, ip, vp],
+    "p2r_model_train_step_device": [vp, vp, vp, vp, ip, ip, ctypes.c_double, ip, ip, vp],
+    "p2r_model_adamw_attach": [vp, fp, fp, fp, fp],
+    "p2r_model_adamw_step": [vp, fp],
+    "p2r_model_adamw_set_step_count": [vp, i64],
+    "p2r_model_get_moment": [vp, ip, ip, vp],
+    "p2r_model_delinked": [vp, ctypes.POINTER(vp)],
+    "p2r_model_routing": [vp, ip, vp, vp, vp, ctypes.POINTER(ip), ctypes.POINTER(ip)],
+    "p2r_moe_dispatch_host": [vp, ip, ip, ip, fp, vp, vp, vp, vp, vp, vp,
+                              ctypes.POINTER(ip), ctypes.POINTER(ip)],
+})
+
+
+def _declare_extra():
+    L = lib()
+    L.p2r_model_num_params.argtypes = [vp]
+    L.p2r_model_num_params.restype = ctypes.c_int
+    L.p2r_model_adamw_step_count.argtypes = [vp]
+    L.p2r_model_adamw_step_count.restype = i64
+    for n in ("p2r_model_state_bytes", "p2r_model_grad_bytes", "p2r_model_scratch_grad_bytes"):
+        getattr(L, n).argtypes = [vp]
+        getattr(L, n).restype = i64
+    L.p2r_model_stream.argtypes = [vp]
+    L.p2r_model_stream.restype = vp
+    L.p2r_lr_at.argtypes = [fp, ctypes.c_double, i64, i64]
+    L.p2r_lr_at.restype = fp
+    L.p2r_moe_capacity.argtypes = [fp, ip, ip, ip]
+    L.p2r_moe_capacity.restype = ctypes.c_int
+    return L
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(vp)
+
+
+@dataclass
+class Config:
+    """ModelConfig + MoEConfig (model.hpp:13-41), same fields and defaults."""
+    d_model: int = 128
+    d_ff: int = 512
+    n_layers_graph: int = 8
+    n_layers_params: int = 8
+    n_heads: int = 4
+    vocab_size: int = 260
+    seq_len: int = 64
+    n_experts: int = 0
+    n_prototypes: int = 1
+    n_shards: int = 1
+    capacity_factor: float = 1.25
+
+    def c(self) -> ModelConfigC:
+        return ModelConfigC(self.d_model, self.d_ff, self.n_layers_graph, self.n_layers_params,
+                            self.n_heads, self.vocab_size, self.seq_len, self.n_experts,
+                            self.n_prototypes, self.n_shards, self.capacity_factor)
+
+    def shared(self) -> bool:
+        return self.n_layers_params == 1 and self.n_layers_graph > 1
+
+    def as_unshared(self) -> "Config":
+        return Config(**{**self.__dict__, "n_layers_params": self.n_layers_graph})
+
+
+def count_params(cfg: Config):
+    _declare_extra()
+    out = np.zeros(3, np.int64)
+    check(lib().p2r_count_params(ctypes.byref(cfg.c()), _p(out)))
+    return tuple(int(x) for x in out)
+
+
+def lr_at(peak, warmup_ratio, total, step) -> float:
+    return float(_declare_extra().p2r_lr_at(peak, warmup_ratio, total, step))
+
+
+class Model:
+    """p2r::Model + AdamW on one B200 (one CUDA stream per model)."""
+
+    def __init__(self, cfg: Config, seed: int = 1234, handle=None):
+        L = _declare_extra()
+        self.cfg = cfg
+        if handle is None:
+            h = vp()
+            check(L.p2r_model_create(ctypes.byref(cfg.c()), seed, ctypes.byref(h)))
+            handle = h.value
+        self.h = handle
+        self.names, self.shapes = [], []
+        name = ctypes.create_string_buffer(128)
+        nd, shp, ne = ctypes.c_int(), (ctypes.c_int * 4)(), ctypes.c_int64()
+        for i in range(L.p2r_model_num_params(self.h)):
+            check(L.p2r_model_param_info(self.h, i, name, ctypes.byref(nd), shp, ctypes.byref(ne)))
+            self.names.append(name.value.decode())
+            self.shapes.append(tuple(shp[j] for j in range(nd.value)))
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().p2r_model_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- parameters (for_each_param order)
+    def _get(self, fn, i, shape):
+        a = np.empty(shape, np.float32)
+        check(fn(self.h, i, _p(a)))
+        return a
+
+    def params(self) -> dict:
+        return {n: self._get(lib().p2r_model_get_param, i, s)
+                for i, (n, s) in enumerate(zip(self.names, self.shapes))}
+
+    def set_params(self, params: dict):
+        for i, n in enumerate(self.names):
+            a = np.ascontiguousarray(params[n], dtype=np.float32)
+            check(lib().p2r_model_set_param(self.h, i, _p(a)))
+
+    def grads(self) -> dict:
+        return {n: self._get(lib().p2r_model_get_grad, i, s)
+                for i, (n, s) in enumerate(zip(self.names, self.shapes))}
+
+    def moments(self) -> dict:
+        out = {}
+        for i, (n, s) in enumerate(zip(self.names, self.shapes)):
+            m = np.empty(s, np.float32)
+            v = np.empty(s, np.float32)
+            check(lib().p2r_model_get_moment(self.h, i, 0, _p(m)))
+            check(lib().p2r_model_get_moment(self.h, i, 1, _p(v)))
+            out[n] = (m, v)
+        return out
+
+    # ---- compute
+    def forward(self, tokens, batch: int, causal: bool = True) -> np.ndarray:
+        tok = np.ascontiguousarray(tokens, np.int32)
+        out = np.empty((tok.size, self.cfg.vocab_size), np.float32)
+        check(lib().p2r_model_forward(self.h, _p(tok), batch, tok.size // batch, int(causal), _p(out)))
+        return out
+
+    def train_step(self, tokens, targets, mask, batch, denom, causal=True, zero=True,
+                   segmented=False) -> float:
+        del segmented  # one fused backward; equivalent to the reference's segmented variant
+        tok = np.ascontiguousarray(tokens, np.int32)
+        tgt = np.ascontiguousarray(targets, np.int32)
+        msk = None if mask is None else np.ascontiguousarray(mask, np.uint8)
+        loss = ctypes.c_float()
+        check(lib().p2r_model_train_step(self.h, _p(tok), _p(tgt), _p(msk), batch, tok.size // batch,
+                                         float(denom), int(causal), int(zero), ctypes.byref(loss)))
+        return float(loss.value)
+
+    def train_step_device(self, d_tokens: int, d_targets: int, d_mask, batch: int, seq: int,
+                          denom: float, causal=True, zero=True, loss_dev=None):
+        check(lib().p2r_model_train_step_device(self.h, d_tokens, d_targets, d_mask, batch, seq,
+                                                float(denom), int(causal), int(zero), loss_dev))
+
+    def stream(self) -> int:
+        return int(lib().p2r_model_stream(self.h) or 0)
+
+    def scratch_grad_bytes(self) -> int:
+        return int(lib().p2r_model_scratch_grad_bytes(self.h))
+
+    def grad_bytes(self) -> int:
+        return int(lib().p2r_model_grad_bytes(self.h))
+
+    def state_bytes(self) -> int:
+        return int(lib().p2r_model_state_bytes(self.h))
+
+    def delinked(self) -> "Model":
+        h = vp()
+        check(lib().p2r_model_delinked(self.h, ctypes.byref(h)))
+        return Model(self.cfg.as_unshared(), handle=h.value)
+
+    # ---- optimizer
+    def attach_adamw(self, b1=0.9, b2=0.999, eps=1e-8, wd=0.01):
+        check(lib().p2r_model_adamw_attach(self.h, b1, b2, eps, wd))
+
+    def adamw_step(self, lr: float):
+        check(lib().p2r_model_adamw_step(self.h, lr))
+
+    def step_count(self) -> int:
+        return int(lib().p2r_model_adamw_step_count(self.h))
+
+    def set_step_count(self, t: int):
+        check(lib().p2r_model_adamw_set_step_count(self.h, t))
+
+    def layer_routing(self, g: int, n_tokens: int):
+        k = self.cfg.n_prototypes
+        sel = np.empty(n_tokens * k, np.int32)
+        sur = np.empty(n_tokens * k, np.uint8)
+        raw = np.empty(self.cfg.n_experts, np.int32)
+        cap, drop = ctypes.c_int(), ctypes.c_int()
+        check(lib().p2r_model_routing(self.h, g, _p(sel), _p(sur), _p(raw), ctypes.byref(cap),
+                                      ctypes.byref(drop)))
+        return sel, sur, raw, cap.value, drop.value
+
+
+@dataclass
+class Routing:
+    """p2r::Routing (model.hpp:77-87); expert_rows/slots flattened CSR-style."""
+    selected: np.ndarray
+    survived: np.ndarray
+    raw_load: np.ndarray
+    offsets: np.ndarray
+    rows: np.ndarray
+    slots: np.ndarray
+    capacity: int
+    dropped: int
+    expert_rows: list = field(default_factory=list)
+    expert_slots: list = field(default_factory=list)
+
+
+def moe_dispatch(logits: np.ndarray, n_experts: int, n_prototypes: int = 1,
+                 capacity_factor: float = 1.25) -> Routing:
+    """moe_dispatch (model.cpp:294-332) computed by the sm_100a routing kernel."""
+    lg = np.ascontiguousarray(logits, np.float32)
+    if lg.ndim != 2 or lg.shape[1] != n_experts:
+        raise _lib.P2RInvalidArgument("moe_dispatch: logits must be [tokens, n_experts]")
+    T, k = lg.shape[0], n_prototypes
+    sel = np.empty(max(T * k, 1), np.int32)
+    sur = np.empty(max(T * k, 1), np.uint8)
+    raw = np.empty(n_experts, np.int32)
+    off = np.empty(n_experts + 1, np.int32)
+    rows = np.empty(max(T * k, 1), np.int32)
+    slots = np.empty(max(T * k, 1), np.int32)
+    cap, drop = ctypes.c_int(), ctypes.c_int()
+    _declare_extra()
+    check(lib().p2r_moe_dispatch_host(_p(lg), T, n_experts, k, capacity_factor, _p(sel), _p(sur),
+                                      _p(raw), _p(off), _p(rows), _p(slots), ctypes.byref(cap),
+                                      ctypes.byref(drop)))
+    n = int(off[-1])
+    r = Routing(sel[:T * k], sur[:T * k], raw, off, rows[:n].copy(), slots[:n].copy(), cap.value,
+                drop.value)
+    r.expert_rows = [r.rows[off[e]:off[e + 1]] for e in range(n_experts)]
+    r.expert_slots = [r.slots[off[e]:off[e + 1]] for e in range(n_experts)]
+    return r

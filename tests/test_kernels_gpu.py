@@ -187,7 +187,9 @@ def test_adamw_bit_exact(cuda, name):
         assert np.array_equal(Pn[o_:o_ + a.size].reshape(sh), d["p1." + n]), n
         assert np.array_equal(Mn[o_:o_ + a.size].reshape(sh), d["m." + n]), n
         assert np.array_equal(Vn[o_:o_ + a.size].reshape(sh), d["v." + n]), n
-    assert np.array_equal(p16.float().cpu().numpy(), bf16_round(Pn))
+    P16 = p16.float().cpu().numpy()
+    for o_, a in zip(offs, chunks):  # segment gaps are never touched
+        assert np.array_equal(P16[o_:o_ + a.size], bf16_round(Pn[o_:o_ + a.size]))
 
 
 def _check_routing(r, pre, d):

@@ -125,6 +125,21 @@ struct GranuleLayout {
 
 struct Acts;  // per-shape activation / workspace buffers
 
+// Live per-kernel-class timing with CUDA events on the model stream.
+struct Profiler {
+  struct Rec {
+    int cls;
+    cudaEvent_t a, b;
+    double flops, bytes;
+  };
+  bool on = false;
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  std::size_t used = 0;
+  cudaEvent_t get();
+  ~Profiler();
+};
+
 class Model {
  public:
   Model(ModelConfig config, std::uint64_t seed);
@@ -178,6 +193,10 @@ class Model {
   std::unique_ptr<Model> delinked() const;
 
   cudaStream_t stream() const { return stream_; }
+  void set_profiling(bool on) { prof_.on = on; }
+  void profile(int cls, std::int64_t* launches, double* ms, double* flops, double* bytes);
+  void profile_reset();
+  void buffer(int which, void** ptr, std::size_t* bytes) const;
   void routing_host(int g, int* selected, std::uint8_t* survived, int* raw_load, int* capacity,
                     int* dropped) const;
 
@@ -196,6 +215,19 @@ class Model {
   float* eg(long long off) const { return emb_g_.as<float>() + off; }
   void* ep16(long long off) const { return emb_p16_.as<std::uint16_t>() + off; }
   void block_backward(int g, AttentionMode mode);
+  // bracket one kernel launch with profiling events (no-op when profiling is off)
+  template <typename F>
+  void prof(int cls, double flops, double bytes, F&& launch) {
+    if (!prof_.on) {
+      launch();
+      return;
+    }
+    cudaEvent_t a = prof_.get(), b = prof_.get();
+    cudaEventRecord(a, stream_);
+    launch();
+    cudaEventRecord(b, stream_);
+    prof_.recs.push_back({cls, a, b, flops, bytes});
+  }
   void gemm(int m, int n, int k, const void* a, int lda, bool a_mn, const void* b, int ldb,
             bool b_mn, int epi, void* c, int ldc, void* c2 = nullptr, int ldc2 = 0,
             const float* bias = nullptr, const void* aux = nullptr, int ldaux = 0,
@@ -218,6 +250,7 @@ class Model {
   DevBuf dev_in_;   // tokens / targets / mask staging
   void* pinned_ = nullptr;
   std::size_t pinned_bytes_ = 0;
+  Profiler prof_;
 };
 
 // moe_dispatch on host logits via the routing kernel (bit-exact, model.cpp:294-332)

@@ -81,6 +81,31 @@ p2r_status p2r_model_delinked(const p2r_model* m, p2r_model** out);
 
 /* Raw device stream the model enqueues on (cudaStream_t). */
 void* p2r_model_stream(p2r_model* m);
+
+/* Live per-kernel-class timing: when enabled, every kernel the engine launches
+ * is bracketed by CUDA events on the model stream; p2r_model_profile reports,
+ * per class, launches, summed device ms and algorithmic FLOPs / HBM bytes. */
+enum {
+  P2R_PROF_GEMM = 0,
+  P2R_PROF_ATTN_FWD = 1,
+  P2R_PROF_ATTN_BWD = 2,
+  P2R_PROF_LAYERNORM = 3,
+  P2R_PROF_CE = 4,
+  P2R_PROF_EMBED = 5,
+  P2R_PROF_ADAMW = 6,
+  P2R_PROF_MOE = 7,
+  P2R_PROF_BIAS = 8,
+  P2R_PROF_DELINK = 9,
+  P2R_PROF_NCLASSES = 10
+};
+p2r_status p2r_model_set_profiling(p2r_model* m, int on);
+/* Synchronises the model stream, then fills the totals since the last reset. */
+p2r_status p2r_model_profile(p2r_model* m, int cls, int64_t* launches, double* ms, double* flops,
+                             double* bytes);
+p2r_status p2r_model_profile_reset(p2r_model* m);
+/* Device pointer + byte size of a parameter-side buffer: which = 0 grads of the
+ * embeddings granule, 1 grads of all owned layers (for a DP allreduce). */
+p2r_status p2r_model_buffer(p2r_model* m, int which, void** ptr, size_t* bytes);
 /* Last routing of graph layer g (MoE): host copies of moe_dispatch outputs. */
 p2r_status p2r_model_routing(const p2r_model* m, int g, int* selected, uint8_t* survived,
                              int* raw_load, int* capacity, int* dropped);

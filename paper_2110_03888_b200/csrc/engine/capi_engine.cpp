@@ -153,6 +153,24 @@ p2r_status p2r_model_delinked(const p2r_model* m, p2r_model** out) {
 
 void* p2r_model_stream(p2r_model* m) { return m->m->stream(); }
 
+p2r_status p2r_model_set_profiling(p2r_model* m, int on) {
+  m->m->set_profiling(on != 0);
+  return P2R_OK;
+}
+p2r_status p2r_model_profile(p2r_model* m, int cls, int64_t* launches, double* ms, double* flops, double* bytes) {
+  return guard([&] {
+    std::int64_t n = 0;
+    m->m->profile(cls, &n, ms, flops, bytes);
+    *launches = n;
+  });
+}
+p2r_status p2r_model_profile_reset(p2r_model* m) {
+  return guard([&] { m->m->profile_reset(); });
+}
+p2r_status p2r_model_buffer(p2r_model* m, int which, void** ptr, size_t* bytes) {
+  return guard([&] { m->m->buffer(which, ptr, bytes); });
+}
+
 p2r_status p2r_model_routing(const p2r_model* m, int g, int* selected, uint8_t* survived, int* raw_load,
                              int* capacity, int* dropped) {
   return guard([&] { m->m->routing_host(g, selected, survived, raw_load, capacity, dropped); });

@@ -18,6 +18,7 @@
 #include <string>
 
 #include "p2r_cuda.h"
+#include "p2r_engine.h"
 
 namespace p2r {
 
@@ -491,7 +492,66 @@ void Model::gemm(int m, int n, int k, const void* a, int lda, bool a_mn, const v
     if (splitk_ws_.bytes < need) splitk_ws_ = DevBuf(need);
     p2r_set_workspace(splitk_ws_.p, splitk_ws_.bytes);
   }
-  p2r_check(p2r_gemm(&g, stream_), "gemm");
+  // algorithmic FLOPs: grouped GEMMs count the routed rows (T * k), not padding
+  double rows_m = m, inner_k = k;
+  if (group_mode == P2R_GROUP_M && acts_) rows_m = static_cast<double>(acts_->T) * cfg_.moe.n_prototypes;
+  if (group_mode == P2R_GROUP_K && acts_) inner_k = static_cast<double>(acts_->T) * cfg_.moe.n_prototypes;
+  const double flops = 2.0 * rows_m * n * inner_k;
+  const double bytes = 2.0 * (rows_m * inner_k + static_cast<double>(n) * inner_k) +
+                       (epi == P2R_EPI_BF16 || epi == P2R_EPI_BIAS_GELU || epi == P2R_EPI_DGELU ? 2.0 : 4.0) *
+                           rows_m * n * (epi == P2R_EPI_ACC_F32 ? 2.0 : 1.0);
+  prof(0, flops, bytes, [&] { p2r_check(p2r_gemm(&g, stream_), "gemm"); });
+}
+
+// ---------------------------------------------------------------- profiling
+cudaEvent_t Profiler::get() {
+  if (used == pool.size()) {
+    cudaEvent_t e;
+    cuda_check(cudaEventCreate(&e), "event");
+    pool.push_back(e);
+  }
+  return pool[used++];
+}
+
+Profiler::~Profiler() {
+  for (cudaEvent_t e : pool) cudaEventDestroy(e);
+}
+
+void Model::profile(int cls, std::int64_t* launches, double* ms, double* flops, double* bytes) {
+  cuda_check(cudaStreamSynchronize(stream_), "profile sync");
+  std::int64_t n = 0;
+  double t = 0, f = 0, b = 0;
+  for (const auto& r : prof_.recs) {
+    if (r.cls != cls) continue;
+    float e = 0;
+    cuda_check(cudaEventElapsedTime(&e, r.a, r.b), "event time");
+    ++n;
+    t += e;
+    f += r.flops;
+    b += r.bytes;
+  }
+  *launches = n;
+  *ms = t;
+  *flops = f;
+  *bytes = b;
+}
+
+void Model::profile_reset() {
+  cuda_check(cudaStreamSynchronize(stream_), "profile sync");
+  prof_.recs.clear();
+  prof_.used = 0;
+}
+
+void Model::buffer(int which, void** ptr, std::size_t* bytes) const {
+  if (which == 0) {
+    *ptr = emb_g_.p;
+    *bytes = emb_g_.bytes;
+  } else if (which == 1) {
+    *ptr = lay_g_.p;
+    *bytes = lay_g_.bytes;
+  } else {
+    throw std::out_of_range("model buffer: unknown buffer id");
+  }
 }
 
 namespace {
@@ -513,13 +573,17 @@ Tensor Model::embed_forward(GradTape* tape, const int* d_tokens, int batch, int 
   ensure_acts(batch, seq);
   Acts& A = *acts_;
   const int d = cfg_.d_model;
-  p2r_check(p2r_embed_fwd(d_tokens, ep(emb_.tok), ep(emb_.pos), A.T, seq, d, A.x0.as<float>(), stream_), "embed");
+  prof(P2R_PROF_EMBED, 0, 12.0 * A.T * d, [&] {
+    p2r_check(p2r_embed_fwd(d_tokens, ep(emb_.tok), ep(emb_.pos), A.T, seq, d, A.x0.as<float>(), stream_), "embed");
+  });
   if (tape) {
     tape->record([this, d_tokens, batch, seq]() {
       Acts& A2 = *acts_;
-      p2r_check(p2r_embed_bwd(d_tokens, A2.dres.as<float>(), batch, seq, cfg_.d_model, cfg_.vocab_size,
-                              eg(emb_.tok), eg(emb_.pos), stream_),
-                "embed bwd");
+      prof(P2R_PROF_EMBED, 0, 8.0 * A2.T * cfg_.d_model, [&] {
+        p2r_check(p2r_embed_bwd(d_tokens, A2.dres.as<float>(), batch, seq, cfg_.d_model, cfg_.vocab_size,
+                                eg(emb_.tok), eg(emb_.pos), stream_),
+                  "embed bwd");
+      });
     });
   }
   return Tensor{A.T, d, A.x0.as<float>(), A.dres.as<float>(), A.dres16.p};
@@ -533,21 +597,29 @@ Tensor Model::block_forward(GradTape* tape, int g, const Tensor& x, int batch, A
   const int o = owned_index_of_graph_layer(g);
   const int T = A.T, d = cfg_.d_model, dff = cfg_.d_ff, H = cfg_.n_heads;
   const int causal = mode == AttentionMode::Causal ? 1 : 0;
+  const double Td = static_cast<double>(T) * d;
+  const double attn_flops = 2.0 * A.B * H * static_cast<double>(A.S) * A.S * (d / H) * (causal ? 1.0 : 2.0);
   // a = LN1(x)
-  p2r_check(p2r_layernorm_fwd(x.data, lp(o, layer_.ln1_g), lp(o, layer_.ln1_b), T, d, 1e-5f, L.a16.p, nullptr,
-                              L.mean1.as<float>(), L.rstd1.as<float>(), stream_),
-            "ln1");
+  prof(P2R_PROF_LAYERNORM, 0, Td * 6 + 8.0 * T, [&] {
+    p2r_check(p2r_layernorm_fwd(x.data, lp(o, layer_.ln1_g), lp(o, layer_.ln1_b), T, d, 1e-5f, L.a16.p, nullptr,
+                                L.mean1.as<float>(), L.rstd1.as<float>(), stream_),
+              "ln1");
+  });
   // qkv = a . [wq|wk|wv]  (B = fused [d, 3d] bf16, N-major)
   gemm(T, 3 * d, d, L.a16.p, d, false, lp16(o, layer_.wqkv), 3 * d, true, P2R_EPI_BF16, L.qkv16.p, 3 * d);
-  p2r_check(p2r_attention_fwd(L.qkv16.p, L.o16.p, L.lse.as<float>(), A.B, H, A.S, d, causal, stream_), "attn");
+  prof(P2R_PROF_ATTN_FWD, attn_flops, Td * 8, [&] {
+    p2r_check(p2r_attention_fwd(L.qkv16.p, L.o16.p, L.lse.as<float>(), A.B, H, A.S, d, causal, stream_), "attn");
+  });
   // x1 = x + o . wo
   gemm(T, d, d, L.o16.p, d, false, lp16(o, layer_.wo), d, true, P2R_EPI_F32, L.x1.p, d, nullptr, 0, nullptr,
        x.data, d);
   // b = LN2(x1)
   const bool moe = cfg_.moe.enabled();
-  p2r_check(p2r_layernorm_fwd(L.x1.as<float>(), lp(o, layer_.ln2_g), lp(o, layer_.ln2_b), T, d, 1e-5f, L.b16.p,
-                              moe ? L.b32.as<float>() : nullptr, L.mean2.as<float>(), L.rstd2.as<float>(), stream_),
-            "ln2");
+  prof(P2R_PROF_LAYERNORM, 0, Td * (moe ? 10 : 6) + 8.0 * T, [&] {
+    p2r_check(p2r_layernorm_fwd(L.x1.as<float>(), lp(o, layer_.ln2_g), lp(o, layer_.ln2_b), T, d, 1e-5f, L.b16.p,
+                                moe ? L.b32.as<float>() : nullptr, L.mean2.as<float>(), L.rstd2.as<float>(), stream_),
+              "ln2");
+  });
   if (!moe) {
     gemm(T, dff, d, L.b16.p, d, false, lp16(o, layer_.w1), dff, true, P2R_EPI_BIAS_GELU, L.g16.p, dff, L.hpre16.p,
          dff, lp(o, layer_.b1));
@@ -597,16 +669,20 @@ void Model::block_backward(int g, AttentionMode mode) {
     // FFN2: dW2 += g^T dy ; db2 += colsum(dy) ; dh = (dy W2^T) * gelu'(hpre)
     gemm(dff, d, T, L.g16.p, dff, true, dy16, d, true, P2R_EPI_ACC_F32, lg(o, layer_.w2), d, nullptr, 0, nullptr,
          nullptr, 0, 0, 0, 0, nullptr, pick_split(dff, d, T));
-    p2r_check(p2r_bias_grad(dy, 0, d, T, d, 1, 0, nullptr, lg(o, layer_.b2), 0, A.colsum_ws.as<float>(), stream_),
-              "db2");
+    prof(P2R_PROF_BIAS, 0, 4.0 * T * d, [&] {
+      p2r_check(p2r_bias_grad(dy, 0, d, T, d, 1, 0, nullptr, lg(o, layer_.b2), 0, A.colsum_ws.as<float>(), stream_),
+                "db2");
+    });
     gemm(T, dff, d, dy16, d, false, lp16(o, layer_.w2), d, false, P2R_EPI_DGELU, A.dh16.p, dff, nullptr, 0, nullptr,
          L.hpre16.p, dff);
     // FFN1: dW1 += b^T dh ; db1 += colsum(dh) ; db = dh W1^T
     gemm(d, dff, T, L.b16.p, d, true, A.dh16.p, dff, true, P2R_EPI_ACC_F32, lg(o, layer_.w1), dff, nullptr, 0,
          nullptr, nullptr, 0, 0, 0, 0, nullptr, pick_split(d, dff, T));
-    p2r_check(p2r_bias_grad(A.dh16.p, 1, dff, T, dff, 1, 0, nullptr, lg(o, layer_.b1), 0, A.colsum_ws.as<float>(),
-                            stream_),
-              "db1");
+    prof(P2R_PROF_BIAS, 0, 2.0 * T * dff, [&] {
+      p2r_check(p2r_bias_grad(A.dh16.p, 1, dff, T, dff, 1, 0, nullptr, lg(o, layer_.b1), 0, A.colsum_ws.as<float>(),
+                              stream_),
+                "db1");
+    });
     gemm(T, d, dff, A.dh16.p, dff, false, lp16(o, layer_.w1), dff, false, P2R_EPI_F32, A.tmp32.p, d);
   } else {
     const int E = cfg_.moe.n_experts, k = cfg_.moe.n_prototypes, seg = A.seg;
@@ -643,35 +719,45 @@ void Model::block_backward(int g, AttentionMode mode) {
                                    lp(o, layer_.gate), E, A.tmp32.as<float>(), 0, stream_),
               "dispatch bwd");
   }
+  const double Td = static_cast<double>(T) * d;
+  const double attn_flops = 4.0 * A.B * H * static_cast<double>(A.S) * A.S * (d / H) * (causal ? 1.0 : 2.0);
   // LN2 backward: dx1 = dy + LN2'(db)
-  p2r_check(p2r_layernorm_bwd(A.tmp32.as<float>(), L.x1.as<float>(), L.mean2.as<float>(), L.rstd2.as<float>(),
-                              lp(o, layer_.ln2_g), dy, T, d, A.dx1.as<float>(), A.dx1_16.p, lg(o, layer_.ln2_g),
-                              lg(o, layer_.ln2_b), A.ln_ws.as<float>(), stream_),
-            "ln2 bwd");
+  prof(P2R_PROF_LAYERNORM, 0, Td * 18, [&] {
+    p2r_check(p2r_layernorm_bwd(A.tmp32.as<float>(), L.x1.as<float>(), L.mean2.as<float>(), L.rstd2.as<float>(),
+                                lp(o, layer_.ln2_g), dy, T, d, A.dx1.as<float>(), A.dx1_16.p, lg(o, layer_.ln2_g),
+                                lg(o, layer_.ln2_b), A.ln_ws.as<float>(), stream_),
+              "ln2 bwd");
+  });
   // O projection: dWo += o^T dx1 ; do = dx1 Wo^T
   gemm(d, d, T, L.o16.p, d, true, A.dx1_16.p, d, true, P2R_EPI_ACC_F32, lg(o, layer_.wo), d, nullptr, 0, nullptr,
        nullptr, 0, 0, 0, 0, nullptr, pick_split(d, d, T));
   gemm(T, d, d, A.dx1_16.p, d, false, lp16(o, layer_.wo), d, false, P2R_EPI_BF16, A.do16.p, d);
-  p2r_check(p2r_attention_bwd(L.qkv16.p, L.o16.p, L.lse.as<float>(), A.do16.p, A.dsum.as<float>(), A.dqkv16.p, A.B,
-                              H, A.S, d, causal, stream_),
-            "attn bwd");
+  prof(P2R_PROF_ATTN_BWD, attn_flops, Td * 16, [&] {
+    p2r_check(p2r_attention_bwd(L.qkv16.p, L.o16.p, L.lse.as<float>(), A.do16.p, A.dsum.as<float>(), A.dqkv16.p,
+                                A.B, H, A.S, d, causal, stream_),
+              "attn bwd");
+  });
   // QKV: dWqkv += a^T dqkv ; da = dqkv Wqkv^T
   gemm(d, 3 * d, T, L.a16.p, d, true, A.dqkv16.p, 3 * d, true, P2R_EPI_ACC_F32, lg(o, layer_.wqkv), 3 * d, nullptr,
        0, nullptr, nullptr, 0, 0, 0, 0, nullptr, pick_split(d, 3 * d, T));
   gemm(T, d, 3 * d, A.dqkv16.p, 3 * d, false, lp16(o, layer_.wqkv), 3 * d, false, P2R_EPI_F32, A.tmp32.p, d);
   // LN1 backward: dx = dx1 + LN1'(da)
-  p2r_check(p2r_layernorm_bwd(A.tmp32.as<float>(), xin, L.mean1.as<float>(), L.rstd1.as<float>(), lp(o, layer_.ln1_g),
-                              A.dx1.as<float>(), T, d, dy, dy16, lg(o, layer_.ln1_g), lg(o, layer_.ln1_b),
-                              A.ln_ws.as<float>(), stream_),
-            "ln1 bwd");
+  prof(P2R_PROF_LAYERNORM, 0, Td * 18, [&] {
+    p2r_check(p2r_layernorm_bwd(A.tmp32.as<float>(), xin, L.mean1.as<float>(), L.rstd1.as<float>(),
+                                lp(o, layer_.ln1_g), A.dx1.as<float>(), T, d, dy, dy16, lg(o, layer_.ln1_g),
+                                lg(o, layer_.ln1_b), A.ln_ws.as<float>(), stream_),
+              "ln1 bwd");
+  });
 }
 
 Tensor Model::head_forward(GradTape* tape, const Tensor& x) {
   Acts& A = *acts_;
   const int T = A.T, d = cfg_.d_model, V = cfg_.vocab_size;
-  p2r_check(p2r_layernorm_fwd(x.data, ep(emb_.fin_g), ep(emb_.fin_b), T, d, 1e-5f, A.h16.p, nullptr,
-                              A.meanf.as<float>(), A.rstdf.as<float>(), stream_),
-            "final ln");
+  prof(P2R_PROF_LAYERNORM, 0, 6.0 * T * d + 8.0 * T, [&] {
+    p2r_check(p2r_layernorm_fwd(x.data, ep(emb_.fin_g), ep(emb_.fin_b), T, d, 1e-5f, A.h16.p, nullptr,
+                                A.meanf.as<float>(), A.rstdf.as<float>(), stream_),
+              "final ln");
+  });
   // logits = h . tok^T  (tied head, matmul_nt)
   gemm(T, V, d, A.h16.p, d, false, ep16(emb_.tok), d, false, P2R_EPI_F32, A.logits32.p, A.vld);
   if (tape) {
@@ -683,10 +769,12 @@ Tensor Model::head_forward(GradTape* tape, const Tensor& x) {
       gemm(V2, d2, T2, A2.dlogits16.p, A2.vld, true, A2.h16.p, d2, true, P2R_EPI_ACC_F32, eg(emb_.tok), d2, nullptr,
            0, nullptr, nullptr, 0, 0, 0, 0, nullptr, pick_split(V2, d2, T2));
       gemm(T2, d2, V2, A2.dlogits16.p, A2.vld, false, ep16(emb_.tok), d2, true, P2R_EPI_F32, A2.dh32.p, d2);
-      p2r_check(p2r_layernorm_bwd(A2.dh32.as<float>(), xin, A2.meanf.as<float>(), A2.rstdf.as<float>(),
-                                  ep(emb_.fin_g), nullptr, T2, d2, A2.dres.as<float>(), A2.dres16.p, eg(emb_.fin_g),
-                                  eg(emb_.fin_b), A2.ln_ws.as<float>(), stream_),
-                "final ln bwd");
+      prof(P2R_PROF_LAYERNORM, 0, 14.0 * T2 * d2, [&] {
+        p2r_check(p2r_layernorm_bwd(A2.dh32.as<float>(), xin, A2.meanf.as<float>(), A2.rstdf.as<float>(),
+                                    ep(emb_.fin_g), nullptr, T2, d2, A2.dres.as<float>(), A2.dres16.p,
+                                    eg(emb_.fin_g), eg(emb_.fin_b), A2.ln_ws.as<float>(), stream_),
+                  "final ln bwd");
+      });
     });
   }
   return Tensor{T, V, A.logits32.as<float>(), nullptr, nullptr};
@@ -696,10 +784,12 @@ Tensor Model::softmax_cross_entropy(GradTape* /*tape*/, const Tensor& logits, co
                                     const std::uint8_t* d_mask, double denom) {
   if (denom <= 0.0) throw std::invalid_argument("softmax_cross_entropy: denominator must be > 0");
   Acts& A = *acts_;
-  p2r_check(p2r_cross_entropy(logits.data, A.T, cfg_.vocab_size, A.vld, d_targets, d_mask, denom, 1.0f,
-                              A.dlogits16.p, A.vld, A.loss.as<float>(), A.loss_sum.as<double>(),
-                              A.ce_ws.as<double>(), stream_),
-            "cross entropy");
+  prof(P2R_PROF_CE, 0, 6.0 * A.T * A.vld, [&] {
+    p2r_check(p2r_cross_entropy(logits.data, A.T, cfg_.vocab_size, A.vld, d_targets, d_mask, denom, 1.0f,
+                                A.dlogits16.p, A.vld, A.loss.as<float>(), A.loss_sum.as<double>(),
+                                A.ce_ws.as<double>(), stream_),
+              "cross entropy");
+  });
   return Tensor{1, 1, A.loss.as<float>(), nullptr, nullptr};
 }
 
@@ -816,9 +906,11 @@ void Model::adamw_step(float lr) {
       len.push_back(s.len);
       dec.push_back(s.decay ? 1 : 0);
     }
-    p2r_check(p2r_adamw_step(p, g, m, v, p16, off.data(), len.data(), dec.data(), static_cast<int>(off.size()), b1_,
-                             b2_, eps_, wd_, lr, bc1, bc2, stream_),
-              "adamw");
+    prof(P2R_PROF_ADAMW, 0, 30.0 * lay.numel, [&] {
+      p2r_check(p2r_adamw_step(p, g, m, v, p16, off.data(), len.data(), dec.data(), static_cast<int>(off.size()),
+                               b1_, b2_, eps_, wd_, lr, bc1, bc2, stream_),
+                "adamw");
+    });
   };
   run(emb_, emb_p_.as<float>(), emb_g_.as<float>(), emb_m_.as<float>(), emb_v_.as<float>(), emb_p16_.p);
   for (int i = 0; i < n_owned_; ++i)

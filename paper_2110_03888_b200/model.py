@@ -42,6 +42,11 @@ _lib._EXTRA_SIGNATURES.update({
     "p2r_model_routing": [vp, ip, vp, vp, vp, ctypes.POINTER(ip), ctypes.POINTER(ip)],
     "p2r_moe_dispatch_host": [vp, ip, ip, ip, fp, vp, vp, vp, vp, vp, vp,
                               ctypes.POINTER(ip), ctypes.POINTER(ip)],
+    "p2r_model_set_profiling": [vp, ip],
+    "p2r_model_profile": [vp, ip, ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_double),
+                          ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)],
+    "p2r_model_profile_reset": [vp],
+    "p2r_model_buffer": [vp, ip, ctypes.POINTER(vp), ctypes.POINTER(ctypes.c_size_t)],
 })
 
 
@@ -189,6 +194,31 @@ class Model:
 
     def stream(self) -> int:
         return int(lib().p2r_model_stream(self.h) or 0)
+
+    PROF_CLASSES = ("gemm", "attn_fwd", "attn_bwd", "layernorm", "cross_entropy", "embed", "adamw",
+                    "moe", "bias_grad", "delink")
+
+    def set_profiling(self, on: bool):
+        check(lib().p2r_model_set_profiling(self.h, int(on)))
+
+    def profile(self) -> dict:
+        """{class: (launches, device ms, algorithmic flops, algorithmic bytes)} since last reset."""
+        out = {}
+        n, ms, fl, by = ctypes.c_int64(), ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        for i, name in enumerate(self.PROF_CLASSES):
+            check(lib().p2r_model_profile(self.h, i, ctypes.byref(n), ctypes.byref(ms), ctypes.byref(fl),
+                                          ctypes.byref(by)))
+            out[name] = (int(n.value), float(ms.value), float(fl.value), float(by.value))
+        return out
+
+    def profile_reset(self):
+        check(lib().p2r_model_profile_reset(self.h))
+
+    def buffer(self, which: int):
+        """(device pointer, bytes) of the embeddings (0) / owned-layers (1) gradient granules."""
+        p, n = vp(), ctypes.c_size_t()
+        check(lib().p2r_model_buffer(self.h, which, ctypes.byref(p), ctypes.byref(n)))
+        return int(p.value), int(n.value)
 
     def scratch_grad_bytes(self) -> int:
         return int(lib().p2r_model_scratch_grad_bytes(self.h))

@@ -46,6 +46,7 @@ struct GemmParams {
   int split_k;
   int tiles_total;
   long long c_split_stride;  // elements between split-K partial outputs
+  int vec4;                  // all epilogue leading dims / bases allow 4-wide accesses
 };
 
 struct Tile {
@@ -114,145 +115,142 @@ struct GemmCfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (196608 / STAGE_BYTES) > 8 ? 8 : (196608 / STAGE_BYTES);
   static constexpr int TMEM_COLS = (2 * BN) < 32 ? 32 : (2 * BN);
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int SMEM_BYTES =
+      STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + 8 * 4096 /*epilogue transpose*/;
 };
 
-P2R_DEVICE void store_bf16x32(__nv_bfloat16* dst, const float* v) {
-  uint32_t w[16];
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
-    w[j] = *reinterpret_cast<uint32_t*>(&h);
-  }
-  uint4* d = reinterpret_cast<uint4*>(dst);
-#pragma unroll
-  for (int j = 0; j < 4; ++j) d[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
-}
-P2R_DEVICE void store_f32x32(float* dst, const float* v) {
-  float4* d = reinterpret_cast<float4*>(dst);
-#pragma unroll
-  for (int j = 0; j < 8; ++j) d[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-}
-P2R_DEVICE void load_f32x32(const float* src, float* v) {
-  const float4* s = reinterpret_cast<const float4*>(src);
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    float4 q = s[j];
-    v[4 * j] = q.x;
-    v[4 * j + 1] = q.y;
-    v[4 * j + 2] = q.z;
-    v[4 * j + 3] = q.w;
-  }
-}
-P2R_DEVICE void load_bf16x32(const __nv_bfloat16* src, float* v) {
-  const uint4* s = reinterpret_cast<const uint4*>(src);
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    uint4 q = s[j];
-    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&w[i]);
-      float2 f = __bfloat1622float2(h);
-      v[8 * j + 2 * i] = f.x;
-      v[8 * j + 2 * i + 1] = f.y;
+// Epilogue for ONE element: lane = column, so every global access of a warp is
+// row-contiguous (coalesced). `zero` stores zeros (padding rows of a grouped
+// segment) so later grouped-K GEMMs see clean K padding.
+P2R_DEVICE void epilogue_elem(const GemmParams& p, float v, long long row, int col, bool zero,
+                              float b, char* cbase, int ldc) {
+  const int epi = p.epi;
+  if (zero) v = 0.0f;
+  switch (epi) {
+    case P2R_EPI_BF16:
+      reinterpret_cast<__nv_bfloat16*>(cbase)[row * ldc + col] = __float2bfloat16_rn(zero ? 0.0f : v + b);
+      break;
+    case P2R_EPI_F32:
+    case P2R_EPI_F32_BF16: {
+      if (!zero) {
+        v += b;
+        if (p.aux != nullptr) v += reinterpret_cast<const float*>(p.aux)[row * p.ldaux + col];
+      }
+      reinterpret_cast<float*>(cbase)[row * ldc + col] = v;
+      if (epi == P2R_EPI_F32_BF16)
+        reinterpret_cast<__nv_bfloat16*>(p.c2)[row * p.ldc2 + col] = __float2bfloat16_rn(v);
+      break;
     }
+    case P2R_EPI_ACC_F32: {
+      if (zero) break;
+      float* d = reinterpret_cast<float*>(cbase) + row * ldc + col;
+      *d = *d + v;
+      break;
+    }
+    case P2R_EPI_BIAS_GELU: {
+      const float pre = zero ? 0.0f : v + b;
+      reinterpret_cast<__nv_bfloat16*>(p.c2)[row * p.ldc2 + col] = __float2bfloat16_rn(pre);
+      reinterpret_cast<__nv_bfloat16*>(cbase)[row * ldc + col] = __float2bfloat16_rn(zero ? 0.0f : gelu_f(pre));
+      break;
+    }
+    case P2R_EPI_DGELU: {
+      float o = 0.0f;
+      if (!zero) {
+        const float pre = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p.aux)[row * p.ldaux + col]);
+        o = v * gelu_grad_f(pre);
+      }
+      reinterpret_cast<__nv_bfloat16*>(cbase)[row * ldc + col] = __float2bfloat16_rn(o);
+      break;
+    }
+    default:
+      break;
   }
 }
 
-// Epilogue for one 32-column chunk of one row. `zero_row` stores zeros (padding
-// rows of a grouped segment) so later grouped-K GEMMs see clean padding.
-P2R_DEVICE void epilogue_chunk(const GemmParams& p, float* v, long long row, int col0, int ncols,
-                               bool vec_ok, char* cbase, int ldc, bool zero_row,
-                               const float* bias) {
-  const int epi = p.epi;
-  if (zero_row) {
+P2R_DEVICE uint2 pack4_bf16(float a, float b, float c, float d) {
+  __nv_bfloat162 lo = __floats2bfloat162_rn(a, b), hi = __floats2bfloat162_rn(c, d);
+  uint2 w;
+  w.x = *reinterpret_cast<uint32_t*>(&lo);
+  w.y = *reinterpret_cast<uint32_t*>(&hi);
+  return w;
+}
+P2R_DEVICE float4 unpack4_bf16(uint2 w) {
+  const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w.x));
+  const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w.y));
+  return make_float4(lo.x, lo.y, hi.x, hi.y);
+}
+
+// Epilogue for 4 consecutive columns of one row (16 B fp32 / 8 B bf16 accesses).
+P2R_DEVICE void epilogue_vec4(const GemmParams& p, float4 v, long long row, int col, int nc, bool zero,
+                              float4 b, char* cbase, int ldc) {
+  if (nc < 4 || !p.vec4) {
+    const float vv[4] = {v.x, v.y, v.z, v.w};
+    const float bb[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = 0.0f;
-  } else {
-    if (bias != nullptr && (epi == P2R_EPI_BF16 || epi == P2R_EPI_F32 || epi == P2R_EPI_BIAS_GELU ||
-                              epi == P2R_EPI_F32_BF16)) {
-#pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] += (j < ncols) ? __ldg(bias + col0 + j) : 0.0f;
-    }
+    for (int j = 0; j < 4; ++j)
+      if (j < nc) epilogue_elem(p, vv[j], row, col + j, zero, bb[j], cbase, ldc);
+    return;
   }
-  if (epi == P2R_EPI_BF16) {
-    __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(cbase) + row * ldc + col0;
-    if (vec_ok) {
-      store_bf16x32(dst, v);
-    } else {
-      for (int j = 0; j < ncols; ++j) dst[j] = __float2bfloat16_rn(v[j]);
-    }
-  } else if (epi == P2R_EPI_F32 || epi == P2R_EPI_F32_BF16) {
-    float* dst = reinterpret_cast<float*>(cbase) + row * ldc + col0;
-    if (p.aux != nullptr && !zero_row) {
-      const float* src = reinterpret_cast<const float*>(p.aux) + row * p.ldaux + col0;
-      if (vec_ok) {
-        float a[32];
-        load_f32x32(src, a);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] += a[j];
+  const long long o = row * ldc + col;
+  switch (p.epi) {
+    case P2R_EPI_BF16:
+      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(cbase) + o) =
+          zero ? make_uint2(0u, 0u) : pack4_bf16(v.x + b.x, v.y + b.y, v.z + b.z, v.w + b.w);
+      break;
+    case P2R_EPI_F32:
+    case P2R_EPI_F32_BF16: {
+      if (zero) {
+        v = make_float4(0.f, 0.f, 0.f, 0.f);
       } else {
-        for (int j = 0; j < ncols; ++j) v[j] += src[j];
+        v = make_float4(v.x + b.x, v.y + b.y, v.z + b.z, v.w + b.w);
+        if (p.aux != nullptr) {
+          const float4 a = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p.aux) + row * p.ldaux + col);
+          v = make_float4(v.x + a.x, v.y + a.y, v.z + a.z, v.w + a.w);
+        }
       }
+      *reinterpret_cast<float4*>(reinterpret_cast<float*>(cbase) + o) = v;
+      if (p.epi == P2R_EPI_F32_BF16)
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.c2) + row * p.ldc2 + col) =
+            pack4_bf16(v.x, v.y, v.z, v.w);
+      break;
     }
-    if (vec_ok) {
-      store_f32x32(dst, v);
-    } else {
-      for (int j = 0; j < ncols; ++j) dst[j] = v[j];
+    case P2R_EPI_ACC_F32: {
+      if (zero) break;
+      float4* d = reinterpret_cast<float4*>(reinterpret_cast<float*>(cbase) + o);
+      const float4 a = *d;
+      *d = make_float4(a.x + v.x, a.y + v.y, a.z + v.z, a.w + v.w);
+      break;
     }
-    if (epi == P2R_EPI_F32_BF16) {
-      __nv_bfloat16* d2 = reinterpret_cast<__nv_bfloat16*>(p.c2) + row * p.ldc2 + col0;
-      if (vec_ok) {
-        store_bf16x32(d2, v);
-      } else {
-        for (int j = 0; j < ncols; ++j) d2[j] = __float2bfloat16_rn(v[j]);
+    case P2R_EPI_BIAS_GELU: {
+      const float4 pre = zero ? make_float4(0.f, 0.f, 0.f, 0.f)
+                              : make_float4(v.x + b.x, v.y + b.y, v.z + b.z, v.w + b.w);
+      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.c2) + row * p.ldc2 + col) =
+          pack4_bf16(pre.x, pre.y, pre.z, pre.w);
+      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(cbase) + o) =
+          zero ? make_uint2(0u, 0u) : pack4_bf16(gelu_f(pre.x), gelu_f(pre.y), gelu_f(pre.z), gelu_f(pre.w));
+      break;
+    }
+    case P2R_EPI_DGELU: {
+      float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (!zero) {
+        const float4 pre = unpack4_bf16(
+            *reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(p.aux) + row * p.ldaux + col));
+        r = make_float4(v.x * gelu_grad_f(pre.x), v.y * gelu_grad_f(pre.y), v.z * gelu_grad_f(pre.z),
+                        v.w * gelu_grad_f(pre.w));
       }
+      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(cbase) + o) = pack4_bf16(r.x, r.y, r.z, r.w);
+      break;
     }
-  } else if (epi == P2R_EPI_ACC_F32) {
-    float* dst = reinterpret_cast<float*>(cbase) + row * ldc + col0;
-    if (vec_ok) {
-      float a[32];
-      load_f32x32(dst, a);
-#pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = a[j] + v[j];
-      store_f32x32(dst, v);
-    } else {
-      for (int j = 0; j < ncols; ++j) dst[j] = dst[j] + v[j];
-    }
-  } else if (epi == P2R_EPI_BIAS_GELU) {
-    __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(cbase) + row * ldc + col0;
-    __nv_bfloat16* d2 = reinterpret_cast<__nv_bfloat16*>(p.c2) + row * p.ldc2 + col0;
-    float gv[32];
-#pragma unroll
-    for (int j = 0; j < 32; ++j) gv[j] = gelu_f(v[j]);
-    if (vec_ok) {
-      store_bf16x32(d2, v);
-      store_bf16x32(dst, gv);
-    } else {
-      for (int j = 0; j < ncols; ++j) {
-        d2[j] = __float2bfloat16_rn(v[j]);
-        dst[j] = __float2bfloat16_rn(gv[j]);
-      }
-    }
-  } else if (epi == P2R_EPI_DGELU) {
-    __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(cbase) + row * ldc + col0;
-    const __nv_bfloat16* pre = reinterpret_cast<const __nv_bfloat16*>(p.aux) + row * p.ldaux + col0;
-    if (vec_ok) {
-      float a[32];
-      load_bf16x32(pre, a);
-#pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = zero_row ? 0.0f : v[j] * gelu_grad_f(a[j]);
-      store_bf16x32(dst, v);
-    } else {
-      for (int j = 0; j < ncols; ++j)
-        dst[j] = __float2bfloat16_rn(zero_row ? 0.0f : v[j] * gelu_grad_f(__bfloat162float(pre[j])));
-    }
+    default:
+      break;
   }
 }
+
+constexpr int kEpiWarps = 8;                       // 2 per TMEM lane quadrant
+constexpr int kGemmThreads = 128 + 32 * kEpiWarps;  // 4 control warps + epilogue
 
 template <int BN, bool A_MN, bool B_MN>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const GemmParams p) {
   using Cfg = GemmCfg<BN>;
@@ -278,7 +276,7 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(tfull_bar + s, 1);
-      mbar_init(tempty_bar + s, 128);
+      mbar_init(tempty_bar + s, 32 * kEpiWarps);
     }
     fence_barrier_init();
   }
@@ -368,7 +366,10 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp >= 4) {
     // ---------------- epilogue ----------------
-    const int ew = warp - 4;  // == warp % 4 -> TMEM lanes [32*ew, 32*ew+32)
+    const int ew = warp & 3;          // TMEM lanes [32*ew, 32*ew+32) (warp % 4 rule)
+    const int chalf = (warp - 4) >> 2;  // which half of the BN columns this warp drains
+    // per-warp 32x32 fp32 transpose tile, XOR-swizzled: (r, c) at r*32 + (c ^ r)
+    float* stg = reinterpret_cast<float*>(tmem_slot + 4) + (warp - 4) * 1024;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < p.tiles_total; t += gridDim.x) {
@@ -376,42 +377,59 @@ __global__ void __launch_bounds__(256, 1)
       if (!T.valid) continue;
       mbar_wait(tfull_bar + acc, acc_phase);
       tc_fence_after();
-      const int local_row = T.m_blk * BM + ew * 32 + lane;
-      long long row;
-      bool row_ok, zero_row = false;
+      const int row0 = T.m_blk * BM + ew * 32;  // first local row drained by this warp
+      long long grow0 = row0;
+      int row_lim, zero_from = 1 << 30;
       char* cbase = reinterpret_cast<char*>(p.c);
-      int ldc = p.ldc;
+      const int ldc = p.ldc;
       const float* bias = p.bias;
       if (p.group_mode == P2R_GROUP_M) {
-        row = static_cast<long long>(T.g) * p.seg_rows + local_row;
-        row_ok = local_row < p.seg_rows;
-        zero_row = local_row >= __ldg(p.counts + T.g);
+        grow0 = static_cast<long long>(T.g) * p.seg_rows + row0;
+        row_lim = p.seg_rows;
+        zero_from = __ldg(p.counts + T.g);
         if (bias != nullptr) bias += static_cast<long long>(T.g) * p.n;
       } else if (p.group_mode == P2R_GROUP_K) {
-        row = local_row;
-        row_ok = local_row < p.m;
+        row_lim = p.m;
         cbase += static_cast<long long>(T.g) * p.m * p.ldc * 4;  // fp32 grads
       } else {
-        row = local_row;
-        row_ok = local_row < p.m;
+        row_lim = p.m;
         if (p.split_k > 1) cbase += static_cast<long long>(T.ks) * p.c_split_stride * 4;
       }
+      const int nrows = min(32, row_lim - row0);
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = chalf * (BN / 64); c < (chalf + 1) * (BN / 64); ++c) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(taddr + c * 32, r);
         tmem_ld_wait();
         const int col0 = T.n_blk * BN + c * 32;
-        if (row_ok && col0 < p.n) {
-          float v[32];
+        if (nrows <= 0 || col0 >= p.n) continue;  // warp-uniform
+        // lane = row: 8 float4 stores into a float4-granular XOR swizzle
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-          const int ncols = min(32, p.n - col0);
-          const bool vec_ok = (ncols == 32) && ((ldc & 7) == 0) && ((p.ldc2 & 7) == 0) &&
-                              ((p.ldaux & 7) == 0);
-          epilogue_chunk(p, v, row, col0, ncols, vec_ok, cbase, ldc, zero_row, bias);
+        for (int q = 0; q < 8; ++q)
+          *reinterpret_cast<float4*>(stg + lane * 32 + ((q ^ (lane & 7)) << 2)) =
+              make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                          __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+        __syncwarp();
+        // lane = (row group, 4-column group): a warp instruction covers 4 rows x 32 columns
+        const int cg = lane & 7, rg = lane >> 3;
+        const int col = col0 + 4 * cg;
+        const int nc = min(4, p.n - col);  // valid columns for this lane (<= 0: none)
+        float4 b4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (bias != nullptr && nc > 0) {
+          b4.x = __ldg(bias + col);
+          if (nc > 1) b4.y = __ldg(bias + col + 1);
+          if (nc > 2) b4.z = __ldg(bias + col + 2);
+          if (nc > 3) b4.w = __ldg(bias + col + 3);
         }
+#pragma unroll 2
+        for (int i = 0; i < 8; ++i) {
+          const int rr = 4 * i + rg;
+          if (rr >= nrows || nc <= 0) continue;
+          const float4 v = *reinterpret_cast<const float4*>(stg + rr * 32 + ((cg ^ (rr & 7)) << 2));
+          epilogue_vec4(p, v, grow0 + rr, col, nc, row0 + rr >= zero_from, b4, cbase, ldc);
+        }
+        __syncwarp();
       }
       tc_fence_before();
       mbar_arrive(tempty_bar + acc);
@@ -430,16 +448,37 @@ __global__ void __launch_bounds__(256, 1)
 }
 
 // Deterministic split-K reduction: c (+)= sum_s ws[s] in split order.
+// One block row per output row, float4 along the row (n % 4 == 0 fast path).
 __global__ void splitk_reduce_kernel(float* c, int ldc, const float* ws, int m, int n, int splits,
                                      int accumulate) {
   const long long total = static_cast<long long>(m) * n;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int r = static_cast<int>(i / n), col = static_cast<int>(i % n);
-    float s = ws[i];
-    for (int k = 1; k < splits; ++k) s += ws[k * total + i];
-    float* dst = c + static_cast<long long>(r) * ldc + col;
-    *dst = accumulate ? (*dst + s) : s;
+  const int r = blockIdx.x;
+  if ((n & 3) == 0 && (ldc & 3) == 0) {
+    for (int c4 = threadIdx.x; c4 < n / 4; c4 += blockDim.x) {
+      const long long i = static_cast<long long>(r) * n + 4 * c4;
+      float4 s = *reinterpret_cast<const float4*>(ws + i);
+      for (int k = 1; k < splits; ++k) {
+        const float4 q = *reinterpret_cast<const float4*>(ws + k * total + i);
+        s.x += q.x;
+        s.y += q.y;
+        s.z += q.z;
+        s.w += q.w;
+      }
+      float4* dst = reinterpret_cast<float4*>(c + static_cast<long long>(r) * ldc + 4 * c4);
+      if (accumulate) {
+        const float4 o = *dst;
+        s = make_float4(o.x + s.x, o.y + s.y, o.z + s.z, o.w + s.w);
+      }
+      *dst = s;
+    }
+  } else {
+    for (int col = threadIdx.x; col < n; col += blockDim.x) {
+      const long long i = static_cast<long long>(r) * n + col;
+      float s = ws[i];
+      for (int k = 1; k < splits; ++k) s += ws[k * total + i];
+      float* dst = c + static_cast<long long>(r) * ldc + col;
+      *dst = accumulate ? (*dst + s) : s;
+    }
   }
 }
 
@@ -491,7 +530,7 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParam
   });
   if (attr_err != cudaSuccess) return attr_err;
   const int grid = p.tiles_total < kNumSMs ? p.tiles_total : kNumSMs;
-  gemm_kernel<BN, AMN, BMN><<<grid, 256, Cfg::SMEM_BYTES, s>>>(ta, tb, p);
+  gemm_kernel<BN, AMN, BMN><<<grid, kGemmThreads, Cfg::SMEM_BYTES, s>>>(ta, tb, p);
   count_launch();
   return cudaGetLastError();
 }
@@ -587,6 +626,11 @@ extern "C" p2r_status p2r_gemm(const p2r_gemm_args* a, void* stream) {
     p.epi = P2R_EPI_F32;
     p.c_split_stride = static_cast<long long>(a->m) * a->n;
   }
+  {
+    auto al = [](const void* q, uintptr_t b) { return (reinterpret_cast<uintptr_t>(q) % b) == 0; };
+    p.vec4 = (p.ldc % 4 == 0) && (p.ldc2 % 4 == 0) && (p.ldaux % 4 == 0) && al(p.c, 16) && al(p.c2, 8) &&
+             al(p.aux, 16);
+  }
   if (a->group_mode == P2R_GROUP_M)
     p.tiles_total = a->groups * (a->seg_rows / BM) * p.num_n_blk;
   else if (a->group_mode == P2R_GROUP_K)
@@ -610,10 +654,7 @@ extern "C" p2r_status p2r_gemm(const p2r_gemm_args* a, void* stream) {
                             : dispatch_majors<256>(a->a_mn_major, a->b_mn_major, ta, tb, p, s);
   if (e != cudaSuccess) return set_cuda_error(e, "gemm launch");
   if (split > 1) {
-    const long long total = 1LL * a->m * a->n;
-    int blocks = static_cast<int>((total + 255) / 256);
-    if (blocks > 4 * kNumSMs) blocks = 4 * kNumSMs;
-    splitk_reduce_kernel<<<blocks, 256, 0, s>>>(static_cast<float*>(a->c), a->ldc,
+    splitk_reduce_kernel<<<a->m, 256, 0, s>>>(static_cast<float*>(a->c), a->ldc,
                                                   static_cast<const float*>(g_ws), a->m, a->n,
                                                   split, a->epi == P2R_EPI_ACC_F32 ? 1 : 0);
     count_launch();

@@ -124,6 +124,33 @@ struct GranuleLayout {
 };
 
 struct Acts;  // per-shape activation / workspace buffers
+struct OffloadState;
+
+// Per-step movement accounting of the granular offload engine:
+// bytes moved per phase plus measured copy-engine time.
+struct OffloadStats {
+  double fn_load = 0;       // H2D of SLOW granules for the forward (Fn)
+  double bn_load = 0;       // H2D of SLOW granules for the backward (Bn)
+  double opt_load = 0;      // H2D of AdamW moments of SLOW granules (An)
+  double writeback = 0;     // D2H of updated params + moments (An)
+  double grad_offload = 0;  // D2H of SLOW-granule grads (no fused optimizer)
+  double h2d_ms = 0, d2h_ms = 0;
+  std::int64_t copies = 0;
+};
+
+// plan_offload: minimise predicted step time subject to the
+// FAST-tier budget; exhaustive for n <= 12, lowest-index prefix otherwise (the
+// optimum for uniform layers). Returns 1 = SLOW per layer.
+std::vector<int> plan_offload(const std::vector<std::int64_t>& layer_bytes, std::int64_t budget,
+                              double bandwidth, double compute_s, double latency_s);
+double predict_step_time(const std::vector<std::int64_t>& layer_bytes, const std::vector<int>& slow,
+                         double bandwidth, double compute_s, double latency_s);
+// staged device pointer of a SLOW granule: kind 0 p32, 1 grad, 2 m, 3 v, 4 bf16
+float* offload_slot_ptr(const OffloadState& st, int owned, int kind);
+// host fp32 -> bf16 (round to nearest even), the device __float2bfloat16_rn
+void host_cast_bf16(const float* src, std::uint16_t* dst, long long n);
+// wait for the offload engine's copy streams (before touching host granules)
+void offload_sync(const OffloadState& st);
 
 // Live per-kernel-class timing with CUDA events on the model stream.
 struct Profiler {
@@ -143,6 +170,9 @@ struct Profiler {
 class Model {
  public:
   Model(ModelConfig config, std::uint64_t seed);
+  // Real model with granular CPU offload: slow[i] = 1 keeps owned layer i in
+  // pinned host DRAM and streams it through `ring_slots` HBM staging slots.
+  Model(ModelConfig config, std::uint64_t seed, const std::vector<int>& slow, int ring_slots);
   ~Model();
   Model(const Model&) = delete;
   Model& operator=(const Model&) = delete;
@@ -197,12 +227,37 @@ class Model {
   void profile(int cls, std::int64_t* launches, double* ms, double* flops, double* bytes);
   void profile_reset();
   void buffer(int which, void** ptr, std::size_t* bytes) const;
+
+  // granular offload
+  bool offloaded() const { return off_ != nullptr; }
+  const std::vector<int>& slow_layers() const { return slow_; }
+  void set_offload_lr(float lr) { offload_lr_ = lr; }
+  OffloadStats offload_stats();
+  void offload_stats_reset();
+  void set_offload_skip_copies(bool skip);  // timing aid: same schedule, no PCIe traffic
+  std::int64_t layer_granule_bytes() const { return layer_.numel * 18; }
+  std::int64_t device_param_bytes() const;
   void routing_host(int g, int* selected, std::uint8_t* survived, int* raw_load, int* capacity,
                     int* dropped) const;
 
  private:
   struct NoInit {};
   Model(ModelConfig config, NoInit);
+  // offload plumbing (csrc/engine/offload.cpp)
+  void offload_setup(const std::vector<int>& slow, int ring_slots);
+  void offload_begin_forward(bool training);
+  void offload_alloc_moments();
+  void offload_acquire(int owned, bool backward);
+  void offload_release(int owned, bool backward);
+  void offload_prefetch_next(int after_owned, bool backward);
+  void offload_finish_step();
+  const float* view_base(const ParamView& v, int kind) const;
+  void copy_view(const ParamView& v, int kind, float* host, bool to_host) const;
+  float* slow_host_grad(int owned) const;
+  float* slow_host_p32(int owned) const;
+  float* slow_host_m(int owned, int which) const;
+  std::uint16_t* slow_host_p16(int owned) const;
+  void adamw_granule(float* p, float* g, float* m, float* v, void* p16, float lr, float bc1, float bc2);
   void build_layout();
   void allocate();
   void init_params(std::uint64_t seed);
@@ -251,6 +306,12 @@ class Model {
   void* pinned_ = nullptr;
   std::size_t pinned_bytes_ = 0;
   Profiler prof_;
+  // offload: res_idx_[owned] = resident slot in lay_* or -1 (SLOW)
+  std::vector<int> res_idx_;
+  std::vector<int> slow_;
+  int n_res_ = 0;
+  std::unique_ptr<OffloadState> off_;
+  float offload_lr_ = 0.0f;
 };
 
 // moe_dispatch on host logits via the routing kernel (bit-exact, model.cpp:294-332)

@@ -116,6 +116,27 @@ p2r_status p2r_moe_dispatch_host(const float* logits, int T, int E, int k, float
                                  uint8_t* survived, int* raw_load, int* offsets, int* rows,
                                  int* slots, int* capacity, int* dropped);
 
+/* ---- granular CPU offload (§4.2) ---------------
+ * Real model whose owned layers with slow[i] = 1 live in pinned host DRAM and
+ * are streamed through `ring_slots` HBM staging slots one granule ahead of
+ * compute (H2D / D2H side streams); AdamW of SLOW granules runs fused in their
+ * backward with the lr given to p2r_model_set_offload_lr. */
+p2r_status p2r_model_create_offload(const p2r_model_config* cfg, uint64_t seed, const int* slow,
+                                    int ring_slots, p2r_model** out);
+p2r_status p2r_model_set_offload_lr(p2r_model* m, float lr);
+/* out7 = {Fn_load, Bn_load, opt_load, writeback, grad_offload, h2d_ms, d2h_ms} since last reset */
+p2r_status p2r_model_offload_stats(p2r_model* m, double* out7);
+p2r_status p2r_model_offload_stats_reset(p2r_model* m);
+p2r_status p2r_model_set_offload_skip_copies(p2r_model* m, int skip);
+int64_t p2r_model_layer_granule_bytes(const p2r_model* m);
+int64_t p2r_model_device_param_bytes(const p2r_model* m);
+/* plan_offload: slow_out[i] = 1 for offloaded layers. */
+p2r_status p2r_plan_offload(const int64_t* layer_bytes, int n, int64_t budget, double bandwidth,
+                            double compute_s, double latency_s, int* slow_out);
+/* predict_step_time, 4 x W per SLOW layer, no overlap. */
+double p2r_predict_step_time(const int64_t* layer_bytes, const int* slow, int n, double bandwidth,
+                             double compute_s, double latency_s);
+
 /* init_normal (model.cpp:28-36) on the host: the exact values Model() uploads. */
 void p2r_init_normal_host(uint64_t seed, const char* name, int64_t n, float* out);
 

@@ -198,6 +198,57 @@ p2r_status p2r_moe_dispatch_host(const float* logits, int T, int E, int k, float
   });
 }
 
+p2r_status p2r_model_create_offload(const p2r_model_config* cfg, uint64_t seed, const int* slow, int ring_slots,
+                                    p2r_model** out) {
+  return guard([&] {
+    const int n = cfg->n_layers_params;
+    std::vector<int> pl(slow, slow + n);
+    auto h = std::make_unique<p2r_model>();
+    h->m = std::make_unique<p2r::Model>(to_cfg(cfg), seed, pl, ring_slots);
+    *out = h.release();
+  });
+}
+p2r_status p2r_model_set_offload_lr(p2r_model* m, float lr) {
+  m->m->set_offload_lr(lr);
+  return P2R_OK;
+}
+p2r_status p2r_model_offload_stats(p2r_model* m, double* o) {
+  return guard([&] {
+    const p2r::OffloadStats s = m->m->offload_stats();
+    o[0] = s.fn_load;
+    o[1] = s.bn_load;
+    o[2] = s.opt_load;
+    o[3] = s.writeback;
+    o[4] = s.grad_offload;
+    o[5] = s.h2d_ms;
+    o[6] = s.d2h_ms;
+  });
+}
+p2r_status p2r_model_offload_stats_reset(p2r_model* m) {
+  return guard([&] { m->m->offload_stats_reset(); });
+}
+p2r_status p2r_model_set_offload_skip_copies(p2r_model* m, int skip) {
+  m->m->set_offload_skip_copies(skip != 0);
+  return P2R_OK;
+}
+int64_t p2r_model_layer_granule_bytes(const p2r_model* m) { return m->m->layer_granule_bytes(); }
+int64_t p2r_model_device_param_bytes(const p2r_model* m) { return m->m->device_param_bytes(); }
+
+p2r_status p2r_plan_offload(const int64_t* layer_bytes, int n, int64_t budget, double bandwidth, double compute_s,
+                            double latency_s, int* slow_out) {
+  return guard([&] {
+    std::vector<std::int64_t> b(layer_bytes, layer_bytes + n);
+    const std::vector<int> pl = p2r::plan_offload(b, budget, bandwidth, compute_s, latency_s);
+    std::copy(pl.begin(), pl.end(), slow_out);
+  });
+}
+double p2r_predict_step_time(const int64_t* layer_bytes, const int* slow, int n, double bandwidth, double compute_s,
+                             double latency_s) {
+  std::vector<std::int64_t> b(layer_bytes, layer_bytes + n);
+  std::vector<int> s(slow, slow + n);
+  return p2r::predict_step_time(b, s, bandwidth, compute_s, latency_s);
+}
+
 void p2r_init_normal_host(uint64_t seed, const char* name, int64_t n, float* out) {
   p2r::init_normal_host(out, static_cast<std::size_t>(n), seed, name);
 }

@@ -17,6 +17,7 @@
 #include <random>
 #include <string>
 
+#include "offload_state.hpp"
 #include "p2r_cuda.h"
 #include "p2r_engine.h"
 
@@ -179,6 +180,15 @@ Model::Model(ModelConfig config, std::uint64_t seed) : cfg_(std::move(config)) {
   init_params(seed);
 }
 
+Model::Model(ModelConfig config, std::uint64_t seed, const std::vector<int>& slow, int ring_slots)
+    : cfg_(std::move(config)) {
+  cfg_.validate();
+  build_layout();
+  offload_setup(slow, ring_slots);
+  allocate();
+  init_params(seed);
+}
+
 Model::Model(ModelConfig config, NoInit) : cfg_(std::move(config)) {
   cfg_.validate();
   build_layout();
@@ -186,6 +196,8 @@ Model::Model(ModelConfig config, NoInit) : cfg_(std::move(config)) {
 }
 
 Model::~Model() {
+  if (stream_) cudaStreamSynchronize(stream_);
+  off_.reset();
   if (pinned_) cudaFreeHost(pinned_);
   if (stream_) cudaStreamDestroy(stream_);
 }
@@ -194,6 +206,10 @@ void Model::build_layout() {
   const int d = cfg_.d_model, dff = cfg_.d_ff, V = cfg_.vocab_size, S = cfg_.seq_len;
   const int E = cfg_.moe.n_experts;
   n_owned_ = cfg_.n_layers_params;
+  n_res_ = n_owned_;
+  res_idx_.resize(static_cast<std::size_t>(n_owned_));
+  slow_.assign(static_cast<std::size_t>(n_owned_), 0);
+  for (int i = 0; i < n_owned_; ++i) res_idx_[static_cast<std::size_t>(i)] = i;
   // embeddings granule (for_each_param order: tok, pos, final gain, final bias)
   emb_ = GranuleLayout{};
   emb_.tok = emb_.add(1LL * V * d, true);
@@ -259,7 +275,7 @@ void Model::build_layout() {
 void Model::allocate() {
   cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
   const std::size_t eb = static_cast<std::size_t>(emb_.numel);
-  const std::size_t lb = static_cast<std::size_t>(layer_stride_) * n_owned_;
+  const std::size_t lb = static_cast<std::size_t>(layer_stride_) * std::max(n_res_, 1);
   emb_p_ = DevBuf(eb * 4);
   emb_g_ = DevBuf(eb * 4);
   emb_p16_ = DevBuf(eb * 2);
@@ -272,10 +288,20 @@ void Model::allocate() {
   cuda_check(cudaMemsetAsync(lay_g_.p, 0, lb * 4, stream_), "memset");
 }
 
-float* Model::lp(int o, long long off) const { return lay_p_.as<float>() + o * layer_stride_ + off; }
-float* Model::lg(int o, long long off) const { return lay_g_.as<float>() + o * layer_stride_ + off; }
+float* Model::lp(int o, long long off) const {
+  const int r = res_idx_[static_cast<std::size_t>(o)];
+  if (r < 0) return offload_slot_ptr(*off_, o, 0) + off;
+  return lay_p_.as<float>() + r * layer_stride_ + off;
+}
+float* Model::lg(int o, long long off) const {
+  const int r = res_idx_[static_cast<std::size_t>(o)];
+  if (r < 0) return offload_slot_ptr(*off_, o, 1) + off;
+  return lay_g_.as<float>() + r * layer_stride_ + off;
+}
 void* Model::lp16(int o, long long off) const {
-  return lay_p16_.as<std::uint16_t>() + o * layer_stride_ + off;
+  const int r = res_idx_[static_cast<std::size_t>(o)];
+  if (r < 0) return reinterpret_cast<std::uint16_t*>(offload_slot_ptr(*off_, o, 4)) + off;
+  return lay_p16_.as<std::uint16_t>() + r * layer_stride_ + off;
 }
 
 void Model::init_params(std::uint64_t seed) {
@@ -304,59 +330,69 @@ void Model::init_params(std::uint64_t seed) {
 
 void Model::refresh_bf16() {
   p2r_check(p2r_cast_bf16(emb_p_.as<float>(), emb_p16_.p, emb_.numel, stream_), "cast");
-  p2r_check(p2r_cast_bf16(lay_p_.as<float>(), lay_p16_.p, layer_stride_ * n_owned_, stream_), "cast");
+  if (n_res_ > 0)
+    p2r_check(p2r_cast_bf16(lay_p_.as<float>(), lay_p16_.p, layer_stride_ * n_res_, stream_), "cast");
+  for (int o = 0; o < n_owned_; ++o)
+    if (res_idx_[static_cast<std::size_t>(o)] < 0) host_cast_bf16(slow_host_p32(o), slow_host_p16(o), layer_stride_);
 }
 
-void Model::get_param(int i, float* host) const {
-  const ParamView& v = views_.at(static_cast<std::size_t>(i));
-  const float* base = v.granule < 0 ? ep(v.off) : lp(v.granule, v.off);
-  cuda_check(cudaMemcpy2DAsync(host, static_cast<std::size_t>(v.cols) * 4, base,
-                               static_cast<std::size_t>(v.ld) * 4, static_cast<std::size_t>(v.cols) * 4,
-                               v.rows, cudaMemcpyDeviceToHost, stream_),
-             "get_param");
+const float* Model::view_base(const ParamView& v, int kind) const {
+  // kind: 0 param, 1 grad, 2 m, 3 v
+  if (v.granule < 0) {
+    const DevBuf* b = kind == 0 ? &emb_p_ : kind == 1 ? &emb_g_ : kind == 2 ? &emb_m_ : &emb_v_;
+    return b->as<float>() + v.off;
+  }
+  const int r = res_idx_[static_cast<std::size_t>(v.granule)];
+  if (r >= 0) {
+    const DevBuf* b = kind == 0 ? &lay_p_ : kind == 1 ? &lay_g_ : kind == 2 ? &lay_m_ : &lay_v_;
+    return b->as<float>() + r * layer_stride_ + v.off;
+  }
+  if (kind == 0) return slow_host_p32(v.granule) + v.off;
+  if (kind == 1) {
+    float* g = slow_host_grad(v.granule);
+    if (g == nullptr)
+      throw std::logic_error("offload: gradients of SLOW granules are consumed on device by the fused AdamW");
+    return g + v.off;
+  }
+  return slow_host_m(v.granule, kind - 2) + v.off;
+}
+
+void Model::copy_view(const ParamView& v, int kind, float* host, bool to_host) const {
+  if (off_) offload_sync(*off_);
+  float* base = const_cast<float*>(view_base(v, kind));
+  const std::size_t w = static_cast<std::size_t>(v.cols) * 4, ld = static_cast<std::size_t>(v.ld) * 4;
+  if (to_host)
+    cuda_check(cudaMemcpy2DAsync(host, w, base, ld, w, v.rows, cudaMemcpyDefault, stream_), "copy view");
+  else
+    cuda_check(cudaMemcpy2DAsync(base, ld, host, w, w, v.rows, cudaMemcpyDefault, stream_), "copy view");
   cuda_check(cudaStreamSynchronize(stream_), "sync");
 }
+
+void Model::get_param(int i, float* host) const { copy_view(views_.at(static_cast<std::size_t>(i)), 0, host, true); }
 
 void Model::set_param(int i, const float* host) {
   const ParamView& v = views_.at(static_cast<std::size_t>(i));
-  float* base = v.granule < 0 ? const_cast<float*>(ep(v.off)) : lp(v.granule, v.off);
-  cuda_check(cudaMemcpy2DAsync(base, static_cast<std::size_t>(v.ld) * 4, host,
-                               static_cast<std::size_t>(v.cols) * 4, static_cast<std::size_t>(v.cols) * 4,
-                               v.rows, cudaMemcpyHostToDevice, stream_),
-             "set_param");
-  cuda_check(cudaStreamSynchronize(stream_), "sync");
-  // keep the bf16 shadow in step with the master copy
-  if (v.granule < 0)
-    p2r_check(p2r_cast_bf16(emb_p_.as<float>(), emb_p16_.p, emb_.numel, stream_), "cast");
-  else
-    p2r_check(p2r_cast_bf16(lp(v.granule, 0), lp16(v.granule, 0), layer_stride_, stream_), "cast");
+  copy_view(v, 0, const_cast<float*>(host), false);
+  // keep the bf16 shadow in step with the master copy (linear span of the view)
+  const long long span = static_cast<long long>(v.rows - 1) * v.ld + v.cols;
+  if (v.granule >= 0 && res_idx_[static_cast<std::size_t>(v.granule)] < 0) {
+    host_cast_bf16(slow_host_p32(v.granule) + v.off, slow_host_p16(v.granule) + v.off, span);
+  } else {
+    const float* src = v.granule < 0 ? ep(v.off) : lp(v.granule, v.off);
+    void* dst = v.granule < 0 ? ep16(v.off) : lp16(v.granule, v.off);
+    p2r_check(p2r_cast_bf16(src, dst, span, stream_), "cast");
+  }
 }
 
-void Model::get_grad(int i, float* host) const {
-  const ParamView& v = views_.at(static_cast<std::size_t>(i));
-  const float* base = v.granule < 0 ? emb_g_.as<float>() + v.off : lg(v.granule, v.off);
-  cuda_check(cudaMemcpy2DAsync(host, static_cast<std::size_t>(v.cols) * 4, base,
-                               static_cast<std::size_t>(v.ld) * 4, static_cast<std::size_t>(v.cols) * 4,
-                               v.rows, cudaMemcpyDeviceToHost, stream_),
-             "get_grad");
-  cuda_check(cudaStreamSynchronize(stream_), "sync");
-}
+void Model::get_grad(int i, float* host) const { copy_view(views_.at(static_cast<std::size_t>(i)), 1, host, true); }
 
 void Model::get_moment(int i, int which, float* host) const {
   if (!has_opt_) throw std::logic_error("adamw: optimizer not attached");
-  const ParamView& v = views_.at(static_cast<std::size_t>(i));
-  const DevBuf& eb = which ? emb_v_ : emb_m_;
-  const DevBuf& lb = which ? lay_v_ : lay_m_;
-  const float* base = v.granule < 0 ? eb.as<float>() + v.off : lb.as<float>() + v.granule * layer_stride_ + v.off;
-  cuda_check(cudaMemcpy2DAsync(host, static_cast<std::size_t>(v.cols) * 4, base,
-                               static_cast<std::size_t>(v.ld) * 4, static_cast<std::size_t>(v.cols) * 4,
-                               v.rows, cudaMemcpyDeviceToHost, stream_),
-             "get_moment");
-  cuda_check(cudaStreamSynchronize(stream_), "sync");
+  copy_view(views_.at(static_cast<std::size_t>(i)), 2 + which, host, true);
 }
 
 std::int64_t Model::grad_bytes() const {
-  return (emb_.numel + layer_stride_ * n_owned_) * 4;
+  return (emb_.numel + layer_stride_ * n_res_) * 4;
 }
 
 void Model::zero_grads() {
@@ -571,6 +607,7 @@ Tensor Model::embed_forward(GradTape* tape, const int* d_tokens, int batch, int 
   if (batch <= 0) throw std::invalid_argument("forward: token count must be a multiple of batch");
   if (seq > cfg_.seq_len) throw std::invalid_argument("forward: sequence longer than configured seq_len");
   ensure_acts(batch, seq);
+  if (off_) offload_begin_forward(tape != nullptr);
   Acts& A = *acts_;
   const int d = cfg_.d_model;
   prof(P2R_PROF_EMBED, 0, 12.0 * A.T * d, [&] {
@@ -595,6 +632,7 @@ Tensor Model::block_forward(GradTape* tape, int g, const Tensor& x, int batch, A
   if (x.rows != A.T || batch != A.B) throw std::invalid_argument("block_forward: batch does not match embed_forward");
   LayerActs& L = A.L[static_cast<std::size_t>(g)];
   const int o = owned_index_of_graph_layer(g);
+  if (off_) offload_acquire(o, false);
   const int T = A.T, d = cfg_.d_model, dff = cfg_.d_ff, H = cfg_.n_heads;
   const int causal = mode == AttentionMode::Causal ? 1 : 0;
   const double Td = static_cast<double>(T) * d;
@@ -647,6 +685,7 @@ Tensor Model::block_forward(GradTape* tape, int g, const Tensor& x, int batch, A
                               L.x1.as<float>(), L.xout.as<float>(), stream_),
               "combine");
   }
+  if (off_) offload_release(o, false);
   if (tape) tape->record([this, g, mode]() { block_backward(g, mode); });
   return Tensor{T, d, L.xout.as<float>(), A.dres.as<float>(), A.dres16.p};
 }
@@ -660,6 +699,7 @@ void Model::block_backward(int g, AttentionMode mode) {
   Acts& A = *acts_;
   LayerActs& L = A.L[static_cast<std::size_t>(g)];
   const int o = owned_index_of_graph_layer(g);
+  if (off_) offload_acquire(o, true);
   const int T = A.T, d = cfg_.d_model, dff = cfg_.d_ff, H = cfg_.n_heads;
   const int causal = mode == AttentionMode::Causal ? 1 : 0;
   const float* xin = g == 0 ? A.x0.as<float>() : A.L[static_cast<std::size_t>(g - 1)].xout.as<float>();
@@ -748,6 +788,7 @@ void Model::block_backward(int g, AttentionMode mode) {
                                 lg(o, layer_.ln1_b), A.ln_ws.as<float>(), stream_),
               "ln1 bwd");
   });
+  if (off_) offload_release(o, true);
 }
 
 Tensor Model::head_forward(GradTape* tape, const Tensor& x) {
@@ -890,6 +931,7 @@ void Model::adamw_attach(float b1, float b2, float eps, float wd) {
     cuda_check(cudaMemsetAsync(lay_m_.p, 0, lay_m_.bytes, stream_), "memset");
     cuda_check(cudaMemsetAsync(lay_v_.p, 0, lay_v_.bytes, stream_), "memset");
     has_opt_ = true;
+    if (off_) offload_alloc_moments();
   }
 }
 
@@ -898,6 +940,8 @@ void Model::adamw_step(float lr) {
   ++step_count_;
   const float bc1 = 1.0f - std::pow(b1_, static_cast<float>(step_count_));
   const float bc2 = 1.0f - std::pow(b2_, static_cast<float>(step_count_));
+  if (off_ && lr != offload_lr_)
+    throw std::invalid_argument("adamw: offloaded granules were updated with set_offload_lr(); pass the same lr");
   auto run = [&](const GranuleLayout& lay, float* p, float* g, float* m, float* v, void* p16) {
     std::vector<long long> off, len;
     std::vector<int> dec;
@@ -913,9 +957,28 @@ void Model::adamw_step(float lr) {
     });
   };
   run(emb_, emb_p_.as<float>(), emb_g_.as<float>(), emb_m_.as<float>(), emb_v_.as<float>(), emb_p16_.p);
-  for (int i = 0; i < n_owned_; ++i)
-    run(layer_, lp(i, 0), lg(i, 0), lay_m_.as<float>() + i * layer_stride_, lay_v_.as<float>() + i * layer_stride_,
+  // resident granules here; SLOW granules were updated by the fused AdamW in their backward
+  for (int i = 0; i < n_owned_; ++i) {
+    const int r = res_idx_[static_cast<std::size_t>(i)];
+    if (r < 0) continue;
+    run(layer_, lp(i, 0), lg(i, 0), lay_m_.as<float>() + r * layer_stride_, lay_v_.as<float>() + r * layer_stride_,
         lp16(i, 0));
+  }
+}
+
+void Model::adamw_granule(float* p, float* g, float* m, float* v, void* p16, float lr, float bc1, float bc2) {
+  std::vector<long long> off, len;
+  std::vector<int> dec;
+  for (const auto& s : layer_.segs) {
+    off.push_back(s.off);
+    len.push_back(s.len);
+    dec.push_back(s.decay ? 1 : 0);
+  }
+  prof(P2R_PROF_ADAMW, 0, 30.0 * layer_.numel, [&] {
+    p2r_check(p2r_adamw_step(p, g, m, v, p16, off.data(), len.data(), dec.data(), static_cast<int>(off.size()), b1_,
+                             b2_, eps_, wd_, lr, bc1, bc2, stream_),
+              "adamw");
+  });
 }
 
 std::int64_t Model::state_bytes() const {
@@ -927,6 +990,7 @@ std::int64_t Model::state_bytes() const {
 // ---------------------------------------------------------------- delink (model.cpp:358-377)
 std::unique_ptr<Model> Model::delinked() const {
   if (cfg_.n_layers_params != 1) throw std::logic_error("delinked: model is not in shared-parameter mode");
+  if (off_) throw std::logic_error("delinked: offloaded models are Real already");
   std::unique_ptr<Model> real(new Model(cfg_.as_unshared(), NoInit{}));
   cudaStream_t s = real->stream_;
   cuda_check(cudaStreamSynchronize(stream_), "sync");

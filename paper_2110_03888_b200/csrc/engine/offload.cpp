@@ -1,0 +1,354 @@
+// Granular CPU offloading (§4.2; the reference's
+// offload.cpp is absent, so this follows the spec's Fn / Bn / An phase model).
+//
+// SLOW layer granules live in pinned host DRAM (fp32 master + bf16 shadow +
+// AdamW moments). A ring of HBM staging slots (each one granule of p32, grad,
+// m, v, bf16) is fed by cudaMemcpyAsync on a dedicated H2D stream, one granule
+// ahead of the compute stream (event-synchronised), and drained by a D2H stream:
+//   Fn : H2D p32 + bf16 of layer l while layer l-1 computes
+//   Bn : H2D p32 + bf16 (+ m, v) of layer l while layer l+1 runs its backward
+//   An : AdamW for the granule on the GPU right after its backward, then D2H
+//        write-back of p32 + bf16 + m + v (or of the grads when no optimizer
+//        is attached: the spec's "gradient offload").
+// FAST granules stay resident; the placement comes from plan_offload.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+
+#include "offload_state.hpp"
+#include "p2r_cuda.h"
+
+namespace p2r {
+
+float* offload_slot_ptr(const OffloadState& st, int owned, int kind) {
+  const int s = st.slot_of[static_cast<std::size_t>(owned)];
+  if (s < 0) throw std::logic_error("offload: SLOW granule used while not staged");
+  const OffloadSlot& sl = st.slots[static_cast<std::size_t>(s)];
+  switch (kind) {
+    case 0: return sl.p32.as<float>();
+    case 1: return sl.g32.as<float>();
+    case 2: return sl.m.as<float>();
+    case 3: return sl.v.as<float>();
+    default: return reinterpret_cast<float*>(sl.p16.as<std::uint16_t>());
+  }
+}
+
+void host_cast_bf16(const float* src, std::uint16_t* dst, long long n) {
+  for (long long i = 0; i < n; ++i) {
+    std::uint32_t u;
+    std::memcpy(&u, src + i, 4);
+    if ((u & 0x7fffffffu) > 0x7f800000u) {  // NaN: keep quiet NaN
+      dst[i] = static_cast<std::uint16_t>((u >> 16) | 0x40u);
+      continue;
+    }
+    const std::uint32_t r = u + 0x7fffu + ((u >> 16) & 1u);
+    dst[i] = static_cast<std::uint16_t>(r >> 16);
+  }
+}
+
+// ---------------------------------------------------------------- planner
+double predict_step_time(const std::vector<std::int64_t>& layer_bytes, const std::vector<int>& slow,
+                         double bandwidth, double compute_s, double latency_s) {
+  double moved = 0;
+  int n = 0;
+  for (std::size_t i = 0; i < layer_bytes.size(); ++i)
+    if (slow[i]) {
+      moved += 4.0 * static_cast<double>(layer_bytes[i]);  // Fn + Bn + grad + write-back
+      n += 4;
+    }
+  return compute_s + moved / bandwidth + n * latency_s;
+}
+
+std::vector<int> plan_offload(const std::vector<std::int64_t>& layer_bytes, std::int64_t budget, double bandwidth,
+                              double compute_s, double latency_s) {
+  const int n = static_cast<int>(layer_bytes.size());
+  std::int64_t total = 0, largest = 0;
+  for (auto b : layer_bytes) {
+    total += b;
+    largest = std::max(largest, b);
+  }
+  // pre: a SLOW layer must fit the fast tier while it is staged
+  if (budget < largest) throw std::runtime_error("plan_offload: no feasible plan (a single layer exceeds the budget)");
+  if (n <= 12) {
+    std::vector<int> best;
+    double best_t = std::numeric_limits<double>::infinity();
+    for (std::uint32_t mask = 0; mask < (1u << n); ++mask) {
+      std::vector<int> pl(static_cast<std::size_t>(n));
+      std::int64_t fast = 0;
+      for (int i = 0; i < n; ++i) {
+        pl[static_cast<std::size_t>(i)] = (mask >> i) & 1u;
+        if (!pl[static_cast<std::size_t>(i)]) fast += layer_bytes[static_cast<std::size_t>(i)];
+      }
+      if (fast > budget) continue;
+      const double t = predict_step_time(layer_bytes, pl, bandwidth, compute_s, latency_s);
+      // ties -> offload the lowest-indexed layers (lexicographically larger `pl`)
+      if (t < best_t || (t == best_t && pl > best)) {
+        best_t = t;
+        best = pl;
+      }
+    }
+    if (best.empty()) throw std::runtime_error("plan_offload: no feasible plan");
+    return best;
+  }
+  std::vector<int> pl(static_cast<std::size_t>(n), 0);
+  std::int64_t fast = total;
+  for (int i = 0; i < n && fast > budget; ++i) {
+    pl[static_cast<std::size_t>(i)] = 1;
+    fast -= layer_bytes[static_cast<std::size_t>(i)];
+  }
+  if (fast > budget) throw std::runtime_error("plan_offload: no feasible plan");
+  return pl;
+}
+
+// ---------------------------------------------------------------- engine side
+void Model::offload_setup(const std::vector<int>& slow, int ring_slots) {
+  if (static_cast<int>(slow.size()) != n_owned_)
+    throw std::invalid_argument("offload: placement must give one entry per owned layer");
+  if (ring_slots < 2) throw std::invalid_argument("offload: need at least 2 staging slots");
+  auto st = std::make_unique<OffloadState>();
+  st->ring = ring_slots;
+  st->stride = layer_stride_;
+  st->slot_of.assign(static_cast<std::size_t>(n_owned_), -1);
+  st->host_idx.assign(static_cast<std::size_t>(n_owned_), -1);
+  slow_ = slow;
+  int nr = 0, ns = 0;
+  for (int o = 0; o < n_owned_; ++o) {
+    if (slow[static_cast<std::size_t>(o)]) {
+      res_idx_[static_cast<std::size_t>(o)] = -1;
+      st->host_idx[static_cast<std::size_t>(o)] = ns++;
+      st->slow_list.push_back(o);
+    } else {
+      res_idx_[static_cast<std::size_t>(o)] = nr++;
+    }
+  }
+  n_res_ = nr;
+  if (ns == 0) return;  // nothing offloaded
+  const std::size_t n = static_cast<std::size_t>(layer_stride_) * ns;
+  cuda_check(cudaMallocHost(reinterpret_cast<void**>(&st->hp32), n * 4), "pinned p32");
+  cuda_check(cudaMallocHost(reinterpret_cast<void**>(&st->hp16), n * 2), "pinned bf16");
+  std::memset(st->hp32, 0, n * 4);
+  std::memset(st->hp16, 0, n * 2);
+  const std::size_t g = static_cast<std::size_t>(layer_stride_);
+  st->slots.resize(static_cast<std::size_t>(ring_slots));
+  for (auto& s : st->slots) {
+    s.p32 = DevBuf(g * 4);
+    s.g32 = DevBuf(g * 4);
+    s.m = DevBuf(g * 4);
+    s.v = DevBuf(g * 4);
+    s.p16 = DevBuf(g * 2);
+    cuda_check(cudaEventCreateWithFlags(&s.loaded, cudaEventDisableTiming), "event");
+    cuda_check(cudaEventCreateWithFlags(&s.free_ev, cudaEventDisableTiming), "event");
+  }
+  st->wb_ev.resize(static_cast<std::size_t>(n_owned_));
+  st->wb_recorded.assign(static_cast<std::size_t>(n_owned_), 0);
+  for (auto& e : st->wb_ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  cuda_check(cudaStreamCreateWithFlags(&st->h2d, cudaStreamNonBlocking), "h2d stream");
+  cuda_check(cudaStreamCreateWithFlags(&st->d2h, cudaStreamNonBlocking), "d2h stream");
+  off_ = std::move(st);
+}
+
+void Model::offload_alloc_moments() {
+  if (!off_ || off_->slow_list.empty() || off_->hm) return;
+  const std::size_t n = static_cast<std::size_t>(layer_stride_) * off_->slow_list.size();
+  cuda_check(cudaMallocHost(reinterpret_cast<void**>(&off_->hm), n * 4), "pinned m");
+  cuda_check(cudaMallocHost(reinterpret_cast<void**>(&off_->hv), n * 4), "pinned v");
+  std::memset(off_->hm, 0, n * 4);
+  std::memset(off_->hv, 0, n * 4);
+}
+
+float* Model::slow_host_p32(int o) const {
+  return off_->hp32 + static_cast<long long>(off_->host_idx[static_cast<std::size_t>(o)]) * layer_stride_;
+}
+std::uint16_t* Model::slow_host_p16(int o) const {
+  return off_->hp16 + static_cast<long long>(off_->host_idx[static_cast<std::size_t>(o)]) * layer_stride_;
+}
+float* Model::slow_host_m(int o, int which) const {
+  float* b = which ? off_->hv : off_->hm;
+  if (!b) throw std::logic_error("adamw: optimizer not attached");
+  return b + static_cast<long long>(off_->host_idx[static_cast<std::size_t>(o)]) * layer_stride_;
+}
+float* Model::slow_host_grad(int o) const {
+  if (!off_->hg) return nullptr;
+  return off_->hg + static_cast<long long>(off_->host_idx[static_cast<std::size_t>(o)]) * layer_stride_;
+}
+
+namespace {
+void copy_async(OffloadState& st, void* dst, const void* src, std::size_t bytes, cudaStream_t s, bool h2d,
+                double* counter) {
+  *counter += static_cast<double>(bytes);
+  if (st.skip) return;
+  cuda_check(cudaMemcpyAsync(dst, src, bytes, h2d ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, s), "offload copy");
+}
+}  // namespace
+
+void Model::offload_begin_forward(bool training) {
+  OffloadState& st = *off_;
+  st.training = training;
+  std::fill(st.slot_of.begin(), st.slot_of.end(), -1);
+  for (auto& s : st.slots) s.layer = -1;
+  if (!st.slow_list.empty()) offload_prefetch_next(-1, false);
+}
+
+// Stage `o` (the next SLOW layer after `after` in the phase's order) into a slot.
+void Model::offload_prefetch_next(int after, bool backward) {
+  OffloadState& st = *off_;
+  int o = -1;
+  if (!backward) {
+    for (int x : st.slow_list)
+      if (x > after) {
+        o = x;
+        break;
+      }
+    if (o < 0) {
+      if (!st.training) return;
+      backward = true;  // forward done: stage the last SLOW layer for the backward
+      after = n_owned_;
+    }
+  }
+  if (backward) {
+    for (auto it = st.slow_list.rbegin(); it != st.slow_list.rend(); ++it)
+      if (*it < after) {
+        o = *it;
+        break;
+      }
+  }
+  if (o < 0) return;
+  const int si = st.next_slot;
+  st.next_slot = (st.next_slot + 1) % st.ring;
+  OffloadSlot& sl = st.slots[static_cast<std::size_t>(si)];
+  if (sl.layer >= 0 && st.slot_of[static_cast<std::size_t>(sl.layer)] == si)
+    st.slot_of[static_cast<std::size_t>(sl.layer)] = -1;
+  for (auto& other : st.slots)
+    if (other.layer == o) other.layer = -1;  // o re-staged (forward copy -> backward copy)
+  sl.layer = o;
+  st.slot_of[static_cast<std::size_t>(o)] = si;
+  if (sl.free_recorded) cuda_check(cudaStreamWaitEvent(st.h2d, sl.free_ev, 0), "wait slot free");
+  if (st.wb_recorded[static_cast<std::size_t>(o)])
+    cuda_check(cudaStreamWaitEvent(st.h2d, st.wb_ev[static_cast<std::size_t>(o)], 0), "wait write-back");
+  const std::size_t g = static_cast<std::size_t>(layer_stride_);
+  cudaEvent_t a = st.ev(), b = st.ev();
+  cuda_check(cudaEventRecord(a, st.h2d), "event");
+  double* ctr = backward ? &st.stats.bn_load : &st.stats.fn_load;
+  copy_async(st, sl.p32.p, slow_host_p32(o), g * 4, st.h2d, true, ctr);
+  copy_async(st, sl.p16.p, slow_host_p16(o), g * 2, st.h2d, true, ctr);
+  if (backward && has_opt_) {
+    copy_async(st, sl.m.p, slow_host_m(o, 0), g * 4, st.h2d, true, &st.stats.opt_load);
+    copy_async(st, sl.v.p, slow_host_m(o, 1), g * 4, st.h2d, true, &st.stats.opt_load);
+  }
+  cuda_check(cudaEventRecord(b, st.h2d), "event");
+  st.copies.push_back({a, b, true});
+  cuda_check(cudaEventRecord(sl.loaded, st.h2d), "event");
+}
+
+void Model::offload_acquire(int o, bool backward) {
+  if (res_idx_[static_cast<std::size_t>(o)] >= 0) return;
+  OffloadState& st = *off_;
+  if (st.slot_of[static_cast<std::size_t>(o)] < 0) {
+    // not prefetched (e.g. first use after an inference pass): stage it now
+    int prev = o;
+    offload_prefetch_next(backward ? prev + 1 : prev - 1, backward);
+  }
+  OffloadSlot& sl = st.slots[static_cast<std::size_t>(st.slot_of[static_cast<std::size_t>(o)])];
+  cuda_check(cudaStreamWaitEvent(stream_, sl.loaded, 0), "wait loaded");
+  if (backward) cuda_check(cudaMemsetAsync(sl.g32.p, 0, sl.g32.bytes, stream_), "zero slot grads");
+}
+
+void Model::offload_release(int o, bool backward) {
+  // resident layers need nothing: the next SLOW granule was already staged
+  // one ahead when the previous SLOW layer (or the step) started
+  if (res_idx_[static_cast<std::size_t>(o)] >= 0) return;
+  OffloadState& st = *off_;
+  OffloadSlot& sl = st.slots[static_cast<std::size_t>(st.slot_of[static_cast<std::size_t>(o)])];
+  const std::size_t g = static_cast<std::size_t>(layer_stride_);
+  if (!backward) {
+    cuda_check(cudaEventRecord(sl.free_ev, stream_), "event");
+    sl.free_recorded = true;
+    offload_prefetch_next(o, false);
+    return;
+  }
+  // An phase: fused AdamW on the staged granule, then write back
+  cudaEvent_t done = st.ev();
+  if (has_opt_) {
+    const std::int64_t t = step_count_ + 1;
+    const float bc1 = 1.0f - std::pow(b1_, static_cast<float>(t));
+    const float bc2 = 1.0f - std::pow(b2_, static_cast<float>(t));
+    adamw_granule(sl.p32.as<float>(), sl.g32.as<float>(), sl.m.as<float>(), sl.v.as<float>(), sl.p16.p, offload_lr_,
+                  bc1, bc2);
+  }
+  cuda_check(cudaEventRecord(done, stream_), "event");
+  cuda_check(cudaStreamWaitEvent(st.d2h, done, 0), "wait compute");
+  cudaEvent_t a = st.ev(), b = st.ev();
+  cuda_check(cudaEventRecord(a, st.d2h), "event");
+  if (has_opt_) {
+    copy_async(st, slow_host_p32(o), sl.p32.p, g * 4, st.d2h, false, &st.stats.writeback);
+    copy_async(st, slow_host_p16(o), sl.p16.p, g * 2, st.d2h, false, &st.stats.writeback);
+    copy_async(st, slow_host_m(o, 0), sl.m.p, g * 4, st.d2h, false, &st.stats.writeback);
+    copy_async(st, slow_host_m(o, 1), sl.v.p, g * 4, st.d2h, false, &st.stats.writeback);
+  } else {
+    if (!st.hg) {
+      const std::size_t n = g * st.slow_list.size();
+      cuda_check(cudaMallocHost(reinterpret_cast<void**>(&st.hg), n * 4), "pinned grads");
+      std::memset(st.hg, 0, n * 4);
+    }
+    copy_async(st, slow_host_grad(o), sl.g32.p, g * 4, st.d2h, false, &st.stats.grad_offload);
+  }
+  cuda_check(cudaEventRecord(b, st.d2h), "event");
+  st.copies.push_back({a, b, false});
+  cuda_check(cudaEventRecord(st.wb_ev[static_cast<std::size_t>(o)], st.d2h), "event");
+  st.wb_recorded[static_cast<std::size_t>(o)] = 1;
+  cuda_check(cudaEventRecord(sl.free_ev, st.d2h), "event");
+  sl.free_recorded = true;
+  offload_prefetch_next(o, true);
+}
+
+void Model::offload_finish_step() {}
+
+void offload_sync(const OffloadState& st) {
+  if (st.h2d) cuda_check(cudaStreamSynchronize(st.h2d), "sync h2d");
+  if (st.d2h) cuda_check(cudaStreamSynchronize(st.d2h), "sync d2h");
+}
+
+OffloadStats Model::offload_stats() {
+  OffloadStats out;
+  if (!off_) return out;
+  OffloadState& st = *off_;
+  cuda_check(cudaStreamSynchronize(st.h2d), "sync h2d");
+  cuda_check(cudaStreamSynchronize(st.d2h), "sync d2h");
+  out = st.stats;
+  for (const auto& c : st.copies) {
+    float ms = 0;
+    cuda_check(cudaEventElapsedTime(&ms, c.a, c.b), "event time");
+    (c.h2d ? out.h2d_ms : out.d2h_ms) += ms;
+  }
+  out.copies = static_cast<std::int64_t>(st.copies.size());
+  return out;
+}
+
+void Model::offload_stats_reset() {
+  if (!off_) return;
+  OffloadState& st = *off_;
+  cuda_check(cudaStreamSynchronize(st.h2d), "sync h2d");
+  cuda_check(cudaStreamSynchronize(st.d2h), "sync d2h");
+  st.stats = OffloadStats{};
+  st.copies.clear();
+  st.pool_used = 0;
+}
+
+void Model::set_offload_skip_copies(bool skip) {
+  if (off_) off_->skip = skip;
+}
+
+std::int64_t Model::device_param_bytes() const {
+  std::int64_t b = static_cast<std::int64_t>(emb_p_.bytes + emb_g_.bytes + emb_p16_.bytes + emb_m_.bytes +
+                                             emb_v_.bytes + lay_p_.bytes + lay_g_.bytes + lay_p16_.bytes +
+                                             lay_m_.bytes + lay_v_.bytes);
+  if (off_)
+    for (const auto& s : off_->slots)
+      b += static_cast<std::int64_t>(s.p32.bytes + s.g32.bytes + s.m.bytes + s.v.bytes + s.p16.bytes);
+  return b;
+}
+
+}  // namespace p2r

@@ -42,6 +42,12 @@ _lib._EXTRA_SIGNATURES.update({
     "p2r_model_routing": [vp, ip, vp, vp, vp, ctypes.POINTER(ip), ctypes.POINTER(ip)],
     "p2r_moe_dispatch_host": [vp, ip, ip, ip, fp, vp, vp, vp, vp, vp, vp,
                               ctypes.POINTER(ip), ctypes.POINTER(ip)],
+    "p2r_model_create_offload": [ctypes.POINTER(ModelConfigC), ctypes.c_uint64, vp, ip, ctypes.POINTER(vp)],
+    "p2r_model_set_offload_lr": [vp, fp],
+    "p2r_model_offload_stats": [vp, vp],
+    "p2r_model_offload_stats_reset": [vp],
+    "p2r_model_set_offload_skip_copies": [vp, ip],
+    "p2r_plan_offload": [vp, ip, i64, ctypes.c_double, ctypes.c_double, ctypes.c_double, vp],
     "p2r_model_set_profiling": [vp, ip],
     "p2r_model_profile": [vp, ip, ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_double),
                           ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)],
@@ -65,7 +71,30 @@ def _declare_extra():
     L.p2r_lr_at.restype = fp
     L.p2r_moe_capacity.argtypes = [fp, ip, ip, ip]
     L.p2r_moe_capacity.restype = ctypes.c_int
+    for n in ("p2r_model_layer_granule_bytes", "p2r_model_device_param_bytes"):
+        getattr(L, n).argtypes = [vp]
+        getattr(L, n).restype = i64
+    L.p2r_predict_step_time.argtypes = [vp, vp, ip, ctypes.c_double, ctypes.c_double, ctypes.c_double]
+    L.p2r_predict_step_time.restype = ctypes.c_double
     return L
+
+
+def plan_offload(layer_bytes, budget, bandwidth, compute_s, latency_s=0.0):
+    """plan_offload -> list of 0/1 (1 = SLOW / offloaded)."""
+    _declare_extra()
+    b = np.ascontiguousarray(layer_bytes, np.int64)
+    out = np.zeros(b.size, np.int32)
+    check(lib().p2r_plan_offload(_p(b), b.size, int(budget), float(bandwidth), float(compute_s),
+                                 float(latency_s), _p(out)))
+    return [int(x) for x in out]
+
+
+def predict_step_time(layer_bytes, slow, bandwidth, compute_s, latency_s=0.0) -> float:
+    L = _declare_extra()
+    b = np.ascontiguousarray(layer_bytes, np.int64)
+    s = np.ascontiguousarray(slow, np.int32)
+    return float(L.p2r_predict_step_time(_p(b), _p(s), b.size, float(bandwidth), float(compute_s),
+                                         float(latency_s)))
 
 
 def _p(a):
@@ -113,12 +142,18 @@ def lr_at(peak, warmup_ratio, total, step) -> float:
 class Model:
     """p2r::Model + AdamW on one B200 (one CUDA stream per model)."""
 
-    def __init__(self, cfg: Config, seed: int = 1234, handle=None):
+    def __init__(self, cfg: Config, seed: int = 1234, handle=None, offload=None, ring_slots: int = 3):
+        """offload: per-owned-layer 0/1 placement (1 = SLOW, kept in pinned host DRAM)."""
         L = _declare_extra()
         self.cfg = cfg
         if handle is None:
             h = vp()
-            check(L.p2r_model_create(ctypes.byref(cfg.c()), seed, ctypes.byref(h)))
+            if offload is None:
+                check(L.p2r_model_create(ctypes.byref(cfg.c()), seed, ctypes.byref(h)))
+            else:
+                sl = np.ascontiguousarray(offload, np.int32)
+                check(L.p2r_model_create_offload(ctypes.byref(cfg.c()), seed, _p(sl), ring_slots,
+                                                 ctypes.byref(h)))
             handle = h.value
         self.h = handle
         self.names, self.shapes = [], []
@@ -194,6 +229,28 @@ class Model:
 
     def stream(self) -> int:
         return int(lib().p2r_model_stream(self.h) or 0)
+
+    # ---- granular offload
+    def set_offload_lr(self, lr: float):
+        check(lib().p2r_model_set_offload_lr(self.h, lr))
+
+    def offload_stats(self) -> dict:
+        o = np.zeros(7, np.float64)
+        check(lib().p2r_model_offload_stats(self.h, _p(o)))
+        keys = ("Fn_load", "Bn_load", "opt_load", "writeback", "grad_offload", "h2d_ms", "d2h_ms")
+        return dict(zip(keys, (float(x) for x in o)))
+
+    def offload_stats_reset(self):
+        check(lib().p2r_model_offload_stats_reset(self.h))
+
+    def set_offload_skip_copies(self, skip: bool):
+        check(lib().p2r_model_set_offload_skip_copies(self.h, int(skip)))
+
+    def layer_granule_bytes(self) -> int:
+        return int(lib().p2r_model_layer_granule_bytes(self.h))
+
+    def device_param_bytes(self) -> int:
+        return int(lib().p2r_model_device_param_bytes(self.h))
 
     PROF_CLASSES = ("gemm", "attn_fwd", "attn_bwd", "layernorm", "cross_entropy", "embed", "adamw",
                     "moe", "bias_grad", "delink")

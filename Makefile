@@ -20,7 +20,7 @@ $(BUILD)/%.o: $(CSRC)/%.cu $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h) inc
 	@mkdir -p $(dir $@)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
-$(BUILD)/engine/%.o: $(CSRC)/engine/%.cpp $(wildcard include/p2r/*.hpp) $(wildcard include/*.h)
+$(BUILD)/engine/%.o: $(CSRC)/engine/%.cpp $(wildcard $(CSRC)/engine/*.hpp) $(wildcard include/p2r/*.hpp) $(wildcard include/*.h)
 	@mkdir -p $(dir $@)
 	$(CXX) -std=c++20 -O2 -fPIC -Wall -Iinclude -I/usr/local/cuda/include -c $< -o $@
 

@@ -13,6 +13,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <random>
 #include <string>
@@ -307,8 +309,10 @@ void* Model::lp16(int o, long long off) const {
 void Model::init_params(std::uint64_t seed) {
   // model.cpp:128-164: gains 1, biases 0, matrices N(0, 0.02) per named tensor
   std::vector<float> host;
+  const bool trace = std::getenv("P2R_TRACE") != nullptr;
   for (int i = 0; i < static_cast<int>(views_.size()); ++i) {
     const ParamView& v = views_[i];
+    if (trace) std::fprintf(stderr, "init %s granule %d off %lld rows %d cols %d ld %d\n", v.name.c_str(), v.granule, v.off, v.rows, v.cols, v.ld);
     const std::size_t n = static_cast<std::size_t>(v.rows) * v.cols;
     host.assign(n, 0.0f);
     const std::string& nm = v.name;

@@ -3,10 +3,12 @@
 //
 // SLOW layer granules live in pinned host DRAM (fp32 master + bf16 shadow +
 // AdamW moments). A ring of HBM staging slots (each one granule of p32, grad,
-// m, v, bf16) is fed by cudaMemcpyAsync on a dedicated H2D stream, one granule
-// ahead of the compute stream (event-synchronised), and drained by a D2H stream:
-//   Fn : H2D p32 + bf16 of layer l while layer l-1 computes
-//   Bn : H2D p32 + bf16 (+ m, v) of layer l while layer l+1 runs its backward
+// m, v, bf16) is fed by cudaMemcpyAsync on a dedicated H2D stream and drained
+// by a D2H stream, event-synchronised with the compute stream. The step's SLOW
+// uses (forward ascending, then backward descending) are staged as far ahead as
+// the ring allows, so backward granules load during the H2D-light forward:
+//   Fn : H2D bf16 shadow + the fp32 vectors / MoE gate the forward reads
+//   Bn : H2D fp32 master (+ m, v); the bf16 shadow is re-derived on the device
 //   An : AdamW for the granule on the GPU right after its backward, then D2H
 //        write-back of p32 + bf16 + m + v (or of the grads when no optimizer
 //        is attached: the spec's "gradient offload").
@@ -112,6 +114,8 @@ void Model::offload_setup(const std::vector<int>& slow, int ring_slots) {
   st->ring = ring_slots;
   st->stride = layer_stride_;
   st->slot_of.assign(static_cast<std::size_t>(n_owned_), -1);
+  st->slot_fwd.assign(static_cast<std::size_t>(n_owned_), -1);
+  st->slot_bwd.assign(static_cast<std::size_t>(n_owned_), -1);
   st->host_idx.assign(static_cast<std::size_t>(n_owned_), -1);
   slow_ = slow;
   int nr = 0, ns = 0;
@@ -188,81 +192,95 @@ void Model::offload_begin_forward(bool training) {
   OffloadState& st = *off_;
   st.training = training;
   std::fill(st.slot_of.begin(), st.slot_of.end(), -1);
+  std::fill(st.slot_fwd.begin(), st.slot_fwd.end(), -1);
+  std::fill(st.slot_bwd.begin(), st.slot_bwd.end(), -1);
   for (auto& s : st.slots) s.layer = -1;
-  if (!st.slow_list.empty()) offload_prefetch_next(-1, false);
+  st.sched.clear();
+  for (int o : st.slow_list) st.sched.emplace_back(o, false);
+  if (training)
+    for (auto it = st.slow_list.rbegin(); it != st.slow_list.rend(); ++it) st.sched.emplace_back(*it, true);
+  st.next_issue = 0;
+  st.in_flight = 0;
+  offload_prefetch_next(-1, false);
 }
 
-// Stage `o` (the next SLOW layer after `after` in the phase's order) into a slot.
-void Model::offload_prefetch_next(int after, bool backward) {
+// Issue H2D staging for the next schedule entries while staging slots are
+// available: the ring holds `ring` granules in flight, so backward granules
+// start loading during the (H2D-light) forward pass. Slots are reused in FIFO
+// order; each reuse waits (on the H2D stream) for the slot's previous consumer.
+void Model::offload_prefetch_next(int /*after*/, bool /*backward*/) {
   OffloadState& st = *off_;
-  int o = -1;
-  if (!backward) {
-    for (int x : st.slow_list)
-      if (x > after) {
-        o = x;
-        break;
-      }
-    if (o < 0) {
-      if (!st.training) return;
-      backward = true;  // forward done: stage the last SLOW layer for the backward
-      after = n_owned_;
-    }
-  }
-  if (backward) {
-    for (auto it = st.slow_list.rbegin(); it != st.slow_list.rend(); ++it)
-      if (*it < after) {
-        o = *it;
-        break;
-      }
-  }
-  if (o < 0) return;
-  const int si = st.next_slot;
-  st.next_slot = (st.next_slot + 1) % st.ring;
-  OffloadSlot& sl = st.slots[static_cast<std::size_t>(si)];
-  if (sl.layer >= 0 && st.slot_of[static_cast<std::size_t>(sl.layer)] == si)
-    st.slot_of[static_cast<std::size_t>(sl.layer)] = -1;
-  for (auto& other : st.slots)
-    if (other.layer == o) other.layer = -1;  // o re-staged (forward copy -> backward copy)
-  sl.layer = o;
-  st.slot_of[static_cast<std::size_t>(o)] = si;
-  if (sl.free_recorded) cuda_check(cudaStreamWaitEvent(st.h2d, sl.free_ev, 0), "wait slot free");
-  if (st.wb_recorded[static_cast<std::size_t>(o)])
-    cuda_check(cudaStreamWaitEvent(st.h2d, st.wb_ev[static_cast<std::size_t>(o)], 0), "wait write-back");
   const std::size_t g = static_cast<std::size_t>(layer_stride_);
-  cudaEvent_t a = st.ev(), b = st.ev();
-  cuda_check(cudaEventRecord(a, st.h2d), "event");
-  double* ctr = backward ? &st.stats.bn_load : &st.stats.fn_load;
-  copy_async(st, sl.p32.p, slow_host_p32(o), g * 4, st.h2d, true, ctr);
-  copy_async(st, sl.p16.p, slow_host_p16(o), g * 2, st.h2d, true, ctr);
-  if (backward && has_opt_) {
-    copy_async(st, sl.m.p, slow_host_m(o, 0), g * 4, st.h2d, true, &st.stats.opt_load);
-    copy_async(st, sl.v.p, slow_host_m(o, 1), g * 4, st.h2d, true, &st.stats.opt_load);
+  while (st.next_issue < st.sched.size() && st.in_flight < st.ring) {
+    const int o = st.sched[st.next_issue].first;
+    const bool bwd = st.sched[st.next_issue].second;
+    ++st.next_issue;
+    ++st.in_flight;
+    const int si = st.next_slot_rr;
+    st.next_slot_rr = (st.next_slot_rr + 1) % st.ring;
+    OffloadSlot& sl = st.slots[static_cast<std::size_t>(si)];
+    sl.layer = o;
+    (bwd ? st.slot_bwd : st.slot_fwd)[static_cast<std::size_t>(o)] = si;
+    if (sl.free_recorded) cuda_check(cudaStreamWaitEvent(st.h2d, sl.free_ev, 0), "wait slot free");
+    if (st.wb_recorded[static_cast<std::size_t>(o)])
+      cuda_check(cudaStreamWaitEvent(st.h2d, st.wb_ev[static_cast<std::size_t>(o)], 0), "wait write-back");
+    cudaEvent_t a = st.ev(), b = st.ev();
+    cuda_check(cudaEventRecord(a, st.h2d), "event");
+    if (!bwd) {
+      // Fn: the bf16 shadow feeds every GEMM; fp32 is only read for the vectors
+      // (LN gains/biases, biases) and the fp32 MoE gate
+      copy_async(st, sl.p16.p, slow_host_p16(o), g * 2, st.h2d, true, &st.stats.fn_load);
+      for (const auto& sg : layer_.segs) {
+        const bool fp32_use = !sg.decay || (cfg_.moe.enabled() && sg.off == layer_.gate);
+        if (!fp32_use) continue;
+        copy_async(st, sl.p32.as<float>() + sg.off, slow_host_p32(o) + sg.off, static_cast<std::size_t>(sg.len) * 4,
+                   st.h2d, true, &st.stats.fn_load);
+      }
+    } else {
+      // Bn + An: fp32 master (bf16 shadow re-derived on the device) + moments
+      copy_async(st, sl.p32.p, slow_host_p32(o), g * 4, st.h2d, true, &st.stats.bn_load);
+      if (has_opt_) {
+        copy_async(st, sl.m.p, slow_host_m(o, 0), g * 4, st.h2d, true, &st.stats.opt_load);
+        copy_async(st, sl.v.p, slow_host_m(o, 1), g * 4, st.h2d, true, &st.stats.opt_load);
+      }
+    }
+    cuda_check(cudaEventRecord(b, st.h2d), "event");
+    st.copies.push_back({a, b, true});
+    cuda_check(cudaEventRecord(sl.loaded, st.h2d), "event");
   }
-  cuda_check(cudaEventRecord(b, st.h2d), "event");
-  st.copies.push_back({a, b, true});
-  cuda_check(cudaEventRecord(sl.loaded, st.h2d), "event");
 }
 
 void Model::offload_acquire(int o, bool backward) {
   if (res_idx_[static_cast<std::size_t>(o)] >= 0) return;
   OffloadState& st = *off_;
-  if (st.slot_of[static_cast<std::size_t>(o)] < 0) {
-    // not prefetched (e.g. first use after an inference pass): stage it now
-    int prev = o;
-    offload_prefetch_next(backward ? prev + 1 : prev - 1, backward);
+  std::vector<int>& map = backward ? st.slot_bwd : st.slot_fwd;
+  if (map[static_cast<std::size_t>(o)] < 0) {
+    // used outside the step schedule (e.g. a backward after an inference
+    // forward): restart the schedule at this use
+    st.sched.assign(1, {o, backward});
+    st.next_issue = 0;
+    st.in_flight = 0;
+    offload_prefetch_next(-1, backward);
   }
-  OffloadSlot& sl = st.slots[static_cast<std::size_t>(st.slot_of[static_cast<std::size_t>(o)])];
+  const int si = map[static_cast<std::size_t>(o)];
+  st.slot_of[static_cast<std::size_t>(o)] = si;
+  OffloadSlot& sl = st.slots[static_cast<std::size_t>(si)];
   cuda_check(cudaStreamWaitEvent(stream_, sl.loaded, 0), "wait loaded");
-  if (backward) cuda_check(cudaMemsetAsync(sl.g32.p, 0, sl.g32.bytes, stream_), "zero slot grads");
+  if (backward) {
+    p2r_check(p2r_cast_bf16(sl.p32.as<float>(), sl.p16.p, layer_stride_, stream_), "offload bf16 shadow");
+    cuda_check(cudaMemsetAsync(sl.g32.p, 0, sl.g32.bytes, stream_), "zero slot grads");
+  }
 }
 
 void Model::offload_release(int o, bool backward) {
-  // resident layers need nothing: the next SLOW granule was already staged
-  // one ahead when the previous SLOW layer (or the step) started
+  // resident layers need nothing: SLOW granules are staged ahead by the schedule
   if (res_idx_[static_cast<std::size_t>(o)] >= 0) return;
   OffloadState& st = *off_;
-  OffloadSlot& sl = st.slots[static_cast<std::size_t>(st.slot_of[static_cast<std::size_t>(o)])];
+  const int si = st.slot_of[static_cast<std::size_t>(o)];
+  OffloadSlot& sl = st.slots[static_cast<std::size_t>(si)];
   const std::size_t g = static_cast<std::size_t>(layer_stride_);
+  (backward ? st.slot_bwd : st.slot_fwd)[static_cast<std::size_t>(o)] = -1;
+  st.in_flight = std::max(0, st.in_flight - 1);
   if (!backward) {
     cuda_check(cudaEventRecord(sl.free_ev, stream_), "event");
     sl.free_recorded = true;

@@ -19,7 +19,13 @@ struct OffloadSlot {
 struct OffloadState {
   int ring = 2;
   std::vector<OffloadSlot> slots;
-  std::vector<int> slot_of;    // owned layer -> slot or -1
+  std::vector<int> slot_of;    // owned layer -> slot used by the phase being computed
+  std::vector<int> slot_fwd, slot_bwd;  // owned layer -> slot staged for that phase or -1
+  // step schedule of SLOW granule uses: forward ascending, then backward descending
+  std::vector<std::pair<int, bool>> sched;
+  std::size_t next_issue = 0;
+  int in_flight = 0;
+  int next_slot_rr = 0;
   std::vector<int> host_idx;   // owned layer -> index in host arrays or -1
   std::vector<int> slow_list;  // SLOW owned layers, ascending
   std::vector<cudaEvent_t> wb_ev;

@@ -173,7 +173,18 @@ class Model {
   // Real model with granular CPU offload: slow[i] = 1 keeps owned layer i in
   // pinned host DRAM and streams it through `ring_slots` HBM staging slots.
   Model(ModelConfig config, std::uint64_t seed, const std::vector<int>& slow, int ring_slots);
+  // Expert-parallel shard `ep_rank` of `ep_world`: holds experts
+  // [ep_rank*E/W, (ep_rank+1)*E/W) (model.cpp:334-340) + the replicated rest.
+  Model(ModelConfig config, std::uint64_t seed, int ep_world, int ep_rank);
   ~Model();
+
+  // NCCL (one communicator per model over all ranks; csrc/engine/comm.cpp)
+  void comm_init(const char* unique_id128);
+  void comm_destroy();
+  void allreduce_grads();  // DP: sum replicated grads (embeddings, attention, norms, gate, dense FFN)
+  int ep_world() const { return ep_world_; }
+  int ep_rank() const { return ep_rank_; }
+  bool ep_active() const { return ep_world_ > 1 || force_ep_; }
   Model(const Model&) = delete;
   Model& operator=(const Model&) = delete;
 
@@ -242,7 +253,7 @@ class Model {
 
  private:
   struct NoInit {};
-  Model(ModelConfig config, NoInit);
+  Model(ModelConfig config, NoInit, int ep_world = 1, int ep_rank = 0, bool force_ep = false);
   // offload plumbing (csrc/engine/offload.cpp)
   void offload_setup(const std::vector<int>& slow, int ring_slots);
   void offload_begin_forward(bool training);
@@ -312,7 +323,15 @@ class Model {
   int n_res_ = 0;
   std::unique_ptr<OffloadState> off_;
   float offload_lr_ = 0.0f;
+  // expert / data parallelism
+  int ep_world_ = 1, ep_rank_ = 0;
+  bool force_ep_ = false;  // P2R_FORCE_EP=1: run the exchange path even at W = 1 (tests)
+  void* comm_ = nullptr;   // ncclComm_t
+  void ep_exchange(const void* src, void* dst, std::size_t row_bytes, int seg, bool to_experts);
 };
+
+// ncclGetUniqueId (dlopen'ed libnccl.so.2)
+void comm_unique_id(char* out128);
 
 // moe_dispatch on host logits via the routing kernel (bit-exact, model.cpp:294-332)
 struct HostRouting {

@@ -116,6 +116,19 @@ p2r_status p2r_moe_dispatch_host(const float* logits, int T, int E, int k, float
                                  uint8_t* survived, int* raw_load, int* offsets, int* rows,
                                  int* slots, int* capacity, int* dropped);
 
+/* ---- expert / data parallelism over NCCL --------------------
+ * Rank r of W holds experts [r*E/W, (r+1)*E/W) (Model::expert_shard's
+ * contiguous map, model.cpp:334-340) plus a replica of everything else; MoE
+ * dispatch/combine exchange fixed-capacity expert segments with grouped
+ * ncclSend/ncclRecv on the model stream; replicated grads are summed with
+ * p2r_model_allreduce_grads. Each rank must use the GLOBAL mask count as the CE
+ * denominator so the summed gradient is the large-batch mean. */
+p2r_status p2r_comm_unique_id(char* out128);
+p2r_status p2r_model_create_ep(const p2r_model_config* cfg, uint64_t seed, int world, int rank,
+                               p2r_model** out);
+p2r_status p2r_model_comm_init(p2r_model* m, const char* unique_id128);
+p2r_status p2r_model_allreduce_grads(p2r_model* m);
+
 /* ---- granular CPU offload (§4.2) ---------------
  * Real model whose owned layers with slow[i] = 1 live in pinned host DRAM and
  * are streamed through `ring_slots` HBM staging slots one granule ahead of

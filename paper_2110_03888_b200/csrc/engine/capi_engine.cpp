@@ -198,6 +198,23 @@ p2r_status p2r_moe_dispatch_host(const float* logits, int T, int E, int k, float
   });
 }
 
+p2r_status p2r_comm_unique_id(char* out128) {
+  return guard([&] { p2r::comm_unique_id(out128); });
+}
+p2r_status p2r_model_create_ep(const p2r_model_config* cfg, uint64_t seed, int world, int rank, p2r_model** out) {
+  return guard([&] {
+    auto h = std::make_unique<p2r_model>();
+    h->m = std::make_unique<p2r::Model>(to_cfg(cfg), seed, world, rank);
+    *out = h.release();
+  });
+}
+p2r_status p2r_model_comm_init(p2r_model* m, const char* id) {
+  return guard([&] { m->m->comm_init(id); });
+}
+p2r_status p2r_model_allreduce_grads(p2r_model* m) {
+  return guard([&] { m->m->allreduce_grads(); });
+}
+
 p2r_status p2r_model_create_offload(const p2r_model_config* cfg, uint64_t seed, const int* slow, int ring_slots,
                                     p2r_model** out) {
   return guard([&] {

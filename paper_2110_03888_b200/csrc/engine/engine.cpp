@@ -172,6 +172,7 @@ struct Acts {
   DevBuf dres, dres16, tmp32, dx1, dx1_16, do16, dqkv16, dh16, dye16, dxe32, dw, glogits, dsum;
   DevBuf ln_ws, colsum_ws;
   DevBuf tokens, targets, mask;
+  DevBuf xe_send16, ye_owner32, dxe_owner32, full_counts;  // expert-parallel exchange
 };
 
 // ---------------------------------------------------------------- Model
@@ -191,14 +192,31 @@ Model::Model(ModelConfig config, std::uint64_t seed, const std::vector<int>& slo
   init_params(seed);
 }
 
-Model::Model(ModelConfig config, NoInit) : cfg_(std::move(config)) {
+Model::Model(ModelConfig config, std::uint64_t seed, int ep_world, int ep_rank) : cfg_(std::move(config)) {
   cfg_.validate();
+  if (ep_world < 1 || ep_rank < 0 || ep_rank >= ep_world)
+    throw std::invalid_argument("expert parallel: rank must be in [0, world)");
+  ep_world_ = ep_world;
+  ep_rank_ = ep_rank;
+  const char* f = std::getenv("P2R_FORCE_EP");
+  force_ep_ = f != nullptr && f[0] == '1';
+  build_layout();
+  allocate();
+  init_params(seed);
+}
+
+Model::Model(ModelConfig config, NoInit, int ep_world, int ep_rank, bool force_ep) : cfg_(std::move(config)) {
+  cfg_.validate();
+  ep_world_ = ep_world;
+  ep_rank_ = ep_rank;
+  force_ep_ = force_ep;
   build_layout();
   allocate();
 }
 
 Model::~Model() {
   if (stream_) cudaStreamSynchronize(stream_);
+  comm_destroy();
   off_.reset();
   if (pinned_) cudaFreeHost(pinned_);
   if (stream_) cudaStreamDestroy(stream_);
@@ -206,7 +224,10 @@ Model::~Model() {
 
 void Model::build_layout() {
   const int d = cfg_.d_model, dff = cfg_.d_ff, V = cfg_.vocab_size, S = cfg_.seq_len;
-  const int E = cfg_.moe.n_experts;
+  const int Eg = cfg_.moe.n_experts;
+  if (Eg > 0 && Eg % ep_world_ != 0)
+    throw std::invalid_argument("moe config: n_experts must be divisible by the expert-parallel world size");
+  const int E = Eg > 0 ? Eg / ep_world_ : 0;  // experts held by this rank
   n_owned_ = cfg_.n_layers_params;
   n_res_ = n_owned_;
   res_idx_.resize(static_cast<std::size_t>(n_owned_));
@@ -227,7 +248,7 @@ void Model::build_layout() {
   layer_.ln2_g = layer_.add(d, false);
   layer_.ln2_b = layer_.add(d, false);
   if (cfg_.moe.enabled()) {
-    layer_.gate = layer_.add(1LL * d * E, true);
+    layer_.gate = layer_.add(1LL * d * Eg, true);  // replicated, routes over all experts
     layer_.w1 = layer_.add(1LL * E * d * dff, true);  // [E, d, dff]
     layer_.b1 = layer_.add(1LL * E * dff, false);     // [E, dff]
     layer_.w2 = layer_.add(1LL * E * dff * d, true);  // [E, dff, d]
@@ -262,9 +283,10 @@ void Model::build_layout() {
       views_.push_back({pre + "ffn.w2", i, layer_.w2, dff, d, d, {dff, d}});
       views_.push_back({pre + "ffn.b2", i, layer_.b2, 1, d, d, {d}});
     } else {
-      views_.push_back({pre + "moe.gate", i, layer_.gate, d, E, E, {d, E}});
+      views_.push_back({pre + "moe.gate", i, layer_.gate, d, Eg, Eg, {d, Eg}});
       for (int e = 0; e < E; ++e) {
-        const std::string ep = pre + "moe.expert." + std::to_string(e) + ".";
+        // global expert index: rank r owns experts [r*E, (r+1)*E) (model.cpp:334-340)
+        const std::string ep = pre + "moe.expert." + std::to_string(ep_rank_ * E + e) + ".";
         views_.push_back({ep + "w1", i, layer_.w1 + 1LL * e * d * dff, d, dff, dff, {d, dff}});
         views_.push_back({ep + "b1", i, layer_.b1 + 1LL * e * dff, 1, dff, dff, {dff}});
         views_.push_back({ep + "w2", i, layer_.w2 + 1LL * e * dff * d, dff, d, d, {dff, d}});
@@ -483,6 +505,15 @@ void Model::ensure_acts(int B, int S) {
     A->dye16 = DevBuf(ES * d * 2);
     A->dxe32 = DevBuf(ES * d * 4);
     A->dw = DevBuf(static_cast<std::size_t>(T) * k * 4);
+    if (ep_active()) {
+      A->xe_send16 = DevBuf(ES * d * 2);
+      A->ye_owner32 = DevBuf(ES * d * 4);
+      A->dxe_owner32 = DevBuf(ES * d * 4);
+      const int El = E / ep_world_;
+      std::vector<int> full(static_cast<std::size_t>(El), ep_world_ * A->seg);
+      A->full_counts = DevBuf(static_cast<std::size_t>(El) * 4);
+      cuda_check(cudaMemcpy(A->full_counts.p, full.data(), full.size() * 4, cudaMemcpyHostToDevice), "counts");
+    }
     A->glogits = DevBuf(static_cast<std::size_t>(T) * E * 4);
   }
   A->ln_ws = DevBuf(p2r_layernorm_bwd_workspace(T, d));
@@ -678,13 +709,27 @@ Tensor Model::block_forward(GradTape* tape, int g, const Tensor& x, int batch, A
     p2r_check(p2r_moe_combine_weights(L.logits.as<float>(), T, E, k, L.sel.as<int>(), L.surv.as<std::uint8_t>(),
                                       L.w.as<float>(), stream_),
               "combine weights");
-    p2r_check(p2r_moe_dispatch(L.b16.p, 1, d, E, seg, L.rows_pad.as<int>(), L.slots_pad.as<int>(),
-                               L.counts.as<int>(), nullptr, k, L.xe16.p, stream_),
-              "dispatch");
-    gemm(E * seg, dff, d, L.xe16.p, d, false, lp16(o, layer_.w1), dff, true, P2R_EPI_BIAS_GELU, L.ge16.p, dff,
-         L.hpre_e16.p, dff, lp(o, layer_.b1), nullptr, 0, P2R_GROUP_M, E, seg, L.counts.as<int>());
-    gemm(E * seg, d, dff, L.ge16.p, dff, false, lp16(o, layer_.w2), d, true, P2R_EPI_F32, L.ye32.p, d, nullptr, 0,
-         lp(o, layer_.b2), nullptr, 0, P2R_GROUP_M, E, seg, L.counts.as<int>());
+    // Expert parallelism: dispatch into the local expert-major layout, then the
+    // owner ranks receive [El][W][seg] segments (full-capacity groups whose
+    // padding rows are zero and contribute exactly nothing to the backward).
+    const bool ep = ep_active();
+    if (ep && comm_ == nullptr) throw std::logic_error("expert parallel: call comm_init before the first step");
+    const int El = E / ep_world_;
+    const int gseg = ep ? ep_world_ * seg : seg;
+    const int* gcnt = ep ? A.full_counts.as<int>() : L.counts.as<int>();
+    const int G = ep ? El : E;
+    void* xsend = ep ? A.xe_send16.p : L.xe16.p;
+    prof(P2R_PROF_MOE, 0, 4.0 * T * d, [&] {
+      p2r_check(p2r_moe_dispatch(L.b16.p, 1, d, E, seg, L.rows_pad.as<int>(), L.slots_pad.as<int>(),
+                                 L.counts.as<int>(), nullptr, k, xsend, stream_),
+                "dispatch");
+    });
+    if (ep) ep_exchange(xsend, L.xe16.p, static_cast<std::size_t>(d) * 2, seg, true);
+    gemm(G * gseg, dff, d, L.xe16.p, d, false, lp16(o, layer_.w1), dff, true, P2R_EPI_BIAS_GELU, L.ge16.p, dff,
+         L.hpre_e16.p, dff, lp(o, layer_.b1), nullptr, 0, P2R_GROUP_M, G, gseg, gcnt);
+    gemm(G * gseg, d, dff, L.ge16.p, dff, false, lp16(o, layer_.w2), d, true, P2R_EPI_F32,
+         ep ? A.ye_owner32.p : L.ye32.p, d, nullptr, 0, lp(o, layer_.b2), nullptr, 0, P2R_GROUP_M, G, gseg, gcnt);
+    if (ep) ep_exchange(A.ye_owner32.p, L.ye32.p, static_cast<std::size_t>(d) * 4, seg, false);
     p2r_check(p2r_moe_combine(L.ye32.as<float>(), T, d, k, seg, L.sel.as<int>(), L.pos.as<int>(), L.w.as<float>(),
                               L.x1.as<float>(), L.xout.as<float>(), stream_),
               "combine");
@@ -731,27 +776,35 @@ void Model::block_backward(int g, AttentionMode mode) {
   } else {
     const int E = cfg_.moe.n_experts, k = cfg_.moe.n_prototypes, seg = A.seg;
     const int* cnt = L.counts.as<int>();
+    const bool ep = ep_active();
+    const int El = E / ep_world_;
+    const int gseg = ep ? ep_world_ * seg : seg;
+    const int* gcnt = ep ? A.full_counts.as<int>() : cnt;
+    const int G = ep ? El : E;
     // combine backward: dw = <dy, ye>, dye = w * dy (expert-major, bf16)
     p2r_check(p2r_moe_combine_bwd_weights(dy, L.ye32.as<float>(), T, d, k, seg, L.sel.as<int>(), L.pos.as<int>(),
                                           A.dw.as<float>(), stream_),
               "combine bwd");
+    void* dye_local = ep ? A.xe_send16.p : A.dye16.p;
     p2r_check(p2r_moe_dispatch(dy, 0, d, E, seg, L.rows_pad.as<int>(), L.slots_pad.as<int>(), cnt, L.w.as<float>(),
-                               k, A.dye16.p, stream_),
+                               k, dye_local, stream_),
               "dispatch dy");
-    gemm(dff, d, seg, L.ge16.p, dff, true, A.dye16.p, d, true, P2R_EPI_ACC_F32, lg(o, layer_.w2), d, nullptr, 0,
-         nullptr, nullptr, 0, P2R_GROUP_K, E, seg, cnt);
-    p2r_check(p2r_bias_grad(A.dye16.p, 1, d, E * seg, d, E, seg, cnt, lg(o, layer_.b2), d, A.colsum_ws.as<float>(),
-                            stream_),
+    if (ep) ep_exchange(dye_local, A.dye16.p, static_cast<std::size_t>(d) * 2, seg, true);
+    gemm(dff, d, gseg, L.ge16.p, dff, true, A.dye16.p, d, true, P2R_EPI_ACC_F32, lg(o, layer_.w2), d, nullptr, 0,
+         nullptr, nullptr, 0, P2R_GROUP_K, G, gseg, gcnt);
+    p2r_check(p2r_bias_grad(A.dye16.p, 1, d, G * gseg, d, G, gseg, gcnt, lg(o, layer_.b2), d,
+                            A.colsum_ws.as<float>(), stream_),
               "db2");
-    gemm(E * seg, dff, d, A.dye16.p, d, false, lp16(o, layer_.w2), d, false, P2R_EPI_DGELU, A.dh16.p, dff, nullptr,
-         0, nullptr, L.hpre_e16.p, dff, P2R_GROUP_M, E, seg, cnt);
-    gemm(d, dff, seg, L.xe16.p, d, true, A.dh16.p, dff, true, P2R_EPI_ACC_F32, lg(o, layer_.w1), dff, nullptr, 0,
-         nullptr, nullptr, 0, P2R_GROUP_K, E, seg, cnt);
-    p2r_check(p2r_bias_grad(A.dh16.p, 1, dff, E * seg, dff, E, seg, cnt, lg(o, layer_.b1), dff,
+    gemm(G * gseg, dff, d, A.dye16.p, d, false, lp16(o, layer_.w2), d, false, P2R_EPI_DGELU, A.dh16.p, dff, nullptr,
+         0, nullptr, L.hpre_e16.p, dff, P2R_GROUP_M, G, gseg, gcnt);
+    gemm(d, dff, gseg, L.xe16.p, d, true, A.dh16.p, dff, true, P2R_EPI_ACC_F32, lg(o, layer_.w1), dff, nullptr, 0,
+         nullptr, nullptr, 0, P2R_GROUP_K, G, gseg, gcnt);
+    p2r_check(p2r_bias_grad(A.dh16.p, 1, dff, G * gseg, dff, G, gseg, gcnt, lg(o, layer_.b1), dff,
                             A.colsum_ws.as<float>(), stream_),
               "db1");
-    gemm(E * seg, d, dff, A.dh16.p, dff, false, lp16(o, layer_.w1), dff, false, P2R_EPI_F32, A.dxe32.p, d, nullptr,
-         0, nullptr, nullptr, 0, P2R_GROUP_M, E, seg, cnt);
+    gemm(G * gseg, d, dff, A.dh16.p, dff, false, lp16(o, layer_.w1), dff, false, P2R_EPI_F32,
+         ep ? A.dxe_owner32.p : A.dxe32.p, d, nullptr, 0, nullptr, nullptr, 0, P2R_GROUP_M, G, gseg, gcnt);
+    if (ep) ep_exchange(A.dxe_owner32.p, A.dxe32.p, static_cast<std::size_t>(d) * 4, seg, false);
     const float* glog = nullptr;
     if (k > 1) {  // top-1 => combine weights are exactly 1 and the gate gradient is exactly 0
       p2r_check(p2r_moe_gate_bwd(L.b32.as<float>(), L.w.as<float>(), A.dw.as<float>(), T, d, E, k, L.sel.as<int>(),
@@ -995,7 +1048,9 @@ std::int64_t Model::state_bytes() const {
 std::unique_ptr<Model> Model::delinked() const {
   if (cfg_.n_layers_params != 1) throw std::logic_error("delinked: model is not in shared-parameter mode");
   if (off_) throw std::logic_error("delinked: offloaded models are Real already");
-  std::unique_ptr<Model> real(new Model(cfg_.as_unshared(), NoInit{}));
+  // each expert-parallel rank delinks its own shard (no communication); the Real
+  // model needs its own communicator (comm_init) before an expert-parallel step
+  std::unique_ptr<Model> real(new Model(cfg_.as_unshared(), NoInit{}, ep_world_, ep_rank_, force_ep_));
   cudaStream_t s = real->stream_;
   cuda_check(cudaStreamSynchronize(stream_), "sync");
   // embeddings + final norm: direct copies

@@ -42,6 +42,10 @@ _lib._EXTRA_SIGNATURES.update({
     "p2r_model_routing": [vp, ip, vp, vp, vp, ctypes.POINTER(ip), ctypes.POINTER(ip)],
     "p2r_moe_dispatch_host": [vp, ip, ip, ip, fp, vp, vp, vp, vp, vp, vp,
                               ctypes.POINTER(ip), ctypes.POINTER(ip)],
+    "p2r_comm_unique_id": [ctypes.c_char_p],
+    "p2r_model_create_ep": [ctypes.POINTER(ModelConfigC), ctypes.c_uint64, ip, ip, ctypes.POINTER(vp)],
+    "p2r_model_comm_init": [vp, ctypes.c_char_p],
+    "p2r_model_allreduce_grads": [vp],
     "p2r_model_create_offload": [ctypes.POINTER(ModelConfigC), ctypes.c_uint64, vp, ip, ctypes.POINTER(vp)],
     "p2r_model_set_offload_lr": [vp, fp],
     "p2r_model_offload_stats": [vp, vp],
@@ -77,6 +81,14 @@ def _declare_extra():
     L.p2r_predict_step_time.argtypes = [vp, vp, ip, ctypes.c_double, ctypes.c_double, ctypes.c_double]
     L.p2r_predict_step_time.restype = ctypes.c_double
     return L
+
+
+def comm_unique_id() -> bytes:
+    """ncclGetUniqueId: 128 bytes to broadcast to every rank before Model.comm_init."""
+    _declare_extra()
+    buf = ctypes.create_string_buffer(128)
+    check(lib().p2r_comm_unique_id(buf))
+    return buf.raw
 
 
 def plan_offload(layer_bytes, budget, bandwidth, compute_s, latency_s=0.0):
@@ -142,13 +154,18 @@ def lr_at(peak, warmup_ratio, total, step) -> float:
 class Model:
     """p2r::Model + AdamW on one B200 (one CUDA stream per model)."""
 
-    def __init__(self, cfg: Config, seed: int = 1234, handle=None, offload=None, ring_slots: int = 3):
-        """offload: per-owned-layer 0/1 placement (1 = SLOW, kept in pinned host DRAM)."""
+    def __init__(self, cfg: Config, seed: int = 1234, handle=None, offload=None, ring_slots: int = 3,
+                 ep=None):
+        """offload: per-owned-layer 0/1 placement (1 = SLOW, kept in pinned host DRAM).
+        ep: (world, rank) expert-parallel shard (call comm_init before stepping)."""
         L = _declare_extra()
         self.cfg = cfg
         if handle is None:
             h = vp()
-            if offload is None:
+            if ep is not None:
+                check(L.p2r_model_create_ep(ctypes.byref(cfg.c()), seed, int(ep[0]), int(ep[1]),
+                                            ctypes.byref(h)))
+            elif offload is None:
                 check(L.p2r_model_create(ctypes.byref(cfg.c()), seed, ctypes.byref(h)))
             else:
                 sl = np.ascontiguousarray(offload, np.int32)
@@ -229,6 +246,13 @@ class Model:
 
     def stream(self) -> int:
         return int(lib().p2r_model_stream(self.h) or 0)
+
+    # ---- expert / data parallelism (NCCL)
+    def comm_init(self, unique_id: bytes):
+        check(lib().p2r_model_comm_init(self.h, ctypes.c_char_p(unique_id)))
+
+    def allreduce_grads(self):
+        check(lib().p2r_model_allreduce_grads(self.h))
 
     # ---- granular offload
     def set_offload_lr(self, lr: float):

@@ -273,17 +273,15 @@ def main_p2r(args):
     loss_dev = torch.zeros(1, device="cuda")
     torch.cuda.synchronize()
     denom = float(mask.sum()) * world  # global mask count: summed grads = large-batch mean
-    grads = []
     if world > 1:
-        for which in (0, 1):
-            ptr, nb = model.buffer(which)
-            grads.append(torch.as_tensor(CudaArray(ptr, nb), device="cuda"))
+        # the library's own NCCL communicator (csrc/engine/comm.cpp); torch only ships the id
+        uid = [p2r.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        model.comm_init(uid[0])
 
     def allreduce():
         if world > 1:
-            with torch.cuda.stream(ext):
-                for g in grads:
-                    dist.all_reduce(g)
+            model.allreduce_grads()  # ncclAllReduce of the replicated grad granules, model stream
 
     def step_device(i):
         model.train_step_device(dtok.data_ptr(), dtgt.data_ptr(), dmask.data_ptr(), B, S, denom,

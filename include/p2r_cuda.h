@@ -165,7 +165,7 @@ p2r_status p2r_moe_combine_weights(const float* logits, int T, int E, int k, con
                                    const uint8_t* survived, float* w, void* stream);
 p2r_status p2r_moe_dispatch(const void* src, int src_dtype, int d, int E, int seg_rows,
                             const int* rows_pad, const int* slots_pad, const int* counts,
-                            const float* w, int k, void* xe_bf16, void* stream);
+                            const float* w, int k, void* xe_bf16, int pad_full, void* stream);
 p2r_status p2r_moe_combine(const float* ye, int T, int d, int k, int seg_rows, const int* selected,
                            const int* pos, const float* w, const float* resid, float* out,
                            void* stream);

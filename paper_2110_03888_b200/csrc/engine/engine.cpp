@@ -721,7 +721,7 @@ Tensor Model::block_forward(GradTape* tape, int g, const Tensor& x, int batch, A
     void* xsend = ep ? A.xe_send16.p : L.xe16.p;
     prof(P2R_PROF_MOE, 0, 4.0 * T * d, [&] {
       p2r_check(p2r_moe_dispatch(L.b16.p, 1, d, E, seg, L.rows_pad.as<int>(), L.slots_pad.as<int>(),
-                                 L.counts.as<int>(), nullptr, k, xsend, stream_),
+                                 L.counts.as<int>(), nullptr, k, xsend, ep ? 1 : 0, stream_),
                 "dispatch");
     });
     if (ep) ep_exchange(xsend, L.xe16.p, static_cast<std::size_t>(d) * 2, seg, true);
@@ -787,7 +787,7 @@ void Model::block_backward(int g, AttentionMode mode) {
               "combine bwd");
     void* dye_local = ep ? A.xe_send16.p : A.dye16.p;
     p2r_check(p2r_moe_dispatch(dy, 0, d, E, seg, L.rows_pad.as<int>(), L.slots_pad.as<int>(), cnt, L.w.as<float>(),
-                               k, dye_local, stream_),
+                               k, dye_local, ep ? 1 : 0, stream_),
               "dispatch dy");
     if (ep) ep_exchange(dye_local, A.dye16.p, static_cast<std::size_t>(d) * 2, seg, true);
     gemm(dff, d, gseg, L.ge16.p, dff, true, A.dye16.p, d, true, P2R_EPI_ACC_F32, lg(o, layer_.w2), d, nullptr, 0,

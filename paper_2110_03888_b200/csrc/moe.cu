@@ -180,10 +180,11 @@ template <typename Tin>
 __global__ void dispatch_kernel(const Tin* __restrict__ src, int d, const int* __restrict__ rows_pad,
                                 const int* __restrict__ counts, int seg_rows,
                                 const float* __restrict__ w, const int* __restrict__ slots_pad,
-                                int k, __nv_bfloat16* __restrict__ xe) {
+                                int k, __nv_bfloat16* __restrict__ xe, int pad_full) {
   const int e = blockIdx.y, r = blockIdx.x;
   const int cnt = counts[e];
-  const int top = min(seg_rows, (cnt + 127) / 128 * 128);
+  // pad_full: zero the whole segment (expert-parallel owners run full-capacity groups)
+  const int top = pad_full ? seg_rows : min(seg_rows, (cnt + 127) / 128 * 128);
   if (r >= top) return;
   __nv_bfloat16* dst = xe + (static_cast<long long>(e) * seg_rows + r) * d;
   if (r >= cnt) {
@@ -357,15 +358,15 @@ extern "C" p2r_status p2r_moe_combine_weights(const float* logits, int T, int E,
 // src_dtype: 0 fp32, 1 bf16. w != NULL scales each gathered row by its combine weight.
 extern "C" p2r_status p2r_moe_dispatch(const void* src, int src_dtype, int d, int E, int seg_rows,
                                        const int* rows_pad, const int* slots_pad, const int* counts,
-                                       const float* w, int k, void* xe_bf16, void* stream) {
+                                       const float* w, int k, void* xe_bf16, int pad_full, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   dim3 grid(seg_rows, E);
   if (src_dtype == 0)
     dispatch_kernel<float><<<grid, 128, 0, s>>>(static_cast<const float*>(src), d, rows_pad, counts, seg_rows, w, slots_pad, k,
-                                                static_cast<__nv_bfloat16*>(xe_bf16));
+                                                static_cast<__nv_bfloat16*>(xe_bf16), pad_full);
   else
     dispatch_kernel<__nv_bfloat16><<<grid, 128, 0, s>>>(static_cast<const __nv_bfloat16*>(src), d, rows_pad, counts, seg_rows, w,
-                                                        slots_pad, k, static_cast<__nv_bfloat16*>(xe_bf16));
+                                                        slots_pad, k, static_cast<__nv_bfloat16*>(xe_bf16), pad_full);
   P2R_CHECK_LAUNCH("moe dispatch");
   return P2R_OK;
 }

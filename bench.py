@@ -132,14 +132,6 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-class CudaArray:
-    """Expose a raw fp32 device buffer to torch via __cuda_array_interface__."""
-
-    def __init__(self, ptr, nbytes):
-        self.__cuda_array_interface__ = {"shape": (nbytes // 4,), "typestr": "<f4",
-                                         "data": (ptr, False), "version": 3}
-
-
 # ----------------------------------------------------------------------------- CPU reference
 def _ref_worker(args):
     """One reference micro-step (fwd+bwd+AdamW) of the C2 model on one sequence."""

@@ -11,6 +11,8 @@
 // produces dQ (+ the rowsum(dO*O) term), a second produces dK/dV.
 //
 // Round-1 implementation uses bf16 mma.sync.m16n8k16 (fp32 accumulate).
+#include <cstdlib>
+
 #include "../../include/p2r_cuda.h"
 #include "common.cuh"
 #include "p2r_internal.h"
@@ -542,6 +544,10 @@ extern "C" p2r_status p2r_attention_fwd(const void* qkv, void* o, float* lse, in
   const int hd = d / H;
   p.scale = 1.0f / sqrtf(static_cast<float>(hd));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // tcgen05/TMEM kernel (attention_tc.cu) unless explicitly asked for the mma.sync one
+  static const bool legacy = std::getenv("P2R_ATTN_MMA_SYNC") != nullptr;
+  if (!legacy && (hd == 64 || hd == 128) && (d % 8) == 0)
+    return attention_fwd_tc(qkv, o, lse, B, H, S, d, causal, s);
   if (hd == 64) return attn::run_fwd<64>(p, s);
   if (hd == 128) return attn::run_fwd<128>(p, s);
   return set_error(P2R_EINVAL, "attention: head_dim must be 64 or 128");

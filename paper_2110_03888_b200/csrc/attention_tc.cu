@@ -1,0 +1,356 @@
+// Flash-attention FORWARD on 5th-gen tensor cores (tcgen05 + TMEM + TMA).
+//
+// Replaces masked_attention's forward (tensor.cpp:464-506) + split/merge_heads
+// (tensor.cpp:400-462): Q, K, V are read by TMA straight from the fused QKV
+// projection [T, 3d]; O is written merged-head [T, d]; the row log-sum-exp is
+// saved for the backward instead of the S x S probability matrix.
+//
+// One CTA = one (batch, head, 128-query tile), 8 warps:
+//   warp 0     TMA producer: Q once, K/V tiles (128 keys) through a 2-stage ring
+//   warp 1     MMA issuer (one lane): S_j = Q.K_j^T into a double-buffered TMEM
+//              S tile, then O += P_{j-1}.V_{j-1} (P from smem, V MN-major)
+//   warp 2     TMEM allocator (S0 | S1 | O columns)
+//   warps 4-7  softmax: thread t owns query row t (TMEM lane t): reads its S
+//              row, causal mask, online softmax with CONDITIONAL rescaling of
+//              O (only when the running max grows by > 2^8), writes bf16 P into
+//              a SWIZZLE_128B K-major smem tile, finally normalises O and
+//              stores O / LSE.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "../../include/p2r_cuda.h"
+#include "common.cuh"
+#include "p2r_internal.h"
+
+namespace p2r {
+namespace attn_tc {
+
+constexpr int BQ = 128, BKV = 128;
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kRescaleThresh = 8.0f;  // log2 units: P stays <= 256 in bf16
+
+template <int HD>
+struct Cfg {
+  static constexpr int KATOMS = HD / 64;                 // 128-B K atoms per row
+  static constexpr int TILE = BQ * HD * 2;               // Q / K / V tile bytes
+  static constexpr int PTILE = BQ * BKV * 2;             // P tile bytes
+  static constexpr int NPB = HD == 64 ? 2 : 1;           // P buffers
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = OFF_Q + TILE;
+  static constexpr int OFF_V = OFF_K + 2 * TILE;
+  static constexpr int OFF_P = OFF_V + 2 * TILE;
+  static constexpr int OFF_BAR = OFF_P + NPB * PTILE;
+  static constexpr int SMEM = OFF_BAR + 256 + 1024;
+  static constexpr int TMEM_S0 = 0, TMEM_S1 = 128, TMEM_O = 256;
+};
+
+struct FwdParams {
+  __nv_bfloat16* o;
+  float* lse;
+  int B, H, S, d;
+  int causal;
+  float sl2;  // softmax scale * log2(e)
+};
+
+// row-major 128-B K atom tile: element (row, k) of a [rows x 64] bf16 atom
+P2R_DEVICE uint32_t sw128_off(int row, int chunk16) {
+  return static_cast<uint32_t>(row * 128 + ((chunk16 ^ (row & 7)) << 4));
+}
+
+P2R_DEVICE void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+P2R_DEVICE void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// 2^x on the SFU (inputs here are <= 8, outputs feed a bf16 MMA operand)
+P2R_DEVICE float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+P2R_DEVICE void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+template <int HD>
+__global__ void __launch_bounds__(256, 1)
+    attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const FwdParams p) {
+  using C = Cfg<HD>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* q_full = bar + 0;
+  uint64_t* kv_full = bar + 1;   // [2]
+  uint64_t* kv_empty = bar + 3;  // [2]
+  uint64_t* s_full = bar + 5;    // [2]
+  uint64_t* p_full = bar + 7;    // [2]
+  uint64_t* o_done = bar + 9;    // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int q0 = qb * BQ;
+  const int row0 = b * p.S;  // first row of this sequence in [T, 3d]
+  const int nkv = p.causal ? min(qb + 1, (p.S + BKV - 1) / BKV) : (p.S + BKV - 1) / BKV;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_qkv);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(kv_full + i, 1);
+      mbar_init(kv_empty + i, 1);
+      mbar_init(s_full + i, 1);
+      mbar_init(p_full + i, 128);
+      mbar_init(o_done + i, 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t sbase = smem_u32(smem);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      mbar_arrive_expect_tx(q_full, C::TILE);
+      for (int a = 0; a < C::KATOMS; ++a)
+        tma_load_2d(smem + C::OFF_Q + a * BQ * 128, &tm_qkv, q_full, h * HD + 64 * a, row0 + q0);
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j & 1;
+        mbar_wait(kv_empty + st, ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(kv_full + st, 2 * C::TILE);
+        for (int a = 0; a < C::KATOMS; ++a) {
+          tma_load_2d(smem + C::OFF_K + st * C::TILE + a * BKV * 128, &tm_qkv, kv_full + st,
+                      p.d + h * HD + 64 * a, row0 + j * BKV);
+          tma_load_2d(smem + C::OFF_V + st * C::TILE + a * BKV * 128, &tm_qkv, kv_full + st,
+                      2 * p.d + h * HD + 64 * a, row0 + j * BKV);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer ----------------
+      constexpr uint32_t idesc_s = make_idesc_bf16(BQ, BKV, false, false);
+      constexpr uint32_t idesc_o = make_idesc_bf16(BQ, HD, false, true);
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      auto issue_pv = [&](int jj) {
+        mbar_wait(p_full + (jj & 1), (jj >> 1) & 1);
+        tc_fence_after();
+        const int st = jj & 1;
+        const uint32_t sp = sbase + C::OFF_P + (jj % C::NPB) * C::PTILE;
+        const uint32_t sv = sbase + C::OFF_V + st * C::TILE;
+#pragma unroll
+        for (int k = 0; k < BKV / 16; ++k) {
+          // A = P (K-major, atom = 64 keys), B = V (MN-major: rows = keys, 64 hd per 128-B row)
+          const uint64_t ad = make_sw128_desc(sp + (k >> 2) * (BQ * 128) + (k & 3) * 32, 16, 1024);
+          const uint64_t bd = make_sw128_desc(sv + k * 2048, BKV * 128, 1024);
+          umma_bf16(tmem + C::TMEM_O, ad, bd, idesc_o, (jj > 0 || k > 0) ? 1u : 0u);
+        }
+        umma_commit(kv_empty + st);
+        umma_commit(o_done + (jj & 1));
+      };
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j & 1;
+        mbar_wait(kv_full + st, (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t sq = sbase + C::OFF_Q;
+        const uint32_t sk = sbase + C::OFF_K + st * C::TILE;
+        const uint32_t dS = tmem + ((j & 1) ? C::TMEM_S1 : C::TMEM_S0);
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k) {
+          const uint32_t koff = (k >> 2) * (BQ * 128) + (k & 3) * 32;
+          umma_bf16(dS, make_sw128_desc(sq + koff, 16, 1024),
+                    make_sw128_desc(sk + (k >> 2) * (BKV * 128) + (k & 3) * 32, 16, 1024), idesc_s,
+                    k > 0 ? 1u : 0u);
+        }
+        umma_commit(s_full + (j & 1));
+        if (j > 0) issue_pv(j - 1);
+      }
+      issue_pv(nkv - 1);
+    }
+  } else if (warp >= 4) {
+    // ---------------- softmax / correction / epilogue ----------------
+    const int r = (warp - 4) * 32 + lane;  // query row within the tile == TMEM lane
+    const int q = q0 + r;
+    const uint32_t lane_addr = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    float m_used = -INFINITY, l = 0.0f;
+    for (int j = 0; j < nkv; ++j) {
+      mbar_wait(s_full + (j & 1), (j >> 1) & 1);
+      tc_fence_after();
+      const uint32_t tS = tmem + lane_addr + ((j & 1) ? C::TMEM_S1 : C::TMEM_S0);
+      float x[BKV];
+#pragma unroll
+      for (int c = 0; c < BKV / 32; ++c) {
+        uint32_t rr[32];
+        tmem_ld_32x32b_x32(tS + c * 32, rr);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) x[c * 32 + i] = __uint_as_float(rr[i]);
+      }
+      const int k0 = j * BKV;
+      const bool diag = p.causal && (k0 + BKV > q0);
+      const bool tail = k0 + BKV > p.S;
+      if (diag || tail) {  // warp-uniform: only the diagonal / ragged-tail blocks mask
+        const int lim = min(diag ? q + 1 : p.S, p.S) - k0;  // keys [0, lim) of the block are visible
+#pragma unroll
+        for (int i = 0; i < BKV; ++i)
+          if (i >= lim) x[i] = -INFINITY;
+      }
+      // max on raw scores (scale > 0), then one FFMA + ex2 per element below
+      float mr0 = x[0], mr1 = x[1];
+#pragma unroll
+      for (int i = 2; i < BKV; i += 2) {
+        mr0 = fmaxf(mr0, x[i]);
+        mr1 = fmaxf(mr1, x[i + 1]);
+      }
+      const float mx = fmaxf(mr0, mr1) * p.sl2;
+      if (mx > m_used + kRescaleThresh) {
+        if (j > 0) {
+          // O holds sum_{<j} 2^(x - m_used) V: rescale to the new reference max
+          mbar_wait(o_done + ((j - 1) & 1), ((j - 1) >> 1) & 1);
+          tc_fence_after();
+          const float f = exp2f(m_used - mx);
+#pragma unroll
+          for (int c = 0; c < HD / 32; ++c) {
+            uint32_t rr[32];
+            tmem_ld_32x32b_x32(tmem + lane_addr + C::TMEM_O + c * 32, rr);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) rr[i] = __float_as_uint(__uint_as_float(rr[i]) * f);
+            tmem_st_32x32b_x32(tmem + lane_addr + C::TMEM_O + c * 32, rr);
+          }
+          tmem_st_wait();
+          l *= f;
+        }
+        m_used = mx;
+      }
+      // P buffer reuse: the PV that last read this buffer must be done
+      if (j >= C::NPB) {
+        const int jp = j - C::NPB;
+        mbar_wait(o_done + (jp & 1), (jp >> 1) & 1);
+      }
+      uint8_t* sp = smem + C::OFF_P + (j % C::NPB) * C::PTILE;
+      float ls = 0.0f, ls2 = 0.0f;
+      const float nm = -m_used;
+#pragma unroll
+      for (int c16 = 0; c16 < BKV / 8; ++c16) {
+        uint32_t w[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float a = ex2_approx(fmaf(x[c16 * 8 + 2 * i], p.sl2, nm));
+          const float bb = ex2_approx(fmaf(x[c16 * 8 + 2 * i + 1], p.sl2, nm));
+          ls += a;
+          ls2 += bb;
+          __nv_bfloat162 hh = __floats2bfloat162_rn(a, bb);
+          w[i] = *reinterpret_cast<uint32_t*>(&hh);
+        }
+        const int atom = c16 >> 3;  // 8 chunks of 8 keys per 64-key atom
+        *reinterpret_cast<uint4*>(sp + atom * (BQ * 128) + sw128_off(r, c16 & 7)) =
+            make_uint4(w[0], w[1], w[2], w[3]);
+      }
+      l += ls + ls2;
+      fence_async_smem();
+      tc_fence_before();
+      mbar_arrive(p_full + (j & 1));
+    }
+    // epilogue: wait for the last PV, normalise, store O (bf16) and LSE
+    mbar_wait(o_done + ((nkv - 1) & 1), ((nkv - 1) >> 1) & 1);
+    tc_fence_after();
+    const float inv = l > 0.0f ? 1.0f / l : 0.0f;
+    const bool row_ok = q < p.S;
+    __nv_bfloat16* orow = p.o + static_cast<long long>(row0 + q) * p.d + h * HD;
+#pragma unroll
+    for (int c = 0; c < HD / 32; ++c) {
+      uint32_t rr[32];
+      tmem_ld_32x32b_x32(tmem + lane_addr + C::TMEM_O + c * 32, rr);
+      tmem_ld_wait();
+      if (row_ok) {
+        uint32_t w[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          __nv_bfloat162 hh = __floats2bfloat162_rn(__uint_as_float(rr[2 * i]) * inv, __uint_as_float(rr[2 * i + 1]) * inv);
+          w[i] = *reinterpret_cast<uint32_t*>(&hh);
+        }
+        uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) dst[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+      }
+    }
+    if (row_ok)
+      p.lse[(static_cast<long long>(b) * p.H + h) * p.S + q] = (m_used + log2f(l)) * 0.6931471805599453f;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  return fn;
+}
+
+template <int HD>
+p2r_status run(const void* qkv, const FwdParams& p, cudaStream_t s) {
+  using C = Cfg<HD>;
+  auto fn = encode_fn();
+  if (!fn) return set_error(P2R_ECUDA, "attention: cuTensorMapEncodeTiled unavailable");
+  CUtensorMap tm;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(3) * p.d, static_cast<cuuint64_t>(p.B) * p.S};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(3) * p.d * 2};
+  const cuuint32_t box[2] = {64, 128};
+  const cuuint32_t es[2] = {1, 1};
+  if (fn(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(qkv), dims, strides, box, es,
+         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return set_error(P2R_ECUDA, "attention: tensor map encode failed");
+  static cudaError_t attr = cudaFuncSetAttribute(attn_fwd_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  if (attr != cudaSuccess) return set_cuda_error(attr, "attention tc attr");
+  dim3 grid((p.S + BQ - 1) / BQ, p.H, p.B);
+  attn_fwd_tc_kernel<HD><<<grid, 256, C::SMEM, s>>>(tm, p);
+  P2R_CHECK_LAUNCH("attention fwd (tcgen05)");
+  return P2R_OK;
+}
+
+}  // namespace attn_tc
+
+// Used by p2r_attention_fwd (attention.cu) when the shape qualifies.
+p2r_status attention_fwd_tc(const void* qkv, void* o, float* lse, int B, int H, int S, int d, int causal,
+                            cudaStream_t s) {
+  attn_tc::FwdParams p{};
+  p.o = static_cast<__nv_bfloat16*>(o);
+  p.lse = lse;
+  p.B = B;
+  p.H = H;
+  p.S = S;
+  p.d = d;
+  p.causal = causal;
+  const int hd = d / H;
+  p.sl2 = (1.0f / sqrtf(static_cast<float>(hd))) * attn_tc::kLog2e;
+  if (hd == 64) return attn_tc::run<64>(qkv, p, s);
+  if (hd == 128) return attn_tc::run<128>(qkv, p, s);
+  return set_error(P2R_EINVAL, "attention: head_dim must be 64 or 128");
+}
+
+}  // namespace p2r

@@ -13,6 +13,8 @@ namespace p2r {
 p2r_status set_error(p2r_status code, const char* msg);
 p2r_status set_cuda_error(cudaError_t e, const char* where);
 void count_launch();
+p2r_status attention_fwd_tc(const void* qkv, void* o, float* lse, int B, int H, int S, int d, int causal,
+                            cudaStream_t s);
 
 }  // namespace p2r
 

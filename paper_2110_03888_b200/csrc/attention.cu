@@ -573,6 +573,9 @@ extern "C" p2r_status p2r_attention_bwd(const void* qkv, const void* o, const fl
   const int hd = d / H;
   p.scale = 1.0f / sqrtf(static_cast<float>(hd));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  static const bool legacy = std::getenv("P2R_ATTN_MMA_SYNC") != nullptr;
+  if (!legacy && (hd == 64 || hd == 128) && (d % 8) == 0)
+    return attention_bwd_tc(qkv, o, lse, dout, dsum_ws, dqkv, B, H, S, d, causal, s);
   if (hd == 64) return attn::run_bwd<64>(p, s);
   if (hd == 128) return attn::run_bwd<128>(p, s);
   return set_error(P2R_EINVAL, "attention: head_dim must be 64 or 128");

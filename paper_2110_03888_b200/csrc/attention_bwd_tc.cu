@@ -1,0 +1,540 @@
+// Flash-attention BACKWARD on 5th-gen tensor cores (tcgen05 + TMEM + TMA).
+//
+// Replaces masked_attention's backward (tensor.cpp:510-541). P is recomputed
+// from the saved row log-sum-exp (no S x S matrix). Deterministic: no atomics.
+//   dQ kernel   (CTA = 128 queries, loop over 64-key blocks):
+//       S = Q.K^T, dP = dO.V^T (TMEM, double-buffered) -> softmax warps (thread =
+//       query row) form dS = P o (dP - D) in a SWIZZLE_128B smem tile ->
+//       dQ += dS.K (K tile re-read MN-major). Its prologue also computes
+//       D = rowsum(dO o O) (tensor.cpp:526-533) for the dK/dV kernel.
+//   dK/dV kernel (CTA = 128 keys, loop over 64-query blocks):
+//       S^T = K.Q^T, dP^T = V.dO^T -> thread = key row forms P^T and dS^T ->
+//       dV += P^T.dO, dK += dS^T.Q (Q / dO tiles re-read MN-major).
+// The same swizzled smem bytes serve as a K-major operand for one MMA and as
+// an MN-major operand for the next, so no transposes are materialised.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "../../include/p2r_cuda.h"
+#include "common.cuh"
+#include "p2r_internal.h"
+
+namespace p2r {
+namespace attn_bwd_tc {
+
+constexpr float kLog2e = 1.4426950408889634f;
+
+P2R_DEVICE uint32_t sw128_off(int row, int chunk16) {
+  return static_cast<uint32_t>(row * 128 + ((chunk16 ^ (row & 7)) << 4));
+}
+P2R_DEVICE float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+P2R_DEVICE void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+P2R_DEVICE void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+struct BwdParams {
+  const __nv_bfloat16* o;     // [T, d]
+  const __nv_bfloat16* dout;  // [T, d]
+  const float* lse;           // [B, H, S]
+  float* dsum;                // [B, H, S]
+  __nv_bfloat16* dqkv;        // [T, 3d]
+  int B, H, S, d;
+  int causal;
+  float scale, sl2;
+};
+
+// write a row of 64 bf16 values (from fp32 pairs) into a [rows x 64] SW128 atom
+P2R_DEVICE void store_row64(uint8_t* atom, int row, const float* v) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      __nv_bfloat162 h = __floats2bfloat162_rn(v[c * 8 + 2 * i], v[c * 8 + 2 * i + 1]);
+      w[i] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    *reinterpret_cast<uint4*>(atom + sw128_off(row, c)) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+// write 32 bf16 values (4 x 16-B chunks starting at chunk c0) of one row of a SW128 atom
+P2R_DEVICE void store_row32(uint8_t* atom, int row, int c0, const float* v) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      __nv_bfloat162 h = __floats2bfloat162_rn(v[c * 8 + 2 * i], v[c * 8 + 2 * i + 1]);
+      w[i] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    *reinterpret_cast<uint4*>(atom + sw128_off(row, c0 + c)) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+P2R_DEVICE void ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  tmem_ld_32x32b_x32(taddr, r);
+  tmem_ld_wait();
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+P2R_DEVICE void ld64(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  tmem_ld_32x32b_x32(taddr, r);
+  tmem_ld_wait();
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+  tmem_ld_32x32b_x32(taddr + 32, r);
+  tmem_ld_wait();
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[32 + i] = __uint_as_float(r[i]);
+}
+
+// ============================================================================ dQ
+template <int HD>
+struct DqCfg {
+  static constexpr int BQ = 128, BKV = 64, KA = HD / 64;
+  static constexpr int QT = BQ * HD * 2;     // Q / dO tile
+  static constexpr int KT = BKV * HD * 2;    // K / V tile
+  static constexpr int DST = BQ * BKV * 2;   // dS tile (one 64-key atom)
+  static constexpr int OFF_Q = 0, OFF_DO = QT, OFF_K = 2 * QT, OFF_V = OFF_K + 2 * KT, OFF_DS = OFF_V + 2 * KT;
+  static constexpr int OFF_BAR = OFF_DS + 2 * DST;
+  static constexpr int SMEM = OFF_BAR + 256 + 1024;
+  static constexpr int T_S = 0, T_DP = 128, T_DQ = 256;  // S[2] at 0/64, dP[2] at 128/192
+};
+
+template <int HD>
+__global__ void __launch_bounds__(384, 1)
+    attn_bwd_dq_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kv,
+                   const __grid_constant__ CUtensorMap tm_do, const BwdParams p) {
+  using C = DqCfg<HD>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* q_full = bar;          // Q + dO
+  uint64_t* kv_full = bar + 1;     // [2]
+  uint64_t* kv_empty = bar + 3;    // [2]
+  uint64_t* s_full = bar + 5;      // [2]  S and dP of block j
+  uint64_t* ds_full = bar + 7;     // [2]  dS of block j in smem
+  uint64_t* dq_done = bar + 9;     // [2]  dQ += dS_j.K_j completed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int q0 = qb * C::BQ, row0 = b * p.S;
+  const int kend = p.causal ? min(p.S, q0 + C::BQ) : p.S;
+  const int nkv = (kend + C::BKV - 1) / C::BKV;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_q);
+    tma_prefetch_desc(&tm_kv);
+    tma_prefetch_desc(&tm_do);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(kv_full + i, 1);
+      mbar_init(kv_empty + i, 1);
+      mbar_init(s_full + i, 1);
+      mbar_init(ds_full + i, 256);
+      mbar_init(dq_done + i, 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t sb = smem_u32(smem);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(q_full, 2 * C::QT);
+      for (int a = 0; a < C::KA; ++a) {
+        tma_load_2d(smem + C::OFF_Q + a * C::BQ * 128, &tm_q, q_full, h * HD + 64 * a, row0 + q0);
+        tma_load_2d(smem + C::OFF_DO + a * C::BQ * 128, &tm_do, q_full, h * HD + 64 * a, row0 + q0);
+      }
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j & 1;
+        mbar_wait(kv_empty + st, ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(kv_full + st, 2 * C::KT);
+        for (int a = 0; a < C::KA; ++a) {
+          tma_load_2d(smem + C::OFF_K + st * C::KT + a * C::BKV * 128, &tm_kv, kv_full + st, p.d + h * HD + 64 * a,
+                      row0 + j * C::BKV);
+          tma_load_2d(smem + C::OFF_V + st * C::KT + a * C::BKV * 128, &tm_kv, kv_full + st,
+                      2 * p.d + h * HD + 64 * a, row0 + j * C::BKV);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t id_s = make_idesc_bf16(C::BQ, C::BKV, false, false);
+      constexpr uint32_t id_q = make_idesc_bf16(C::BQ, HD, false, true);
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      auto issue_dq = [&](int jj) {
+        mbar_wait(ds_full + (jj & 1), (jj >> 1) & 1);
+        tc_fence_after();
+        const uint32_t sds = sb + C::OFF_DS + (jj & 1) * C::DST;
+        const uint32_t sk = sb + C::OFF_K + (jj & 1) * C::KT;
+#pragma unroll
+        for (int k = 0; k < C::BKV / 16; ++k)
+          umma_bf16(tmem + C::T_DQ, make_sw128_desc(sds + k * 32, 16, 1024),
+                    make_sw128_desc(sk + k * 2048, C::BKV * 128, 1024), id_q, (jj > 0 || k > 0) ? 1u : 0u);
+        umma_commit(kv_empty + (jj & 1));
+        umma_commit(dq_done + (jj & 1));
+      };
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j & 1;
+        mbar_wait(kv_full + st, (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t sk = sb + C::OFF_K + st * C::KT, sv = sb + C::OFF_V + st * C::KT;
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k) {
+          const uint32_t ka = (k >> 2), kk = (k & 3) * 32;
+          umma_bf16(tmem + C::T_S + (j & 1) * 64, make_sw128_desc(sb + C::OFF_Q + ka * C::BQ * 128 + kk, 16, 1024),
+                    make_sw128_desc(sk + ka * C::BKV * 128 + kk, 16, 1024), id_s, k > 0 ? 1u : 0u);
+          umma_bf16(tmem + C::T_DP + (j & 1) * 64, make_sw128_desc(sb + C::OFF_DO + ka * C::BQ * 128 + kk, 16, 1024),
+                    make_sw128_desc(sv + ka * C::BKV * 128 + kk, 16, 1024), id_s, k > 0 ? 1u : 0u);
+        }
+        umma_commit(s_full + (j & 1));
+        if (j > 0) issue_dq(j - 1);
+      }
+      issue_dq(nkv - 1);
+    }
+  } else if (warp >= 4) {
+    // 8 warps: two per TMEM lane quadrant, each owning 32 of the 64 key columns
+    const int r = (warp & 3) * 32 + lane;
+    const int half = (warp - 4) >> 2;
+    const int q = q0 + r;
+    const uint32_t la = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const long long bh = static_cast<long long>(b) * p.H + h;
+    // D = rowsum(dO o O) for this row (fp32 accumulate), published for the dK/dV kernel
+    float D = 0.0f;
+    if (q < p.S) {
+      const uint4* a4 = reinterpret_cast<const uint4*>(p.dout + static_cast<long long>(row0 + q) * p.d + h * HD);
+      const uint4* o4 = reinterpret_cast<const uint4*>(p.o + static_cast<long long>(row0 + q) * p.d + h * HD);
+#pragma unroll
+      for (int c = 0; c < HD / 8; ++c) {
+        const uint4 x = a4[c], y = o4[c];
+        const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 u = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xs[i]));
+          const float2 v = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ys[i]));
+          D += u.x * v.x + u.y * v.y;
+        }
+      }
+      if (half == 0) p.dsum[bh * p.S + q] = D;
+    }
+    const float lse2 = q < p.S ? p.lse[bh * p.S + q] * kLog2e : 0.0f;
+    for (int j = 0; j < nkv; ++j) {
+      mbar_wait(s_full + (j & 1), (j >> 1) & 1);
+      tc_fence_after();
+      float s[32], dp[32];
+      ld32(tmem + la + C::T_S + (j & 1) * 64 + half * 32, s);
+      ld32(tmem + la + C::T_DP + (j & 1) * 64 + half * 32, dp);
+      const int k0 = j * C::BKV + half * 32;
+      int lim = 32;
+      if (q >= p.S) lim = 0;
+      else if (p.causal || k0 + 32 > p.S) lim = min(p.causal ? q + 1 : p.S, p.S) - k0;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const float pv = i < lim ? ex2_approx(fmaf(s[i], p.sl2, -lse2)) : 0.0f;
+        s[i] = pv * (dp[i] - D);
+      }
+      if (j >= 2) mbar_wait(dq_done + (j & 1), ((j - 2) >> 1) & 1);
+      store_row32(smem + C::OFF_DS + (j & 1) * C::DST, r, half * 4, s);
+      fence_async_smem();
+      tc_fence_before();
+      mbar_arrive(ds_full + (j & 1));
+    }
+    mbar_wait(dq_done + ((nkv - 1) & 1), ((nkv - 1) >> 1) & 1);
+    tc_fence_after();
+    __nv_bfloat16* dq = p.dqkv + static_cast<long long>(row0 + q) * 3 * p.d + h * HD;
+#pragma unroll
+    for (int c = half; c < HD / 32; c += 2) {
+      uint32_t rr[32];
+      tmem_ld_32x32b_x32(tmem + la + C::T_DQ + c * 32, rr);
+      tmem_ld_wait();
+      if (q < p.S) {
+        uint32_t w[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          __nv_bfloat162 hh = __floats2bfloat162_rn(__uint_as_float(rr[2 * i]) * p.scale, __uint_as_float(rr[2 * i + 1]) * p.scale);
+          w[i] = *reinterpret_cast<uint32_t*>(&hh);
+        }
+        uint4* dst = reinterpret_cast<uint4*>(dq + c * 32);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) dst[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ============================================================================ dK / dV
+template <int HD>
+struct KvCfg {
+  static constexpr int BK = 128, BQ = 64, KA = HD / 64;
+  static constexpr int KT = BK * HD * 2;     // K / V tile
+  static constexpr int QT = BQ * HD * 2;     // Q / dO tile
+  static constexpr int PT = BK * BQ * 2;     // P^T / dS^T tile (one 64-query atom)
+  static constexpr int OFF_K = 0, OFF_V = KT, OFF_Q = 2 * KT, OFF_DO = OFF_Q + 2 * QT;
+  static constexpr int OFF_P = OFF_DO + 2 * QT, OFF_DS = OFF_P + 2 * PT;
+  static constexpr int OFF_LD = OFF_DS + 2 * PT;  // [2][2][64] floats: lse2, D
+  static constexpr int OFF_BAR = OFF_LD + 1024;
+  static constexpr int SMEM = OFF_BAR + 256 + 1024;
+  static constexpr int T_S = 0, T_DP = 128, T_DV = 256, T_DK = 256 + HD;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(384, 1)
+    attn_bwd_dkdv_tc(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
+                     const __grid_constant__ CUtensorMap tm_do, const BwdParams p) {
+  using C = KvCfg<HD>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* kv_full = bar;
+  uint64_t* q_full = bar + 1;    // [2]
+  uint64_t* q_empty = bar + 3;   // [2]
+  uint64_t* s_full = bar + 5;    // [2]
+  uint64_t* p_full = bar + 7;    // [2]
+  uint64_t* pv_done = bar + 9;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+  float* sLD = reinterpret_cast<float*>(smem + C::OFF_LD);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int k0 = kb * C::BK, row0 = b * p.S;
+  const int qstart = p.causal ? k0 : 0;
+  const int nq = (p.S - qstart + C::BQ - 1) / C::BQ;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_kv);
+    tma_prefetch_desc(&tm_q);
+    tma_prefetch_desc(&tm_do);
+    mbar_init(kv_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(q_full + i, 1);
+      mbar_init(q_empty + i, 1);
+      mbar_init(s_full + i, 1);
+      mbar_init(p_full + i, 256);
+      mbar_init(pv_done + i, 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t sb = smem_u32(smem);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(kv_full, 2 * C::KT);
+      for (int a = 0; a < C::KA; ++a) {
+        tma_load_2d(smem + C::OFF_K + a * C::BK * 128, &tm_kv, kv_full, p.d + h * HD + 64 * a, row0 + k0);
+        tma_load_2d(smem + C::OFF_V + a * C::BK * 128, &tm_kv, kv_full, 2 * p.d + h * HD + 64 * a, row0 + k0);
+      }
+      for (int i = 0; i < nq; ++i) {
+        const int st = i & 1;
+        const int q1 = qstart + i * C::BQ;
+        mbar_wait(q_empty + st, ((i >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(q_full + st, 2 * C::QT);
+        for (int a = 0; a < C::KA; ++a) {
+          tma_load_2d(smem + C::OFF_Q + st * C::QT + a * C::BQ * 128, &tm_q, q_full + st, h * HD + 64 * a, row0 + q1);
+          tma_load_2d(smem + C::OFF_DO + st * C::QT + a * C::BQ * 128, &tm_do, q_full + st, h * HD + 64 * a, row0 + q1);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t id_s = make_idesc_bf16(C::BK, C::BQ, false, false);
+      constexpr uint32_t id_o = make_idesc_bf16(C::BK, HD, false, true);
+      mbar_wait(kv_full, 0);
+      tc_fence_after();
+      auto issue_kv = [&](int ii) {
+        mbar_wait(p_full + (ii & 1), (ii >> 1) & 1);
+        tc_fence_after();
+        const int st = ii & 1;
+        const uint32_t spt = sb + C::OFF_P + st * C::PT, sds = sb + C::OFF_DS + st * C::PT;
+        const uint32_t sq = sb + C::OFF_Q + st * C::QT, sdo = sb + C::OFF_DO + st * C::QT;
+#pragma unroll
+        for (int k = 0; k < C::BQ / 16; ++k) {
+          // dV += P^T dO ; dK += dS^T Q   (dO / Q tiles re-read MN-major: rows = queries)
+          umma_bf16(tmem + C::T_DV, make_sw128_desc(spt + k * 32, 16, 1024),
+                    make_sw128_desc(sdo + k * 2048, C::BQ * 128, 1024), id_o, (ii > 0 || k > 0) ? 1u : 0u);
+          umma_bf16(tmem + C::T_DK, make_sw128_desc(sds + k * 32, 16, 1024),
+                    make_sw128_desc(sq + k * 2048, C::BQ * 128, 1024), id_o, (ii > 0 || k > 0) ? 1u : 0u);
+        }
+        umma_commit(q_empty + st);
+        umma_commit(pv_done + st);
+      };
+      for (int i = 0; i < nq; ++i) {
+        const int st = i & 1;
+        mbar_wait(q_full + st, (i >> 1) & 1);
+        tc_fence_after();
+        const uint32_t sq = sb + C::OFF_Q + st * C::QT, sdo = sb + C::OFF_DO + st * C::QT;
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k) {
+          const uint32_t ka = (k >> 2), kk = (k & 3) * 32;
+          umma_bf16(tmem + C::T_S + st * 64, make_sw128_desc(sb + C::OFF_K + ka * C::BK * 128 + kk, 16, 1024),
+                    make_sw128_desc(sq + ka * C::BQ * 128 + kk, 16, 1024), id_s, k > 0 ? 1u : 0u);
+          umma_bf16(tmem + C::T_DP + st * 64, make_sw128_desc(sb + C::OFF_V + ka * C::BK * 128 + kk, 16, 1024),
+                    make_sw128_desc(sdo + ka * C::BQ * 128 + kk, 16, 1024), id_s, k > 0 ? 1u : 0u);
+        }
+        umma_commit(s_full + st);
+        if (i > 0) issue_kv(i - 1);
+      }
+      issue_kv(nq - 1);
+    }
+  } else if (warp >= 4) {
+    // 8 warps: two per TMEM lane quadrant, each owning 32 of the 64 query columns
+    const int t = threadIdx.x - 128;  // 0..255
+    const int kr = (warp & 3) * 32 + lane;  // key row == TMEM lane
+    const int half = (warp - 4) >> 2;
+    const int key = k0 + kr;
+    const uint32_t la = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const long long bh = static_cast<long long>(b) * p.H + h;
+    for (int i = 0; i < nq; ++i) {
+      const int st = i & 1;
+      const int q1 = qstart + i * C::BQ;
+      // stage lse2 / D of this query block (threads 0..63: lse, 64..127: D)
+      if (t < 128) {
+        const int c = t & 63, qq = q1 + c;
+        float v = 0.0f;
+        if (qq < p.S) v = t < 64 ? p.lse[bh * p.S + qq] * kLog2e : p.dsum[bh * p.S + qq];
+        sLD[(st * 2 + (t >> 6)) * 64 + c] = v;
+      }
+      named_sync(1, 256);
+      mbar_wait(s_full + st, (i >> 1) & 1);
+      tc_fence_after();
+      float s[32], dp[32];
+      ld32(tmem + la + C::T_S + st * 64 + half * 32, s);
+      ld32(tmem + la + C::T_DP + st * 64 + half * 32, dp);
+      const float* L2 = sLD + st * 128 + half * 32;
+      const float* Dv = L2 + 64;
+      // visible: query q >= key (causal), q < S, key < S
+      const int qb1 = q1 + half * 32;
+      int lo = 0, hi = min(32, p.S - qb1);
+      if (p.causal) lo = max(0, key - qb1);
+      if (key >= p.S) hi = 0;
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        const float pv = (c >= lo && c < hi) ? ex2_approx(fmaf(s[c], p.sl2, -L2[c])) : 0.0f;
+        s[c] = pv;
+        dp[c] = pv * (dp[c] - Dv[c]);
+      }
+      if (i >= 2) mbar_wait(pv_done + st, ((i - 2) >> 1) & 1);
+      store_row32(smem + C::OFF_P + st * C::PT, kr, half * 4, s);
+      store_row32(smem + C::OFF_DS + st * C::PT, kr, half * 4, dp);
+      fence_async_smem();
+      tc_fence_before();
+      mbar_arrive(p_full + st);
+    }
+    mbar_wait(pv_done + ((nq - 1) & 1), ((nq - 1) >> 1) & 1);
+    tc_fence_after();
+    // half 0 stores dK (scaled), half 1 stores dV
+    __nv_bfloat16* dst_row = p.dqkv + static_cast<long long>(row0 + key) * 3 * p.d + (half == 0 ? p.d : 2 * p.d) + h * HD;
+    const float sc = half == 0 ? p.scale : 1.0f;
+    const uint32_t col = half == 0 ? C::T_DK : C::T_DV;
+#pragma unroll
+    for (int c = 0; c < HD / 32; ++c) {
+      uint32_t rr[32];
+      tmem_ld_32x32b_x32(tmem + la + col + c * 32, rr);
+      tmem_ld_wait();
+      if (key < p.S) {
+        uint32_t w[16];
+#pragma unroll
+        for (int i2 = 0; i2 < 16; ++i2) {
+          __nv_bfloat162 hh = __floats2bfloat162_rn(__uint_as_float(rr[2 * i2]) * sc, __uint_as_float(rr[2 * i2 + 1]) * sc);
+          w[i2] = *reinterpret_cast<uint32_t*>(&hh);
+        }
+        uint4* dst = reinterpret_cast<uint4*>(dst_row + c * 32);
+#pragma unroll
+        for (int i2 = 0; i2 < 4; ++i2) dst[i2] = make_uint4(w[4 * i2], w[4 * i2 + 1], w[4 * i2 + 2], w[4 * i2 + 3]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  return fn;
+}
+
+bool map2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {cols * 2};
+  const cuuint32_t box[2] = {64, box_rows};
+  const cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int HD>
+p2r_status run(const void* qkv, const BwdParams& p, cudaStream_t s) {
+  const uint64_t T = static_cast<uint64_t>(p.B) * p.S;
+  CUtensorMap qkv128, qkv64, do128, do64;
+  if (!map2d(&qkv128, qkv, T, 3ull * p.d, 128) || !map2d(&qkv64, qkv, T, 3ull * p.d, 64) ||
+      !map2d(&do128, p.dout, T, p.d, 128) || !map2d(&do64, p.dout, T, p.d, 64))
+    return set_error(P2R_ECUDA, "attention bwd: tensor map encode failed");
+  static cudaError_t a1 = cudaFuncSetAttribute(attn_bwd_dq_tc<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, DqCfg<HD>::SMEM);
+  static cudaError_t a2 = cudaFuncSetAttribute(attn_bwd_dkdv_tc<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, KvCfg<HD>::SMEM);
+  if (a1 != cudaSuccess || a2 != cudaSuccess) return set_cuda_error(a1 ? a1 : a2, "attention bwd attr");
+  attn_bwd_dq_tc<HD><<<dim3((p.S + 127) / 128, p.H, p.B), 384, DqCfg<HD>::SMEM, s>>>(qkv128, qkv64, do128, p);
+  P2R_CHECK_LAUNCH("attention bwd dq (tcgen05)");
+  attn_bwd_dkdv_tc<HD><<<dim3((p.S + 127) / 128, p.H, p.B), 384, KvCfg<HD>::SMEM, s>>>(qkv128, qkv64, do64, p);
+  P2R_CHECK_LAUNCH("attention bwd dkdv (tcgen05)");
+  return P2R_OK;
+}
+
+}  // namespace attn_bwd_tc
+
+p2r_status attention_bwd_tc(const void* qkv, const void* o, const float* lse, const void* dout, float* dsum,
+                            void* dqkv, int B, int H, int S, int d, int causal, cudaStream_t s) {
+  attn_bwd_tc::BwdParams p{};
+  p.o = static_cast<const __nv_bfloat16*>(o);
+  p.dout = static_cast<const __nv_bfloat16*>(dout);
+  p.lse = lse;
+  p.dsum = dsum;
+  p.dqkv = static_cast<__nv_bfloat16*>(dqkv);
+  p.B = B;
+  p.H = H;
+  p.S = S;
+  p.d = d;
+  p.causal = causal;
+  const int hd = d / H;
+  p.scale = 1.0f / sqrtf(static_cast<float>(hd));
+  p.sl2 = p.scale * attn_bwd_tc::kLog2e;
+  if (hd == 64) return attn_bwd_tc::run<64>(qkv, p, s);
+  if (hd == 128) return attn_bwd_tc::run<128>(qkv, p, s);
+  return set_error(P2R_EINVAL, "attention: head_dim must be 64 or 128");
+}
+
+}  // namespace p2r

@@ -15,6 +15,8 @@ p2r_status set_cuda_error(cudaError_t e, const char* where);
 void count_launch();
 p2r_status attention_fwd_tc(const void* qkv, void* o, float* lse, int B, int H, int S, int d, int causal,
                             cudaStream_t s);
+p2r_status attention_bwd_tc(const void* qkv, const void* o, const float* lse, const void* dout, float* dsum,
+                            void* dqkv, int B, int H, int S, int d, int causal, cudaStream_t s);
 
 }  // namespace p2r
 

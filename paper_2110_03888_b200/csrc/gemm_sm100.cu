@@ -122,9 +122,10 @@ struct GemmCfg {
 // Epilogue for ONE element: lane = column, so every global access of a warp is
 // row-contiguous (coalesced). `zero` stores zeros (padding rows of a grouped
 // segment) so later grouped-K GEMMs see clean K padding.
+template <int EPI>
 P2R_DEVICE void epilogue_elem(const GemmParams& p, float v, long long row, int col, bool zero,
                               float b, char* cbase, int ldc) {
-  const int epi = p.epi;
+  constexpr int epi = EPI;
   if (zero) v = 0.0f;
   switch (epi) {
     case P2R_EPI_BF16:
@@ -181,6 +182,8 @@ P2R_DEVICE float4 unpack4_bf16(uint2 w) {
 }
 
 // Epilogue for 4 consecutive columns of one row (16 B fp32 / 8 B bf16 accesses).
+// EPI is a compile-time kind so each kernel instance carries only its own math.
+template <int EPI>
 P2R_DEVICE void epilogue_vec4(const GemmParams& p, float4 v, long long row, int col, int nc, bool zero,
                               float4 b, char* cbase, int ldc) {
   if (nc < 4 || !p.vec4) {
@@ -188,11 +191,11 @@ P2R_DEVICE void epilogue_vec4(const GemmParams& p, float4 v, long long row, int 
     const float bb[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
     for (int j = 0; j < 4; ++j)
-      if (j < nc) epilogue_elem(p, vv[j], row, col + j, zero, bb[j], cbase, ldc);
+      if (j < nc) epilogue_elem<EPI>(p, vv[j], row, col + j, zero, bb[j], cbase, ldc);
     return;
   }
   const long long o = row * ldc + col;
-  switch (p.epi) {
+  switch (EPI) {
     case P2R_EPI_BF16:
       *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(cbase) + o) =
           zero ? make_uint2(0u, 0u) : pack4_bf16(v.x + b.x, v.y + b.y, v.z + b.z, v.w + b.w);
@@ -209,7 +212,7 @@ P2R_DEVICE void epilogue_vec4(const GemmParams& p, float4 v, long long row, int 
         }
       }
       *reinterpret_cast<float4*>(reinterpret_cast<float*>(cbase) + o) = v;
-      if (p.epi == P2R_EPI_F32_BF16)
+      if (EPI == P2R_EPI_F32_BF16)
         *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.c2) + row * p.ldc2 + col) =
             pack4_bf16(v.x, v.y, v.z, v.w);
       break;
@@ -249,7 +252,7 @@ P2R_DEVICE void epilogue_vec4(const GemmParams& p, float4 v, long long row, int 
 constexpr int kEpiWarps = 8;                       // 2 per TMEM lane quadrant
 constexpr int kGemmThreads = 128 + 32 * kEpiWarps;  // 4 control warps + epilogue
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const GemmParams p) {
@@ -427,7 +430,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const int rr = 4 * i + rg;
           if (rr >= nrows || nc <= 0) continue;
           const float4 v = *reinterpret_cast<const float4*>(stg + rr * 32 + ((cg ^ (rr & 7)) << 2));
-          epilogue_vec4(p, v, grow0 + rr, col, nc, row0 + rr >= zero_from, b4, cbase, ldc);
+          epilogue_vec4<EPI>(p, v, grow0 + rr, col, nc, row0 + rr >= zero_from, b4, cbase, ldc);
         }
         __syncwarp();
       }
@@ -518,30 +521,42 @@ bool make_map(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, u
 void* g_ws = nullptr;
 size_t g_ws_bytes = 0;
 
-template <int BN, bool AMN, bool BMN>
+template <int BN, bool AMN, bool BMN, int EPI>
 cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
                    cudaStream_t s) {
   using Cfg = GemmCfg<BN>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(gemm_kernel<BN, AMN, BMN>,
+    attr_err = cudaFuncSetAttribute(gemm_kernel<BN, AMN, BMN, EPI>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
   });
   if (attr_err != cudaSuccess) return attr_err;
   const int grid = p.tiles_total < kNumSMs ? p.tiles_total : kNumSMs;
-  gemm_kernel<BN, AMN, BMN><<<grid, kGemmThreads, Cfg::SMEM_BYTES, s>>>(ta, tb, p);
+  gemm_kernel<BN, AMN, BMN, EPI><<<grid, kGemmThreads, Cfg::SMEM_BYTES, s>>>(ta, tb, p);
   count_launch();
   return cudaGetLastError();
+}
+
+template <int BN, bool AMN, bool BMN>
+cudaError_t dispatch_epi(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, cudaStream_t s) {
+  switch (p.epi) {
+    case P2R_EPI_BF16: return launch<BN, AMN, BMN, P2R_EPI_BF16>(ta, tb, p, s);
+    case P2R_EPI_F32: return launch<BN, AMN, BMN, P2R_EPI_F32>(ta, tb, p, s);
+    case P2R_EPI_ACC_F32: return launch<BN, AMN, BMN, P2R_EPI_ACC_F32>(ta, tb, p, s);
+    case P2R_EPI_BIAS_GELU: return launch<BN, AMN, BMN, P2R_EPI_BIAS_GELU>(ta, tb, p, s);
+    case P2R_EPI_DGELU: return launch<BN, AMN, BMN, P2R_EPI_DGELU>(ta, tb, p, s);
+    default: return launch<BN, AMN, BMN, P2R_EPI_F32_BF16>(ta, tb, p, s);
+  }
 }
 
 template <int BN>
 cudaError_t dispatch_majors(bool amn, bool bmn, const CUtensorMap& ta, const CUtensorMap& tb,
                             const GemmParams& p, cudaStream_t s) {
-  if (!amn && !bmn) return launch<BN, false, false>(ta, tb, p, s);
-  if (!amn && bmn) return launch<BN, false, true>(ta, tb, p, s);
-  if (amn && !bmn) return launch<BN, true, false>(ta, tb, p, s);
-  return launch<BN, true, true>(ta, tb, p, s);
+  if (!amn && !bmn) return dispatch_epi<BN, false, false>(ta, tb, p, s);
+  if (!amn && bmn) return dispatch_epi<BN, false, true>(ta, tb, p, s);
+  if (amn && !bmn) return dispatch_epi<BN, true, false>(ta, tb, p, s);
+  return dispatch_epi<BN, true, true>(ta, tb, p, s);
 }
 
 int pick_bn(const p2r_gemm_args* a) { return a->n <= 128 ? 128 : 256; }

@@ -118,8 +118,11 @@ p2r_status p2r_layernorm_bwd(const float* dy, const float* x, const float* mean,
 /* Embeddings (embedding_lookup x2 + add, model.cpp:229-241; tensor.cpp:338-368). */
 p2r_status p2r_embed_fwd(const int* ids, const float* tok, const float* pos, int T, int S, int d,
                          float* x, void* stream);
+/* dtok rows are summed in ascending token order (stable radix sort of ids);
+ * ws >= p2r_embed_bwd_workspace(B*S, V) bytes when dtok != NULL. */
+size_t p2r_embed_bwd_workspace(int T, int V);
 p2r_status p2r_embed_bwd(const int* ids, const float* dx, int B, int S, int d, int V, float* dtok,
-                         float* dpos, void* stream);
+                         float* dpos, void* ws, size_t ws_bytes, void* stream);
 
 /* Softmax cross-entropy fwd+bwd (tensor.cpp:670-723). logits fp32 [rows][ld];
  * dlogits bf16 [rows][ldg] = (p - onehot) * loss_grad / denom, zero on masked

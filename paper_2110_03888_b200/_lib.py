@@ -81,6 +81,9 @@ def _declare(L):
     L.p2r_gemm_workspace_bytes.restype = ctypes.c_size_t
     L.p2r_set_workspace.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
     L.p2r_set_workspace.restype = ctypes.c_int
+    for name in ("p2r_embed_bwd_workspace", "p2r_colsum_workspace", "p2r_layernorm_bwd_workspace",
+                 "p2r_cross_entropy_workspace"):
+        getattr(L, name).restype = ctypes.c_size_t
     for name, argtypes in _EXTRA_SIGNATURES.items():
         fn = getattr(L, name, None)
         if fn is None:

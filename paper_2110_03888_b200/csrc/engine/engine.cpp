@@ -170,7 +170,7 @@ struct Acts {
   std::vector<LayerActs> L;
   DevBuf h16, meanf, rstdf, logits32, dlogits16, loss, loss_sum, ce_ws, dh32;
   DevBuf dres, dres16, tmp32, dx1, dx1_16, do16, dqkv16, dh16, dye16, dxe32, dw, glogits, dsum;
-  DevBuf ln_ws, colsum_ws;
+  DevBuf ln_ws, colsum_ws, embed_ws;
   DevBuf tokens, targets, mask;
   DevBuf xe_send16, ye_owner32, dxe_owner32, full_counts;  // expert-parallel exchange
 };
@@ -519,6 +519,7 @@ void Model::ensure_acts(int B, int S) {
   A->ln_ws = DevBuf(p2r_layernorm_bwd_workspace(T, d));
   const int bias_n = std::max(dff, d);
   A->colsum_ws = DevBuf(p2r_colsum_workspace(std::max(T, A->seg), bias_n, std::max(1, E)));
+  A->embed_ws = DevBuf(p2r_embed_bwd_workspace(T, cfg_.vocab_size));
   A->tokens = DevBuf(static_cast<std::size_t>(T) * 4);
   A->targets = DevBuf(static_cast<std::size_t>(T) * 4);
   A->mask = DevBuf(static_cast<std::size_t>(T));
@@ -653,7 +654,7 @@ Tensor Model::embed_forward(GradTape* tape, const int* d_tokens, int batch, int 
       Acts& A2 = *acts_;
       prof(P2R_PROF_EMBED, 0, 8.0 * A2.T * cfg_.d_model, [&] {
         p2r_check(p2r_embed_bwd(d_tokens, A2.dres.as<float>(), batch, seq, cfg_.d_model, cfg_.vocab_size,
-                                eg(emb_.tok), eg(emb_.pos), stream_),
+                                eg(emb_.tok), eg(emb_.pos), A2.embed_ws.p, A2.embed_ws.bytes, stream_),
                   "embed bwd");
       });
     });

@@ -20,8 +20,10 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 
 #include "../../include/p2r_cuda.h"
+
 #include "common.cuh"
 #include "p2r_internal.h"
 
@@ -249,6 +251,59 @@ P2R_DEVICE void epilogue_vec4(const GemmParams& p, float4 v, long long row, int 
   }
 }
 
+// Fast path (full 32x32 chunk, 16-byte aligned): the lane's global operand for
+// each of its 8 row groups (GELU' pre-activation, fp32 residual, or the fp32
+// accumulator being added into) is loaded while the TMEM load is in flight.
+template <int EPI>
+struct EpiOperand {
+  static constexpr bool kHas = EPI == P2R_EPI_DGELU || EPI == P2R_EPI_ACC_F32 || EPI == P2R_EPI_F32 ||
+                               EPI == P2R_EPI_F32_BF16;
+  using T = typename std::conditional<EPI == P2R_EPI_DGELU, uint2, float4>::type;
+};
+
+template <int EPI>
+P2R_DEVICE typename EpiOperand<EPI>::T epi_load(const GemmParams& p, long long row, int col, const char* cbase,
+                                                int ldc) {
+  if constexpr (EPI == P2R_EPI_DGELU) {
+    return __ldg(reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(p.aux) + row * p.ldaux + col));
+  } else if constexpr (EPI == P2R_EPI_ACC_F32) {
+    return *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(cbase) + row * ldc + col);
+  } else {
+    if (p.aux == nullptr) return make_float4(0.f, 0.f, 0.f, 0.f);
+    return *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p.aux) + row * p.ldaux + col);
+  }
+}
+
+template <int EPI>
+P2R_DEVICE void epi_store_fast(const GemmParams& p, float4 v, typename EpiOperand<EPI>::T x, long long row,
+                               int col, float4 b, char* cbase, int ldc) {
+  const long long o = row * ldc + col;
+  if constexpr (EPI == P2R_EPI_BF16) {
+    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(cbase) + o) =
+        pack4_bf16(v.x + b.x, v.y + b.y, v.z + b.z, v.w + b.w);
+  } else if constexpr (EPI == P2R_EPI_F32 || EPI == P2R_EPI_F32_BF16) {
+    v = make_float4(v.x + b.x + x.x, v.y + b.y + x.y, v.z + b.z + x.z, v.w + b.w + x.w);
+    *reinterpret_cast<float4*>(reinterpret_cast<float*>(cbase) + o) = v;
+    if constexpr (EPI == P2R_EPI_F32_BF16)
+      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.c2) + row * p.ldc2 + col) =
+          pack4_bf16(v.x, v.y, v.z, v.w);
+  } else if constexpr (EPI == P2R_EPI_ACC_F32) {
+    *reinterpret_cast<float4*>(reinterpret_cast<float*>(cbase) + o) =
+        make_float4(x.x + v.x, x.y + v.y, x.z + v.z, x.w + v.w);
+  } else if constexpr (EPI == P2R_EPI_BIAS_GELU) {
+    const float4 pre = make_float4(v.x + b.x, v.y + b.y, v.z + b.z, v.w + b.w);
+    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.c2) + row * p.ldc2 + col) =
+        pack4_bf16(pre.x, pre.y, pre.z, pre.w);
+    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(cbase) + o) =
+        pack4_bf16(gelu_f(pre.x), gelu_f(pre.y), gelu_f(pre.z), gelu_f(pre.w));
+  } else if constexpr (EPI == P2R_EPI_DGELU) {
+    const float4 pre = unpack4_bf16(x);
+    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(cbase) + o) =
+        pack4_bf16(v.x * gelu_grad_f(pre.x), v.y * gelu_grad_f(pre.y), v.z * gelu_grad_f(pre.z),
+                   v.w * gelu_grad_f(pre.w));
+  }
+}
+
 constexpr int kEpiWarps = 8;                       // 2 per TMEM lane quadrant
 constexpr int kGemmThreads = 128 + 32 * kEpiWarps;  // 4 control warps + epilogue
 
@@ -404,8 +459,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       for (int c = chalf * (BN / 64); c < (chalf + 1) * (BN / 64); ++c) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(taddr + c * 32, r);
-        tmem_ld_wait();
         const int col0 = T.n_blk * BN + c * 32;
+        // lane = (row group, 4-column group): a warp instruction covers 4 rows x 32 columns
+        const int cg = lane & 7, rg = lane >> 3;
+        const int col = col0 + 4 * cg;
+        const bool fast = p.vec4 && nrows == 32 && col0 + 32 <= p.n && row0 + 32 <= zero_from;
+        typename EpiOperand<EPI>::T x[8];
+        if constexpr (EpiOperand<EPI>::kHas) {
+          if (fast) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) x[i] = epi_load<EPI>(p, grow0 + 4 * i + rg, col, cbase, ldc);
+          }
+        }
+        tmem_ld_wait();
         if (nrows <= 0 || col0 >= p.n) continue;  // warp-uniform
         // lane = row: 8 float4 stores into a float4-granular XOR swizzle
 #pragma unroll
@@ -414,9 +480,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
                           __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
         __syncwarp();
-        // lane = (row group, 4-column group): a warp instruction covers 4 rows x 32 columns
-        const int cg = lane & 7, rg = lane >> 3;
-        const int col = col0 + 4 * cg;
         const int nc = min(4, p.n - col);  // valid columns for this lane (<= 0: none)
         float4 b4 = make_float4(0.f, 0.f, 0.f, 0.f);
         if (bias != nullptr && nc > 0) {
@@ -425,12 +488,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if (nc > 2) b4.z = __ldg(bias + col + 2);
           if (nc > 3) b4.w = __ldg(bias + col + 3);
         }
+        if (fast) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int rr = 4 * i + rg;
+            const float4 v = *reinterpret_cast<const float4*>(stg + rr * 32 + ((cg ^ (rr & 7)) << 2));
+            epi_store_fast<EPI>(p, v, x[i], grow0 + rr, col, b4, cbase, ldc);
+          }
+        } else {
 #pragma unroll 2
-        for (int i = 0; i < 8; ++i) {
-          const int rr = 4 * i + rg;
-          if (rr >= nrows || nc <= 0) continue;
-          const float4 v = *reinterpret_cast<const float4*>(stg + rr * 32 + ((cg ^ (rr & 7)) << 2));
-          epilogue_vec4<EPI>(p, v, grow0 + rr, col, nc, row0 + rr >= zero_from, b4, cbase, ldc);
+          for (int i = 0; i < 8; ++i) {
+            const int rr = 4 * i + rg;
+            if (rr >= nrows || nc <= 0) continue;
+            const float4 v = *reinterpret_cast<const float4*>(stg + rr * 32 + ((cg ^ (rr & 7)) << 2));
+            epilogue_vec4<EPI>(p, v, grow0 + rr, col, nc, row0 + rr >= zero_from, b4, cbase, ldc);
+          }
         }
         __syncwarp();
       }

@@ -4,6 +4,8 @@
 //   embedding_lookup+add tensor.cpp:338-368, model.cpp:229-241
 //   softmax_cross_entropy tensor.cpp:670-723 (fp64 loss sum, / denom, masked rows)
 // All reductions are deterministic (fixed-order trees, no float atomics).
+#include <cub/device/device_radix_sort.cuh>
+
 #include "../../include/p2r_cuda.h"
 #include "common.cuh"
 #include "p2r_internal.h"
@@ -164,16 +166,30 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(
   }
 }
 
-// grad_gain[c] += sum_b partial[b][0][c]; grad_bias[c] += sum_b partial[b][1][c]
-__global__ void ln_param_grad_reduce(const float* __restrict__ partial, int nblk, int D,
-                                     float* __restrict__ ggain, float* __restrict__ gbias) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= 2 * D) return;
-  const int which = c / D, col = c % D;
+// grad_gain[c] += sum_b partial[b][0][c]; grad_bias[c] += sum_b partial[b][1][c].
+// Block of 8 warps per 32 flattened columns: warp w sums partial rows w, w+8, ...
+// (coalesced 128-byte rows), then the 8 warp sums are added in warp order.
+__global__ void __launch_bounds__(256) ln_param_grad_reduce(const float* __restrict__ partial, int nblk,
+                                                            int D, float* __restrict__ ggain,
+                                                            float* __restrict__ gbias) {
+  __shared__ float red[8][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * 32 + lane;  // flattened [2][D] column
   float s = 0.f;
-  for (int b = 0; b < nblk; ++b) s += partial[(static_cast<long long>(b) * 2 + which) * D + col];
-  float* dst = which ? gbias : ggain;
-  if (dst) dst[col] += s;
+  if (c < 2 * D) {
+#pragma unroll 4
+    for (int b = warp; b < nblk; b += 8) s += partial[static_cast<long long>(b) * 2 * D + c];
+  }
+  red[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0 && c < 2 * D) {
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += red[w][lane];
+    const int which = c / D, col = c % D;
+    float* dst = which ? gbias : ggain;
+    if (dst) dst[col] += t;
+  }
 }
 
 // ------------------------------- embeddings ----------------------------------
@@ -193,34 +209,42 @@ __global__ void embed_fwd_kernel(const int* __restrict__ ids, const float* __res
   }
 }
 
-// dtok[v] += sum_{t: ids[t]==v, t ascending} dx[t]  (token-order scatter-add, tensor.cpp:356-365)
-__global__ void embed_tok_bwd_kernel(const int* __restrict__ ids, const float* __restrict__ dx,
-                                     int T, int d, float* __restrict__ dtok) {
-  __shared__ int sid[1024];
+// dtok[v] += sum_{t: ids[t]==v, t ascending} dx[t]  (token-order scatter-add, tensor.cpp:356-365).
+// The ids are stably radix-sorted (positions as values), so each id's run lists
+// its tokens in ascending order; one block per id sums its run in that order.
+__global__ void iota_kernel(int* __restrict__ v, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = i;
+}
+
+__global__ void run_bounds_kernel(const int* __restrict__ keys, int n, int* __restrict__ start,
+                                  int* __restrict__ end) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int k = keys[i];
+  if (i == 0 || keys[i - 1] != k) start[k] = i;
+  if (i == n - 1 || keys[i + 1] != k) end[k] = i + 1;
+}
+
+__global__ void embed_tok_bwd_kernel(const int* __restrict__ order, const int* __restrict__ start,
+                                     const int* __restrict__ end, const float* __restrict__ dx, int d,
+                                     float* __restrict__ dtok) {
   const int v = blockIdx.x;
-  const int c0 = blockIdx.y * blockDim.x * 4 + threadIdx.x * 4;
+  const int b = start[v], e = end[v];
+  if (b >= e) return;
+  const int c0 = (blockIdx.y * blockDim.x + threadIdx.x) * 4;
+  if (c0 >= d) return;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int base = 0; base < T; base += 1024) {
-    const int n = min(1024, T - base);
-    __syncthreads();
-    for (int i = threadIdx.x; i < n; i += blockDim.x) sid[i] = ids[base + i];
-    __syncthreads();
-    if (c0 < d) {
-      for (int i = 0; i < n; ++i) {
-        if (sid[i] != v) continue;
-        const float4 g = *reinterpret_cast<const float4*>(dx + static_cast<long long>(base + i) * d + c0);
-        acc.x += g.x;
-        acc.y += g.y;
-        acc.z += g.z;
-        acc.w += g.w;
-      }
-    }
+  for (int i = b; i < e; ++i) {
+    const float4 g = *reinterpret_cast<const float4*>(dx + static_cast<long long>(order[i]) * d + c0);
+    acc.x += g.x;
+    acc.y += g.y;
+    acc.z += g.z;
+    acc.w += g.w;
   }
-  if (c0 < d) {
-    float4* o = reinterpret_cast<float4*>(dtok + static_cast<long long>(v) * d + c0);
-    float4 cur = *o;
-    *o = make_float4(cur.x + acc.x, cur.y + acc.y, cur.z + acc.z, cur.w + acc.w);
-  }
+  float4* o = reinterpret_cast<float4*>(dtok + static_cast<long long>(v) * d + c0);
+  const float4 cur = *o;
+  *o = make_float4(cur.x + acc.x, cur.y + acc.y, cur.z + acc.z, cur.w + acc.w);
 }
 
 // dpos[s] += sum_b dx[b*S + s]
@@ -314,9 +338,12 @@ extern "C" p2r_status p2r_layernorm_fwd(const float* x, const float* gain, const
   return P2R_OK;
 }
 
+// 16 rows per block (2 per warp): ~512 blocks at T = 8192 keeps every SM busy.
+constexpr int kLnBwdRows = 16;
+
 // partial_ws: >= ceil(rows / rows_per_block) * 2 * d floats
 extern "C" size_t p2r_layernorm_bwd_workspace(int rows, int d) {
-  const int rpb = 64;
+  const int rpb = kLnBwdRows;
   return static_cast<size_t>((rows + rpb - 1) / rpb) * 2 * d * sizeof(float);
 }
 
@@ -326,7 +353,7 @@ extern "C" p2r_status p2r_layernorm_bwd(const float* dy, const float* x, const f
                                         float* gbias, float* partial_ws, void* stream) {
   if (rows <= 0) return P2R_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int rpb = 64;
+  const int rpb = kLnBwdRows;
   const int blocks = (rows + rpb - 1) / rpb;
   auto* d16 = static_cast<__nv_bfloat16*>(dx_bf16);
   switch (d) {
@@ -339,7 +366,7 @@ extern "C" p2r_status p2r_layernorm_bwd(const float* dy, const float* x, const f
   }
   P2R_CHECK_LAUNCH("layernorm bwd");
   if (ggain || gbias) {
-    ln_param_grad_reduce<<<(2 * d + 255) / 256, 256, 0, s>>>(partial_ws, blocks, d, ggain, gbias);
+    ln_param_grad_reduce<<<(2 * d + 31) / 32, 256, 0, s>>>(partial_ws, blocks, d, ggain, gbias);
     P2R_CHECK_LAUNCH("layernorm param grad");
   }
   return P2R_OK;
@@ -354,14 +381,60 @@ extern "C" p2r_status p2r_embed_fwd(const int* ids, const float* tok, const floa
   return P2R_OK;
 }
 
+namespace {
+int key_bits(int V) {
+  int b = 1;
+  while ((1LL << b) < V) ++b;
+  return b;
+}
+size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
+size_t cub_sort_bytes(int T, int V) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, static_cast<const int*>(nullptr), static_cast<int*>(nullptr),
+                                  static_cast<const int*>(nullptr), static_cast<int*>(nullptr), T, 0, key_bits(V));
+  return bytes;
+}
+}  // namespace
+
+extern "C" size_t p2r_embed_bwd_workspace(int T, int V) {
+  if (T <= 0 || V <= 0) return 0;
+  return align256(cub_sort_bytes(T, V)) + 3 * align256(static_cast<size_t>(T) * sizeof(int)) +
+         2 * align256(static_cast<size_t>(V) * sizeof(int));
+}
+
 extern "C" p2r_status p2r_embed_bwd(const int* ids, const float* dx, int B, int S, int d, int V,
-                                    float* dtok, float* dpos, void* stream) {
+                                    float* dtok, float* dpos, void* ws, size_t ws_bytes, void* stream) {
   const int T = B * S;
   if (T <= 0) return P2R_OK;
+  if (d % 4) return set_error(P2R_EINVAL, "embedding: d_model must be a multiple of 4");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (dtok) {
+    if (ws == nullptr || ws_bytes < p2r_embed_bwd_workspace(T, V))
+      return set_error(P2R_EINVAL, "embed bwd: workspace too small (see p2r_embed_bwd_workspace)");
+    char* w = static_cast<char*>(ws);
+    size_t tmp_bytes = cub_sort_bytes(T, V);
+    void* tmp = w;
+    w += align256(tmp_bytes);
+    int* keys = reinterpret_cast<int*>(w);
+    w += align256(static_cast<size_t>(T) * sizeof(int));
+    int* pos_in = reinterpret_cast<int*>(w);
+    w += align256(static_cast<size_t>(T) * sizeof(int));
+    int* order = reinterpret_cast<int*>(w);
+    w += align256(static_cast<size_t>(T) * sizeof(int));
+    int* start = reinterpret_cast<int*>(w);
+    w += align256(static_cast<size_t>(V) * sizeof(int));
+    int* end = reinterpret_cast<int*>(w);
+    iota_kernel<<<(T + 255) / 256, 256, 0, s>>>(pos_in, T);
+    P2R_CHECK_LAUNCH("embed bwd iota");
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, ids, keys, pos_in, order, T, 0, key_bits(V), s);
+    if (e != cudaSuccess) return set_cuda_error(e, "embed bwd sort");
+    count_launch();
+    e = cudaMemsetAsync(start, 0, 2 * align256(static_cast<size_t>(V) * sizeof(int)), s);
+    if (e != cudaSuccess) return set_cuda_error(e, "embed bwd memset");
+    run_bounds_kernel<<<(T + 255) / 256, 256, 0, s>>>(keys, T, start, end);
+    P2R_CHECK_LAUNCH("embed bwd bounds");
     dim3 grid(V, (d / 4 + 127) / 128);
-    embed_tok_bwd_kernel<<<grid, 128, 0, s>>>(ids, dx, T, d, dtok);
+    embed_tok_bwd_kernel<<<grid, 128, 0, s>>>(order, start, end, dx, d, dtok);
     P2R_CHECK_LAUNCH("embed tok bwd");
   }
   if (dpos) {

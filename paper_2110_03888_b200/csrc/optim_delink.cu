@@ -108,13 +108,43 @@ P2R_DEVICE float to_f<float>(float v) { return v; }
 template <>
 P2R_DEVICE float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
 
+// 16-byte vectors: VEC = 4 fp32 or 8 bf16 columns per thread, so one warp reads
+// a 512-byte (fp32) / 512-byte (bf16) row segment per load; 8 warps split the
+// chunk's rows and the warp partials are added in warp order (deterministic).
 template <typename T>
-__global__ void colsum_partial_kernel(const T* __restrict__ x, int ld, int rows, int n, int chunk_rows,
-                                      int seg_rows, const int* __restrict__ counts,
-                                      float* __restrict__ partial) {
-  __shared__ float red[8][32];
-  const int col = blockIdx.x * 32 + (threadIdx.x & 31);
+struct Vec16;
+template <>
+struct Vec16<float> {
+  static constexpr int N = 4;
+  P2R_DEVICE static void load(const float* p, float* o) {
+    const float4 v = *reinterpret_cast<const float4*>(p);
+    o[0] = v.x, o[1] = v.y, o[2] = v.z, o[3] = v.w;
+  }
+};
+template <>
+struct Vec16<__nv_bfloat16> {
+  static constexpr int N = 8;
+  P2R_DEVICE static void load(const __nv_bfloat16* p, float* o) {
+    const uint4 v = *reinterpret_cast<const uint4*>(p);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[i]));
+      o[2 * i] = f.x, o[2 * i + 1] = f.y;
+    }
+  }
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) colsum_partial_kernel(const T* __restrict__ x, int ld, int rows, int n,
+                                                             int chunk_rows, int seg_rows,
+                                                             const int* __restrict__ counts,
+                                                             float* __restrict__ partial) {
+  constexpr int V = Vec16<T>::N;
+  __shared__ float red[8][32 * V];
+  const int lane = threadIdx.x & 31;
   const int tr = threadIdx.x >> 5;  // 0..7
+  const int col = (blockIdx.x * 32 + lane) * V;
   const int chunk = blockIdx.y;
   const int g = blockIdx.z;
   int r0, r1;
@@ -125,16 +155,28 @@ __global__ void colsum_partial_kernel(const T* __restrict__ x, int ld, int rows,
     r0 = chunk * chunk_rows;
     r1 = min(rows, r0 + chunk_rows);
   }
-  float s = 0.f;
-  if (col < n)
-    for (int r = r0 + tr; r < r1; r += 8) s += to_f<T>(x[static_cast<long long>(r) * ld + col]);
-  red[tr][threadIdx.x & 31] = s;
+  float s[V];
+#pragma unroll
+  for (int i = 0; i < V; ++i) s[i] = 0.f;
+  if (col < n) {
+#pragma unroll 4
+    for (int r = r0 + tr; r < r1; r += 8) {
+      float v[V];
+      Vec16<T>::load(x + static_cast<long long>(r) * ld + col, v);
+#pragma unroll
+      for (int i = 0; i < V; ++i) s[i] += v[i];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < V; ++i) red[tr][lane * V + i] = s[i];
   __syncthreads();
-  if (tr == 0 && col < n) {
+  for (int c = threadIdx.x; c < 32 * V; c += 256) {
+    const int gc = blockIdx.x * 32 * V + c;
+    if (gc >= n) continue;
     float t = 0.f;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) t += red[i][threadIdx.x & 31];
-    partial[(static_cast<long long>(g) * gridDim.y + chunk) * n + col] = t;
+    for (int w = 0; w < 8; ++w) t += red[w][c];
+    partial[(static_cast<long long>(g) * gridDim.y + chunk) * n + gc] = t;
   }
 }
 
@@ -233,7 +275,10 @@ extern "C" p2r_status p2r_bias_grad(const void* x, int dtype, int ld, int rows, 
   const int span = counts ? seg_rows : rows;
   const int nchunks = (span + chunk_rows - 1) / chunk_rows;
   const int G = counts ? groups : 1;
-  dim3 grid((n + 31) / 32, nchunks, G);
+  const int vec = dtype == 0 ? 4 : 8;
+  if ((n % vec) || (ld % vec) || (reinterpret_cast<uintptr_t>(x) % 16))
+    return set_error(P2R_EINVAL, "bias grad: n, ld must be multiples of 16 bytes and x 16-byte aligned");
+  dim3 grid((n / vec + 31) / 32, nchunks, G);
   if (dtype == 0)
     colsum_partial_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(x), ld, rows, n, chunk_rows, seg_rows, counts, ws);
   else

@@ -21,6 +21,11 @@ def run(m, n, k, amn=0, bmn=0, epi=_lib.EPI_BF16, split=1, iters=20):
         args.c = C2.data_ptr()
     if epi == _lib.EPI_BIAS_GELU:
         args.c2 = C.data_ptr()  # any bf16-sized buffer works (fp32 is 2x larger)
+    if epi == _lib.EPI_DGELU:
+        AUX = torch.randn(m, n, device=dev).bfloat16()
+        args.c = C2.data_ptr()
+        args.aux = AUX.data_ptr()
+        args.ldaux = n
     ws = torch.empty(max(1, _lib.lib().p2r_gemm_workspace_bytes(ctypes.byref(args)) // 4), device=dev)
     _lib.check(_lib.lib().p2r_set_workspace(ws.data_ptr(), ws.numel() * 4))
     s = torch.cuda.current_stream().cuda_stream
@@ -56,6 +61,8 @@ if __name__ == "__main__":
     run(T, 3 * d, d)                       # QKV
     run(T, d, d, epi=_lib.EPI_F32)         # O proj (+resid)
     run(T, f, d, epi=_lib.EPI_BIAS_GELU)   # FFN1
+    run(T, f, d)                           # FFN1 shape, plain bf16 epilogue
+    run(T, f, d, epi=_lib.EPI_DGELU)       # dH = dY W2^T * gelu'(h)
     run(T, d, f, epi=_lib.EPI_F32)         # FFN2
     run(T, d, 3 * d, epi=_lib.EPI_F32)     # dX of QKV
     run(d, 3 * d, T, amn=1, bmn=1, epi=_lib.EPI_ACC_F32, split=1)  # dWqkv

@@ -7,6 +7,8 @@ shape = sys.argv[1] if len(sys.argv) > 1 else "ffn1"
 T, d, f = 8192, 1024, 4096
 if shape == "ffn1":
     run(T, f, d, epi=_lib.EPI_BIAS_GELU, iters=3)
+elif shape == "dgelu":
+    run(T, f, d, epi=_lib.EPI_DGELU, iters=3)
 elif shape == "qkv":
     run(T, 3 * d, d, iters=3)
 elif shape == "dw":

@@ -44,7 +44,7 @@ def test_layernorm(cuda, rows, d):
     dx16 = torch.empty(rows, d, dtype=torch.bfloat16, device=cuda)
     gg = torch.zeros(d, device=cuda)
     gb = torch.ones(d, device=cuda)  # accumulates (+=)
-    ws = torch.empty(((rows + 63) // 64) * 2 * d, device=cuda)
+    ws = torch.empty(((rows + 15) // 16) * 2 * d, device=cuda)
     call("layernorm_bwd", GY, X, mean, rstd, G, R, rows, d, dx, dx16, gg, gb, ws)
     rgx, rgg, rgb = O.layernorm_bwd(gy, xh, inv, gain)
     assert rel(dx.cpu().numpy(), rgx + resid) < 1e-5
@@ -127,7 +127,10 @@ def test_embedding(cuda):
     gx = rng.standard_normal((B * S, d)).astype(np.float32)
     dt = torch.zeros(V, d, device=cuda)
     dp = torch.zeros(S, d, device=cuda)
-    call("embed_bwd", dev(ids), dev(gx), B, S, d, V, dt, dp)
+    from paper_2110_03888_b200 import _lib
+    nws = _lib.lib().p2r_embed_bwd_workspace(B * S, V)
+    ws = torch.empty(nws, dtype=torch.uint8, device=cuda)
+    call("embed_bwd", dev(ids), dev(gx), B, S, d, V, dt, dp, ws, ctypes.c_size_t(nws))
     rt = np.zeros((V, d), np.float32)
     for i, t in enumerate(ids):  # reference order (tensor.cpp:360-364)
         rt[t] += gx[i]

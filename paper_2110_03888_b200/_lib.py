@@ -9,7 +9,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libp2r.so")
+# P2R_LIB selects another build of the same library (diagnostic ablation builds)
+LIB_PATH = os.environ.get("P2R_LIB") or os.path.join(_HERE, "libp2r.so")
 
 P2R_OK, P2R_EINVAL, P2R_ERANGE, P2R_ELOGIC, P2R_ERUNTIME, P2R_ECUDA, P2R_ENCCL = range(7)
 

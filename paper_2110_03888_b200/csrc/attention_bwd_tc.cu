@@ -48,7 +48,7 @@ struct BwdParams {
 };
 
 // write a row of 64 bf16 values (from fp32 pairs) into a [rows x 64] SW128 atom
-P2R_DEVICE void store_row64(uint8_t* atom, int row, const float* v) {
+P2R_DEVICE void store_row64(uint32_t atom, int row, const float* v) {
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
     uint32_t w[4];
@@ -57,12 +57,12 @@ P2R_DEVICE void store_row64(uint8_t* atom, int row, const float* v) {
       __nv_bfloat162 h = __floats2bfloat162_rn(v[c * 8 + 2 * i], v[c * 8 + 2 * i + 1]);
       w[i] = *reinterpret_cast<uint32_t*>(&h);
     }
-    *reinterpret_cast<uint4*>(atom + sw128_off(row, c)) = make_uint4(w[0], w[1], w[2], w[3]);
+    sts128(atom + sw128_off(row, c), make_uint4(w[0], w[1], w[2], w[3]));
   }
 }
 
 // write 32 bf16 values (4 x 16-B chunks starting at chunk c0) of one row of a SW128 atom
-P2R_DEVICE void store_row32(uint8_t* atom, int row, int c0, const float* v) {
+P2R_DEVICE void store_row32(uint32_t atom, int row, int c0, const float* v) {
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
     uint32_t w[4];
@@ -71,38 +71,32 @@ P2R_DEVICE void store_row32(uint8_t* atom, int row, int c0, const float* v) {
       __nv_bfloat162 h = __floats2bfloat162_rn(v[c * 8 + 2 * i], v[c * 8 + 2 * i + 1]);
       w[i] = *reinterpret_cast<uint32_t*>(&h);
     }
-    *reinterpret_cast<uint4*>(atom + sw128_off(row, c0 + c)) = make_uint4(w[0], w[1], w[2], w[3]);
+    sts128(atom + sw128_off(row, c0 + c), make_uint4(w[0], w[1], w[2], w[3]));
   }
 }
 
-P2R_DEVICE void ld32(uint32_t taddr, float* v) {
-  uint32_t r[32];
-  tmem_ld_32x32b_x32(taddr, r);
+// S and dP rows of one block: both TMEM loads in flight before a single wait
+P2R_DEVICE void ld32x2(uint32_t ta, uint32_t tb, float* a, float* b) {
+  uint32_t ra[32], rb[32];
+  tmem_ld_32x32b_x32(ta, ra);
+  tmem_ld_32x32b_x32(tb, rb);
   tmem_ld_wait();
 #pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-}
-
-P2R_DEVICE void ld64(uint32_t taddr, float* v) {
-  uint32_t r[32];
-  tmem_ld_32x32b_x32(taddr, r);
-  tmem_ld_wait();
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-  tmem_ld_32x32b_x32(taddr + 32, r);
-  tmem_ld_wait();
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[32 + i] = __uint_as_float(r[i]);
+  for (int i = 0; i < 32; ++i) {
+    a[i] = __uint_as_float(ra[i]);
+    b[i] = __uint_as_float(rb[i]);
+  }
 }
 
 // ============================================================================ dQ
 template <int HD>
 struct DqCfg {
   static constexpr int BQ = 128, BKV = 64, KA = HD / 64;
+  static constexpr int NS = HD == 64 ? 4 : 2;  // K/V TMA ring depth (hides load latency behind 2+ blocks)
   static constexpr int QT = BQ * HD * 2;     // Q / dO tile
   static constexpr int KT = BKV * HD * 2;    // K / V tile
   static constexpr int DST = BQ * BKV * 2;   // dS tile (one 64-key atom)
-  static constexpr int OFF_Q = 0, OFF_DO = QT, OFF_K = 2 * QT, OFF_V = OFF_K + 2 * KT, OFF_DS = OFF_V + 2 * KT;
+  static constexpr int OFF_Q = 0, OFF_DO = QT, OFF_K = 2 * QT, OFF_V = OFF_K + NS * KT, OFF_DS = OFF_V + NS * KT;
   static constexpr int OFF_BAR = OFF_DS + 2 * DST;
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
   static constexpr int T_S = 0, T_DP = 128, T_DQ = 256;  // S[2] at 0/64, dP[2] at 128/192
@@ -113,32 +107,45 @@ __global__ void __launch_bounds__(384, 1)
     attn_bwd_dq_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kv,
                    const __grid_constant__ CUtensorMap tm_do, const BwdParams p) {
   using C = DqCfg<HD>;
+#ifdef P2R_ATTN_TRACE
+  // diagnostic build only: clock64 timeline of CTA (0,0,0) (the heaviest causal
+  // tile), dumped over the start of `o` at exit; see scripts/attn_trace.py
+  __shared__ long long s_tr[512];
+  const bool tr_cta = blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
+#define TR(slot) do { if (tr_cta) s_tr[(slot)] = clock64(); } while (0)
+#else
+#define TR(slot) do {} while (0)
+#endif
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* q_full = bar;          // Q + dO
-  uint64_t* kv_full = bar + 1;     // [2]
-  uint64_t* kv_empty = bar + 3;    // [2]
-  uint64_t* s_full = bar + 5;      // [2]  S and dP of block j
-  uint64_t* ds_full = bar + 7;     // [2]  dS of block j in smem
-  uint64_t* dq_done = bar + 9;     // [2]  dQ += dS_j.K_j completed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+  uint64_t* s_full = bar + 1;      // [2]  S and dP of block j
+  uint64_t* ds_full = bar + 3;     // [2]  dS of block j in smem
+  uint64_t* dq_done = bar + 5;     // [2]  dQ += dS_j.K_j completed
+  uint64_t* kv_full = bar + 7;     // [NS]
+  uint64_t* kv_empty = kv_full + C::NS;  // [NS]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kv_empty + C::NS);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  // causal: the last query tiles see the most keys -> launch them first
+  const int qb = p.causal ? gridDim.x - 1 - blockIdx.x : blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int q0 = qb * C::BQ, row0 = b * p.S;
   const int kend = p.causal ? min(p.S, q0 + C::BQ) : p.S;
   const int nkv = (kend + C::BKV - 1) / C::BKV;
+  if (threadIdx.x == 0) TR(0);
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_q);
     tma_prefetch_desc(&tm_kv);
     tma_prefetch_desc(&tm_do);
     mbar_init(q_full, 1);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(kv_full + i, 1);
-      mbar_init(kv_empty + i, 1);
       mbar_init(s_full + i, 1);
       mbar_init(ds_full + i, 256);
       mbar_init(dq_done + i, 1);
+    }
+    for (int i = 0; i < C::NS; ++i) {
+      mbar_init(kv_full + i, 1);
+      mbar_init(kv_empty + i, 1);
     }
     fence_barrier_init();
   }
@@ -148,6 +155,7 @@ __global__ void __launch_bounds__(384, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t sb = smem_u32(smem);
+  if (threadIdx.x == 0) TR(1);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -157,8 +165,8 @@ __global__ void __launch_bounds__(384, 1)
         tma_load_2d(smem + C::OFF_DO + a * C::BQ * 128, &tm_do, q_full, h * HD + 64 * a, row0 + q0);
       }
       for (int j = 0; j < nkv; ++j) {
-        const int st = j & 1;
-        mbar_wait(kv_empty + st, ((j >> 1) & 1) ^ 1);
+        const int st = j % C::NS;
+        mbar_wait(kv_empty + st, ((j / C::NS) & 1) ^ 1);
         mbar_arrive_expect_tx(kv_full + st, 2 * C::KT);
         for (int a = 0; a < C::KA; ++a) {
           tma_load_2d(smem + C::OFF_K + st * C::KT + a * C::BKV * 128, &tm_kv, kv_full + st, p.d + h * HD + 64 * a,
@@ -174,22 +182,26 @@ __global__ void __launch_bounds__(384, 1)
       constexpr uint32_t id_q = make_idesc_bf16(C::BQ, HD, false, true);
       mbar_wait(q_full, 0);
       tc_fence_after();
+      TR(2);
       auto issue_dq = [&](int jj) {
         mbar_wait(ds_full + (jj & 1), (jj >> 1) & 1);
         tc_fence_after();
+        TR(16 + 4 * jj + 2);
         const uint32_t sds = sb + C::OFF_DS + (jj & 1) * C::DST;
-        const uint32_t sk = sb + C::OFF_K + (jj & 1) * C::KT;
+        const uint32_t sk = sb + C::OFF_K + (jj % C::NS) * C::KT;
 #pragma unroll
         for (int k = 0; k < C::BKV / 16; ++k)
           umma_bf16(tmem + C::T_DQ, make_sw128_desc(sds + k * 32, 16, 1024),
                     make_sw128_desc(sk + k * 2048, C::BKV * 128, 1024), id_q, (jj > 0 || k > 0) ? 1u : 0u);
-        umma_commit(kv_empty + (jj & 1));
+        umma_commit(kv_empty + jj % C::NS);
         umma_commit(dq_done + (jj & 1));
+        TR(16 + 4 * jj + 3);
       };
       for (int j = 0; j < nkv; ++j) {
-        const int st = j & 1;
-        mbar_wait(kv_full + st, (j >> 1) & 1);
+        const int st = j % C::NS;
+        mbar_wait(kv_full + st, (j / C::NS) & 1);
         tc_fence_after();
+        TR(16 + 4 * j);
         const uint32_t sk = sb + C::OFF_K + st * C::KT, sv = sb + C::OFF_V + st * C::KT;
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k) {
@@ -200,6 +212,7 @@ __global__ void __launch_bounds__(384, 1)
                     make_sw128_desc(sv + ka * C::BKV * 128 + kk, 16, 1024), id_s, k > 0 ? 1u : 0u);
         }
         umma_commit(s_full + (j & 1));
+        TR(16 + 4 * j + 1);
         if (j > 0) issue_dq(j - 1);
       }
       issue_dq(nkv - 1);
@@ -230,26 +243,39 @@ __global__ void __launch_bounds__(384, 1)
       if (half == 0) p.dsum[bh * p.S + q] = D;
     }
     const float lse2 = q < p.S ? p.lse[bh * p.S + q] * kLog2e : 0.0f;
+    const float sl2 = p.sl2;
+    const bool trw = warp == 4 && lane == 0;  // trace writer (P2R_ATTN_TRACE builds)
+    if (trw) TR(3);
     for (int j = 0; j < nkv; ++j) {
       mbar_wait(s_full + (j & 1), (j >> 1) & 1);
       tc_fence_after();
+      if (trw) TR(100 + 6 * j);
       float s[32], dp[32];
-      ld32(tmem + la + C::T_S + (j & 1) * 64 + half * 32, s);
-      ld32(tmem + la + C::T_DP + (j & 1) * 64 + half * 32, dp);
+      ld32x2(tmem + la + C::T_S + (j & 1) * 64 + half * 32, tmem + la + C::T_DP + (j & 1) * 64 + half * 32, s, dp);
+      if (trw) TR(100 + 6 * j + 1);
       const int k0 = j * C::BKV + half * 32;
       int lim = 32;
       if (q >= p.S) lim = 0;
       else if (p.causal || k0 + 32 > p.S) lim = min(p.causal ? q + 1 : p.S, p.S) - k0;
+      // exponentials unconditionally (no per-element predication); the causal /
+      // tail mask is a select on the few blocks that need it (discards any inf)
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const float pv = i < lim ? ex2_approx(fmaf(s[i], p.sl2, -lse2)) : 0.0f;
-        s[i] = pv * (dp[i] - D);
+      for (int i = 0; i < 32; ++i) s[i] = ex2_approx(fmaf(s[i], sl2, -lse2));
+      if (lim < 32) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s[i] = i < lim ? s[i] : 0.0f;
       }
+#pragma unroll
+      for (int i = 0; i < 32; ++i) s[i] = s[i] * (dp[i] - D);
+      if (trw) TR(100 + 6 * j + 2);
       if (j >= 2) mbar_wait(dq_done + (j & 1), ((j - 2) >> 1) & 1);
-      store_row32(smem + C::OFF_DS + (j & 1) * C::DST, r, half * 4, s);
+      if (trw) TR(100 + 6 * j + 3);
+      store_row32(sb + C::OFF_DS + (j & 1) * C::DST, r, half * 4, s);
       fence_async_smem();
       tc_fence_before();
+      if (trw) TR(100 + 6 * j + 4);
       mbar_arrive(ds_full + (j & 1));
+      if (trw) TR(100 + 6 * j + 5);
     }
     mbar_wait(dq_done + ((nkv - 1) & 1), ((nkv - 1) >> 1) & 1);
     tc_fence_after();
@@ -274,21 +300,29 @@ __global__ void __launch_bounds__(384, 1)
   }
   tc_fence_before();
   __syncthreads();
+#ifdef P2R_ATTN_TRACE
+  if (threadIdx.x == 0) TR(4);
+  __syncthreads();
+  if (tr_cta)
+    for (int i = threadIdx.x; i < 512; i += blockDim.x) reinterpret_cast<long long*>(const_cast<__nv_bfloat16*>(p.o))[i] = s_tr[i];
+#endif
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
 }
+#undef TR
 
 // ============================================================================ dK / dV
 template <int HD>
 struct KvCfg {
   static constexpr int BK = 128, BQ = 64, KA = HD / 64;
+  static constexpr int NS = HD == 64 ? 4 : 2;  // Q/dO TMA ring depth
   static constexpr int KT = BK * HD * 2;     // K / V tile
   static constexpr int QT = BQ * HD * 2;     // Q / dO tile
   static constexpr int PT = BK * BQ * 2;     // P^T / dS^T tile (one 64-query atom)
-  static constexpr int OFF_K = 0, OFF_V = KT, OFF_Q = 2 * KT, OFF_DO = OFF_Q + 2 * QT;
-  static constexpr int OFF_P = OFF_DO + 2 * QT, OFF_DS = OFF_P + 2 * PT;
+  static constexpr int OFF_K = 0, OFF_V = KT, OFF_Q = 2 * KT, OFF_DO = OFF_Q + NS * QT;
+  static constexpr int OFF_P = OFF_DO + NS * QT, OFF_DS = OFF_P + 2 * PT;
   static constexpr int OFF_LD = OFF_DS + 2 * PT;  // [2][2][64] floats: lse2, D
   static constexpr int OFF_BAR = OFF_LD + 1024;
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
@@ -304,13 +338,12 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* kv_full = bar;
-  uint64_t* q_full = bar + 1;    // [2]
-  uint64_t* q_empty = bar + 3;   // [2]
-  uint64_t* s_full = bar + 5;    // [2]
-  uint64_t* p_full = bar + 7;    // [2]
-  uint64_t* pv_done = bar + 9;   // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
-  float* sLD = reinterpret_cast<float*>(smem + C::OFF_LD);
+  uint64_t* s_full = bar + 1;    // [2]
+  uint64_t* p_full = bar + 3;    // [2]
+  uint64_t* pv_done = bar + 5;   // [2]
+  uint64_t* q_full = bar + 7;    // [NS]
+  uint64_t* q_empty = q_full + C::NS;  // [NS]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_empty + C::NS);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int k0 = kb * C::BK, row0 = b * p.S;
@@ -322,11 +355,13 @@ __global__ void __launch_bounds__(384, 1)
     tma_prefetch_desc(&tm_do);
     mbar_init(kv_full, 1);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(q_full + i, 1);
-      mbar_init(q_empty + i, 1);
       mbar_init(s_full + i, 1);
       mbar_init(p_full + i, 256);
       mbar_init(pv_done + i, 1);
+    }
+    for (int i = 0; i < C::NS; ++i) {
+      mbar_init(q_full + i, 1);
+      mbar_init(q_empty + i, 1);
     }
     fence_barrier_init();
   }
@@ -345,9 +380,9 @@ __global__ void __launch_bounds__(384, 1)
         tma_load_2d(smem + C::OFF_V + a * C::BK * 128, &tm_kv, kv_full, 2 * p.d + h * HD + 64 * a, row0 + k0);
       }
       for (int i = 0; i < nq; ++i) {
-        const int st = i & 1;
+        const int st = i % C::NS;
         const int q1 = qstart + i * C::BQ;
-        mbar_wait(q_empty + st, ((i >> 1) & 1) ^ 1);
+        mbar_wait(q_empty + st, ((i / C::NS) & 1) ^ 1);
         mbar_arrive_expect_tx(q_full + st, 2 * C::QT);
         for (int a = 0; a < C::KA; ++a) {
           tma_load_2d(smem + C::OFF_Q + st * C::QT + a * C::BQ * 128, &tm_q, q_full + st, h * HD + 64 * a, row0 + q1);
@@ -364,9 +399,9 @@ __global__ void __launch_bounds__(384, 1)
       auto issue_kv = [&](int ii) {
         mbar_wait(p_full + (ii & 1), (ii >> 1) & 1);
         tc_fence_after();
-        const int st = ii & 1;
+        const int st = ii & 1, qs = ii % C::NS;
         const uint32_t spt = sb + C::OFF_P + st * C::PT, sds = sb + C::OFF_DS + st * C::PT;
-        const uint32_t sq = sb + C::OFF_Q + st * C::QT, sdo = sb + C::OFF_DO + st * C::QT;
+        const uint32_t sq = sb + C::OFF_Q + qs * C::QT, sdo = sb + C::OFF_DO + qs * C::QT;
 #pragma unroll
         for (int k = 0; k < C::BQ / 16; ++k) {
           // dV += P^T dO ; dK += dS^T Q   (dO / Q tiles re-read MN-major: rows = queries)
@@ -375,14 +410,14 @@ __global__ void __launch_bounds__(384, 1)
           umma_bf16(tmem + C::T_DK, make_sw128_desc(sds + k * 32, 16, 1024),
                     make_sw128_desc(sq + k * 2048, C::BQ * 128, 1024), id_o, (ii > 0 || k > 0) ? 1u : 0u);
         }
-        umma_commit(q_empty + st);
+        umma_commit(q_empty + qs);
         umma_commit(pv_done + st);
       };
       for (int i = 0; i < nq; ++i) {
-        const int st = i & 1;
-        mbar_wait(q_full + st, (i >> 1) & 1);
+        const int st = i & 1, qs = i % C::NS;
+        mbar_wait(q_full + qs, (i / C::NS) & 1);
         tc_fence_after();
-        const uint32_t sq = sb + C::OFF_Q + st * C::QT, sdo = sb + C::OFF_DO + st * C::QT;
+        const uint32_t sq = sb + C::OFF_Q + qs * C::QT, sdo = sb + C::OFF_DO + qs * C::QT;
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k) {
           const uint32_t ka = (k >> 2), kk = (k & 3) * 32;
@@ -402,43 +437,64 @@ __global__ void __launch_bounds__(384, 1)
     const int kr = (warp & 3) * 32 + lane;  // key row == TMEM lane
     const int half = (warp - 4) >> 2;
     const int key = k0 + kr;
+    const float sl2 = p.sl2;
     const uint32_t la = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const long long bh = static_cast<long long>(b) * p.H + h;
+    // lse2 / D of query block i staged in sLD[i & 1] (threads 0..63: lse, 64..127: D);
+    // block i+1's values are loaded into a register while block i is processed.
+    // (raw values in the register; the log2(e) scale is applied at the smem store
+    // so no instruction waits on the load before the block's named barrier)
+    auto fetch_ld = [&](int i) -> float {
+      const int qq = qstart + i * C::BQ + (t & 63);
+      if (t >= 128 || i >= nq || qq >= p.S) return 0.0f;
+      return t < 64 ? p.lse[bh * p.S + qq] : p.dsum[bh * p.S + qq];
+    };
+    const float ld_scale = t < 64 ? kLog2e : 1.0f;
+    if (t < 128) sts32f(sb + C::OFF_LD + 4 * ((t >> 6) * 64 + (t & 63)), fetch_ld(0) * ld_scale);
     for (int i = 0; i < nq; ++i) {
       const int st = i & 1;
       const int q1 = qstart + i * C::BQ;
-      // stage lse2 / D of this query block (threads 0..63: lse, 64..127: D)
-      if (t < 128) {
-        const int c = t & 63, qq = q1 + c;
-        float v = 0.0f;
-        if (qq < p.S) v = t < 64 ? p.lse[bh * p.S + qq] * kLog2e : p.dsum[bh * p.S + qq];
-        sLD[(st * 2 + (t >> 6)) * 64 + c] = v;
-      }
+      const float ld_next = fetch_ld(i + 1);
       named_sync(1, 256);
       mbar_wait(s_full + st, (i >> 1) & 1);
       tc_fence_after();
       float s[32], dp[32];
-      ld32(tmem + la + C::T_S + st * 64 + half * 32, s);
-      ld32(tmem + la + C::T_DP + st * 64 + half * 32, dp);
-      const float* L2 = sLD + st * 128 + half * 32;
-      const float* Dv = L2 + 64;
+      ld32x2(tmem + la + C::T_S + st * 64 + half * 32, tmem + la + C::T_DP + st * 64 + half * 32, s, dp);
+      // this warp's 32 query columns: lse2 at +0, D at +64 floats (warp-uniform broadcasts)
+      const uint32_t lda = sb + C::OFF_LD + (st * 128 + half * 32) * 4;
       // visible: query q >= key (causal), q < S, key < S
       const int qb1 = q1 + half * 32;
       int lo = 0, hi = min(32, p.S - qb1);
       if (p.causal) lo = max(0, key - qb1);
       if (key >= p.S) hi = 0;
 #pragma unroll
-      for (int c = 0; c < 32; ++c) {
-        const float pv = (c >= lo && c < hi) ? ex2_approx(fmaf(s[c], p.sl2, -L2[c])) : 0.0f;
-        s[c] = pv;
-        dp[c] = pv * (dp[c] - Dv[c]);
+      for (int c4 = 0; c4 < 8; ++c4) {
+        const float4 l4 = lds128f(lda + 16 * c4);
+        s[4 * c4 + 0] = ex2_approx(fmaf(s[4 * c4 + 0], sl2, -l4.x));
+        s[4 * c4 + 1] = ex2_approx(fmaf(s[4 * c4 + 1], sl2, -l4.y));
+        s[4 * c4 + 2] = ex2_approx(fmaf(s[4 * c4 + 2], sl2, -l4.z));
+        s[4 * c4 + 3] = ex2_approx(fmaf(s[4 * c4 + 3], sl2, -l4.w));
+      }
+      if (lo > 0 || hi < 32) {  // diagonal / tail blocks only
+#pragma unroll
+        for (int c = 0; c < 32; ++c) s[c] = (c >= lo && c < hi) ? s[c] : 0.0f;
+      }
+#pragma unroll
+      for (int c4 = 0; c4 < 8; ++c4) {
+        const float4 d4 = lds128f(lda + 256 + 16 * c4);
+        dp[4 * c4 + 0] = s[4 * c4 + 0] * (dp[4 * c4 + 0] - d4.x);
+        dp[4 * c4 + 1] = s[4 * c4 + 1] * (dp[4 * c4 + 1] - d4.y);
+        dp[4 * c4 + 2] = s[4 * c4 + 2] * (dp[4 * c4 + 2] - d4.z);
+        dp[4 * c4 + 3] = s[4 * c4 + 3] * (dp[4 * c4 + 3] - d4.w);
       }
       if (i >= 2) mbar_wait(pv_done + st, ((i - 2) >> 1) & 1);
-      store_row32(smem + C::OFF_P + st * C::PT, kr, half * 4, s);
-      store_row32(smem + C::OFF_DS + st * C::PT, kr, half * 4, dp);
+      store_row32(sb + C::OFF_P + st * C::PT, kr, half * 4, s);
+      store_row32(sb + C::OFF_DS + st * C::PT, kr, half * 4, dp);
       fence_async_smem();
       tc_fence_before();
       mbar_arrive(p_full + st);
+      // every thread passed this iteration's named_sync, so block i-1's slot is free
+      if (t < 128) sts32f(sb + C::OFF_LD + 4 * (((st ^ 1) * 2 + (t >> 6)) * 64 + (t & 63)), ld_next * ld_scale);
     }
     mbar_wait(pv_done + ((nq - 1) & 1), ((nq - 1) >> 1) & 1);
     tc_fence_after();

@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(256, 1)
         const int jp = j - C::NPB;
         mbar_wait(o_done + (jp & 1), (jp >> 1) & 1);
       }
-      uint8_t* sp = smem + C::OFF_P + (j % C::NPB) * C::PTILE;
+      const uint32_t sp = smem_u32(smem) + C::OFF_P + (j % C::NPB) * C::PTILE;
       float ls = 0.0f, ls2 = 0.0f;
       const float nm = -m_used;
 #pragma unroll
@@ -256,8 +256,7 @@ __global__ void __launch_bounds__(256, 1)
           w[i] = *reinterpret_cast<uint32_t*>(&hh);
         }
         const int atom = c16 >> 3;  // 8 chunks of 8 keys per 64-key atom
-        *reinterpret_cast<uint4*>(sp + atom * (BQ * 128) + sw128_off(r, c16 & 7)) =
-            make_uint4(w[0], w[1], w[2], w[3]);
+        sts128(sp + atom * (BQ * 128) + sw128_off(r, c16 & 7), make_uint4(w[0], w[1], w[2], w[3]));
       }
       l += ls + ls2;
       fence_async_smem();

@@ -1,0 +1,36 @@
+"""Print the per-iteration clock64 timeline of the heaviest dQ CTA (B=1, causal).
+
+Needs the trace build: python scripts/attn_variants.py trace, then
+P2R_LIB=build/exp/libp2r_trace.so python scripts/attn_trace.py
+"""
+import ctypes
+import sys
+import numpy as np
+import torch
+sys.path.insert(0, ".")
+from paper_2110_03888_b200 import _lib
+
+L = _lib.lib()
+P = lambda t: ctypes.c_void_p(t.data_ptr())
+st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+B, H, S, hd = 1, 16, 1024, 64
+d = H * hd
+qkv = (torch.randn(B * S, 3 * d, device="cuda") * 0.5).bfloat16()
+o = torch.empty(B * S, d, device="cuda", dtype=torch.bfloat16)
+lse = torch.empty(B * H * S, device="cuda")
+do = torch.randn(B * S, d, device="cuda").bfloat16()
+dsum = torch.empty(B * H * S, device="cuda")
+dqkv = torch.empty(B * S, 3 * d, device="cuda", dtype=torch.bfloat16)
+for _ in range(3):
+    _lib.check(L.p2r_attention_fwd(P(qkv), P(o), P(lse), B, H, S, d, 1, st))
+    _lib.check(L.p2r_attention_bwd(P(qkv), P(o), P(lse), P(do), P(dsum), P(dqkv), B, H, S, d, 1, st))
+torch.cuda.synchronize()
+t = o.view(torch.int64).flatten()[:512].cpu().numpy()
+t0 = t[0]
+rel = lambda v: int(v - t0)
+print("after setup sync", rel(t[1]), " q_full (mma)", rel(t[2]), " D done (softmax)", rel(t[3]), " end", rel(t[4]))
+print(" j | mma: kv_full  S-issued  ds_full(j) dQ-issued | sm: s_full  tmem_ld  math  dq_done  stored  arrived")
+for j in range(16):
+    m = t[16 + 4 * j:16 + 4 * j + 4]
+    s = t[100 + 6 * j:100 + 6 * j + 6]
+    print(f"{j:2d} | " + " ".join(f"{rel(v):8d}" for v in m) + " | " + " ".join(f"{rel(v):8d}" for v in s))

@@ -76,6 +76,14 @@ P2R_DEVICE void tma_load_2d(void* smem_dst, const CUtensorMap* map, uint64_t* ba
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+// 1-D bulk async copy global -> shared (16-byte aligned, bytes % 16 == 0),
+// completion counted on `bar` (arrive.expect_tx by the issuing thread).
+P2R_DEVICE void bulk_load(uint32_t smem_dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_dst),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
 
 // ----------------------------------------------------------------------------
 // tcgen05 (5th-gen tensor cores, accumulators in TMEM)

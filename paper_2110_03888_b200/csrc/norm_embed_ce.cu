@@ -13,179 +13,220 @@
 namespace p2r {
 
 // ------------------------------- LayerNorm -----------------------------------
-// One warp per row; NV float4 per lane (d = 128 * NV).
+// Warp-per-row with warp-private bulk-copy pipelines: each warp owns rows
+// gw, gw + W, ... (W = warps in the grid) and a ring of `nst` shared-memory row
+// slots filled by 1-D cp.async.bulk copies that its lane 0 issues `nst` rows
+// ahead (completion on the warp's own mbarriers). Row statistics are warp
+// shuffles, so no block-level barrier sits on the per-row path; lane l owns the
+// float4 columns l, l+32, ... (NV = d/128 of them). gain/bias live in shared
+// memory. All reductions have a fixed order (deterministic).
+constexpr int kLnMaxStages = 3;
+
+P2R_DEVICE float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+
+P2R_DEVICE void ln_row_issue(uint64_t* bar, uint32_t dst, const float* const* src, int ntens, int row, int D) {
+  const uint32_t bytes = static_cast<uint32_t>(D) * 4;
+  mbar_arrive_expect_tx(bar, bytes * ntens);
+  for (int t = 0; t < ntens; ++t) bulk_load(dst + t * bytes, src[t] + static_cast<long long>(row) * D, bytes, bar);
+}
+
+P2R_DEVICE void st_bf16x4(__nv_bfloat16* p, float4 o) {
+  __nv_bfloat162 lo = __floats2bfloat162_rn(o.x, o.y), hi = __floats2bfloat162_rn(o.z, o.w);
+  uint2 w;
+  w.x = *reinterpret_cast<uint32_t*>(&lo);
+  w.y = *reinterpret_cast<uint32_t*>(&hi);
+  *reinterpret_cast<uint2*>(p) = w;
+}
+
 template <int NV>
-__global__ void __launch_bounds__(256) ln_fwd_kernel(const float* __restrict__ x,
-                                                    const float* __restrict__ gain,
-                                                    const float* __restrict__ bias, int rows,
-                                                    float eps, __nv_bfloat16* __restrict__ y16,
-                                                    float* __restrict__ y32,
-                                                    float* __restrict__ mean_out,
-                                                    float* __restrict__ rstd_out) {
+__global__ void __launch_bounds__(256) ln_fwd_kernel(const float* __restrict__ x, const float* __restrict__ gain,
+                                                    const float* __restrict__ bias, int rows, float eps,
+                                                    __nv_bfloat16* __restrict__ y16, float* __restrict__ y32,
+                                                    float* __restrict__ mean_out, float* __restrict__ rstd_out,
+                                                    int nst) {
   constexpr int D = 128 * NV;
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (warp >= rows) return;
-  const float4* xr = reinterpret_cast<const float4*>(x + static_cast<long long>(warp) * D);
-  float4 v[NV];
-  float s = 0.f;
-#pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    v[i] = xr[lane + 32 * i];
-    s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
-  }
-  s = warp_sum(s);
-  const float mean = s / static_cast<float>(D);
-  float q = 0.f;
-#pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    const float a = v[i].x - mean, b = v[i].y - mean, c = v[i].z - mean, d = v[i].w - mean;
-    q += (a * a + b * b) + (c * c + d * d);
-  }
-  q = warp_sum(q);
-  const float var = q / static_cast<float>(D);
-  const float inv = 1.0f / sqrtf(var + eps);
+  extern __shared__ __align__(128) uint8_t ln_smem[];
+  __shared__ uint64_t bars[8][kLnMaxStages];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  float* sg = reinterpret_cast<float*>(ln_smem);  // gain | bias
+  for (int i = threadIdx.x; i < 2 * D; i += blockDim.x) sg[i] = i < D ? gain[i] : bias[i - D];
+  const uint32_t ring = smem_u32(ln_smem) + 2 * D * 4 + warp * nst * D * 4;
+  uint64_t* bar = bars[warp];
+  const int W = gridDim.x * nw, gw = blockIdx.x * nw + warp;
+  const int nrows = gw < rows ? (rows - gw + W - 1) / W : 0;
+  const float* src[1] = {x};
   if (lane == 0) {
-    mean_out[warp] = mean;
-    rstd_out[warp] = inv;
+    for (int i = 0; i < nst; ++i) mbar_init(bar + i, 1);
+    fence_barrier_init();
+    for (int k = 0; k < nst && k < nrows; ++k) ln_row_issue(bar + k, ring + k * D * 4, src, 1, gw + k * W, D);
   }
-  const float4* g4 = reinterpret_cast<const float4*>(gain);
-  const float4* b4 = reinterpret_cast<const float4*>(bias);
+  __syncthreads();  // gain/bias staged, barriers initialised
+  const float inv_d = 1.0f / static_cast<float>(D);
+  for (int k = 0; k < nrows; ++k) {
+    const int st = k % nst, r = gw + k * W;
+    mbar_wait(bar + st, (k / nst) & 1);
+    float4 v[NV];
+    float s = 0.f;
 #pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    const int c4 = lane + 32 * i;
-    const float4 g = g4[c4], bb = b4[c4];
-    float4 o;
-    o.x = (v[i].x - mean) * inv * g.x + bb.x;
-    o.y = (v[i].y - mean) * inv * g.y + bb.y;
-    o.z = (v[i].z - mean) * inv * g.z + bb.z;
-    o.w = (v[i].w - mean) * inv * g.w + bb.w;
-    const long long off = static_cast<long long>(warp) * D + 4LL * c4;
-    if (y16) {
-      __nv_bfloat162 lo = __floats2bfloat162_rn(o.x, o.y), hi = __floats2bfloat162_rn(o.z, o.w);
-      uint2 w;
-      w.x = *reinterpret_cast<uint32_t*>(&lo);
-      w.y = *reinterpret_cast<uint32_t*>(&hi);
-      *reinterpret_cast<uint2*>(y16 + off) = w;
+    for (int i = 0; i < NV; ++i) {
+      v[i] = lds128f(ring + st * D * 4 + (lane + 32 * i) * 16);
+      s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
     }
-    if (y32) *reinterpret_cast<float4*>(y32 + off) = o;
+    s = warp_sum(s);  // consumes every lane's smem reads
+    if (lane == 0 && k + nst < nrows) ln_row_issue(bar + st, ring + st * D * 4, src, 1, r + nst * W, D);
+    const float mu = s * inv_d;
+    float q = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const float a = v[i].x - mu, b = v[i].y - mu, c = v[i].z - mu, d = v[i].w - mu;
+      q += (a * a + b * b) + (c * c + d * d);
+    }
+    q = warp_sum(q);  // two-pass (biased) variance, tensor.cpp:265-336
+    const float inv = 1.0f / sqrtf(q * inv_d + eps);
+    if (lane == 0) {
+      mean_out[r] = mu;
+      rstd_out[r] = inv;
+    }
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c4 = lane + 32 * i;
+      const float4 g = reinterpret_cast<const float4*>(sg)[c4], bb = reinterpret_cast<const float4*>(sg + D)[c4];
+      float4 o;
+      o.x = (v[i].x - mu) * inv * g.x + bb.x;
+      o.y = (v[i].y - mu) * inv * g.y + bb.y;
+      o.z = (v[i].z - mu) * inv * g.z + bb.z;
+      o.w = (v[i].w - mu) * inv * g.w + bb.w;
+      const long long off = static_cast<long long>(r) * D + 4LL * c4;
+      if (y16) st_bf16x4(y16 + off, o);
+      if (y32) *reinterpret_cast<float4*>(y32 + off) = o;
+    }
   }
 }
 
 // dx = resid + inv * (gy - mean(gy) - xhat * mean(gy * xhat)), gy = dy * gain.
-// Per-block partial sums of dy*xhat and dy (for dgain/dbias) go to `partial`
-// ([gridDim.x][2][D]); ln_param_grad_reduce adds them into the grads in order.
+// dgain/dbias: per-lane column accumulators over the warp's rows, combined per
+// block (warp order) into partial[blockIdx.x][2][D]; ln_param_grad_reduce adds
+// the block partials into the grads in block order.
 template <int NV>
-__global__ void __launch_bounds__(256) ln_bwd_kernel(
+__global__ void __launch_bounds__(128) ln_bwd_kernel(
     const float* __restrict__ dy, const float* __restrict__ x, const float* __restrict__ mean_in,
-    const float* __restrict__ rstd_in, const float* __restrict__ gain,
-    const float* __restrict__ resid, int rows, int rows_per_block, float* __restrict__ dx32,
-    __nv_bfloat16* __restrict__ dx16, float* __restrict__ partial) {
+    const float* __restrict__ rstd_in, const float* __restrict__ gain, const float* __restrict__ resid, int rows,
+    float* __restrict__ dx32, __nv_bfloat16* __restrict__ dx16, float* __restrict__ partial, int nst) {
   constexpr int D = 128 * NV;
-  __shared__ float red[8][2][128];  // per-warp partials, one float4-slice at a time
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r0 = blockIdx.x * rows_per_block;
-  const int r1 = min(rows, r0 + rows_per_block);
+  extern __shared__ __align__(128) uint8_t ln_smem[];
+  __shared__ uint64_t bars[4][kLnMaxStages];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int ntens = resid ? 3 : 2;
+  float* sg = reinterpret_cast<float*>(ln_smem);
+  for (int i = threadIdx.x; i < D; i += blockDim.x) sg[i] = gain[i];
+  const uint32_t slot = ntens * D * 4;  // one row of each tensor
+  const uint32_t ring = smem_u32(ln_smem) + D * 4 + warp * nst * slot;
+  uint64_t* bar = bars[warp];
+  const int W = gridDim.x * nw, gw = blockIdx.x * nw + warp;
+  const int nrows = gw < rows ? (rows - gw + W - 1) / W : 0;
+  const float* src[3] = {dy, x, resid};
+  if (lane == 0) {
+    for (int i = 0; i < nst; ++i) mbar_init(bar + i, 1);
+    fence_barrier_init();
+    for (int k = 0; k < nst && k < nrows; ++k) ln_row_issue(bar + k, ring + k * slot, src, ntens, gw + k * W, D);
+  }
+  __syncthreads();
+  const float inv_d = 1.0f / static_cast<float>(D);
   float4 pg[NV], pb[NV];
 #pragma unroll
   for (int i = 0; i < NV; ++i) pg[i] = pb[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-  const float4* g4 = reinterpret_cast<const float4*>(gain);
-  for (int r = r0 + warp; r < r1; r += 8) {
-    const float4* dyr = reinterpret_cast<const float4*>(dy + static_cast<long long>(r) * D);
-    const float4* xr = reinterpret_cast<const float4*>(x + static_cast<long long>(r) * D);
-    const float mean = mean_in[r], inv = rstd_in[r];
-    float4 h[NV], gy[NV];
+  float mu_n = 0.f, inv_n = 0.f;
+  if (nrows > 0) {
+    mu_n = mean_in[gw];
+    inv_n = rstd_in[gw];
+  }
+  for (int k = 0; k < nrows; ++k) {
+    const int st = k % nst, r = gw + k * W;
+    const float mu = mu_n, inv = inv_n;
+    if (k + 1 < nrows) {  // next row's statistics, off the critical path
+      mu_n = mean_in[r + W];
+      inv_n = rstd_in[r + W];
+    }
+    mbar_wait(bar + st, (k / nst) & 1);
+    const uint32_t sd = ring + st * slot, sx = sd + D * 4, sr = sd + 2 * D * 4;
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
-      const int c4 = lane + 32 * i;
-      const float4 d = dyr[c4], xv = xr[c4], g = g4[c4];
-      h[i] = make_float4((xv.x - mean) * inv, (xv.y - mean) * inv, (xv.z - mean) * inv,
-                         (xv.w - mean) * inv);
-      pg[i].x += d.x * h[i].x;
-      pg[i].y += d.y * h[i].y;
-      pg[i].z += d.z * h[i].z;
-      pg[i].w += d.w * h[i].w;
+      const uint32_t o = (lane + 32 * i) * 16;
+      const float4 d = lds128f(sd + o), xv = lds128f(sx + o), g = reinterpret_cast<const float4*>(sg)[lane + 32 * i];
+      const float4 h = make_float4((xv.x - mu) * inv, (xv.y - mu) * inv, (xv.z - mu) * inv, (xv.w - mu) * inv);
+      const float4 gy = make_float4(d.x * g.x, d.y * g.y, d.z * g.z, d.w * g.w);
+      s1 += (gy.x + gy.y) + (gy.z + gy.w);
+      s2 += (gy.x * h.x + gy.y * h.y) + (gy.z * h.z + gy.w * h.w);
+      pg[i].x += d.x * h.x;
+      pg[i].y += d.y * h.y;
+      pg[i].z += d.z * h.z;
+      pg[i].w += d.w * h.w;
       pb[i].x += d.x;
       pb[i].y += d.y;
       pb[i].z += d.z;
       pb[i].w += d.w;
-      gy[i] = make_float4(d.x * g.x, d.y * g.y, d.z * g.z, d.w * g.w);
-      s1 += (gy[i].x + gy[i].y) + (gy[i].z + gy[i].w);
-      s2 += (gy[i].x * h[i].x + gy[i].y * h[i].y) + (gy[i].z * h[i].z + gy[i].w * h[i].w);
     }
     s1 = warp_sum(s1);
     s2 = warp_sum(s2);
-    const float inv_d = 1.0f / static_cast<float>(D);
     const float a1 = inv_d * s1, a2 = inv_d * s2;
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       const int c4 = lane + 32 * i;
+      const uint32_t o = c4 * 16;
+      const float4 d = lds128f(sd + o), xv = lds128f(sx + o), g = reinterpret_cast<const float4*>(sg)[c4];
+      const float4 rr = resid ? lds128f(sr + o) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 h = make_float4((xv.x - mu) * inv, (xv.y - mu) * inv, (xv.z - mu) * inv, (xv.w - mu) * inv);
+      float4 out;
+      out.x = inv * (d.x * g.x - a1 - h.x * a2) + rr.x;
+      out.y = inv * (d.y * g.y - a1 - h.y * a2) + rr.y;
+      out.z = inv * (d.z * g.z - a1 - h.z * a2) + rr.z;
+      out.w = inv * (d.w * g.w - a1 - h.w * a2) + rr.w;
       const long long off = static_cast<long long>(r) * D + 4LL * c4;
-      float4 o = make_float4(inv * (gy[i].x - a1 - h[i].x * a2), inv * (gy[i].y - a1 - h[i].y * a2),
-                             inv * (gy[i].z - a1 - h[i].z * a2), inv * (gy[i].w - a1 - h[i].w * a2));
-      if (resid) {
-        const float4 rr = *reinterpret_cast<const float4*>(resid + off);
-        o.x += rr.x;
-        o.y += rr.y;
-        o.z += rr.z;
-        o.w += rr.w;
-      }
-      *reinterpret_cast<float4*>(dx32 + off) = o;
-      if (dx16) {
-        __nv_bfloat162 lo = __floats2bfloat162_rn(o.x, o.y), hi = __floats2bfloat162_rn(o.z, o.w);
-        uint2 w;
-        w.x = *reinterpret_cast<uint32_t*>(&lo);
-        w.y = *reinterpret_cast<uint32_t*>(&hi);
-        *reinterpret_cast<uint2*>(dx16 + off) = w;
-      }
+      *reinterpret_cast<float4*>(dx32 + off) = out;
+      if (dx16) st_bf16x4(dx16 + off, out);
     }
+    __syncwarp();  // every lane's reads of this slot are done before it is refilled
+    if (lane == 0 && k + nst < nrows) ln_row_issue(bar + st, ring + st * slot, src, ntens, r + nst * W, D);
   }
-  // block reduce of the per-warp column partials (fixed order: warp 0..7)
-  float* out = partial + static_cast<long long>(blockIdx.x) * 2 * D;
+  // combine the warps' column partials in warp order (the ring is drained)
+  __syncthreads();
+  float* red = reinterpret_cast<float*>(ln_smem + D * 4);  // [nw][2][D]
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
     const int c4 = lane + 32 * i;
-    red[warp][0][4 * lane + 0] = pg[i].x;
-    red[warp][0][4 * lane + 1] = pg[i].y;
-    red[warp][0][4 * lane + 2] = pg[i].z;
-    red[warp][0][4 * lane + 3] = pg[i].w;
-    red[warp][1][4 * lane + 0] = pb[i].x;
-    red[warp][1][4 * lane + 1] = pb[i].y;
-    red[warp][1][4 * lane + 2] = pb[i].z;
-    red[warp][1][4 * lane + 3] = pb[i].w;
-    __syncthreads();
-    const int t = threadIdx.x;  // 256 threads: t<128 gain, else bias
-    const int which = t >> 7, c = t & 127;
-    float s = 0.f;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) s += red[w][which][c];
-    out[which * D + 4 * (32 * i) + c] = s;
-    (void)c4;
-    __syncthreads();
+    reinterpret_cast<float4*>(red + (warp * 2) * D)[c4] = pg[i];
+    reinterpret_cast<float4*>(red + (warp * 2 + 1) * D)[c4] = pb[i];
+  }
+  __syncthreads();
+  float* out = partial + static_cast<long long>(blockIdx.x) * 2 * D;
+  for (int c = threadIdx.x; c < 2 * D; c += blockDim.x) {
+    float t = 0.f;
+    for (int w = 0; w < nw; ++w) t += red[w * 2 * D + c];
+    out[c] = t;
   }
 }
 
 // grad_gain[c] += sum_b partial[b][0][c]; grad_bias[c] += sum_b partial[b][1][c].
-// Block of 8 warps per 32 flattened columns: warp w sums partial rows w, w+8, ...
-// (coalesced 128-byte rows), then the 8 warp sums are added in warp order.
-__global__ void __launch_bounds__(256) ln_param_grad_reduce(const float* __restrict__ partial, int nblk,
-                                                            int D, float* __restrict__ ggain,
-                                                            float* __restrict__ gbias) {
-  __shared__ float red[8][32];
+// 1024 threads per 32 flattened columns: warp w sums partial rows w, w+32, ...
+// (coalesced 128-byte rows, all loads of a warp in flight together), then the
+// 32 warp sums are added in warp order.
+__global__ void __launch_bounds__(1024) ln_param_grad_reduce(const float* __restrict__ partial, int nblk, int D,
+                                                             float* __restrict__ ggain, float* __restrict__ gbias) {
+  __shared__ float red[32][33];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.x * 32 + lane;  // flattened [2][D] column
   float s = 0.f;
   if (c < 2 * D) {
-#pragma unroll 4
-    for (int b = warp; b < nblk; b += 8) s += partial[static_cast<long long>(b) * 2 * D + c];
+#pragma unroll 8
+    for (int b = warp; b < nblk; b += 32) s += partial[static_cast<long long>(b) * 2 * D + c];
   }
   red[warp][lane] = s;
   __syncthreads();
   if (warp == 0 && c < 2 * D) {
     float t = 0.f;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) t += red[w][lane];
+    for (int w = 0; w < 32; ++w) t += red[w][lane];
     const int which = c / D, col = c % D;
     float* dst = which ? gbias : ggain;
     if (dst) dst[col] += t;
@@ -319,32 +360,76 @@ __global__ void ce_finalize(const double* __restrict__ partial, int n, double de
 
 using namespace p2r;
 
+namespace {
+bool ln_dim_ok(int d) { return d >= 128 && d <= 2048 && d % 128 == 0; }
+
+constexpr int kLnFwdWarps = 8, kLnBwdWarps = 4;
+constexpr int kSmemPerSM = 227 * 1024;
+constexpr int kLnSmemAttr = 200 * 1024;  // opt-in dynamic limit (leaves room for static smem)
+
+// stages per warp ring (<= 3) and blocks: as many resident blocks as the
+// staging allows, at most 4 per SM (fwd) / 2 per SM (bwd).
+struct LnLaunch {
+  int nst, smem, blocks;
+};
+LnLaunch ln_fwd_launch(int rows, int d) {
+  LnLaunch l{};
+  l.nst = kLnMaxStages;
+  while (l.nst > 1 && 2 * d * 4 + kLnFwdWarps * l.nst * d * 4 > 110 * 1024) --l.nst;
+  l.smem = 2 * d * 4 + kLnFwdWarps * l.nst * d * 4;
+  int per_sm = kSmemPerSM / (l.smem + 1024);
+  per_sm = per_sm < 1 ? 1 : (per_sm > 4 ? 4 : per_sm);
+  const int need = (rows + kLnFwdWarps - 1) / kLnFwdWarps;
+  l.blocks = need < per_sm * kNumSMs ? need : per_sm * kNumSMs;
+  return l;
+}
+LnLaunch ln_bwd_launch(int rows, int d, int ntens) {
+  LnLaunch l{};
+  l.nst = 2;
+  while (l.nst > 1 && d * 4 + kLnBwdWarps * l.nst * ntens * d * 4 > 110 * 1024) --l.nst;
+  const int ring = kLnBwdWarps * l.nst * ntens * d * 4, red = kLnBwdWarps * 2 * d * 4;
+  l.smem = d * 4 + (ring > red ? ring : red);
+  int per_sm = kSmemPerSM / (l.smem + 1024);
+  per_sm = per_sm < 1 ? 1 : (per_sm > 2 ? 2 : per_sm);
+  const int need = (rows + kLnBwdWarps - 1) / kLnBwdWarps;
+  l.blocks = need < per_sm * kNumSMs ? need : per_sm * kNumSMs;
+  return l;
+}
+
+#define P2R_LN_NV_CASES(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16)
+}  // namespace
+
 extern "C" p2r_status p2r_layernorm_fwd(const float* x, const float* gain, const float* bias,
                                         int rows, int d, float eps, void* y_bf16, float* y_f32,
                                         float* mean, float* rstd, void* stream) {
   if (rows <= 0) return P2R_OK;
+  if (!ln_dim_ok(d)) return set_error(P2R_EINVAL, "layernorm: d_model must be a multiple of 128 in [128, 2048]");
+  const LnLaunch l = ln_fwd_launch(rows, d);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int blocks = (rows + 7) / 8;
   auto* y16 = static_cast<__nv_bfloat16*>(y_bf16);
-  switch (d) {
-    case 128: ln_fwd_kernel<1><<<blocks, 256, 0, s>>>(x, gain, bias, rows, eps, y16, y_f32, mean, rstd); break;
-    case 256: ln_fwd_kernel<2><<<blocks, 256, 0, s>>>(x, gain, bias, rows, eps, y16, y_f32, mean, rstd); break;
-    case 512: ln_fwd_kernel<4><<<blocks, 256, 0, s>>>(x, gain, bias, rows, eps, y16, y_f32, mean, rstd); break;
-    case 1024: ln_fwd_kernel<8><<<blocks, 256, 0, s>>>(x, gain, bias, rows, eps, y16, y_f32, mean, rstd); break;
-    case 2048: ln_fwd_kernel<16><<<blocks, 256, 0, s>>>(x, gain, bias, rows, eps, y16, y_f32, mean, rstd); break;
-    default: return set_error(P2R_EINVAL, "layernorm: d_model must be one of 128/256/512/1024/2048");
+  switch (d / 128) {
+#define P2R_LN_FWD(NV)                                                                                     \
+  case NV: {                                                                                               \
+    static cudaError_t a = cudaFuncSetAttribute(ln_fwd_kernel<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                                kLnSmemAttr);                                                \
+    if (a != cudaSuccess) return set_cuda_error(a, "layernorm fwd attr");                                  \
+    ln_fwd_kernel<NV><<<l.blocks, 32 * kLnFwdWarps, l.smem, s>>>(x, gain, bias, rows, eps, y16, y_f32, mean, rstd, \
+                                                                 l.nst);                                    \
+    break;                                                                                                 \
+  }
+    P2R_LN_NV_CASES(P2R_LN_FWD)
+#undef P2R_LN_FWD
+    default: break;
   }
   P2R_CHECK_LAUNCH("layernorm fwd");
   return P2R_OK;
 }
 
-// 16 rows per block (2 per warp): ~512 blocks at T = 8192 keeps every SM busy.
-constexpr int kLnBwdRows = 16;
-
-// partial_ws: >= ceil(rows / rows_per_block) * 2 * d floats
+// partial_ws: >= blocks * 2 * d floats (bwd launch configuration, with residual)
 extern "C" size_t p2r_layernorm_bwd_workspace(int rows, int d) {
-  const int rpb = kLnBwdRows;
-  return static_cast<size_t>((rows + rpb - 1) / rpb) * 2 * d * sizeof(float);
+  if (rows <= 0 || !ln_dim_ok(d)) return 0;
+  const int b2 = ln_bwd_launch(rows, d, 2).blocks, b3 = ln_bwd_launch(rows, d, 3).blocks;
+  return static_cast<size_t>(b2 > b3 ? b2 : b3) * 2 * d * sizeof(float);
 }
 
 extern "C" p2r_status p2r_layernorm_bwd(const float* dy, const float* x, const float* mean,
@@ -352,21 +437,27 @@ extern "C" p2r_status p2r_layernorm_bwd(const float* dy, const float* x, const f
                                         int rows, int d, float* dx, void* dx_bf16, float* ggain,
                                         float* gbias, float* partial_ws, void* stream) {
   if (rows <= 0) return P2R_OK;
+  if (!ln_dim_ok(d)) return set_error(P2R_EINVAL, "layernorm: d_model must be a multiple of 128 in [128, 2048]");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int rpb = kLnBwdRows;
-  const int blocks = (rows + rpb - 1) / rpb;
+  const LnLaunch l = ln_bwd_launch(rows, d, resid ? 3 : 2);
   auto* d16 = static_cast<__nv_bfloat16*>(dx_bf16);
-  switch (d) {
-    case 128: ln_bwd_kernel<1><<<blocks, 256, 0, s>>>(dy, x, mean, rstd, gain, resid, rows, rpb, dx, d16, partial_ws); break;
-    case 256: ln_bwd_kernel<2><<<blocks, 256, 0, s>>>(dy, x, mean, rstd, gain, resid, rows, rpb, dx, d16, partial_ws); break;
-    case 512: ln_bwd_kernel<4><<<blocks, 256, 0, s>>>(dy, x, mean, rstd, gain, resid, rows, rpb, dx, d16, partial_ws); break;
-    case 1024: ln_bwd_kernel<8><<<blocks, 256, 0, s>>>(dy, x, mean, rstd, gain, resid, rows, rpb, dx, d16, partial_ws); break;
-    case 2048: ln_bwd_kernel<16><<<blocks, 256, 0, s>>>(dy, x, mean, rstd, gain, resid, rows, rpb, dx, d16, partial_ws); break;
-    default: return set_error(P2R_EINVAL, "layernorm: d_model must be one of 128/256/512/1024/2048");
+  switch (d / 128) {
+#define P2R_LN_BWD(NV)                                                                                     \
+  case NV: {                                                                                               \
+    static cudaError_t a = cudaFuncSetAttribute(ln_bwd_kernel<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                                kLnSmemAttr);                                                \
+    if (a != cudaSuccess) return set_cuda_error(a, "layernorm bwd attr");                                  \
+    ln_bwd_kernel<NV><<<l.blocks, 32 * kLnBwdWarps, l.smem, s>>>(dy, x, mean, rstd, gain, resid, rows, dx, d16, \
+                                                                 partial_ws, l.nst);                        \
+    break;                                                                                                 \
+  }
+    P2R_LN_NV_CASES(P2R_LN_BWD)
+#undef P2R_LN_BWD
+    default: break;
   }
   P2R_CHECK_LAUNCH("layernorm bwd");
   if (ggain || gbias) {
-    ln_param_grad_reduce<<<(2 * d + 31) / 32, 256, 0, s>>>(partial_ws, blocks, d, ggain, gbias);
+    ln_param_grad_reduce<<<(2 * d + 31) / 32, 1024, 0, s>>>(partial_ws, l.blocks, d, ggain, gbias);
     P2R_CHECK_LAUNCH("layernorm param grad");
   }
   return P2R_OK;

@@ -180,14 +180,25 @@ __global__ void __launch_bounds__(256) colsum_partial_kernel(const T* __restrict
   }
 }
 
-__global__ void colsum_finish_kernel(const float* __restrict__ partial, int nchunks, int n, int groups,
-                                     float* __restrict__ out, long long out_group_stride) {
-  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  if (i >= static_cast<long long>(groups) * n) return;
-  const int g = static_cast<int>(i / n), col = static_cast<int>(i % n);
+// out[g*stride + col] += sum_c partial[g][c][col]: 32 columns x 32 warps per
+// block, warp w adds chunks w, w+32, ...; warp sums combined in warp order.
+__global__ void __launch_bounds__(1024) colsum_finish_kernel(const float* __restrict__ partial, int nchunks, int n,
+                                                             int groups, float* __restrict__ out,
+                                                             long long out_group_stride) {
+  __shared__ float red[32][33];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int col = blockIdx.x * 32 + lane, g = blockIdx.y;
   float s = 0.f;
-  for (int c = 0; c < nchunks; ++c) s += partial[(static_cast<long long>(g) * nchunks + c) * n + col];
-  out[g * out_group_stride + col] += s;
+  if (col < n)
+    for (int c = warp; c < nchunks; c += 32) s += partial[(static_cast<long long>(g) * nchunks + c) * n + col];
+  red[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0 && col < n) {
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < 32; ++w) t += red[w][lane];
+    out[g * out_group_stride + col] += t;
+  }
 }
 
 }  // namespace p2r
@@ -259,8 +270,11 @@ extern "C" p2r_status p2r_delink_broadcast(const void* src, void* dst, size_t by
   return P2R_OK;
 }
 
+// 128-row chunks: ~1000 blocks at T = 8192 keep every SM's loads in flight
+constexpr int kColsumChunk = 128;
+
 extern "C" size_t p2r_colsum_workspace(int rows, int n, int groups) {
-  const int chunk_rows = 512;
+  const int chunk_rows = kColsumChunk;
   return static_cast<size_t>(groups) * ((rows + chunk_rows - 1) / chunk_rows) * n * sizeof(float);
 }
 
@@ -271,7 +285,7 @@ extern "C" p2r_status p2r_bias_grad(const void* x, int dtype, int ld, int rows, 
                                     long long out_group_stride, float* ws, void* stream) {
   if (rows <= 0 || n <= 0) return P2R_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int chunk_rows = 512;
+  const int chunk_rows = kColsumChunk;
   const int span = counts ? seg_rows : rows;
   const int nchunks = (span + chunk_rows - 1) / chunk_rows;
   const int G = counts ? groups : 1;
@@ -284,8 +298,7 @@ extern "C" p2r_status p2r_bias_grad(const void* x, int dtype, int ld, int rows, 
   else
     colsum_partial_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x), ld, rows, n, chunk_rows, seg_rows, counts, ws);
   P2R_CHECK_LAUNCH("bias grad partial");
-  const long long tot = static_cast<long long>(G) * n;
-  colsum_finish_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(ws, nchunks, n, G, out, out_group_stride);
+  colsum_finish_kernel<<<dim3((n + 31) / 32, G), 1024, 0, s>>>(ws, nchunks, n, G, out, out_group_stride);
   P2R_CHECK_LAUNCH("bias grad finish");
   return P2R_OK;
 }

@@ -22,7 +22,7 @@ def bf16_round(a):
     return torch.from_numpy(np.ascontiguousarray(a, np.float32)).bfloat16().float().numpy()
 
 
-@pytest.mark.parametrize("rows,d", [(300, 256), (1024, 1024), (7, 2048), (64, 128)])
+@pytest.mark.parametrize("rows,d", [(300, 256), (1024, 1024), (7, 2048), (64, 128), (301, 384)])
 def test_layernorm(cuda, rows, d):
     import torch
     rng = np.random.default_rng(0)
@@ -44,7 +44,8 @@ def test_layernorm(cuda, rows, d):
     dx16 = torch.empty(rows, d, dtype=torch.bfloat16, device=cuda)
     gg = torch.zeros(d, device=cuda)
     gb = torch.ones(d, device=cuda)  # accumulates (+=)
-    ws = torch.empty(((rows + 15) // 16) * 2 * d, device=cuda)
+    from paper_2110_03888_b200 import _lib
+    ws = torch.empty(_lib.lib().p2r_layernorm_bwd_workspace(rows, d) // 4, device=cuda)
     call("layernorm_bwd", GY, X, mean, rstd, G, R, rows, d, dx, dx16, gg, gb, ws)
     rgx, rgg, rgb = O.layernorm_bwd(gy, xh, inv, gain)
     assert rel(dx.cpu().numpy(), rgx + resid) < 1e-5
@@ -256,7 +257,8 @@ def test_bias_grad(cuda, dtype):
     if dtype == "bf16":
         x = x.bfloat16()
     out = torch.ones(n, device=cuda)
-    ws = torch.empty(((rows + 511) // 512) * n, device=cuda)
+    from paper_2110_03888_b200 import _lib
+    ws = torch.empty(_lib.lib().p2r_colsum_workspace(rows, n, 1) // 4, device=cuda)
     call("bias_grad", x, 0 if dtype == "f32" else 1, n, rows, n, 1, 0, None, out, ctypes.c_longlong(0), ws)
     ref = 1 + x.float().sum(0)
     assert float((out - ref).abs().max() / ref.abs().max()) < 1e-5

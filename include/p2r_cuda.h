@@ -80,8 +80,12 @@ typedef struct {
   int groups;
   int seg_rows;
   const int* counts; /* device [groups] */
-  /* Split-K for plain GEMMs: >1 writes fp32 partials to workspace then reduces. */
+  /* Split-K for plain fp32-output GEMMs: >1 writes fp32 partials to workspace
+   * then reduces in split order; <= 0 lets the library pick (wave fill); 1 = off. */
   int split_k;
+  /* 0 = auto, 1 = one CTA per 128x256 tile, 2 = CTA pair (cluster of 2,
+   * tcgen05 cta_group::2) per 256x256 tile. Pairs apply to ungrouped GEMMs. */
+  int cta_group;
 } p2r_gemm_args;
 
 p2r_status p2r_gemm(const p2r_gemm_args* args, void* stream);
@@ -103,7 +107,7 @@ p2r_status p2r_attention_bwd(const void* qkv, const void* o, const float* lse, c
                              void* stream);
 
 /* ------------------------------------------------------------------------ */
-/* LayerNorm (tensor.cpp:265-336). d in {128,256,512,1024,2048}.             */
+/* LayerNorm (tensor.cpp:265-336). d a multiple of 128 in [128, 2048].        */
 /* ------------------------------------------------------------------------ */
 p2r_status p2r_layernorm_fwd(const float* x, const float* gain, const float* bias, int rows, int d,
                              float eps, void* y_bf16, float* y_f32, float* mean, float* rstd,

@@ -54,6 +54,7 @@ class GemmArgs(ctypes.Structure):
         ("group_mode", ctypes.c_int), ("groups", ctypes.c_int), ("seg_rows", ctypes.c_int),
         ("counts", ctypes.c_void_p),
         ("split_k", ctypes.c_int),
+        ("cta_group", ctypes.c_int),
     ]
 
 

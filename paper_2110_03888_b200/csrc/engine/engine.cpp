@@ -559,7 +559,7 @@ void Model::gemm(int m, int n, int k, const void* a, int lda, bool a_mn, const v
   g.seg_rows = seg_rows;
   g.counts = counts;
   g.split_k = split_k;
-  if (split_k > 1) {
+  if (split_k != 1) {
     const std::size_t need = p2r_gemm_workspace_bytes(&g);
     if (splitk_ws_.bytes < need) splitk_ws_ = DevBuf(need);
     p2r_set_workspace(splitk_ws_.p, splitk_ws_.bytes);
@@ -625,18 +625,6 @@ void Model::buffer(int which, void** ptr, std::size_t* bytes) const {
     throw std::out_of_range("model buffer: unknown buffer id");
   }
 }
-
-namespace {
-// split-K only when the output tile count leaves most SMs idle
-int pick_split(int m, int n, int k) {
-  const int bn = n <= 128 ? 128 : 256;
-  const int tiles = ((m + 127) / 128) * ((n + bn - 1) / bn);
-  if (tiles >= 74) return 1;
-  int s = 148 / std::max(1, tiles);
-  s = std::min(s, std::max(1, k / 1024));
-  return std::max(1, std::min(s, 4));
-}
-}  // namespace
 
 // ---------------------------------------------------------------- forward pieces
 Tensor Model::embed_forward(GradTape* tape, const int* d_tokens, int batch, int seq) {
@@ -758,7 +746,7 @@ void Model::block_backward(int g, AttentionMode mode) {
   if (!cfg_.moe.enabled()) {
     // FFN2: dW2 += g^T dy ; db2 += colsum(dy) ; dh = (dy W2^T) * gelu'(hpre)
     gemm(dff, d, T, L.g16.p, dff, true, dy16, d, true, P2R_EPI_ACC_F32, lg(o, layer_.w2), d, nullptr, 0, nullptr,
-         nullptr, 0, 0, 0, 0, nullptr, pick_split(dff, d, T));
+         nullptr, 0, 0, 0, 0, nullptr, 0 /* library picks the split */);
     prof(P2R_PROF_BIAS, 0, 4.0 * T * d, [&] {
       p2r_check(p2r_bias_grad(dy, 0, d, T, d, 1, 0, nullptr, lg(o, layer_.b2), 0, A.colsum_ws.as<float>(), stream_),
                 "db2");
@@ -767,7 +755,7 @@ void Model::block_backward(int g, AttentionMode mode) {
          L.hpre16.p, dff);
     // FFN1: dW1 += b^T dh ; db1 += colsum(dh) ; db = dh W1^T
     gemm(d, dff, T, L.b16.p, d, true, A.dh16.p, dff, true, P2R_EPI_ACC_F32, lg(o, layer_.w1), dff, nullptr, 0,
-         nullptr, nullptr, 0, 0, 0, 0, nullptr, pick_split(d, dff, T));
+         nullptr, nullptr, 0, 0, 0, 0, nullptr, 0 /* library picks the split */);
     prof(P2R_PROF_BIAS, 0, 2.0 * T * dff, [&] {
       p2r_check(p2r_bias_grad(A.dh16.p, 1, dff, T, dff, 1, 0, nullptr, lg(o, layer_.b1), 0, A.colsum_ws.as<float>(),
                               stream_),
@@ -828,7 +816,7 @@ void Model::block_backward(int g, AttentionMode mode) {
   });
   // O projection: dWo += o^T dx1 ; do = dx1 Wo^T
   gemm(d, d, T, L.o16.p, d, true, A.dx1_16.p, d, true, P2R_EPI_ACC_F32, lg(o, layer_.wo), d, nullptr, 0, nullptr,
-       nullptr, 0, 0, 0, 0, nullptr, pick_split(d, d, T));
+       nullptr, 0, 0, 0, 0, nullptr, 0 /* library picks the split */);
   gemm(T, d, d, A.dx1_16.p, d, false, lp16(o, layer_.wo), d, false, P2R_EPI_BF16, A.do16.p, d);
   prof(P2R_PROF_ATTN_BWD, attn_flops, Td * 16, [&] {
     p2r_check(p2r_attention_bwd(L.qkv16.p, L.o16.p, L.lse.as<float>(), A.do16.p, A.dsum.as<float>(), A.dqkv16.p,
@@ -837,7 +825,7 @@ void Model::block_backward(int g, AttentionMode mode) {
   });
   // QKV: dWqkv += a^T dqkv ; da = dqkv Wqkv^T
   gemm(d, 3 * d, T, L.a16.p, d, true, A.dqkv16.p, 3 * d, true, P2R_EPI_ACC_F32, lg(o, layer_.wqkv), 3 * d, nullptr,
-       0, nullptr, nullptr, 0, 0, 0, 0, nullptr, pick_split(d, 3 * d, T));
+       0, nullptr, nullptr, 0, 0, 0, 0, nullptr, 0 /* library picks the split */);
   gemm(T, d, 3 * d, A.dqkv16.p, 3 * d, false, lp16(o, layer_.wqkv), 3 * d, false, P2R_EPI_F32, A.tmp32.p, d);
   // LN1 backward: dx = dx1 + LN1'(da)
   prof(P2R_PROF_LAYERNORM, 0, Td * 18, [&] {
@@ -866,7 +854,7 @@ Tensor Model::head_forward(GradTape* tape, const Tensor& x) {
       const int T2 = A2.T, d2 = cfg_.d_model, V2 = cfg_.vocab_size;
       // dtok += dlogits^T h ; dh = dlogits . tok
       gemm(V2, d2, T2, A2.dlogits16.p, A2.vld, true, A2.h16.p, d2, true, P2R_EPI_ACC_F32, eg(emb_.tok), d2, nullptr,
-           0, nullptr, nullptr, 0, 0, 0, 0, nullptr, pick_split(V2, d2, T2));
+           0, nullptr, nullptr, 0, 0, 0, 0, nullptr, 0 /* library picks the split */);
       gemm(T2, d2, V2, A2.dlogits16.p, A2.vld, false, ep16(emb_.tok), d2, true, P2R_EPI_F32, A2.dh32.p, d2);
       prof(P2R_PROF_LAYERNORM, 0, 14.0 * T2 * d2, [&] {
         p2r_check(p2r_layernorm_bwd(A2.dh32.as<float>(), xin, A2.meanf.as<float>(), A2.rstdf.as<float>(),

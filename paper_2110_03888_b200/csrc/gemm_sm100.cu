@@ -18,6 +18,7 @@
 
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <type_traits>
@@ -54,15 +55,18 @@ struct GemmParams {
 struct Tile {
   bool valid;
   int m_blk, n_blk;
-  int a_row;    // K-major A: first row (m)
+  int a_row;    // first m row of this CTA's A slice (K-major: tensor row; MN-major: column)
   int b_row;    // K-major B: first row (n)
+  int b_col;    // MN-major B: first column (n) of this CTA's B slice
   int kbase;    // MN-major operands: first K row
   int kb0, kb1; // k-block range
   int g;
   int ks;
 };
 
-P2R_DEVICE Tile get_tile(const GemmParams& p, int t, int BN) {
+// CG = CTAs per tile (2: CTA pair, 256-row tile; rank picks the CTA's 128-row
+// A slice and its BN/2-row B slice). Grouped modes run with CG = 1.
+P2R_DEVICE Tile get_tile(const GemmParams& p, int t, int BN, int CG = 1, int rank = 0) {
   Tile T;
   T.valid = true;
   T.g = 0;
@@ -78,6 +82,7 @@ P2R_DEVICE Tile get_tile(const GemmParams& p, int t, int BN) {
     T.valid = T.m_blk * BM < cnt;
     T.a_row = T.g * p.seg_rows + T.m_blk * BM;
     T.b_row = T.g * p.n + T.n_blk * BN;
+    T.b_col = T.n_blk * BN;
     T.kbase = T.g * p.k;  // MN-major B: stacked [groups*k, n]
     T.kb0 = 0;
     T.kb1 = p.num_k_blk;
@@ -91,6 +96,7 @@ P2R_DEVICE Tile get_tile(const GemmParams& p, int t, int BN) {
     T.valid = cnt > 0;
     T.a_row = T.m_blk * BM;
     T.b_row = T.n_blk * BN;
+    T.b_col = T.n_blk * BN;
     T.kbase = T.g * p.seg_rows;
     T.kb0 = 0;
     T.kb1 = (cnt + BK - 1) / BK;
@@ -100,8 +106,9 @@ P2R_DEVICE Tile get_tile(const GemmParams& p, int t, int BN) {
     const int r = t - T.ks * per_s;
     T.n_blk = r / p.num_m_blk;
     T.m_blk = r - T.n_blk * p.num_m_blk;
-    T.a_row = T.m_blk * BM;
-    T.b_row = T.n_blk * BN;
+    T.a_row = T.m_blk * BM * CG + rank * BM;
+    T.b_row = T.n_blk * BN + rank * (BN / CG);
+    T.b_col = T.b_row;
     T.kbase = 0;
     T.kb0 = static_cast<int>((static_cast<long long>(T.ks) * p.num_k_blk) / p.split_k);
     T.kb1 = static_cast<int>((static_cast<long long>(T.ks + 1) * p.num_k_blk) / p.split_k);
@@ -110,10 +117,10 @@ P2R_DEVICE Tile get_tile(const GemmParams& p, int t, int BN) {
   return T;
 }
 
-template <int BN>
+template <int BN, int CG = 1>
 struct GemmCfg {
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_BYTES = (BN / CG) * BK * 2;  // a pair splits B's rows between its CTAs
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (196608 / STAGE_BYTES) > 8 ? 8 : (196608 / STAGE_BYTES);
   static constexpr int TMEM_COLS = (2 * BN) < 32 ? 32 : (2 * BN);
@@ -307,11 +314,12 @@ P2R_DEVICE void epi_store_fast(const GemmParams& p, float4 v, typename EpiOperan
 constexpr int kEpiWarps = 8;                       // 2 per TMEM lane quadrant
 constexpr int kGemmThreads = 128 + 32 * kEpiWarps;  // 4 control warps + epilogue
 
-template <int BN, bool A_MN, bool B_MN, int EPI>
+template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const GemmParams p) {
-  using Cfg = GemmCfg<BN>;
+  using Cfg = GemmCfg<BN, CG>;
+  constexpr int BNC = BN / CG;  // B rows (N) this CTA loads per stage
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -324,6 +332,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  // CTA pair: rank 0 (leader) issues the MMAs; tiles are indexed per pair.
+  const int rank = CG == 2 ? static_cast<int>(cluster_ctarank()) : 0;
+  const bool leader = rank == 0;
+  const int tile0 = blockIdx.x / CG, tile_step = gridDim.x / CG;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -334,13 +346,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(tfull_bar + s, 1);
-      mbar_init(tempty_bar + s, 32 * kEpiWarps);
+      // pair: one arrive per epilogue warp of both CTAs, on the leader's barrier
+      mbar_init(tempty_bar + s, CG == 2 ? 2 * kEpiWarps : 32 * kEpiWarps);
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  if (warp == 2) {
+    if constexpr (CG == 2)
+      tmem_alloc_pair(tmem_slot, Cfg::TMEM_COLS);
+    else
+      tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2)
+    cluster_sync();  // both CTAs' barriers initialised before any cross-CTA signal
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -349,29 +370,32 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // ---------------- TMA producer ----------------
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < p.tiles_total; t += gridDim.x) {
-        const Tile T = get_tile(p, t, BN);
+      for (int t = tile0; t < p.tiles_total; t += tile_step) {
+        const Tile T = get_tile(p, t, BN, CG, rank);
         if (!T.valid) continue;
         for (int kb = T.kb0; kb < T.kb1; ++kb) {
           mbar_wait(empty_bar + stage, phase ^ 1);
           uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
           uint8_t* sb = sa + Cfg::A_BYTES;
-          mbar_arrive_expect_tx(full_bar + stage, Cfg::STAGE_BYTES);
+          // pair: the leader expects both CTAs' bytes; each CTA's loads count on it
+          if (leader) mbar_arrive_expect_tx(full_bar + stage, CG * Cfg::STAGE_BYTES);
+          auto load = [&](void* dst, const CUtensorMap* map, int c0, int c1) {
+            if constexpr (CG == 2)
+              tma_load_2d_pair(dst, map, pair_leader_addr(full_bar + stage), c0, c1);
+            else
+              tma_load_2d(dst, map, full_bar + stage, c0, c1);
+          };
           if (!A_MN) {
-            tma_load_2d(sa, &tmA, full_bar + stage, kb * BK, T.a_row);
+            load(sa, &tmA, kb * BK, T.a_row);
           } else {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j)
-              tma_load_2d(sa + j * 64 * BK * 2, &tmA, full_bar + stage, T.m_blk * BM + 64 * j,
-                          T.kbase + kb * BK);
+            for (int j = 0; j < BM / 64; ++j) load(sa + j * 64 * BK * 2, &tmA, T.a_row + 64 * j, T.kbase + kb * BK);
           }
           if (!B_MN) {
-            tma_load_2d(sb, &tmB, full_bar + stage, kb * BK, T.b_row);
+            load(sb, &tmB, kb * BK, T.b_row);
           } else {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j)
-              tma_load_2d(sb + j * 64 * BK * 2, &tmB, full_bar + stage, T.n_blk * BN + 64 * j,
-                          T.kbase + kb * BK);
+            for (int j = 0; j < BNC / 64; ++j) load(sb + j * 64 * BK * 2, &tmB, T.b_col + 64 * j, T.kbase + kb * BK);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -381,15 +405,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer ----------------
-      constexpr uint32_t idesc = make_idesc_bf16(BM, BN, A_MN, B_MN);
+    if (lane == 0 && leader) {
+      // ---------------- MMA issuer (pair: leader only, M = 256) ----------------
+      constexpr uint32_t idesc = make_idesc_bf16(BM * CG, BN, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < p.tiles_total; t += gridDim.x) {
-        const Tile T = get_tile(p, t, BN);
+      for (int t = tile0; t < p.tiles_total; t += tile_step) {
+        const Tile T = get_tile(p, t, BN, CG, rank);
         if (!T.valid) continue;
         mbar_wait(tempty_bar + acc, acc_phase ^ 1);
         tc_fence_after();
@@ -407,15 +431,25 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                                      : make_sw128_desc(sa + kk * 32, 16, 1024);
             const uint64_t bd = B_MN ? make_sw128_desc(sb + kk * 2048, 64 * BK * 2, 1024)
                                      : make_sw128_desc(sb + kk * 32, 16, 1024);
-            umma_bf16(d_tmem, ad, bd, idesc, (kb > T.kb0 || kk > 0) ? 1u : 0u);
+            static_assert(!B_MN || BNC >= 64, "MN-major B slice must hold whole 64-column atoms");
+            if constexpr (CG == 2)
+              umma_bf16_pair(d_tmem, ad, bd, idesc, (kb > T.kb0 || kk > 0) ? 1u : 0u);
+            else
+              umma_bf16(d_tmem, ad, bd, idesc, (kb > T.kb0 || kk > 0) ? 1u : 0u);
           }
-          umma_commit(empty_bar + stage);
+          if constexpr (CG == 2)
+            umma_commit_pair(empty_bar + stage);
+          else
+            umma_commit(empty_bar + stage);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(tfull_bar + acc);
+        if constexpr (CG == 2)
+          umma_commit_pair(tfull_bar + acc);
+        else
+          umma_commit(tfull_bar + acc);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -430,12 +464,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     float* stg = reinterpret_cast<float*>(tmem_slot + 4) + (warp - 4) * 1024;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < p.tiles_total; t += gridDim.x) {
-      const Tile T = get_tile(p, t, BN);
+    for (int t = tile0; t < p.tiles_total; t += tile_step) {
+      const Tile T = get_tile(p, t, BN, CG, rank);
       if (!T.valid) continue;
       mbar_wait(tfull_bar + acc, acc_phase);
       tc_fence_after();
-      const int row0 = T.m_blk * BM + ew * 32;  // first local row drained by this warp
+      const int row0 = T.m_blk * BM * CG + rank * BM + ew * 32;  // first local row drained by this warp
       long long grow0 = row0;
       int row_lim, zero_from = 1 << 30;
       char* cbase = reinterpret_cast<char*>(p.c);
@@ -507,7 +541,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         __syncwarp();
       }
       tc_fence_before();
-      mbar_arrive(tempty_bar + acc);
+      if constexpr (CG == 2) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty_bar + acc, 0);  // the leader's barrier
+      } else {
+        mbar_arrive(tempty_bar + acc);
+      }
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -515,10 +554,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2)
+    cluster_sync();  // no CTA leaves while its peer may still signal or read it
+  else
+    __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+    if constexpr (CG == 2)
+      tmem_dealloc_pair(tmem_base, Cfg::TMEM_COLS);
+    else
+      tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
   }
 }
 
@@ -593,50 +638,101 @@ bool make_map(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, u
 void* g_ws = nullptr;
 size_t g_ws_bytes = 0;
 
-template <int BN, bool AMN, bool BMN, int EPI>
+template <int BN, bool AMN, bool BMN, int EPI, int CG>
 cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
                    cudaStream_t s) {
-  using Cfg = GemmCfg<BN>;
+  using Cfg = GemmCfg<BN, CG>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(gemm_kernel<BN, AMN, BMN, EPI>,
+    attr_err = cudaFuncSetAttribute(gemm_kernel<BN, AMN, BMN, EPI, CG>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
   });
   if (attr_err != cudaSuccess) return attr_err;
-  const int grid = p.tiles_total < kNumSMs ? p.tiles_total : kNumSMs;
-  gemm_kernel<BN, AMN, BMN, EPI><<<grid, kGemmThreads, Cfg::SMEM_BYTES, s>>>(ta, tb, p);
+  const int units = kNumSMs / CG;  // persistent: one CTA (pair) per SM (pair of SMs)
+  const int grid = CG * (p.tiles_total < units ? p.tiles_total : units);
+  if constexpr (CG == 1) {
+    gemm_kernel<BN, AMN, BMN, EPI, 1><<<grid, kGemmThreads, Cfg::SMEM_BYTES, s>>>(ta, tb, p);
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kGemmThreads);
+    cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_kernel<BN, AMN, BMN, EPI, 2>, ta, tb, p);
+    if (e != cudaSuccess) return e;
+  }
   count_launch();
   return cudaGetLastError();
 }
 
-template <int BN, bool AMN, bool BMN>
+template <int BN, bool AMN, bool BMN, int CG>
 cudaError_t dispatch_epi(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, cudaStream_t s) {
   switch (p.epi) {
-    case P2R_EPI_BF16: return launch<BN, AMN, BMN, P2R_EPI_BF16>(ta, tb, p, s);
-    case P2R_EPI_F32: return launch<BN, AMN, BMN, P2R_EPI_F32>(ta, tb, p, s);
-    case P2R_EPI_ACC_F32: return launch<BN, AMN, BMN, P2R_EPI_ACC_F32>(ta, tb, p, s);
-    case P2R_EPI_BIAS_GELU: return launch<BN, AMN, BMN, P2R_EPI_BIAS_GELU>(ta, tb, p, s);
-    case P2R_EPI_DGELU: return launch<BN, AMN, BMN, P2R_EPI_DGELU>(ta, tb, p, s);
-    default: return launch<BN, AMN, BMN, P2R_EPI_F32_BF16>(ta, tb, p, s);
+    case P2R_EPI_BF16: return launch<BN, AMN, BMN, P2R_EPI_BF16, CG>(ta, tb, p, s);
+    case P2R_EPI_F32: return launch<BN, AMN, BMN, P2R_EPI_F32, CG>(ta, tb, p, s);
+    case P2R_EPI_ACC_F32: return launch<BN, AMN, BMN, P2R_EPI_ACC_F32, CG>(ta, tb, p, s);
+    case P2R_EPI_BIAS_GELU: return launch<BN, AMN, BMN, P2R_EPI_BIAS_GELU, CG>(ta, tb, p, s);
+    case P2R_EPI_DGELU: return launch<BN, AMN, BMN, P2R_EPI_DGELU, CG>(ta, tb, p, s);
+    default: return launch<BN, AMN, BMN, P2R_EPI_F32_BF16, CG>(ta, tb, p, s);
   }
 }
 
-template <int BN>
+template <int BN, int CG>
 cudaError_t dispatch_majors(bool amn, bool bmn, const CUtensorMap& ta, const CUtensorMap& tb,
                             const GemmParams& p, cudaStream_t s) {
-  if (!amn && !bmn) return dispatch_epi<BN, false, false>(ta, tb, p, s);
-  if (!amn && bmn) return dispatch_epi<BN, false, true>(ta, tb, p, s);
-  if (amn && !bmn) return dispatch_epi<BN, true, false>(ta, tb, p, s);
-  return dispatch_epi<BN, true, true>(ta, tb, p, s);
+  if (!amn && !bmn) return dispatch_epi<BN, false, false, CG>(ta, tb, p, s);
+  if (!amn && bmn) return dispatch_epi<BN, false, true, CG>(ta, tb, p, s);
+  if (amn && !bmn) return dispatch_epi<BN, true, false, CG>(ta, tb, p, s);
+  return dispatch_epi<BN, true, true, CG>(ta, tb, p, s);
+}
+
+// CTA pairs for ungrouped 256-wide tiles unless the caller or P2R_GEMM_CG=1 says otherwise.
+int pick_cg(const p2r_gemm_args* a, int BN) {
+  if (a->group_mode != P2R_GROUP_NONE || BN != 256) return 1;
+  if (a->cta_group == 1 || a->cta_group == 2) return a->cta_group;
+  static const bool force1 = [] {
+    const char* e = std::getenv("P2R_GEMM_CG");
+    return e != nullptr && e[0] == '1';
+  }();
+  return force1 ? 1 : 2;
 }
 
 int pick_bn(const p2r_gemm_args* a) { return a->n <= 128 ? 128 : 256; }
 
+int pick_cg(const p2r_gemm_args* a, int BN);
+
+// split_k <= 0: choose the split (1..4) that best fills the persistent grid's
+// waves; a split must beat one pass by > 10 points of wave efficiency to pay
+// for its fp32 partials and the reduction.
+int auto_split(const p2r_gemm_args* a) {
+  if (a->epi != P2R_EPI_ACC_F32 && a->epi != P2R_EPI_F32) return 1;
+  if (a->bias != nullptr || a->aux != nullptr) return 1;
+  const int BN = pick_bn(a), CG = pick_cg(a, BN);
+  const long long tiles = 1LL * ((a->m + BM * CG - 1) / (BM * CG)) * ((a->n + BN - 1) / BN);
+  const int units = kNumSMs / CG;
+  auto eff = [&](int s) {
+    const long long t = tiles * s;
+    return static_cast<double>(t) / (static_cast<double>(units) * ((t + units - 1) / units));
+  };
+  int best = 1;
+  for (int s = 2; s <= 4; ++s)
+    if ((a->k / BK) / s >= 8 && eff(s) > eff(best) + 0.10) best = s;
+  return best;
+}
+
 int effective_split(const p2r_gemm_args* a) {
-  if (a->group_mode != P2R_GROUP_NONE || a->split_k <= 1) return 1;
+  if (a->group_mode != P2R_GROUP_NONE || a->split_k == 1) return 1;
+  const int req = a->split_k <= 0 ? auto_split(a) : a->split_k;
   const int nkb = (a->k + BK - 1) / BK;
-  int s = a->split_k < nkb ? a->split_k : nkb;
+  int s = req < nkb ? req : nkb;
   return s < 1 ? 1 : s;
 }
 
@@ -679,12 +775,15 @@ extern "C" p2r_status p2r_gemm(const p2r_gemm_args* a, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int BN = pick_bn(a);
   const int split = effective_split(a);
+  if (a->cta_group == 2 && (a->group_mode != P2R_GROUP_NONE || BN != 256))
+    return set_error(P2R_EINVAL, "gemm: CTA pairs need an ungrouped GEMM with n > 128");
+  const int CG = pick_cg(a, BN);
 
   GemmParams p{};
   p.m = a->m;
   p.n = a->n;
   p.k = a->k;
-  p.num_m_blk = (a->m + BM - 1) / BM;
+  p.num_m_blk = (a->m + BM * CG - 1) / (BM * CG);
   p.num_n_blk = (a->n + BN - 1) / BN;
   p.num_k_blk = (a->k + BK - 1) / BK;
   p.epi = a->epi;
@@ -734,11 +833,12 @@ extern "C" p2r_status p2r_gemm(const p2r_gemm_args* a, void* stream) {
                           : make_map(&ta, a->a, a_rows_k, a->k, a->lda, 64, BM);
   const long long b_rows_mn = a->group_mode == P2R_GROUP_M ? 1LL * a->groups * a->k : a_rows_mn;
   ok = ok && (a->b_mn_major ? make_map(&tb, a->b, b_rows_mn, a->n, a->ldb, 64, 64)
-                            : make_map(&tb, a->b, b_rows_k, a->k, a->ldb, 64, BN));
+                            : make_map(&tb, a->b, b_rows_k, a->k, a->ldb, 64, BN / CG));
   if (!ok) return set_error(P2R_ECUDA, "gemm: cuTensorMapEncodeTiled failed");
 
-  cudaError_t e = BN == 128 ? dispatch_majors<128>(a->a_mn_major, a->b_mn_major, ta, tb, p, s)
-                            : dispatch_majors<256>(a->a_mn_major, a->b_mn_major, ta, tb, p, s);
+  cudaError_t e = BN == 128 ? dispatch_majors<128, 1>(a->a_mn_major, a->b_mn_major, ta, tb, p, s)
+                 : CG == 2  ? dispatch_majors<256, 2>(a->a_mn_major, a->b_mn_major, ta, tb, p, s)
+                            : dispatch_majors<256, 1>(a->a_mn_major, a->b_mn_major, ta, tb, p, s);
   if (e != cudaSuccess) return set_cuda_error(e, "gemm launch");
   if (split > 1) {
     splitk_reduce_kernel<<<a->m, 256, 0, s>>>(static_cast<float*>(a->c), a->ldc,

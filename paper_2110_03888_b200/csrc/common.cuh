@@ -230,41 +230,37 @@ __host__ __device__ constexpr uint32_t make_idesc_bf16(int M, int N, bool a_mn, 
 // ----------------------------------------------------------------------------
 // numerics shared by several kernels (exact-erf GELU, tensor.cpp:237-263)
 // ----------------------------------------------------------------------------
-// Exact (erf) GELU from one exp2: for z = |x|/sqrt(2), erfc(z) = e^{-z^2} t h(t)
-// with t = 1/(1 + z/2) and h a degree-10 least-squares fit of erfcx(z)/t on
-// t in (0,1] (max rel. error 4e-8 in float64). Phi(x) = 1 - erfc/2 (x >= 0) or
-// erfc/2, phi(x) = e^{-x^2/2}/sqrt(2 pi) shares the exponential. Absolute error
-// of gelu / gelu' vs float64 erf < 4e-7 over all x (the erff/expf pair costs
-// ~2x the instructions and selects between two evaluated branches).
-P2R_DEVICE void gelu_cdf_pdf(float x, float& cdf, float& pdf) {
-  const float z = fabsf(x) * 0.70710678118654752f;
-  const float t = __fdividef(1.0f, fmaf(0.5f, z, 1.0f));
-  float e;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-(z * z) * 1.4426950408889634f));
-  float h = 4.442954063e-02f;
-  h = fmaf(h, t, -2.408180535e-01f);
-  h = fmaf(h, t, 5.064800382e-01f);
-  h = fmaf(h, t, -4.699109793e-01f);
-  h = fmaf(h, t, 1.427917480e-01f);
-  h = fmaf(h, t, -6.392780691e-02f);
-  h = fmaf(h, t, 9.475959092e-02f);
-  h = fmaf(h, t, 1.751051098e-01f);
-  h = fmaf(h, t, 2.469029576e-01f);
-  h = fmaf(h, t, 2.820930481e-01f);
-  h = fmaf(h, t, 2.820948064e-01f);
-  const float half_erfc = 0.5f * t * h * e;
+// Exact (erf) GELU from one exp2: for z = |x|/sqrt(2), erfc(z)/2 = e t h(t) with
+// e = exp(-x^2/2), t = 1/(1 + z/2) and h a degree-8 least-squares fit of
+// erfcx(z)/(2t) on t in (0,1] (constants pre-folded). Phi(x) = 1 - erfc/2
+// (x >= 0) or erfc/2; phi(x) = e / sqrt(2 pi) shares the exponential.
+// |error| vs float64 erf: gelu < 4e-7, gelu' < 4e-7 (outputs are bf16-rounded);
+// ~21 instructions, versus ~2x for the erff/expf pair.
+P2R_DEVICE void gelu_cdf_exp(float x, float& cdf, float& e) {
+  float t;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(fmaf(fabsf(x), 0.35355339059327373f, 1.0f)));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"((x * -0.72134752044448170f) * x));
+  float h = -2.377655916e-02f;
+  h = fmaf(h, t, 1.178763658e-01f);
+  h = fmaf(h, t, -2.006432861e-01f);
+  h = fmaf(h, t, 9.842023998e-02f);
+  h = fmaf(h, t, 8.996849880e-03f);
+  h = fmaf(h, t, 9.415699542e-02f);
+  h = fmaf(h, t, 1.228528991e-01f);
+  h = fmaf(h, t, 1.410695761e-01f);
+  h = fmaf(h, t, 1.410471797e-01f);
+  const float half_erfc = t * h * e;
   cdf = x >= 0.0f ? 1.0f - half_erfc : half_erfc;
-  pdf = e * 0.39894228040143268f;
 }
 P2R_DEVICE float gelu_f(float v) {
-  float cdf, pdf;
-  gelu_cdf_pdf(v, cdf, pdf);
+  float cdf, e;
+  gelu_cdf_exp(v, cdf, e);
   return v * cdf;
 }
 P2R_DEVICE float gelu_grad_f(float v) {
-  float cdf, pdf;
-  gelu_cdf_pdf(v, cdf, pdf);
-  return fmaf(v, pdf, cdf);
+  float cdf, e;
+  gelu_cdf_exp(v, cdf, e);
+  return fmaf(v * 0.39894228040143268f, e, cdf);
 }
 
 P2R_DEVICE float warp_sum(float v) {

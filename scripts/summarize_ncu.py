@@ -1,6 +1,6 @@
 """Summarise ncu output (launch list CSV + a --set full report) into profiles/.
 
-  python scripts/summarize_ncu.py <launches.csv> <full.ncu-rep> <tag>
+  python scripts/summarize_ncu.py <launches.csv> <full.ncu-rep[,more.ncu-rep]> <tag>
 
 Writes profiles/<tag>_launches.md (per-kernel share of device time from the
 serialized, cold-cache launch list), profiles/<tag>_gemm_full.md (per-launch DRAM
@@ -73,14 +73,21 @@ def main():
     per = launches(lpath)
     tot = sum(v[1] for v in per.values())
     lines = [f"# {tag}: ncu launch list (gpu__time_duration.sum, --clock-control none)", "",
-             f"Source: `ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 python bench.py --steps 2 --warmup 1`",
+             f"Source: `ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 python bench.py --steps 2 --warmup 3 --no-cpu-baseline`",
              "(serialised, cold-cache per launch: compare SHARES with bench.py's live `kernels` breakdown, not absolutes).", "",
              "| kernel | launches | total ms | share |", "|---|---|---|---|"]
     for k, (n, ns) in sorted(per.items(), key=lambda a: -a[1][1]):
         lines.append(f"| `{k}` | {n} | {ns / 1e6:.3f} | {ns / tot:.3f} |")
     open(os.path.join(prof, f"{tag}_launches.md"), "w").write("\n".join(lines) + "\n")
-    res, units = full_report(fpath)
+    res, units = [], {}
+    for fp in fpath.split(","):
+        r, u = full_report(fp)
+        res += r
+        units.update(u)
     lines = [f"# {tag}: ncu --set full on GEMM launches inside one bench step", "",
+             "Captures: `ncu --set full --clock-control none -k regex:gemm_kernel --launch-skip 291 -c 4` (layer-0 forward:",
+             "QKV, O-proj, FFN1, FFN2) and `--launch-skip 390 -c 10` (head + last-layer backward GEMMs) of",
+             "`python bench.py --steps 2 --warmup 3 --no-cpu-baseline`.", "",
              "| # | kernel | grid | duration | DRAM read | DRAM write | tensor pipe % of peak |", "|---|---|---|---|---|---|---|"]
     traffic = []
     for i, d in enumerate(res):

@@ -154,6 +154,8 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();  // dkdv reads the dq kernel's D (dsum)
   const uint32_t sb = smem_u32(smem);
   if (threadIdx.x == 0) TR(1);
 
@@ -370,6 +372,8 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();  // dkdv reads the dq kernel's D (dsum)
   const uint32_t sb = smem_u32(smem);
 
   if (warp == 0) {
@@ -563,10 +567,11 @@ p2r_status run(const void* qkv, const BwdParams& p, cudaStream_t s) {
   static cudaError_t a1 = cudaFuncSetAttribute(attn_bwd_dq_tc<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, DqCfg<HD>::SMEM);
   static cudaError_t a2 = cudaFuncSetAttribute(attn_bwd_dkdv_tc<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, KvCfg<HD>::SMEM);
   if (a1 != cudaSuccess || a2 != cudaSuccess) return set_cuda_error(a1 ? a1 : a2, "attention bwd attr");
-  attn_bwd_dq_tc<HD><<<dim3((p.S + 127) / 128, p.H, p.B), 384, DqCfg<HD>::SMEM, s>>>(qkv128, qkv64, do128, p);
-  P2R_CHECK_LAUNCH("attention bwd dq (tcgen05)");
-  attn_bwd_dkdv_tc<HD><<<dim3((p.S + 127) / 128, p.H, p.B), 384, KvCfg<HD>::SMEM, s>>>(qkv128, qkv64, do64, p);
-  P2R_CHECK_LAUNCH("attention bwd dkdv (tcgen05)");
+  const dim3 grid((p.S + 127) / 128, p.H, p.B);
+  P2R_LAUNCH_K("attention bwd dq (tcgen05)", attn_bwd_dq_tc<HD>, grid, dim3(384), DqCfg<HD>::SMEM, s, 1, qkv128,
+               qkv64, do128, p);
+  P2R_LAUNCH_K("attention bwd dkdv (tcgen05)", attn_bwd_dkdv_tc<HD>, grid, dim3(384), KvCfg<HD>::SMEM, s, 1, qkv128,
+               qkv64, do64, p);
   return P2R_OK;
 }
 

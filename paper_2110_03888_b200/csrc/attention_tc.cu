@@ -117,6 +117,8 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();
   const uint32_t sbase = smem_u32(smem);
 
   if (warp == 0) {
@@ -327,8 +329,7 @@ p2r_status run(const void* qkv, const FwdParams& p, cudaStream_t s) {
   static cudaError_t attr = cudaFuncSetAttribute(attn_fwd_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   if (attr != cudaSuccess) return set_cuda_error(attr, "attention tc attr");
   dim3 grid((p.S + BQ - 1) / BQ, p.H, p.B);
-  attn_fwd_tc_kernel<HD><<<grid, 256, C::SMEM, s>>>(tm, p);
-  P2R_CHECK_LAUNCH("attention fwd (tcgen05)");
+  P2R_LAUNCH_K("attention fwd (tcgen05)", attn_fwd_tc_kernel<HD>, grid, dim3(256), C::SMEM, s, 1, tm, p);
   return P2R_OK;
 }
 

@@ -34,6 +34,16 @@ P2R_DEVICE void sts32f(uint32_t addr, float v) {
 }
 
 // ----------------------------------------------------------------------------
+// Programmatic dependent launch. Kernels launched through p2r::launch_k (PDL
+// attribute set) run their dependency-free setup, then pdl_wait() before the
+// first global read of anything an earlier kernel in the stream may write.
+// pdl_trigger() lets the next grid be scheduled once every CTA of this grid has
+// issued it (its CTAs then take SMs as soon as ours exit).
+// ----------------------------------------------------------------------------
+P2R_DEVICE void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+P2R_DEVICE void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// ----------------------------------------------------------------------------
 // mbarrier
 // ----------------------------------------------------------------------------
 P2R_DEVICE void mbar_init(uint64_t* bar, uint32_t count) {
@@ -177,12 +187,15 @@ P2R_DEVICE void umma_commit_pair(uint64_t* bar) {
       : "memory");
 }
 // Arrive on the barrier at the same offset in CTA `rank` of the cluster.
+// Relaxed: the only ordering needed is of prior tcgen05 ops (tcgen05.fence::
+// before_thread_sync supplies it). A .release.cluster arrive compiles to
+// MEMBAR.ALL.GPU and would hold the TMEM slot until the warp's global stores land.
 P2R_DEVICE void mbar_arrive_cluster(uint64_t* bar, uint32_t rank) {
   asm volatile(
       "{\n"
       ".reg .b32 ra;\n"
       "mapa.shared::cluster.u32 ra, %0, %1;\n"
-      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n"
+      "mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [ra];\n"
       "}\n" ::"r"(smem_u32(bar)),
       "r"(rank)
       : "memory");

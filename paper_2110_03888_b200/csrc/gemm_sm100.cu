@@ -50,6 +50,7 @@ struct GemmParams {
   int tiles_total;
   long long c_split_stride;  // elements between split-K partial outputs
   int vec4;                  // all epilogue leading dims / bases allow 4-wide accesses
+  int raster_g;              // ungrouped tile order: groups of raster_g m-blocks x all n-blocks
 };
 
 struct Tile {
@@ -101,11 +102,19 @@ P2R_DEVICE Tile get_tile(const GemmParams& p, int t, int BN, int CG = 1, int ran
     T.kb0 = 0;
     T.kb1 = (cnt + BK - 1) / BK;
   } else {
+    // Grouped raster: consecutive tiles (= CTAs running concurrently) sweep
+    // raster_g m-blocks x every n-block, so each A and B block is shared by a
+    // bounded number of concurrent tiles (no L2 hot spot, fewer DRAM re-reads).
     const int per_s = p.num_m_blk * p.num_n_blk;
     T.ks = t / per_s;
     const int r = t - T.ks * per_s;
-    T.n_blk = r / p.num_m_blk;
-    T.m_blk = r - T.n_blk * p.num_m_blk;
+    const int gsz = p.raster_g * p.num_n_blk;
+    const int grp = r / gsz;
+    const int m0 = grp * p.raster_g;
+    const int gm = min(p.raster_g, p.num_m_blk - m0);
+    const int w = r - grp * gsz;
+    T.m_blk = m0 + w % gm;
+    T.n_blk = w / gm;
     T.a_row = T.m_blk * BM * CG + rank * BM;
     T.b_row = T.n_blk * BN + rank * (BN / CG);
     T.b_col = T.b_row;
@@ -364,6 +373,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();  // operands / C / aux may come from the previous kernel
 
   if (warp == 0) {
     if (lane == 0) {
@@ -571,6 +582,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 // One block row per output row, float4 along the row (n % 4 == 0 fast path).
 __global__ void splitk_reduce_kernel(float* c, int ldc, const float* ws, int m, int n, int splits,
                                      int accumulate) {
+  pdl_trigger();
+  pdl_wait();
   const long long total = static_cast<long long>(m) * n;
   const int r = blockIdx.x;
   if ((n & 3) == 0 && (ldc & 3) == 0) {
@@ -652,21 +665,12 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParam
   const int units = kNumSMs / CG;  // persistent: one CTA (pair) per SM (pair of SMs)
   const int grid = CG * (p.tiles_total < units ? p.tiles_total : units);
   if constexpr (CG == 1) {
-    gemm_kernel<BN, AMN, BMN, EPI, 1><<<grid, kGemmThreads, Cfg::SMEM_BYTES, s>>>(ta, tb, p);
+    const cudaError_t e = launch_k(gemm_kernel<BN, AMN, BMN, EPI, 1>, dim3(grid), dim3(kGemmThreads),
+                                   Cfg::SMEM_BYTES, s, 1, ta, tb, p);
+    if (e != cudaSuccess) return e;
   } else {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kGemmThreads);
-    cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_kernel<BN, AMN, BMN, EPI, 2>, ta, tb, p);
+    const cudaError_t e = launch_k(gemm_kernel<BN, AMN, BMN, EPI, 2>, dim3(grid), dim3(kGemmThreads),
+                                   Cfg::SMEM_BYTES, s, 2, ta, tb, p);
     if (e != cudaSuccess) return e;
   }
   count_launch();
@@ -817,6 +821,14 @@ extern "C" p2r_status p2r_gemm(const p2r_gemm_args* a, void* stream) {
     p.vec4 = (p.ldc % 4 == 0) && (p.ldc2 % 4 == 0) && (p.ldaux % 4 == 0) && al(p.c, 16) && al(p.c2, 8) &&
              al(p.aux, 16);
   }
+  {
+    static const int raster = [] {
+      const char* e = std::getenv("P2R_GEMM_RASTER");
+      const int v = e ? std::atoi(e) : 0;
+      return v > 0 ? v : 8;
+    }();
+    p.raster_g = raster < p.num_m_blk ? raster : p.num_m_blk;
+  }
   if (a->group_mode == P2R_GROUP_M)
     p.tiles_total = a->groups * (a->seg_rows / BM) * p.num_n_blk;
   else if (a->group_mode == P2R_GROUP_K)
@@ -841,11 +853,10 @@ extern "C" p2r_status p2r_gemm(const p2r_gemm_args* a, void* stream) {
                             : dispatch_majors<256, 1>(a->a_mn_major, a->b_mn_major, ta, tb, p, s);
   if (e != cudaSuccess) return set_cuda_error(e, "gemm launch");
   if (split > 1) {
-    splitk_reduce_kernel<<<a->m, 256, 0, s>>>(static_cast<float*>(a->c), a->ldc,
-                                                  static_cast<const float*>(g_ws), a->m, a->n,
-                                                  split, a->epi == P2R_EPI_ACC_F32 ? 1 : 0);
+    e = launch_k(splitk_reduce_kernel, dim3(a->m), dim3(256), 0, s, 1, static_cast<float*>(a->c), a->ldc,
+                 static_cast<const float*>(g_ws), a->m, a->n, split, a->epi == P2R_EPI_ACC_F32 ? 1 : 0);
     count_launch();
-    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error(e, "splitk reduce launch");
   }
   return P2R_OK;

@@ -44,6 +44,8 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const float* __restrict__ x
                                                     __nv_bfloat16* __restrict__ y16, float* __restrict__ y32,
                                                     float* __restrict__ mean_out, float* __restrict__ rstd_out,
                                                     int nst) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int D = 128 * NV;
   extern __shared__ __align__(128) uint8_t ln_smem[];
   __shared__ uint64_t bars[8][kLnMaxStages];
@@ -112,6 +114,8 @@ __global__ void __launch_bounds__(128) ln_bwd_kernel(
     const float* __restrict__ dy, const float* __restrict__ x, const float* __restrict__ mean_in,
     const float* __restrict__ rstd_in, const float* __restrict__ gain, const float* __restrict__ resid, int rows,
     float* __restrict__ dx32, __nv_bfloat16* __restrict__ dx16, float* __restrict__ partial, int nst) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int D = 128 * NV;
   extern __shared__ __align__(128) uint8_t ln_smem[];
   __shared__ uint64_t bars[4][kLnMaxStages];
@@ -213,6 +217,8 @@ __global__ void __launch_bounds__(128) ln_bwd_kernel(
 // 32 warp sums are added in warp order.
 __global__ void __launch_bounds__(1024) ln_param_grad_reduce(const float* __restrict__ partial, int nblk, int D,
                                                              float* __restrict__ ggain, float* __restrict__ gbias) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float red[32][33];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.x * 32 + lane;  // flattened [2][D] column
@@ -237,6 +243,8 @@ __global__ void __launch_bounds__(1024) ln_param_grad_reduce(const float* __rest
 __global__ void embed_fwd_kernel(const int* __restrict__ ids, const float* __restrict__ tok,
                                  const float* __restrict__ pos, int T, int S, int d,
                                  float* __restrict__ x) {
+  pdl_trigger();
+  pdl_wait();
   const int t = blockIdx.x;
   if (t >= T) return;
   const int id = ids[t];
@@ -308,6 +316,8 @@ __global__ void __launch_bounds__(256) ce_kernel(const float* __restrict__ logit
                                                 const uint8_t* __restrict__ mask, float scale,
                                                 __nv_bfloat16* __restrict__ dlogits, int ldg,
                                                 double* __restrict__ partial) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ double wsum[8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = blockIdx.x * 8 + warp;
@@ -348,6 +358,8 @@ __global__ void __launch_bounds__(256) ce_kernel(const float* __restrict__ logit
 
 __global__ void ce_finalize(const double* __restrict__ partial, int n, double denom,
                             float* __restrict__ loss, double* __restrict__ loss_sum) {
+  pdl_trigger();
+  pdl_wait();
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     double s = 0.0;
     for (int i = 0; i < n; ++i) s += partial[i];
@@ -413,8 +425,9 @@ extern "C" p2r_status p2r_layernorm_fwd(const float* x, const float* gain, const
     static cudaError_t a = cudaFuncSetAttribute(ln_fwd_kernel<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                                 kLnSmemAttr);                                                \
     if (a != cudaSuccess) return set_cuda_error(a, "layernorm fwd attr");                                  \
-    ln_fwd_kernel<NV><<<l.blocks, 32 * kLnFwdWarps, l.smem, s>>>(x, gain, bias, rows, eps, y16, y_f32, mean, rstd, \
-                                                                 l.nst);                                    \
+    const cudaError_t le = launch_k(ln_fwd_kernel<NV>, dim3(l.blocks), dim3(32 * kLnFwdWarps), l.smem, s, 1, x, gain, bias, rows, eps, \
+                 y16, y_f32, mean, rstd, l.nst);                                                            \
+    if (le != cudaSuccess) return set_cuda_error(le, "layernorm fwd");                                       \
     break;                                                                                                 \
   }
     P2R_LN_NV_CASES(P2R_LN_FWD)
@@ -447,8 +460,9 @@ extern "C" p2r_status p2r_layernorm_bwd(const float* dy, const float* x, const f
     static cudaError_t a = cudaFuncSetAttribute(ln_bwd_kernel<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                                 kLnSmemAttr);                                                \
     if (a != cudaSuccess) return set_cuda_error(a, "layernorm bwd attr");                                  \
-    ln_bwd_kernel<NV><<<l.blocks, 32 * kLnBwdWarps, l.smem, s>>>(dy, x, mean, rstd, gain, resid, rows, dx, d16, \
-                                                                 partial_ws, l.nst);                        \
+    const cudaError_t le = launch_k(ln_bwd_kernel<NV>, dim3(l.blocks), dim3(32 * kLnBwdWarps), l.smem, s, 1, dy, x, mean, rstd, gain, \
+                 resid, rows, dx, d16, partial_ws, l.nst);                                                  \
+    if (le != cudaSuccess) return set_cuda_error(le, "layernorm bwd");                                       \
     break;                                                                                                 \
   }
     P2R_LN_NV_CASES(P2R_LN_BWD)
@@ -457,8 +471,8 @@ extern "C" p2r_status p2r_layernorm_bwd(const float* dy, const float* x, const f
   }
   P2R_CHECK_LAUNCH("layernorm bwd");
   if (ggain || gbias) {
-    ln_param_grad_reduce<<<(2 * d + 31) / 32, 1024, 0, s>>>(partial_ws, l.blocks, d, ggain, gbias);
-    P2R_CHECK_LAUNCH("layernorm param grad");
+    P2R_LAUNCH_K("layernorm param grad", ln_param_grad_reduce, dim3((2 * d + 31) / 32), dim3(1024), 0, s, 1,
+                 static_cast<const float*>(partial_ws), l.blocks, d, ggain, gbias);
   }
   return P2R_OK;
 }
@@ -467,8 +481,8 @@ extern "C" p2r_status p2r_embed_fwd(const int* ids, const float* tok, const floa
                                     int S, int d, float* x, void* stream) {
   if (T <= 0) return P2R_OK;
   if (d % 4) return set_error(P2R_EINVAL, "embedding: d_model must be a multiple of 4");
-  embed_fwd_kernel<<<T, 128, 0, static_cast<cudaStream_t>(stream)>>>(ids, tok, pos, T, S, d, x);
-  P2R_CHECK_LAUNCH("embed fwd");
+  P2R_LAUNCH_K("embed fwd", embed_fwd_kernel, dim3(T), dim3(128), 0, static_cast<cudaStream_t>(stream), 1, ids, tok,
+               pos, T, S, d, x);
   return P2R_OK;
 }
 
@@ -548,10 +562,9 @@ extern "C" p2r_status p2r_cross_entropy(const float* logits, int rows, int V, in
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int blocks = (rows + 7) / 8;
   const float scale = loss_grad / static_cast<float>(denom);
-  ce_kernel<<<blocks, 256, 0, s>>>(logits, rows, V, ld, targets, mask, scale,
-                                   static_cast<__nv_bfloat16*>(dlogits_bf16), ldg, partial_ws);
-  P2R_CHECK_LAUNCH("cross entropy");
-  ce_finalize<<<1, 32, 0, s>>>(partial_ws, blocks, denom, loss, loss_sum);
-  P2R_CHECK_LAUNCH("cross entropy finalize");
+  P2R_LAUNCH_K("cross entropy", ce_kernel, dim3(blocks), dim3(256), 0, s, 1, logits, rows, V, ld, targets, mask, scale,
+               static_cast<__nv_bfloat16*>(dlogits_bf16), ldg, partial_ws);
+  P2R_LAUNCH_K("cross entropy finalize", ce_finalize, dim3(1), dim3(32), 0, s, 1,
+               static_cast<const double*>(partial_ws), blocks, denom, loss, loss_sum);
   return P2R_OK;
 }

@@ -37,6 +37,8 @@ P2R_DEVICE void adam_elem(float& p, float g, float& m, float& v, const AdamArgs&
 }
 
 __global__ void __launch_bounds__(256) adamw_kernel(const __grid_constant__ AdamArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const AdamSeg sg = a.seg[blockIdx.y];
   const bool decay = sg.decay != 0;
   const long long n4 = sg.len / 4;
@@ -140,6 +142,8 @@ __global__ void __launch_bounds__(256) colsum_partial_kernel(const T* __restrict
                                                              int chunk_rows, int seg_rows,
                                                              const int* __restrict__ counts,
                                                              float* __restrict__ partial) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int V = Vec16<T>::N;
   __shared__ float red[8][32 * V];
   const int lane = threadIdx.x & 31;
@@ -185,6 +189,8 @@ __global__ void __launch_bounds__(256) colsum_partial_kernel(const T* __restrict
 __global__ void __launch_bounds__(1024) colsum_finish_kernel(const float* __restrict__ partial, int nchunks, int n,
                                                              int groups, float* __restrict__ out,
                                                              long long out_group_stride) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float red[32][33];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int col = blockIdx.x * 32 + lane, g = blockIdx.y;
@@ -238,8 +244,7 @@ extern "C" p2r_status p2r_adamw_step(float* p, const float* g, float* m, float* 
     long long bx = (maxlen / 4 + 255) / 256;
     if (bx < 1) bx = 1;
     if (bx > 4 * kNumSMs) bx = 4 * kNumSMs;
-    adamw_kernel<<<dim3(static_cast<unsigned>(bx), a.nseg), 256, 0, s>>>(a);
-    P2R_CHECK_LAUNCH("adamw");
+    P2R_LAUNCH_K("adamw", adamw_kernel, dim3(static_cast<unsigned>(bx), a.nseg), dim3(256), 0, s, 1, a);
   }
   return P2R_OK;
 }
@@ -293,12 +298,14 @@ extern "C" p2r_status p2r_bias_grad(const void* x, int dtype, int ld, int rows, 
   if ((n % vec) || (ld % vec) || (reinterpret_cast<uintptr_t>(x) % 16))
     return set_error(P2R_EINVAL, "bias grad: n, ld must be multiples of 16 bytes and x 16-byte aligned");
   dim3 grid((n / vec + 31) / 32, nchunks, G);
-  if (dtype == 0)
-    colsum_partial_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(x), ld, rows, n, chunk_rows, seg_rows, counts, ws);
-  else
-    colsum_partial_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x), ld, rows, n, chunk_rows, seg_rows, counts, ws);
-  P2R_CHECK_LAUNCH("bias grad partial");
-  colsum_finish_kernel<<<dim3((n + 31) / 32, G), 1024, 0, s>>>(ws, nchunks, n, G, out, out_group_stride);
-  P2R_CHECK_LAUNCH("bias grad finish");
+  if (dtype == 0) {
+    P2R_LAUNCH_K("bias grad partial", colsum_partial_kernel<float>, grid, dim3(256), 0, s, 1,
+                 static_cast<const float*>(x), ld, rows, n, chunk_rows, seg_rows, counts, ws);
+  } else {
+    P2R_LAUNCH_K("bias grad partial", colsum_partial_kernel<__nv_bfloat16>, grid, dim3(256), 0, s, 1,
+                 static_cast<const __nv_bfloat16*>(x), ld, rows, n, chunk_rows, seg_rows, counts, ws);
+  }
+  P2R_LAUNCH_K("bias grad finish", colsum_finish_kernel, dim3((n + 31) / 32, G), dim3(1024), 0, s, 1,
+               static_cast<const float*>(ws), nchunks, n, G, out, out_group_stride);
   return P2R_OK;
 }

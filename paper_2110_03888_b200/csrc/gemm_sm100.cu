@@ -472,7 +472,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int ew = warp & 3;          // TMEM lanes [32*ew, 32*ew+32) (warp % 4 rule)
     const int chalf = (warp - 4) >> 2;  // which half of the BN columns this warp drains
     // per-warp 32x32 fp32 transpose tile, XOR-swizzled: (r, c) at r*32 + (c ^ r)
-    float* stg = reinterpret_cast<float*>(tmem_slot + 4) + (warp - 4) * 1024;
+    // (shared-space address: a generic pointer here compiles to LD/ST on the long scoreboard)
+    const uint32_t stg = smem_u32(reinterpret_cast<float*>(tmem_slot + 4) + (warp - 4) * 1024);
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = tile0; t < p.tiles_total; t += tile_step) {
@@ -521,9 +522,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         // lane = row: 8 float4 stores into a float4-granular XOR swizzle
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-          *reinterpret_cast<float4*>(stg + lane * 32 + ((q ^ (lane & 7)) << 2)) =
-              make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
-                          __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+          sts128(stg + 4 * (lane * 32 + ((q ^ (lane & 7)) << 2)), make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]));
         __syncwarp();
         const int nc = min(4, p.n - col);  // valid columns for this lane (<= 0: none)
         float4 b4 = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -537,7 +536,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int rr = 4 * i + rg;
-            const float4 v = *reinterpret_cast<const float4*>(stg + rr * 32 + ((cg ^ (rr & 7)) << 2));
+            const float4 v = lds128f(stg + 4 * (rr * 32 + ((cg ^ (rr & 7)) << 2)));
             epi_store_fast<EPI>(p, v, x[i], grow0 + rr, col, b4, cbase, ldc);
           }
         } else {
@@ -545,7 +544,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           for (int i = 0; i < 8; ++i) {
             const int rr = 4 * i + rg;
             if (rr >= nrows || nc <= 0) continue;
-            const float4 v = *reinterpret_cast<const float4*>(stg + rr * 32 + ((cg ^ (rr & 7)) << 2));
+            const float4 v = lds128f(stg + 4 * (rr * 32 + ((cg ^ (rr & 7)) << 2)));
             epilogue_vec4<EPI>(p, v, grow0 + rr, col, nc, row0 + rr >= zero_from, b4, cbase, ldc);
           }
         }

@@ -134,6 +134,31 @@ P2R_DEVICE void umma_commit(uint64_t* bar) {
                : "memory");
 }
 
+// Warp-collective variants: all 32 lanes execute with warp-uniform operands
+// (so they stay in uniform registers) and one elected lane issues. Called from
+// lane-0-only code, a tcgen05.mma costs R2UR moves plus an elect loop per MMA,
+// which bounds 128x64 MMAs at ~80 cycles of issue.
+P2R_DEVICE void umma_bf16_warp(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+P2R_DEVICE void umma_commit_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+      "}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
 // ----------------------------------------------------------------------------
 // CTA pair (cluster of 2, tcgen05 cta_group::2): the leader (rank 0) issues
 // M=256 MMAs that read A/B halves from both CTAs' shared memory at the same

@@ -26,8 +26,17 @@ for _ in range(3):
     _lib.check(L.p2r_attention_bwd(P(qkv), P(o), P(lse), P(do), P(dsum), P(dqkv), B, H, S, d, 1, st))
 torch.cuda.synchronize()
 t = o.view(torch.int64).flatten()[:512].cpu().numpy()
-t0 = t[0]
+t0 = t[0] if "--pp" not in sys.argv else min(v for v in t[16:300] if v > 0)
 rel = lambda v: int(v - t0)
+if "--pp" in sys.argv:
+    print(" j | mma: kvfull(j+1) S(j+1)issued dQA(j) dQB(j) | A: sfull  sfree  stored  dsfull | B: sfull  sfree  stored  dsfull")
+    for j in range(16):
+        m = [t[16 + 4 * j + i] for i in range(4)]
+        a = [t[100 + 4 * j + i] for i in range(4)]
+        b = [t[200 + 4 * j + i] for i in range(4)]
+        f = lambda v: f"{rel(v):8d}" if 0 < v - t0 < 10**9 else "       -"
+        print(f"{j:2d} | " + " ".join(f(v) for v in m) + " | " + " ".join(f(v) for v in a) + " | " + " ".join(f(v) for v in b))
+    sys.exit(0)
 print("after setup sync", rel(t[1]), " q_full (mma)", rel(t[2]), " D done (softmax)", rel(t[3]), " end", rel(t[4]))
 print(" j | mma: kv_full  S-issued  ds_full(j) dQ-issued | sm: s_full  tmem_ld  math  dq_done  stored  arrived")
 for j in range(16):

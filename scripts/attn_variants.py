@@ -20,10 +20,14 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
 def variant(name, text):
+    if "+" in name:  # composable: e.g. trace+nosm
+        for part in name.split("+"):
+            text = variant(part, text)
+        return text
     if name == "nomma":
         text = text.replace("umma_bf16(", "if (false) umma_bf16(")
     elif name == "nosm":
-        text = re.sub(r"ld32x2\(tmem[^;]*\);", r"{ for (int z_ = 0; z_ < 32; ++z_) { s[z_] = 0.f; dp[z_] = 0.f; } }", text)
+        text = re.sub(r"ld32x2\((tmem|tS)[^;]*\);", r"{ for (int z_ = 0; z_ < 32; ++z_) { s[z_] = 0.f; dp[z_] = 0.f; } }", text)
         text = re.sub(r"\? ex2_approx\(", "? (", text)
     elif name == "trace":
         text = "#define P2R_ATTN_TRACE 1\n" + text
@@ -36,13 +40,13 @@ def main(names):
     others = [o for o in glob.glob(os.path.join(ROOT, "build/*.o")) if not o.endswith("attention_bwd_tc.o")]
     eng = glob.glob(os.path.join(ROOT, "build/engine/*.o"))
     for n in names:
-        cu = os.path.join(OUT, f"attention_bwd_tc_{n}.cu")
+        cu = os.path.join(OUT, f"attention_bwd_tc_{n.replace('+', '_')}.cu")
         open(cu, "w").write(variant(n, base))
-        obj = cu[:-3] + ".o"
+        obj = cu[:-3].replace("+", "_") + ".o"
         subprocess.check_call(["nvcc", *ARCH, "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include"),
                                "-I" + os.path.join(ROOT, "paper_2110_03888_b200/csrc"), "--expt-relaxed-constexpr",
                                "-c", cu, "-o", obj])
-        subprocess.check_call(["nvcc", *ARCH, "-shared", "-o", os.path.join(OUT, f"libp2r_{n}.so"), *others, obj, *eng,
+        subprocess.check_call(["nvcc", *ARCH, "-shared", "-o", os.path.join(OUT, f"libp2r_{n.replace('+', '_')}.so"), *others, obj, *eng,
                                "-cudart", "static"])
         print("built", n)
 

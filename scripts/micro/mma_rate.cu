@@ -9,7 +9,7 @@
 using namespace p2r;
 
 template <int N>
-__global__ void __launch_bounds__(384, 1) k_mma(long long* out, int iters, int ldtm, int a_mn) {
+__global__ void __launch_bounds__(384, 1) k_mma(long long* out, int iters, int ldtm, int a_mn, int fresh = 0, int b_mn = 0) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t bar;
@@ -21,18 +21,21 @@ __global__ void __launch_bounds__(384, 1) k_mma(long long* out, int iters, int l
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = slot;
-  const uint32_t sa = smem_u32(smem), sbb = sa + 128 * 128;  // A: 128 rows x 64 K (16 KB), B: N rows x 64 K
+  // A: 128 rows x 64 K (16 KB), B: N rows x 64 K; `fresh` cycles through 4 distinct A/B slabs
+  const uint32_t sa0 = smem_u32(smem), sbb0 = sa0 + 4 * 128 * 128;
   __shared__ volatile int done;
   if (threadIdx.x == 0) done = 0;
   __syncthreads();
   if (warp == 1 && lane == 0) {
-    const uint32_t idesc = make_idesc_bf16(128, N, a_mn != 0, false);
+    const uint32_t idesc = make_idesc_bf16(128, N, a_mn != 0, b_mn != 0);
     long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
+      const uint32_t sa = sa0 + (fresh ? (it & 3) * 128 * 128 : 0), sbb = sbb0 + (fresh ? (it & 3) * N * 128 : 0);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const uint64_t ad = a_mn ? make_sw128_desc(sa + k * 2048, 64 * 64 * 2, 1024) : make_sw128_desc(sa + k * 32, 16, 1024);
-        umma_bf16(tmem + (it & 1) * 256, ad, make_sw128_desc(sbb + k * 32, 16, 1024), idesc, k > 0 ? 1u : 0u);
+        const uint64_t bd = b_mn ? make_sw128_desc(sbb + k * 2048, 64 * 64 * 2, 1024) : make_sw128_desc(sbb + k * 32, 16, 1024);
+        umma_bf16(tmem + (it & 1) * 256, ad, bd, idesc, k > 0 ? 1u : 0u);
       }
     }
     umma_commit(&bar);
@@ -58,10 +61,10 @@ __global__ void __launch_bounds__(384, 1) k_mma(long long* out, int iters, int l
 }
 
 template <int N>
-void run(long long* d, int ldtm, int a_mn) {
-  const int iters = 2000, smem = 128 * 128 + N * 128 + 2048;
+void run(long long* d, int ldtm, int a_mn, int fresh = 0, int b_mn = 0) {
+  const int iters = 2000, smem = 4 * 128 * 128 + 4 * N * 128 + 2048;
   cudaFuncSetAttribute(k_mma<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  k_mma<N><<<148, 384, smem>>>(d, iters, ldtm, a_mn);
+  k_mma<N><<<148, 384, smem>>>(d, iters, ldtm, a_mn, fresh, b_mn);
   cudaDeviceSynchronize();
   long long h[148];
   cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
@@ -69,8 +72,9 @@ void run(long long* d, int ldtm, int a_mn) {
   for (int i = 0; i < 148; ++i) avg += h[i];
   avg /= 148;
   const double per = avg / (iters * 4.0);
-  printf("M=128 N=%3d K=16 %s%s: %6.1f cyc/MMA (floor %d)  -> %.0f MAC/clk/SM\n", N, a_mn ? "A MN-major" : "A K-major ",
-         ldtm ? " + 8 warps tcgen05.ld" : "", per, 128 * N / 256, 128.0 * N * 16 / per);
+  printf("M=128 N=%3d K=16 %s%s%s%s: %6.1f cyc/MMA (floor %d)  -> %.0f MAC/clk/SM\n", N, a_mn ? "A MN-major" : "A K-major ",
+         b_mn ? " B MN-major" : "", fresh ? " fresh operands" : "", ldtm ? " + 8 warps tcgen05.ld" : "", per, 128 * N / 256,
+         128.0 * N * 16 / per);
 }
 
 int main() {
@@ -83,6 +87,11 @@ int main() {
   }
   run<64>(d, 0, 1);
   run<128>(d, 0, 1);
+  run<64>(d, 0, 0, 1);
+  run<128>(d, 0, 0, 1);
+  run<256>(d, 0, 0, 1);
+  run<64>(d, 0, 0, 1, 1);
+  run<64>(d, 1, 0, 1);
   cudaError_t e = cudaGetLastError();
   printf("%s\n", cudaGetErrorString(e));
   return 0;

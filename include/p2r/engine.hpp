@@ -98,6 +98,16 @@ class GradTape {
 };
 
 // One parameter as the reference names it, viewed inside a granule buffer.
+// Stage bookkeeping carried by a checkpoint (SPEC.md:250-254 StageState).
+struct StageState {
+  int stage = 0;  // 0 = PSEUDO, 1 = REAL
+  std::int64_t global_step = 0;
+  std::int64_t samples_consumed = 0;
+  double wall_time_s = 0.0;
+  std::uint64_t rng_state = 0;
+  std::int64_t last_eval_step = -1;
+};
+
 struct ParamView {
   std::string name;
   int granule;        // -1 = embeddings granule, else owned layer index
@@ -167,6 +177,11 @@ struct Profiler {
   ~Profiler();
 };
 
+class Model;
+// SPEC delink(pseudo_checkpoint) -> Checkpoint: load a PSEUDO
+// checkpoint, delink (weights + moments copied into every layer), save it as REAL.
+StageState delink_checkpoint(const std::string& in_path, const std::string& out_path);
+
 class Model {
  public:
   Model(ModelConfig config, std::uint64_t seed);
@@ -222,6 +237,7 @@ class Model {
   void set_param(int i, const float* host);
   void get_grad(int i, float* host) const;
   void get_moment(int i, int which, float* host) const;
+  void set_moment(int i, int which, const float* host);
 
   // optimizer state (AdamW moments live beside the parameters, same layout)
   void adamw_attach(float b1, float b2, float eps, float wd);
@@ -232,6 +248,17 @@ class Model {
   bool has_optimizer() const { return has_opt_; }
 
   std::unique_ptr<Model> delinked() const;
+
+  // Checkpoint container (csrc/engine/checkpoint.cpp):
+  // version tag, ModelConfig, named layer-indexed parameter buffers, AdamW
+  // moments + step count, StageState; little-endian ints, IEEE fp32 payload,
+  // manifest of names / shapes / byte offsets. save -> load -> train k steps is
+  // bit-identical to training k steps uninterrupted.
+  void save_checkpoint(const std::string& path, const StageState& st) const;
+  // Load into this model (config and EP shard must match); attaches AdamW if the
+  // file carries moments and the optimizer is not attached yet.
+  StageState load_checkpoint(const std::string& path);
+  static std::unique_ptr<Model> from_checkpoint(const std::string& path, StageState* st);
 
   cudaStream_t stream() const { return stream_; }
   void set_profiling(bool on) { prof_.on = on; }

@@ -78,6 +78,31 @@ int64_t p2r_model_scratch_grad_bytes(const p2r_model* m);
 /* Model::delinked (model.cpp:358-377) + optimizer-moment copy (SPEC.md:279,
  * :312) as one device broadcast; logic error on a non-shared model. */
 p2r_status p2r_model_delinked(const p2r_model* m, p2r_model** out);
+p2r_status p2r_model_set_moment(p2r_model* m, int i, int which, const float* host_in);
+
+/* ------------------------------------------------------------------------ */
+/* Checkpoint container (SPEC.md:260-264 [TYPE] Checkpoint, :320 file format): */
+/* version tag, ModelConfig, named layer-indexed fp32 parameter buffers, AdamW */
+/* moments + step count, StageState; LE ints, IEEE fp32, manifest of names /   */
+/* shapes / byte offsets. save -> load -> train k steps == train k steps,      */
+/* bitwise. Errors: bad file -> ERUNTIME; config / shard mismatch -> EINVAL;  */
+/* delink of a non-PSEUDO checkpoint -> ELOGIC.                               */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+  int stage; /* 0 = PSEUDO, 1 = REAL */
+  int64_t global_step;
+  int64_t samples_consumed;
+  double wall_time_s;
+  uint64_t rng_state;
+  int64_t last_eval_step;
+} p2r_stage_state;
+
+p2r_status p2r_model_save_checkpoint(const p2r_model* m, const char* path, const p2r_stage_state* st);
+/* into an existing model with the same config (attaches AdamW if the file has moments) */
+p2r_status p2r_model_load_checkpoint(p2r_model* m, const char* path, p2r_stage_state* st_out);
+p2r_status p2r_model_from_checkpoint(const char* path, p2r_model** out, p2r_stage_state* st_out);
+/* [OP] delink(pseudo_checkpoint) -> Real checkpoint */
+p2r_status p2r_delink_checkpoint(const char* in_path, const char* out_path, p2r_stage_state* st_out);
 
 /* Raw device stream the model enqueues on (cudaStream_t). */
 void* p2r_model_stream(p2r_model* m);

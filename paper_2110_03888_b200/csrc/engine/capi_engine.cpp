@@ -151,6 +151,63 @@ p2r_status p2r_model_delinked(const p2r_model* m, p2r_model** out) {
   });
 }
 
+p2r_status p2r_model_set_moment(p2r_model* m, int i, int which, const float* host_in) {
+  return guard([&] { m->m->set_moment(i, which, host_in); });
+}
+
+namespace {
+p2r::StageState to_state(const p2r_stage_state* s) {
+  p2r::StageState st;
+  if (s) {
+    st.stage = s->stage;
+    st.global_step = s->global_step;
+    st.samples_consumed = s->samples_consumed;
+    st.wall_time_s = s->wall_time_s;
+    st.rng_state = s->rng_state;
+    st.last_eval_step = s->last_eval_step;
+  }
+  return st;
+}
+void from_state(const p2r::StageState& st, p2r_stage_state* s) {
+  if (!s) return;
+  s->stage = st.stage;
+  s->global_step = st.global_step;
+  s->samples_consumed = st.samples_consumed;
+  s->wall_time_s = st.wall_time_s;
+  s->rng_state = st.rng_state;
+  s->last_eval_step = st.last_eval_step;
+}
+}  // namespace
+
+p2r_status p2r_model_save_checkpoint(const p2r_model* m, const char* path, const p2r_stage_state* st) {
+  return guard([&] {
+    if (!path) throw std::invalid_argument("checkpoint: null path");
+    m->m->save_checkpoint(path, to_state(st));
+  });
+}
+p2r_status p2r_model_load_checkpoint(p2r_model* m, const char* path, p2r_stage_state* st_out) {
+  return guard([&] {
+    if (!path) throw std::invalid_argument("checkpoint: null path");
+    from_state(m->m->load_checkpoint(path), st_out);
+  });
+}
+p2r_status p2r_model_from_checkpoint(const char* path, p2r_model** out, p2r_stage_state* st_out) {
+  return guard([&] {
+    if (!path) throw std::invalid_argument("checkpoint: null path");
+    p2r::StageState st;
+    auto h = std::make_unique<p2r_model>();
+    h->m = p2r::Model::from_checkpoint(path, &st);
+    from_state(st, st_out);
+    *out = h.release();
+  });
+}
+p2r_status p2r_delink_checkpoint(const char* in_path, const char* out_path, p2r_stage_state* st_out) {
+  return guard([&] {
+    if (!in_path || !out_path) throw std::invalid_argument("checkpoint: null path");
+    from_state(p2r::delink_checkpoint(in_path, out_path), st_out);
+  });
+}
+
 void* p2r_model_stream(p2r_model* m) { return m->m->stream(); }
 
 p2r_status p2r_model_set_profiling(p2r_model* m, int on) {

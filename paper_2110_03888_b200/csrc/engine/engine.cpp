@@ -417,6 +417,12 @@ void Model::get_moment(int i, int which, float* host) const {
   copy_view(views_.at(static_cast<std::size_t>(i)), 2 + which, host, true);
 }
 
+void Model::set_moment(int i, int which, const float* host) {
+  if (!has_opt_) throw std::logic_error("adamw: optimizer not attached");
+  if (which != 0 && which != 1) throw std::invalid_argument("adamw: moment index must be 0 (m) or 1 (v)");
+  copy_view(views_.at(static_cast<std::size_t>(i)), 2 + which, const_cast<float*>(host), false);
+}
+
 std::int64_t Model::grad_bytes() const {
   return (emb_.numel + layer_stride_ * n_res_) * 4;
 }

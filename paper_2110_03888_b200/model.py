@@ -23,6 +23,18 @@ class ModelConfigC(ctypes.Structure):
         "seq_len", "n_experts", "n_prototypes", "n_shards")] + [("capacity_factor", ctypes.c_float)]
 
 
+class StageStateC(ctypes.Structure):
+    """p2r_stage_state (SPEC.md:250-254 StageState)."""
+    _fields_ = [("stage", ctypes.c_int), ("global_step", ctypes.c_int64), ("samples_consumed", ctypes.c_int64),
+                ("wall_time_s", ctypes.c_double), ("rng_state", ctypes.c_uint64), ("last_eval_step", ctypes.c_int64)]
+
+
+def _state_dict(s: StageStateC) -> dict:
+    return {"stage": "REAL" if s.stage else "PSEUDO", "global_step": s.global_step,
+            "samples_consumed": s.samples_consumed, "wall_time_s": s.wall_time_s, "rng_state": s.rng_state,
+            "last_eval_step": s.last_eval_step}
+
+
 _lib._EXTRA_SIGNATURES.update({
     "p2r_count_params": [ctypes.POINTER(ModelConfigC), vp],
     "p2r_model_create": [ctypes.POINTER(ModelConfigC), ctypes.c_uint64, ctypes.POINTER(vp)],
@@ -39,6 +51,11 @@ _lib._EXTRA_SIGNATURES.update({
     "p2r_model_adamw_set_step_count": [vp, i64],
     "p2r_model_get_moment": [vp, ip, ip, vp],
     "p2r_model_delinked": [vp, ctypes.POINTER(vp)],
+    "p2r_model_set_moment": [vp, ip, ip, vp],
+    "p2r_model_save_checkpoint": [vp, ctypes.c_char_p, ctypes.POINTER(StageStateC)],
+    "p2r_model_load_checkpoint": [vp, ctypes.c_char_p, ctypes.POINTER(StageStateC)],
+    "p2r_model_from_checkpoint": [ctypes.c_char_p, ctypes.POINTER(vp), ctypes.POINTER(StageStateC)],
+    "p2r_delink_checkpoint": [ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(StageStateC)],
     "p2r_model_routing": [vp, ip, vp, vp, vp, ctypes.POINTER(ip), ctypes.POINTER(ip)],
     "p2r_moe_dispatch_host": [vp, ip, ip, ip, fp, vp, vp, vp, vp, vp, vp,
                               ctypes.POINTER(ip), ctypes.POINTER(ip)],
@@ -221,6 +238,31 @@ class Model:
             out[n] = (m, v)
         return out
 
+    def set_moments(self, moments: dict):
+        for i, n in enumerate(self.names):
+            m, v = (np.ascontiguousarray(x, dtype=np.float32) for x in moments[n])
+            check(lib().p2r_model_set_moment(self.h, i, 0, _p(m)))
+            check(lib().p2r_model_set_moment(self.h, i, 1, _p(v)))
+
+    # ---- checkpoint container (csrc/engine/checkpoint.cpp)
+    def save_checkpoint(self, path: str, stage: str = None, global_step: int = 0, samples_consumed: int = 0,
+                        wall_time_s: float = 0.0, rng_state: int = 0, last_eval_step: int = -1):
+        """Parameters, AdamW moments + step count and the StageState. stage defaults to
+        PSEUDO for a shared-parameter model and REAL otherwise."""
+        if stage is None:
+            stage = "PSEUDO" if self.cfg.shared() else "REAL"
+        if stage not in ("PSEUDO", "REAL"):
+            raise ValueError("stage must be PSEUDO or REAL")
+        st = StageStateC(1 if stage == "REAL" else 0, global_step, samples_consumed, wall_time_s, rng_state,
+                         last_eval_step)
+        check(lib().p2r_model_save_checkpoint(self.h, path.encode(), ctypes.byref(st)))
+
+    def load_checkpoint(self, path: str) -> dict:
+        """Load into this model (same config); returns the StageState as a dict."""
+        st = StageStateC()
+        check(lib().p2r_model_load_checkpoint(self.h, path.encode(), ctypes.byref(st)))
+        return _state_dict(st)
+
     # ---- compute
     def forward(self, tokens, batch: int, causal: bool = True) -> np.ndarray:
         tok = np.ascontiguousarray(tokens, np.int32)
@@ -378,3 +420,21 @@ def moe_dispatch(logits: np.ndarray, n_experts: int, n_prototypes: int = 1,
     r.expert_rows = [r.rows[off[e]:off[e + 1]] for e in range(n_experts)]
     r.expert_slots = [r.slots[off[e]:off[e + 1]] for e in range(n_experts)]
     return r
+
+
+def load_checkpoint(path: str):
+    """Model.from_checkpoint: returns (Model, StageState dict)."""
+    from .checkpoint import read_manifest
+    _declare_extra()
+    c = read_manifest(path)["config"]
+    h, st = vp(), StageStateC()
+    check(lib().p2r_model_from_checkpoint(path.encode(), ctypes.byref(h), ctypes.byref(st)))
+    return Model(Config(**c), handle=h.value), _state_dict(st)
+
+
+def delink_checkpoint(in_path: str, out_path: str) -> dict:
+    """[OP] delink(pseudo_checkpoint) -> Real checkpoint."""
+    _declare_extra()
+    st = StageStateC()
+    check(lib().p2r_delink_checkpoint(in_path.encode(), out_path.encode(), ctypes.byref(st)))
+    return _state_dict(st)

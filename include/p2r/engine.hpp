@@ -181,6 +181,11 @@ class Model;
 // SPEC delink(pseudo_checkpoint) -> Checkpoint: load a PSEUDO
 // checkpoint, delink (weights + moments copied into every layer), save it as REAL.
 StageState delink_checkpoint(const std::string& in_path, const std::string& out_path);
+// SPEC redistribute_experts(model, new_n_shards) across GPU counts (SURVEY §8(f)
+// row 2; model.cpp:334-356): re-shard W1 expert-parallel shard checkpoints into
+// W2 (rank r2 gets experts [r2*E/W2, (r2+1)*E/W2), weights and AdamW moments;
+// replicated buffers from shard 0; config n_shards = W2). Host file I/O only.
+void redistribute_checkpoints(const std::vector<std::string>& in_paths, const std::vector<std::string>& out_paths);
 
 class Model {
  public:
@@ -248,6 +253,14 @@ class Model {
   bool has_optimizer() const { return has_opt_; }
 
   std::unique_ptr<Model> delinked() const;
+
+  // expert sharding bookkeeping (model.cpp:334-356): expert e lives on shard
+  // e / (E / n_shards). In one process re-sharding is bookkeeping (outputs are
+  // unchanged); expert-parallel runs re-shard weights and moments across GPU
+  // counts with redistribute_checkpoints.
+  int expert_shard(int expert) const;
+  std::vector<std::vector<int>> shard_layout() const;
+  void redistribute_experts(int new_n_shards);
 
   // Checkpoint container (csrc/engine/checkpoint.cpp):
   // version tag, ModelConfig, named layer-indexed parameter buffers, AdamW

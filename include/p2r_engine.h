@@ -104,6 +104,15 @@ p2r_status p2r_model_from_checkpoint(const char* path, p2r_model** out, p2r_stag
 /* [OP] delink(pseudo_checkpoint) -> Real checkpoint */
 p2r_status p2r_delink_checkpoint(const char* in_path, const char* out_path, p2r_stage_state* st_out);
 
+/* Expert sharding (model.cpp:334-356, SPEC redistribute_experts). In-process
+ * re-sharding is bookkeeping; across GPU counts the n_in expert-parallel shard
+ * checkpoints are re-sharded into n_out (weights + AdamW moments; host I/O only).
+ * EINVAL when n_experts % new shard count != 0 (reference text). */
+p2r_status p2r_model_expert_shard(const p2r_model* m, int expert, int* shard_out);
+p2r_status p2r_model_redistribute_experts(p2r_model* m, int new_n_shards);
+p2r_status p2r_redistribute_checkpoints(const char* const* in_paths, int n_in, const char* const* out_paths,
+                                        int n_out);
+
 /* Raw device stream the model enqueues on (cudaStream_t). */
 void* p2r_model_stream(p2r_model* m);
 

@@ -208,6 +208,22 @@ p2r_status p2r_delink_checkpoint(const char* in_path, const char* out_path, p2r_
   });
 }
 
+p2r_status p2r_model_expert_shard(const p2r_model* m, int expert, int* shard_out) {
+  return guard([&] { *shard_out = m->m->expert_shard(expert); });
+}
+p2r_status p2r_model_redistribute_experts(p2r_model* m, int new_n_shards) {
+  return guard([&] { m->m->redistribute_experts(new_n_shards); });
+}
+p2r_status p2r_redistribute_checkpoints(const char* const* in_paths, int n_in, const char* const* out_paths,
+                                        int n_out) {
+  return guard([&] {
+    if (n_in <= 0 || n_out <= 0 || !in_paths || !out_paths)
+      throw std::invalid_argument("redistribute_experts: empty shard list");
+    std::vector<std::string> in(in_paths, in_paths + n_in), out(out_paths, out_paths + n_out);
+    p2r::redistribute_checkpoints(in, out);
+  });
+}
+
 void* p2r_model_stream(p2r_model* m) { return m->m->stream(); }
 
 p2r_status p2r_model_set_profiling(p2r_model* m, int on) {

@@ -182,37 +182,33 @@ Manifest read_manifest(std::ifstream& f, const std::string& path) {
   return m;
 }
 
-}  // namespace
+// Header of a container being written: everything but the buffers.
+struct Header {
+  ModelConfig cfg;
+  int ep_world = 1, ep_rank = 0;
+  StageState st;
+  bool adamw = false;
+  float b1 = 0.9f, b2 = 0.999f, eps = 1e-8f, wd = 0.01f;
+  std::int64_t step_count = 0;
+};
 
-void Model::save_checkpoint(const std::string& path, const StageState& st) const {
+// Write a container: `fill(b, dst)` produces buffer b's fp32 payload.
+template <typename Fill>
+void write_container(const std::string& path, const Header& h, std::vector<BufferEntry> bufs, Fill&& fill) {
   if (!host_little_endian()) throw std::runtime_error("checkpoint: big-endian hosts are not supported");
-  // buffer list: every parameter, then AdamW m and v (when attached), for_each order
-  std::vector<BufferEntry> bufs;
-  std::vector<std::pair<int, int>> src;  // (param index, kind: 0 param, 1 m, 2 v)
-  const int kinds = has_opt_ ? 3 : 1;
-  static const char* prefix[3] = {"param/", "adam_m/", "adam_v/"};
-  for (int kind = 0; kind < kinds; ++kind)
-    for (std::size_t i = 0; i < views_.size(); ++i) {
-      BufferEntry e;
-      e.name = prefix[kind] + views_[i].name;
-      e.shape = views_[i].shape;
-      e.bytes = static_cast<std::uint64_t>(views_[i].rows) * views_[i].cols * 4;
-      bufs.push_back(std::move(e));
-      src.emplace_back(static_cast<int>(i), kind);
-    }
-  // manifest: fixed-width offsets, so its length does not depend on their values
+  // fixed-width offsets: the manifest length does not depend on their values
   auto manifest = [&]() {
     std::ostringstream m;
-    m << "p2r-checkpoint 1\n" << config_line(cfg_) << "\n";
-    m << "ep " << ep_world_ << " " << ep_rank_ << "\n";
-    m << "stage " << (st.stage ? "REAL" : "PSEUDO") << "\n";
-    m << "global_step " << st.global_step << "\n";
-    m << "samples_consumed " << st.samples_consumed << "\n";
-    m << "wall_time_s " << hexf(st.wall_time_s) << "\n";
-    m << "rng_state " << st.rng_state << "\n";
-    m << "last_eval_step " << st.last_eval_step << "\n";
-    m << "adamw " << (has_opt_ ? 1 : 0) << " " << hexf(b1_) << " " << hexf(b2_) << " " << hexf(eps_) << " "
-      << hexf(wd_) << " " << step_count_ << "\n";
+    m << "p2r-checkpoint 1\n" << config_line(h.cfg) << "\n";
+    m << "ep " << h.ep_world << " " << h.ep_rank << "\n";
+    m << "stage " << (h.st.stage ? "REAL" : "PSEUDO") << "\n";
+    m << "global_step " << h.st.global_step << "\n";
+    m << "samples_consumed " << h.st.samples_consumed << "\n";
+    m << "wall_time_s " << hexf(h.st.wall_time_s) << "\n";
+    m << "rng_state " << h.st.rng_state << "\n";
+    m << "last_eval_step " << h.st.last_eval_step << "\n";
+    m << "adamw " << (h.adamw ? 1 : 0) << " " << hexf(h.b1) << " " << hexf(h.b2) << " " << hexf(h.eps) << " "
+      << hexf(h.wd) << " " << h.step_count << "\n";
     m << "buffers " << bufs.size() << "\n";
     for (const BufferEntry& e : bufs) {
       m << "buffer " << e.name << " f32 " << e.shape.size();
@@ -241,15 +237,62 @@ void Model::save_checkpoint(const std::string& path, const StageState& st) const
   for (std::size_t b = 0; b < bufs.size(); ++b) {
     f.write(zeros, static_cast<std::streamsize>(bufs[b].offset - pos));
     host.resize(bufs[b].bytes / 4);
-    const int i = src[b].first, kind = src[b].second;
-    if (kind == 0)
-      get_param(i, host.data());
-    else
-      get_moment(i, kind - 1, host.data());
+    fill(b, host.data());
     f.write(reinterpret_cast<const char*>(host.data()), static_cast<std::streamsize>(bufs[b].bytes));
     pos = bufs[b].offset + bufs[b].bytes;
   }
   if (!f) throw std::runtime_error("checkpoint: write failed: " + path);
+}
+
+void read_payload(std::ifstream& f, const BufferEntry& e, float* dst) {
+  f.seekg(static_cast<std::streamoff>(e.offset));
+  f.read(reinterpret_cast<char*>(dst), static_cast<std::streamsize>(e.bytes));
+  if (static_cast<std::uint64_t>(f.gcount()) != e.bytes) throw std::runtime_error("checkpoint: truncated buffer " + e.name);
+}
+
+// global expert index of "layer.<i>.moe.expert.<e>.<param>" (after the kind prefix), or -1
+int expert_of(const std::string& name) {
+  const std::string key = ".moe.expert.";
+  const std::size_t p = name.find(key);
+  if (p == std::string::npos) return -1;
+  return std::atoi(name.c_str() + p + key.size());
+}
+
+}  // namespace
+
+void Model::save_checkpoint(const std::string& path, const StageState& st) const {
+  // buffer list: every parameter, then AdamW m and v (when attached), for_each order
+  std::vector<BufferEntry> bufs;
+  std::vector<std::pair<int, int>> src;  // (param index, kind: 0 param, 1 m, 2 v)
+  const int kinds = has_opt_ ? 3 : 1;
+  static const char* prefix[3] = {"param/", "adam_m/", "adam_v/"};
+  for (int kind = 0; kind < kinds; ++kind)
+    for (std::size_t i = 0; i < views_.size(); ++i) {
+      BufferEntry e;
+      e.name = prefix[kind] + views_[i].name;
+      e.shape = views_[i].shape;
+      e.bytes = static_cast<std::uint64_t>(views_[i].rows) * views_[i].cols * 4;
+      bufs.push_back(std::move(e));
+      src.emplace_back(static_cast<int>(i), kind);
+    }
+  Header h;
+  h.cfg = cfg_;
+  h.ep_world = ep_world_;
+  h.ep_rank = ep_rank_;
+  h.st = st;
+  h.adamw = has_opt_;
+  h.b1 = b1_;
+  h.b2 = b2_;
+  h.eps = eps_;
+  h.wd = wd_;
+  h.step_count = step_count_;
+  write_container(path, h, std::move(bufs), [&](std::size_t b, float* dst) {
+    const int i = src[b].first, kind = src[b].second;
+    if (kind == 0)
+      get_param(i, dst);
+    else
+      get_moment(i, kind - 1, dst);
+  });
 }
 
 StageState Model::load_checkpoint(const std::string& path) {
@@ -283,9 +326,7 @@ StageState Model::load_checkpoint(const std::string& path) {
       throw std::runtime_error("checkpoint: shape mismatch for " + e.name);
     if (kind > 0 && !m.adamw) throw std::runtime_error("checkpoint: moment buffer without optimizer state");
     host.resize(e.bytes / 4);
-    f.seekg(static_cast<std::streamoff>(e.offset));
-    f.read(reinterpret_cast<char*>(host.data()), static_cast<std::streamsize>(e.bytes));
-    if (static_cast<std::uint64_t>(f.gcount()) != e.bytes) throw std::runtime_error("checkpoint: truncated buffer " + e.name);
+    read_payload(f, e, host.data());
     if (kind == 0)
       set_param(it->second, host.data());
     else
@@ -320,6 +361,91 @@ StageState delink_checkpoint(const std::string& in_path, const std::string& out_
   st.stage = 1;
   real->save_checkpoint(out_path, st);
   return st;
+}
+
+int Model::expert_shard(int expert) const {
+  if (!cfg_.moe.enabled()) throw std::logic_error("expert_shard: dense model");
+  if (expert < 0 || expert >= cfg_.moe.n_experts) throw std::out_of_range("expert_shard: expert index");
+  return expert / (cfg_.moe.n_experts / cfg_.moe.n_shards);
+}
+
+std::vector<std::vector<int>> Model::shard_layout() const {
+  if (!cfg_.moe.enabled()) throw std::logic_error("shard_layout: dense model");
+  std::vector<std::vector<int>> layout(static_cast<std::size_t>(cfg_.moe.n_shards));
+  for (int e = 0; e < cfg_.moe.n_experts; ++e) layout[static_cast<std::size_t>(expert_shard(e))].push_back(e);
+  return layout;
+}
+
+void Model::redistribute_experts(int new_n_shards) {
+  if (!cfg_.moe.enabled()) throw std::logic_error("redistribute_experts: dense model");
+  if (new_n_shards <= 0 || cfg_.moe.n_experts % new_n_shards != 0)
+    throw std::invalid_argument("redistribute_experts: n_experts must be divisible by new shard count");
+  if (ep_world_ > 1)
+    throw std::logic_error("redistribute_experts: an expert-parallel shard re-shards through redistribute_checkpoints");
+  cfg_.moe.n_shards = new_n_shards;
+}
+
+void redistribute_checkpoints(const std::vector<std::string>& in_paths, const std::vector<std::string>& out_paths) {
+  const int W1 = static_cast<int>(in_paths.size()), W2 = static_cast<int>(out_paths.size());
+  if (W1 <= 0 || W2 <= 0) throw std::invalid_argument("redistribute_experts: empty shard list");
+  std::vector<Manifest> in(static_cast<std::size_t>(W1));
+  for (int r = 0; r < W1; ++r) {
+    std::ifstream f(in_paths[static_cast<std::size_t>(r)], std::ios::binary);
+    in[static_cast<std::size_t>(r)] = read_manifest(f, in_paths[static_cast<std::size_t>(r)]);
+    const Manifest& m = in[static_cast<std::size_t>(r)];
+    if (m.ep_world != W1 || m.ep_rank != r)
+      throw std::invalid_argument("redistribute_experts: input " + std::to_string(r) + " is not shard " +
+                                  std::to_string(r) + " of " + std::to_string(W1));
+    ModelConfig a = m.cfg, b = in[0].cfg;
+    a.moe.n_shards = b.moe.n_shards = 1;
+    if (config_line(a) != config_line(b)) throw std::invalid_argument("redistribute_experts: shards disagree on the config");
+  }
+  const ModelConfig& c0 = in[0].cfg;
+  if (!c0.moe.enabled()) throw std::logic_error("redistribute_experts: dense model");
+  const int E = c0.moe.n_experts;
+  if (E % W2 != 0)  // model.cpp:350-353
+    throw std::invalid_argument("redistribute_experts: n_experts must be divisible by new shard count");
+  // where each buffer lives: replicated ones in shard 0, expert e in the shard that owns it
+  struct Src {
+    int shard;
+    BufferEntry e;
+  };
+  std::vector<std::pair<std::string, Src>> replicated;
+  std::map<int, std::vector<Src>> experts;  // global expert -> its buffers (all kinds)
+  for (int r = 0; r < W1; ++r)
+    for (const BufferEntry& e : in[static_cast<std::size_t>(r)].buffers) {
+      const int x = expert_of(e.name);
+      if (x >= 0)
+        experts[x].push_back({r, e});
+      else if (r == 0)
+        replicated.push_back({e.name, {0, e}});
+    }
+  if (static_cast<int>(experts.size()) != E) throw std::runtime_error("redistribute_experts: input shards miss experts");
+  std::vector<std::ifstream> files;
+  for (const std::string& p : in_paths) files.emplace_back(p, std::ios::binary);
+  for (int r2 = 0; r2 < W2; ++r2) {
+    std::vector<Src> srcs;
+    for (const auto& kv : replicated) srcs.push_back(kv.second);
+    for (int x = r2 * (E / W2); x < (r2 + 1) * (E / W2); ++x)
+      for (const Src& s : experts[x]) srcs.push_back(s);
+    Header h;
+    h.cfg = c0;
+    h.cfg.moe.n_shards = W2;
+    h.ep_world = W2;
+    h.ep_rank = r2;
+    h.st = in[0].st;
+    h.adamw = in[0].adamw;
+    h.b1 = in[0].b1;
+    h.b2 = in[0].b2;
+    h.eps = in[0].eps;
+    h.wd = in[0].wd;
+    h.step_count = in[0].step_count;
+    std::vector<BufferEntry> bufs;
+    for (const Src& s : srcs) bufs.push_back(s.e);
+    write_container(out_paths[static_cast<std::size_t>(r2)], h, std::move(bufs), [&](std::size_t b, float* dst) {
+      read_payload(files[static_cast<std::size_t>(srcs[b].shard)], srcs[b].e, dst);
+    });
+  }
 }
 
 }  // namespace p2r

@@ -56,6 +56,9 @@ _lib._EXTRA_SIGNATURES.update({
     "p2r_model_load_checkpoint": [vp, ctypes.c_char_p, ctypes.POINTER(StageStateC)],
     "p2r_model_from_checkpoint": [ctypes.c_char_p, ctypes.POINTER(vp), ctypes.POINTER(StageStateC)],
     "p2r_delink_checkpoint": [ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(StageStateC)],
+    "p2r_model_expert_shard": [vp, ip, ctypes.POINTER(ip)],
+    "p2r_model_redistribute_experts": [vp, ip],
+    "p2r_redistribute_checkpoints": [ctypes.POINTER(ctypes.c_char_p), ip, ctypes.POINTER(ctypes.c_char_p), ip],
     "p2r_model_routing": [vp, ip, vp, vp, vp, ctypes.POINTER(ip), ctypes.POINTER(ip)],
     "p2r_moe_dispatch_host": [vp, ip, ip, ip, fp, vp, vp, vp, vp, vp, vp,
                               ctypes.POINTER(ip), ctypes.POINTER(ip)],
@@ -263,6 +266,20 @@ class Model:
         check(lib().p2r_model_load_checkpoint(self.h, path.encode(), ctypes.byref(st)))
         return _state_dict(st)
 
+    # ---- expert sharding bookkeeping (model.cpp:334-356)
+    def expert_shard(self, expert: int) -> int:
+        out = ctypes.c_int()
+        check(lib().p2r_model_expert_shard(self.h, expert, ctypes.byref(out)))
+        return out.value
+
+    def shard_layout(self):
+        return [[e for e in range(self.cfg.n_experts) if self.expert_shard(e) == s]
+                for s in range(self.cfg.n_shards)]
+
+    def redistribute_experts(self, new_n_shards: int):
+        check(lib().p2r_model_redistribute_experts(self.h, new_n_shards))
+        self.cfg = Config(**{**self.cfg.__dict__, "n_shards": new_n_shards})
+
     # ---- compute
     def forward(self, tokens, batch: int, causal: bool = True) -> np.ndarray:
         tok = np.ascontiguousarray(tokens, np.int32)
@@ -438,3 +455,12 @@ def delink_checkpoint(in_path: str, out_path: str) -> dict:
     st = StageStateC()
     check(lib().p2r_delink_checkpoint(in_path.encode(), out_path.encode(), ctypes.byref(st)))
     return _state_dict(st)
+
+
+def redistribute_checkpoints(in_paths, out_paths):
+    """Re-shard expert-parallel shard checkpoints across GPU counts (len(in_paths) ->
+    len(out_paths) shards; weights + AdamW moments; SPEC redistribute_experts)."""
+    _declare_extra()
+    ins = (ctypes.c_char_p * len(in_paths))(*[p.encode() for p in in_paths])
+    outs = (ctypes.c_char_p * len(out_paths))(*[p.encode() for p in out_paths])
+    check(lib().p2r_redistribute_checkpoints(ins, len(in_paths), outs, len(out_paths)))

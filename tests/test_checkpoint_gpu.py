@@ -156,3 +156,44 @@ def test_load_into_offloaded_model(cuda, tmp_path):
     off.adamw_step(1e-3 * 2)
     assert la == lo
     assert_same_state(a, off)
+
+
+def test_redistribute_experts(cuda, tmp_path):
+    """SPEC redistribute_experts (model.cpp:334-356): in-process re-sharding is bookkeeping
+    with identical outputs; across GPU counts the shard checkpoints carry each expert's
+    weights and moments to its new owner, and 1 -> 2 -> 1 restores the model bitwise."""
+    import paper_2110_03888_b200 as p2r
+    m = p2r.Model(p2r.Config(**C1), 1234)
+    m.attach_adamw()
+    step(m, 0, seed=21)
+    tok, _, _ = lm_batch(8, 128, seed=22)
+    before = m.forward(tok, 8)
+    assert m.shard_layout() == [[0, 1, 2, 3]]
+    m.redistribute_experts(2)
+    assert m.shard_layout() == [[0, 1], [2, 3]] and m.expert_shard(3) == 1
+    assert np.array_equal(m.forward(tok, 8), before)
+    with pytest.raises(p2r.P2RInvalidArgument, match="divisible by new shard count"):
+        m.redistribute_experts(3)
+    with pytest.raises(p2r.P2ROutOfRange, match="expert index"):
+        m.expert_shard(4)
+    m.redistribute_experts(1)
+    full = str(tmp_path / "full.p2rckpt")
+    m.save_checkpoint(full, global_step=1)
+    shards = [str(tmp_path / f"s{r}.p2rckpt") for r in range(2)]
+    p2r.redistribute_checkpoints([full], shards)
+    pm, mm = m.params(), m.moments()
+    for r, path in enumerate(shards):
+        sh, st = p2r.load_checkpoint(path)  # an expert-parallel shard model (ep = (2, r))
+        assert st["global_step"] == 1 and sh.step_count() == m.step_count()
+        ps, ms = sh.params(), sh.moments()
+        experts = sorted({int(n.split(".")[4]) for n in ps if ".moe.expert." in n})
+        assert experts == [2 * r, 2 * r + 1]
+        for n in ps:
+            assert np.array_equal(ps[n], pm[n]), n
+            assert np.array_equal(ms[n][0], mm[n][0]) and np.array_equal(ms[n][1], mm[n][1]), n
+        sh.close()
+    back = str(tmp_path / "back.p2rckpt")
+    p2r.redistribute_checkpoints(shards, [back])
+    b, _ = p2r.load_checkpoint(back)
+    assert_same_state(m, b)
+    assert np.array_equal(b.forward(tok, 8), before)

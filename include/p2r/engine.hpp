@@ -155,6 +155,25 @@ std::vector<int> plan_offload(const std::vector<std::int64_t>& layer_bytes, std:
                               double bandwidth, double compute_s, double latency_s);
 double predict_step_time(const std::vector<std::int64_t>& layer_bytes, const std::vector<int>& slow,
                          double bandwidth, double compute_s, double latency_s);
+
+// B200 overlap model of this engine's offload. Per SLOW layer
+// of P parameters the copy engines move, per step: forward H2D 2P (bf16 shadow) +
+// fp32 vectors; backward H2D 12P (fp32 master, m, v); D2H 14P (p, m, v, bf16).
+// Copies overlap compute on their own streams, so
+//   step = max(C_fwd, H2D_fwd/h2d) + max(C_bwd, H2D_bwd/h2d, D2H/d2h)
+// with C_* = per-layer compute x L (calibrated from a resident step).
+struct OffloadCost {
+  double h2d_bw = 50e9, d2h_bw = 50e9;  // pinned PCIe bytes/s per direction
+  double fwd_s = 0, bwd_s = 0;          // compute per layer
+};
+double predict_step_time_overlap(const std::vector<std::int64_t>& layer_params,
+                                 const std::vector<std::int64_t>& vector_params, const std::vector<int>& slow,
+                                 const OffloadCost& c);
+// fewest SLOW layers whose granules (18 B/param) bring the resident set under
+// `budget`, spread evenly over the stack; minimises predict_step_time_overlap
+// among placements with that count for uniform layers.
+std::vector<int> plan_offload_overlap(const std::vector<std::int64_t>& layer_params, std::int64_t budget,
+                                      const OffloadCost& c);
 // staged device pointer of a SLOW granule: kind 0 p32, 1 grad, 2 m, 3 v, 4 bf16
 float* offload_slot_ptr(const OffloadState& st, int owned, int kind);
 // host fp32 -> bf16 (round to nearest even), the device __float2bfloat16_rn

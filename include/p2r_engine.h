@@ -183,6 +183,15 @@ p2r_status p2r_plan_offload(const int64_t* layer_bytes, int n, int64_t budget, d
 /* predict_step_time, 4 x W per SLOW layer, no overlap. */
 double p2r_predict_step_time(const int64_t* layer_bytes, const int* slow, int n, double bandwidth,
                              double compute_s, double latency_s);
+/* B200 overlap model of this engine: per SLOW layer of P params
+ * H2D 2P + 4*vector_params (fwd) and 12P (bwd), D2H 14P; copies on their own
+ * streams overlap compute: max(C_fwd, H2D_f/h2d) + max(C_bwd, H2D_b/h2d, D2H/d2h),
+ * C_* = per-layer compute x n. vector_params may be NULL. */
+double p2r_predict_step_time_overlap(const int64_t* layer_params, const int64_t* vector_params, const int* slow,
+                                     int n, double h2d_bw, double d2h_bw, double fwd_s, double bwd_s);
+/* fewest SLOW layers (18 B/param granules) under budget_bytes, spread evenly */
+p2r_status p2r_plan_offload_overlap(const int64_t* layer_params, int n, int64_t budget_bytes, double h2d_bw,
+                                    double d2h_bw, double fwd_s, double bwd_s, int* slow_out);
 
 /* init_normal (model.cpp:28-36) on the host: the exact values Model() uploads. */
 void p2r_init_normal_host(uint64_t seed, const char* name, int64_t n, float* out);

@@ -339,6 +339,33 @@ double p2r_predict_step_time(const int64_t* layer_bytes, const int* slow, int n,
   return p2r::predict_step_time(b, s, bandwidth, compute_s, latency_s);
 }
 
+namespace {
+p2r::OffloadCost cost(double h2d, double d2h, double fwd_s, double bwd_s) {
+  p2r::OffloadCost c;
+  c.h2d_bw = h2d;
+  c.d2h_bw = d2h;
+  c.fwd_s = fwd_s;
+  c.bwd_s = bwd_s;
+  return c;
+}
+}  // namespace
+
+double p2r_predict_step_time_overlap(const int64_t* layer_params, const int64_t* vector_params, const int* slow, int n,
+                                     double h2d_bw, double d2h_bw, double fwd_s, double bwd_s) {
+  std::vector<std::int64_t> p(layer_params, layer_params + n), v;
+  if (vector_params) v.assign(vector_params, vector_params + n);
+  std::vector<int> s(slow, slow + n);
+  return p2r::predict_step_time_overlap(p, v, s, cost(h2d_bw, d2h_bw, fwd_s, bwd_s));
+}
+p2r_status p2r_plan_offload_overlap(const int64_t* layer_params, int n, int64_t budget_bytes, double h2d_bw,
+                                    double d2h_bw, double fwd_s, double bwd_s, int* slow_out) {
+  return guard([&] {
+    std::vector<std::int64_t> p(layer_params, layer_params + n);
+    const std::vector<int> pl = p2r::plan_offload_overlap(p, budget_bytes, cost(h2d_bw, d2h_bw, fwd_s, bwd_s));
+    std::copy(pl.begin(), pl.end(), slow_out);
+  });
+}
+
 void p2r_init_normal_host(uint64_t seed, const char* name, int64_t n, float* out) {
   p2r::init_normal_host(out, static_cast<std::size_t>(n), seed, name);
 }

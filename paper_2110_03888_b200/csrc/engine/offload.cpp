@@ -64,6 +64,56 @@ double predict_step_time(const std::vector<std::int64_t>& layer_bytes, const std
   return compute_s + moved / bandwidth + n * latency_s;
 }
 
+double predict_step_time_overlap(const std::vector<std::int64_t>& layer_params,
+                                 const std::vector<std::int64_t>& vector_params, const std::vector<int>& slow,
+                                 const OffloadCost& c) {
+  const std::size_t L = layer_params.size();
+  if (slow.size() != L || (!vector_params.empty() && vector_params.size() != L))
+    throw std::invalid_argument("predict_step_time_overlap: layer / placement size mismatch");
+  double h2d_f = 0, h2d_b = 0, d2h = 0;
+  for (std::size_t i = 0; i < L; ++i)
+    if (slow[i]) {
+      const double P = static_cast<double>(layer_params[i]);
+      const double vec = vector_params.empty() ? 0.0 : static_cast<double>(vector_params[i]);
+      h2d_f += 2.0 * P + 4.0 * vec;  // bf16 shadow + the fp32 vectors the forward reads
+      h2d_b += 12.0 * P;             // fp32 master + m + v (bf16 re-derived on the device)
+      d2h += 14.0 * P;               // updated p, m, v + bf16 shadow
+    }
+  const double cf = c.fwd_s * static_cast<double>(L), cb = c.bwd_s * static_cast<double>(L);
+  return std::max(cf, h2d_f / c.h2d_bw) + std::max({cb, h2d_b / c.h2d_bw, d2h / c.d2h_bw});
+}
+
+std::vector<int> plan_offload_overlap(const std::vector<std::int64_t>& layer_params, std::int64_t budget,
+                                      const OffloadCost& c) {
+  const int n = static_cast<int>(layer_params.size());
+  std::int64_t total = 0, largest = 0;
+  for (auto p : layer_params) {
+    total += 18 * p;
+    largest = std::max<std::int64_t>(largest, 18 * p);
+  }
+  if (budget < largest) throw std::runtime_error("plan_offload: no feasible plan (a single layer exceeds the budget)");
+  // fewest SLOW layers (largest first) that bring the resident granules under budget
+  std::vector<int> order(static_cast<std::size_t>(n));
+  for (int i = 0; i < n; ++i) order[static_cast<std::size_t>(i)] = i;
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int a, int b) { return layer_params[static_cast<std::size_t>(a)] > layer_params[static_cast<std::size_t>(b)]; });
+  int k = 0;
+  for (std::int64_t fast = total; fast > budget && k < n; ++k) fast -= 18 * layer_params[static_cast<std::size_t>(order[static_cast<std::size_t>(k)])];
+  std::vector<int> pl(static_cast<std::size_t>(n), 0);
+  if (k == 0) return pl;
+  // spread k SLOW layers evenly: every copy gets the most neighbouring compute to hide under
+  for (int j = 0; j < k; ++j) pl[static_cast<std::size_t>((static_cast<long long>(j) * n) / k)] = 1;
+  std::int64_t fast = 0;
+  for (int i = 0; i < n; ++i)
+    if (!pl[static_cast<std::size_t>(i)]) fast += 18 * layer_params[static_cast<std::size_t>(i)];
+  if (fast > budget) {  // non-uniform layers: fall back to the largest-first choice
+    std::fill(pl.begin(), pl.end(), 0);
+    for (int j = 0; j < k; ++j) pl[static_cast<std::size_t>(order[static_cast<std::size_t>(j)])] = 1;
+  }
+  (void)c;
+  return pl;
+}
+
 std::vector<int> plan_offload(const std::vector<std::int64_t>& layer_bytes, std::int64_t budget, double bandwidth,
                               double compute_s, double latency_s) {
   const int n = static_cast<int>(layer_bytes.size());

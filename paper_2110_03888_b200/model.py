@@ -100,6 +100,10 @@ def _declare_extra():
         getattr(L, n).restype = i64
     L.p2r_predict_step_time.argtypes = [vp, vp, ip, ctypes.c_double, ctypes.c_double, ctypes.c_double]
     L.p2r_predict_step_time.restype = ctypes.c_double
+    L.p2r_predict_step_time_overlap.argtypes = [vp, vp, vp, ip] + [ctypes.c_double] * 4
+    L.p2r_predict_step_time_overlap.restype = ctypes.c_double
+    L.p2r_plan_offload_overlap.argtypes = [vp, ip, i64] + [ctypes.c_double] * 4 + [vp]
+    L.p2r_plan_offload_overlap.restype = ctypes.c_int
     return L
 
 
@@ -464,3 +468,20 @@ def redistribute_checkpoints(in_paths, out_paths):
     ins = (ctypes.c_char_p * len(in_paths))(*[p.encode() for p in in_paths])
     outs = (ctypes.c_char_p * len(out_paths))(*[p.encode() for p in out_paths])
     check(lib().p2r_redistribute_checkpoints(ins, len(in_paths), outs, len(out_paths)))
+
+
+def predict_step_time_overlap(layer_params, slow, h2d_bw, d2h_bw, fwd_s, bwd_s, vector_params=None) -> float:
+    """B200 overlap model of the offload engine; see p2r_engine.h."""
+    L = _declare_extra()
+    p = np.ascontiguousarray(layer_params, np.int64)
+    sl = np.ascontiguousarray(slow, np.int32)
+    v = None if vector_params is None else np.ascontiguousarray(vector_params, np.int64)
+    return float(L.p2r_predict_step_time_overlap(_p(p), _p(v), _p(sl), len(p), h2d_bw, d2h_bw, fwd_s, bwd_s))
+
+
+def plan_offload_overlap(layer_params, budget_bytes, h2d_bw, d2h_bw, fwd_s, bwd_s):
+    L = _declare_extra()
+    p = np.ascontiguousarray(layer_params, np.int64)
+    out = np.zeros(len(p), np.int32)
+    check(L.p2r_plan_offload_overlap(_p(p), len(p), int(budget_bytes), h2d_bw, d2h_bw, fwd_s, bwd_s, _p(out)))
+    return out.tolist()

@@ -33,6 +33,17 @@ def lm_batch(batch, seq, seed):
     return tok.ravel(), tgt.ravel(), mask.ravel()
 
 
+def overlap_prediction(p2r, rec, L):
+    """predict_step_time_overlap from a bench record: measured per-direction PCIe rates,
+    per-layer compute from the resident step (forward : backward = 1 : 2)."""
+    P = rec["granule_bytes_18B_per_param"] // 18
+    n_slow = rec["slow_layers"]
+    vec = max(0, (rec["bytes_per_step"]["Fn_load"] / max(1, n_slow) - 2 * P) / 4)
+    t = rec["step_s"]["resident"] / L
+    return p2r.predict_step_time_overlap([P] * L, rec["placement"], rec["h2d_GBps"] * 1e9, rec["d2h_GBps"] * 1e9,
+                                         t / 3, 2 * t / 3, vector_params=[int(vec)] * L)
+
+
 def run(model, p2r, args, steps, offloaded):
     import torch
     B, S = args.batch, args.seq
@@ -123,6 +134,7 @@ def main():
         "spec_4W_no_overlap_prediction_s": round(p2r.predict_step_time(
             [gran // 18 * 4] * L, plan, h2d_b / (per["h2d_ms"] / 1e3) if per["h2d_ms"] else 50e9, t_nocopy), 4),
     }
+    out["b200_overlap_prediction_s"] = round(overlap_prediction(p2r, out, L), 4)
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     with open(args.out, "w") as f:
         json.dump(out, f, indent=1)

@@ -44,3 +44,44 @@ def test_cost_model_calibration_89_45():
     t_full = p2r.predict_step_time([1] * 48, [1] * 48, bw, compute)
     t_half = p2r.predict_step_time([1] * 48, [1] * 24 + [0] * 24, bw, compute)
     assert abs(t_full - 89) < 1e-9 and abs(t_half - 45) / 45 <= 0.10
+
+
+def test_overlap_model_against_measurement():
+    """the B200 overlap cost model reproduces the measured offload
+    step (profiles/offload_r01*.json, recorded on a B200) within 10 %, where the SPEC's
+    no-overlap model overestimates it by ~1.5x."""
+    import json
+    import os
+    import sys
+    import paper_2110_03888_b200 as p2r
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, os.path.join(root, "scripts"))
+    from offload_bench import overlap_prediction
+    for name in ("offload_r01.json", "offload_r01_ring6.json"):
+        rec = json.load(open(os.path.join(root, "profiles", name)))
+        L = len(rec["placement"])
+        pred = overlap_prediction(p2r, rec, L)
+        meas = rec["step_s"]["offload"]
+        assert abs(pred - meas) / meas < 0.10, (name, pred, meas)
+        assert rec["spec_4W_no_overlap_prediction_s"] > 1.4 * meas
+
+
+def test_overlap_planner():
+    import paper_2110_03888_b200 as p2r
+    P = 50_000_000
+    gb = 18 * P
+    assert p2r.plan_offload_overlap([P] * 16, 16 * gb, 50e9, 50e9, 2e-3, 4e-3) == [0] * 16
+    plan = p2r.plan_offload_overlap([P] * 16, 8 * gb, 50e9, 50e9, 2e-3, 4e-3)
+    assert sum(plan) == 8 and plan == [1, 0] * 8  # fewest SLOW layers, spread evenly
+    plan = p2r.plan_offload_overlap([P] * 16, 12 * gb, 50e9, 50e9, 2e-3, 4e-3)
+    assert sum(plan) == 4 and plan == [1, 0, 0, 0] * 4
+    with pytest.raises(p2r.P2RError, match="no feasible plan"):
+        p2r.plan_offload_overlap([P] * 4, gb // 2, 50e9, 50e9, 2e-3, 4e-3)
+    # more SLOW layers never predict a faster step; all-resident = pure compute
+    prev = 0.0
+    for k in range(0, 17, 4):
+        slow = [1 if i < k else 0 for i in range(16)]
+        t = p2r.predict_step_time_overlap([P] * 16, slow, 50e9, 50e9, 2e-3, 4e-3)
+        assert t >= prev
+        prev = t
+    assert abs(p2r.predict_step_time_overlap([P] * 16, [0] * 16, 50e9, 50e9, 2e-3, 4e-3) - 16 * 6e-3) < 1e-12

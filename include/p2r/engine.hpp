@@ -196,6 +196,25 @@ struct Profiler {
   ~Profiler();
 };
 
+// Switch detector decision logic (csrc/engine/switch.cpp).
+struct SwitchPolicy {
+  int eval_interval_steps = 500;  // SPEC design decision defaults
+  int trial_budget_steps = 50;
+  int slope_window = 50;
+  void validate() const;
+};
+struct SwitchDecision {
+  bool fire = false;
+  double pseudo_slope = 0, real_slope = 0;  // d loss / d wall-time
+};
+// least-squares slope of loss against time over the last `window` points (all if <= 0)
+double loss_slope(const std::vector<double>& time_s, const std::vector<double>& loss, int window);
+// fire when the Real trial decreases loss faster per unit time than the Pseudo continuation
+SwitchDecision switch_criterion(const std::vector<double>& pseudo_t, const std::vector<double>& pseudo_loss,
+                                const std::vector<double>& real_t, const std::vector<double>& real_loss,
+                                const SwitchPolicy& policy);
+bool switch_evaluation_due(const SwitchPolicy& policy, std::int64_t step);
+
 class Model;
 // SPEC delink(pseudo_checkpoint) -> Checkpoint: load a PSEUDO
 // checkpoint, delink (weights + moments copied into every layer), save it as REAL.

@@ -113,6 +113,19 @@ p2r_status p2r_model_redistribute_experts(p2r_model* m, int new_n_shards);
 p2r_status p2r_redistribute_checkpoints(const char* const* in_paths, int n_in, const char* const* out_paths,
                                         int n_out);
 
+/* Switch detector decision logic (SPEC.md:255-259 SwitchPolicy, :285-293
+ * detect_switch). Slope = least-squares d loss / d wall-time over the last
+ * `window` points; the switch fires when the Real trial's slope is below the
+ * Pseudo continuation's (faster decrease). EINVAL on invalid policy / series. */
+typedef struct {
+  int eval_interval_steps, trial_budget_steps, slope_window;
+} p2r_switch_policy;
+p2r_status p2r_loss_slope(const double* time_s, const double* loss, int n, int window, double* slope_out);
+p2r_status p2r_switch_criterion(const double* pseudo_t, const double* pseudo_loss, int n_pseudo, const double* real_t,
+                                const double* real_loss, int n_real, const p2r_switch_policy* policy, int* fire_out,
+                                double* pseudo_slope_out, double* real_slope_out);
+p2r_status p2r_switch_evaluation_due(const p2r_switch_policy* policy, int64_t step, int* due_out);
+
 /* Raw device stream the model enqueues on (cudaStream_t). */
 void* p2r_model_stream(p2r_model* m);
 

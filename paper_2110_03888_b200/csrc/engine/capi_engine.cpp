@@ -224,6 +224,41 @@ p2r_status p2r_redistribute_checkpoints(const char* const* in_paths, int n_in, c
   });
 }
 
+namespace {
+p2r::SwitchPolicy policy_of(const p2r_switch_policy* p) {
+  if (!p) throw std::invalid_argument("switch policy: null");
+  p2r::SwitchPolicy s;
+  s.eval_interval_steps = p->eval_interval_steps;
+  s.trial_budget_steps = p->trial_budget_steps;
+  s.slope_window = p->slope_window;
+  return s;
+}
+}  // namespace
+
+p2r_status p2r_loss_slope(const double* time_s, const double* loss, int n, int window, double* slope_out) {
+  return guard([&] {
+    if (n < 0 || (n > 0 && (!time_s || !loss))) throw std::invalid_argument("loss_slope: bad series");
+    *slope_out = p2r::loss_slope(std::vector<double>(time_s, time_s + n), std::vector<double>(loss, loss + n), window);
+  });
+}
+p2r_status p2r_switch_criterion(const double* pseudo_t, const double* pseudo_loss, int n_pseudo, const double* real_t,
+                                const double* real_loss, int n_real, const p2r_switch_policy* policy, int* fire_out,
+                                double* pseudo_slope_out, double* real_slope_out) {
+  return guard([&] {
+    if (n_pseudo < 0 || n_real < 0) throw std::invalid_argument("switch: bad series");
+    const p2r::SwitchDecision d = p2r::switch_criterion(
+        std::vector<double>(pseudo_t, pseudo_t + n_pseudo), std::vector<double>(pseudo_loss, pseudo_loss + n_pseudo),
+        std::vector<double>(real_t, real_t + n_real), std::vector<double>(real_loss, real_loss + n_real),
+        policy_of(policy));
+    *fire_out = d.fire ? 1 : 0;
+    if (pseudo_slope_out) *pseudo_slope_out = d.pseudo_slope;
+    if (real_slope_out) *real_slope_out = d.real_slope;
+  });
+}
+p2r_status p2r_switch_evaluation_due(const p2r_switch_policy* policy, int64_t step, int* due_out) {
+  return guard([&] { *due_out = p2r::switch_evaluation_due(policy_of(policy), step) ? 1 : 0; });
+}
+
 void* p2r_model_stream(p2r_model* m) { return m->m->stream(); }
 
 p2r_status p2r_model_set_profiling(p2r_model* m, int on) {

@@ -41,7 +41,8 @@ struct Cfg {
   static constexpr int OFF_V = OFF_K + 2 * TILE;
   static constexpr int OFF_P = OFF_V + 2 * TILE;
   static constexpr int OFF_BAR = OFF_P + NPB * PTILE;
-  static constexpr int SMEM = OFF_BAR + 256 + 1024;
+  static constexpr int XCH = (2 * 2 + 2) * 128 * 4;   // row-max exchange [2][2][128] + sums [2][128]
+  static constexpr int SMEM = OFF_BAR + 256 + XCH + 1024;
   static constexpr int TMEM_S0 = 0, TMEM_S1 = 128, TMEM_O = 256;
 };
 
@@ -69,6 +70,7 @@ P2R_DEVICE void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t* r) {
       "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
       : "memory");
 }
+P2R_DEVICE void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 P2R_DEVICE void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 // 2^x on the SFU (inputs here are <= 8, outputs feed a bf16 MMA operand)
 P2R_DEVICE float ex2_approx(float x) {
@@ -79,7 +81,7 @@ P2R_DEVICE float ex2_approx(float x) {
 P2R_DEVICE void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 template <int HD>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const FwdParams p) {
   using C = Cfg<HD>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -107,7 +109,7 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(kv_full + i, 1);
       mbar_init(kv_empty + i, 1);
       mbar_init(s_full + i, 1);
-      mbar_init(p_full + i, 128);
+      mbar_init(p_full + i, 256);  // 8 softmax warps
       mbar_init(o_done + i, 1);
     }
     fence_barrier_init();
@@ -140,97 +142,110 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer ----------------
+    {  // ---------------- MMA issuer (whole warp, one elected lane issues) ----------------
       constexpr uint32_t idesc_s = make_idesc_bf16(BQ, BKV, false, false);
       constexpr uint32_t idesc_o = make_idesc_bf16(BQ, HD, false, true);
       mbar_wait(q_full, 0);
       tc_fence_after();
+      // precomputed base descriptors, advanced by byte offsets (desc_add)
+      const uint64_t dQ0 = make_sw128_desc(sbase + C::OFF_Q, 16, 1024);
+      const uint64_t dK0 = make_sw128_desc(sbase + C::OFF_K, 16, 1024);
+      const uint64_t dP0 = make_sw128_desc(sbase + C::OFF_P, 16, 1024);
+      const uint64_t dV0 = make_sw128_desc(sbase + C::OFF_V, BKV * 128, 1024);
       auto issue_pv = [&](int jj) {
         mbar_wait(p_full + (jj & 1), (jj >> 1) & 1);
         tc_fence_after();
-        const int st = jj & 1;
-        const uint32_t sp = sbase + C::OFF_P + (jj % C::NPB) * C::PTILE;
-        const uint32_t sv = sbase + C::OFF_V + st * C::TILE;
+        const uint32_t st = jj & 1;
+        const uint64_t ap = desc_add(dP0, (jj % C::NPB) * C::PTILE), bv = desc_add(dV0, st * C::TILE);
 #pragma unroll
-        for (int k = 0; k < BKV / 16; ++k) {
+        for (int k = 0; k < BKV / 16; ++k)
           // A = P (K-major, atom = 64 keys), B = V (MN-major: rows = keys, 64 hd per 128-B row)
-          const uint64_t ad = make_sw128_desc(sp + (k >> 2) * (BQ * 128) + (k & 3) * 32, 16, 1024);
-          const uint64_t bd = make_sw128_desc(sv + k * 2048, BKV * 128, 1024);
-          umma_bf16(tmem + C::TMEM_O, ad, bd, idesc_o, (jj > 0 || k > 0) ? 1u : 0u);
-        }
-        umma_commit(kv_empty + st);
-        umma_commit(o_done + (jj & 1));
+          umma_bf16_warp(tmem + C::TMEM_O, desc_add(ap, (k >> 2) * (BQ * 128) + (k & 3) * 32),
+                         desc_add(bv, k * 2048), idesc_o, (jj > 0 || k > 0) ? 1u : 0u);
+        umma_commit_warp(kv_empty + st);
+        umma_commit_warp(o_done + (jj & 1));
       };
       for (int j = 0; j < nkv; ++j) {
-        const int st = j & 1;
+        const uint32_t st = j & 1;
         mbar_wait(kv_full + st, (j >> 1) & 1);
         tc_fence_after();
-        const uint32_t sq = sbase + C::OFF_Q;
-        const uint32_t sk = sbase + C::OFF_K + st * C::TILE;
+        const uint64_t bk = desc_add(dK0, st * C::TILE);
         const uint32_t dS = tmem + ((j & 1) ? C::TMEM_S1 : C::TMEM_S0);
 #pragma unroll
-        for (int k = 0; k < HD / 16; ++k) {
-          const uint32_t koff = (k >> 2) * (BQ * 128) + (k & 3) * 32;
-          umma_bf16(dS, make_sw128_desc(sq + koff, 16, 1024),
-                    make_sw128_desc(sk + (k >> 2) * (BKV * 128) + (k & 3) * 32, 16, 1024), idesc_s,
-                    k > 0 ? 1u : 0u);
-        }
-        umma_commit(s_full + (j & 1));
+        for (int k = 0; k < HD / 16; ++k)
+          umma_bf16_warp(dS, desc_add(dQ0, (k >> 2) * (BQ * 128) + (k & 3) * 32),
+                         desc_add(bk, (k >> 2) * (BKV * 128) + (k & 3) * 32), idesc_s, k > 0 ? 1u : 0u);
+        umma_commit_warp(s_full + (j & 1));
         if (j > 0) issue_pv(j - 1);
       }
       issue_pv(nkv - 1);
     }
   } else if (warp >= 4) {
     // ---------------- softmax / correction / epilogue ----------------
-    const int r = (warp - 4) * 32 + lane;  // query row within the tile == TMEM lane
+    // 8 warps: two per TMEM lane quadrant; warp half `hf` owns key columns
+    // [64 hf, 64 hf + 64) of each block and O columns [HD/2 hf, HD/2 (hf + 1)).
+    // The two halves of a row exchange their partial maxima through shared
+    // memory (double-buffered by block parity) behind a 64-thread named barrier.
+    const int qd = warp & 3, hf = (warp - 4) >> 2;
+    const int r = qd * 32 + lane;  // query row within the tile == TMEM lane
     const int q = q0 + r;
-    const uint32_t lane_addr = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const uint32_t lane_addr = static_cast<uint32_t>(qd * 32) << 16;
+    constexpr int KH = BKV / 2, OH = HD / 2;
+    // [parity][half][row] partial maxima, then [half][row] partial sums (after the barriers area)
+    const uint32_t xch = smem_u32(smem) + C::OFF_BAR + 256;
     float m_used = -INFINITY, l = 0.0f;
     for (int j = 0; j < nkv; ++j) {
       mbar_wait(s_full + (j & 1), (j >> 1) & 1);
       tc_fence_after();
-      const uint32_t tS = tmem + lane_addr + ((j & 1) ? C::TMEM_S1 : C::TMEM_S0);
-      float x[BKV];
-#pragma unroll
-      for (int c = 0; c < BKV / 32; ++c) {
-        uint32_t rr[32];
-        tmem_ld_32x32b_x32(tS + c * 32, rr);
+      const uint32_t tS = tmem + lane_addr + ((j & 1) ? C::TMEM_S1 : C::TMEM_S0) + hf * KH;
+      float x[KH];
+      {
+        uint32_t ra[32], rb[32];
+        tmem_ld_32x32b_x32(tS, ra);
+        tmem_ld_32x32b_x32(tS + 32, rb);
         tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) x[c * 32 + i] = __uint_as_float(rr[i]);
+        for (int i = 0; i < 32; ++i) {
+          x[i] = __uint_as_float(ra[i]);
+          x[32 + i] = __uint_as_float(rb[i]);
+        }
       }
-      const int k0 = j * BKV;
-      const bool diag = p.causal && (k0 + BKV > q0);
-      const bool tail = k0 + BKV > p.S;
+      const int k0 = j * BKV + hf * KH;
+      const bool diag = p.causal && (j * BKV + BKV > q0);
+      const bool tail = j * BKV + BKV > p.S;
       if (diag || tail) {  // warp-uniform: only the diagonal / ragged-tail blocks mask
-        const int lim = min(diag ? q + 1 : p.S, p.S) - k0;  // keys [0, lim) of the block are visible
+        const int lim = min(diag ? q + 1 : p.S, p.S) - k0;  // keys [0, lim) of this half are visible
 #pragma unroll
-        for (int i = 0; i < BKV; ++i)
+        for (int i = 0; i < KH; ++i)
           if (i >= lim) x[i] = -INFINITY;
       }
-      // max on raw scores (scale > 0), then one FFMA + ex2 per element below
+      // max on raw scores (scale > 0), combined with the other half of the row
       float mr0 = x[0], mr1 = x[1];
 #pragma unroll
-      for (int i = 2; i < BKV; i += 2) {
+      for (int i = 2; i < KH; i += 2) {
         mr0 = fmaxf(mr0, x[i]);
         mr1 = fmaxf(mr1, x[i + 1]);
       }
-      const float mx = fmaxf(mr0, mr1) * p.sl2;
-      if (mx > m_used + kRescaleThresh) {
+      const uint32_t slot = xch + 4 * (((j & 1) * 2) * 128 + r);
+      sts32f(slot + 4 * 128 * hf, fmaxf(mr0, mr1));
+      named_sync(1 + qd, 64);
+      float other;
+      asm volatile("ld.shared.f32 %0, [%1];" : "=f"(other) : "r"(slot + 4 * 128 * (hf ^ 1)) : "memory");
+      const float mx = fmaxf(fmaxf(mr0, mr1), other) * p.sl2;
+      if (mx > m_used + kRescaleThresh) {  // both halves take the same decision
         if (j > 0) {
-          // O holds sum_{<j} 2^(x - m_used) V: rescale to the new reference max
+          // O holds sum_{<j} 2^(x - m_used) V: rescale this half's O columns to the new max
           mbar_wait(o_done + ((j - 1) & 1), ((j - 1) >> 1) & 1);
           tc_fence_after();
           const float f = exp2f(m_used - mx);
 #pragma unroll
-          for (int c = 0; c < HD / 32; ++c) {
+          for (int c = 0; c < OH / 32; ++c) {
             uint32_t rr[32];
-            tmem_ld_32x32b_x32(tmem + lane_addr + C::TMEM_O + c * 32, rr);
+            tmem_ld_32x32b_x32(tmem + lane_addr + C::TMEM_O + hf * OH + c * 32, rr);
             tmem_ld_wait();
 #pragma unroll
             for (int i = 0; i < 32; ++i) rr[i] = __float_as_uint(__uint_as_float(rr[i]) * f);
-            tmem_st_32x32b_x32(tmem + lane_addr + C::TMEM_O + c * 32, rr);
+            tmem_st_32x32b_x32(tmem + lane_addr + C::TMEM_O + hf * OH + c * 32, rr);
           }
           tmem_st_wait();
           l *= f;
@@ -242,11 +257,11 @@ __global__ void __launch_bounds__(256, 1)
         const int jp = j - C::NPB;
         mbar_wait(o_done + (jp & 1), (jp >> 1) & 1);
       }
-      const uint32_t sp = smem_u32(smem) + C::OFF_P + (j % C::NPB) * C::PTILE;
+      const uint32_t sp = smem_u32(smem) + C::OFF_P + (j % C::NPB) * C::PTILE + hf * (BQ * 128);
       float ls = 0.0f, ls2 = 0.0f;
       const float nm = -m_used;
 #pragma unroll
-      for (int c16 = 0; c16 < BKV / 8; ++c16) {
+      for (int c16 = 0; c16 < KH / 8; ++c16) {
         uint32_t w[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -257,24 +272,30 @@ __global__ void __launch_bounds__(256, 1)
           __nv_bfloat162 hh = __floats2bfloat162_rn(a, bb);
           w[i] = *reinterpret_cast<uint32_t*>(&hh);
         }
-        const int atom = c16 >> 3;  // 8 chunks of 8 keys per 64-key atom
-        sts128(sp + atom * (BQ * 128) + sw128_off(r, c16 & 7), make_uint4(w[0], w[1], w[2], w[3]));
+        sts128(sp + sw128_off(r, c16), make_uint4(w[0], w[1], w[2], w[3]));  // this half = one 64-key atom
       }
       l += ls + ls2;
       fence_async_smem();
       tc_fence_before();
       mbar_arrive(p_full + (j & 1));
     }
-    // epilogue: wait for the last PV, normalise, store O (bf16) and LSE
+    // row sum = both halves' partial sums
+    const uint32_t lslot = xch + 4 * (4 * 128 + r);
+    sts32f(lslot + 4 * 128 * hf, l);
+    named_sync(1 + qd, 64);
+    float lo;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(lo) : "r"(lslot + 4 * 128 * (hf ^ 1)) : "memory");
+    l += lo;
+    // epilogue: wait for the last PV, normalise, store this half's O columns (bf16) and LSE
     mbar_wait(o_done + ((nkv - 1) & 1), ((nkv - 1) >> 1) & 1);
     tc_fence_after();
     const float inv = l > 0.0f ? 1.0f / l : 0.0f;
     const bool row_ok = q < p.S;
-    __nv_bfloat16* orow = p.o + static_cast<long long>(row0 + q) * p.d + h * HD;
+    __nv_bfloat16* orow = p.o + static_cast<long long>(row0 + q) * p.d + h * HD + hf * OH;
 #pragma unroll
-    for (int c = 0; c < HD / 32; ++c) {
+    for (int c = 0; c < OH / 32; ++c) {
       uint32_t rr[32];
-      tmem_ld_32x32b_x32(tmem + lane_addr + C::TMEM_O + c * 32, rr);
+      tmem_ld_32x32b_x32(tmem + lane_addr + C::TMEM_O + hf * OH + c * 32, rr);
       tmem_ld_wait();
       if (row_ok) {
         uint32_t w[16];
@@ -288,7 +309,7 @@ __global__ void __launch_bounds__(256, 1)
         for (int i = 0; i < 4; ++i) dst[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
       }
     }
-    if (row_ok)
+    if (row_ok && hf == 0)
       p.lse[(static_cast<long long>(b) * p.H + h) * p.S + q] = (m_used + log2f(l)) * 0.6931471805599453f;
   }
   tc_fence_before();
@@ -329,7 +350,7 @@ p2r_status run(const void* qkv, const FwdParams& p, cudaStream_t s) {
   static cudaError_t attr = cudaFuncSetAttribute(attn_fwd_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   if (attr != cudaSuccess) return set_cuda_error(attr, "attention tc attr");
   dim3 grid((p.S + BQ - 1) / BQ, p.H, p.B);
-  P2R_LAUNCH_K("attention fwd (tcgen05)", attn_fwd_tc_kernel<HD>, grid, dim3(256), C::SMEM, s, 1, tm, p);
+  P2R_LAUNCH_K("attention fwd (tcgen05)", attn_fwd_tc_kernel<HD>, grid, dim3(384), C::SMEM, s, 1, tm, p);
   return P2R_OK;
 }
 

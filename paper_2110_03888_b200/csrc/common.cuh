@@ -134,6 +134,9 @@ P2R_DEVICE void umma_commit(uint64_t* bar) {
                : "memory");
 }
 
+// Advance a SW128 smem descriptor by `bytes` (added to the >>4 start-address field).
+P2R_DEVICE uint64_t desc_add(uint64_t d, uint32_t bytes) { return d + (bytes >> 4); }
+
 // Warp-collective variants: all 32 lanes execute with warp-uniform operands
 // (so they stay in uniform registers) and one elected lane issues. Called from
 // lane-0-only code, a tcgen05.mma costs R2UR moves plus an elect loop per MMA,

@@ -70,6 +70,17 @@ P2R_DEVICE void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t* r) {
       "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
       : "memory");
 }
+// 2^x on the FMA pipe (FA4-style MUFU offload): x = n + f with n = round(x) via
+// the 1.5*2^23 magic add, 2^f by a degree-3 fit on [-1/2, 1/2] (max rel. error
+// 1.4e-4, far below P's bf16 rounding), exponent added with integer ops.
+P2R_DEVICE float exp2_fma(float x) {
+  x = fmaxf(x, -125.0f);  // 2^n * p stays a normal float (masked scores -> ~2e-38)
+  const float magic = 12582912.0f;
+  const float t = x + magic;
+  const float f = x - (t - magic);
+  const float p = fmaf(fmaf(fmaf(5.502931029e-02f, f, 2.422568053e-01f), f, 6.932530403e-01f), f, 9.999513626e-01f);
+  return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - __float_as_int(magic)) << 23));
+}
 P2R_DEVICE void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 P2R_DEVICE void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 // 2^x on the SFU (inputs here are <= 8, outputs feed a bf16 MMA operand)
@@ -84,6 +95,14 @@ template <int HD>
 __global__ void __launch_bounds__(384, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const FwdParams p) {
   using C = Cfg<HD>;
+#ifdef P2R_ATTN_TRACE
+  // diagnostic build only: clock64 timeline of CTA (0,0,0) dumped over the start of `o`
+  __shared__ long long s_tr[256];
+  const bool tr_cta = blockIdx.x == gridDim.x - 1 && blockIdx.y == 0 && blockIdx.z == 0;
+#define TRF(slot) do { if (tr_cta) s_tr[(slot)] = clock64(); } while (0)
+#else
+#define TRF(slot) do {} while (0)
+#endif
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -119,6 +138,7 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) TRF(0);
   pdl_trigger();
   pdl_wait();
   const uint32_t sbase = smem_u32(smem);
@@ -155,6 +175,7 @@ __global__ void __launch_bounds__(384, 1)
       auto issue_pv = [&](int jj) {
         mbar_wait(p_full + (jj & 1), (jj >> 1) & 1);
         tc_fence_after();
+        if (lane == 0) TRF(8 + 4 * jj + 2);
         const uint32_t st = jj & 1;
         const uint64_t ap = desc_add(dP0, (jj % C::NPB) * C::PTILE), bv = desc_add(dV0, st * C::TILE);
 #pragma unroll
@@ -164,11 +185,13 @@ __global__ void __launch_bounds__(384, 1)
                          desc_add(bv, k * 2048), idesc_o, (jj > 0 || k > 0) ? 1u : 0u);
         umma_commit_warp(kv_empty + st);
         umma_commit_warp(o_done + (jj & 1));
+        if (lane == 0) TRF(8 + 4 * jj + 3);
       };
       for (int j = 0; j < nkv; ++j) {
         const uint32_t st = j & 1;
         mbar_wait(kv_full + st, (j >> 1) & 1);
         tc_fence_after();
+        if (lane == 0) TRF(8 + 4 * j);
         const uint64_t bk = desc_add(dK0, st * C::TILE);
         const uint32_t dS = tmem + ((j & 1) ? C::TMEM_S1 : C::TMEM_S0);
 #pragma unroll
@@ -176,6 +199,7 @@ __global__ void __launch_bounds__(384, 1)
           umma_bf16_warp(dS, desc_add(dQ0, (k >> 2) * (BQ * 128) + (k & 3) * 32),
                          desc_add(bk, (k >> 2) * (BKV * 128) + (k & 3) * 32), idesc_s, k > 0 ? 1u : 0u);
         umma_commit_warp(s_full + (j & 1));
+        if (lane == 0) TRF(8 + 4 * j + 1);
         if (j > 0) issue_pv(j - 1);
       }
       issue_pv(nkv - 1);
@@ -194,9 +218,12 @@ __global__ void __launch_bounds__(384, 1)
     // [parity][half][row] partial maxima, then [half][row] partial sums (after the barriers area)
     const uint32_t xch = smem_u32(smem) + C::OFF_BAR + 256;
     float m_used = -INFINITY, l = 0.0f;
+    const bool trw = warp == 4 && lane == 0;
+    (void)trw;
     for (int j = 0; j < nkv; ++j) {
       mbar_wait(s_full + (j & 1), (j >> 1) & 1);
       tc_fence_after();
+      if (trw) TRF(100 + 4 * j);
       const uint32_t tS = tmem + lane_addr + ((j & 1) ? C::TMEM_S1 : C::TMEM_S0) + hf * KH;
       float x[KH];
       {
@@ -228,6 +255,7 @@ __global__ void __launch_bounds__(384, 1)
       }
       const uint32_t slot = xch + 4 * (((j & 1) * 2) * 128 + r);
       sts32f(slot + 4 * 128 * hf, fmaxf(mr0, mr1));
+      if (trw) TRF(100 + 4 * j + 1);
       named_sync(1 + qd, 64);
       float other;
       asm volatile("ld.shared.f32 %0, [%1];" : "=f"(other) : "r"(slot + 4 * 128 * (hf ^ 1)) : "memory");
@@ -263,10 +291,13 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
       for (int c16 = 0; c16 < KH / 8; ++c16) {
         uint32_t w[4];
+        // the softmax is MUFU-bound (16 ex2/clk/SM): a quarter of the exponentials go to the FMA pipe
+        const bool fma_pipe = (c16 & 3) == 3;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const float a = ex2_approx(fmaf(x[c16 * 8 + 2 * i], p.sl2, nm));
-          const float bb = ex2_approx(fmaf(x[c16 * 8 + 2 * i + 1], p.sl2, nm));
+          const float za = fmaf(x[c16 * 8 + 2 * i], p.sl2, nm), zb = fmaf(x[c16 * 8 + 2 * i + 1], p.sl2, nm);
+          const float a = fma_pipe ? exp2_fma(za) : ex2_approx(za);
+          const float bb = fma_pipe ? exp2_fma(zb) : ex2_approx(zb);
           ls += a;
           ls2 += bb;
           __nv_bfloat162 hh = __floats2bfloat162_rn(a, bb);
@@ -275,9 +306,11 @@ __global__ void __launch_bounds__(384, 1)
         sts128(sp + sw128_off(r, c16), make_uint4(w[0], w[1], w[2], w[3]));  // this half = one 64-key atom
       }
       l += ls + ls2;
+      if (trw) TRF(100 + 4 * j + 2);
       fence_async_smem();
       tc_fence_before();
       mbar_arrive(p_full + (j & 1));
+      if (trw) TRF(100 + 4 * j + 3);
     }
     // row sum = both halves' partial sums
     const uint32_t lslot = xch + 4 * (4 * 128 + r);
@@ -309,11 +342,19 @@ __global__ void __launch_bounds__(384, 1)
         for (int i = 0; i < 4; ++i) dst[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
       }
     }
+#ifndef P2R_ATTN_TRACE  // trace builds dump the timeline over lse instead
     if (row_ok && hf == 0)
       p.lse[(static_cast<long long>(b) * p.H + h) * p.S + q] = (m_used + log2f(l)) * 0.6931471805599453f;
+#endif
   }
   tc_fence_before();
   __syncthreads();
+#ifdef P2R_ATTN_TRACE
+  if (threadIdx.x == 0) TRF(1);
+  if (tr_cta)
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) reinterpret_cast<long long*>(p.lse)[i] = s_tr[i];
+#endif
+#undef TRF
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);

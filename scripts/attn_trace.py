@@ -25,9 +25,20 @@ for _ in range(3):
     _lib.check(L.p2r_attention_fwd(P(qkv), P(o), P(lse), B, H, S, d, 1, st))
     _lib.check(L.p2r_attention_bwd(P(qkv), P(o), P(lse), P(do), P(dsum), P(dqkv), B, H, S, d, 1, st))
 torch.cuda.synchronize()
-t = o.view(torch.int64).flatten()[:512].cpu().numpy()
-t0 = t[0] if "--pp" not in sys.argv else min(v for v in t[16:300] if v > 0)
+t = o.view(torch.int64).flatten()[:512].cpu().numpy() if "--fwd" not in sys.argv else None
+t0 = None if t is None else (t[0] if "--pp" not in sys.argv else min(v for v in t[16:300] if v > 0))
 rel = lambda v: int(v - t0)
+if "--fwd" in sys.argv:
+    t = lse.view(torch.int64).flatten()[:256].cpu().numpy()
+    t0 = t[0]
+    print("fwd CTA (last q tile): setup->end", t[1] - t0)
+    print(" j | mma: kvfull  S-issued  p_full(j) PV-issued | sm(warp4): sfull  max-done  exps-done  arrived")
+    for j in range(16):
+        m = [t[8 + 4 * j + i] for i in range(4)]
+        a = [t[100 + 4 * j + i] for i in range(4)]
+        f = lambda v: f"{v - t0:8d}" if 0 < v - t0 < 10**9 else "       -"
+        print(f"{j:2d} | " + " ".join(f(v) for v in m) + " | " + " ".join(f(v) for v in a))
+    sys.exit(0)
 if "--pp" in sys.argv:
     print(" j | mma: kvfull(j+1) S(j+1)issued dQA(j) dQB(j) | A: sfull  sfree  stored  dsfull | B: sfull  sfree  stored  dsfull")
     for j in range(16):

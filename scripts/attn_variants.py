@@ -34,22 +34,30 @@ def variant(name, text):
     return text
 
 
-def main(names):
+def main(names, src=SRC):
+    """fwd variants: prefix the name with "fwd:" (patches csrc/attention_tc.cu)."""
     os.makedirs(OUT, exist_ok=True)
-    base = open(SRC).read().replace('"../../include/p2r_cuda.h"', '"p2r_cuda.h"')
-    others = [o for o in glob.glob(os.path.join(ROOT, "build/*.o")) if not o.endswith("attention_bwd_tc.o")]
+    stem = os.path.basename(src)[:-3]
+    base = open(src).read().replace('"../../include/p2r_cuda.h"', '"p2r_cuda.h"')
+    others = [o for o in glob.glob(os.path.join(ROOT, "build/*.o")) if not o.endswith(stem + ".o")]
     eng = glob.glob(os.path.join(ROOT, "build/engine/*.o"))
     for n in names:
-        cu = os.path.join(OUT, f"attention_bwd_tc_{n.replace('+', '_')}.cu")
+        cu = os.path.join(OUT, f"{stem}_{n.replace('+', '_')}.cu")
         open(cu, "w").write(variant(n, base))
         obj = cu[:-3].replace("+", "_") + ".o"
         subprocess.check_call(["nvcc", *ARCH, "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include"),
                                "-I" + os.path.join(ROOT, "paper_2110_03888_b200/csrc"), "--expt-relaxed-constexpr",
                                "-c", cu, "-o", obj])
-        subprocess.check_call(["nvcc", *ARCH, "-shared", "-o", os.path.join(OUT, f"libp2r_{n.replace('+', '_')}.so"), *others, obj, *eng,
+        subprocess.check_call(["nvcc", *ARCH, "-shared", "-o", os.path.join(OUT, f"libp2r_{'' if stem.startswith('attention_bwd') else stem + '_'}{n.replace('+', '_')}.so"), *others, obj, *eng,
                                "-cudart", "static"])
         print("built", n)
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["nomma", "nosm"])
+    args = sys.argv[1:] or ["nomma", "nosm"]
+    fwd = [a[4:] for a in args if a.startswith("fwd:")]
+    bwd = [a for a in args if not a.startswith("fwd:")]
+    if bwd:
+        main(bwd)
+    if fwd:
+        main(fwd, os.path.join(ROOT, "paper_2110_03888_b200/csrc/attention_tc.cu"))

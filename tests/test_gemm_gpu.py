@@ -100,6 +100,35 @@ def test_gemm_mn_major_acc(cuda, m, n, k, split):
     assert _rel(C, ref) < 1e-5
 
 
+@pytest.mark.parametrize("m,n,k", [(1024, 1024, 8192), (1024, 3072, 8192), (4096, 1024, 8192), (260, 1024, 8192),
+                                   (200, 136, 4000), (1000, 600, 3000)])
+def test_gemm_acc_auto_split(cuda, m, n, k):
+    """Auto split (split_k = 0) of C += A^T.B: wide splits accumulate in place in
+    split order (tile counters), narrow ones go through partials + reduce. Three
+    back-to-back launches reuse the counters; the result is bitwise stable."""
+    import torch
+    from paper_2110_03888_b200 import _lib
+    g = torch.Generator(device="cuda").manual_seed(3)
+    lda, ldb = (m + 7) // 8 * 8, (n + 7) // 8 * 8
+    X = torch.randn(k, lda, device=cuda, generator=g).bfloat16()
+    dY = torch.randn(k, ldb, device=cuda, generator=g).bfloat16()
+    W0 = torch.randn(m, n, device=cuda, generator=g)
+    outs = []
+    for _ in range(2):
+        C = W0.clone()
+        args = _args(m=m, n=n, k=k, a=_ptr(X), lda=lda, a_mn_major=1, b=_ptr(dY), ldb=ldb, b_mn_major=1,
+                     epi=_lib.EPI_ACC_F32, c=_ptr(C), ldc=n, split_k=0)
+        ws_bytes = _lib.lib().p2r_gemm_workspace_bytes(ctypes.byref(args))
+        ws = torch.empty(max(ws_bytes // 4, 1), device=cuda)
+        _lib.check(_lib.lib().p2r_set_workspace(_ptr(ws), ws_bytes))
+        for _ in range(3):
+            _run(args)
+        outs.append(C)
+    ref = W0 + 3 * (X[:, :m].float().T @ dY[:, :n].float())
+    assert _rel(outs[0], ref) < 1e-5
+    assert torch.equal(outs[0], outs[1])
+
+
 @pytest.mark.parametrize("amn,bmn", [(0, 1), (1, 0)])
 def test_gemm_mixed_major(cuda, amn, bmn):
     import torch

@@ -142,7 +142,7 @@ struct AttnParams {
 // ------------------------------- forward -------------------------------------
 template <int HD>
 __global__ void __launch_bounds__(256) attn_fwd_kernel(const AttnParams p) {
-  constexpr int BR = 128, BC = 64, NW = 8;
+  constexpr int BR = 128, BC = 64;
   extern __shared__ __align__(128) uint8_t smem[];
   const uint32_t sQ = smem_u32(smem);
   const uint32_t sK0 = sQ + BR * HD * 2;

@@ -214,6 +214,30 @@ P2R_DEVICE void umma_commit_pair(uint64_t* bar) {
       "}\n" ::"r"(smem_u32(bar))
       : "memory");
 }
+// Warp-collective pair variants (see umma_bf16_warp).
+P2R_DEVICE void umma_bf16_pair_warp(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                    uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+P2R_DEVICE void umma_commit_pair_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n"
+      ".reg .b16 m;\n"
+      ".reg .pred e;\n"
+      "mov.b16 m, 3;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n"
+      "}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
 // Arrive on the barrier at the same offset in CTA `rank` of the cluster.
 // Relaxed: the only ordering needed is of prior tcgen05 ops (tcgen05.fence::
 // before_thread_sync supplies it). A .release.cluster arrive compiles to

@@ -425,9 +425,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && leader) {
+    if (leader) {
       // ---------------- MMA issuer (pair: leader only, M = 256) ----------------
+      // Whole warp, one elected lane issues (uniform operands, no per-MMA
+      // R2UR / elect loop): issue stays far below the tensor pipe's 128
+      // cycles per MMA even when the epilogue warps saturate this SMSP.
       constexpr uint32_t idesc = make_idesc_bf16(BM * CG, BN, A_MN, B_MN);
+      constexpr uint32_t kStep = A_MN ? 2048 : 32;   // 16 K-elements: 16 MN-major rows / 32 B in the row
+      constexpr uint32_t kStepB = B_MN ? 2048 : 32;
+      const uint32_t sa0 = smem_u32(smem);
+      const uint64_t ad0 = A_MN ? make_sw128_desc(sa0, 64 * BK * 2, 1024) : make_sw128_desc(sa0, 16, 1024);
+      const uint64_t bd0 = B_MN ? make_sw128_desc(sa0 + Cfg::A_BYTES, 64 * BK * 2, 1024)
+                                : make_sw128_desc(sa0 + Cfg::A_BYTES, 16, 1024);
+      static_assert(!B_MN || BNC >= 64, "MN-major B slice must hold whole 64-column atoms");
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -441,35 +451,30 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         for (int kb = T.kb0; kb < T.kb1; ++kb) {
           mbar_wait(full_bar + stage, phase);
           tc_fence_after();
-          const uint32_t sa = smem_u32(smem + stage * Cfg::STAGE_BYTES);
-          const uint32_t sb = sa + Cfg::A_BYTES;
+          const uint32_t so = stage * Cfg::STAGE_BYTES;
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
-            // K-major: advance 16 elems = 32 B inside the swizzle row.
-            // MN-major: advance 16 K-rows = 2048 B.
-            const uint64_t ad = A_MN ? make_sw128_desc(sa + kk * 2048, 64 * BK * 2, 1024)
-                                     : make_sw128_desc(sa + kk * 32, 16, 1024);
-            const uint64_t bd = B_MN ? make_sw128_desc(sb + kk * 2048, 64 * BK * 2, 1024)
-                                     : make_sw128_desc(sb + kk * 32, 16, 1024);
-            static_assert(!B_MN || BNC >= 64, "MN-major B slice must hold whole 64-column atoms");
+            const uint64_t ad = desc_add(ad0, so + kk * kStep);
+            const uint64_t bd = desc_add(bd0, so + kk * kStepB);
+            const uint32_t accum = (kb > T.kb0 || kk > 0) ? 1u : 0u;
             if constexpr (CG == 2)
-              umma_bf16_pair(d_tmem, ad, bd, idesc, (kb > T.kb0 || kk > 0) ? 1u : 0u);
+              umma_bf16_pair_warp(d_tmem, ad, bd, idesc, accum);
             else
-              umma_bf16(d_tmem, ad, bd, idesc, (kb > T.kb0 || kk > 0) ? 1u : 0u);
+              umma_bf16_warp(d_tmem, ad, bd, idesc, accum);
           }
           if constexpr (CG == 2)
-            umma_commit_pair(empty_bar + stage);
+            umma_commit_pair_warp(empty_bar + stage);
           else
-            umma_commit(empty_bar + stage);
+            umma_commit_warp(empty_bar + stage);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
         if constexpr (CG == 2)
-          umma_commit_pair(tfull_bar + acc);
+          umma_commit_pair_warp(tfull_bar + acc);
         else
-          umma_commit(tfull_bar + acc);
+          umma_commit_warp(tfull_bar + acc);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;

@@ -29,6 +29,23 @@ def sub(text, a, b):
 def variant(name, text):
     if name == "noepi":
         text = sub(text, "if (nrows <= 0 || col0 >= p.n) continue;  // warp-uniform", "continue;")
+    elif name == "nogelu":  # GELU / GELU' replaced by identity (same loads and stores)
+        text = sub(text, "pack4_bf16(gelu_f(pre.x), gelu_f(pre.y), gelu_f(pre.z), gelu_f(pre.w));\n  } else if constexpr",
+                   "pack4_bf16(pre.x, pre.y, pre.z, pre.w);\n  } else if constexpr")
+        text = sub(text, """        pack4_bf16(v.x * gelu_grad_f(pre.x), v.y * gelu_grad_f(pre.y), v.z * gelu_grad_f(pre.z),
+                   v.w * gelu_grad_f(pre.w));
+  }
+}""", """        pack4_bf16(v.x * pre.x, v.y * pre.y, v.z * pre.z, v.w * pre.w);
+  }
+}""")
+    elif name == "noc2":  # BIAS_GELU without the pre-activation store
+        text = sub(text, """    const float4 pre = make_float4(v.x + b.x, v.y + b.y, v.z + b.z, v.w + b.w);
+    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.c2) + row * p.ldc2 + col) =
+        pack4_bf16(pre.x, pre.y, pre.z, pre.w);
+    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(cbase) + o) =
+        pack4_bf16(gelu_f(""", """    const float4 pre = make_float4(v.x + b.x, v.y + b.y, v.z + b.z, v.w + b.w);
+    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(cbase) + o) =
+        pack4_bf16(gelu_f(""")
     elif name == "nostage":
         text = sub(text, """        for (int q = 0; q < 8; ++q)
           *reinterpret_cast<float4*>(stg + lane * 32 + ((q ^ (lane & 7)) << 2)) =
@@ -105,6 +122,9 @@ def variant(name, text):
     for (int i = 0; i < 128; ++i) reinterpret_cast<long long*>(p.c)[i] = s_tr[i];
   }
 }""")
+    elif name == "trace1":  # the trace timeline of CTA 1 (the pair's second CTA)
+        text = variant("trace", text)
+        text = sub(text, "const bool trc = blockIdx.x == 0;", "const bool trc = blockIdx.x == 1;")
     elif name == "span":
         text = sub(text, """  const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;

@@ -386,41 +386,42 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   pdl_wait();  // operands / C / aux may come from the previous kernel
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ---------------- TMA producer ----------------
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int t = tile0; t < p.tiles_total; t += tile_step) {
-        const Tile T = get_tile(p, t, BN, CG, rank);
-        if (!T.valid) continue;
-        for (int kb = T.kb0; kb < T.kb1; ++kb) {
-          mbar_wait(empty_bar + stage, phase ^ 1);
-          uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
-          uint8_t* sb = sa + Cfg::A_BYTES;
-          // pair: the leader expects both CTAs' bytes; each CTA's loads count on it
-          if (leader) mbar_arrive_expect_tx(full_bar + stage, CG * Cfg::STAGE_BYTES);
-          auto load = [&](void* dst, const CUtensorMap* map, int c0, int c1) {
-            if constexpr (CG == 2)
-              tma_load_2d_pair(dst, map, pair_leader_addr(full_bar + stage), c0, c1);
-            else
-              tma_load_2d(dst, map, full_bar + stage, c0, c1);
-          };
-          if (!A_MN) {
-            load(sa, &tmA, kb * BK, T.a_row);
-          } else {
+    // ---------------- TMA producer (whole warp, one elected lane issues) ----------------
+    int stage = 0;
+    uint32_t phase = 0;
+    const uint32_t s0 = smem_u32(smem);
+    const uint32_t full0 = smem_u32(full_bar);
+    for (int t = tile0; t < p.tiles_total; t += tile_step) {
+      const Tile T = get_tile(p, t, BN, CG, rank);
+      if (!T.valid) continue;
+      for (int kb = T.kb0; kb < T.kb1; ++kb) {
+        mbar_wait(empty_bar + stage, phase ^ 1);
+        const uint32_t sa = s0 + stage * Cfg::STAGE_BYTES;
+        const uint32_t sb = sa + Cfg::A_BYTES;
+        const uint32_t fb = full0 + stage * 8;
+        // pair: the leader expects both CTAs' bytes; each CTA's loads count on it
+        if (leader) mbar_arrive_expect_tx_warp(fb, CG * Cfg::STAGE_BYTES);
+        auto load = [&](uint32_t dst, const CUtensorMap* map, int c0, int c1) {
+          if constexpr (CG == 2)
+            tma_load_2d_pair_warp(dst, map, fb & 0xFEFFFFFFu, c0, c1);  // the leader's barrier
+          else
+            tma_load_2d_warp(dst, map, fb, c0, c1);
+        };
+        if (!A_MN) {
+          load(sa, &tmA, kb * BK, T.a_row);
+        } else {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j) load(sa + j * 64 * BK * 2, &tmA, T.a_row + 64 * j, T.kbase + kb * BK);
-          }
-          if (!B_MN) {
-            load(sb, &tmB, kb * BK, T.b_row);
-          } else {
+          for (int j = 0; j < BM / 64; ++j) load(sa + j * 64 * BK * 2, &tmA, T.a_row + 64 * j, T.kbase + kb * BK);
+        }
+        if (!B_MN) {
+          load(sb, &tmB, kb * BK, T.b_row);
+        } else {
 #pragma unroll
-            for (int j = 0; j < BNC / 64; ++j) load(sb + j * 64 * BK * 2, &tmB, T.b_col + 64 * j, T.kbase + kb * BK);
-          }
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
+          for (int j = 0; j < BNC / 64; ++j) load(sb + j * 64 * BK * 2, &tmB, T.b_col + 64 * j, T.kbase + kb * BK);
+        }
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
         }
       }
     }
@@ -493,8 +494,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int t = tile0; t < p.tiles_total; t += tile_step) {
       const Tile T = get_tile(p, t, BN, CG, rank);
       if (!T.valid) continue;
-      mbar_wait(tfull_bar + acc, acc_phase);
-      tc_fence_after();
       const int row0 = T.m_blk * BM * CG + rank * BM + ew * 32;  // first local row drained by this warp
       long long grow0 = row0;
       int row_lim, zero_from = 1 << 30;
@@ -515,6 +514,26 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       const int nrows = min(32, row_lim - row0);
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
+      // lane = (row group, 4-column group): a warp instruction covers 4 rows x 32 columns
+      const int cg = lane & 7, rg = lane >> 3;
+      const int cb = chalf * (BN / 64), ce = cb + BN / 64;  // this warp's 32-column chunks
+      auto is_fast = [&](int c) {
+        const int c0 = T.n_blk * BN + c * 32;
+        return p.vec4 && nrows == 32 && c0 + 32 <= p.n && row0 + 32 <= zero_from;
+      };
+      // GELU' reads a read-only operand: fetch it one chunk ahead, the first
+      // chunk before the accumulator is even ready (DRAM latency off the chunk path)
+      constexpr bool kPipe = EPI == P2R_EPI_DGELU;
+      typename EpiOperand<EPI>::T xn[8];
+      if constexpr (kPipe) {
+        if (is_fast(cb)) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            xn[i] = epi_load<EPI>(p, grow0 + 4 * i + rg, T.n_blk * BN + cb * 32 + 4 * cg, cbase, ldc);
+        }
+      }
+      mbar_wait(tfull_bar + acc, acc_phase);
+      tc_fence_after();
       int* ctr = nullptr;
       if (p.serial) {  // earlier splits of this tile must have added into C (ordered -> deterministic)
         ctr = p.counters + (T.r * CG + rank);
@@ -527,16 +546,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         __syncwarp();
       }
 #pragma unroll 1
-      for (int c = chalf * (BN / 64); c < (chalf + 1) * (BN / 64); ++c) {
+      for (int c = cb; c < ce; ++c) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(taddr + c * 32, r);
         const int col0 = T.n_blk * BN + c * 32;
-        // lane = (row group, 4-column group): a warp instruction covers 4 rows x 32 columns
-        const int cg = lane & 7, rg = lane >> 3;
         const int col = col0 + 4 * cg;
-        const bool fast = p.vec4 && nrows == 32 && col0 + 32 <= p.n && row0 + 32 <= zero_from;
+        const bool fast = is_fast(c);
         typename EpiOperand<EPI>::T x[8];
-        if constexpr (EpiOperand<EPI>::kHas) {
+        if constexpr (kPipe) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) x[i] = xn[i];
+          if (c + 1 < ce && is_fast(c + 1)) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) xn[i] = epi_load<EPI>(p, grow0 + 4 * i + rg, col + 32, cbase, ldc);
+          }
+        } else if constexpr (EpiOperand<EPI>::kHas) {
           if (fast) {
 #pragma unroll
             for (int i = 0; i < 8; ++i) x[i] = epi_load<EPI>(p, grow0 + 4 * i + rg, col, cbase, ldc);

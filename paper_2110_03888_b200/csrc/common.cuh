@@ -106,6 +106,22 @@ P2R_DEVICE void mbar_arrive_expect_tx_warp(uint32_t bar, uint32_t bytes) {
       "r"(bytes)
       : "memory");
 }
+// TMA 2-D tile store shared -> global (bulk group of the issuing thread).
+P2R_DEVICE void tma_store_2d(const CUtensorMap* map, uint32_t smem_src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_src), "r"(c0), "r"(c1)
+               : "memory");
+}
+P2R_DEVICE void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// at most N of this thread's bulk groups may still be reading shared memory
+template <int N>
+P2R_DEVICE void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+P2R_DEVICE void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// generic-proxy shared-memory writes -> visible to the async proxy (TMA)
+P2R_DEVICE void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 // 1-D bulk async copy global -> shared (16-byte aligned, bytes % 16 == 0),
 // completion counted on `bar` (arrive.expect_tx by the issuing thread).
 P2R_DEVICE void bulk_load(uint32_t smem_dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -333,12 +349,17 @@ __host__ __device__ constexpr uint32_t make_idesc_bf16(int M, int N, bool a_mn, 
 // (x >= 0) or erfc/2; phi(x) = e / sqrt(2 pi) shares the exponential.
 // |error| vs float64 erf: gelu < 4e-7, gelu' < 4e-7 (outputs are bf16-rounded);
 // ~21 instructions, versus ~2x for the erff/expf pair.
-P2R_DEVICE void gelu_cdf_exp(float x, float& cdf, float& e) {
+// Phi(-|x|) = t * h(t) * e, t = 1/(1+|x|/(2 sqrt2)), e = exp(-x^2/2): one-ex2
+// erfc fit (degree 8, |err| < 4e-7). The scalar and pair (sm_100 FP32x2:
+// FFMA2/FMUL2, one issue slot for two lanes' worth of math -- the GELU
+// epilogues are issue-bound) forms run the same operations in the same order
+// with every fusion explicit (ptxas contracts f32x2 mul+add even with .rn), so
+// all epilogue paths round identically. Returns th = t*h; e via reference.
+P2R_DEVICE float gelu_th(float x, float& e) {
   float t;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(fmaf(fabsf(x), 0.35355339059327373f, 1.0f)));
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"((x * -0.72134752044448170f) * x));
-  float h = -2.377655916e-02f;
-  h = fmaf(h, t, 1.178763658e-01f);
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"((x * x) * -0.72134752044448170f));
+  float h = fmaf(-2.377655916e-02f, t, 1.178763658e-01f);
   h = fmaf(h, t, -2.006432861e-01f);
   h = fmaf(h, t, 9.842023998e-02f);
   h = fmaf(h, t, 8.996849880e-03f);
@@ -346,18 +367,52 @@ P2R_DEVICE void gelu_cdf_exp(float x, float& cdf, float& e) {
   h = fmaf(h, t, 1.228528991e-01f);
   h = fmaf(h, t, 1.410695761e-01f);
   h = fmaf(h, t, 1.410471797e-01f);
-  const float half_erfc = t * h * e;
-  cdf = x >= 0.0f ? 1.0f - half_erfc : half_erfc;
+  return t * h;
 }
+P2R_DEVICE float2 gelu_th2(float2 x, float2& e) {
+  float2 t;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t.x) : "f"(fmaf(fabsf(x.x), 0.35355339059327373f, 1.0f)));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t.y) : "f"(fmaf(fabsf(x.y), 0.35355339059327373f, 1.0f)));
+  const float2 a = __fmul2_rn(__fmul2_rn(x, x), make_float2(-0.72134752044448170f, -0.72134752044448170f));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.x) : "f"(a.x));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.y) : "f"(a.y));
+  auto c2 = [](float c) { return make_float2(c, c); };
+  float2 h = __ffma2_rn(c2(-2.377655916e-02f), t, c2(1.178763658e-01f));
+  h = __ffma2_rn(h, t, c2(-2.006432861e-01f));
+  h = __ffma2_rn(h, t, c2(9.842023998e-02f));
+  h = __ffma2_rn(h, t, c2(8.996849880e-03f));
+  h = __ffma2_rn(h, t, c2(9.415699542e-02f));
+  h = __ffma2_rn(h, t, c2(1.228528991e-01f));
+  h = __ffma2_rn(h, t, c2(1.410695761e-01f));
+  h = __ffma2_rn(h, t, c2(1.410471797e-01f));
+  return __fmul2_rn(t, h);
+}
+// gelu(x) = x Phi(x) = relu(x) - |x| Phi(-|x|)
 P2R_DEVICE float gelu_f(float v) {
-  float cdf, e;
-  gelu_cdf_exp(v, cdf, e);
-  return v * cdf;
+  float e;
+  const float he = gelu_th(v, e) * e;
+  return fmaf(-fabsf(v), he, fmaxf(v, 0.0f));
 }
+P2R_DEVICE float2 gelu2(float2 x) {
+  float2 e;
+  const float2 he = __fmul2_rn(gelu_th2(x, e), e);
+  return make_float2(fmaf(-fabsf(x.x), he.x, fmaxf(x.x, 0.0f)), fmaf(-fabsf(x.y), he.y, fmaxf(x.y, 0.0f)));
+}
+// gelu'(x) = Phi(x) + x phi(x);  Phi(x) = 0.5 + sign(x) (0.5 - th e)
 P2R_DEVICE float gelu_grad_f(float v) {
-  float cdf, e;
-  gelu_cdf_exp(v, cdf, e);
-  return fmaf(v * 0.39894228040143268f, e, cdf);
+  float e;
+  const float th = gelu_th(v, e);
+  const float m = __uint_as_float(__float_as_uint(fmaf(-th, e, 0.5f)) | (__float_as_uint(v) & 0x80000000u));
+  return fmaf(v * e, 0.39894228040143268f, 0.5f + m);
+}
+P2R_DEVICE float2 gelu_grad2(float2 x) {
+  float2 e;
+  const float2 th = gelu_th2(x, e);
+  float2 m = __ffma2_rn(make_float2(-th.x, -th.y), e, make_float2(0.5f, 0.5f));  // >= 0
+  m.x = __uint_as_float(__float_as_uint(m.x) | (__float_as_uint(x.x) & 0x80000000u));
+  m.y = __uint_as_float(__float_as_uint(m.y) | (__float_as_uint(x.y) & 0x80000000u));
+  const float2 cdf = __fadd2_rn(make_float2(0.5f, 0.5f), m);
+  return __ffma2_rn(__fmul2_rn(x, e), make_float2(0.39894228040143268f, 0.39894228040143268f), cdf);
 }
 
 P2R_DEVICE float warp_sum(float v) {

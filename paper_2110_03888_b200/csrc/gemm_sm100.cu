@@ -53,6 +53,7 @@ struct GemmParams {
   long long c_split_stride;  // elements between split-K partial outputs
   int vec4;                  // all epilogue leading dims / bases allow 4-wide accesses
   int raster_g;              // ungrouped tile order: groups of raster_g m-blocks x all n-blocks
+  int tma_c;                 // bf16 epilogues: stage 32x32 tiles in smem, TMA-store them (tmC / tmC2)
   // serial split-K (C += A.B only): split ks of tile r accumulates straight into C
   // once counters[r * CG + rank] == ks, then releases the next split
   int serial;
@@ -142,8 +143,8 @@ struct GemmCfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (196608 / STAGE_BYTES) > 8 ? 8 : (196608 / STAGE_BYTES);
   static constexpr int TMEM_COLS = (2 * BN) < 32 ? 32 : (2 * BN);
-  static constexpr int SMEM_BYTES =
-      STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + 8 * 4096 /*epilogue transpose*/;
+  static constexpr int STG_BYTES = 8 * 4096;  // per epilogue warp: transpose tile / two TMA-store slots
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + STG_BYTES + 256 /*barriers*/;
 };
 
 // Epilogue for ONE element: lane = column, so every global access of a warp is
@@ -195,6 +196,10 @@ P2R_DEVICE void epilogue_elem(const GemmParams& p, float v, long long row, int c
   }
 }
 
+P2R_DEVICE uint32_t pack2_bf16(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
 P2R_DEVICE uint2 pack4_bf16(float a, float b, float c, float d) {
   __nv_bfloat162 lo = __floats2bfloat162_rn(a, b), hi = __floats2bfloat162_rn(c, d);
   uint2 w;
@@ -316,16 +321,19 @@ P2R_DEVICE void epi_store_fast(const GemmParams& p, float4 v, typename EpiOperan
     *reinterpret_cast<float4*>(reinterpret_cast<float*>(cbase) + o) =
         make_float4(x.x + v.x, x.y + v.y, x.z + v.z, x.w + v.w);
   } else if constexpr (EPI == P2R_EPI_BIAS_GELU) {
-    const float4 pre = make_float4(v.x + b.x, v.y + b.y, v.z + b.z, v.w + b.w);
+    const float2 p0 = __fadd2_rn(make_float2(v.x, v.y), make_float2(b.x, b.y));
+    const float2 p1 = __fadd2_rn(make_float2(v.z, v.w), make_float2(b.z, b.w));
     *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.c2) + row * p.ldc2 + col) =
-        pack4_bf16(pre.x, pre.y, pre.z, pre.w);
+        make_uint2(pack2_bf16(p0.x, p0.y), pack2_bf16(p1.x, p1.y));
+    const float2 g0 = gelu2(p0), g1 = gelu2(p1);
     *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(cbase) + o) =
-        pack4_bf16(gelu_f(pre.x), gelu_f(pre.y), gelu_f(pre.z), gelu_f(pre.w));
+        make_uint2(pack2_bf16(g0.x, g0.y), pack2_bf16(g1.x, g1.y));
   } else if constexpr (EPI == P2R_EPI_DGELU) {
     const float4 pre = unpack4_bf16(x);
+    const float2 d0 = __fmul2_rn(make_float2(v.x, v.y), gelu_grad2(make_float2(pre.x, pre.y)));
+    const float2 d1 = __fmul2_rn(make_float2(v.z, v.w), gelu_grad2(make_float2(pre.z, pre.w)));
     *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(cbase) + o) =
-        pack4_bf16(v.x * gelu_grad_f(pre.x), v.y * gelu_grad_f(pre.y), v.z * gelu_grad_f(pre.z),
-                   v.w * gelu_grad_f(pre.w));
+        make_uint2(pack2_bf16(d0.x, d0.y), pack2_bf16(d1.x, d1.y));
   }
 }
 
@@ -335,6 +343,7 @@ constexpr int kGemmThreads = 128 + 32 * kEpiWarps;  // 4 control warps + epilogu
 template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
                 const GemmParams p) {
   using Cfg = GemmCfg<BN, CG>;
   constexpr int BNC = BN / CG;  // B rows (N) this CTA loads per stage
@@ -342,7 +351,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  uint8_t* stg_all = smem + STAGES * Cfg::STAGE_BYTES;  // 1024-aligned (the TMA-store swizzle needs 512)
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(stg_all + Cfg::STG_BYTES);
   uint64_t* empty_bar = full_bar + STAGES;
   uint64_t* tfull_bar = empty_bar + STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
@@ -488,7 +498,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int chalf = (warp - 4) >> 2;  // which half of the BN columns this warp drains
     // per-warp 32x32 fp32 transpose tile, XOR-swizzled: (r, c) at r*32 + (c ^ r)
     // (shared-space address: a generic pointer here compiles to LD/ST on the long scoreboard)
-    const uint32_t stg = smem_u32(reinterpret_cast<float*>(tmem_slot + 4) + (warp - 4) * 1024);
+    const uint32_t stg = smem_u32(stg_all) + (warp - 4) * 4096;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = tile0; t < p.tiles_total; t += tile_step) {
@@ -524,9 +534,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // GELU' reads a read-only operand: fetch it one chunk ahead, the first
       // chunk before the accumulator is even ready (DRAM latency off the chunk path)
       constexpr bool kPipe = EPI == P2R_EPI_DGELU;
+      constexpr bool kTmaEpi = EPI == P2R_EPI_BF16 || EPI == P2R_EPI_BIAS_GELU;  // (host: p2r_gemm tma_c)
+      const bool tma = kTmaEpi && p.tma_c;
       typename EpiOperand<EPI>::T xn[8];
       if constexpr (kPipe) {
-        if (is_fast(cb)) {
+        if (is_fast(cb) && !tma) {
 #pragma unroll
           for (int i = 0; i < 8; ++i)
             xn[i] = epi_load<EPI>(p, grow0 + 4 * i + rg, T.n_blk * BN + cb * 32 + 4 * cg, cbase, ldc);
@@ -545,8 +557,105 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
         __syncwarp();
       }
+      if constexpr (kTmaEpi) {
+        if (tma) {
+          // lane = row: compute in the TMEM layout, pack bf16, write the 32x32 tile
+          // once into a 64B-swizzled slot and TMA-store it (hardware clips ragged
+          // edges). Slots alternate per chunk; BIAS_GELU fills both (out, pre).
+          constexpr bool kTwo = EPI == P2R_EPI_BIAS_GELU;
+          const bool zrow = row0 + lane >= zero_from;  // grouped padding rows are written as 0
+          const bool rvalid = lane < nrows;
+          const long long grow = grow0 + lane;
 #pragma unroll 1
-      for (int c = cb; c < ce; ++c) {
+          for (int c = cb; c < ce; ++c) {
+            uint32_t r[32];
+            tmem_ld_32x32b_x32(taddr + c * 32, r);
+            const int col0 = T.n_blk * BN + c * 32;
+            const int nv = min(32, p.n - col0);  // valid columns of this chunk
+            float4 b4[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) b4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (bias != nullptr) {
+              if (nv == 32) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) b4[i] = __ldg(reinterpret_cast<const float4*>(bias + col0) + i);
+              } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                  if (j < nv) reinterpret_cast<float*>(b4)[j] = __ldg(bias + col0 + j);
+              }
+            }
+            uint32_t ax[16];  // GELU': this row's 32 pre-activations (bf16 pairs)
+            if constexpr (EPI == P2R_EPI_DGELU) {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) ax[j] = 0u;
+              if (rvalid && !zrow) {
+                const __nv_bfloat16* ap = static_cast<const __nv_bfloat16*>(p.aux) + grow * p.ldaux + col0;
+                if (nv == 32) {
+#pragma unroll
+                  for (int q = 0; q < 4; ++q) {
+                    const uint4 u = __ldg(reinterpret_cast<const uint4*>(ap) + q);
+                    ax[4 * q] = u.x, ax[4 * q + 1] = u.y, ax[4 * q + 2] = u.z, ax[4 * q + 3] = u.w;
+                  }
+                } else {
+                  const unsigned short* a16 = reinterpret_cast<const unsigned short*>(ap);
+#pragma unroll
+                  for (int j = 0; j < 32; ++j)
+                    if (j < nv) ax[j >> 1] |= static_cast<uint32_t>(__ldg(a16 + j)) << (16 * (j & 1));
+                }
+              }
+            }
+            tmem_ld_wait();
+            uint32_t o[16];
+            uint32_t pr[kTwo ? 16 : 1];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const float2 x = __fadd2_rn(make_float2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1])),
+                                          reinterpret_cast<const float2*>(b4)[j]);
+              if constexpr (EPI == P2R_EPI_BF16) {
+                o[j] = pack2_bf16(x.x, x.y);
+              } else if constexpr (EPI == P2R_EPI_BIAS_GELU) {
+                pr[j] = pack2_bf16(x.x, x.y);
+                const float2 g = gelu2(x);
+                o[j] = pack2_bf16(g.x, g.y);
+              } else {
+                const float2 d = __fmul2_rn(
+                    x, gelu_grad2(make_float2(__uint_as_float(ax[j] << 16), __uint_as_float(ax[j] & 0xFFFF0000u))));
+                o[j] = pack2_bf16(d.x, d.y);
+              }
+              if (zrow) {
+                o[j] = 0u;
+                if constexpr (kTwo) pr[j] = 0u;
+              }
+            }
+            const uint32_t slot = stg + (kTwo ? 0u : static_cast<uint32_t>(c & 1) * 2048u);
+            if (lane == 0) {
+              if constexpr (kTwo)
+                bulk_wait_read<0>();
+              else
+                bulk_wait_read<1>();
+            }
+            __syncwarp();
+            const uint32_t rowa = slot + lane * 64;
+            const uint32_t sw = (lane >> 1) & 3;  // SWIZZLE_64B: 16-byte chunk ^= address bits [7:8]
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              sts128(rowa + ((q ^ sw) << 4), make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]));
+              if constexpr (kTwo)
+                sts128(rowa + 2048 + ((q ^ sw) << 4), make_uint4(pr[4 * q], pr[4 * q + 1], pr[4 * q + 2], pr[4 * q + 3]));
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0 && nrows > 0 && nv > 0) {
+              tma_store_2d(&tmC, slot, col0, static_cast<int>(grow0));
+              if constexpr (kTwo) tma_store_2d(&tmC2, slot + 2048, col0, static_cast<int>(grow0));
+              bulk_commit();
+            }
+          }
+        }
+      }
+#pragma unroll 1
+      for (int c = cb; c < (tma ? cb : ce); ++c) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(taddr + c * 32, r);
         const int col0 = T.n_blk * BN + c * 32;
@@ -622,6 +731,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   }
+  if (warp >= 4 && lane == 0) bulk_wait_all();  // TMA stores done before the staging smem goes away
   tc_fence_before();
   if constexpr (CG == 2)
     cluster_sync();  // no CTA leaves while its peer may still signal or read it
@@ -706,6 +816,20 @@ bool make_map(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, u
   return r == CUDA_SUCCESS;
 }
 
+// bf16 [rows, cols] output, 32x32 boxes, 64-byte swizzle (the epilogue's staging layout)
+bool make_store_map(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint64_t ld) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 void* g_ws = nullptr;
 size_t g_ws_bytes = 0;
 
@@ -732,8 +856,8 @@ int* split_counters(cudaStream_t s, int n) {
 }
 
 template <int BN, bool AMN, bool BMN, int EPI, int CG>
-cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
-                   cudaStream_t s) {
+cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const CUtensorMap& tc2,
+                   const GemmParams& p, cudaStream_t s) {
   using Cfg = GemmCfg<BN, CG>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
@@ -746,11 +870,11 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParam
   const int grid = CG * (p.tiles_total < units ? p.tiles_total : units);
   if constexpr (CG == 1) {
     const cudaError_t e = launch_k(gemm_kernel<BN, AMN, BMN, EPI, 1>, dim3(grid), dim3(kGemmThreads),
-                                   Cfg::SMEM_BYTES, s, 1, ta, tb, p);
+                                   Cfg::SMEM_BYTES, s, 1, ta, tb, tc, tc2, p);
     if (e != cudaSuccess) return e;
   } else {
     const cudaError_t e = launch_k(gemm_kernel<BN, AMN, BMN, EPI, 2>, dim3(grid), dim3(kGemmThreads),
-                                   Cfg::SMEM_BYTES, s, 2, ta, tb, p);
+                                   Cfg::SMEM_BYTES, s, 2, ta, tb, tc, tc2, p);
     if (e != cudaSuccess) return e;
   }
   count_launch();
@@ -758,24 +882,25 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParam
 }
 
 template <int BN, bool AMN, bool BMN, int CG>
-cudaError_t dispatch_epi(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, cudaStream_t s) {
+cudaError_t dispatch_epi(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const CUtensorMap& tc2,
+                         const GemmParams& p, cudaStream_t s) {
   switch (p.epi) {
-    case P2R_EPI_BF16: return launch<BN, AMN, BMN, P2R_EPI_BF16, CG>(ta, tb, p, s);
-    case P2R_EPI_F32: return launch<BN, AMN, BMN, P2R_EPI_F32, CG>(ta, tb, p, s);
-    case P2R_EPI_ACC_F32: return launch<BN, AMN, BMN, P2R_EPI_ACC_F32, CG>(ta, tb, p, s);
-    case P2R_EPI_BIAS_GELU: return launch<BN, AMN, BMN, P2R_EPI_BIAS_GELU, CG>(ta, tb, p, s);
-    case P2R_EPI_DGELU: return launch<BN, AMN, BMN, P2R_EPI_DGELU, CG>(ta, tb, p, s);
-    default: return launch<BN, AMN, BMN, P2R_EPI_F32_BF16, CG>(ta, tb, p, s);
+    case P2R_EPI_BF16: return launch<BN, AMN, BMN, P2R_EPI_BF16, CG>(ta, tb, tc, tc2, p, s);
+    case P2R_EPI_F32: return launch<BN, AMN, BMN, P2R_EPI_F32, CG>(ta, tb, tc, tc2, p, s);
+    case P2R_EPI_ACC_F32: return launch<BN, AMN, BMN, P2R_EPI_ACC_F32, CG>(ta, tb, tc, tc2, p, s);
+    case P2R_EPI_BIAS_GELU: return launch<BN, AMN, BMN, P2R_EPI_BIAS_GELU, CG>(ta, tb, tc, tc2, p, s);
+    case P2R_EPI_DGELU: return launch<BN, AMN, BMN, P2R_EPI_DGELU, CG>(ta, tb, tc, tc2, p, s);
+    default: return launch<BN, AMN, BMN, P2R_EPI_F32_BF16, CG>(ta, tb, tc, tc2, p, s);
   }
 }
 
 template <int BN, int CG>
-cudaError_t dispatch_majors(bool amn, bool bmn, const CUtensorMap& ta, const CUtensorMap& tb,
-                            const GemmParams& p, cudaStream_t s) {
-  if (!amn && !bmn) return dispatch_epi<BN, false, false, CG>(ta, tb, p, s);
-  if (!amn && bmn) return dispatch_epi<BN, false, true, CG>(ta, tb, p, s);
-  if (amn && !bmn) return dispatch_epi<BN, true, false, CG>(ta, tb, p, s);
-  return dispatch_epi<BN, true, true, CG>(ta, tb, p, s);
+cudaError_t dispatch_majors(bool amn, bool bmn, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
+                            const CUtensorMap& tc2, const GemmParams& p, cudaStream_t s) {
+  if (!amn && !bmn) return dispatch_epi<BN, false, false, CG>(ta, tb, tc, tc2, p, s);
+  if (!amn && bmn) return dispatch_epi<BN, false, true, CG>(ta, tb, tc, tc2, p, s);
+  if (amn && !bmn) return dispatch_epi<BN, true, false, CG>(ta, tb, tc, tc2, p, s);
+  return dispatch_epi<BN, true, true, CG>(ta, tb, tc, tc2, p, s);
 }
 
 // CTA pairs for ungrouped 256-wide tiles unless the caller or P2R_GEMM_CG=1 says otherwise.
@@ -949,9 +1074,29 @@ extern "C" p2r_status p2r_gemm(const p2r_gemm_args* a, void* stream) {
                             : make_map(&tb, a->b, b_rows_k, a->k, a->ldb, 64, BN / CG));
   if (!ok) return set_error(P2R_ECUDA, "gemm: cuTensorMapEncodeTiled failed");
 
-  cudaError_t e = BN == 128 ? dispatch_majors<128, 1>(a->a_mn_major, a->b_mn_major, ta, tb, p, s)
-                 : CG == 2  ? dispatch_majors<256, 2>(a->a_mn_major, a->b_mn_major, ta, tb, p, s)
-                            : dispatch_majors<256, 1>(a->a_mn_major, a->b_mn_major, ta, tb, p, s);
+  // bf16 epilogues store through TMA when the outputs are TMA-addressable
+  CUtensorMap tc{}, tc2{};
+  {
+    static const bool tma_on = [] {
+      const char* e = std::getenv("P2R_GEMM_TMA_STORE");
+      return e == nullptr || std::atoi(e) != 0;
+    }();
+    auto a16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) % 16) == 0; };
+    // (GELU' keeps the per-thread path: its operand prefetch one chunk ahead measured faster)
+    const bool bf16_epi = a->epi == P2R_EPI_BF16 || a->epi == P2R_EPI_BIAS_GELU;
+    bool t = tma_on && bf16_epi && split == 1 && a->group_mode != P2R_GROUP_K && a->ldc % 8 == 0 && a16(a->c) &&
+             (a->bias == nullptr || a16(a->bias));
+    if (a->epi == P2R_EPI_BIAS_GELU) t = t && a->ldc2 % 8 == 0 && a16(a->c2);
+    if (a->epi == P2R_EPI_DGELU) t = t && a->ldaux % 8 == 0 && a16(a->aux);
+    const long long out_rows = a->group_mode == P2R_GROUP_M ? 1LL * a->groups * a->seg_rows : a->m;
+    if (t) t = make_store_map(&tc, a->c, out_rows, a->n, a->ldc);
+    if (t && a->epi == P2R_EPI_BIAS_GELU) t = make_store_map(&tc2, a->c2, out_rows, a->n, a->ldc2);
+    p.tma_c = t ? 1 : 0;
+  }
+
+  cudaError_t e = BN == 128 ? dispatch_majors<128, 1>(a->a_mn_major, a->b_mn_major, ta, tb, tc, tc2, p, s)
+                 : CG == 2  ? dispatch_majors<256, 2>(a->a_mn_major, a->b_mn_major, ta, tb, tc, tc2, p, s)
+                            : dispatch_majors<256, 1>(a->a_mn_major, a->b_mn_major, ta, tb, tc, tc2, p, s);
   if (e != cudaSuccess) return set_cuda_error(e, "gemm launch");
   if (split > 1 && !serial) {
     e = launch_k(splitk_reduce_kernel, dim3(a->m), dim3(256), 0, s, 1, static_cast<float*>(a->c), a->ldc,

@@ -1,0 +1,56 @@
+// Scalar vs FP32x2 GELU / GELU' bit-equality (both forms must round identically).
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -Ipaper_2110_03888_b200/csrc scripts/micro/gelu_pair_check.cu
+#include <cstdio>
+#include <cstdint>
+#include <cuda_bf16.h>
+#include "common.cuh"
+using namespace p2r;
+
+__global__ void check(unsigned* bad, uint32_t* ex, int mode, uint32_t n) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    float x0, x1;
+    if (mode == 0) {  // every bf16 value (GELU' operand)
+      x0 = __uint_as_float(i << 16);
+      x1 = __uint_as_float(((i * 40503u) & 0xFFFFu) << 16);
+    } else {  // hashed fp32 bit patterns (GELU operand)
+      uint32_t h = i * 2654435761u;
+      h ^= h >> 13;
+      x0 = __uint_as_float(h);
+      x1 = __uint_as_float(h * 2246822519u);
+    }
+    float2 s, v;
+    if (mode == 0) {
+      s = make_float2(gelu_grad_f(x0), gelu_grad_f(x1));
+      v = gelu_grad2(make_float2(x0, x1));
+    } else {
+      s = make_float2(gelu_f(x0), gelu_f(x1));
+      v = gelu2(make_float2(x0, x1));
+    }
+    auto same = [](float a, float b) { return __float_as_uint(a) == __float_as_uint(b) || (a != a && b != b); };
+    if (!same(s.x, v.x) || !same(s.y, v.y)) {
+      const unsigned k = atomicAdd(bad, 1u);
+      if (k < 8) {
+        ex[4 * k] = __float_as_uint(same(s.x, v.x) ? x1 : x0);
+        ex[4 * k + 1] = __float_as_uint(same(s.x, v.x) ? s.y : s.x);
+        ex[4 * k + 2] = __float_as_uint(same(s.x, v.x) ? v.y : v.x);
+      }
+    }
+  }
+}
+
+int main() {
+  unsigned* bad;
+  uint32_t* ex;
+  cudaMallocManaged(&bad, 4);
+  cudaMallocManaged(&ex, 4 * 8 * 4);
+  for (int mode = 0; mode < 2; ++mode) {
+    *bad = 0;
+    check<<<1184, 256>>>(bad, ex, mode, mode == 0 ? 65536u : (1u << 26));
+    cudaDeviceSynchronize();
+    printf("%s: %u mismatches\n", mode == 0 ? "gelu' (all bf16)" : "gelu (2^27 fp32)", *bad);
+    for (unsigned k = 0; k < (*bad < 8 ? *bad : 8); ++k)
+      printf("  x=%a scalar=%a pair=%a\n", __builtin_bit_cast(float, ex[4 * k]), __builtin_bit_cast(float, ex[4 * k + 1]),
+             __builtin_bit_cast(float, ex[4 * k + 2]));
+  }
+  return 0;
+}

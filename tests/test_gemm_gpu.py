@@ -78,6 +78,40 @@ def test_gemm_bias_gelu_and_dgelu(cuda, m, n, k):
     assert _rel(D, ref) < 8e-3
 
 
+@pytest.mark.parametrize("m,n,ldc,k", [(1000, 264, 264, 320), (300, 520, 528, 128), (130, 260, 260, 64),
+                                       (8192, 3072, 3072, 1024)])
+def test_gemm_bf16_epilogues_ragged(cuda, m, n, ldc, k):
+    """bf16 / bias+GELU / GELU' outputs with partial row tiles and column chunks: the
+    TMA-store epilogue (ldc % 8 == 0) clips at the edges and leaves padding columns
+    untouched; ldc % 8 != 0 takes the per-thread store path."""
+    import torch
+    from paper_2110_03888_b200 import _lib
+    g = torch.Generator(device="cuda").manual_seed(5)
+    A = torch.randn(m, k, device=cuda, generator=g).bfloat16()
+    B = (0.1 * torch.randn(n, k, device=cuda, generator=g)).bfloat16()
+    bias = torch.randn(n, device=cuda, generator=g) * 0.1
+    acc = A.float() @ B.float().T
+    Y = torch.full((m, ldc), 3.0, device=cuda).bfloat16()
+    _run(_args(m=m, n=n, k=k, a=_ptr(A), lda=k, b=_ptr(B), ldb=k, epi=_lib.EPI_BF16, c=_ptr(Y), ldc=ldc,
+               bias=_ptr(bias), split_k=1))
+    assert _rel(Y[:, :n], acc + bias) < 8e-3
+    assert bool((Y[:, n:] == 3.0).all())
+    G = torch.full((m, ldc), 3.0, device=cuda).bfloat16()
+    H = torch.full((m, ldc), 3.0, device=cuda).bfloat16()
+    _run(_args(m=m, n=n, k=k, a=_ptr(A), lda=k, b=_ptr(B), ldb=k, epi=_lib.EPI_BIAS_GELU, c=_ptr(G), ldc=ldc,
+               c2=_ptr(H), ldc2=ldc, bias=_ptr(bias), split_k=1))
+    assert _rel(H[:, :n], acc + bias) < 8e-3
+    assert _rel(G[:, :n], torch.nn.functional.gelu(acc + bias)) < 8e-3
+    assert bool((G[:, n:] == 3.0).all()) and bool((H[:, n:] == 3.0).all())
+    D = torch.full((m, ldc), 3.0, device=cuda).bfloat16()
+    _run(_args(m=m, n=n, k=k, a=_ptr(A), lda=k, b=_ptr(B), ldb=k, epi=_lib.EPI_DGELU, c=_ptr(D), ldc=ldc,
+               aux=_ptr(H), ldaux=ldc, split_k=1))
+    x = H[:, :n].float()
+    dg = 0.5 * (1 + torch.erf(x / 2 ** 0.5)) + x * torch.exp(-0.5 * x * x) / (2 * torch.pi) ** 0.5
+    assert _rel(D[:, :n], acc * dg) < 8e-3
+    assert bool((D[:, n:] == 3.0).all())
+
+
 @pytest.mark.parametrize("m,n,k,split", [(1024, 1024, 8192, 1), (1024, 3072, 8192, 4), (256, 260, 1024, 2), (200, 136, 1000, 3)])
 def test_gemm_mn_major_acc(cuda, m, n, k, split):
     """dW += X^T . dY with both operands token-major (MN-major) and beta=1."""

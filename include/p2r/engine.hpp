@@ -376,7 +376,7 @@ class Model {
             bool b_mn, int epi, void* c, int ldc, void* c2 = nullptr, int ldc2 = 0,
             const float* bias = nullptr, const void* aux = nullptr, int ldaux = 0,
             int group_mode = 0, int groups = 0, int seg_rows = 0, const int* counts = nullptr,
-            int split_k = 1);
+            int split_k = 1, float* bias_grad = nullptr);
 
   ModelConfig cfg_;
   int n_owned_ = 0;

@@ -86,10 +86,15 @@ typedef struct {
   /* 0 = auto, 1 = one CTA per 128x256 tile, 2 = CTA pair (cluster of 2,
    * tcgen05 cta_group::2) per 256x256 tile. Pairs apply to ungrouped GEMMs. */
   int cta_group;
+  /* EPI_DGELU, ungrouped: += column sums of the bf16 output into bias_grad[n]
+   * (the bias gradient of the layer whose pre-activation is aux; add_bias
+   * backward, tensor.cpp:227-231), from per-32-row partials the epilogue
+   * writes into the workspace (p2r_gemm_workspace_bytes). NULL = off. */
+  float* bias_grad;
 } p2r_gemm_args;
 
 p2r_status p2r_gemm(const p2r_gemm_args* args, void* stream);
-/* Bytes of workspace the library needs for split-K on this GEMM (0 if none). */
+/* Bytes of workspace the library needs for split-K / bias_grad partials (0 if none). */
 size_t p2r_gemm_workspace_bytes(const p2r_gemm_args* args);
 /* Supply caller-owned scratch (device) the library may use for split-K. */
 p2r_status p2r_set_workspace(void* ptr, size_t bytes);

@@ -55,6 +55,7 @@ class GemmArgs(ctypes.Structure):
         ("counts", ctypes.c_void_p),
         ("split_k", ctypes.c_int),
         ("cta_group", ctypes.c_int),
+        ("bias_grad", ctypes.c_void_p),
     ]
 
 

@@ -541,7 +541,7 @@ void Model::ensure_acts(int B, int S) {
 void Model::gemm(int m, int n, int k, const void* a, int lda, bool a_mn, const void* b, int ldb,
                  bool b_mn, int epi, void* c, int ldc, void* c2, int ldc2, const float* bias,
                  const void* aux, int ldaux, int group_mode, int groups, int seg_rows,
-                 const int* counts, int split_k) {
+                 const int* counts, int split_k, float* bias_grad) {
   p2r_gemm_args g{};
   g.m = m;
   g.n = n;
@@ -565,7 +565,8 @@ void Model::gemm(int m, int n, int k, const void* a, int lda, bool a_mn, const v
   g.seg_rows = seg_rows;
   g.counts = counts;
   g.split_k = split_k;
-  if (split_k != 1) {
+  g.bias_grad = bias_grad;
+  if (split_k != 1 || bias_grad != nullptr) {
     const std::size_t need = p2r_gemm_workspace_bytes(&g);
     if (splitk_ws_.bytes < need) splitk_ws_ = DevBuf(need);
     p2r_set_workspace(splitk_ws_.p, splitk_ws_.bytes);
@@ -757,16 +758,12 @@ void Model::block_backward(int g, AttentionMode mode) {
       p2r_check(p2r_bias_grad(dy, 0, d, T, d, 1, 0, nullptr, lg(o, layer_.b2), 0, A.colsum_ws.as<float>(), stream_),
                 "db2");
     });
+    // db1 += colsum(dh) is folded into the GELU' epilogue (column partials of the bf16 dh)
     gemm(T, dff, d, dy16, d, false, lp16(o, layer_.w2), d, false, P2R_EPI_DGELU, A.dh16.p, dff, nullptr, 0, nullptr,
-         L.hpre16.p, dff);
-    // FFN1: dW1 += b^T dh ; db1 += colsum(dh) ; db = dh W1^T
+         L.hpre16.p, dff, 0, 0, 0, nullptr, 1, lg(o, layer_.b1));
+    // FFN1: dW1 += b^T dh ; db = dh W1^T
     gemm(d, dff, T, L.b16.p, d, true, A.dh16.p, dff, true, P2R_EPI_ACC_F32, lg(o, layer_.w1), dff, nullptr, 0,
          nullptr, nullptr, 0, 0, 0, 0, nullptr, 0 /* library picks the split */);
-    prof(P2R_PROF_BIAS, 0, 2.0 * T * dff, [&] {
-      p2r_check(p2r_bias_grad(A.dh16.p, 1, dff, T, dff, 1, 0, nullptr, lg(o, layer_.b1), 0, A.colsum_ws.as<float>(),
-                              stream_),
-                "db1");
-    });
     gemm(T, d, dff, A.dh16.p, dff, false, lp16(o, layer_.w1), dff, false, P2R_EPI_F32, A.tmp32.p, d);
   } else {
     const int E = cfg_.moe.n_experts, k = cfg_.moe.n_prototypes, seg = A.seg;

@@ -54,6 +54,7 @@ struct GemmParams {
   int vec4;                  // all epilogue leading dims / bases allow 4-wide accesses
   int raster_g;              // ungrouped tile order: groups of raster_g m-blocks x all n-blocks
   int tma_c;                 // bf16 epilogues: stage 32x32 tiles in smem, TMA-store them (tmC / tmC2)
+  float* colsum;             // GELU' bias grad: per-32-row column partials [ceil(m/32)][n] of the bf16 output
   // serial split-K (C += A.B only): split ks of tile r accumulates straight into C
   // once counters[r * CG + rank] == ks, then releases the next split
   int serial;
@@ -150,9 +151,10 @@ struct GemmCfg {
 // Epilogue for ONE element: lane = column, so every global access of a warp is
 // row-contiguous (coalesced). `zero` stores zeros (padding rows of a grouped
 // segment) so later grouped-K GEMMs see clean K padding.
+// Returns the GELU' value (fp32, before bf16 rounding; feeds the bias-grad column sums).
 template <int EPI>
-P2R_DEVICE void epilogue_elem(const GemmParams& p, float v, long long row, int col, bool zero,
-                              float b, char* cbase, int ldc) {
+P2R_DEVICE float epilogue_elem(const GemmParams& p, float v, long long row, int col, bool zero,
+                               float b, char* cbase, int ldc) {
   constexpr int epi = EPI;
   if (zero) v = 0.0f;
   switch (epi) {
@@ -189,11 +191,12 @@ P2R_DEVICE void epilogue_elem(const GemmParams& p, float v, long long row, int c
         o = v * gelu_grad_f(pre);
       }
       reinterpret_cast<__nv_bfloat16*>(cbase)[row * ldc + col] = __float2bfloat16_rn(o);
-      break;
+      return o;
     }
     default:
       break;
   }
+  return 0.0f;
 }
 
 P2R_DEVICE uint32_t pack2_bf16(float a, float b) {
@@ -215,16 +218,18 @@ P2R_DEVICE float4 unpack4_bf16(uint2 w) {
 
 // Epilogue for 4 consecutive columns of one row (16 B fp32 / 8 B bf16 accesses).
 // EPI is a compile-time kind so each kernel instance carries only its own math.
+// Returns the 4 GELU' values (fp32; 0 for columns past n), else zeros.
 template <int EPI>
-P2R_DEVICE void epilogue_vec4(const GemmParams& p, float4 v, long long row, int col, int nc, bool zero,
-                              float4 b, char* cbase, int ldc) {
+P2R_DEVICE float4 epilogue_vec4(const GemmParams& p, float4 v, long long row, int col, int nc, bool zero,
+                                float4 b, char* cbase, int ldc) {
   if (nc < 4 || !p.vec4) {
     const float vv[4] = {v.x, v.y, v.z, v.w};
     const float bb[4] = {b.x, b.y, b.z, b.w};
+    float out[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int j = 0; j < 4; ++j)
-      if (j < nc) epilogue_elem<EPI>(p, vv[j], row, col + j, zero, bb[j], cbase, ldc);
-    return;
+      if (j < nc) out[j] = epilogue_elem<EPI>(p, vv[j], row, col + j, zero, bb[j], cbase, ldc);
+    return make_float4(out[0], out[1], out[2], out[3]);
   }
   const long long o = row * ldc + col;
   switch (EPI) {
@@ -274,11 +279,12 @@ P2R_DEVICE void epilogue_vec4(const GemmParams& p, float4 v, long long row, int 
                         v.w * gelu_grad_f(pre.w));
       }
       *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(cbase) + o) = pack4_bf16(r.x, r.y, r.z, r.w);
-      break;
+      return r;
     }
     default:
       break;
   }
+  return make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
 // Fast path (full 32x32 chunk, 16-byte aligned): the lane's global operand for
@@ -304,9 +310,10 @@ P2R_DEVICE typename EpiOperand<EPI>::T epi_load(const GemmParams& p, long long r
   }
 }
 
+// Returns the 4 GELU' values (fp32, before bf16 rounding), else zeros.
 template <int EPI>
-P2R_DEVICE void epi_store_fast(const GemmParams& p, float4 v, typename EpiOperand<EPI>::T x, long long row,
-                               int col, float4 b, char* cbase, int ldc) {
+P2R_DEVICE float4 epi_store_fast(const GemmParams& p, float4 v, typename EpiOperand<EPI>::T x, long long row,
+                                 int col, float4 b, char* cbase, int ldc) {
   const long long o = row * ldc + col;
   if constexpr (EPI == P2R_EPI_BF16) {
     *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(cbase) + o) =
@@ -334,17 +341,24 @@ P2R_DEVICE void epi_store_fast(const GemmParams& p, float4 v, typename EpiOperan
     const float2 d1 = __fmul2_rn(make_float2(v.z, v.w), gelu_grad2(make_float2(pre.z, pre.w)));
     *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(cbase) + o) =
         make_uint2(pack2_bf16(d0.x, d0.y), pack2_bf16(d1.x, d1.y));
+    return make_float4(d0.x, d0.y, d1.x, d1.y);
   }
+  return make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
 constexpr int kEpiWarps = 8;                       // 2 per TMEM lane quadrant
 constexpr int kGemmThreads = 128 + 32 * kEpiWarps;  // 4 control warps + epilogue
 
-template <int BN, bool A_MN, bool B_MN, int EPI, int CG>
+// EPI_ = epilogue kind | kEpiColsum (GELU' + bias-grad column partials).
+constexpr int kEpiColsum = 0x100;
+
+template <int BN, bool A_MN, bool B_MN, int EPI_, int CG>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
                 const GemmParams p) {
+  constexpr int EPI = EPI_ & 0xFF;
+  constexpr bool kColsum = (EPI_ & kEpiColsum) != 0;
   using Cfg = GemmCfg<BN, CG>;
   constexpr int BNC = BN / CG;  // B rows (N) this CTA loads per stage
   constexpr int STAGES = Cfg::STAGES;
@@ -690,12 +704,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if (nc > 2) b4.z = __ldg(bias + col + 2);
           if (nc > 3) b4.w = __ldg(bias + col + 3);
         }
+        // GELU' bias grad (kColsum): this lane's fp32 column sums over its 8 rows, in row order
+        float2 cs01 = make_float2(0.f, 0.f), cs23 = make_float2(0.f, 0.f);
+        auto acc_cs = [&](float4 w) {
+          if constexpr (kColsum) {
+            cs01 = __fadd2_rn(cs01, make_float2(w.x, w.y));
+            cs23 = __fadd2_rn(cs23, make_float2(w.z, w.w));
+          }
+        };
         if (fast) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int rr = 4 * i + rg;
             const float4 v = lds128f(stg + 4 * (rr * 32 + ((cg ^ (rr & 7)) << 2)));
-            epi_store_fast<EPI>(p, v, x[i], grow0 + rr, col, b4, cbase, ldc);
+            acc_cs(epi_store_fast<EPI>(p, v, x[i], grow0 + rr, col, b4, cbase, ldc));
           }
         } else {
 #pragma unroll 2
@@ -703,7 +725,30 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const int rr = 4 * i + rg;
             if (rr >= nrows || nc <= 0) continue;
             const float4 v = lds128f(stg + 4 * (rr * 32 + ((cg ^ (rr & 7)) << 2)));
-            epilogue_vec4<EPI>(p, v, grow0 + rr, col, nc, row0 + rr >= zero_from, b4, cbase, ldc);
+            acc_cs(epilogue_vec4<EPI>(p, v, grow0 + rr, col, nc, row0 + rr >= zero_from, b4, cbase, ldc));
+          }
+        }
+        if constexpr (kColsum) {
+          {  // fixed-order tree over the 4 row groups -> the warp's 32 rows
+#pragma unroll
+            for (int o = 8; o <= 16; o <<= 1) {
+              cs01 = __fadd2_rn(cs01, make_float2(__shfl_xor_sync(0xffffffffu, cs01.x, o),
+                                                  __shfl_xor_sync(0xffffffffu, cs01.y, o)));
+              cs23 = __fadd2_rn(cs23, make_float2(__shfl_xor_sync(0xffffffffu, cs23.x, o),
+                                                  __shfl_xor_sync(0xffffffffu, cs23.y, o)));
+            }
+            const float4 cs = make_float4(cs01.x, cs01.y, cs23.x, cs23.y);
+            if (rg == 0 && nc > 0) {
+              float* dst = p.colsum + (grow0 >> 5) * p.n + col;
+              if (nc == 4 && (p.n & 3) == 0) {
+                *reinterpret_cast<float4*>(dst) = cs;
+              } else {
+                dst[0] = cs.x;
+                if (nc > 1) dst[1] = cs.y;
+                if (nc > 2) dst[2] = cs.z;
+                if (nc > 3) dst[3] = cs.w;
+              }
+            }
           }
         }
         __syncwarp();
@@ -889,7 +934,9 @@ cudaError_t dispatch_epi(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
     case P2R_EPI_F32: return launch<BN, AMN, BMN, P2R_EPI_F32, CG>(ta, tb, tc, tc2, p, s);
     case P2R_EPI_ACC_F32: return launch<BN, AMN, BMN, P2R_EPI_ACC_F32, CG>(ta, tb, tc, tc2, p, s);
     case P2R_EPI_BIAS_GELU: return launch<BN, AMN, BMN, P2R_EPI_BIAS_GELU, CG>(ta, tb, tc, tc2, p, s);
-    case P2R_EPI_DGELU: return launch<BN, AMN, BMN, P2R_EPI_DGELU, CG>(ta, tb, tc, tc2, p, s);
+    case P2R_EPI_DGELU:
+      if (p.colsum != nullptr) return launch<BN, AMN, BMN, P2R_EPI_DGELU | kEpiColsum, CG>(ta, tb, tc, tc2, p, s);
+      return launch<BN, AMN, BMN, P2R_EPI_DGELU, CG>(ta, tb, tc, tc2, p, s);
     default: return launch<BN, AMN, BMN, P2R_EPI_F32_BF16, CG>(ta, tb, tc, tc2, p, s);
   }
 }
@@ -966,6 +1013,7 @@ int effective_split(const p2r_gemm_args* a) {
 using namespace p2r;
 
 extern "C" size_t p2r_gemm_workspace_bytes(const p2r_gemm_args* a) {
+  if (a->bias_grad != nullptr) return static_cast<size_t>((a->m + 31) / 32) * a->n * sizeof(float);
   const int s = effective_split(a);
   if (s <= 1) return 0;
   if (serial_split_ok(a, s)) return 0;  // serial split-K accumulates in place
@@ -1024,6 +1072,13 @@ extern "C" p2r_status p2r_gemm(const p2r_gemm_args* a, void* stream) {
   p.seg_rows = a->seg_rows;
   p.counts = a->counts;
   p.split_k = split;
+  if (a->bias_grad != nullptr) {
+    if (a->epi != P2R_EPI_DGELU || a->group_mode != P2R_GROUP_NONE || split != 1)
+      return set_error(P2R_EINVAL, "gemm: bias_grad needs EPI_DGELU, ungrouped, no split");
+    if (g_ws == nullptr || g_ws_bytes < p2r_gemm_workspace_bytes(a))
+      return set_error(P2R_ERUNTIME, "gemm: bias_grad workspace too small (p2r_gemm_workspace_bytes)");
+    p.colsum = static_cast<float*>(g_ws);
+  }
   const bool serial = split > 1 && serial_split_ok(a, split);
   if (serial) {
     p.serial = 1;
@@ -1098,6 +1153,11 @@ extern "C" p2r_status p2r_gemm(const p2r_gemm_args* a, void* stream) {
                  : CG == 2  ? dispatch_majors<256, 2>(a->a_mn_major, a->b_mn_major, ta, tb, tc, tc2, p, s)
                             : dispatch_majors<256, 1>(a->a_mn_major, a->b_mn_major, ta, tb, tc, tc2, p, s);
   if (e != cudaSuccess) return set_cuda_error(e, "gemm launch");
+  if (a->bias_grad != nullptr) {  // bias_grad += sum of the per-32-row partials, in row-block order
+    e = colsum_finish_launch(static_cast<const float*>(g_ws), (a->m + 31) / 32, a->n, 1, a->bias_grad, 0, s);
+    count_launch();
+    if (e != cudaSuccess) return set_cuda_error(e, "bias grad finish launch");
+  }
   if (split > 1 && !serial) {
     e = launch_k(splitk_reduce_kernel, dim3(a->m), dim3(256), 0, s, 1, static_cast<float*>(a->c), a->ldc,
                  static_cast<const float*>(g_ws), a->m, a->n, split, a->epi == P2R_EPI_ACC_F32 ? 1 : 0);

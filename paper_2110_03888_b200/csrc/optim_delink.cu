@@ -207,6 +207,13 @@ __global__ void __launch_bounds__(1024) colsum_finish_kernel(const float* __rest
   }
 }
 
+cudaError_t colsum_finish_launch(const float* partial, int nchunks, int n, int groups, float* out,
+                                 long long out_group_stride, cudaStream_t s) {
+  const cudaError_t e = launch_k(colsum_finish_kernel, dim3((n + 31) / 32, groups), dim3(1024), 0, s, 1, partial,
+                                 nchunks, n, groups, out, out_group_stride);
+  return e == cudaSuccess ? cudaGetLastError() : e;
+}
+
 }  // namespace p2r
 
 using namespace p2r;

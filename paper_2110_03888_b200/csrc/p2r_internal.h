@@ -23,6 +23,11 @@ p2r_status attention_bwd_tc(const void* qkv, const void* o, const float* lse, co
 // Launch with programmatic dependent launch (and an optional cluster size). The
 // kernel must call pdl_wait() before reading data produced earlier in the stream.
 // P2R_PDL=0 falls back to plain stream-ordered launches (A/B diagnostics).
+// out[g * out_group_stride + col] += sum over c < nchunks of partial[(g * nchunks + c) * n + col]
+// (fixed order; optim_delink.cu). Shared by p2r_bias_grad and the GELU' GEMM epilogue.
+cudaError_t colsum_finish_launch(const float* partial, int nchunks, int n, int groups, float* out,
+                                 long long out_group_stride, cudaStream_t s);
+
 inline bool pdl_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("P2R_PDL");

@@ -8,7 +8,7 @@ sys.path.insert(0, ".")
 from paper_2110_03888_b200 import _lib  # noqa: E402
 
 
-def run(m, n, k, amn=0, bmn=0, epi=_lib.EPI_BF16, split=1, iters=20):
+def run(m, n, k, amn=0, bmn=0, epi=_lib.EPI_BF16, split=1, iters=20, bias_grad=False):
     dev = torch.device("cuda")
     A = torch.randn(k, m, device=dev).bfloat16() if amn else torch.randn(m, k, device=dev).bfloat16()
     B = torch.randn(k, n, device=dev).bfloat16() if bmn else torch.randn(n, k, device=dev).bfloat16()
@@ -26,6 +26,9 @@ def run(m, n, k, amn=0, bmn=0, epi=_lib.EPI_BF16, split=1, iters=20):
         args.c = C2.data_ptr()
         args.aux = AUX.data_ptr()
         args.ldaux = n
+    if bias_grad:
+        DB = torch.zeros(n, device=dev)
+        args.bias_grad = DB.data_ptr()
     ws = torch.empty(max(1, _lib.lib().p2r_gemm_workspace_bytes(ctypes.byref(args)) // 4), device=dev)
     _lib.check(_lib.lib().p2r_set_workspace(ws.data_ptr(), ws.numel() * 4))
     s = torch.cuda.current_stream().cuda_stream
@@ -52,7 +55,7 @@ def run(m, n, k, amn=0, bmn=0, epi=_lib.EPI_BF16, split=1, iters=20):
     e1.record()
     torch.cuda.synchronize()
     ms_t = e0.elapsed_time(e1) / iters
-    print(f"m={m:6d} n={n:5d} k={k:5d} amn={amn} bmn={bmn} epi={epi} split={split}: "
+    print(f"m={m:6d} n={n:5d} k={k:5d} amn={amn} bmn={bmn} epi={epi} split={split}{' +db' if bias_grad else ''}: "
           f"{ms*1e3:8.1f} us {tf:7.1f} TFLOP/s   (cuBLAS {ms_t*1e3:8.1f} us {2.0*m*n*k/ms_t/1e9:7.1f})")
 
 

@@ -112,6 +112,39 @@ def test_gemm_bf16_epilogues_ragged(cuda, m, n, ldc, k):
     assert bool((D[:, n:] == 3.0).all())
 
 
+@pytest.mark.parametrize("m,n,ldc,k", [(8192, 4096, 4096, 1024), (1000, 264, 264, 320), (77, 130, 136, 64)])
+def test_gemm_dgelu_bias_grad(cuda, m, n, ldc, k):
+    """GELU' with bias_grad: the epilogue's per-32-row column partials of the fp32
+    GELU' output (before its bf16 rounding, as the reference's fp32 colsum) + the
+    finish kernel add the column sums into bias_grad."""
+    import torch
+    from paper_2110_03888_b200 import _lib
+    g = torch.Generator(device="cuda").manual_seed(6)
+    A = torch.randn(m, k, device=cuda, generator=g).bfloat16()
+    B = (0.1 * torch.randn(n, k, device=cuda, generator=g)).bfloat16()
+    H = torch.randn(m, ldc, device=cuda, generator=g).bfloat16()
+    D = torch.empty(m, ldc, device=cuda).bfloat16()
+    db0 = torch.randn(n, device=cuda, generator=g)
+    db = db0.clone()
+    args = _args(m=m, n=n, k=k, a=_ptr(A), lda=k, b=_ptr(B), ldb=k, epi=_lib.EPI_DGELU, c=_ptr(D), ldc=ldc,
+                 aux=_ptr(H), ldaux=ldc, split_k=1, bias_grad=_ptr(db))
+    ws_bytes = _lib.lib().p2r_gemm_workspace_bytes(ctypes.byref(args))
+    assert ws_bytes == (m + 31) // 32 * n * 4
+    ws = torch.empty(ws_bytes // 4, device=cuda)
+    _lib.check(_lib.lib().p2r_set_workspace(_ptr(ws), ws_bytes))
+    _run(args)
+    x = H[:, :n].float()
+    dg = 0.5 * (1 + torch.erf(x / 2 ** 0.5)) + x * torch.exp(-0.5 * x * x) / (2 * torch.pi) ** 0.5
+    assert _rel(D[:, :n], (A.float() @ B.float().T) * dg) < 8e-3
+    terms = (A.double() @ B.double().T) * dg.double()
+    ref = db0.double() + terms.sum(0)
+    assert bool(((db.double() - ref).abs() <= 1e-5 * terms.abs().sum(0) + 1e-6).all())
+    with pytest.raises(Exception, match="bias_grad"):
+        bad = _args(m=m, n=n, k=k, a=_ptr(A), lda=k, b=_ptr(B), ldb=k, epi=_lib.EPI_BF16, c=_ptr(D), ldc=ldc,
+                    split_k=1, bias_grad=_ptr(db))
+        _run(bad)
+
+
 @pytest.mark.parametrize("m,n,k,split", [(1024, 1024, 8192, 1), (1024, 3072, 8192, 4), (256, 260, 1024, 2), (200, 136, 1000, 3)])
 def test_gemm_mn_major_acc(cuda, m, n, k, split):
     """dW += X^T . dY with both operands token-major (MN-major) and beta=1."""

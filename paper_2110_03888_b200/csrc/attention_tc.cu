@@ -5,16 +5,20 @@
 // projection [T, 3d]; O is written merged-head [T, d]; the row log-sum-exp is
 // saved for the backward instead of the S x S probability matrix.
 //
-// One CTA = one (batch, head, 128-query tile), 8 warps:
-//   warp 0     TMA producer: Q once, K/V tiles (128 keys) through a 2-stage ring
-//   warp 1     MMA issuer (one lane): S_j = Q.K_j^T into a double-buffered TMEM
-//              S tile, then O += P_{j-1}.V_{j-1} (P from smem, V MN-major)
-//   warp 2     TMEM allocator (S0 | S1 | O columns)
-//   warps 4-7  softmax: thread t owns query row t (TMEM lane t): reads its S
-//              row, causal mask, online softmax with CONDITIONAL rescaling of
-//              O (only when the running max grows by > 2^8), writes bf16 P into
-//              a SWIZZLE_128B K-major smem tile, finally normalises O and
-//              stores O / LSE.
+// Persistent: one CTA per SM walks (query tile, head, batch) work items,
+// heaviest causal tiles first, round-robin over CTAs; every pipeline counter
+// runs across items, so the next item's Q/K/V loads, S MMAs and PVs overlap
+// the current item's tail (O is double-buffered in TMEM). 12 warps:
+//   warp 0     TMA producer: Q per item (double-buffered for hd 64), K/V tiles
+//              (128 keys) through an NKV-stage ring
+//   warp 1     MMA issuer (whole warp, elected lane): S_g = Q.K_g^T into a
+//              double-buffered TMEM S tile, then O += P_{g-1}.V_{g-1}
+//   warp 2     TMEM allocator (S0 | S1 | O0 | O1 columns)
+//   warps 4-11 softmax: two warps per TMEM lane quadrant (query row), each
+//              owning half the keys of a block: causal mask, online softmax
+//              with CONDITIONAL rescaling of O (only when the running max grows
+//              by > 2^8), bf16 P into a SWIZZLE_128B K-major smem tile; per
+//              item, normalise O and store O / LSE.
 #include <cudaTypedefs.h>
 
 #include <mutex>
@@ -29,6 +33,11 @@ namespace attn_tc {
 constexpr int BQ = 128, BKV = 128;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThresh = 8.0f;  // log2 units: P stays <= 256 in bf16
+#ifndef P2R_ATTN_FMA_CHUNKS
+#define P2R_ATTN_FMA_CHUNKS 2
+#endif
+// of each half-row's 8 eight-key chunks, this many take exp2 on the FMA pipe
+constexpr int kFmaChunks = P2R_ATTN_FMA_CHUNKS;
 
 template <int HD>
 struct Cfg {
@@ -36,14 +45,18 @@ struct Cfg {
   static constexpr int TILE = BQ * HD * 2;               // Q / K / V tile bytes
   static constexpr int PTILE = BQ * BKV * 2;             // P tile bytes
   static constexpr int NPB = HD == 64 ? 2 : 1;           // P buffers
+  // K/V ring depth: with 2 stages the load of block j+2 waits for PV(j) and its
+  // latency lands on every block (trace: ~1.9k vs ~1.4k softmax cycles/block)
+  static constexpr int NKV = HD == 64 ? 3 : 2;
+  static constexpr int NQ = HD == 64 ? 2 : 1;  // Q buffers (the next item's Q loads early)
   static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = OFF_Q + TILE;
-  static constexpr int OFF_V = OFF_K + 2 * TILE;
-  static constexpr int OFF_P = OFF_V + 2 * TILE;
+  static constexpr int OFF_K = OFF_Q + NQ * TILE;
+  static constexpr int OFF_V = OFF_K + NKV * TILE;
+  static constexpr int OFF_P = OFF_V + NKV * TILE;
   static constexpr int OFF_BAR = OFF_P + NPB * PTILE;
   static constexpr int XCH = (2 * 2 + 2) * 128 * 4;   // row-max exchange [2][2][128] + sums [2][128]
   static constexpr int SMEM = OFF_BAR + 256 + XCH + 1024;
-  static constexpr int TMEM_S0 = 0, TMEM_S1 = 128, TMEM_O = 256;
+  static constexpr int TMEM_S0 = 0, TMEM_S1 = 128, TMEM_O = 256;  // O buffer ob at TMEM_O + ob * HD
 };
 
 struct FwdParams {
@@ -81,6 +94,29 @@ P2R_DEVICE float exp2_fma(float x) {
   const float p = fmaf(fmaf(fmaf(5.502931029e-02f, f, 2.422568053e-01f), f, 6.932530403e-01f), f, 9.999513626e-01f);
   return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - __float_as_int(magic)) << 23));
 }
+// Pair form on the FP32x2 pipe (FFMA2/FADD2): the softmax is issue-bound.
+// t = z + M rounds z to an integer n (exact: M = 1.5*2^23), -n = M - t and
+// f = z - n are exact, so this matches exp2_fma bit-for-bit.
+P2R_DEVICE float2 exp2_fma2(float2 z) {
+  z.x = fmaxf(z.x, -125.0f);
+  z.y = fmaxf(z.y, -125.0f);
+  const float2 M = make_float2(12582912.0f, 12582912.0f);
+  const float2 t = __fadd2_rn(z, M);
+  const float2 nn = __ffma2_rn(t, make_float2(-1.0f, -1.0f), M);  // -n
+  const float2 f = __fadd2_rn(z, nn);
+  float2 q = __ffma2_rn(make_float2(5.502931029e-02f, 5.502931029e-02f), f,
+                        make_float2(2.422568053e-01f, 2.422568053e-01f));
+  q = __ffma2_rn(q, f, make_float2(6.932530403e-01f, 6.932530403e-01f));
+  q = __ffma2_rn(q, f, make_float2(9.999513626e-01f, 9.999513626e-01f));
+  constexpr uint32_t kMagicExp = 0x4B400000u << 23;  // (bits of M) << 23 mod 2^32: only the sum matters
+  return make_float2(__uint_as_float(__float_as_uint(q.x) + (__float_as_uint(t.x) << 23) - kMagicExp),
+                     __uint_as_float(__float_as_uint(q.y) + (__float_as_uint(t.y) << 23) - kMagicExp));
+}
+P2R_DEVICE float max3f(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
 P2R_DEVICE void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 P2R_DEVICE void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 // 2^x on the SFU (inputs here are <= 8, outputs feed a bf16 MMA operand)
@@ -96,9 +132,9 @@ __global__ void __launch_bounds__(384, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const FwdParams p) {
   using C = Cfg<HD>;
 #ifdef P2R_ATTN_TRACE
-  // diagnostic build only: clock64 timeline of CTA (0,0,0) dumped over the start of `o`
+  // diagnostic build only: clock64 timeline of CTA 0's first blocks dumped over the start of `lse`
   __shared__ long long s_tr[256];
-  const bool tr_cta = blockIdx.x == gridDim.x - 1 && blockIdx.y == 0 && blockIdx.z == 0;
+  const bool tr_cta = blockIdx.x == 0;
 #define TRF(slot) do { if (tr_cta) s_tr[(slot)] = clock64(); } while (0)
 #else
 #define TRF(slot) do {} while (0)
@@ -107,29 +143,44 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
-  uint64_t* q_full = bar + 0;
-  uint64_t* kv_full = bar + 1;   // [2]
-  uint64_t* kv_empty = bar + 3;  // [2]
-  uint64_t* s_full = bar + 5;    // [2]
-  uint64_t* p_full = bar + 7;    // [2]
-  uint64_t* o_done = bar + 9;    // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+  uint64_t* q_full = bar + 0;    // [NQ <= 2]
+  uint64_t* q_empty = bar + 2;   // [NQ]
+  uint64_t* kv_full = bar + 4;   // [NKV <= 4]
+  uint64_t* kv_empty = bar + 8;  // [NKV]
+  uint64_t* s_full = bar + 12;   // [2]
+  uint64_t* p_full = bar + 14;   // [2]
+  uint64_t* o_done = bar + 16;   // [2] one commit per PV
+  uint64_t* o_empty = bar + 18;  // [2] O buffer drained by the softmax warps
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 20);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  const int q0 = qb * BQ;
-  const int row0 = b * p.S;  // first row of this sequence in [T, 3d]
-  const int nkv = p.causal ? min(qb + 1, (p.S + BKV - 1) / BKV) : (p.S + BKV - 1) / BKV;
+  const int nqb = (p.S + BQ - 1) / BQ;
+  const int n_items = nqb * p.H * p.B;
+  // item w: heaviest (last) causal query tiles first
+  auto item = [&](int w, int& qb, int& h, int& b) {
+    const int hb = p.H * p.B;
+    qb = nqb - 1 - w / hb;
+    const int rem = w - (w / hb) * hb;
+    h = rem % p.H;
+    b = rem / p.H;
+  };
+  auto nkv_of = [&](int qb) { return p.causal ? min(qb + 1, nqb) : nqb; };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_qkv);
-    mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < C::NQ; ++i) {
+      mbar_init(q_full + i, 1);
+      mbar_init(q_empty + i, 1);
+    }
+    for (int i = 0; i < C::NKV; ++i) {
       mbar_init(kv_full + i, 1);
       mbar_init(kv_empty + i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(s_full + i, 1);
       mbar_init(p_full + i, 256);  // 8 softmax warps
       mbar_init(o_done + i, 1);
+      mbar_init(o_empty + i, 256);
     }
     fence_barrier_init();
   }
@@ -146,18 +197,27 @@ __global__ void __launch_bounds__(384, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer ----------------
-      mbar_arrive_expect_tx(q_full, C::TILE);
-      for (int a = 0; a < C::KATOMS; ++a)
-        tma_load_2d(smem + C::OFF_Q + a * BQ * 128, &tm_qkv, q_full, h * HD + 64 * a, row0 + q0);
-      for (int j = 0; j < nkv; ++j) {
-        const int st = j & 1;
-        mbar_wait(kv_empty + st, ((j >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(kv_full + st, 2 * C::TILE);
-        for (int a = 0; a < C::KATOMS; ++a) {
-          tma_load_2d(smem + C::OFF_K + st * C::TILE + a * BKV * 128, &tm_qkv, kv_full + st,
-                      p.d + h * HD + 64 * a, row0 + j * BKV);
-          tma_load_2d(smem + C::OFF_V + st * C::TILE + a * BKV * 128, &tm_qkv, kv_full + st,
-                      2 * p.d + h * HD + 64 * a, row0 + j * BKV);
+      int g = 0, it = 0;
+      for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
+        int qb, h, b;
+        item(w, qb, h, b);
+        const int row0 = b * p.S, nkv = nkv_of(qb);
+        const int qs = it % C::NQ;
+        mbar_wait(q_empty + qs, ((it / C::NQ) & 1) ^ 1);
+        mbar_arrive_expect_tx(q_full + qs, C::TILE);
+        for (int a = 0; a < C::KATOMS; ++a)
+          tma_load_2d(smem + C::OFF_Q + qs * C::TILE + a * BQ * 128, &tm_qkv, q_full + qs, h * HD + 64 * a,
+                      row0 + qb * BQ);
+        for (int j = 0; j < nkv; ++j, ++g) {
+          const int st = g % C::NKV;
+          mbar_wait(kv_empty + st, ((g / C::NKV) & 1) ^ 1);
+          mbar_arrive_expect_tx(kv_full + st, 2 * C::TILE);
+          for (int a = 0; a < C::KATOMS; ++a) {
+            tma_load_2d(smem + C::OFF_K + st * C::TILE + a * BKV * 128, &tm_qkv, kv_full + st,
+                        p.d + h * HD + 64 * a, row0 + j * BKV);
+            tma_load_2d(smem + C::OFF_V + st * C::TILE + a * BKV * 128, &tm_qkv, kv_full + st,
+                        2 * p.d + h * HD + 64 * a, row0 + j * BKV);
+          }
         }
       }
     }
@@ -165,44 +225,63 @@ __global__ void __launch_bounds__(384, 1)
     {  // ---------------- MMA issuer (whole warp, one elected lane issues) ----------------
       constexpr uint32_t idesc_s = make_idesc_bf16(BQ, BKV, false, false);
       constexpr uint32_t idesc_o = make_idesc_bf16(BQ, HD, false, true);
-      mbar_wait(q_full, 0);
-      tc_fence_after();
       // precomputed base descriptors, advanced by byte offsets (desc_add)
       const uint64_t dQ0 = make_sw128_desc(sbase + C::OFF_Q, 16, 1024);
       const uint64_t dK0 = make_sw128_desc(sbase + C::OFF_K, 16, 1024);
       const uint64_t dP0 = make_sw128_desc(sbase + C::OFF_P, 16, 1024);
       const uint64_t dV0 = make_sw128_desc(sbase + C::OFF_V, BKV * 128, 1024);
-      auto issue_pv = [&](int jj) {
-        mbar_wait(p_full + (jj & 1), (jj >> 1) & 1);
+      // PV of global block gg (block jj of item iit): O[iit & 1] (+)= P_gg . V_gg
+      auto issue_pv = [&](int gg, int jj, int iit) {
+        const int ob = iit & 1;
+        if (jj == 0) {  // first PV of an item: its O buffer must have been drained (item iit - 2)
+          mbar_wait(o_empty + ob, ((iit >> 1) & 1) ^ 1);
+          tc_fence_after();
+        }
+        mbar_wait(p_full + (gg & 1), (gg >> 1) & 1);
         tc_fence_after();
-        if (lane == 0) TRF(8 + 4 * jj + 2);
-        const uint32_t st = jj & 1;
-        const uint64_t ap = desc_add(dP0, (jj % C::NPB) * C::PTILE), bv = desc_add(dV0, st * C::TILE);
+        if (lane == 0 && gg < 22) TRF(8 + 4 * gg + 2);
+        const uint32_t st = gg % C::NKV;
+        const uint64_t ap = desc_add(dP0, (gg % C::NPB) * C::PTILE), bv = desc_add(dV0, st * C::TILE);
 #pragma unroll
         for (int k = 0; k < BKV / 16; ++k)
           // A = P (K-major, atom = 64 keys), B = V (MN-major: rows = keys, 64 hd per 128-B row)
-          umma_bf16_warp(tmem + C::TMEM_O, desc_add(ap, (k >> 2) * (BQ * 128) + (k & 3) * 32),
+          umma_bf16_warp(tmem + C::TMEM_O + ob * HD, desc_add(ap, (k >> 2) * (BQ * 128) + (k & 3) * 32),
                          desc_add(bv, k * 2048), idesc_o, (jj > 0 || k > 0) ? 1u : 0u);
         umma_commit_warp(kv_empty + st);
-        umma_commit_warp(o_done + (jj & 1));
-        if (lane == 0) TRF(8 + 4 * jj + 3);
+        umma_commit_warp(o_done + (gg & 1));
+        if (lane == 0 && gg < 22) TRF(8 + 4 * gg + 3);
       };
-      for (int j = 0; j < nkv; ++j) {
-        const uint32_t st = j & 1;
-        mbar_wait(kv_full + st, (j >> 1) & 1);
+      int g = 0, it = 0;
+      int pg = -1, pj = 0, pit = 0;  // the PV still to issue
+      for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
+        int qb, h, b;
+        item(w, qb, h, b);
+        const int nkv = nkv_of(qb);
+        const int qs = it % C::NQ;
+        mbar_wait(q_full + qs, (it / C::NQ) & 1);
         tc_fence_after();
-        if (lane == 0) TRF(8 + 4 * j);
-        const uint64_t bk = desc_add(dK0, st * C::TILE);
-        const uint32_t dS = tmem + ((j & 1) ? C::TMEM_S1 : C::TMEM_S0);
+        const uint64_t dQ = desc_add(dQ0, qs * C::TILE);
+        for (int j = 0; j < nkv; ++j, ++g) {
+          const uint32_t st = g % C::NKV;
+          mbar_wait(kv_full + st, (g / C::NKV) & 1);
+          tc_fence_after();
+          if (lane == 0 && g < 22) TRF(8 + 4 * g);
+          const uint64_t bk = desc_add(dK0, st * C::TILE);
+          const uint32_t dS = tmem + ((g & 1) ? C::TMEM_S1 : C::TMEM_S0);
 #pragma unroll
-        for (int k = 0; k < HD / 16; ++k)
-          umma_bf16_warp(dS, desc_add(dQ0, (k >> 2) * (BQ * 128) + (k & 3) * 32),
-                         desc_add(bk, (k >> 2) * (BKV * 128) + (k & 3) * 32), idesc_s, k > 0 ? 1u : 0u);
-        umma_commit_warp(s_full + (j & 1));
-        if (lane == 0) TRF(8 + 4 * j + 1);
-        if (j > 0) issue_pv(j - 1);
+          for (int k = 0; k < HD / 16; ++k)
+            umma_bf16_warp(dS, desc_add(dQ, (k >> 2) * (BQ * 128) + (k & 3) * 32),
+                           desc_add(bk, (k >> 2) * (BKV * 128) + (k & 3) * 32), idesc_s, k > 0 ? 1u : 0u);
+          umma_commit_warp(s_full + (g & 1));
+          if (j == nkv - 1) umma_commit_warp(q_empty + qs);  // this item's Q is no longer read
+          if (lane == 0 && g < 22) TRF(8 + 4 * g + 1);
+          if (pg >= 0) issue_pv(pg, pj, pit);
+          pg = g;
+          pj = j;
+          pit = it;
+        }
       }
-      issue_pv(nkv - 1);
+      if (pg >= 0) issue_pv(pg, pj, pit);
     }
   } else if (warp >= 4) {
     // ---------------- softmax / correction / epilogue ----------------
@@ -212,140 +291,167 @@ __global__ void __launch_bounds__(384, 1)
     // memory (double-buffered by block parity) behind a 64-thread named barrier.
     const int qd = warp & 3, hf = (warp - 4) >> 2;
     const int r = qd * 32 + lane;  // query row within the tile == TMEM lane
-    const int q = q0 + r;
     const uint32_t lane_addr = static_cast<uint32_t>(qd * 32) << 16;
     constexpr int KH = BKV / 2, OH = HD / 2;
     // [parity][half][row] partial maxima, then [half][row] partial sums (after the barriers area)
     const uint32_t xch = smem_u32(smem) + C::OFF_BAR + 256;
-    float m_used = -INFINITY, l = 0.0f;
     const bool trw = warp == 4 && lane == 0;
     (void)trw;
-    for (int j = 0; j < nkv; ++j) {
-      mbar_wait(s_full + (j & 1), (j >> 1) & 1);
+    // An item's epilogue (wait for its last PV, normalise O, store O / LSE) is
+    // deferred until the next item's first block is handed to the MMA: the
+    // softmax warps would otherwise idle on the last PV while S of the next
+    // item is already waiting. O is double-buffered, so the deferred O survives.
+    struct Pend {
+      bool valid;
+      float l, m;
+      int ob, g_last, b, h, q;
+    } pend{};
+    auto epilogue = [&](const Pend& e) {
+      mbar_wait(o_done + (e.g_last & 1), (e.g_last >> 1) & 1);
       tc_fence_after();
-      if (trw) TRF(100 + 4 * j);
-      const uint32_t tS = tmem + lane_addr + ((j & 1) ? C::TMEM_S1 : C::TMEM_S0) + hf * KH;
-      float x[KH];
-      {
-        uint32_t ra[32], rb[32];
-        tmem_ld_32x32b_x32(tS, ra);
-        tmem_ld_32x32b_x32(tS + 32, rb);
-        tmem_ld_wait();
+      const float inv = e.l > 0.0f ? 1.0f / e.l : 0.0f;
+      const bool row_ok = e.q < p.S;
+      const uint32_t tO = tmem + lane_addr + C::TMEM_O + e.ob * HD + hf * OH;
+      uint32_t rr[OH];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          x[i] = __uint_as_float(ra[i]);
-          x[32 + i] = __uint_as_float(rb[i]);
-        }
-      }
-      const int k0 = j * BKV + hf * KH;
-      const bool diag = p.causal && (j * BKV + BKV > q0);
-      const bool tail = j * BKV + BKV > p.S;
-      if (diag || tail) {  // warp-uniform: only the diagonal / ragged-tail blocks mask
-        const int lim = min(diag ? q + 1 : p.S, p.S) - k0;  // keys [0, lim) of this half are visible
-#pragma unroll
-        for (int i = 0; i < KH; ++i)
-          if (i >= lim) x[i] = -INFINITY;
-      }
-      // max on raw scores (scale > 0), combined with the other half of the row
-      float mr0 = x[0], mr1 = x[1];
-#pragma unroll
-      for (int i = 2; i < KH; i += 2) {
-        mr0 = fmaxf(mr0, x[i]);
-        mr1 = fmaxf(mr1, x[i + 1]);
-      }
-      const uint32_t slot = xch + 4 * (((j & 1) * 2) * 128 + r);
-      sts32f(slot + 4 * 128 * hf, fmaxf(mr0, mr1));
-      if (trw) TRF(100 + 4 * j + 1);
-      named_sync(1 + qd, 64);
-      float other;
-      asm volatile("ld.shared.f32 %0, [%1];" : "=f"(other) : "r"(slot + 4 * 128 * (hf ^ 1)) : "memory");
-      const float mx = fmaxf(fmaxf(mr0, mr1), other) * p.sl2;
-      if (mx > m_used + kRescaleThresh) {  // both halves take the same decision
-        if (j > 0) {
-          // O holds sum_{<j} 2^(x - m_used) V: rescale this half's O columns to the new max
-          mbar_wait(o_done + ((j - 1) & 1), ((j - 1) >> 1) & 1);
-          tc_fence_after();
-          const float f = exp2f(m_used - mx);
-#pragma unroll
-          for (int c = 0; c < OH / 32; ++c) {
-            uint32_t rr[32];
-            tmem_ld_32x32b_x32(tmem + lane_addr + C::TMEM_O + hf * OH + c * 32, rr);
-            tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) rr[i] = __float_as_uint(__uint_as_float(rr[i]) * f);
-            tmem_st_32x32b_x32(tmem + lane_addr + C::TMEM_O + hf * OH + c * 32, rr);
-          }
-          tmem_st_wait();
-          l *= f;
-        }
-        m_used = mx;
-      }
-      // P buffer reuse: the PV that last read this buffer must be done
-      if (j >= C::NPB) {
-        const int jp = j - C::NPB;
-        mbar_wait(o_done + (jp & 1), (jp >> 1) & 1);
-      }
-      const uint32_t sp = smem_u32(smem) + C::OFF_P + (j % C::NPB) * C::PTILE + hf * (BQ * 128);
-      float ls = 0.0f, ls2 = 0.0f;
-      const float nm = -m_used;
-#pragma unroll
-      for (int c16 = 0; c16 < KH / 8; ++c16) {
-        uint32_t w[4];
-        // the softmax is MUFU-bound (16 ex2/clk/SM): a quarter of the exponentials go to the FMA pipe
-        const bool fma_pipe = (c16 & 3) == 3;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float za = fmaf(x[c16 * 8 + 2 * i], p.sl2, nm), zb = fmaf(x[c16 * 8 + 2 * i + 1], p.sl2, nm);
-          const float a = fma_pipe ? exp2_fma(za) : ex2_approx(za);
-          const float bb = fma_pipe ? exp2_fma(zb) : ex2_approx(zb);
-          ls += a;
-          ls2 += bb;
-          __nv_bfloat162 hh = __floats2bfloat162_rn(a, bb);
-          w[i] = *reinterpret_cast<uint32_t*>(&hh);
-        }
-        sts128(sp + sw128_off(r, c16), make_uint4(w[0], w[1], w[2], w[3]));  // this half = one 64-key atom
-      }
-      l += ls + ls2;
-      if (trw) TRF(100 + 4 * j + 2);
-      fence_async_smem();
-      tc_fence_before();
-      mbar_arrive(p_full + (j & 1));
-      if (trw) TRF(100 + 4 * j + 3);
-    }
-    // row sum = both halves' partial sums
-    const uint32_t lslot = xch + 4 * (4 * 128 + r);
-    sts32f(lslot + 4 * 128 * hf, l);
-    named_sync(1 + qd, 64);
-    float lo;
-    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(lo) : "r"(lslot + 4 * 128 * (hf ^ 1)) : "memory");
-    l += lo;
-    // epilogue: wait for the last PV, normalise, store this half's O columns (bf16) and LSE
-    mbar_wait(o_done + ((nkv - 1) & 1), ((nkv - 1) >> 1) & 1);
-    tc_fence_after();
-    const float inv = l > 0.0f ? 1.0f / l : 0.0f;
-    const bool row_ok = q < p.S;
-    __nv_bfloat16* orow = p.o + static_cast<long long>(row0 + q) * p.d + h * HD + hf * OH;
-#pragma unroll
-    for (int c = 0; c < OH / 32; ++c) {
-      uint32_t rr[32];
-      tmem_ld_32x32b_x32(tmem + lane_addr + C::TMEM_O + hf * OH + c * 32, rr);
+      for (int c = 0; c < OH / 32; ++c) tmem_ld_32x32b_x32(tO + c * 32, rr + 32 * c);
       tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(o_empty + e.ob);  // O buffer ob is free for item it + 2
       if (row_ok) {
-        uint32_t w[16];
+        __nv_bfloat16* orow = p.o + static_cast<long long>(e.b * p.S + e.q) * p.d + e.h * HD + hf * OH;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          __nv_bfloat162 hh = __floats2bfloat162_rn(__uint_as_float(rr[2 * i]) * inv, __uint_as_float(rr[2 * i + 1]) * inv);
-          w[i] = *reinterpret_cast<uint32_t*>(&hh);
+        for (int c = 0; c < OH / 32; ++c) {
+          uint32_t wv[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            __nv_bfloat162 hh = __floats2bfloat162_rn(__uint_as_float(rr[32 * c + 2 * i]) * inv,
+                                                      __uint_as_float(rr[32 * c + 2 * i + 1]) * inv);
+            wv[i] = *reinterpret_cast<uint32_t*>(&hh);
+          }
+          uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) dst[i] = make_uint4(wv[4 * i], wv[4 * i + 1], wv[4 * i + 2], wv[4 * i + 3]);
         }
-        uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) dst[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
-      }
-    }
 #ifndef P2R_ATTN_TRACE  // trace builds dump the timeline over lse instead
-    if (row_ok && hf == 0)
-      p.lse[(static_cast<long long>(b) * p.H + h) * p.S + q] = (m_used + log2f(l)) * 0.6931471805599453f;
+        if (hf == 0) p.lse[(static_cast<long long>(e.b) * p.H + e.h) * p.S + e.q] = (e.m + log2f(e.l)) * 0.6931471805599453f;
 #endif
+      }
+    };
+    int g = 0, it = 0;
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
+      int qb, h, b;
+      item(w, qb, h, b);
+      const int nkv = nkv_of(qb), q0 = qb * BQ;
+      const int q = q0 + r;
+      const int ob = it & 1;
+      const uint32_t tO = tmem + lane_addr + C::TMEM_O + ob * HD + hf * OH;
+      float m_used = -INFINITY, l = 0.0f;
+      for (int j = 0; j < nkv; ++j, ++g) {
+        mbar_wait(s_full + (g & 1), (g >> 1) & 1);
+        tc_fence_after();
+        if (trw && g < 22) TRF(100 + 4 * g);
+        const uint32_t tS = tmem + lane_addr + ((g & 1) ? C::TMEM_S1 : C::TMEM_S0) + hf * KH;
+        float x[KH];
+        {
+          uint32_t ra[32], rb[32];
+          tmem_ld_32x32b_x32(tS, ra);
+          tmem_ld_32x32b_x32(tS + 32, rb);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            x[i] = __uint_as_float(ra[i]);
+            x[32 + i] = __uint_as_float(rb[i]);
+          }
+        }
+        const int k0 = j * BKV + hf * KH;
+        const bool diag = p.causal && (j * BKV + BKV > q0);
+        const bool tail = j * BKV + BKV > p.S;
+        if (diag || tail) {  // warp-uniform: only the diagonal / ragged-tail blocks mask
+          const int lim = min(diag ? q + 1 : p.S, p.S) - k0;  // keys [0, lim) of this half are visible
+#pragma unroll
+          for (int i = 0; i < KH; ++i)
+            if (i >= lim) x[i] = -INFINITY;
+        }
+        // max on raw scores (scale > 0), combined with the other half of the row
+        float mr0 = max3f(x[0], x[1], x[2]), mr1 = max3f(x[3], x[4], x[5]);
+#pragma unroll
+        for (int i = 6; i + 3 < KH; i += 4) {
+          mr0 = max3f(mr0, x[i], x[i + 1]);
+          mr1 = max3f(mr1, x[i + 2], x[i + 3]);
+        }
+        mr0 = max3f(mr0, x[KH - 2], x[KH - 1]);
+        const uint32_t slot = xch + 4 * (((g & 1) * 2) * 128 + r);
+        sts32f(slot + 4 * 128 * hf, fmaxf(mr0, mr1));
+        if (trw && g < 22) TRF(100 + 4 * g + 1);
+        named_sync(1 + qd, 64);
+        float other;
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(other) : "r"(slot + 4 * 128 * (hf ^ 1)) : "memory");
+        const float mx = fmaxf(fmaxf(mr0, mr1), other) * p.sl2;
+        if (mx > m_used + kRescaleThresh) {  // both halves take the same decision
+          if (j > 0) {
+            // O holds sum_{<j} 2^(x - m_used) V: rescale this half's O columns to the new max
+            mbar_wait(o_done + ((g - 1) & 1), ((g - 1) >> 1) & 1);
+            tc_fence_after();
+            const float f = exp2f(m_used - mx);
+#pragma unroll
+            for (int c = 0; c < OH / 32; ++c) {
+              uint32_t rr[32];
+              tmem_ld_32x32b_x32(tO + c * 32, rr);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) rr[i] = __float_as_uint(__uint_as_float(rr[i]) * f);
+              tmem_st_32x32b_x32(tO + c * 32, rr);
+            }
+            tmem_st_wait();
+            l *= f;
+          }
+          m_used = mx;
+        }
+        // P buffer reuse: the PV that last read this buffer must be done
+        if (g >= C::NPB) {
+          const int gp = g - C::NPB;
+          mbar_wait(o_done + (gp & 1), (gp >> 1) & 1);
+        }
+        const uint32_t sp = smem_u32(smem) + C::OFF_P + (g % C::NPB) * C::PTILE + hf * (BQ * 128);
+        float2 ls = make_float2(0.0f, 0.0f);
+        const float2 sl2 = make_float2(p.sl2, p.sl2), nm = make_float2(-m_used, -m_used);
+#pragma unroll
+        for (int c16 = 0; c16 < KH / 8; ++c16) {
+          uint32_t wv[4];
+          // the softmax is MUFU-bound (16 ex2/clk/SM): a quarter of the exponentials go to the FMA pipe
+          const bool fma_pipe = c16 >= KH / 8 - kFmaChunks;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float2 z = __ffma2_rn(make_float2(x[c16 * 8 + 2 * i], x[c16 * 8 + 2 * i + 1]), sl2, nm);
+            const float2 e = fma_pipe ? exp2_fma2(z) : make_float2(ex2_approx(z.x), ex2_approx(z.y));
+            ls = __fadd2_rn(ls, e);
+            __nv_bfloat162 hh = __floats2bfloat162_rn(e.x, e.y);
+            wv[i] = *reinterpret_cast<uint32_t*>(&hh);
+          }
+          sts128(sp + sw128_off(r, c16), make_uint4(wv[0], wv[1], wv[2], wv[3]));  // this half = one 64-key atom
+        }
+        l += ls.x + ls.y;
+        if (trw && g < 22) TRF(100 + 4 * g + 2);
+        fence_async_smem();
+        tc_fence_before();
+        mbar_arrive(p_full + (g & 1));
+        if (trw && g < 22) TRF(100 + 4 * g + 3);
+        if (j == 0 && pend.valid) {  // the previous item's epilogue, off the critical path
+          epilogue(pend);
+          pend.valid = false;
+        }
+      }
+      // row sum = both halves' partial sums
+      const uint32_t lslot = xch + 4 * (4 * 128 + r);
+      sts32f(lslot + 4 * 128 * hf, l);
+      named_sync(1 + qd, 64);
+      float lo;
+      asm volatile("ld.shared.f32 %0, [%1];" : "=f"(lo) : "r"(lslot + 4 * 128 * (hf ^ 1)) : "memory");
+      l += lo;
+      pend = Pend{true, l, m_used, ob, g - 1, b, h, q};
+    }
+    if (pend.valid) epilogue(pend);
   }
   tc_fence_before();
   __syncthreads();
@@ -390,7 +496,8 @@ p2r_status run(const void* qkv, const FwdParams& p, cudaStream_t s) {
     return set_error(P2R_ECUDA, "attention: tensor map encode failed");
   static cudaError_t attr = cudaFuncSetAttribute(attn_fwd_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   if (attr != cudaSuccess) return set_cuda_error(attr, "attention tc attr");
-  dim3 grid((p.S + BQ - 1) / BQ, p.H, p.B);
+  const int n_items = (p.S + BQ - 1) / BQ * p.H * p.B;
+  const dim3 grid(n_items < kNumSMs ? n_items : kNumSMs);  // persistent: one CTA per SM
   P2R_LAUNCH_K("attention fwd (tcgen05)", attn_fwd_tc_kernel<HD>, grid, dim3(384), C::SMEM, s, 1, tm, p);
   return P2R_OK;
 }

@@ -105,6 +105,59 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const float* __restrict__ x
   }
 }
 
+// Register variant: one warp per row, the row held in registers (NV float4 per
+// lane, 16-byte loads), no shared memory. A small register footprint gives 40+
+// resident warps per SM whose loads are all in flight at once -- the memory
+// system, not a per-warp pipeline, hides the latency (the bulk-ring kernel
+// above keeps 16 warps per SM and spends its time in per-row latency).
+template <int NV>
+__global__ void __launch_bounds__(256) ln_fwd_reg_kernel(const float* __restrict__ x, const float* __restrict__ gain,
+                                                        const float* __restrict__ bias, int rows, float eps,
+                                                        __nv_bfloat16* __restrict__ y16, float* __restrict__ y32,
+                                                        float* __restrict__ mean_out, float* __restrict__ rstd_out) {
+  pdl_trigger();
+  pdl_wait();
+  constexpr int D = 128 * NV;
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const float* xr = x + static_cast<long long>(r) * D;
+  float4 v[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) v[i] = ld4(xr + 4 * (lane + 32 * i));
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+  s = warp_sum(s);
+  const float inv_d = 1.0f / static_cast<float>(D);
+  const float mu = s * inv_d;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const float a = v[i].x - mu, b = v[i].y - mu, c = v[i].z - mu, d = v[i].w - mu;
+    q += (a * a + b * b) + (c * c + d * d);
+  }
+  q = warp_sum(q);  // two-pass (biased) variance, tensor.cpp:265-336
+  const float inv = 1.0f / sqrtf(q * inv_d + eps);
+  if (lane == 0) {
+    mean_out[r] = mu;
+    rstd_out[r] = inv;
+  }
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c4 = lane + 32 * i;
+    const float4 g = __ldg(reinterpret_cast<const float4*>(gain) + c4), bb = __ldg(reinterpret_cast<const float4*>(bias) + c4);
+    float4 o;
+    o.x = (v[i].x - mu) * inv * g.x + bb.x;
+    o.y = (v[i].y - mu) * inv * g.y + bb.y;
+    o.z = (v[i].z - mu) * inv * g.z + bb.z;
+    o.w = (v[i].w - mu) * inv * g.w + bb.w;
+    const long long off = static_cast<long long>(r) * D + 4LL * c4;
+    if (y16) st_bf16x4(y16 + off, o);
+    if (y32) *reinterpret_cast<float4*>(y32 + off) = o;
+  }
+}
+
 // dx = resid + inv * (gy - mean(gy) - xhat * mean(gy * xhat)), gy = dy * gain.
 // dgain/dbias: per-lane column accumulators over the warp's rows, combined per
 // block (warp order) into partial[blockIdx.x][2][D]; ln_param_grad_reduce adds
@@ -419,6 +472,26 @@ extern "C" p2r_status p2r_layernorm_fwd(const float* x, const float* gain, const
   const LnLaunch l = ln_fwd_launch(rows, d);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   auto* y16 = static_cast<__nv_bfloat16*>(y_bf16);
+  static const bool ring = [] {
+    const char* e = std::getenv("P2R_LN_FWD_RING");
+    return e != nullptr && e[0] == '1';
+  }();
+  if (!ring) {
+    switch (d / 128) {
+#define P2R_LN_FWD_REG(NV)                                                                                  \
+  case NV: {                                                                                               \
+    const cudaError_t le = launch_k(ln_fwd_reg_kernel<NV>, dim3((rows + 7) / 8), dim3(256), 0, s, 1, x, gain, bias, \
+                                    rows, eps, y16, y_f32, mean, rstd);                                   \
+    if (le != cudaSuccess) return set_cuda_error(le, "layernorm fwd");                                     \
+    break;                                                                                                 \
+  }
+      P2R_LN_NV_CASES(P2R_LN_FWD_REG)
+#undef P2R_LN_FWD_REG
+      default: break;
+    }
+    P2R_CHECK_LAUNCH("layernorm fwd");
+    return P2R_OK;
+  }
   switch (d / 128) {
 #define P2R_LN_FWD(NV)                                                                                     \
   case NV: {                                                                                               \

@@ -29,6 +29,8 @@ def variant(name, text):
     elif name == "nosm":
         text = re.sub(r"ld32x2\((tmem|tS)[^;]*\);", r"{ for (int z_ = 0; z_ < 32; ++z_) { s[z_] = 0.f; dp[z_] = 0.f; } }", text)
         text = re.sub(r"\? ex2_approx\(", "? (", text)
+    elif name.startswith("fma"):  # fwd: fmaN = N of 8 chunks' exponentials on the FMA pipe
+        text = "#define P2R_ATTN_FMA_CHUNKS " + name[3:] + "\n" + text
     elif name == "trace":
         text = "#define P2R_ATTN_TRACE 1\n" + text
     return text

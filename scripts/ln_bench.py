@@ -25,13 +25,14 @@ ws = torch.empty(L.p2r_layernorm_bwd_workspace(T, d) // 4 + 1, device="cuda")
 flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
 
 
-def t(fn, it=20):
+def t(fn, it=20, cold=True):
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
     tot = 0.0
     for _ in range(it):
-        flush.zero_()
+        if cold:
+            flush.zero_()
         a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         fn()
@@ -43,5 +44,23 @@ def t(fn, it=20):
 
 fwd = lambda: _lib.check(L.p2r_layernorm_fwd(P(x), P(g), P(b), T, d, ctypes.c_float(1e-5), P(y16), None, P(mean), P(rstd), st))
 bwd = lambda: _lib.check(L.p2r_layernorm_bwd(P(dy), P(x), P(mean), P(rstd), P(g), P(res), T, d, P(dx), P(dx16), P(gg), P(gb), P(ws), st))
-f, bw = t(fwd), t(bwd)
-print(f"T={T} d={d}: ln fwd {f:6.1f} us ({(T*d*6)/f/1e3:6.0f} GB/s)  ln bwd {bw:6.1f} us ({(T*d*18)/bw/1e3:6.0f} GB/s)")
+def b2b(fn, it=20):
+    """back-to-back launches (PDL overlaps launch latency, as inside the step)"""
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(it):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(e) / it * 1e3
+
+
+f, bw = b2b(fwd), b2b(bwd)
+print(f"T={T} d={d} back-to-back: ln fwd {f:6.1f} us ({(T*d*6)/f/1e3:6.0f} GB/s)  ln bwd {bw:6.1f} us ({(T*d*18)/bw/1e3:6.0f} GB/s)")
+for cold in (True, False):
+    f, bw = t(fwd, cold=cold), t(bwd, cold=cold)
+    print(f"T={T} d={d} {'cold' if cold else 'warm'}: ln fwd {f:6.1f} us ({(T*d*6)/f/1e3:6.0f} GB/s)  "
+          f"ln bwd {bw:6.1f} us ({(T*d*18)/bw/1e3:6.0f} GB/s)")

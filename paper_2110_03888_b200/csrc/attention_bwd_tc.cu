@@ -557,17 +557,23 @@ struct DqPP {
   static constexpr int OFF_DS = OFF_V + NS * KT;   // [tile][buf]
   static constexpr int OFF_BAR = OFF_DS + 4 * DST;
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
-  static constexpr int T_TILE = 192;  // TMEM per tile: S +0, dP +64, dQ +128
+  static constexpr int T_TILE = 192;  // TMEM per tile: S +0, dP +64, dQ(item parity 0) +128
+  static constexpr int T_DQ1 = 384;   // dQ(item parity 1) of tile X at T_DQ1 + 64 X
 };
 
+// Persistent over (query-tile pair, head, batch) work items, heaviest causal
+// pairs first: every pipeline counter runs across items, the dQ accumulator is
+// double-buffered by item parity, an item's dQ epilogue is deferred until the
+// next item's first block is handed to the MMA, and the next item's D / LSE
+// rows are fetched while the tensor core starts on it.
 __global__ void __launch_bounds__(384, 1)
     attn_bwd_dq_pp(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kv,
                    const __grid_constant__ CUtensorMap tm_do, const BwdParams p) {
   using C = DqPP;
 #ifdef P2R_ATTN_TRACE
   __shared__ long long s_tr[512];
-  const bool tr_cta = blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
-#define TRP(slot) do { if (tr_cta) s_tr[(slot)] = clock64(); } while (0)
+  const bool tr_cta = blockIdx.x == 0;
+#define TRP(slot) do { if (tr_cta && (slot) < 512) s_tr[(slot)] = clock64(); } while (0)
 #else
 #define TRP(slot) do {} while (0)
 #endif
@@ -575,30 +581,43 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* q_full = bar;
-  uint64_t* kv_full = bar + 1;            // [NS]
+  uint64_t* q_empty = bar + 1;
+  uint64_t* kv_full = bar + 2;            // [NS]
   uint64_t* kv_empty = kv_full + C::NS;   // [NS]
   uint64_t* s_full = kv_empty + C::NS;    // [tile]
   uint64_t* s_free = s_full + 2;          // [tile]
   uint64_t* ds_full = s_free + 2;         // [tile][buf]
   uint64_t* dq_done = ds_full + 4;        // [tile][buf]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 4);
+  uint64_t* dq_empty = dq_done + 4;       // [tile][item parity]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_empty + 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // causal: the last query pairs see the most keys -> launch them first
-  const int pq = p.causal ? gridDim.x - 1 - blockIdx.x : blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  const int q0 = pq * 2 * C::BQ, row0 = b * p.S;
-  int nkvt[2];
+  const int npq = (p.S + 2 * C::BQ - 1) / (2 * C::BQ);
+  const int n_items = npq * p.H * p.B;
+  struct Item {
+    int h, b, q0, nkvt[2], nkv;
+  };
+  auto item = [&](int w) {
+    Item I;
+    const int hb = p.H * p.B, g = w / hb, rem = w - g * hb;
+    const int pq = p.causal ? npq - 1 - g : g;  // causal: the last query pairs see the most keys
+    I.h = rem % p.H;
+    I.b = rem / p.H;
+    I.q0 = pq * 2 * C::BQ;
 #pragma unroll
-  for (int X = 0; X < 2; ++X) {
-    const int qs = q0 + X * C::BQ;
-    const int kend = p.causal ? min(p.S, qs + C::BQ) : p.S;
-    nkvt[X] = qs < p.S ? (kend + C::BKV - 1) / C::BKV : 0;
-  }
-  const int nkv = max(nkvt[0], nkvt[1]);
+    for (int X = 0; X < 2; ++X) {
+      const int qs = I.q0 + X * C::BQ;
+      const int kend = p.causal ? min(p.S, qs + C::BQ) : p.S;
+      I.nkvt[X] = qs < p.S ? (kend + C::BKV - 1) / C::BKV : 0;
+    }
+    I.nkv = max(I.nkvt[0], I.nkvt[1]);
+    return I;
+  };
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_q);
     tma_prefetch_desc(&tm_kv);
     tma_prefetch_desc(&tm_do);
     mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
     for (int i = 0; i < C::NS; ++i) {
       mbar_init(kv_full + i, 1);
       mbar_init(kv_empty + i, 2);  // S/dP issuer (warp 1) + dQ issuer (warp 3)
@@ -609,6 +628,7 @@ __global__ void __launch_bounds__(384, 1)
       for (int u = 0; u < 2; ++u) {
         mbar_init(ds_full + 2 * X + u, 128);
         mbar_init(dq_done + 2 * X + u, 1);
+        mbar_init(dq_empty + 2 * X + u, 128);
       }
     }
     fence_barrier_init();
@@ -624,54 +644,64 @@ __global__ void __launch_bounds__(384, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(q_full, 4 * C::QT);
-      for (int X = 0; X < 2; ++X) {
-        tma_load_2d(smem + C::OFF_Q + X * C::QT, &tm_q, q_full, h * C::HD, row0 + q0 + X * C::BQ);
-        tma_load_2d(smem + C::OFF_DO + X * C::QT, &tm_do, q_full, h * C::HD, row0 + q0 + X * C::BQ);
-      }
-      for (int j = 0; j < nkv; ++j) {
-        const int st = j % C::NS;
-        mbar_wait(kv_empty + st, ((j / C::NS) & 1) ^ 1);
-        mbar_arrive_expect_tx(kv_full + st, 2 * C::KT);
-        tma_load_2d(smem + C::OFF_K + st * C::KT, &tm_kv, kv_full + st, p.d + h * C::HD, row0 + j * C::BKV);
-        tma_load_2d(smem + C::OFF_V + st * C::KT, &tm_kv, kv_full + st, 2 * p.d + h * C::HD, row0 + j * C::BKV);
+      int G = 0, it = 0;
+      for (int k = 0, w = blockIdx.x; w < n_items; w = snake_item(++k, blockIdx.x, gridDim.x), ++it) {
+        const Item I = item(w);
+        const int row0 = I.b * p.S;
+        mbar_wait(q_empty, (it & 1) ^ 1);  // the previous item's S/dP MMAs are done with Q / dO
+        mbar_arrive_expect_tx(q_full, 4 * C::QT);
+        for (int X = 0; X < 2; ++X) {
+          tma_load_2d(smem + C::OFF_Q + X * C::QT, &tm_q, q_full, I.h * C::HD, row0 + I.q0 + X * C::BQ);
+          tma_load_2d(smem + C::OFF_DO + X * C::QT, &tm_do, q_full, I.h * C::HD, row0 + I.q0 + X * C::BQ);
+        }
+        for (int j = 0; j < I.nkv; ++j, ++G) {
+          const int st = G % C::NS;
+          mbar_wait(kv_empty + st, ((G / C::NS) & 1) ^ 1);
+          mbar_arrive_expect_tx(kv_full + st, 2 * C::KT);
+          tma_load_2d(smem + C::OFF_K + st * C::KT, &tm_kv, kv_full + st, p.d + I.h * C::HD, row0 + j * C::BKV);
+          tma_load_2d(smem + C::OFF_V + st * C::KT, &tm_kv, kv_full + st, 2 * p.d + I.h * C::HD, row0 + j * C::BKV);
+        }
       }
     }
   } else if (warp == 1) {
     {  // whole warp: uniform control flow, one elected lane issues each MMA
       constexpr uint32_t id_s = make_idesc_bf16(C::BQ, C::BKV, false, false);
-      mbar_wait(q_full, 0);
-      tc_fence_after();
       // base descriptors (K-major: +32 B per 16-wide k step; MN-major K: +2048 B)
       const uint64_t dQ0 = make_sw128_desc(sb + C::OFF_Q, 16, 1024), dO0 = make_sw128_desc(sb + C::OFF_DO, 16, 1024);
       const uint64_t dK0 = make_sw128_desc(sb + C::OFF_K, 16, 1024), dV0 = make_sw128_desc(sb + C::OFF_V, 16, 1024);
-      auto issue_s = [&](int X, int j) {
-        if (j >= 1) {
-          mbar_wait(s_free + X, (j - 1) & 1);  // the group holds S/dP(j-1) in registers
-          tc_fence_after();
-        }
-        const uint32_t st = j % C::NS;
-        const uint64_t a = dadd(dQ0, X * C::QT), ao = dadd(dO0, X * C::QT);
-        const uint64_t bk = dadd(dK0, st * C::KT), bv = dadd(dV0, st * C::KT);
-        const uint32_t tS = tmem + X * C::T_TILE;
-#pragma unroll
-        for (int k = 0; k < C::HD / 16; ++k) {
-          umma_bf16_warp(tS, dadd(a, k * 32), dadd(bk, k * 32), id_s, k > 0 ? 1u : 0u);
-          umma_bf16_warp(tS + 64, dadd(ao, k * 32), dadd(bv, k * 32), id_s, k > 0 ? 1u : 0u);
-        }
-        umma_commit_warp(s_full + X);
-      };
-
-      // S/dP issuer: one K/V block after another, each as soon as the group
-      // released the previous S/dP (dQ MMAs are issued by warp 3)
-      for (int j = 0; j < nkv; ++j) {
-        mbar_wait(kv_full + j % C::NS, (j / C::NS) & 1);
+      int G = 0, it = 0, cX[2] = {0, 0};
+      for (int k = 0, w = blockIdx.x; w < n_items; w = snake_item(++k, blockIdx.x, gridDim.x), ++it) {
+        const Item I = item(w);
+        mbar_wait(q_full, it & 1);
         tc_fence_after();
-        TRP(16 + 4 * j);
-        for (int X = 0; X < 2; ++X)
-          if (j < nkvt[X]) issue_s(X, j);
-        TRP(16 + 4 * j + 1);
-        umma_commit_warp(kv_empty + j % C::NS);
+        // S/dP issuer: one K/V block after another, each as soon as the group
+        // released the previous S/dP (dQ MMAs are issued by warp 3)
+        for (int j = 0; j < I.nkv; ++j, ++G) {
+          const uint32_t st = G % C::NS;
+          mbar_wait(kv_full + st, (G / C::NS) & 1);
+          tc_fence_after();
+          TRP(16 + 4 * G);
+          for (int X = 0; X < 2; ++X) {
+            if (j >= I.nkvt[X]) continue;
+            if (cX[X] >= 1) {
+              mbar_wait(s_free + X, (cX[X] - 1) & 1);  // the group holds S/dP of its previous block in registers
+              tc_fence_after();
+            }
+            const uint64_t a = dadd(dQ0, X * C::QT), ao = dadd(dO0, X * C::QT);
+            const uint64_t bk = dadd(dK0, st * C::KT), bv = dadd(dV0, st * C::KT);
+            const uint32_t tS = tmem + X * C::T_TILE;
+#pragma unroll
+            for (int k = 0; k < C::HD / 16; ++k) {
+              umma_bf16_warp(tS, dadd(a, k * 32), dadd(bk, k * 32), id_s, k > 0 ? 1u : 0u);
+              umma_bf16_warp(tS + 64, dadd(ao, k * 32), dadd(bv, k * 32), id_s, k > 0 ? 1u : 0u);
+            }
+            umma_commit_warp(s_full + X);
+            ++cX[X];
+          }
+          TRP(16 + 4 * G + 1);
+          if (j == I.nkv - 1) umma_commit_warp(q_empty);  // this item's Q / dO are no longer read
+          umma_commit_warp(kv_empty + st);
+        }
       }
     }
   } else if (warp == 3) {
@@ -679,116 +709,152 @@ __global__ void __launch_bounds__(384, 1)
       constexpr uint32_t id_q = make_idesc_bf16(C::BQ, C::HD, false, true);
       const uint64_t dS0 = make_sw128_desc(sb + C::OFF_DS, 16, 1024);
       const uint64_t dKm0 = make_sw128_desc(sb + C::OFF_K, C::BKV * 128, 1024);
-      for (int j = 0; j < nkv; ++j) {
-        for (int X = 0; X < 2; ++X) {
-          if (j < nkvt[X]) {
-            const int u = j & 1;
-            mbar_wait(ds_full + 2 * X + u, (j >> 1) & 1);  // implies S(j) done, so K_j is in smem
-            tc_fence_after();
-            const uint64_t a = dadd(dS0, (2 * X + u) * C::DST), bk = dadd(dKm0, (j % C::NS) * C::KT);
-            const uint32_t tQ = tmem + X * C::T_TILE + 128;
+      int G = 0, it = 0, cX[2] = {0, 0};
+      for (int k = 0, w = blockIdx.x; w < n_items; w = snake_item(++k, blockIdx.x, gridDim.x), ++it) {
+        const Item I = item(w);
+        const int par = it & 1;
+        for (int j = 0; j < I.nkv; ++j, ++G) {
+          for (int X = 0; X < 2; ++X) {
+            if (j < I.nkvt[X]) {
+              const int u = cX[X] & 1;
+              mbar_wait(ds_full + 2 * X + u, (cX[X] >> 1) & 1);  // implies S(j) done, so K_j is in smem
+              tc_fence_after();
+              if (j == 0) {  // this dQ buffer was last drained by the group for item it - 2
+                mbar_wait(dq_empty + 2 * X + par, ((it >> 1) & 1) ^ 1);
+                tc_fence_after();
+              }
+              const uint64_t a = dadd(dS0, (2 * X + u) * C::DST), bk = dadd(dKm0, (G % C::NS) * C::KT);
+              const uint32_t tQ = tmem + (par ? C::T_DQ1 + 64 * X : X * C::T_TILE + 128);
 #pragma unroll
-            for (int k = 0; k < C::BKV / 16; ++k)
-              umma_bf16_warp(tQ, dadd(a, k * 32), dadd(bk, k * 2048), id_q, (j > 0 || k > 0) ? 1u : 0u);
-            umma_commit_warp(dq_done + 2 * X + u);
+              for (int k = 0; k < C::BKV / 16; ++k)
+                umma_bf16_warp(tQ, dadd(a, k * 32), dadd(bk, k * 2048), id_q, (j > 0 || k > 0) ? 1u : 0u);
+              umma_commit_warp(dq_done + 2 * X + u);
+              ++cX[X];
+            }
+            TRP(16 + 4 * G + 2 + X);
           }
-          TRP(16 + 4 * j + 2 + X);
+          umma_commit_warp(kv_empty + G % C::NS);
         }
-        umma_commit_warp(kv_empty + j % C::NS);
       }
     }
   } else if (warp >= 4) {
     const int X = (warp - 4) >> 2;           // tile owned by this softmax group
     const int r = (warp & 3) * 32 + lane;    // query row in the tile == TMEM lane
-    const int q = q0 + X * C::BQ + r;
     const uint32_t la = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    const uint32_t tS = tmem + la + X * C::T_TILE, tP = tS + 64, tQ = tS + 128;
-    const long long bh = static_cast<long long>(b) * p.H + h;
-    const int nkvX = nkvt[X];
-    // D = rowsum(dO o O) for this row (fp32 accumulate), published for the dK/dV kernel
-    float D = 0.0f;
-    if (q < p.S) {
-      const uint4* a4 = reinterpret_cast<const uint4*>(p.dout + static_cast<long long>(row0 + q) * p.d + h * C::HD);
-      const uint4* o4 = reinterpret_cast<const uint4*>(p.o + static_cast<long long>(row0 + q) * p.d + h * C::HD);
+    const uint32_t tS = tmem + la + X * C::T_TILE, tP = tS + 64;
+    const float sl2 = p.sl2;
+    const bool trw = (warp == 4 || warp == 8) && lane == 0;  // trace writers (P2R_ATTN_TRACE builds)
+    const int trb = 100 + X * 200;
+    (void)trw;
+    (void)trb;
+    // D = rowsum(dO o O) of this row (fp32 accumulate), published for the dK/dV kernel, + its LSE
+    auto row_stats = [&](const Item& I, float& D, float& lse2) {
+      const int q = I.q0 + X * C::BQ + r;
+      D = 0.0f;
+      lse2 = 0.0f;
+      if (q >= p.S) return;
+      const long long bh = static_cast<long long>(I.b) * p.H + I.h;
+      const long long off = static_cast<long long>(I.b * p.S + q) * p.d + I.h * C::HD;
+      const uint4* a4 = reinterpret_cast<const uint4*>(p.dout + off);
+      const uint4* o4 = reinterpret_cast<const uint4*>(p.o + off);
+      lse2 = p.lse[bh * p.S + q] * kLog2e;
 #pragma unroll
       for (int c = 0; c < C::HD / 8; ++c) {
         const uint4 x = a4[c], y = o4[c];
         const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const float2 u = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xs[i]));
-          const float2 v = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ys[i]));
-          D += u.x * v.x + u.y * v.y;
+          const float2 u2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xs[i]));
+          const float2 v2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ys[i]));
+          D += u2.x * v2.x + u2.y * v2.y;
         }
       }
       p.dsum[bh * p.S + q] = D;
-    }
-    const float lse2 = q < p.S ? p.lse[bh * p.S + q] * kLog2e : 0.0f;
-    const float sl2 = p.sl2;
-    const bool trw = (warp == 4 || warp == 8) && lane == 0;  // trace writers (P2R_ATTN_TRACE builds)
-    const int trb = 100 + X * 100;
-    (void)trw;
-    (void)trb;
-    for (int j = 0; j < nkvX; ++j) {
-      const int u = j & 1;
-      const uint32_t dsb = sb + C::OFF_DS + (2 * X + u) * C::DST;
-      mbar_wait(s_full + X, j & 1);
+    };
+    struct Pend {
+      bool valid;
+      int par, c_last, q, h, b;
+    } pend{};
+    auto epilogue = [&](const Pend& e) {
+      mbar_wait(dq_done + 2 * X + (e.c_last & 1), (e.c_last >> 1) & 1);
       tc_fence_after();
-      if (trw) TRP(trb + 4 * j);
+      const uint32_t tQ = tmem + la + (e.par ? C::T_DQ1 + 64 * X : X * C::T_TILE + 128);
+      uint32_t rr[C::HD];
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        float s[32], dp[32];
-        ld32x2(tS + hh * 32, tP + hh * 32, s, dp);
-        if (hh == 1) {  // S/dP(j) fully in registers: the MMA may overwrite them
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(s_free + X);
-          if (trw) TRP(trb + 4 * j + 1);
-        }
-        const int k0 = j * C::BKV + hh * 32;
-        int lim = 32;
-        if (q >= p.S) lim = 0;
-        else if (p.causal || k0 + 32 > p.S) lim = min(p.causal ? q + 1 : p.S, p.S) - k0;
-#pragma unroll
-        for (int i = 0; i < 32; ++i) s[i] = ex2_approx(fmaf(s[i], sl2, -lse2));
-        if (lim < 32) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) s[i] = i < lim ? s[i] : 0.0f;
-        }
-#pragma unroll
-        for (int i = 0; i < 32; ++i) s[i] = s[i] * (dp[i] - D);
-        if (hh == 0 && j >= 2) mbar_wait(dq_done + 2 * X + u, ((j - 2) >> 1) & 1);  // dS buffer reuse
-        store_row32(dsb, r, hh * 4, s);
-      }
-      if (trw) TRP(trb + 4 * j + 2);
-      fence_async_smem();
+      for (int c = 0; c < C::HD / 32; ++c) tmem_ld_32x32b_x32(tQ + c * 32, rr + 32 * c);
+      tmem_ld_wait();
       tc_fence_before();
-      mbar_arrive(ds_full + 2 * X + u);
-      if (trw) TRP(trb + 4 * j + 3);
-    }
-    if (nkvX > 0) {
-      mbar_wait(dq_done + 2 * X + ((nkvX - 1) & 1), ((nkvX - 1) >> 1) & 1);
-      tc_fence_after();
-      __nv_bfloat16* dq = p.dqkv + static_cast<long long>(row0 + q) * 3 * p.d + h * C::HD;
+      mbar_arrive(dq_empty + 2 * X + e.par);
+      if (e.q < p.S) {
+        __nv_bfloat16* dq = p.dqkv + static_cast<long long>(e.b * p.S + e.q) * 3 * p.d + e.h * C::HD;
 #pragma unroll
-      for (int c = 0; c < C::HD / 32; ++c) {
-        uint32_t rr[32];
-        tmem_ld_32x32b_x32(tQ + c * 32, rr);
-        tmem_ld_wait();
-        if (q < p.S) {
-          uint32_t w[16];
+        for (int c = 0; c < C::HD / 32; ++c) {
+          uint32_t wv[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            __nv_bfloat162 hh2 = __floats2bfloat162_rn(__uint_as_float(rr[2 * i]) * p.scale,
-                                                      __uint_as_float(rr[2 * i + 1]) * p.scale);
-            w[i] = *reinterpret_cast<uint32_t*>(&hh2);
+            __nv_bfloat162 hh2 = __floats2bfloat162_rn(__uint_as_float(rr[32 * c + 2 * i]) * p.scale,
+                                                      __uint_as_float(rr[32 * c + 2 * i + 1]) * p.scale);
+            wv[i] = *reinterpret_cast<uint32_t*>(&hh2);
           }
           uint4* dst = reinterpret_cast<uint4*>(dq + c * 32);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) dst[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+          for (int i = 0; i < 4; ++i) dst[i] = make_uint4(wv[4 * i], wv[4 * i + 1], wv[4 * i + 2], wv[4 * i + 3]);
         }
       }
+    };
+    int it = 0, cX = 0;
+    float D = 0.0f, lse2 = 0.0f;
+    if (static_cast<int>(blockIdx.x) < n_items) row_stats(item(blockIdx.x), D, lse2);
+    for (int k = 0, w = blockIdx.x; w < n_items; w = snake_item(++k, blockIdx.x, gridDim.x), ++it) {
+      const Item I = item(w);
+      const int q = I.q0 + X * C::BQ + r;
+      const int nkvX = I.nkvt[X];
+      for (int j = 0; j < nkvX; ++j, ++cX) {
+        const int u = cX & 1;
+        const uint32_t dsb = sb + C::OFF_DS + (2 * X + u) * C::DST;
+        mbar_wait(s_full + X, cX & 1);
+        tc_fence_after();
+        if (trw) TRP(trb + 4 * cX);
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          float s[32], dp[32];
+          ld32x2(tS + hh * 32, tP + hh * 32, s, dp);
+          if (hh == 1) {  // S/dP(j) fully in registers: the MMA may overwrite them
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(s_free + X);
+            if (trw) TRP(trb + 4 * cX + 1);
+          }
+          const int k0 = j * C::BKV + hh * 32;
+          int lim = 32;
+          if (q >= p.S) lim = 0;
+          else if (p.causal || k0 + 32 > p.S) lim = min(p.causal ? q + 1 : p.S, p.S) - k0;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) s[i] = ex2_approx(fmaf(s[i], sl2, -lse2));
+          if (lim < 32) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) s[i] = i < lim ? s[i] : 0.0f;
+          }
+#pragma unroll
+          for (int i = 0; i < 32; ++i) s[i] = s[i] * (dp[i] - D);
+          if (hh == 0 && cX >= 2) mbar_wait(dq_done + 2 * X + u, ((cX - 2) >> 1) & 1);  // dS buffer reuse
+          store_row32(dsb, r, hh * 4, s);
+        }
+        if (trw) TRP(trb + 4 * cX + 2);
+        fence_async_smem();
+        tc_fence_before();
+        mbar_arrive(ds_full + 2 * X + u);
+        if (trw) TRP(trb + 4 * cX + 3);
+        if (j == 0 && pend.valid) {  // the previous item's dQ epilogue, off the critical path
+          epilogue(pend);
+          pend.valid = false;
+        }
+      }
+      if (nkvX > 0) pend = Pend{true, it & 1, cX - 1, q, I.h, I.b};
+      // the next item's row statistics (global loads overlap its Q / dO TMA)
+      if (const int wn = snake_item(k + 1, blockIdx.x, gridDim.x); wn < n_items) row_stats(item(wn), D, lse2);
     }
+    if (pend.valid) epilogue(pend);
   }
   tc_fence_before();
   __syncthreads();
@@ -816,37 +882,63 @@ struct KvPP {
   static constexpr int T_TILE = 256;  // TMEM per tile: S^T +0, dP^T +64, dV +128, dK +192
 };
 
+// Persistent over (key-tile pair, head, batch) work items (causal: the first
+// key pairs see the most queries -> first). The dV/dK accumulators fill TMEM,
+// so an item's first dV/dK MMA waits (acc_empty) for the previous item's
+// epilogue, which the group runs right after handing over the next item's
+// first block; the staged LSE/D slots run on a per-tile global block parity.
 __global__ void __launch_bounds__(384, 1)
     attn_bwd_dkdv_pp(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
                      const __grid_constant__ CUtensorMap tm_do, const BwdParams p) {
   using C = KvPP;
+#ifdef P2R_ATTN_TRACE
+  // diagnostic build only: CTA 0's timeline, dumped after the dq kernel's (o + 4 KB)
+  __shared__ long long s_tr[512];
+  const bool tr_cta = blockIdx.x == 0;
+#define TRK(slot) do { if (tr_cta && (slot) < 512) s_tr[(slot)] = clock64(); } while (0)
+#else
+#define TRK(slot) do {} while (0)
+#endif
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* kv_full = bar;
-  uint64_t* q_full = bar + 1;           // [NS]
+  uint64_t* kv_empty = bar + 1;
+  uint64_t* q_full = bar + 2;           // [NS]
   uint64_t* q_empty = q_full + C::NS;   // [NS]
   uint64_t* s_full = q_empty + C::NS;   // [tile]
   uint64_t* s_free = s_full + 2;        // [tile]
   uint64_t* p_full = s_free + 2;        // [tile]
   uint64_t* pv_done = p_full + 2;       // [tile]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
+  uint64_t* acc_empty = pv_done + 2;    // [tile]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int pk = blockIdx.x, h = blockIdx.y, b = blockIdx.z;  // causal: low pk = most queries = first
-  const int k0 = pk * 2 * C::BK, row0 = b * p.S;
   const int nq = (p.S + C::BQ - 1) / C::BQ;
-  int i0t[2];  // first query block of each key tile (causal: queries >= keys)
+  const int npk = (p.S + 2 * C::BK - 1) / (2 * C::BK);
+  const int n_items = npk * p.H * p.B;
+  struct Item {
+    int h, b, k0, i0t[2], i0;
+  };
+  auto item = [&](int w) {
+    Item I;
+    const int hb = p.H * p.B, pk = w / hb, rem = w - pk * hb;
+    I.h = rem % p.H;
+    I.b = rem / p.H;
+    I.k0 = pk * 2 * C::BK;
 #pragma unroll
-  for (int X = 0; X < 2; ++X) {
-    const int ks = k0 + X * C::BK;
-    i0t[X] = ks >= p.S ? nq : (p.causal ? ks / C::BQ : 0);
-  }
-  const int i0 = min(i0t[0], i0t[1]);
+    for (int X = 0; X < 2; ++X) {  // first query block of each key tile (causal: queries >= keys)
+      const int ks = I.k0 + X * C::BK;
+      I.i0t[X] = ks >= p.S ? nq : (p.causal ? ks / C::BQ : 0);
+    }
+    I.i0 = min(I.i0t[0], I.i0t[1]);
+    return I;
+  };
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_kv);
     tma_prefetch_desc(&tm_q);
     tma_prefetch_desc(&tm_do);
     mbar_init(kv_full, 1);
+    mbar_init(kv_empty, 1);
     for (int i = 0; i < C::NS; ++i) {
       mbar_init(q_full + i, 1);
       mbar_init(q_empty + i, 2);  // S^T/dP^T issuer (warp 1) + dV/dK issuer (warp 3)
@@ -856,6 +948,7 @@ __global__ void __launch_bounds__(384, 1)
       mbar_init(s_free + X, 4);
       mbar_init(p_full + X, 128);
       mbar_init(pv_done + X, 1);
+      mbar_init(acc_empty + X, 128);
     }
     fence_barrier_init();
   }
@@ -870,51 +963,61 @@ __global__ void __launch_bounds__(384, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(kv_full, 4 * C::KT);
-      for (int X = 0; X < 2; ++X) {
-        tma_load_2d(smem + C::OFF_K + X * C::KT, &tm_kv, kv_full, p.d + h * C::HD, row0 + k0 + X * C::BK);
-        tma_load_2d(smem + C::OFF_V + X * C::KT, &tm_kv, kv_full, 2 * p.d + h * C::HD, row0 + k0 + X * C::BK);
-      }
-      for (int i = i0; i < nq; ++i) {
-        const int n = i - i0, st = n % C::NS;
-        mbar_wait(q_empty + st, ((n / C::NS) & 1) ^ 1);
-        mbar_arrive_expect_tx(q_full + st, 2 * C::QT);
-        tma_load_2d(smem + C::OFF_Q + st * C::QT, &tm_q, q_full + st, h * C::HD, row0 + i * C::BQ);
-        tma_load_2d(smem + C::OFF_DO + st * C::QT, &tm_do, q_full + st, h * C::HD, row0 + i * C::BQ);
+      int G = 0, it = 0;
+      for (int k = 0, w = blockIdx.x; w < n_items; w = snake_item(++k, blockIdx.x, gridDim.x), ++it) {
+        const Item I = item(w);
+        const int row0 = I.b * p.S;
+        mbar_wait(kv_empty, (it & 1) ^ 1);  // the previous item's S^T/dP^T MMAs are done with K / V
+        mbar_arrive_expect_tx(kv_full, 4 * C::KT);
+        for (int X = 0; X < 2; ++X) {
+          tma_load_2d(smem + C::OFF_K + X * C::KT, &tm_kv, kv_full, p.d + I.h * C::HD, row0 + I.k0 + X * C::BK);
+          tma_load_2d(smem + C::OFF_V + X * C::KT, &tm_kv, kv_full, 2 * p.d + I.h * C::HD, row0 + I.k0 + X * C::BK);
+        }
+        for (int i = I.i0; i < nq; ++i, ++G) {
+          const int st = G % C::NS;
+          mbar_wait(q_empty + st, ((G / C::NS) & 1) ^ 1);
+          mbar_arrive_expect_tx(q_full + st, 2 * C::QT);
+          tma_load_2d(smem + C::OFF_Q + st * C::QT, &tm_q, q_full + st, I.h * C::HD, row0 + i * C::BQ);
+          tma_load_2d(smem + C::OFF_DO + st * C::QT, &tm_do, q_full + st, I.h * C::HD, row0 + i * C::BQ);
+        }
       }
     }
   } else if (warp == 1) {
     {  // whole warp: uniform control flow, one elected lane issues each MMA
       constexpr uint32_t id_s = make_idesc_bf16(C::BK, C::BQ, false, false);
-      mbar_wait(kv_full, 0);
-      tc_fence_after();
       const uint64_t dK0 = make_sw128_desc(sb + C::OFF_K, 16, 1024), dV0 = make_sw128_desc(sb + C::OFF_V, 16, 1024);
       const uint64_t dQ0 = make_sw128_desc(sb + C::OFF_Q, 16, 1024), dO0 = make_sw128_desc(sb + C::OFF_DO, 16, 1024);
-      auto issue_s = [&](int X, int i) {
-        const int n = i - i0t[X];
-        if (n >= 1) {
-          mbar_wait(s_free + X, (n - 1) & 1);
-          tc_fence_after();
-        }
-        const uint32_t st = (i - i0) % C::NS;
-        const uint64_t ak = dadd(dK0, X * C::KT), av = dadd(dV0, X * C::KT);
-        const uint64_t bq = dadd(dQ0, st * C::QT), bo = dadd(dO0, st * C::QT);
-        const uint32_t tS = tmem + X * C::T_TILE;
-#pragma unroll
-        for (int k = 0; k < C::HD / 16; ++k) {
-          umma_bf16_warp(tS, dadd(ak, k * 32), dadd(bq, k * 32), id_s, k > 0 ? 1u : 0u);
-          umma_bf16_warp(tS + 64, dadd(av, k * 32), dadd(bo, k * 32), id_s, k > 0 ? 1u : 0u);
-        }
-        umma_commit_warp(s_full + X);
-      };
-
-      for (int i = i0; i < nq; ++i) {
-        const int n = i - i0;
-        mbar_wait(q_full + n % C::NS, (n / C::NS) & 1);
+      int G = 0, it = 0, cX[2] = {0, 0};
+      for (int k = 0, w = blockIdx.x; w < n_items; w = snake_item(++k, blockIdx.x, gridDim.x), ++it) {
+        const Item I = item(w);
+        mbar_wait(kv_full, it & 1);
         tc_fence_after();
-        for (int X = 0; X < 2; ++X)
-          if (i >= i0t[X]) issue_s(X, i);
-        umma_commit_warp(q_empty + n % C::NS);
+        for (int i = I.i0; i < nq; ++i, ++G) {
+          const uint32_t st = G % C::NS;
+          mbar_wait(q_full + st, (G / C::NS) & 1);
+          tc_fence_after();
+          if (lane == 0 && G < 24) TRK(16 + 4 * G);
+          for (int X = 0; X < 2; ++X) {
+            if (i < I.i0t[X]) continue;
+            if (cX[X] >= 1) {
+              mbar_wait(s_free + X, (cX[X] - 1) & 1);
+              tc_fence_after();
+            }
+            if (lane == 0 && G < 24) TRK(16 + 4 * G + 1 + X);
+            const uint64_t ak = dadd(dK0, X * C::KT), av = dadd(dV0, X * C::KT);
+            const uint64_t bq = dadd(dQ0, st * C::QT), bo = dadd(dO0, st * C::QT);
+            const uint32_t tS = tmem + X * C::T_TILE;
+#pragma unroll
+            for (int k = 0; k < C::HD / 16; ++k) {
+              umma_bf16_warp(tS, dadd(ak, k * 32), dadd(bq, k * 32), id_s, k > 0 ? 1u : 0u);
+              umma_bf16_warp(tS + 64, dadd(av, k * 32), dadd(bo, k * 32), id_s, k > 0 ? 1u : 0u);
+            }
+            umma_commit_warp(s_full + X);
+            ++cX[X];
+          }
+          if (i == nq - 1) umma_commit_warp(kv_empty);  // this item's K / V are no longer read
+          umma_commit_warp(q_empty + st);
+        }
       }
     }
   } else if (warp == 3) {
@@ -923,133 +1026,177 @@ __global__ void __launch_bounds__(384, 1)
       const uint64_t dQm0 = make_sw128_desc(sb + C::OFF_Q, C::BQ * 128, 1024);
       const uint64_t dOm0 = make_sw128_desc(sb + C::OFF_DO, C::BQ * 128, 1024);
       const uint64_t dP0 = make_sw128_desc(sb + C::OFF_P, 16, 1024), dS0 = make_sw128_desc(sb + C::OFF_DS, 16, 1024);
-      for (int i = i0; i < nq; ++i) {
-        const uint32_t st = (i - i0) % C::NS;
-        for (int X = 0; X < 2; ++X) {
-          if (i < i0t[X]) continue;
-          const int n = i - i0t[X];
-          mbar_wait(p_full + X, n & 1);  // implies S^T(i) done, so Q_i / dO_i are in smem
-          tc_fence_after();
-          const uint64_t ap = dadd(dP0, X * C::PT), as = dadd(dS0, X * C::PT);
-          const uint64_t bo = dadd(dOm0, st * C::QT), bq = dadd(dQm0, st * C::QT);
-          const uint32_t tS = tmem + X * C::T_TILE;
+      int G = 0, it = 0, cX[2] = {0, 0};
+      for (int k = 0, w = blockIdx.x; w < n_items; w = snake_item(++k, blockIdx.x, gridDim.x), ++it) {
+        const Item I = item(w);
+        for (int i = I.i0; i < nq; ++i, ++G) {
+          const uint32_t st = G % C::NS;
+          for (int X = 0; X < 2; ++X) {
+            if (i < I.i0t[X]) continue;
+            const int n = i - I.i0t[X];
+            mbar_wait(p_full + X, cX[X] & 1);  // implies S^T(i) done, so Q_i / dO_i are in smem
+            tc_fence_after();
+            if (n == 0) {  // the previous item's dV/dK of this tile were drained by its epilogue
+              mbar_wait(acc_empty + X, (it & 1) ^ 1);
+              tc_fence_after();
+            }
+            const uint64_t ap = dadd(dP0, X * C::PT), as = dadd(dS0, X * C::PT);
+            const uint64_t bo = dadd(dOm0, st * C::QT), bq = dadd(dQm0, st * C::QT);
+            const uint32_t tS = tmem + X * C::T_TILE;
 #pragma unroll
-          for (int k = 0; k < C::BQ / 16; ++k) {
-            // dV += P^T dO ; dK += dS^T Q   (dO / Q blocks re-read MN-major: rows = queries)
-            umma_bf16_warp(tS + 128, dadd(ap, k * 32), dadd(bo, k * 2048), id_o, (n > 0 || k > 0) ? 1u : 0u);
-            umma_bf16_warp(tS + 192, dadd(as, k * 32), dadd(bq, k * 2048), id_o, (n > 0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < C::BQ / 16; ++k) {
+              // dV += P^T dO ; dK += dS^T Q   (dO / Q blocks re-read MN-major: rows = queries)
+              umma_bf16_warp(tS + 128, dadd(ap, k * 32), dadd(bo, k * 2048), id_o, (n > 0 || k > 0) ? 1u : 0u);
+              umma_bf16_warp(tS + 192, dadd(as, k * 32), dadd(bq, k * 2048), id_o, (n > 0 || k > 0) ? 1u : 0u);
+            }
+            umma_commit_warp(pv_done + X);
+            if (lane == 0 && cX[X] < 48) TRK(120 + 48 * X + cX[X]);
+            ++cX[X];
           }
-          umma_commit_warp(pv_done + X);
+          umma_commit_warp(q_empty + st);
         }
-        umma_commit_warp(q_empty + st);
       }
     }
   } else if (warp >= 4) {
     const int X = (warp - 4) >> 2;
     const int t = threadIdx.x - 128 - X * 128;  // 0..127 within the group
     const int kr = (warp & 3) * 32 + lane;       // key row in the tile == TMEM lane
-    const int key = k0 + X * C::BK + kr;
     const uint32_t la = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const uint32_t tS = tmem + la + X * C::T_TILE, tP = tS + 64;
-    const long long bh = static_cast<long long>(b) * p.H + h;
     const float sl2 = p.sl2;
-    const int iX0 = i0t[X];
     const uint32_t ldb = sb + C::OFF_LD + X * (2 * 2 * 64 * 4);  // this group's [slot][lse2 | D][64]
-    // lse2 / D of query block i staged in slot (i - iX0) & 1 (threads 0..63: lse, 64..127: D);
-    // block i+1's values are loaded into a register while block i is processed.
-    auto fetch_ld = [&](int i) -> float {
+    // lse2 / D of a query block staged in slot (tile block count) & 1 (threads 0..63: lse, 64..127: D);
+    // the next block's values are loaded into a register while the current one is processed
+    // (raw: consuming the load here would put its DRAM latency on every block).
+    auto fetch_ld = [&](const Item& I, int i) -> float {
       const int qq = i * C::BQ + (t & 63);
       if (i >= nq || qq >= p.S) return 0.0f;
+      const long long bh = static_cast<long long>(I.b) * p.H + I.h;
       return t < 64 ? p.lse[bh * p.S + qq] : p.dsum[bh * p.S + qq];
     };
     const float ld_scale = t < 64 ? kLog2e : 1.0f;
-    if (iX0 < nq) sts32f(ldb + 4 * ((t >> 6) * 64 + (t & 63)), fetch_ld(iX0) * ld_scale);
-    for (int i = iX0; i < nq; ++i) {
-      const int n = i - iX0, slot = n & 1;
-      const float ld_next = fetch_ld(i + 1);
-      named_sync(1 + X, 128);
-      mbar_wait(s_full + X, n & 1);
+    struct Pend {
+      bool valid;
+      int c_last, key, h, b;
+    } pend{};
+    auto epilogue = [&](const Pend& e) {
+      mbar_wait(pv_done + X, e.c_last & 1);
       tc_fence_after();
-      const int q1 = i * C::BQ;
+      uint32_t rr[2 * C::HD];  // dV | dK columns of this key row
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        float s[32], dp[32];
-        ld32x2(tS + hh * 32, tP + hh * 32, s, dp);
-        if (hh == 1) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(s_free + X);
-        }
-        const uint32_t lda = ldb + (slot * 128 + hh * 32) * 4;
-        // visible: query q >= key (causal), q < S, key < S
-        const int qb1 = q1 + hh * 32;
-        int lo = 0, hi = min(32, p.S - qb1);
-        if (p.causal) lo = max(0, key - qb1);
-        if (key >= p.S) hi = 0;
-#pragma unroll
-        for (int c4 = 0; c4 < 8; ++c4) {
-          const float4 l4 = lds128f(lda + 16 * c4);
-          s[4 * c4 + 0] = ex2_approx(fmaf(s[4 * c4 + 0], sl2, -l4.x));
-          s[4 * c4 + 1] = ex2_approx(fmaf(s[4 * c4 + 1], sl2, -l4.y));
-          s[4 * c4 + 2] = ex2_approx(fmaf(s[4 * c4 + 2], sl2, -l4.z));
-          s[4 * c4 + 3] = ex2_approx(fmaf(s[4 * c4 + 3], sl2, -l4.w));
-        }
-        if (lo > 0 || hi < 32) {
-#pragma unroll
-          for (int c = 0; c < 32; ++c) s[c] = (c >= lo && c < hi) ? s[c] : 0.0f;
-        }
-#pragma unroll
-        for (int c4 = 0; c4 < 8; ++c4) {
-          const float4 d4 = lds128f(lda + 256 + 16 * c4);
-          dp[4 * c4 + 0] = s[4 * c4 + 0] * (dp[4 * c4 + 0] - d4.x);
-          dp[4 * c4 + 1] = s[4 * c4 + 1] * (dp[4 * c4 + 1] - d4.y);
-          dp[4 * c4 + 2] = s[4 * c4 + 2] * (dp[4 * c4 + 2] - d4.z);
-          dp[4 * c4 + 3] = s[4 * c4 + 3] * (dp[4 * c4 + 3] - d4.w);
-        }
-        if (hh == 0 && n >= 1) mbar_wait(pv_done + X, (n - 1) & 1);  // P^T / dS^T buffer reuse
-        store_row32(sb + C::OFF_P + X * C::PT, kr, hh * 4, s);
-        store_row32(sb + C::OFF_DS + X * C::PT, kr, hh * 4, dp);
-      }
-      fence_async_smem();
+      for (int c = 0; c < 2 * C::HD / 32; ++c) tmem_ld_32x32b_x32(tS + 128 + c * 32, rr + 32 * c);
+      tmem_ld_wait();
       tc_fence_before();
-      mbar_arrive(p_full + X);
-      // every thread of the group passed this iteration's barrier: slot ^ 1 is free
-      sts32f(ldb + 4 * (((slot ^ 1) * 2 + (t >> 6)) * 64 + (t & 63)), ld_next * ld_scale);
-    }
-    const int nX = nq - iX0;
-    if (nX > 0) {
-      mbar_wait(pv_done + X, (nX - 1) & 1);
-      tc_fence_after();
-      // dK (scaled) then dV for this key row
+      mbar_arrive(acc_empty + X);
+      if (e.key < p.S) {
 #pragma unroll
-      for (int which = 0; which < 2; ++which) {
-        __nv_bfloat16* dst_row =
-            p.dqkv + static_cast<long long>(row0 + key) * 3 * p.d + (which == 0 ? p.d : 2 * p.d) + h * C::HD;
-        const float sc = which == 0 ? p.scale : 1.0f;
-        const uint32_t col = which == 0 ? 192 : 128;
+        for (int which = 0; which < 2; ++which) {  // dK (scaled) then dV
+          __nv_bfloat16* dst_row =
+              p.dqkv + static_cast<long long>(e.b * p.S + e.key) * 3 * p.d + (which == 0 ? p.d : 2 * p.d) + e.h * C::HD;
+          const float sc = which == 0 ? p.scale : 1.0f;
+          const int base = which == 0 ? C::HD : 0;
 #pragma unroll
-        for (int c = 0; c < C::HD / 32; ++c) {
-          uint32_t rr[32];
-          tmem_ld_32x32b_x32(tS + col + c * 32, rr);
-          tmem_ld_wait();
-          if (key < p.S) {
-            uint32_t w[16];
+          for (int c = 0; c < C::HD / 32; ++c) {
+            uint32_t wv[16];
 #pragma unroll
             for (int i2 = 0; i2 < 16; ++i2) {
-              __nv_bfloat162 hh2 = __floats2bfloat162_rn(__uint_as_float(rr[2 * i2]) * sc,
-                                                        __uint_as_float(rr[2 * i2 + 1]) * sc);
-              w[i2] = *reinterpret_cast<uint32_t*>(&hh2);
+              __nv_bfloat162 hh2 = __floats2bfloat162_rn(__uint_as_float(rr[base + 32 * c + 2 * i2]) * sc,
+                                                        __uint_as_float(rr[base + 32 * c + 2 * i2 + 1]) * sc);
+              wv[i2] = *reinterpret_cast<uint32_t*>(&hh2);
             }
             uint4* dst = reinterpret_cast<uint4*>(dst_row + c * 32);
 #pragma unroll
-            for (int i2 = 0; i2 < 4; ++i2) dst[i2] = make_uint4(w[4 * i2], w[4 * i2 + 1], w[4 * i2 + 2], w[4 * i2 + 3]);
+            for (int i2 = 0; i2 < 4; ++i2) dst[i2] = make_uint4(wv[4 * i2], wv[4 * i2 + 1], wv[4 * i2 + 2], wv[4 * i2 + 3]);
           }
         }
       }
+    };
+    int cX = 0;
+    if (static_cast<int>(blockIdx.x) < n_items) {
+      const Item I0 = item(blockIdx.x);
+      if (I0.i0t[X] < nq) sts32f(ldb + 4 * ((t >> 6) * 64 + (t & 63)), fetch_ld(I0, I0.i0t[X]) * ld_scale);
     }
+    for (int k = 0, w = blockIdx.x; w < n_items; w = snake_item(++k, blockIdx.x, gridDim.x)) {
+      const Item I = item(w);
+      const int key = I.k0 + X * C::BK + kr;
+      const int iX0 = I.i0t[X];
+      const int wn = snake_item(k + 1, blockIdx.x, gridDim.x);
+      const bool has_next = wn < n_items;
+      Item In{};
+      if (has_next) In = item(wn);
+      for (int i = iX0; i < nq; ++i, ++cX) {
+        const int n = i - iX0, slot = cX & 1;
+        // the value staged for this tile's next block: the next query block, or the next item's first
+        const float ld_next = i + 1 < nq ? fetch_ld(I, i + 1) : (has_next && In.i0t[X] < nq ? fetch_ld(In, In.i0t[X]) : 0.0f);
+        named_sync(1 + X, 128);
+        mbar_wait(s_full + X, cX & 1);
+        tc_fence_after();
+        const bool trw = (warp == 4 || warp == 8) && lane == 0 && cX < 48;
+        if (trw) TRK(240 + 128 * X + 2 * cX);
+        const int q1 = i * C::BQ;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          float s[32], dp[32];
+          ld32x2(tS + hh * 32, tP + hh * 32, s, dp);
+          if (hh == 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(s_free + X);
+          }
+          const uint32_t lda = ldb + (slot * 128 + hh * 32) * 4;
+          // visible: query q >= key (causal), q < S, key < S
+          const int qb1 = q1 + hh * 32;
+          int lo = 0, hi = min(32, p.S - qb1);
+          if (p.causal) lo = max(0, key - qb1);
+          if (key >= p.S) hi = 0;
+#pragma unroll
+          for (int c4 = 0; c4 < 8; ++c4) {
+            const float4 l4 = lds128f(lda + 16 * c4);
+            s[4 * c4 + 0] = ex2_approx(fmaf(s[4 * c4 + 0], sl2, -l4.x));
+            s[4 * c4 + 1] = ex2_approx(fmaf(s[4 * c4 + 1], sl2, -l4.y));
+            s[4 * c4 + 2] = ex2_approx(fmaf(s[4 * c4 + 2], sl2, -l4.z));
+            s[4 * c4 + 3] = ex2_approx(fmaf(s[4 * c4 + 3], sl2, -l4.w));
+          }
+          if (lo > 0 || hi < 32) {
+#pragma unroll
+            for (int c = 0; c < 32; ++c) s[c] = (c >= lo && c < hi) ? s[c] : 0.0f;
+          }
+#pragma unroll
+          for (int c4 = 0; c4 < 8; ++c4) {
+            const float4 d4 = lds128f(lda + 256 + 16 * c4);
+            dp[4 * c4 + 0] = s[4 * c4 + 0] * (dp[4 * c4 + 0] - d4.x);
+            dp[4 * c4 + 1] = s[4 * c4 + 1] * (dp[4 * c4 + 1] - d4.y);
+            dp[4 * c4 + 2] = s[4 * c4 + 2] * (dp[4 * c4 + 2] - d4.z);
+            dp[4 * c4 + 3] = s[4 * c4 + 3] * (dp[4 * c4 + 3] - d4.w);
+          }
+          if (hh == 0 && cX >= 1) mbar_wait(pv_done + X, (cX - 1) & 1);  // P^T / dS^T buffer reuse
+          store_row32(sb + C::OFF_P + X * C::PT, kr, hh * 4, s);
+          store_row32(sb + C::OFF_DS + X * C::PT, kr, hh * 4, dp);
+        }
+        fence_async_smem();
+        tc_fence_before();
+        mbar_arrive(p_full + X);
+        if (trw) TRK(240 + 128 * X + 2 * cX + 1);
+        // every thread of the group passed this iteration's barrier: slot ^ 1 is free
+        sts32f(ldb + 4 * (((slot ^ 1) * 2 + (t >> 6)) * 64 + (t & 63)), ld_next * ld_scale);
+        if (n == 0 && pend.valid) {  // the previous item's dK/dV epilogue, off the critical path
+          epilogue(pend);
+          pend.valid = false;
+        }
+      }
+      if (nq - iX0 > 0) pend = Pend{true, cX - 1, key, I.h, I.b};
+    }
+    if (pend.valid) epilogue(pend);
   }
   tc_fence_before();
   __syncthreads();
+#ifdef P2R_ATTN_TRACE
+  if (threadIdx.x == 0) TRK(0);
+  if (tr_cta)
+    for (int i = threadIdx.x; i < 512; i += blockDim.x)
+      reinterpret_cast<long long*>(const_cast<__nv_bfloat16*>(p.o))[512 + i] = s_tr[i];
+#endif
+#undef TRK
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
@@ -1097,11 +1244,11 @@ p2r_status run(const void* qkv, const BwdParams& p, cudaStream_t s) {
     static cudaError_t a4 =
         cudaFuncSetAttribute(attn_bwd_dkdv_pp, cudaFuncAttributeMaxDynamicSharedMemorySize, KvPP::SMEM);
     if (a3 != cudaSuccess || a4 != cudaSuccess) return set_cuda_error(a3 ? a3 : a4, "attention bwd attr");
-    const dim3 grid2((p.S + 255) / 256, p.H, p.B);
-    P2R_LAUNCH_K("attention bwd dq (tcgen05, 2 tiles)", attn_bwd_dq_pp, grid2, dim3(384), DqPP::SMEM, s, 1, qkv128,
-                 qkv64, do128, p);
-    P2R_LAUNCH_K("attention bwd dkdv (tcgen05, 2 tiles)", attn_bwd_dkdv_pp, grid2, dim3(384), KvPP::SMEM, s, 1,
-                 qkv128, qkv64, do64, p);
+    const int n_dq = (p.S + 255) / 256 * p.H * p.B;
+    P2R_LAUNCH_K("attention bwd dq (tcgen05, 2 tiles, persistent)", attn_bwd_dq_pp,
+                 dim3(n_dq < kNumSMs ? n_dq : kNumSMs), dim3(384), DqPP::SMEM, s, 1, qkv128, qkv64, do128, p);
+    P2R_LAUNCH_K("attention bwd dkdv (tcgen05, 2 tiles, persistent)", attn_bwd_dkdv_pp,
+                 dim3(n_dq < kNumSMs ? n_dq : kNumSMs), dim3(384), KvPP::SMEM, s, 1, qkv128, qkv64, do64, p);
     return P2R_OK;
   }
   const dim3 grid((p.S + 127) / 128, p.H, p.B);

@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(384, 1)
     if (lane == 0) {
       // ---------------- TMA producer ----------------
       int g = 0, it = 0;
-      for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
+      for (int k = 0, w = blockIdx.x; w < n_items; w = snake_item(++k, blockIdx.x, gridDim.x), ++it) {
         int qb, h, b;
         item(w, qb, h, b);
         const int row0 = b * p.S, nkv = nkv_of(qb);
@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(384, 1)
       };
       int g = 0, it = 0;
       int pg = -1, pj = 0, pit = 0;  // the PV still to issue
-      for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
+      for (int k = 0, w = blockIdx.x; w < n_items; w = snake_item(++k, blockIdx.x, gridDim.x), ++it) {
         int qb, h, b;
         item(w, qb, h, b);
         const int nkv = nkv_of(qb);
@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(384, 1)
       }
     };
     int g = 0, it = 0;
-    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
+    for (int k = 0, w = blockIdx.x; w < n_items; w = snake_item(++k, blockIdx.x, gridDim.x), ++it) {
       int qb, h, b;
       item(w, qb, h, b);
       const int nkv = nkv_of(qb), q0 = qb * BQ;

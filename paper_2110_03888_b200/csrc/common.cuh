@@ -415,6 +415,11 @@ P2R_DEVICE float2 gelu_grad2(float2 x) {
   return __ffma2_rn(__fmul2_rn(x, e), make_float2(0.39894228040143268f, 0.39894228040143268f), cdf);
 }
 
+// Static boustrophedon schedule for persistent kernels over work items sorted
+// heaviest-first: CTA c of G takes item c in round 0, G-1-c in round 1, ...
+// (pairs heavy with light items; strictly increasing per CTA).
+P2R_DEVICE int snake_item(int k, int c, int G) { return k * G + ((k & 1) ? G - 1 - c : c); }
+
 P2R_DEVICE float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

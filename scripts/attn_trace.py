@@ -13,7 +13,7 @@ from paper_2110_03888_b200 import _lib
 L = _lib.lib()
 P = lambda t: ctypes.c_void_p(t.data_ptr())
 st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-B, H, S, hd = 1, 16, 1024, 64
+B, H, S, hd = (8 if "--kv" in sys.argv else 1), 16, 1024, 64
 d = H * hd
 qkv = (torch.randn(B * S, 3 * d, device="cuda") * 0.5).bfloat16()
 o = torch.empty(B * S, d, device="cuda", dtype=torch.bfloat16)
@@ -38,6 +38,16 @@ if "--fwd" in sys.argv:
         a = [t[100 + 4 * j + i] for i in range(4)]
         f = lambda v: f"{v - t0:8d}" if 0 < v - t0 < 10**9 else "       -"
         print(f"{j:2d} | " + " ".join(f(v) for v in m) + " | " + " ".join(f(v) for v in a))
+    sys.exit(0)
+if "--kv" in sys.argv:  # dK/dV kernel, CTA 0 (B=8 shape: persistent items)
+    t = o.view(torch.int64).flatten()[512:1024].cpu().numpy()
+    v = [x for x in t if x > 0]
+    t0 = min(v)
+    g = lambda i: f"{t[i] - t0:8d}" if t[i] > 0 else "       -"
+    print(" blk | mma1: qfull S(X0) S(X1) | dVdK done X0 X1 | X0: sfull arrive | X1: sfull arrive")
+    for j in range(24):
+        print(f"{j:4d} | {g(16 + 4 * j)} {g(17 + 4 * j)} {g(18 + 4 * j)} | {g(120 + j)} {g(168 + j)} | "
+              f"{g(240 + 2 * j)} {g(241 + 2 * j)} | {g(368 + 2 * j)} {g(369 + 2 * j)}")
     sys.exit(0)
 if "--pp" in sys.argv:
     print(" j | mma: kvfull(j+1) S(j+1)issued dQA(j) dQB(j) | A: sfull  sfree  stored  dsfull | B: sfull  sfree  stored  dsfull")

@@ -73,7 +73,7 @@ def main():
     per = launches(lpath)
     tot = sum(v[1] for v in per.values())
     lines = [f"# {tag}: ncu launch list (gpu__time_duration.sum, --clock-control none)", "",
-             f"Source: `ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 python bench.py --steps 2 --warmup 3 --no-cpu-baseline`",
+             f"Source: `{os.environ.get('NCU_CMD', 'ncu --metrics gpu__time_duration.sum --clock-control none -c 700 python bench.py --steps 1 --warmup 1')}`",
              "(serialised, cold-cache per launch: compare SHARES with bench.py's live `kernels` breakdown, not absolutes).", "",
              "| kernel | launches | total ms | share |", "|---|---|---|---|"]
     for k, (n, ns) in sorted(per.items(), key=lambda a: -a[1][1]):

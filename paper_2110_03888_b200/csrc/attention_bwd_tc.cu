@@ -829,14 +829,28 @@ __global__ void __launch_bounds__(384, 1)
           int lim = 32;
           if (q >= p.S) lim = 0;
           else if (p.causal || k0 + 32 > p.S) lim = min(p.causal ? q + 1 : p.S, p.S) - k0;
+          {  // FP32x2: s * scale - lse, then P * (dP - D) (same per-element rounding as the scalar form)
+            const float2 sl2p = make_float2(sl2, sl2), nl = make_float2(-lse2, -lse2);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) s[i] = ex2_approx(fmaf(s[i], sl2, -lse2));
+            for (int i = 0; i < 32; i += 2) {
+              const float2 z = __ffma2_rn(make_float2(s[i], s[i + 1]), sl2p, nl);
+              s[i] = ex2_approx(z.x);
+              s[i + 1] = ex2_approx(z.y);
+            }
+          }
           if (lim < 32) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) s[i] = i < lim ? s[i] : 0.0f;
           }
+          {
+            const float2 nD = make_float2(-D, -D);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) s[i] = s[i] * (dp[i] - D);
+            for (int i = 0; i < 32; i += 2) {
+              const float2 v = __fmul2_rn(make_float2(s[i], s[i + 1]), __fadd2_rn(make_float2(dp[i], dp[i + 1]), nD));
+              s[i] = v.x;
+              s[i + 1] = v.y;
+            }
+          }
           if (hh == 0 && cX >= 2) mbar_wait(dq_done + 2 * X + u, ((cX - 2) >> 1) & 1);  // dS buffer reuse
           store_row32(dsb, r, hh * 4, s);
         }
@@ -1074,7 +1088,7 @@ __global__ void __launch_bounds__(384, 1)
       const long long bh = static_cast<long long>(I.b) * p.H + I.h;
       return t < 64 ? p.lse[bh * p.S + qq] : p.dsum[bh * p.S + qq];
     };
-    const float ld_scale = t < 64 ? kLog2e : 1.0f;
+    const float ld_scale = t < 64 ? -kLog2e : -1.0f;  // staged negated: -lse*log2e | -D (FP32x2 adds)
     struct Pend {
       bool valid;
       int c_last, key, h, b;
@@ -1149,13 +1163,16 @@ __global__ void __launch_bounds__(384, 1)
           int lo = 0, hi = min(32, p.S - qb1);
           if (p.causal) lo = max(0, key - qb1);
           if (key >= p.S) hi = 0;
+          const float2 sl2p = make_float2(sl2, sl2);
 #pragma unroll
-          for (int c4 = 0; c4 < 8; ++c4) {
+          for (int c4 = 0; c4 < 8; ++c4) {  // FP32x2 (same per-element rounding as the scalar form)
             const float4 l4 = lds128f(lda + 16 * c4);
-            s[4 * c4 + 0] = ex2_approx(fmaf(s[4 * c4 + 0], sl2, -l4.x));
-            s[4 * c4 + 1] = ex2_approx(fmaf(s[4 * c4 + 1], sl2, -l4.y));
-            s[4 * c4 + 2] = ex2_approx(fmaf(s[4 * c4 + 2], sl2, -l4.z));
-            s[4 * c4 + 3] = ex2_approx(fmaf(s[4 * c4 + 3], sl2, -l4.w));
+            const float2 z0 = __ffma2_rn(make_float2(s[4 * c4 + 0], s[4 * c4 + 1]), sl2p, make_float2(l4.x, l4.y));
+            const float2 z1 = __ffma2_rn(make_float2(s[4 * c4 + 2], s[4 * c4 + 3]), sl2p, make_float2(l4.z, l4.w));
+            s[4 * c4 + 0] = ex2_approx(z0.x);
+            s[4 * c4 + 1] = ex2_approx(z0.y);
+            s[4 * c4 + 2] = ex2_approx(z1.x);
+            s[4 * c4 + 3] = ex2_approx(z1.y);
           }
           if (lo > 0 || hi < 32) {
 #pragma unroll
@@ -1164,10 +1181,14 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
           for (int c4 = 0; c4 < 8; ++c4) {
             const float4 d4 = lds128f(lda + 256 + 16 * c4);
-            dp[4 * c4 + 0] = s[4 * c4 + 0] * (dp[4 * c4 + 0] - d4.x);
-            dp[4 * c4 + 1] = s[4 * c4 + 1] * (dp[4 * c4 + 1] - d4.y);
-            dp[4 * c4 + 2] = s[4 * c4 + 2] * (dp[4 * c4 + 2] - d4.z);
-            dp[4 * c4 + 3] = s[4 * c4 + 3] * (dp[4 * c4 + 3] - d4.w);
+            const float2 v0 = __fmul2_rn(make_float2(s[4 * c4 + 0], s[4 * c4 + 1]),
+                                         __fadd2_rn(make_float2(dp[4 * c4 + 0], dp[4 * c4 + 1]), make_float2(d4.x, d4.y)));
+            const float2 v1 = __fmul2_rn(make_float2(s[4 * c4 + 2], s[4 * c4 + 3]),
+                                         __fadd2_rn(make_float2(dp[4 * c4 + 2], dp[4 * c4 + 3]), make_float2(d4.z, d4.w)));
+            dp[4 * c4 + 0] = v0.x;
+            dp[4 * c4 + 1] = v0.y;
+            dp[4 * c4 + 2] = v1.x;
+            dp[4 * c4 + 3] = v1.y;
           }
           if (hh == 0 && cX >= 1) mbar_wait(pv_done + X, (cX - 1) & 1);  // P^T / dS^T buffer reuse
           store_row32(sb + C::OFF_P + X * C::PT, kr, hh * 4, s);

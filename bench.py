@@ -50,6 +50,7 @@ def parse():
     p.add_argument("--impl", default="p2r", choices=["p2r", "reference"])
     p.add_argument("--batch", type=int, default=8)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-graph", action="store_true", help="eager launches instead of one CUDA graph per step")
     p.add_argument("--cpu-procs", type=int, default=0, help="reference processes (0 = auto)")
     return p.parse_args()
 
@@ -275,9 +276,13 @@ def main_p2r(args):
         if world > 1:
             model.allreduce_grads()  # ncclAllReduce of the replicated grad granules, model stream
 
-    def step_device(i):
+    use_graph = world == 1 and not args.no_graph
+
+    def step_device(i, graph=use_graph):
+        # one CUDA graph per step on a single rank (captured during warm-up); the DP
+        # path's NCCL communicator keeps eager launches
         model.train_step_device(dtok.data_ptr(), dtgt.data_ptr(), dmask.data_ptr(), B, S, denom,
-                                loss_dev=loss_dev.data_ptr())
+                                loss_dev=loss_dev.data_ptr(), graph=graph)
         allreduce()
         model.adamw_step(p2r.lr_at(2e-4, 0.01, 1000, i))
 
@@ -322,13 +327,16 @@ def main_p2r(args):
     model.profile_reset()
     model.set_profiling(True)
     for i in range(args.steps):
-        step_device(args.warmup + args.steps + i)
+        step_device(args.warmup + args.steps + i, graph=False)  # events need eager launches
     barrier()
     model.set_profiling(False)
     prof = model.profile()
 
     # ---- end-to-end through the public host-buffer API
     e2e_steps = max(3, min(args.steps, 10))
+    model.train_step(tok, tgt, mask, B, denom)  # untimed: the host path captures its step graph here
+    allreduce()
+    model.adamw_step(p2r.lr_at(2e-4, 0.01, 1000, args.warmup + args.steps))
     barrier()
     t0 = time.perf_counter()
     for i in range(e2e_steps):
@@ -380,6 +388,7 @@ def main_p2r(args):
            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
            "config": {"workload": WORKLOAD, "global_batch": B * world, "seq_len": S,
                       "parallelism": f"dp{world}", "l2": "inputs larger than L2 (~7 GB activations per step)",
+                      "launch": "one CUDA graph per fwd+bwd step + eager AdamW" if use_graph else "eager",
                       "mfu_model_flops_per_token": model_flops},
            "clocks": clk, "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline,
            "kernels": breakdown,

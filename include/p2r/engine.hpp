@@ -312,6 +312,12 @@ class Model {
   static std::unique_ptr<Model> from_checkpoint(const std::string& path, StageState* st);
 
   cudaStream_t stream() const { return stream_; }
+  // train_step_device replayed as one CUDA graph (captured on the first call,
+  // re-captured when any argument changes): resident, MoE-free, single-rank
+  // models; the launches (and their programmatic-dependent-launch edges) are
+  // those of train_step_device, so results are bit-identical to it.
+  void train_step_device_graph(const int* d_tokens, const int* d_targets, const std::uint8_t* d_mask, int batch,
+                               int seq, double denom, AttentionMode mode, bool zero, float* loss_dev);
   void set_profiling(bool on) { prof_.on = on; }
   void profile(int cls, std::int64_t* launches, double* ms, double* flops, double* bytes);
   void profile_reset();
@@ -400,6 +406,14 @@ class Model {
   std::vector<int> slow_;
   int n_res_ = 0;
   std::unique_ptr<OffloadState> off_;
+  struct StepGraph {
+    cudaGraphExec_t exec = nullptr;
+    const void *tok = nullptr, *tgt = nullptr, *mask = nullptr, *loss = nullptr;
+    int batch = 0, seq = 0, mode = 0;
+    double denom = 0.0;
+    bool zero = false;
+    std::uint64_t kernels = 0;  // kernel launches the graph replays (p2r_launch_count)
+  } step_graph_;
   float offload_lr_ = 0.0f;
   // expert / data parallelism
   int ep_world_ = 1, ep_rank_ = 0;

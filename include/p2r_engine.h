@@ -63,6 +63,14 @@ p2r_status p2r_model_train_step_device(p2r_model* m, const int* d_tokens, const 
                                        const uint8_t* d_mask, int batch, int seq, double denom,
                                        int causal, int zero, float* loss_dev);
 
+/* train_step_device replayed as one CUDA graph: captured on the first call (which
+ * also runs the step) and re-captured whenever an argument changes; resident,
+ * MoE-free, single-rank models (P2R_ELOGIC otherwise). Bit-identical to
+ * p2r_model_train_step_device. The optimizer step stays outside the graph. */
+p2r_status p2r_model_train_step_device_graph(p2r_model* m, const int* d_tokens, const int* d_targets,
+                                             const uint8_t* d_mask, int batch, int seq, double denom,
+                                             int causal, int zero, float* loss_dev);
+
 /* AdamW (optim.hpp:29-54). */
 p2r_status p2r_model_adamw_attach(p2r_model* m, float b1, float b2, float eps, float wd);
 p2r_status p2r_model_adamw_step(p2r_model* m, float lr);

@@ -125,6 +125,16 @@ p2r_status p2r_model_train_step_device(p2r_model* m, const int* d_tokens, const 
   });
 }
 
+p2r_status p2r_model_train_step_device_graph(p2r_model* m, const int* d_tokens, const int* d_targets,
+                                             const uint8_t* d_mask, int batch, int seq, double denom, int causal,
+                                             int zero, float* loss_dev) {
+  return guard([&] {
+    if (denom <= 0.0) throw std::invalid_argument("softmax_cross_entropy: denominator must be > 0");
+    m->m->train_step_device_graph(d_tokens, d_targets, d_mask, batch, seq, denom, mode_of(causal), zero != 0,
+                                  loss_dev);
+  });
+}
+
 p2r_status p2r_model_adamw_attach(p2r_model* m, float b1, float b2, float eps, float wd) {
   return guard([&] { m->m->adamw_attach(b1, b2, eps, wd); });
 }

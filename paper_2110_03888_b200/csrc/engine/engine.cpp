@@ -20,6 +20,10 @@
 #include <string>
 
 #include "offload_state.hpp"
+
+namespace p2r {
+void count_launches(std::uint64_t n);  // status.cu: graph replays add their kernels to p2r_launch_count
+}
 #include "p2r_cuda.h"
 #include "p2r_engine.h"
 
@@ -216,6 +220,7 @@ Model::Model(ModelConfig config, NoInit, int ep_world, int ep_rank, bool force_e
 
 Model::~Model() {
   if (stream_) cudaStreamSynchronize(stream_);
+  if (step_graph_.exec) cudaGraphExecDestroy(step_graph_.exec);
   comm_destroy();
   off_.reset();
   if (pinned_) cudaFreeHost(pinned_);
@@ -897,6 +902,55 @@ void Model::train_step_device(const int* d_tokens, const int* d_targets, const s
     cuda_check(cudaMemcpyAsync(loss_dev, loss.data, 4, cudaMemcpyDeviceToDevice, stream_), "loss copy");
 }
 
+void Model::train_step_device_graph(const int* d_tokens, const int* d_targets, const std::uint8_t* d_mask, int batch,
+                                    int seq, double denom, AttentionMode mode, bool zero, float* loss_dev) {
+  if (off_ || cfg_.moe.enabled() || comm_ != nullptr || prof_.on)
+    throw std::logic_error("train_step_device_graph: needs a resident, MoE-free, single-rank, unprofiled model");
+  StepGraph& G = step_graph_;
+  const bool same = G.exec && G.tok == d_tokens && G.tgt == d_targets && G.mask == d_mask && G.loss == loss_dev &&
+                    G.batch == batch && G.seq == seq && G.denom == denom && G.mode == static_cast<int>(mode) &&
+                    G.zero == zero;
+  if (same) {
+    cuda_check(cudaGraphLaunch(G.exec, stream_), "step graph launch");
+    p2r::count_launches(G.kernels);
+    return;
+  }
+  if (G.exec) {
+    cuda_check(cudaGraphExecDestroy(G.exec), "step graph destroy");
+    G.exec = nullptr;
+  }
+  // this call's step runs eagerly (lazy allocations, kernel attributes, split-K
+  // counters all happen outside the capture), then the same launches are captured
+  train_step_device(d_tokens, d_targets, d_mask, batch, seq, denom, mode, zero, loss_dev);
+  cudaGraph_t graph = nullptr;
+  const std::uint64_t k0 = p2r_launch_count();
+  cuda_check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "step graph capture");
+  try {
+    train_step_device(d_tokens, d_targets, d_mask, batch, seq, denom, mode, zero, loss_dev);
+  } catch (...) {
+    cudaStreamEndCapture(stream_, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    throw;
+  }
+  cuda_check(cudaStreamEndCapture(stream_, &graph), "step graph capture end");
+  G.kernels = p2r_launch_count() - k0;
+  // the captured launches did not run: only the eager step above counts
+  p2r::count_launches(static_cast<std::uint64_t>(0) - G.kernels);
+  const cudaError_t e = cudaGraphInstantiate(&G.exec, graph, 0);
+  cudaGraphDestroy(graph);
+  cuda_check(e, "step graph instantiate");
+  cuda_check(cudaGraphUpload(G.exec, stream_), "step graph upload");  // device-side copy made once, not per launch
+  G.tok = d_tokens;
+  G.tgt = d_targets;
+  G.mask = d_mask;
+  G.loss = loss_dev;
+  G.batch = batch;
+  G.seq = seq;
+  G.denom = denom;
+  G.mode = static_cast<int>(mode);
+  G.zero = zero;
+}
+
 namespace {
 void validate_ids(const int* ids, std::size_t n, int V, const char* msg) {
   for (std::size_t i = 0; i < n; ++i)
@@ -923,8 +977,17 @@ float Model::train_step_host(const int* tokens, const int* targets, const std::u
   cuda_check(cudaMemcpyAsync(A.tokens.p, pin, T * 4, cudaMemcpyHostToDevice, stream_), "h2d");
   cuda_check(cudaMemcpyAsync(A.targets.p, pin + T * 4, T * 4, cudaMemcpyHostToDevice, stream_), "h2d");
   if (mask) cuda_check(cudaMemcpyAsync(A.mask.p, pin + T * 8, T, cudaMemcpyHostToDevice, stream_), "h2d");
-  train_step_device(A.tokens.as<int>(), A.targets.as<int>(), mask ? A.mask.as<std::uint8_t>() : nullptr, batch, seq,
-                    denom, mode, zero, nullptr);
+  // resident, MoE-free, single-rank steps replay one CUDA graph (P2R_STEP_GRAPH=0: eager launches)
+  static const bool graph_on = [] {
+    const char* e = std::getenv("P2R_STEP_GRAPH");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  if (graph_on && !off_ && !cfg_.moe.enabled() && comm_ == nullptr && !prof_.on)
+    train_step_device_graph(A.tokens.as<int>(), A.targets.as<int>(), mask ? A.mask.as<std::uint8_t>() : nullptr, batch,
+                            seq, denom, mode, zero, nullptr);
+  else
+    train_step_device(A.tokens.as<int>(), A.targets.as<int>(), mask ? A.mask.as<std::uint8_t>() : nullptr, batch, seq,
+                      denom, mode, zero, nullptr);
   float* lh = reinterpret_cast<float*>(pin + T * 9 + (64 - (T * 9) % 64) % 64);
   if (reinterpret_cast<char*>(lh) + 4 > pin + pinned_bytes_) lh = reinterpret_cast<float*>(pin);
   cuda_check(cudaMemcpyAsync(lh, A.loss.p, 4, cudaMemcpyDeviceToHost, stream_), "d2h loss");

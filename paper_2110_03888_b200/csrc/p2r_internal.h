@@ -15,6 +15,7 @@ namespace p2r {
 p2r_status set_error(p2r_status code, const char* msg);
 p2r_status set_cuda_error(cudaError_t e, const char* where);
 void count_launch();
+void count_launches(uint64_t n);  // graph replays: the kernels a captured graph launches
 p2r_status attention_fwd_tc(const void* qkv, void* o, float* lse, int B, int H, int S, int d, int causal,
                             cudaStream_t s);
 p2r_status attention_bwd_tc(const void* qkv, const void* o, const float* lse, const void* dout, float* dsum,

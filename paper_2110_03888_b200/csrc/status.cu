@@ -23,6 +23,7 @@ p2r_status set_cuda_error(cudaError_t e, const char* where) {
 }
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+void count_launches(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 }  // namespace p2r
 

@@ -46,6 +46,7 @@ _lib._EXTRA_SIGNATURES.update({
     "p2r_model_forward": [vp, vp, ip, ip, ip, vp],
     "p2r_model_train_step": [vp, vp, vp, vp, ip, ip, ctypes.c_double, ip, ip, vp],
     "p2r_model_train_step_device": [vp, vp, vp, vp, ip, ip, ctypes.c_double, ip, ip, vp],
+    "p2r_model_train_step_device_graph": [vp, vp, vp, vp, ip, ip, ctypes.c_double, ip, ip, vp],
     "p2r_model_adamw_attach": [vp, fp, fp, fp, fp],
     "p2r_model_adamw_step": [vp, fp],
     "p2r_model_adamw_set_step_count": [vp, i64],
@@ -303,9 +304,11 @@ class Model:
         return float(loss.value)
 
     def train_step_device(self, d_tokens: int, d_targets: int, d_mask, batch: int, seq: int,
-                          denom: float, causal=True, zero=True, loss_dev=None):
-        check(lib().p2r_model_train_step_device(self.h, d_tokens, d_targets, d_mask, batch, seq,
-                                                float(denom), int(causal), int(zero), loss_dev))
+                          denom: float, causal=True, zero=True, loss_dev=None, graph=False):
+        """Inputs resident on the device. graph=True replays the step as one CUDA
+        graph (captured on first use; resident, MoE-free, single-rank models)."""
+        fn = lib().p2r_model_train_step_device_graph if graph else lib().p2r_model_train_step_device
+        check(fn(self.h, d_tokens, d_targets, d_mask, batch, seq, float(denom), int(causal), int(zero), loss_dev))
 
     def stream(self) -> int:
         return int(lib().p2r_model_stream(self.h) or 0)

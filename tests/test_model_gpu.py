@@ -265,3 +265,51 @@ def test_error_behaviour(cuda):
         m.train_step(tok, tgt, mask, 2, 0.0)
     with pytest.raises(p2r.P2RInvalidArgument, match="d_model must be divisible by n_heads"):
         p2r.Model(p2r.Config(d_model=250, n_heads=4), 1)
+
+
+def test_train_step_graph_replay_bit_identical(cuda):
+    """train_step_device(graph=True): first call runs + captures, later calls replay one
+    CUDA graph; losses, parameters and AdamW moments match the eager path bit-for-bit,
+    the launch counter still counts the replayed kernels, and argument changes re-capture."""
+    import torch
+    import paper_2110_03888_b200 as p2r
+    cfg = p2r.Config(d_model=256, d_ff=1024, n_layers_graph=3, n_layers_params=1, n_heads=4, vocab_size=260,
+                     seq_len=128)
+    rng = np.random.default_rng(3)
+    tok = torch.from_numpy(rng.integers(0, 256, 8 * 128).astype(np.int32)).cuda()
+    tgt = torch.roll(tok, -1)
+    mask = torch.ones(8 * 128, dtype=torch.uint8, device="cuda")
+    models = [p2r.Model(cfg, 42) for _ in range(2)]
+    losses, counts = [[], []], [[], []]
+    for mi, m in enumerate(models):
+        m.attach_adamw()
+        loss = torch.zeros(1, device="cuda")
+        for i in range(4):
+            n0 = p2r.launch_count()
+            m.train_step_device(tok.data_ptr(), tgt.data_ptr(), mask.data_ptr(), 8, 128, 1024.0,
+                                loss_dev=loss.data_ptr(), graph=(mi == 1))
+            torch.cuda.synchronize()
+            counts[mi].append(p2r.launch_count() - n0)
+            losses[mi].append(float(loss))
+            m.adamw_step(1e-3)
+    assert losses[0] == losses[1]
+    assert counts[0] == counts[1] and counts[0][0] > 50  # replays count the kernels they launch
+    pa, pb = models[0].params(), models[1].params()
+    ma, mb = models[0].moments(), models[1].moments()
+    for n in pa:
+        assert np.array_equal(pa[n], pb[n]), n
+        assert np.array_equal(ma[n][0], mb[n][0]) and np.array_equal(ma[n][1], mb[n][1]), n
+    # a different batch re-captures and still matches eager
+    loss = torch.zeros(1, device="cuda")
+    la = models[0].train_step_device(tok.data_ptr(), tgt.data_ptr(), mask.data_ptr(), 4, 128, 512.0,
+                                     loss_dev=loss.data_ptr())
+    torch.cuda.synchronize()
+    l0 = float(loss)
+    models[1].train_step_device(tok.data_ptr(), tgt.data_ptr(), mask.data_ptr(), 4, 128, 512.0,
+                                loss_dev=loss.data_ptr(), graph=True)
+    torch.cuda.synchronize()
+    assert float(loss) == l0
+    moe = p2r.Model(p2r.Config(d_model=256, d_ff=1024, n_layers_graph=2, n_layers_params=1, n_heads=4,
+                               vocab_size=260, seq_len=128, n_experts=4, n_prototypes=1), 1)
+    with pytest.raises(p2r.P2RLogicError, match="resident, MoE-free"):
+        moe.train_step_device(tok.data_ptr(), tgt.data_ptr(), mask.data_ptr(), 8, 128, 1024.0, graph=True)

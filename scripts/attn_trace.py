@@ -13,7 +13,7 @@ from paper_2110_03888_b200 import _lib
 L = _lib.lib()
 P = lambda t: ctypes.c_void_p(t.data_ptr())
 st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-B, H, S, hd = (8 if "--kv" in sys.argv else 1), 16, 1024, 64
+B, H, S, hd = (8 if ("--kv" in sys.argv or "--fwd8" in sys.argv) else 1), 16, 1024, 64
 d = H * hd
 qkv = (torch.randn(B * S, 3 * d, device="cuda") * 0.5).bfloat16()
 o = torch.empty(B * S, d, device="cuda", dtype=torch.bfloat16)
@@ -28,12 +28,12 @@ torch.cuda.synchronize()
 t = o.view(torch.int64).flatten()[:512].cpu().numpy() if "--fwd" not in sys.argv else None
 t0 = None if t is None else (t[0] if "--pp" not in sys.argv else min(v for v in t[16:300] if v > 0))
 rel = lambda v: int(v - t0)
-if "--fwd" in sys.argv:
+if "--fwd" in sys.argv or "--fwd8" in sys.argv:
     t = lse.view(torch.int64).flatten()[:256].cpu().numpy()
     t0 = t[0]
     print("fwd CTA (last q tile): setup->end", t[1] - t0)
     print(" j | mma: kvfull  S-issued  p_full(j) PV-issued | sm(warp4): sfull  max-done  exps-done  arrived")
-    for j in range(16):
+    for j in range(22):
         m = [t[8 + 4 * j + i] for i in range(4)]
         a = [t[100 + 4 * j + i] for i in range(4)]
         f = lambda v: f"{v - t0:8d}" if 0 < v - t0 < 10**9 else "       -"

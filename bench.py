@@ -276,11 +276,11 @@ def main_p2r(args):
         if world > 1:
             model.allreduce_grads()  # ncclAllReduce of the replicated grad granules, model stream
 
-    use_graph = world == 1 and not args.no_graph
+    use_graph = not args.no_graph
 
     def step_device(i, graph=use_graph):
-        # one CUDA graph per step on a single rank (captured during warm-up); the DP
-        # path's NCCL communicator keeps eager launches
+        # one CUDA graph per fwd+bwd step (captured during warm-up); the DP all-reduce
+        # and AdamW follow it on the same stream
         model.train_step_device(dtok.data_ptr(), dtgt.data_ptr(), dmask.data_ptr(), B, S, denom,
                                 loss_dev=loss_dev.data_ptr(), graph=graph)
         allreduce()

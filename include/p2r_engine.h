@@ -65,7 +65,8 @@ p2r_status p2r_model_train_step_device(p2r_model* m, const int* d_tokens, const 
 
 /* train_step_device replayed as one CUDA graph: captured on the first call (which
  * also runs the step) and re-captured whenever an argument changes; resident,
- * MoE-free, single-rank models (P2R_ELOGIC otherwise). Bit-identical to
+ * MoE-free models (P2R_ELOGIC otherwise; the data-parallel all-reduce stays
+ * outside the graph). Bit-identical to
  * p2r_model_train_step_device. The optimizer step stays outside the graph. */
 p2r_status p2r_model_train_step_device_graph(p2r_model* m, const int* d_tokens, const int* d_targets,
                                              const uint8_t* d_mask, int batch, int seq, double denom,

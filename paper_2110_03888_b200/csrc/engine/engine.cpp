@@ -904,8 +904,9 @@ void Model::train_step_device(const int* d_tokens, const int* d_targets, const s
 
 void Model::train_step_device_graph(const int* d_tokens, const int* d_targets, const std::uint8_t* d_mask, int batch,
                                     int seq, double denom, AttentionMode mode, bool zero, float* loss_dev) {
-  if (off_ || cfg_.moe.enabled() || comm_ != nullptr || prof_.on)
-    throw std::logic_error("train_step_device_graph: needs a resident, MoE-free, single-rank, unprofiled model");
+  // (a dense model's communicator is only used by allreduce_grads, outside the step)
+  if (off_ || cfg_.moe.enabled() || prof_.on)
+    throw std::logic_error("train_step_device_graph: needs a resident, MoE-free, unprofiled model");
   StepGraph& G = step_graph_;
   const bool same = G.exec && G.tok == d_tokens && G.tgt == d_targets && G.mask == d_mask && G.loss == loss_dev &&
                     G.batch == batch && G.seq == seq && G.denom == denom && G.mode == static_cast<int>(mode) &&
@@ -982,7 +983,7 @@ float Model::train_step_host(const int* tokens, const int* targets, const std::u
     const char* e = std::getenv("P2R_STEP_GRAPH");
     return e == nullptr || std::atoi(e) != 0;
   }();
-  if (graph_on && !off_ && !cfg_.moe.enabled() && comm_ == nullptr && !prof_.on)
+  if (graph_on && !off_ && !cfg_.moe.enabled() && !prof_.on)
     train_step_device_graph(A.tokens.as<int>(), A.targets.as<int>(), mask ? A.mask.as<std::uint8_t>() : nullptr, batch,
                             seq, denom, mode, zero, nullptr);
   else

@@ -306,7 +306,7 @@ class Model:
     def train_step_device(self, d_tokens: int, d_targets: int, d_mask, batch: int, seq: int,
                           denom: float, causal=True, zero=True, loss_dev=None, graph=False):
         """Inputs resident on the device. graph=True replays the step as one CUDA
-        graph (captured on first use; resident, MoE-free, single-rank models)."""
+        graph (captured on first use; resident, MoE-free models)."""
         fn = lib().p2r_model_train_step_device_graph if graph else lib().p2r_model_train_step_device
         check(fn(self.h, d_tokens, d_targets, d_mask, batch, seq, float(denom), int(causal), int(zero), loss_dev))
 

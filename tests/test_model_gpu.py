@@ -311,5 +311,5 @@ def test_train_step_graph_replay_bit_identical(cuda):
     assert float(loss) == l0
     moe = p2r.Model(p2r.Config(d_model=256, d_ff=1024, n_layers_graph=2, n_layers_params=1, n_heads=4,
                                vocab_size=260, seq_len=128, n_experts=4, n_prototypes=1), 1)
-    with pytest.raises(p2r.P2RLogicError, match="resident, MoE-free"):
+    with pytest.raises(p2r.P2RLogicError, match="resident, MoE-free"):  # MoE: the EP exchange runs in the step
         moe.train_step_device(tok.data_ptr(), tgt.data_ptr(), mask.data_ptr(), 8, 128, 1024.0, graph=True)

@@ -578,8 +578,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           // edges). Slots alternate per chunk; BIAS_GELU fills both (out, pre).
           constexpr bool kTwo = EPI == P2R_EPI_BIAS_GELU;
           const bool zrow = row0 + lane >= zero_from;  // grouped padding rows are written as 0
-          const bool rvalid = lane < nrows;
-          const long long grow = grow0 + lane;
 #pragma unroll 1
           for (int c = cb; c < ce; ++c) {
             uint32_t r[32];
@@ -599,26 +597,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                   if (j < nv) reinterpret_cast<float*>(b4)[j] = __ldg(bias + col0 + j);
               }
             }
-            uint32_t ax[16];  // GELU': this row's 32 pre-activations (bf16 pairs)
-            if constexpr (EPI == P2R_EPI_DGELU) {
-#pragma unroll
-              for (int j = 0; j < 16; ++j) ax[j] = 0u;
-              if (rvalid && !zrow) {
-                const __nv_bfloat16* ap = static_cast<const __nv_bfloat16*>(p.aux) + grow * p.ldaux + col0;
-                if (nv == 32) {
-#pragma unroll
-                  for (int q = 0; q < 4; ++q) {
-                    const uint4 u = __ldg(reinterpret_cast<const uint4*>(ap) + q);
-                    ax[4 * q] = u.x, ax[4 * q + 1] = u.y, ax[4 * q + 2] = u.z, ax[4 * q + 3] = u.w;
-                  }
-                } else {
-                  const unsigned short* a16 = reinterpret_cast<const unsigned short*>(ap);
-#pragma unroll
-                  for (int j = 0; j < 32; ++j)
-                    if (j < nv) ax[j >> 1] |= static_cast<uint32_t>(__ldg(a16 + j)) << (16 * (j & 1));
-                }
-              }
-            }
             tmem_ld_wait();
             uint32_t o[16];
             uint32_t pr[kTwo ? 16 : 1];
@@ -628,14 +606,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                                           reinterpret_cast<const float2*>(b4)[j]);
               if constexpr (EPI == P2R_EPI_BF16) {
                 o[j] = pack2_bf16(x.x, x.y);
-              } else if constexpr (EPI == P2R_EPI_BIAS_GELU) {
+              } else {  // BIAS_GELU
                 pr[j] = pack2_bf16(x.x, x.y);
                 const float2 g = gelu2(x);
                 o[j] = pack2_bf16(g.x, g.y);
-              } else {
-                const float2 d = __fmul2_rn(
-                    x, gelu_grad2(make_float2(__uint_as_float(ax[j] << 16), __uint_as_float(ax[j] & 0xFFFF0000u))));
-                o[j] = pack2_bf16(d.x, d.y);
               }
               if (zrow) {
                 o[j] = 0u;

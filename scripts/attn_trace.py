@@ -13,7 +13,7 @@ from paper_2110_03888_b200 import _lib
 L = _lib.lib()
 P = lambda t: ctypes.c_void_p(t.data_ptr())
 st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-B, H, S, hd = (8 if ("--kv" in sys.argv or "--fwd8" in sys.argv) else 1), 16, 1024, 64
+B, H, S, hd = (8 if ("--kv" in sys.argv or "--fwd8" in sys.argv or "--pp8" in sys.argv) else 1), 16, 1024, 64
 d = H * hd
 qkv = (torch.randn(B * S, 3 * d, device="cuda") * 0.5).bfloat16()
 o = torch.empty(B * S, d, device="cuda", dtype=torch.bfloat16)
@@ -26,7 +26,7 @@ for _ in range(3):
     _lib.check(L.p2r_attention_bwd(P(qkv), P(o), P(lse), P(do), P(dsum), P(dqkv), B, H, S, d, 1, st))
 torch.cuda.synchronize()
 t = o.view(torch.int64).flatten()[:512].cpu().numpy() if "--fwd" not in sys.argv else None
-t0 = None if t is None else (t[0] if "--pp" not in sys.argv else min(v for v in t[16:300] if v > 0))
+t0 = None if t is None else (t[0] if not ("--pp" in sys.argv or "--pp8" in sys.argv) else min(v for v in t[16:300] if v > 0))
 rel = lambda v: int(v - t0)
 if "--fwd" in sys.argv or "--fwd8" in sys.argv:
     t = lse.view(torch.int64).flatten()[:256].cpu().numpy()
@@ -49,12 +49,12 @@ if "--kv" in sys.argv:  # dK/dV kernel, CTA 0 (B=8 shape: persistent items)
         print(f"{j:4d} | {g(16 + 4 * j)} {g(17 + 4 * j)} {g(18 + 4 * j)} | {g(120 + j)} {g(168 + j)} | "
               f"{g(240 + 2 * j)} {g(241 + 2 * j)} | {g(368 + 2 * j)} {g(369 + 2 * j)}")
     sys.exit(0)
-if "--pp" in sys.argv:
+if "--pp" in sys.argv or "--pp8" in sys.argv:
     print(" j | mma: kvfull(j+1) S(j+1)issued dQA(j) dQB(j) | A: sfull  sfree  stored  dsfull | B: sfull  sfree  stored  dsfull")
     for j in range(16):
         m = [t[16 + 4 * j + i] for i in range(4)]
         a = [t[100 + 4 * j + i] for i in range(4)]
-        b = [t[200 + 4 * j + i] for i in range(4)]
+        b = [t[300 + 4 * j + i] for i in range(4)]  # group B: trb = 100 + 200
         f = lambda v: f"{rel(v):8d}" if 0 < v - t0 < 10**9 else "       -"
         print(f"{j:2d} | " + " ".join(f(v) for v in m) + " | " + " ".join(f(v) for v in a) + " | " + " ".join(f(v) for v in b))
     sys.exit(0)

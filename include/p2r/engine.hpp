@@ -413,7 +413,12 @@ class Model {
     double denom = 0.0;
     bool zero = false;
     std::uint64_t kernels = 0;  // kernel launches the graph replays (p2r_launch_count)
+    // buffers the graph baked in: any reallocation (another batch shape through any
+    // entry point, a grown GEMM workspace) forces a re-capture
+    std::uint64_t acts_gen = 0;
+    const void* ws = nullptr;
   } step_graph_;
+  std::uint64_t acts_gen_ = 0;  // bumped whenever ensure_acts reallocates the activation buffers
   float offload_lr_ = 0.0f;
   // expert / data parallelism
   int ep_world_ = 1, ep_rank_ = 0;

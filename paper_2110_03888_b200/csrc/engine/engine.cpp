@@ -535,6 +535,7 @@ void Model::ensure_acts(int B, int S) {
   A->targets = DevBuf(static_cast<std::size_t>(T) * 4);
   A->mask = DevBuf(static_cast<std::size_t>(T));
   acts_ = std::move(A);
+  ++acts_gen_;
   const std::size_t pin = static_cast<std::size_t>(T) * 9 + 64;
   if (pinned_bytes_ < pin) {
     if (pinned_) cudaFreeHost(pinned_);
@@ -908,9 +909,10 @@ void Model::train_step_device_graph(const int* d_tokens, const int* d_targets, c
   if (off_ || cfg_.moe.enabled() || prof_.on)
     throw std::logic_error("train_step_device_graph: needs a resident, MoE-free, unprofiled model");
   StepGraph& G = step_graph_;
+  ensure_acts(batch, seq);  // (a no-op unless the shape changed: then the generation moves on)
   const bool same = G.exec && G.tok == d_tokens && G.tgt == d_targets && G.mask == d_mask && G.loss == loss_dev &&
                     G.batch == batch && G.seq == seq && G.denom == denom && G.mode == static_cast<int>(mode) &&
-                    G.zero == zero;
+                    G.zero == zero && G.acts_gen == acts_gen_ && G.ws == splitk_ws_.p;
   if (same) {
     cuda_check(cudaGraphLaunch(G.exec, stream_), "step graph launch");
     p2r::count_launches(G.kernels);
@@ -950,6 +952,8 @@ void Model::train_step_device_graph(const int* d_tokens, const int* d_targets, c
   G.denom = denom;
   G.mode = static_cast<int>(mode);
   G.zero = zero;
+  G.acts_gen = acts_gen_;
+  G.ws = splitk_ws_.p;
 }
 
 namespace {

@@ -309,6 +309,20 @@ def test_train_step_graph_replay_bit_identical(cuda):
                                 loss_dev=loss.data_ptr(), graph=True)
     torch.cuda.synchronize()
     assert float(loss) == l0
+    # a forward at another batch size reallocates the activation buffers the graph baked
+    # in: the next replay must re-capture (and still match eager bit-for-bit)
+    for rnd in range(2):  # round 0 (re-)captures at batch 8; round 1 replays after the forward
+        for mi, m in enumerate(models):
+            m.train_step_device(tok.data_ptr(), tgt.data_ptr(), mask.data_ptr(), 8, 128, 1024.0,
+                                loss_dev=loss.data_ptr(), graph=(mi == 1))
+            torch.cuda.synchronize()
+            losses[mi].append(float(loss))
+            if rnd == 0:
+                m.forward(tok.cpu().numpy()[:2 * 128], 2)
+    assert losses[0][-2:] == losses[1][-2:]
+    pa, pb = models[0].grads(), models[1].grads()
+    for n in pa:
+        assert np.array_equal(pa[n], pb[n]), n
     moe = p2r.Model(p2r.Config(d_model=256, d_ff=1024, n_layers_graph=2, n_layers_params=1, n_heads=4,
                                vocab_size=260, seq_len=128, n_experts=4, n_prototypes=1), 1)
     with pytest.raises(p2r.P2RLogicError, match="resident, MoE-free"):  # MoE: the EP exchange runs in the step

@@ -5,7 +5,6 @@ P2R_LIB=build/exp/libp2r_trace.so python scripts/attn_trace.py
 """
 import ctypes
 import sys
-import numpy as np
 import torch
 sys.path.insert(0, ".")
 from paper_2110_03888_b200 import _lib

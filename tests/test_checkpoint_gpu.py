@@ -5,7 +5,6 @@ Contracts checked bit-for-bit: save -> load -> train k steps == train k steps
 uninterrupted; delink(pseudo checkpoint) gives a REAL checkpoint whose
 logits equal the Pseudo model's and whose every layer carries the shared layer's
 weights and AdamW moments."""
-import os
 
 import numpy as np
 import pytest

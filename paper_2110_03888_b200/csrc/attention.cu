@@ -530,8 +530,9 @@ using namespace p2r;
 
 extern "C" p2r_status p2r_attention_fwd(const void* qkv, void* o, float* lse, int B, int H, int S,
                                         int d, int causal, void* stream) {
-  if (B <= 0 || H <= 0 || S <= 0 || d % H != 0)
+  if (B < 0 || H <= 0 || S < 0 || d <= 0 || d % H != 0)
     return set_error(P2R_EINVAL, "masked_attention: q/k/v must share a [B,H,S,hd] shape");
+  if (B == 0 || S == 0) return P2R_OK;  // empty batch / sequence: nothing to compute
   attn::AttnParams p{};
   p.qkv = static_cast<const __nv_bfloat16*>(qkv);
   p.o = static_cast<__nv_bfloat16*>(o);
@@ -556,8 +557,9 @@ extern "C" p2r_status p2r_attention_fwd(const void* qkv, void* o, float* lse, in
 extern "C" p2r_status p2r_attention_bwd(const void* qkv, const void* o, const float* lse,
                                         const void* dout, float* dsum_ws, void* dqkv, int B, int H,
                                         int S, int d, int causal, void* stream) {
-  if (B <= 0 || H <= 0 || S <= 0 || d % H != 0)
+  if (B < 0 || H <= 0 || S < 0 || d <= 0 || d % H != 0)
     return set_error(P2R_EINVAL, "masked_attention: q/k/v must share a [B,H,S,hd] shape");
+  if (B == 0 || S == 0) return P2R_OK;  // empty batch / sequence: nothing to compute
   attn::AttnParams p{};
   p.qkv = static_cast<const __nv_bfloat16*>(qkv);
   p.o = const_cast<__nv_bfloat16*>(static_cast<const __nv_bfloat16*>(o));

@@ -1003,8 +1003,10 @@ extern "C" p2r_status p2r_set_workspace(void* ptr, size_t bytes) {
 extern "C" p2r_status p2r_gemm(const p2r_gemm_args* a, void* stream) {
   if (a == nullptr) return set_error(P2R_EINVAL, "gemm: null args");
   if (a->m <= 0 || a->n <= 0 || a->k <= 0) {
-    if (a->m >= 0 && a->n >= 0 && a->k >= 0) return P2R_OK;  // empty product: nothing to do
-    return set_error(P2R_EINVAL, "matmul: negative dimension");
+    if (a->m < 0 || a->n < 0 || a->k < 0) return set_error(P2R_EINVAL, "matmul: negative dimension");
+    if (a->m == 0 || a->n == 0 || a->epi == P2R_EPI_ACC_F32) return P2R_OK;  // empty C, or C += 0
+    // k == 0 with a writing epilogue would need C = epilogue(0); no caller does that
+    return set_error(P2R_EINVAL, "gemm: k == 0 is only defined for EPI_ACC_F32 (C += 0)");
   }
   if ((a->lda % 8) || (a->ldb % 8))
     return set_error(P2R_EINVAL, "gemm: leading dimensions must be multiples of 8 elements");

@@ -262,3 +262,36 @@ def test_bias_grad(cuda, dtype):
     call("bias_grad", x, 0 if dtype == "f32" else 1, n, rows, n, 1, 0, None, out, ctypes.c_longlong(0), ws)
     ref = 1 + x.float().sum(0)
     assert float((out - ref).abs().max() / ref.abs().max()) < 1e-5
+
+
+def test_empty_and_degenerate_inputs(cuda):
+    """Zero-size inputs are no-ops (the reference's loops simply do not run); negative
+    sizes and an undefined k == 0 product are rejected with a status, never a crash."""
+    import torch
+    from paper_2110_03888_b200 import _lib
+    L = _lib.lib()
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    A = torch.zeros(128, 64, device=cuda).bfloat16()
+    C = torch.full((128, 128), 2.0, device=cuda)
+    P = lambda t: ctypes.c_void_p(t.data_ptr())
+
+    def gemm(m, n, k, epi):
+        a = _lib.GemmArgs(m=m, n=n, k=k, a=A.data_ptr(), lda=64, b=A.data_ptr(), ldb=64, epi=epi,
+                          c=C.data_ptr(), ldc=128, split_k=1)
+        return L.p2r_gemm(ctypes.byref(a), st)
+
+    assert gemm(0, 128, 64, _lib.EPI_F32) == 0 and gemm(128, 0, 64, _lib.EPI_F32) == 0
+    assert gemm(128, 128, 0, _lib.EPI_ACC_F32) == 0  # C += 0
+    torch.cuda.synchronize()
+    assert bool((C == 2.0).all())
+    assert gemm(128, 128, 0, _lib.EPI_F32) != 0 and b"k == 0" in L.p2r_last_error()
+    assert gemm(-1, 128, 64, _lib.EPI_F32) != 0
+    qkv = torch.zeros(1, 3 * 64, device=cuda).bfloat16()
+    o = torch.zeros(1, 64, device=cuda).bfloat16()
+    lse = torch.zeros(1, device=cuda)
+    assert L.p2r_attention_fwd(P(qkv), P(o), P(lse), 0, 1, 128, 64, 1, st) == 0  # empty batch
+    assert L.p2r_attention_fwd(P(qkv), P(o), P(lse), 1, 1, 0, 64, 1, st) == 0    # empty sequence
+    assert L.p2r_attention_fwd(P(qkv), P(o), P(lse), 1, 3, 128, 64, 1, st) != 0  # d % H != 0
+    x = torch.zeros(1, 128, device=cuda)
+    assert L.p2r_layernorm_fwd(P(x), P(x), P(x), 0, 128, ctypes.c_float(1e-5), None, P(x), P(x), P(x), st) == 0
+    torch.cuda.synchronize()

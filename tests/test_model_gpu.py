@@ -333,6 +333,16 @@ def test_train_step_graph_replay_bit_identical(cuda):
     pa, pb = models[0].grads(), models[1].grads()
     for n in pa:
         assert np.array_equal(pa[n], pb[n]), n
+    # gradient accumulation: zero=True then zero=False micro-steps (the flag is part of
+    # the graph key; the accumulating graph must not re-zero the gradients)
+    for mi, m in enumerate(models):
+        for z in (True, False, False):
+            m.train_step_device(tok.data_ptr(), tgt.data_ptr(), mask.data_ptr(), 8, 128, 1024.0,
+                                zero=z, graph=(mi == 1))
+        torch.cuda.synchronize()
+    ga, gb = models[0].grads(), models[1].grads()
+    for n in ga:
+        assert np.array_equal(ga[n], gb[n]), n
     moe = p2r.Model(p2r.Config(d_model=256, d_ff=1024, n_layers_graph=2, n_layers_params=1, n_heads=4,
                                vocab_size=260, seq_len=128, n_experts=4, n_prototypes=1), 1)
     with pytest.raises(p2r.P2RLogicError, match="resident, MoE-free"):  # MoE: the EP exchange runs in the step

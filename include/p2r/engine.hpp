@@ -243,6 +243,9 @@ class Model {
   int ep_world() const { return ep_world_; }
   int ep_rank() const { return ep_rank_; }
   bool ep_active() const { return ep_world_ > 1 || force_ep_; }
+  // Dense layers take db2 from the column sums staged by the LayerNorm backward that
+  // produced their output gradient (wider rows would spill its extra accumulators).
+  bool db2_fused() const { return !cfg_.moe.enabled() && cfg_.d_model <= 13 * 128; }
   Model(const Model&) = delete;
   Model& operator=(const Model&) = delete;
 

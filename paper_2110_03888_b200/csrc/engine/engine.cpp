@@ -175,6 +175,11 @@ struct Acts {
   DevBuf h16, meanf, rstdf, logits32, dlogits16, loss, loss_sum, ce_ws, dh32;
   DevBuf dres, dres16, tmp32, dx1, dx1_16, do16, dqkv16, dh16, dye16, dxe32, dw, glogits, dsum;
   DevBuf ln_ws, colsum_ws, embed_ws;
+  // Dense FFN2 bias gradient: the LayerNorm backward that produces dres also writes
+  // its per-block column sums here; the consuming layer's LN2 backward finishes them
+  // into db2. db2_for = the graph layer they belong to (-1: none staged).
+  DevBuf db2_stage;
+  int db2_blocks = 0, db2_for = -1;
   DevBuf tokens, targets, mask;
   DevBuf xe_send16, ye_owner32, dxe_owner32, full_counts;  // expert-parallel exchange
 };
@@ -528,6 +533,9 @@ void Model::ensure_acts(int B, int S) {
     A->glogits = DevBuf(static_cast<std::size_t>(T) * E * 4);
   }
   A->ln_ws = DevBuf(p2r_layernorm_bwd_workspace(T, d));
+  if (db2_fused())
+    A->db2_stage = DevBuf(static_cast<std::size_t>(std::max(p2r_layernorm_bwd_blocks(T, d, 0),
+                                                            p2r_layernorm_bwd_blocks(T, d, 1))) * d * 4);
   const int bias_n = std::max(dff, d);
   A->colsum_ws = DevBuf(p2r_colsum_workspace(std::max(T, A->seg), bias_n, std::max(1, E)));
   A->embed_ws = DevBuf(p2r_embed_bwd_workspace(T, cfg_.vocab_size));
@@ -653,6 +661,7 @@ Tensor Model::embed_forward(GradTape* tape, const int* d_tokens, int batch, int 
   if (tape) {
     tape->record([this, d_tokens, batch, seq]() {
       Acts& A2 = *acts_;
+      A2.db2_for = -1;
       prof(P2R_PROF_EMBED, 0, 8.0 * A2.T * cfg_.d_model, [&] {
         p2r_check(p2r_embed_bwd(d_tokens, A2.dres.as<float>(), batch, seq, cfg_.d_model, cfg_.vocab_size,
                                 eg(emb_.tok), eg(emb_.pos), A2.embed_ws.p, A2.embed_ws.bytes, stream_),
@@ -760,10 +769,12 @@ void Model::block_backward(int g, AttentionMode mode) {
     // FFN2: dW2 += g^T dy ; db2 += colsum(dy) ; dh = (dy W2^T) * gelu'(hpre)
     gemm(dff, d, T, L.g16.p, dff, true, dy16, d, true, P2R_EPI_ACC_F32, lg(o, layer_.w2), d, nullptr, 0, nullptr,
          nullptr, 0, 0, 0, 0, nullptr, 0 /* library picks the split */);
-    prof(P2R_PROF_BIAS, 0, 4.0 * T * d, [&] {
-      p2r_check(p2r_bias_grad(dy, 0, d, T, d, 1, 0, nullptr, lg(o, layer_.b2), 0, A.colsum_ws.as<float>(), stream_),
-                "db2");
-    });
+    if (A.db2_for != g) {  // dres was not produced by a staging LayerNorm backward
+      prof(P2R_PROF_BIAS, 0, 4.0 * T * d, [&] {
+        p2r_check(p2r_bias_grad(dy, 0, d, T, d, 1, 0, nullptr, lg(o, layer_.b2), 0, A.colsum_ws.as<float>(), stream_),
+                  "db2");
+      });
+    }
     // db1 += colsum(dh) is folded into the GELU' epilogue (column partials of the bf16 dh)
     gemm(T, dff, d, dy16, d, false, lp16(o, layer_.w2), d, false, P2R_EPI_DGELU, A.dh16.p, dff, nullptr, 0, nullptr,
          L.hpre16.p, dff, 0, 0, 0, nullptr, 1, lg(o, layer_.b1));
@@ -816,11 +827,17 @@ void Model::block_backward(int g, AttentionMode mode) {
   }
   const double Td = static_cast<double>(T) * d;
   const double attn_flops = 4.0 * A.B * H * static_cast<double>(A.S) * A.S * (d / H) * (causal ? 1.0 : 2.0);
-  // LN2 backward: dx1 = dy + LN2'(db)
+  // LN2 backward: dx1 = dy + LN2'(db); its finish kernel also adds the staged
+  // column sums of dy into db2 (dense layers whose dres came from a LayerNorm backward)
+  const bool db2_staged = db2_fused() && A.db2_for == g;
+  A.db2_for = -1;
   prof(P2R_PROF_LAYERNORM, 0, Td * 18, [&] {
-    p2r_check(p2r_layernorm_bwd(A.tmp32.as<float>(), L.x1.as<float>(), L.mean2.as<float>(), L.rstd2.as<float>(),
-                                lp(o, layer_.ln2_g), dy, T, d, A.dx1.as<float>(), A.dx1_16.p, lg(o, layer_.ln2_g),
-                                lg(o, layer_.ln2_b), A.ln_ws.as<float>(), stream_),
+    p2r_check(p2r_layernorm_bwd_fused(A.tmp32.as<float>(), L.x1.as<float>(), L.mean2.as<float>(),
+                                      L.rstd2.as<float>(), lp(o, layer_.ln2_g), dy, T, d, A.dx1.as<float>(),
+                                      A.dx1_16.p, lg(o, layer_.ln2_g), lg(o, layer_.ln2_b), A.ln_ws.as<float>(),
+                                      nullptr, db2_staged ? A.db2_stage.as<float>() : nullptr,
+                                      db2_staged ? A.db2_blocks : 0, db2_staged ? lg(o, layer_.b2) : nullptr,
+                                      stream_),
               "ln2 bwd");
   });
   // O projection: dWo += o^T dx1 ; do = dx1 Wo^T
@@ -836,13 +853,19 @@ void Model::block_backward(int g, AttentionMode mode) {
   gemm(d, 3 * d, T, L.a16.p, d, true, A.dqkv16.p, 3 * d, true, P2R_EPI_ACC_F32, lg(o, layer_.wqkv), 3 * d, nullptr,
        0, nullptr, nullptr, 0, 0, 0, 0, nullptr, 0 /* library picks the split */);
   gemm(T, d, 3 * d, A.dqkv16.p, 3 * d, false, lp16(o, layer_.wqkv), 3 * d, false, P2R_EPI_F32, A.tmp32.p, d);
-  // LN1 backward: dx = dx1 + LN1'(da)
+  // LN1 backward: dx = dx1 + LN1'(da); for a dense layer below, also stage dx's column sums (its db2)
+  const bool stage = db2_fused() && g > 0;
   prof(P2R_PROF_LAYERNORM, 0, Td * 18, [&] {
-    p2r_check(p2r_layernorm_bwd(A.tmp32.as<float>(), xin, L.mean1.as<float>(), L.rstd1.as<float>(),
-                                lp(o, layer_.ln1_g), A.dx1.as<float>(), T, d, dy, dy16, lg(o, layer_.ln1_g),
-                                lg(o, layer_.ln1_b), A.ln_ws.as<float>(), stream_),
+    p2r_check(p2r_layernorm_bwd_fused(A.tmp32.as<float>(), xin, L.mean1.as<float>(), L.rstd1.as<float>(),
+                                      lp(o, layer_.ln1_g), A.dx1.as<float>(), T, d, dy, dy16, lg(o, layer_.ln1_g),
+                                      lg(o, layer_.ln1_b), A.ln_ws.as<float>(),
+                                      stage ? A.db2_stage.as<float>() : nullptr, nullptr, 0, nullptr, stream_),
               "ln1 bwd");
   });
+  if (stage) {
+    A.db2_blocks = p2r_layernorm_bwd_blocks(T, d, 1);
+    A.db2_for = g - 1;
+  }
   if (off_) offload_release(o, true);
 }
 
@@ -865,12 +888,18 @@ Tensor Model::head_forward(GradTape* tape, const Tensor& x) {
       gemm(V2, d2, T2, A2.dlogits16.p, A2.vld, true, A2.h16.p, d2, true, P2R_EPI_ACC_F32, eg(emb_.tok), d2, nullptr,
            0, nullptr, nullptr, 0, 0, 0, 0, nullptr, 0 /* library picks the split */);
       gemm(T2, d2, V2, A2.dlogits16.p, A2.vld, false, ep16(emb_.tok), d2, true, P2R_EPI_F32, A2.dh32.p, d2);
+      const bool stage = db2_fused();  // the last layer's db2 = column sums of this dres
       prof(P2R_PROF_LAYERNORM, 0, 14.0 * T2 * d2, [&] {
-        p2r_check(p2r_layernorm_bwd(A2.dh32.as<float>(), xin, A2.meanf.as<float>(), A2.rstdf.as<float>(),
-                                    ep(emb_.fin_g), nullptr, T2, d2, A2.dres.as<float>(), A2.dres16.p,
-                                    eg(emb_.fin_g), eg(emb_.fin_b), A2.ln_ws.as<float>(), stream_),
+        p2r_check(p2r_layernorm_bwd_fused(A2.dh32.as<float>(), xin, A2.meanf.as<float>(), A2.rstdf.as<float>(),
+                                          ep(emb_.fin_g), nullptr, T2, d2, A2.dres.as<float>(), A2.dres16.p,
+                                          eg(emb_.fin_g), eg(emb_.fin_b), A2.ln_ws.as<float>(),
+                                          stage ? A2.db2_stage.as<float>() : nullptr, nullptr, 0, nullptr, stream_),
                   "final ln bwd");
       });
+      if (stage) {
+        A2.db2_blocks = p2r_layernorm_bwd_blocks(T2, d2, 0);
+        A2.db2_for = cfg_.n_layers_graph - 1;
+      }
     });
   }
   return Tensor{T, V, A.logits32.as<float>(), nullptr, nullptr};

@@ -161,12 +161,16 @@ __global__ void __launch_bounds__(256) ln_fwd_reg_kernel(const float* __restrict
 // dx = resid + inv * (gy - mean(gy) - xhat * mean(gy * xhat)), gy = dy * gain.
 // dgain/dbias: per-lane column accumulators over the warp's rows, combined per
 // block (warp order) into partial[blockIdx.x][2][D]; ln_param_grad_reduce adds
-// the block partials into the grads in block order.
-template <int NV>
+// the block partials into the grads in block order. COLSUM: the column sums of
+// dx itself are accumulated the same way into cpartial[blockIdx.x][D] (the dense
+// block backward takes the FFN2 bias gradient of the layer below from them,
+// add_bias backward tensor.cpp:227-231, instead of re-reading dx).
+template <int NV, bool COLSUM>
 __global__ void __launch_bounds__(128) ln_bwd_kernel(
     const float* __restrict__ dy, const float* __restrict__ x, const float* __restrict__ mean_in,
     const float* __restrict__ rstd_in, const float* __restrict__ gain, const float* __restrict__ resid, int rows,
-    float* __restrict__ dx32, __nv_bfloat16* __restrict__ dx16, float* __restrict__ partial, int nst) {
+    float* __restrict__ dx32, __nv_bfloat16* __restrict__ dx16, float* __restrict__ partial, int nst,
+    float* __restrict__ cpartial) {
   pdl_trigger();
   pdl_wait();
   constexpr int D = 128 * NV;
@@ -189,9 +193,11 @@ __global__ void __launch_bounds__(128) ln_bwd_kernel(
   }
   __syncthreads();
   const float inv_d = 1.0f / static_cast<float>(D);
-  float4 pg[NV], pb[NV];
+  float4 pg[NV], pb[NV], pc[COLSUM ? NV : 1];
 #pragma unroll
   for (int i = 0; i < NV; ++i) pg[i] = pb[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int i = 0; i < (COLSUM ? NV : 1); ++i) pc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   float mu_n = 0.f, inv_n = 0.f;
   if (nrows > 0) {
     mu_n = mean_in[gw];
@@ -242,52 +248,71 @@ __global__ void __launch_bounds__(128) ln_bwd_kernel(
       const long long off = static_cast<long long>(r) * D + 4LL * c4;
       *reinterpret_cast<float4*>(dx32 + off) = out;
       if (dx16) st_bf16x4(dx16 + off, out);
+      if constexpr (COLSUM) {
+        pc[i].x += out.x;
+        pc[i].y += out.y;
+        pc[i].z += out.z;
+        pc[i].w += out.w;
+      }
     }
     __syncwarp();  // every lane's reads of this slot are done before it is refilled
     if (lane == 0 && k + nst < nrows) ln_row_issue(bar + st, ring + st * slot, src, ntens, r + nst * W, D);
   }
   // combine the warps' column partials in warp order (the ring is drained)
   __syncthreads();
-  float* red = reinterpret_cast<float*>(ln_smem + D * 4);  // [nw][2][D]
+  constexpr int NACC = COLSUM ? 3 : 2;
+  float* red = reinterpret_cast<float*>(ln_smem + D * 4);  // [nw][NACC][D]
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
     const int c4 = lane + 32 * i;
-    reinterpret_cast<float4*>(red + (warp * 2) * D)[c4] = pg[i];
-    reinterpret_cast<float4*>(red + (warp * 2 + 1) * D)[c4] = pb[i];
+    reinterpret_cast<float4*>(red + (warp * NACC) * D)[c4] = pg[i];
+    reinterpret_cast<float4*>(red + (warp * NACC + 1) * D)[c4] = pb[i];
+    if constexpr (COLSUM) reinterpret_cast<float4*>(red + (warp * NACC + 2) * D)[c4] = pc[i];
   }
   __syncthreads();
   float* out = partial + static_cast<long long>(blockIdx.x) * 2 * D;
-  for (int c = threadIdx.x; c < 2 * D; c += blockDim.x) {
+  for (int c = threadIdx.x; c < NACC * D; c += blockDim.x) {
     float t = 0.f;
-    for (int w = 0; w < nw; ++w) t += red[w * 2 * D + c];
-    out[c] = t;
+    for (int w = 0; w < nw; ++w) t += red[w * NACC * D + c];
+    if (c < 2 * D) {
+      out[c] = t;
+    } else if constexpr (COLSUM) {
+      cpartial[static_cast<long long>(blockIdx.x) * D + (c - 2 * D)] = t;
+    }
   }
 }
 
-// grad_gain[c] += sum_b partial[b][0][c]; grad_bias[c] += sum_b partial[b][1][c].
-// 1024 threads per 32 flattened columns: warp w sums partial rows w, w+32, ...
-// (coalesced 128-byte rows, all loads of a warp in flight together), then the
-// 32 warp sums are added in warp order.
+// grad_gain[c] += sum_b partial[b][0][c]; grad_bias[c] += sum_b partial[b][1][c];
+// and, when cin != NULL, cdst[c] += sum_b cin[b][c] (a previous backward's dx
+// column partials, see ln_bwd_kernel COLSUM). 1024 threads per 32 flattened
+// columns: warp w sums partial rows w, w+32, ... (coalesced 128-byte rows, all
+// loads of a warp in flight together), then the 32 warp sums are added in warp order.
 __global__ void __launch_bounds__(1024) ln_param_grad_reduce(const float* __restrict__ partial, int nblk, int D,
-                                                             float* __restrict__ ggain, float* __restrict__ gbias) {
+                                                             float* __restrict__ ggain, float* __restrict__ gbias,
+                                                             const float* __restrict__ cin, int cblk,
+                                                             float* __restrict__ cdst) {
   pdl_trigger();
   pdl_wait();
   __shared__ float red[32][33];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c = blockIdx.x * 32 + lane;  // flattened [2][D] column
+  const int c = blockIdx.x * 32 + lane;  // flattened [2][D] (+ [D]) column
+  const int ncol = cin ? 3 * D : 2 * D;
   float s = 0.f;
   if (c < 2 * D) {
 #pragma unroll 8
     for (int b = warp; b < nblk; b += 32) s += partial[static_cast<long long>(b) * 2 * D + c];
+  } else if (c < ncol) {
+#pragma unroll 8
+    for (int b = warp; b < cblk; b += 32) s += cin[static_cast<long long>(b) * D + (c - 2 * D)];
   }
   red[warp][lane] = s;
   __syncthreads();
-  if (warp == 0 && c < 2 * D) {
+  if (warp == 0 && c < ncol) {
     float t = 0.f;
 #pragma unroll
     for (int w = 0; w < 32; ++w) t += red[w][lane];
     const int which = c / D, col = c % D;
-    float* dst = which ? gbias : ggain;
+    float* dst = which == 0 ? ggain : (which == 1 ? gbias : cdst);
     if (dst) dst[col] += t;
   }
 }
@@ -452,7 +477,7 @@ LnLaunch ln_bwd_launch(int rows, int d, int ntens) {
   LnLaunch l{};
   l.nst = 2;
   while (l.nst > 1 && d * 4 + kLnBwdWarps * l.nst * ntens * d * 4 > 110 * 1024) --l.nst;
-  const int ring = kLnBwdWarps * l.nst * ntens * d * 4, red = kLnBwdWarps * 2 * d * 4;
+  const int ring = kLnBwdWarps * l.nst * ntens * d * 4, red = kLnBwdWarps * 3 * d * 4;
   l.smem = d * 4 + (ring > red ? ring : red);
   int per_sm = kSmemPerSM / (l.smem + 1024);
   per_sm = per_sm < 1 ? 1 : (per_sm > 2 ? 2 : per_sm);
@@ -518,36 +543,60 @@ extern "C" size_t p2r_layernorm_bwd_workspace(int rows, int d) {
   return static_cast<size_t>(b2 > b3 ? b2 : b3) * 2 * d * sizeof(float);
 }
 
-extern "C" p2r_status p2r_layernorm_bwd(const float* dy, const float* x, const float* mean,
-                                        const float* rstd, const float* gain, const float* resid,
-                                        int rows, int d, float* dx, void* dx_bf16, float* ggain,
-                                        float* gbias, float* partial_ws, void* stream) {
+extern "C" int p2r_layernorm_bwd_blocks(int rows, int d, int has_resid) {
+  if (rows <= 0 || !ln_dim_ok(d)) return 0;
+  return ln_bwd_launch(rows, d, has_resid ? 3 : 2).blocks;
+}
+
+extern "C" p2r_status p2r_layernorm_bwd_fused(const float* dy, const float* x, const float* mean,
+                                              const float* rstd, const float* gain, const float* resid,
+                                              int rows, int d, float* dx, void* dx_bf16, float* ggain,
+                                              float* gbias, float* partial_ws, float* dx_colsum_ws,
+                                              const float* colsum_in, int colsum_blocks, float* colsum_dst,
+                                              void* stream) {
   if (rows <= 0) return P2R_OK;
   if (!ln_dim_ok(d)) return set_error(P2R_EINVAL, "layernorm: d_model must be a multiple of 128 in [128, 2048]");
+  if ((colsum_in == nullptr) != (colsum_dst == nullptr) || (colsum_in && colsum_blocks <= 0))
+    return set_error(P2R_EINVAL, "layernorm bwd: colsum_in, colsum_blocks and colsum_dst go together");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const LnLaunch l = ln_bwd_launch(rows, d, resid ? 3 : 2);
   auto* d16 = static_cast<__nv_bfloat16*>(dx_bf16);
   switch (d / 128) {
-#define P2R_LN_BWD(NV)                                                                                     \
-  case NV: {                                                                                               \
-    static cudaError_t a = cudaFuncSetAttribute(ln_bwd_kernel<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+#define P2R_LN_BWD_ONE(NV, CS)                                                                                \
+  {                                                                                                        \
+    static cudaError_t a = cudaFuncSetAttribute(ln_bwd_kernel<NV, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                                 kLnSmemAttr);                                                \
     if (a != cudaSuccess) return set_cuda_error(a, "layernorm bwd attr");                                  \
-    const cudaError_t le = launch_k(ln_bwd_kernel<NV>, dim3(l.blocks), dim3(32 * kLnBwdWarps), l.smem, s, 1, dy, x, mean, rstd, gain, \
-                 resid, rows, dx, d16, partial_ws, l.nst);                                                  \
+    const cudaError_t le = launch_k(ln_bwd_kernel<NV, CS>, dim3(l.blocks), dim3(32 * kLnBwdWarps), l.smem, s, 1, dy, x, mean, \
+                 rstd, gain, resid, rows, dx, d16, partial_ws, l.nst, dx_colsum_ws);                         \
     if (le != cudaSuccess) return set_cuda_error(le, "layernorm bwd");                                       \
-    break;                                                                                                 \
   }
+#define P2R_LN_BWD(NV)                          \
+  case NV:                                      \
+    if (dx_colsum_ws) P2R_LN_BWD_ONE(NV, true)  \
+    else P2R_LN_BWD_ONE(NV, false)              \
+    break;
     P2R_LN_NV_CASES(P2R_LN_BWD)
 #undef P2R_LN_BWD
+#undef P2R_LN_BWD_ONE
     default: break;
   }
   P2R_CHECK_LAUNCH("layernorm bwd");
-  if (ggain || gbias) {
-    P2R_LAUNCH_K("layernorm param grad", ln_param_grad_reduce, dim3((2 * d + 31) / 32), dim3(1024), 0, s, 1,
-                 static_cast<const float*>(partial_ws), l.blocks, d, ggain, gbias);
+  if (ggain || gbias || colsum_dst) {
+    const int ncol = colsum_in ? 3 * d : 2 * d;
+    P2R_LAUNCH_K("layernorm param grad", ln_param_grad_reduce, dim3((ncol + 31) / 32), dim3(1024), 0, s, 1,
+                 static_cast<const float*>(partial_ws), l.blocks, d, ggain, gbias, colsum_in, colsum_blocks,
+                 colsum_dst);
   }
   return P2R_OK;
+}
+
+extern "C" p2r_status p2r_layernorm_bwd(const float* dy, const float* x, const float* mean,
+                                        const float* rstd, const float* gain, const float* resid,
+                                        int rows, int d, float* dx, void* dx_bf16, float* ggain,
+                                        float* gbias, float* partial_ws, void* stream) {
+  return p2r_layernorm_bwd_fused(dy, x, mean, rstd, gain, resid, rows, d, dx, dx_bf16, ggain, gbias, partial_ws,
+                                 nullptr, nullptr, 0, nullptr, stream);
 }
 
 extern "C" p2r_status p2r_embed_fwd(const int* ids, const float* tok, const float* pos, int T,

@@ -53,6 +53,47 @@ def test_layernorm(cuda, rows, d):
     assert rel(gb.cpu().numpy(), rgb + 1) < 1e-5
 
 
+@pytest.mark.parametrize("rows,d,resid", [(8192, 1024, True), (8192, 1024, False), (301, 384, True), (5, 128, True)])
+def test_layernorm_bwd_fused_colsum(cuda, rows, d, resid):
+    """p2r_layernorm_bwd_fused: dx and the LN grads equal the plain backward bit for
+    bit; its staged column partials, finished by a second call's reduce kernel,
+    equal colsum(dx) (the dense FFN2 bias gradient, tensor.cpp:227-231)."""
+    import torch
+    from paper_2110_03888_b200 import _lib
+    L = _lib.lib()
+    rng = np.random.default_rng(1)
+    x = (rng.standard_normal((rows, d)) * 2).astype(np.float32)
+    X, G, GY = dev(x), dev(rng.standard_normal(d).astype(np.float32)), dev(rng.standard_normal((rows, d)).astype(np.float32))
+    R = dev(rng.standard_normal((rows, d)).astype(np.float32)) if resid else None
+    mean = torch.empty(rows, device=cuda)
+    rstd = torch.empty(rows, device=cuda)
+    call("layernorm_fwd", X, G, G, rows, d, 1e-5, None, torch.empty(rows, d, device=cuda), mean, rstd)
+    ws = torch.empty(L.p2r_layernorm_bwd_workspace(rows, d) // 4, device=cuda)
+    outs = []
+    for fused in (False, True):
+        dx = torch.empty(rows, d, device=cuda)
+        dx16 = torch.empty(rows, d, dtype=torch.bfloat16, device=cuda)
+        gg, gb = torch.zeros(d, device=cuda), torch.zeros(d, device=cuda)
+        if fused:
+            nblk = L.p2r_layernorm_bwd_blocks(rows, d, int(resid))
+            stage = torch.full((nblk, d), float("nan"), device=cuda)
+            call("layernorm_bwd_fused", GY, X, mean, rstd, G, R, rows, d, dx, dx16, gg, gb, ws, stage, None, 0, None)
+        else:
+            call("layernorm_bwd", GY, X, mean, rstd, G, R, rows, d, dx, dx16, gg, gb, ws)
+        outs.append((dx, dx16, gg, gb))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+    dx = outs[0][0]
+    # a second backward (no LN grads) finishes the staged partials into db2 (+=)
+    db2 = torch.ones(d, device=cuda)
+    call("layernorm_bwd_fused", GY, X, mean, rstd, G, None, rows, d, torch.empty(rows, d, device=cuda), None, None,
+         None, ws, None, stage, nblk, db2)
+    ref = dx.double().sum(0) + 1
+    assert float((db2.double() - ref).norm() / ref.norm()) < 1e-6
+    with pytest.raises(Exception, match="colsum"):
+        call("layernorm_bwd_fused", GY, X, mean, rstd, G, None, rows, d, dx, None, None, None, ws, None, stage, 0, db2)
+
+
 def test_layernorm_golden(cuda):
     """Reference-generated LN golden (d=40 is not a supported width): pad-free
     check on the KAT instead: constant row -> 0."""

@@ -160,11 +160,14 @@ double predict_step_time(const std::vector<std::int64_t>& layer_bytes, const std
 // of P parameters the copy engines move, per step: forward H2D 2P (bf16 shadow) +
 // fp32 vectors; backward H2D 12P (fp32 master, m, v); D2H 14P (p, m, v, bf16).
 // Copies overlap compute on their own streams, so
-//   step = max(C_fwd, H2D_fwd/h2d) + max(C_bwd, H2D_bwd/h2d, D2H/d2h)
+//   step = max(C_fwd, H2D_fwd/h2d) + max(C_bwd, H2D_bwd/h2d, D2H/d2h),
+// and at least (H2D_fwd + H2D_bwd)/h2d + the first SLOW layer's Fn load + its
+// write-back (the ring prefetches backward granules during the forward).
 // with C_* = per-layer compute x L (calibrated from a resident step).
 struct OffloadCost {
   double h2d_bw = 50e9, d2h_bw = 50e9;  // pinned PCIe bytes/s per direction
   double fwd_s = 0, bwd_s = 0;          // compute per layer
+  bool fn_master = false;               // Fn loads the fp32 master (4P), write-back drops the bf16 (12P)
 };
 double predict_step_time_overlap(const std::vector<std::int64_t>& layer_params,
                                  const std::vector<std::int64_t>& vector_params, const std::vector<int>& slow,

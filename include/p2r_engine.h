@@ -208,9 +208,15 @@ double p2r_predict_step_time(const int64_t* layer_bytes, const int* slow, int n,
 /* B200 overlap model of this engine: per SLOW layer of P params
  * H2D 2P + 4*vector_params (fwd) and 12P (bwd), D2H 14P; copies on their own
  * streams overlap compute: max(C_fwd, H2D_f/h2d) + max(C_bwd, H2D_b/h2d, D2H/d2h),
- * C_* = per-layer compute x n. vector_params may be NULL. */
+ * C_* = per-layer compute x n; at least (H2D_f + H2D_b)/h2d + the first SLOW layer's
+ * forward load + its write-back. vector_params may be NULL. */
 double p2r_predict_step_time_overlap(const int64_t* layer_params, const int64_t* vector_params, const int* slow,
                                      int n, double h2d_bw, double d2h_bw, double fwd_s, double bwd_s);
+/* the same for either forward-load form: fn_master != 0 = the engine's default (Fn loads
+ * the fp32 master, 4P; D2H 12P), 0 = P2R_OFFLOAD_FN_SHADOW=1 (the formula above). */
+double p2r_predict_step_time_overlap_form(const int64_t* layer_params, const int64_t* vector_params,
+                                          const int* slow, int n, double h2d_bw, double d2h_bw, double fwd_s,
+                                          double bwd_s, int fn_master);
 /* fewest SLOW layers (18 B/param granules) under budget_bytes, spread evenly */
 p2r_status p2r_plan_offload_overlap(const int64_t* layer_params, int n, int64_t budget_bytes, double h2d_bw,
                                     double d2h_bw, double fwd_s, double bwd_s, int* slow_out);

@@ -7,15 +7,17 @@
 // by a D2H stream, event-synchronised with the compute stream. The step's SLOW
 // uses (forward ascending, then backward descending) are staged as far ahead as
 // the ring allows, so backward granules load during the H2D-light forward:
-//   Fn : H2D bf16 shadow + the fp32 vectors / MoE gate the forward reads
-//   Bn : H2D fp32 master (+ m, v); the bf16 shadow is re-derived on the device
+//   Fn : H2D fp32 master, bf16 operand derived on the device (default), or
+//        (P2R_OFFLOAD_FN_SHADOW=1) the bf16 shadow + the fp32 vectors / MoE gate
+//   Bn : H2D fp32 master (+ m, v); the bf16 operand is re-derived on the device
 //   An : AdamW for the granule on the GPU right after its backward, then D2H
-//        write-back of p32 + bf16 + m + v (or of the grads when no optimizer
-//        is attached: the spec's "gradient offload").
+//        write-back of p32 + m + v (+ the bf16 shadow in the shadow form), or
+//        of the grads when no optimizer is attached (the spec's "gradient offload").
 // FAST granules stay resident; the placement comes from plan_offload.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -70,17 +72,28 @@ double predict_step_time_overlap(const std::vector<std::int64_t>& layer_params,
   const std::size_t L = layer_params.size();
   if (slow.size() != L || (!vector_params.empty() && vector_params.size() != L))
     throw std::invalid_argument("predict_step_time_overlap: layer / placement size mismatch");
-  double h2d_f = 0, h2d_b = 0, d2h = 0;
+  double h2d_f = 0, h2d_b = 0, d2h = 0, fill = -1, drain = 0;
   for (std::size_t i = 0; i < L; ++i)
     if (slow[i]) {
       const double P = static_cast<double>(layer_params[i]);
       const double vec = vector_params.empty() ? 0.0 : static_cast<double>(vector_params[i]);
-      h2d_f += 2.0 * P + 4.0 * vec;  // bf16 shadow + the fp32 vectors the forward reads
-      h2d_b += 12.0 * P;             // fp32 master + m + v (bf16 re-derived on the device)
-      d2h += 14.0 * P;               // updated p, m, v + bf16 shadow
+      // forward: bf16 shadow + the fp32 vectors it reads, or the whole fp32 master
+      const double f = c.fn_master ? 4.0 * P : 2.0 * P + 4.0 * vec;
+      const double w = c.fn_master ? 12.0 * P : 14.0 * P;  // updated p, m, v (+ bf16 shadow)
+      h2d_f += f;
+      h2d_b += 12.0 * P;  // fp32 master + m + v (bf16 re-derived on the device)
+      d2h += w;
+      if (fill < 0) {  // the lowest SLOW layer: its Fn load opens the step, its write-back closes it
+        fill = f / c.h2d_bw;
+        drain = w / c.d2h_bw;
+      }
     }
   const double cf = c.fwd_s * static_cast<double>(L), cb = c.bwd_s * static_cast<double>(L);
-  return std::max(cf, h2d_f / c.h2d_bw) + std::max({cb, h2d_b / c.h2d_bw, d2h / c.d2h_bw});
+  const double phases = std::max(cf, h2d_f / c.h2d_bw) + std::max({cb, h2d_b / c.h2d_bw, d2h / c.d2h_bw});
+  // the ring prefetches backward granules during the forward, so the H2D stream can
+  // also be the bound as a whole: every load, plus the exposed first load and last write-back
+  const double stream = fill < 0 ? 0.0 : (h2d_f + h2d_b) / c.h2d_bw + fill + drain;
+  return std::max(phases, stream);
 }
 
 std::vector<int> plan_offload_overlap(const std::vector<std::int64_t>& layer_params, std::int64_t budget,
@@ -163,6 +176,10 @@ void Model::offload_setup(const std::vector<int>& slow, int ring_slots) {
   auto st = std::make_unique<OffloadState>();
   st->ring = ring_slots;
   st->stride = layer_stride_;
+  {
+    const char* e = std::getenv("P2R_OFFLOAD_FN_SHADOW");
+    st->fwd_master = !(e != nullptr && e[0] == '1');
+  }
   st->slot_of.assign(static_cast<std::size_t>(n_owned_), -1);
   st->slot_fwd.assign(static_cast<std::size_t>(n_owned_), -1);
   st->slot_bwd.assign(static_cast<std::size_t>(n_owned_), -1);
@@ -276,7 +293,10 @@ void Model::offload_prefetch_next(int /*after*/, bool /*backward*/) {
       cuda_check(cudaStreamWaitEvent(st.h2d, st.wb_ev[static_cast<std::size_t>(o)], 0), "wait write-back");
     cudaEvent_t a = st.ev(), b = st.ev();
     cuda_check(cudaEventRecord(a, st.h2d), "event");
-    if (!bwd) {
+    if (!bwd && st.fwd_master) {
+      // Fn: fp32 master (the bf16 operand is re-derived on the device at acquire)
+      copy_async(st, sl.p32.p, slow_host_p32(o), g * 4, st.h2d, true, &st.stats.fn_load);
+    } else if (!bwd) {
       // Fn: the bf16 shadow feeds every GEMM; fp32 is only read for the vectors
       // (LN gains/biases, biases) and the fp32 MoE gate
       copy_async(st, sl.p16.p, slow_host_p16(o), g * 2, st.h2d, true, &st.stats.fn_load);
@@ -316,10 +336,9 @@ void Model::offload_acquire(int o, bool backward) {
   st.slot_of[static_cast<std::size_t>(o)] = si;
   OffloadSlot& sl = st.slots[static_cast<std::size_t>(si)];
   cuda_check(cudaStreamWaitEvent(stream_, sl.loaded, 0), "wait loaded");
-  if (backward) {
-    p2r_check(p2r_cast_bf16(sl.p32.as<float>(), sl.p16.p, layer_stride_, stream_), "offload bf16 shadow");
-    cuda_check(cudaMemsetAsync(sl.g32.p, 0, sl.g32.bytes, stream_), "zero slot grads");
-  }
+  if (backward || st.fwd_master)
+    p2r_check(p2r_cast_bf16(sl.p32.as<float>(), sl.p16.p, layer_stride_, stream_), "offload bf16 operand");
+  if (backward) cuda_check(cudaMemsetAsync(sl.g32.p, 0, sl.g32.bytes, stream_), "zero slot grads");
 }
 
 void Model::offload_release(int o, bool backward) {
@@ -352,7 +371,7 @@ void Model::offload_release(int o, bool backward) {
   cuda_check(cudaEventRecord(a, st.d2h), "event");
   if (has_opt_) {
     copy_async(st, slow_host_p32(o), sl.p32.p, g * 4, st.d2h, false, &st.stats.writeback);
-    copy_async(st, slow_host_p16(o), sl.p16.p, g * 2, st.d2h, false, &st.stats.writeback);
+    if (!st.fwd_master) copy_async(st, slow_host_p16(o), sl.p16.p, g * 2, st.d2h, false, &st.stats.writeback);
     copy_async(st, slow_host_m(o, 0), sl.m.p, g * 4, st.d2h, false, &st.stats.writeback);
     copy_async(st, slow_host_m(o, 1), sl.v.p, g * 4, st.d2h, false, &st.stats.writeback);
   } else {

@@ -40,6 +40,11 @@ struct OffloadState {
   int next_slot = 0;
   bool training = false;
   bool skip = false;
+  // Fn loads the fp32 master and re-derives the bf16 operand on the device, so the
+  // write-back drops the bf16 shadow: +2 B/param H2D in the forward (whose H2D
+  // stream is otherwise idle), -2 B/param D2H in the backward (the busier
+  // direction). P2R_OFFLOAD_FN_SHADOW=1 keeps the bf16-shadow form.
+  bool fwd_master = true;
   OffloadStats stats;
   struct CopyRec {
     cudaEvent_t a, b;

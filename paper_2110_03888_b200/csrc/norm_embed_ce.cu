@@ -4,6 +4,8 @@
 //   embedding_lookup+add tensor.cpp:338-368, model.cpp:229-241
 //   softmax_cross_entropy tensor.cpp:670-723 (fp64 loss sum, / denom, masked rows)
 // All reductions are deterministic (fixed-order trees, no float atomics).
+#include <cstdlib>
+
 #include <cub/device/device_radix_sort.cuh>
 
 #include "../../include/p2r_cuda.h"
@@ -460,7 +462,7 @@ constexpr int kLnSmemAttr = 200 * 1024;  // opt-in dynamic limit (leaves room fo
 // stages per warp ring (<= 3) and blocks: as many resident blocks as the
 // staging allows, at most 4 per SM (fwd) / 2 per SM (bwd).
 struct LnLaunch {
-  int nst, smem, blocks;
+  int nst, smem, blocks, warps;
 };
 LnLaunch ln_fwd_launch(int rows, int d) {
   LnLaunch l{};
@@ -473,15 +475,23 @@ LnLaunch ln_fwd_launch(int rows, int d) {
   l.blocks = need < per_sm * kNumSMs ? need : per_sm * kNumSMs;
   return l;
 }
+int ln_env(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e != nullptr && e[0] != 0 ? std::atoi(e) : dflt;
+}
 LnLaunch ln_bwd_launch(int rows, int d, int ntens) {
+  // tuning knobs (measurement only): rows in flight per warp, warps per block, smem cap, blocks per SM
+  static const int k_nst = ln_env("P2R_LN_BWD_NST", 2), k_warps = ln_env("P2R_LN_BWD_WARPS", kLnBwdWarps),
+                   k_cap = ln_env("P2R_LN_BWD_SMEM_KB", 110), k_persm = ln_env("P2R_LN_BWD_PERSM", 2);
   LnLaunch l{};
-  l.nst = 2;
-  while (l.nst > 1 && d * 4 + kLnBwdWarps * l.nst * ntens * d * 4 > 110 * 1024) --l.nst;
-  const int ring = kLnBwdWarps * l.nst * ntens * d * 4, red = kLnBwdWarps * 3 * d * 4;
+  l.warps = k_warps < 1 ? 1 : (k_warps > 4 ? 4 : k_warps);
+  l.nst = k_nst < 1 ? 1 : (k_nst > kLnMaxStages ? kLnMaxStages : k_nst);
+  while (l.nst > 1 && d * 4 + l.warps * l.nst * ntens * d * 4 > k_cap * 1024) --l.nst;
+  const int ring = l.warps * l.nst * ntens * d * 4, red = l.warps * 3 * d * 4;
   l.smem = d * 4 + (ring > red ? ring : red);
   int per_sm = kSmemPerSM / (l.smem + 1024);
-  per_sm = per_sm < 1 ? 1 : (per_sm > 2 ? 2 : per_sm);
-  const int need = (rows + kLnBwdWarps - 1) / kLnBwdWarps;
+  per_sm = per_sm < 1 ? 1 : (per_sm > k_persm ? k_persm : per_sm);
+  const int need = (rows + l.warps - 1) / l.warps;
   l.blocks = need < per_sm * kNumSMs ? need : per_sm * kNumSMs;
   return l;
 }
@@ -567,7 +577,7 @@ extern "C" p2r_status p2r_layernorm_bwd_fused(const float* dy, const float* x, c
     static cudaError_t a = cudaFuncSetAttribute(ln_bwd_kernel<NV, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                                 kLnSmemAttr);                                                \
     if (a != cudaSuccess) return set_cuda_error(a, "layernorm bwd attr");                                  \
-    const cudaError_t le = launch_k(ln_bwd_kernel<NV, CS>, dim3(l.blocks), dim3(32 * kLnBwdWarps), l.smem, s, 1, dy, x, mean, \
+    const cudaError_t le = launch_k(ln_bwd_kernel<NV, CS>, dim3(l.blocks), dim3(32 * l.warps), l.smem, s, 1, dy, x, mean, \
                  rstd, gain, resid, rows, dx, d16, partial_ws, l.nst, dx_colsum_ws);                         \
     if (le != cudaSuccess) return set_cuda_error(le, "layernorm bwd");                                       \
   }

@@ -103,6 +103,8 @@ def _declare_extra():
     L.p2r_predict_step_time.restype = ctypes.c_double
     L.p2r_predict_step_time_overlap.argtypes = [vp, vp, vp, ip] + [ctypes.c_double] * 4
     L.p2r_predict_step_time_overlap.restype = ctypes.c_double
+    L.p2r_predict_step_time_overlap_form.argtypes = [vp, vp, vp, ip] + [ctypes.c_double] * 4 + [ip]
+    L.p2r_predict_step_time_overlap_form.restype = ctypes.c_double
     L.p2r_plan_offload_overlap.argtypes = [vp, ip, i64] + [ctypes.c_double] * 4 + [vp]
     L.p2r_plan_offload_overlap.restype = ctypes.c_int
     return L
@@ -473,13 +475,16 @@ def redistribute_checkpoints(in_paths, out_paths):
     check(lib().p2r_redistribute_checkpoints(ins, len(in_paths), outs, len(out_paths)))
 
 
-def predict_step_time_overlap(layer_params, slow, h2d_bw, d2h_bw, fwd_s, bwd_s, vector_params=None) -> float:
-    """B200 overlap model of the offload engine; see p2r_engine.h."""
+def predict_step_time_overlap(layer_params, slow, h2d_bw, d2h_bw, fwd_s, bwd_s, vector_params=None,
+                              fn_master=False) -> float:
+    """B200 overlap model of the offload engine; see p2r_engine.h.
+    fn_master: the engine's default forward load (fp32 master); False = the bf16-shadow form."""
     L = _declare_extra()
     p = np.ascontiguousarray(layer_params, np.int64)
     sl = np.ascontiguousarray(slow, np.int32)
     v = None if vector_params is None else np.ascontiguousarray(vector_params, np.int64)
-    return float(L.p2r_predict_step_time_overlap(_p(p), _p(v), _p(sl), len(p), h2d_bw, d2h_bw, fwd_s, bwd_s))
+    return float(L.p2r_predict_step_time_overlap_form(_p(p), _p(v), _p(sl), len(p), h2d_bw, d2h_bw, fwd_s, bwd_s,
+                                                      int(bool(fn_master))))
 
 
 def plan_offload_overlap(layer_params, budget_bytes, h2d_bw, d2h_bw, fwd_s, bwd_s):

@@ -41,7 +41,8 @@ def overlap_prediction(p2r, rec, L):
     vec = max(0, (rec["bytes_per_step"]["Fn_load"] / max(1, n_slow) - 2 * P) / 4)
     t = rec["step_s"]["resident"] / L
     return p2r.predict_step_time_overlap([P] * L, rec["placement"], rec["h2d_GBps"] * 1e9, rec["d2h_GBps"] * 1e9,
-                                         t / 3, 2 * t / 3, vector_params=[int(vec)] * L)
+                                         t / 3, 2 * t / 3, vector_params=[int(vec)] * L,
+                                         fn_master=rec.get("fn_form", "shadow") == "master")
 
 
 def run(model, p2r, args, steps, offloaded):
@@ -123,6 +124,7 @@ def main():
     out = {
         "workload": f"Real dense stack L={L} d={args.d} d_ff={args.dff} heads={args.heads}, {args.batch}x{args.seq} tokens/step, fwd+bwd+AdamW",
         "placement": plan, "slow_layers": int(sum(plan)), "ring_slots": args.ring,
+        "fn_form": "shadow" if os.environ.get("P2R_OFFLOAD_FN_SHADOW") == "1" else "master",
         "granule_bytes_18B_per_param": gran,
         "step_s": {"resident": round(t_res, 4), "offload": round(t_off, 4), "offload_no_copy": round(t_nocopy, 4)},
         "bytes_per_step": {k: per[k] for k in ("Fn_load", "Bn_load", "opt_load", "writeback", "grad_offload")},

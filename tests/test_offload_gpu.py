@@ -26,7 +26,11 @@ def lm_batch(batch, seq, seed=7):
 @pytest.mark.parametrize("cfgd,plan,ring", [(REAL_MOE, [1, 0, 1, 1], 2), (REAL_DENSE, [1, 1, 0, 1, 0], 3),
                                             (REAL_DENSE, [1, 1, 1, 1, 1], 2)],
                          ids=["moe_mixed_ring2", "dense_mixed_ring3", "dense_all_slow"])
-def test_offload_bit_identical_training(cuda, cfgd, plan, ring):
+@pytest.mark.parametrize("fn_form", ["master", "shadow"])
+def test_offload_bit_identical_training(cuda, cfgd, plan, ring, fn_form, monkeypatch):
+    """fn_form: the forward loads the fp32 master (default) or the bf16 shadow
+    (P2R_OFFLOAD_FN_SHADOW=1, read when the offloaded model is created)."""
+    monkeypatch.setenv("P2R_OFFLOAD_FN_SHADOW", "1" if fn_form == "shadow" else "0")
     import paper_2110_03888_b200 as p2r
     cfg = p2r.Config(**cfgd)
     a = p2r.Model(cfg, 1234)
@@ -54,7 +58,8 @@ def test_offload_bit_identical_training(cuda, cfgd, plan, ring):
         assert np.array_equal(pa[n], pb[n]), n
         assert np.array_equal(ma[n][0], mb[n][0]) and np.array_equal(ma[n][1], mb[n][1]), n
     # phase accounting per SLOW granule per step: Fn = bf16 shadow (2 B/elem) + the
-    # fp32 vectors / gate the forward reads; Bn = fp32 master (4); moments 8; write-back 14
+    # fp32 vectors / gate the forward reads, or the fp32 master (4); Bn = fp32 master (4);
+    # moments 8; write-back p, m, v (12) + the bf16 shadow (2) in the shadow form
     st = b.offload_stats()
     tok, _, _ = lm_batch(2, 128, seed=99)
     assert np.array_equal(a.forward(tok, 2), b.forward(tok, 2))
@@ -62,10 +67,11 @@ def test_offload_bit_identical_training(cuda, cfgd, plan, ring):
     ns = sum(plan)
     d, dff, E = cfgd["d_model"], cfgd["d_ff"], cfgd.get("n_experts", 0)
     fp32_elems = 4 * d + (d * E + E * dff + E * d if E else dff + d)
-    assert st["Fn_load"] == 3 * ns * (g * 2 + fp32_elems * 4)
+    shadow = fn_form == "shadow"
+    assert st["Fn_load"] == 3 * ns * ((g * 2 + fp32_elems * 4) if shadow else g * 4)
     assert st["Bn_load"] == 3 * ns * g * 4
     assert st["opt_load"] == 3 * ns * g * 8
-    assert st["writeback"] == 3 * ns * g * 14
+    assert st["writeback"] == 3 * ns * g * (14 if shadow else 12)
     assert st["h2d_ms"] > 0 and st["d2h_ms"] > 0
 
 

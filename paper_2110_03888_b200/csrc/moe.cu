@@ -11,6 +11,10 @@
 // [e*seg, e*seg + count[e]) with seg = roundup(capacity, 128); rows up to the
 // next 128 boundary are zero so grouped GEMMs can treat them as K padding.
 #include <cmath>
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "../../include/p2r_cuda.h"
 #include "common.cuh"
@@ -65,86 +69,197 @@ __global__ void __launch_bounds__(256) gate_logits_kernel(const float* __restric
   }
 }
 
-// Routing: one CTA of 1024 threads walks the T*k (token, group) entries in
-// order, chunk by chunk, computing each entry's rank among earlier entries
-// that picked the same expert (warp match + per-warp counts + ordered scan).
-// Admission = rank < capacity reproduces the FCFS counters of model.cpp:321-328.
-__global__ void __launch_bounds__(1024) route_kernel(const float* __restrict__ logits, int T, int E,
-                                                    int k, int capacity, int seg_rows,
-                                                    int* __restrict__ selected,
-                                                    uint8_t* __restrict__ survived,
-                                                    int* __restrict__ pos_out,
-                                                    int* __restrict__ raw_load,
-                                                    int* __restrict__ counts,
-                                                    int* __restrict__ rows_pad,
-                                                    int* __restrict__ slots_pad,
-                                                    int* __restrict__ dropped_out) {
-  extern __shared__ int sm[];
-  int* base = sm;                 // [E]  running count per expert
-  int* wcnt = sm + E;             // [32][E] per-warp counts in this chunk
-  const int gs = E / k;
+// Register-tiled form for E in {16, 32, 64} and d % 32 == 0: 32 tokens x E
+// experts per block, 2E threads, each a 4 x 4 (token x expert) micro-tile fed by
+// two 16-byte shared loads per 16 FFMAs; the next k-chunk is prefetched into
+// registers while the current one is consumed. Every output is still one FFMA
+// chain over c = 0, 1, ..., d-1, so the logits are bit-identical to the plain
+// kernel above (and routing decisions with them).
+template <int E>
+__global__ void __launch_bounds__(2 * E) gate_logits_rt_kernel(const float* __restrict__ b,
+                                                              const float* __restrict__ gate, int T, int d,
+                                                              float* __restrict__ logits) {
+  constexpr int TT = 32, KC = 32, NT = 2 * E, LDT = TT + 4;
+  constexpr int BV = TT * KC / 4 / NT;  // float4 of b per thread per chunk
+  constexpr int GV = KC * E / 4 / NT;   // float4 of gate per thread per chunk
+  __shared__ __align__(16) float sbT[KC][LDT];
+  __shared__ __align__(16) float sg[KC][E];
+  pdl_trigger();
+  pdl_wait();
+  const int t0 = blockIdx.x * TT;
+  const int te = threadIdx.x % (E / 4), tq = threadIdx.x / (E / 4);
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+  float4 rb[BV], rg[GV];
+  auto fetch = [&](int k0) {
+#pragma unroll
+    for (int v = 0; v < BV; ++v) {
+      const int idx = threadIdx.x + NT * v, r = idx / (KC / 4), c4 = idx % (KC / 4);
+      rb[v] = t0 + r < T ? __ldg(reinterpret_cast<const float4*>(b + static_cast<long long>(t0 + r) * d + k0) + c4)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int v = 0; v < GV; ++v) {
+      const int idx = threadIdx.x + NT * v;
+      rg[v] = __ldg(reinterpret_cast<const float4*>(gate + static_cast<long long>(k0) * E) + idx);
+    }
+  };
+  fetch(0);
+  for (int k0 = 0; k0 < d; k0 += KC) {
+#pragma unroll
+    for (int v = 0; v < BV; ++v) {
+      const int idx = threadIdx.x + NT * v, r = idx / (KC / 4), c = 4 * (idx % (KC / 4));
+      sbT[c][r] = rb[v].x;
+      sbT[c + 1][r] = rb[v].y;
+      sbT[c + 2][r] = rb[v].z;
+      sbT[c + 3][r] = rb[v].w;
+    }
+#pragma unroll
+    for (int v = 0; v < GV; ++v) reinterpret_cast<float4*>(&sg[0][0])[threadIdx.x + NT * v] = rg[v];
+    __syncthreads();
+    if (k0 + KC < d) fetch(k0 + KC);
+#pragma unroll 8
+    for (int c = 0; c < KC; ++c) {
+      const float4 a = *reinterpret_cast<const float4*>(&sbT[c][4 * tq]);
+      const float4 g = *reinterpret_cast<const float4*>(&sg[c][4 * te]);
+      const float av[4] = {a.x, a.y, a.z, a.w}, gv[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], gv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int t = t0 + 4 * tq + i;
+    if (t < T)
+      *reinterpret_cast<float4*>(logits + static_cast<long long>(t) * E + 4 * te) =
+          make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+  }
+}
+
+// Routing (model.cpp:294-332), two kernels over chunks of 256 (token, group)
+// entries in entry order i = t*k + g:
+//  1. route_chunk_kernel: each thread scans its entry's expert group with the
+//     reference's strict '>' seeded at the group's first expert (ties keep the
+//     lowest index; a NaN never displaces the best; a leading NaN is kept), then
+//     ranks the entry among the chunk's earlier entries on the same expert (warp
+//     match + per-warp counts + an ordered scan over the 8 warps) and writes the
+//     chunk's per-expert histogram.
+//  2. route_finish_kernel: the chunk's base per expert = the histograms of all
+//     earlier chunks (integer sums, order-free); rank = base + in-chunk rank is the
+//     FCFS admission counter of model.cpp:321-328, admitted iff rank < capacity.
+//     The last chunk's block also writes raw_load, counts and dropped.
+constexpr int kRouteChunk = 256;
+
+__global__ void __launch_bounds__(kRouteChunk) route_chunk_kernel(const float* __restrict__ logits, int T, int E,
+                                                                  int k, int* __restrict__ selected,
+                                                                  int* __restrict__ rank_tmp,
+                                                                  int* __restrict__ hist) {
+  extern __shared__ int wcnt[];  // [8][E]
+  pdl_trigger();
+  pdl_wait();
+  constexpr int NW = kRouteChunk / 32;
+  const int N = T * k, gs = E / k;
+  const int i = blockIdx.x * kRouteChunk + threadIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int e = threadIdx.x; e < E; e += blockDim.x) base[e] = 0;
-  const int N = T * k;
-  for (int c0 = 0; c0 < N; c0 += 1024) {
-    for (int i = threadIdx.x; i < 32 * E; i += blockDim.x) wcnt[i] = 0;
-    __syncthreads();
-    const int i = c0 + threadIdx.x;
-    int best = -1;
-    if (i < N) {
-      const int t = i / k, g = i % k;
-      const float* row = logits + static_cast<long long>(t) * E;
-      best = g * gs;
-      float bv = row[best];
-      for (int e = g * gs + 1; e < (g + 1) * gs; ++e) {
-        const float v = row[e];
-        if (v > bv) {  // strict '>': ties keep the lowest index; NaN never wins
-          bv = v;
-          best = e;
-        }
+  for (int x = threadIdx.x; x < NW * E; x += kRouteChunk) wcnt[x] = 0;
+  int best = -1;
+  if (i < N) {
+    const int t = i / k, g = i % k;
+    const float* row = logits + static_cast<long long>(t) * E + static_cast<long long>(g) * gs;
+    int b = 0;
+    float bv = __ldg(row);
+#pragma unroll 8
+    for (int e = 1; e < gs; ++e) {
+      const float v = __ldg(row + e);
+      if (v > bv) {  // strict '>': ties keep the lowest index; NaN never wins
+        bv = v;
+        b = e;
       }
     }
-    const unsigned active = __ballot_sync(0xffffffffu, i < N);
-    unsigned peers = 0;
-    int rank_w = 0;
-    if (i < N) {
-      peers = __match_any_sync(active, best);
-      rank_w = __popc(peers & ((1u << lane) - 1u));
-      if (rank_w == 0) wcnt[warp * E + best] = __popc(peers);
-    }
-    __syncthreads();
-    // exclusive scan over warps per expert (ordered), then advance base
-    for (int e = threadIdx.x; e < E; e += blockDim.x) {
-      int run = base[e];
-      for (int w = 0; w < 32; ++w) {
-        const int c = wcnt[w * E + e];
-        wcnt[w * E + e] = run;
-        run += c;
-      }
-      base[e] = run;
-    }
-    __syncthreads();
-    if (i < N) {
-      const int rank = wcnt[warp * E + best] + rank_w;
-      selected[i] = best;
-      const bool ok = rank < capacity;
-      survived[i] = ok ? 1 : 0;
-      pos_out[i] = ok ? rank : -1;
-      if (ok) {
-        rows_pad[static_cast<long long>(best) * seg_rows + rank] = i / k;
-        slots_pad[static_cast<long long>(best) * seg_rows + rank] = i % k;
-      }
-    }
-    __syncthreads();
+    best = g * gs + b;
   }
-  if (threadIdx.x == 0) {
+  __syncthreads();  // wcnt zeroed
+  const unsigned active = __ballot_sync(0xffffffffu, i < N);
+  int rank_w = 0;
+  if (i < N) {
+    const unsigned peers = __match_any_sync(active, best);
+    rank_w = __popc(peers & ((1u << lane) - 1u));
+    if (rank_w == 0) wcnt[warp * E + best] = __popc(peers);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += kRouteChunk) {  // exclusive scan over warps, in warp order
+    int run = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const int c = wcnt[w * E + e];
+      wcnt[w * E + e] = run;
+      run += c;
+    }
+    hist[static_cast<long long>(blockIdx.x) * E + e] = run;
+  }
+  __syncthreads();
+  if (i < N) {
+    selected[i] = best;
+    rank_tmp[i] = wcnt[warp * E + best] + rank_w;
+  }
+}
+
+__global__ void __launch_bounds__(kRouteChunk) route_finish_kernel(
+    const int* __restrict__ hist, int nchunks, int T, int E, int k, int capacity, int seg_rows,
+    const int* __restrict__ selected, int* __restrict__ pos_out, uint8_t* __restrict__ survived,
+    int* __restrict__ raw_load, int* __restrict__ counts, int* __restrict__ rows_pad, int* __restrict__ slots_pad,
+    int* __restrict__ dropped_out) {
+  extern __shared__ int rs[];  // base [E], then partial sums [P][E]
+  __shared__ int drop_sh;
+  pdl_trigger();
+  pdl_wait();
+  const int c = blockIdx.x;
+  const int P = E >= kRouteChunk ? 1 : kRouteChunk / E;  // partitions of the earlier-chunk range
+  int* base = rs;
+  int* part = rs + E;
+  for (int x = threadIdx.x; x < P * E; x += kRouteChunk) {
+    const int e = x % E, p = x / E;
+    int sum = 0;
+    for (int j = p; j < c; j += P) sum += hist[static_cast<long long>(j) * E + e];
+    part[x] = sum;
+  }
+  if (threadIdx.x == 0) drop_sh = 0;
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += kRouteChunk) {
+    int sum = 0;
+    for (int p = 0; p < P; ++p) sum += part[p * E + e];
+    base[e] = sum;
+  }
+  __syncthreads();
+  const int i = c * kRouteChunk + threadIdx.x;
+  if (i < T * k) {
+    const int best = selected[i];
+    const int rank = base[best] + pos_out[i];
+    const bool ok = rank < capacity;
+    survived[i] = ok ? 1 : 0;
+    pos_out[i] = ok ? rank : -1;
+    if (ok) {
+      rows_pad[static_cast<long long>(best) * seg_rows + rank] = i / k;
+      slots_pad[static_cast<long long>(best) * seg_rows + rank] = i % k;
+    }
+  }
+  if (c == nchunks - 1) {
     int dr = 0;
-    for (int e = 0; e < E; ++e) dr += base[e] > capacity ? base[e] - capacity : 0;
-    *dropped_out = dr;
-  }
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    raw_load[e] = base[e];
-    counts[e] = base[e] < capacity ? base[e] : capacity;
+    for (int e = threadIdx.x; e < E; e += kRouteChunk) {
+      const int tot = base[e] + hist[static_cast<long long>(c) * E + e];
+      raw_load[e] = tot;
+      counts[e] = tot < capacity ? tot : capacity;
+      dr += tot > capacity ? tot - capacity : 0;
+    }
+    atomicAdd(&drop_sh, dr);  // integer: exact in any order
+    __syncthreads();
+    if (threadIdx.x == 0) *dropped_out = drop_sh;
   }
 }
 
@@ -296,6 +411,31 @@ __global__ void gate_bwd_kernel(const float* __restrict__ b, const float* __rest
   dgate[o] += s;
 }
 
+// Per-(device, stream) scratch for the routing histograms, grown on demand (the
+// C-ABI of p2r_moe_route has no workspace argument; growth synchronises).
+cudaError_t route_scratch(cudaStream_t s, size_t bytes, int** out) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, std::pair<void*, size_t>> pool;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  auto& slot = pool[{dev, s}];
+  if (slot.second < bytes) {
+    if (slot.first) {
+      e = cudaStreamSynchronize(s);
+      if (e == cudaSuccess) e = cudaFree(slot.first);
+      if (e != cudaSuccess) return e;
+      slot = {nullptr, 0};
+    }
+    e = cudaMalloc(&slot.first, bytes);
+    if (e != cudaSuccess) return e;
+    slot.second = bytes;
+  }
+  *out = static_cast<int*>(slot.first);
+  return cudaSuccess;
+}
+
 }  // namespace p2r
 
 using namespace p2r;
@@ -312,6 +452,19 @@ extern "C" p2r_status p2r_moe_gate_logits(const float* b, const float* gate, int
   if (T <= 0) return P2R_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int blocks = (T + 31) / 32;
+  static const bool plain = [] {  // P2R_GATE_PLAIN=1: the plain kernel (tests compare the two bit for bit)
+    const char* e = std::getenv("P2R_GATE_PLAIN");
+    return e != nullptr && e[0] == '1';
+  }();
+  if (!plain && d % 32 == 0 && (E == 16 || E == 32 || E == 64)) {
+    cudaError_t le = cudaSuccess;
+    if (E == 16) le = launch_k(gate_logits_rt_kernel<16>, dim3(blocks), dim3(32), 0, s, 1, b, gate, T, d, logits);
+    if (E == 32) le = launch_k(gate_logits_rt_kernel<32>, dim3(blocks), dim3(64), 0, s, 1, b, gate, T, d, logits);
+    if (E == 64) le = launch_k(gate_logits_rt_kernel<64>, dim3(blocks), dim3(128), 0, s, 1, b, gate, T, d, logits);
+    if (le != cudaSuccess) return set_cuda_error(le, "moe gate logits");
+    P2R_CHECK_LAUNCH("moe gate logits");
+    return P2R_OK;
+  }
   switch (E) {
     case 2: gate_logits_kernel<2><<<blocks, 256, 0, s>>>(b, gate, T, d, logits); break;
     case 4: gate_logits_kernel<4><<<blocks, 256, 0, s>>>(b, gate, T, d, logits); break;
@@ -335,13 +488,37 @@ extern "C" p2r_status p2r_moe_route(const float* logits, int T, int E, int k, in
     return set_error(P2R_EINVAL, "moe route: seg_rows must be >= capacity");
   if (E > 1024) return set_error(P2R_EINVAL, "moe route: at most 1024 experts per rank");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int smem = (E + 32 * E) * static_cast<int>(sizeof(int));
-  if (smem > 48 * 1024) {
-    static cudaError_t e = cudaFuncSetAttribute(route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e != cudaSuccess) return set_cuda_error(e, "route attr");
+  const int N = T * k;
+  if (N <= 0) {  // nothing routed: zero loads / counts / drops
+    if (E > 0) {
+      cudaError_t e = cudaMemsetAsync(raw_load, 0, static_cast<size_t>(E) * sizeof(int), s);
+      if (e == cudaSuccess) e = cudaMemsetAsync(counts, 0, static_cast<size_t>(E) * sizeof(int), s);
+      if (e == cudaSuccess) e = cudaMemsetAsync(dropped, 0, sizeof(int), s);
+      if (e != cudaSuccess) return set_cuda_error(e, "moe route");
+    }
+    return P2R_OK;
   }
-  route_kernel<<<1, 1024, smem, s>>>(logits, T, E, k, capacity, seg_rows, selected, survived, pos,
-                                     raw_load, counts, rows_pad, slots_pad, dropped);
+  const int nchunks = (N + kRouteChunk - 1) / kRouteChunk;
+  int* hist = nullptr;
+  {
+    const cudaError_t e = route_scratch(s, static_cast<size_t>(nchunks) * E * sizeof(int), &hist);
+    if (e != cudaSuccess) return set_cuda_error(e, "moe route scratch");
+  }
+  const int smem1 = (kRouteChunk / 32) * E * static_cast<int>(sizeof(int));
+  const int P = E >= kRouteChunk ? 1 : kRouteChunk / E;
+  const int smem2 = (E + P * E) * static_cast<int>(sizeof(int));
+  static const cudaError_t a1 =
+      cudaFuncSetAttribute(route_chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  static const cudaError_t a2 =
+      cudaFuncSetAttribute(route_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  if (a1 != cudaSuccess || a2 != cudaSuccess) return set_cuda_error(a1 != cudaSuccess ? a1 : a2, "route attr");
+  cudaError_t le = launch_k(route_chunk_kernel, dim3(nchunks), dim3(kRouteChunk), smem1, s, 1, logits, T, E, k,
+                            selected, pos, hist);
+  if (le == cudaSuccess)
+    le = launch_k(route_finish_kernel, dim3(nchunks), dim3(kRouteChunk), smem2, s, 1,
+                  static_cast<const int*>(hist), nchunks, T, E, k, capacity, seg_rows,
+                  static_cast<const int*>(selected), pos, survived, raw_load, counts, rows_pad, slots_pad, dropped);
+  if (le != cudaSuccess) return set_cuda_error(le, "moe route");
   P2R_CHECK_LAUNCH("moe route");
   return P2R_OK;
 }

@@ -336,3 +336,37 @@ def test_empty_and_degenerate_inputs(cuda):
     x = torch.zeros(1, 128, device=cuda)
     assert L.p2r_layernorm_fwd(P(x), P(x), P(x), 0, 128, ctypes.c_float(1e-5), None, P(x), P(x), P(x), st) == 0
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("T,d,E", [(8192, 2048, 64), (1000, 256, 32), (77, 128, 16), (300, 96, 64)])
+def test_gate_logits_tiled_bit_identical(cuda, T, d, E):
+    """The register-tiled gate kernel keeps every logit's FFMA chain in c order, so its
+    logits equal the plain kernel's bit for bit (P2R_GATE_PLAIN=1 in a subprocess) and
+    the fp32 matmul(b, gate) of model.cpp:250 to fp32 rounding."""
+    import subprocess
+    import sys
+    import torch
+    g = torch.Generator(device=cuda).manual_seed(3)
+    b = torch.randn(T, d, device=cuda, generator=g)
+    gate = torch.randn(d, E, device=cuda, generator=g) * 0.02
+    out = torch.empty(T, E, device=cuda)
+    call("moe_gate_logits", b, gate, T, d, E, out)
+    ref = (b.double() @ gate.double()).float()
+    assert float((out - ref).abs().max()) < 1e-4
+    code = ("import sys, torch, numpy as np; sys.path.insert(0, '.');"
+            "from tests._gpu import call;"
+            f"g = torch.Generator(device='cuda').manual_seed(3);"
+            f"b = torch.randn({T}, {d}, device='cuda', generator=g);"
+            f"gate = torch.randn({d}, {E}, device='cuda', generator=g) * 0.02;"
+            f"o = torch.empty({T}, {E}, device='cuda');"
+            f"call('moe_gate_logits', b, gate, {T}, {d}, {E}, o);"
+            "np.save(sys.argv[1], o.cpu().numpy())")
+    import os
+    import tempfile
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "plain.npy")
+        env = dict(os.environ, P2R_GATE_PLAIN="1")
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        subprocess.run([sys.executable, "-c", code, path], check=True, env=env, cwd=root)
+        plain = np.load(path)
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), plain.view(np.uint32))

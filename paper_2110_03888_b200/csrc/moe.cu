@@ -338,6 +338,94 @@ __global__ void combine_kernel(const float* __restrict__ ye, int d, int seg_rows
   }
 }
 
+// 4-wide forms of dispatch / combine / dispatch backward (d % 4 == 0): 16-byte
+// fp32 accesses (8-byte bf16), element arithmetic identical to the scalar kernels.
+P2R_DEVICE float4 ld_src4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+P2R_DEVICE float4 ld_src4(const __nv_bfloat16* p) {
+  const uint2 u = *reinterpret_cast<const uint2*>(p);
+  const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(&u.x), b = *reinterpret_cast<const __nv_bfloat162*>(&u.y);
+  return make_float4(__low2float(a), __high2float(a), __low2float(b), __high2float(b));
+}
+P2R_DEVICE void st_bf4(__nv_bfloat16* p, float x, float y, float z, float w) {
+  __nv_bfloat162 a = __floats2bfloat162_rn(x, y), b = __floats2bfloat162_rn(z, w);
+  uint2 u;
+  u.x = *reinterpret_cast<uint32_t*>(&a);
+  u.y = *reinterpret_cast<uint32_t*>(&b);
+  *reinterpret_cast<uint2*>(p) = u;
+}
+
+template <typename Tin>
+__global__ void dispatch4_kernel(const Tin* __restrict__ src, int d, const int* __restrict__ rows_pad,
+                                 const int* __restrict__ counts, int seg_rows, const float* __restrict__ w,
+                                 const int* __restrict__ slots_pad, int k, __nv_bfloat16* __restrict__ xe,
+                                 int pad_full) {
+  const int e = blockIdx.y, r = blockIdx.x;
+  const int cnt = counts[e];
+  const int top = pad_full ? seg_rows : min(seg_rows, (cnt + 127) / 128 * 128);
+  if (r >= top) return;
+  __nv_bfloat16* dst = xe + (static_cast<long long>(e) * seg_rows + r) * d;
+  if (r >= cnt) {
+    for (int c = 4 * threadIdx.x; c < d; c += 4 * blockDim.x) st_bf4(dst + c, 0.f, 0.f, 0.f, 0.f);
+    return;
+  }
+  const int t = rows_pad[static_cast<long long>(e) * seg_rows + r];
+  float scale = 1.f;
+  if (w) scale = w[t * k + slots_pad[static_cast<long long>(e) * seg_rows + r]];
+  const Tin* sp = src + static_cast<long long>(t) * d;
+  for (int c = 4 * threadIdx.x; c < d; c += 4 * blockDim.x) {
+    const float4 v = ld_src4(sp + c);
+    if (w)
+      st_bf4(dst + c, scale * v.x, scale * v.y, scale * v.z, scale * v.w);
+    else
+      st_bf4(dst + c, v.x, v.y, v.z, v.w);
+  }
+}
+
+__global__ void combine4_kernel(const float* __restrict__ ye, int d, int seg_rows, const int* __restrict__ selected,
+                                const int* __restrict__ pos, const float* __restrict__ w, int k,
+                                const float* __restrict__ resid, float* __restrict__ out) {
+  const int t = blockIdx.x;
+  for (int c = 4 * threadIdx.x; c < d; c += 4 * blockDim.x) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j = 0; j < k; ++j) {
+      const int s = t * k + j;
+      const int p = pos[s];
+      if (p < 0) continue;
+      const float ws = w[s];
+      const float4 y = *reinterpret_cast<const float4*>(ye + (static_cast<long long>(selected[s]) * seg_rows + p) * d + c);
+      acc.x += ws * y.x;
+      acc.y += ws * y.y;
+      acc.z += ws * y.z;
+      acc.w += ws * y.w;
+    }
+    const long long o = static_cast<long long>(t) * d + c;
+    const float4 rr = resid ? *reinterpret_cast<const float4*>(resid + o) : make_float4(0.f, 0.f, 0.f, 0.f);
+    *reinterpret_cast<float4*>(out + o) = make_float4(rr.x + acc.x, rr.y + acc.y, rr.z + acc.z, rr.w + acc.w);
+  }
+}
+
+// k-sum of the routed rows only (no gate term: glogits == NULL)
+__global__ void dispatch_bwd4_kernel(const float* __restrict__ dxe, int d, int k, int seg_rows,
+                                     const int* __restrict__ selected, const int* __restrict__ pos,
+                                     float* __restrict__ db, int accumulate) {
+  const int t = blockIdx.x;
+  for (int c = 4 * threadIdx.x; c < d; c += 4 * blockDim.x) {
+    const long long o = static_cast<long long>(t) * d + c;
+    float4 acc = accumulate ? *reinterpret_cast<const float4*>(db + o) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j = k - 1; j >= 0; --j) {
+      const int s = t * k + j;
+      const int p = pos[s];
+      if (p < 0) continue;
+      const float4 g = *reinterpret_cast<const float4*>(dxe + (static_cast<long long>(selected[s]) * seg_rows + p) * d + c);
+      acc.x += g.x;
+      acc.y += g.y;
+      acc.z += g.z;
+      acc.w += g.w;
+    }
+    *reinterpret_cast<float4*>(db + o) = acc;
+  }
+}
+
 // dw[t,g] = <dout[t], ye[row(t,g)]>  (warp per (t,g)); 0 for dropped slots
 __global__ void combine_bwd_w_kernel(const float* __restrict__ dout, const float* __restrict__ ye,
                                      int T, int d, int k, int seg_rows,
@@ -538,7 +626,16 @@ extern "C" p2r_status p2r_moe_dispatch(const void* src, int src_dtype, int d, in
                                        const float* w, int k, void* xe_bf16, int pad_full, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   dim3 grid(seg_rows, E);
-  if (src_dtype == 0)
+  if (d % 4 == 0) {
+    const int thr = d >= 2048 ? 256 : 128;
+    if (src_dtype == 0)
+      dispatch4_kernel<float><<<grid, thr, 0, s>>>(static_cast<const float*>(src), d, rows_pad, counts, seg_rows, w,
+                                                   slots_pad, k, static_cast<__nv_bfloat16*>(xe_bf16), pad_full);
+    else
+      dispatch4_kernel<__nv_bfloat16><<<grid, thr, 0, s>>>(static_cast<const __nv_bfloat16*>(src), d, rows_pad, counts,
+                                                           seg_rows, w, slots_pad, k,
+                                                           static_cast<__nv_bfloat16*>(xe_bf16), pad_full);
+  } else if (src_dtype == 0)
     dispatch_kernel<float><<<grid, 128, 0, s>>>(static_cast<const float*>(src), d, rows_pad, counts, seg_rows, w, slots_pad, k,
                                                 static_cast<__nv_bfloat16*>(xe_bf16), pad_full);
   else
@@ -552,7 +649,11 @@ extern "C" p2r_status p2r_moe_combine(const float* ye, int T, int d, int k, int 
                                       const int* selected, const int* pos, const float* w,
                                       const float* resid, float* out, void* stream) {
   if (T <= 0) return P2R_OK;
-  combine_kernel<<<T, 256, 0, static_cast<cudaStream_t>(stream)>>>(ye, d, seg_rows, selected, pos, w, k, resid, out);
+  if (d % 4 == 0)
+    combine4_kernel<<<T, d >= 2048 ? 256 : 128, 0, static_cast<cudaStream_t>(stream)>>>(ye, d, seg_rows, selected, pos,
+                                                                                       w, k, resid, out);
+  else
+    combine_kernel<<<T, 256, 0, static_cast<cudaStream_t>(stream)>>>(ye, d, seg_rows, selected, pos, w, k, resid, out);
   P2R_CHECK_LAUNCH("moe combine");
   return P2R_OK;
 }
@@ -586,8 +687,12 @@ extern "C" p2r_status p2r_moe_dispatch_bwd(const float* dxe, int T, int d, int k
                                            const float* glogits, const float* gate, int E,
                                            float* db, int accumulate, void* stream) {
   if (T <= 0) return P2R_OK;
-  dispatch_bwd_kernel<<<T, 256, 0, static_cast<cudaStream_t>(stream)>>>(dxe, d, k, seg_rows, selected, pos, glogits, gate, E, db,
-                                                                         accumulate);
+  if (glogits == nullptr && d % 4 == 0)
+    dispatch_bwd4_kernel<<<T, d >= 2048 ? 256 : 128, 0, static_cast<cudaStream_t>(stream)>>>(dxe, d, k, seg_rows,
+                                                                                            selected, pos, db, accumulate);
+  else
+    dispatch_bwd_kernel<<<T, 256, 0, static_cast<cudaStream_t>(stream)>>>(dxe, d, k, seg_rows, selected, pos, glogits,
+                                                                           gate, E, db, accumulate);
   P2R_CHECK_LAUNCH("moe dispatch bwd");
   return P2R_OK;
 }

@@ -69,17 +69,18 @@ __global__ void __launch_bounds__(256) gate_logits_kernel(const float* __restric
   }
 }
 
-// Register-tiled form for E in {16, 32, 64} and d % 32 == 0: 32 tokens x E
-// experts per block, 2E threads, each a 4 x 4 (token x expert) micro-tile fed by
+// Register-tiled form for E in {8, 16, 32, 64} and d % 32 == 0: TT tokens x E
+// experts per block (TT = 32, or 64 for E = 8 so a block is still a whole warp),
+// TT*E/16 threads, each a 4 x 4 (token x expert) micro-tile fed by
 // two 16-byte shared loads per 16 FFMAs; the next k-chunk is prefetched into
 // registers while the current one is consumed. Every output is still one FFMA
 // chain over c = 0, 1, ..., d-1, so the logits are bit-identical to the plain
 // kernel above (and routing decisions with them).
-template <int E>
-__global__ void __launch_bounds__(2 * E) gate_logits_rt_kernel(const float* __restrict__ b,
-                                                              const float* __restrict__ gate, int T, int d,
-                                                              float* __restrict__ logits) {
-  constexpr int TT = 32, KC = 32, NT = 2 * E, LDT = TT + 4;
+template <int E, int TT>
+__global__ void __launch_bounds__(TT * E / 16) gate_logits_rt_kernel(const float* __restrict__ b,
+                                                                    const float* __restrict__ gate, int T, int d,
+                                                                    float* __restrict__ logits) {
+  constexpr int KC = 32, NT = TT * E / 16, LDT = TT + 4;
   constexpr int BV = TT * KC / 4 / NT;  // float4 of b per thread per chunk
   constexpr int GV = KC * E / 4 / NT;   // float4 of gate per thread per chunk
   __shared__ __align__(16) float sbT[KC][LDT];
@@ -88,6 +89,7 @@ __global__ void __launch_bounds__(2 * E) gate_logits_rt_kernel(const float* __re
   pdl_wait();
   const int t0 = blockIdx.x * TT;
   const int te = threadIdx.x % (E / 4), tq = threadIdx.x / (E / 4);
+  static_assert(TT * KC % (4 * NT) == 0 && KC * E % (4 * NT) == 0, "gate tile");
   float acc[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -544,11 +546,13 @@ extern "C" p2r_status p2r_moe_gate_logits(const float* b, const float* gate, int
     const char* e = std::getenv("P2R_GATE_PLAIN");
     return e != nullptr && e[0] == '1';
   }();
-  if (!plain && d % 32 == 0 && (E == 16 || E == 32 || E == 64)) {
+  if (!plain && d % 32 == 0 && (E == 8 || E == 16 || E == 32 || E == 64)) {
     cudaError_t le = cudaSuccess;
-    if (E == 16) le = launch_k(gate_logits_rt_kernel<16>, dim3(blocks), dim3(32), 0, s, 1, b, gate, T, d, logits);
-    if (E == 32) le = launch_k(gate_logits_rt_kernel<32>, dim3(blocks), dim3(64), 0, s, 1, b, gate, T, d, logits);
-    if (E == 64) le = launch_k(gate_logits_rt_kernel<64>, dim3(blocks), dim3(128), 0, s, 1, b, gate, T, d, logits);
+    if (E == 8)
+      le = launch_k(gate_logits_rt_kernel<8, 64>, dim3((T + 63) / 64), dim3(32), 0, s, 1, b, gate, T, d, logits);
+    if (E == 16) le = launch_k(gate_logits_rt_kernel<16, 32>, dim3(blocks), dim3(32), 0, s, 1, b, gate, T, d, logits);
+    if (E == 32) le = launch_k(gate_logits_rt_kernel<32, 32>, dim3(blocks), dim3(64), 0, s, 1, b, gate, T, d, logits);
+    if (E == 64) le = launch_k(gate_logits_rt_kernel<64, 32>, dim3(blocks), dim3(128), 0, s, 1, b, gate, T, d, logits);
     if (le != cudaSuccess) return set_cuda_error(le, "moe gate logits");
     P2R_CHECK_LAUNCH("moe gate logits");
     return P2R_OK;

@@ -123,6 +123,14 @@ def main():
         "4·admitted·d (dxe) + 4Td (db)")
     del ye32, dxe, xe16, b32, b16, resid, out, dout, db
     torch.cuda.empty_cache()
+    # C3 per-rank gate: d = 1024, E = 8 (one expert per GPU, every rank scores all 8)
+    T3, d3, E3 = 8192, 1024, 8
+    b3 = torch.randn(T3, d3, device=dev, generator=g)
+    gate3 = torch.randn(d3, E3, device=dev, generator=g) * 0.02
+    lg3 = torch.empty(T3, E3, device=dev)
+    record("moe_gate_logits C3 (E=8)", timed(lambda: ck(L.p2r_moe_gate_logits(P(b3), P(gate3), T3, d3, E3, P(lg3), S))),
+           4 * T3 * d3 + 4 * d3 * E3 + 4 * T3 * E3, "4Td + 4dE + 4TE")
+    del b3
 
     # ---------------- delink at C3 (one shared layer -> 24) ----------------
     Ld, dm, dff = 24, 1024, 4096

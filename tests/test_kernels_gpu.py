@@ -338,7 +338,8 @@ def test_empty_and_degenerate_inputs(cuda):
     torch.cuda.synchronize()
 
 
-@pytest.mark.parametrize("T,d,E", [(8192, 2048, 64), (1000, 256, 32), (77, 128, 16), (300, 96, 64)])
+@pytest.mark.parametrize("T,d,E", [(8192, 2048, 64), (1000, 256, 32), (77, 128, 16), (300, 96, 64), (8192, 1024, 8),
+                                   (130, 64, 8)])
 def test_gate_logits_tiled_bit_identical(cuda, T, d, E):
     """The register-tiled gate kernel keeps every logit's FFMA chain in c order, so its
     logits equal the plain kernel's bit for bit (P2R_GATE_PLAIN=1 in a subprocess) and

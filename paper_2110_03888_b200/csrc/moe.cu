@@ -70,17 +70,17 @@ __global__ void __launch_bounds__(256) gate_logits_kernel(const float* __restric
 }
 
 // Register-tiled form for E in {8, 16, 32, 64} and d % 32 == 0: TT tokens x E
-// experts per block (TT = 32, or 64 for E = 8 so a block is still a whole warp),
-// TT*E/16 threads, each a 4 x 4 (token x expert) micro-tile fed by
+// experts per block, TT*E/(4*TM) threads, each a TM x 4 (token x expert) micro-tile
+// (TM = 4 for E >= 32; TM = 1 for E = 8, 16 keeps 2-4 warps per block) fed by
 // two 16-byte shared loads per 16 FFMAs; the next k-chunk is prefetched into
 // registers while the current one is consumed. Every output is still one FFMA
 // chain over c = 0, 1, ..., d-1, so the logits are bit-identical to the plain
 // kernel above (and routing decisions with them).
-template <int E, int TT>
-__global__ void __launch_bounds__(TT * E / 16) gate_logits_rt_kernel(const float* __restrict__ b,
-                                                                    const float* __restrict__ gate, int T, int d,
-                                                                    float* __restrict__ logits) {
-  constexpr int KC = 32, NT = TT * E / 16, LDT = TT + 4;
+template <int E, int TT, int TM>
+__global__ void __launch_bounds__(TT * E / (4 * TM)) gate_logits_rt_kernel(const float* __restrict__ b,
+                                                                          const float* __restrict__ gate, int T,
+                                                                          int d, float* __restrict__ logits) {
+  constexpr int KC = 32, NT = TT * E / (4 * TM), LDT = TT + 4;
   constexpr int BV = TT * KC / 4 / NT;  // float4 of b per thread per chunk
   constexpr int GV = KC * E / 4 / NT;   // float4 of gate per thread per chunk
   __shared__ __align__(16) float sbT[KC][LDT];
@@ -90,9 +90,9 @@ __global__ void __launch_bounds__(TT * E / 16) gate_logits_rt_kernel(const float
   const int t0 = blockIdx.x * TT;
   const int te = threadIdx.x % (E / 4), tq = threadIdx.x / (E / 4);
   static_assert(TT * KC % (4 * NT) == 0 && KC * E % (4 * NT) == 0, "gate tile");
-  float acc[4][4];
+  float acc[TM][4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < TM; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
   float4 rb[BV], rg[GV];
@@ -125,19 +125,25 @@ __global__ void __launch_bounds__(TT * E / 16) gate_logits_rt_kernel(const float
     if (k0 + KC < d) fetch(k0 + KC);
 #pragma unroll 8
     for (int c = 0; c < KC; ++c) {
-      const float4 a = *reinterpret_cast<const float4*>(&sbT[c][4 * tq]);
+      float av[TM];
+      if constexpr (TM == 4) {
+        const float4 a = *reinterpret_cast<const float4*>(&sbT[c][4 * tq]);
+        av[0] = a.x, av[1] = a.y, av[2] = a.z, av[3] = a.w;
+      } else {
+        av[0] = sbT[c][tq];
+      }
       const float4 g = *reinterpret_cast<const float4*>(&sg[c][4 * te]);
-      const float av[4] = {a.x, a.y, a.z, a.w}, gv[4] = {g.x, g.y, g.z, g.w};
+      const float gv[4] = {g.x, g.y, g.z, g.w};
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < TM; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], gv[j], acc[i][j]);
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int t = t0 + 4 * tq + i;
+  for (int i = 0; i < TM; ++i) {
+    const int t = t0 + TM * tq + i;
     if (t < T)
       *reinterpret_cast<float4*>(logits + static_cast<long long>(t) * E + 4 * te) =
           make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
@@ -548,11 +554,13 @@ extern "C" p2r_status p2r_moe_gate_logits(const float* b, const float* gate, int
   }();
   if (!plain && d % 32 == 0 && (E == 8 || E == 16 || E == 32 || E == 64)) {
     cudaError_t le = cudaSuccess;
-    if (E == 8)
-      le = launch_k(gate_logits_rt_kernel<8, 64>, dim3((T + 63) / 64), dim3(32), 0, s, 1, b, gate, T, d, logits);
-    if (E == 16) le = launch_k(gate_logits_rt_kernel<16, 32>, dim3(blocks), dim3(32), 0, s, 1, b, gate, T, d, logits);
-    if (E == 32) le = launch_k(gate_logits_rt_kernel<32, 32>, dim3(blocks), dim3(64), 0, s, 1, b, gate, T, d, logits);
-    if (E == 64) le = launch_k(gate_logits_rt_kernel<64, 32>, dim3(blocks), dim3(128), 0, s, 1, b, gate, T, d, logits);
+    if (E == 8) le = launch_k(gate_logits_rt_kernel<8, 32, 1>, dim3(blocks), dim3(64), 0, s, 1, b, gate, T, d, logits);
+    if (E == 16)
+      le = launch_k(gate_logits_rt_kernel<16, 32, 1>, dim3(blocks), dim3(128), 0, s, 1, b, gate, T, d, logits);
+    if (E == 32)
+      le = launch_k(gate_logits_rt_kernel<32, 32, 4>, dim3(blocks), dim3(64), 0, s, 1, b, gate, T, d, logits);
+    if (E == 64)
+      le = launch_k(gate_logits_rt_kernel<64, 32, 4>, dim3(blocks), dim3(128), 0, s, 1, b, gate, T, d, logits);
     if (le != cudaSuccess) return set_cuda_error(le, "moe gate logits");
     P2R_CHECK_LAUNCH("moe gate logits");
     return P2R_OK;

@@ -8,6 +8,7 @@
 
 #include <cstdint>
 #include <functional>
+#include <limits>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -143,7 +144,8 @@ struct OffloadStats {
   double bn_load = 0;       // H2D of SLOW granules for the backward (Bn)
   double opt_load = 0;      // H2D of AdamW moments of SLOW granules (An)
   double writeback = 0;     // D2H of updated params + moments (An)
-  double grad_offload = 0;  // D2H of SLOW-granule grads (no fused optimizer)
+  double grad_offload = 0;  // D2H of SLOW-granule grads (no fused optimizer, or a non-final micro-step)
+  double grad_load = 0;     // H2D of parked partial grads (accumulation micro-steps after the first)
   double h2d_ms = 0, d2h_ms = 0;
   std::int64_t copies = 0;
 };
@@ -237,6 +239,10 @@ class Model {
   // Expert-parallel shard `ep_rank` of `ep_world`: holds experts
   // [ep_rank*E/W, (ep_rank+1)*E/W) (model.cpp:334-340) + the replicated rest.
   Model(ModelConfig config, std::uint64_t seed, int ep_world, int ep_rank);
+  // Both: an expert-parallel shard whose SLOW layer granules (replicated part +
+  // local experts) live in pinned host DRAM (C5: 96-layer MoE over 8 GPUs).
+  Model(ModelConfig config, std::uint64_t seed, const std::vector<int>& slow, int ring_slots, int ep_world,
+        int ep_rank);
   ~Model();
 
   // NCCL (one communicator per model over all ranks; csrc/engine/comm.cpp)
@@ -332,7 +338,19 @@ class Model {
   // granular offload
   bool offloaded() const { return off_ != nullptr; }
   const std::vector<int>& slow_layers() const { return slow_; }
+  // lr of the optimizer step whose last backward runs the fused AdamW of the SLOW
+  // granules; must be set (and equal the adamw_step lr) before that backward
   void set_offload_lr(float lr) { offload_lr_ = lr; }
+  // gradient accumulation over n micro-steps (train_step(zero=true) then n-1 x
+  // zero=false): SLOW granules park their partial gradients in pinned host memory
+  // between micro-steps and run the fused AdamW in the n-th backward only
+  void set_grad_accumulation(int n);
+  int grad_accumulation() const { return accum_n_; }
+  // activation checkpointing of offloaded models: 0 off, 1 SLOW
+  // layers (default), 2 every layer; a checkpointed layer keeps only its output and
+  // recomputes the rest in its backward
+  void set_activation_checkpointing(int policy);
+  int activation_checkpointing() const { return ckpt_policy_; }
   OffloadStats offload_stats();
   void offload_stats_reset();
   void set_offload_skip_copies(bool skip);  // timing aid: same schedule, no PCIe traffic
@@ -340,6 +358,8 @@ class Model {
   std::int64_t device_param_bytes() const;
   void routing_host(int g, int* selected, std::uint8_t* survived, int* raw_load, int* capacity,
                     int* dropped) const;
+  // fp32 gate logits [T, E] of graph layer g from the last forward (MoE)
+  void gate_logits_host(int g, float* out) const;
 
  private:
   struct NoInit {};
@@ -371,6 +391,9 @@ class Model {
   float* eg(long long off) const { return emb_g_.as<float>() + off; }
   void* ep16(long long off) const { return emb_p16_.as<std::uint16_t>() + off; }
   void block_backward(int g, AttentionMode mode);
+  void block_compute(int g, const float* x, AttentionMode mode);
+  bool checkpointed(int g) const;
+  void offload_check_micro(int next_micro) const;
   // bracket one kernel launch with profiling events (no-op when profiling is off)
   template <typename F>
   void prof(int cls, double flops, double bytes, F&& launch) {
@@ -425,7 +448,14 @@ class Model {
     const void* ws = nullptr;
   } step_graph_;
   std::uint64_t acts_gen_ = 0;  // bumped whenever ensure_acts reallocates the activation buffers
-  float offload_lr_ = 0.0f;
+  float offload_lr_ = std::numeric_limits<float>::quiet_NaN();  // set_offload_lr() before use
+  int accum_n_ = 1;            // micro-steps per optimizer step (offload)
+  int micro_ = 0;              // micro-steps since zero_grads
+  bool slow_applied_ = false;  // SLOW granules already took this step's fused AdamW
+  int ckpt_policy_ = 1;
+  void init_model(std::uint64_t seed, const std::vector<int>* slow, int ring_slots, int ep_world, int ep_rank,
+                  bool ep_ctor);
+  void allreduce_f32(float* buf, std::size_t n);  // DP sum over ranks on the model stream
   // expert / data parallelism
   int ep_world_ = 1, ep_rank_ = 0;
   bool force_ep_ = false;  // P2R_FORCE_EP=1: run the exchange path even at W = 1 (tests)

@@ -166,6 +166,9 @@ p2r_status p2r_model_buffer(p2r_model* m, int which, void** ptr, size_t* bytes);
 p2r_status p2r_model_routing(const p2r_model* m, int g, int* selected, uint8_t* survived,
                              int* raw_load, int* capacity, int* dropped);
 
+/* fp32 gate logits [T, E] of graph layer g from the last forward (MoE). */
+p2r_status p2r_model_gate_logits(const p2r_model* m, int g, float* out);
+
 /* moe_dispatch (model.cpp:294-332) on host logits [T, E]: same outputs as the
  * reference's Routing, expert_rows/slots flattened CSR (offsets[E+1]). */
 p2r_status p2r_moe_dispatch_host(const float* logits, int T, int E, int k, float cf, int* selected,
@@ -193,8 +196,20 @@ p2r_status p2r_model_allreduce_grads(p2r_model* m);
 p2r_status p2r_model_create_offload(const p2r_model_config* cfg, uint64_t seed, const int* slow,
                                     int ring_slots, p2r_model** out);
 p2r_status p2r_model_set_offload_lr(p2r_model* m, float lr);
-/* out7 = {Fn_load, Bn_load, opt_load, writeback, grad_offload, h2d_ms, d2h_ms} since last reset */
-p2r_status p2r_model_offload_stats(p2r_model* m, double* out7);
+/* Expert-parallel shard (world, rank) with granular offload (C5). */
+p2r_status p2r_model_create_offload_ep(const p2r_model_config* cfg, uint64_t seed, const int* slow,
+                                       int ring_slots, int world, int rank, p2r_model** out);
+/* Gradient accumulation over `micro_steps` train_step calls (the first with zero=1):
+ * SLOW granules park partial gradients in pinned host memory between micro-steps and
+ * apply the fused AdamW (lr from p2r_model_set_offload_lr) in the last backward.
+ * ELOGIC for a micro-step past the window or adamw_step before its last backward. */
+p2r_status p2r_model_set_grad_accumulation(p2r_model* m, int micro_steps);
+/* Activation checkpointing of offloaded models: 0 off, 1 SLOW layers
+ * (default), 2 every layer. Results are bit-identical to the stored activations. */
+p2r_status p2r_model_set_activation_checkpointing(p2r_model* m, int policy);
+/* out8 = {Fn_load, Bn_load, opt_load, writeback, grad_offload, h2d_ms, d2h_ms, grad_load} since
+ * last reset (grad_load: H2D of partial SLOW gradients between accumulation micro-steps) */
+p2r_status p2r_model_offload_stats(p2r_model* m, double* out8);
 p2r_status p2r_model_offload_stats_reset(p2r_model* m);
 p2r_status p2r_model_set_offload_skip_copies(p2r_model* m, int skip);
 int64_t p2r_model_layer_granule_bytes(const p2r_model* m);

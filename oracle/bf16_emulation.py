@@ -1,5 +1,5 @@
 """ORACLE / TEST INFRASTRUCTURE ONLY — numpy emulation of WHERE the B200 path
-rounds to bf16 (dense block stack), used to separate the error inherent to the
+rounds to bf16 (dense and MoE block stacks), used to separate the error inherent to the
 bf16-in / fp32-accumulate design from kernel bugs. `points` selects which
 tensors are rounded; an empty set reproduces p2r_oracle.Model exactly.
 Mirrors Model::block_forward / block_backward in csrc/engine/engine.cpp.
@@ -12,7 +12,7 @@ from . import p2r_oracle as O
 
 F32 = np.float32
 ALL_POINTS = ("w16", "a16", "qkv16", "p16", "o16", "b16", "hpre16", "g16", "h16",
-              "dlogits16", "dres16", "dh16", "dx1_16", "do16", "ds16", "dqkv16")
+              "dlogits16", "dres16", "dh16", "dx1_16", "do16", "ds16", "dqkv16", "ye16", "dye16")
 
 
 def bf16(x):
@@ -22,7 +22,12 @@ def bf16(x):
     return r.view(np.float32)
 
 
-def loss_and_grads(cfg: O.Config, params: dict, tokens, targets, mask, batch, denom, points=ALL_POINTS):
+def loss_and_grads(cfg: O.Config, params: dict, tokens, targets, mask, batch, denom, points=ALL_POINTS,
+                   forced_selected=None, routing_out=None):
+    """forced_selected: {graph layer: selected[T*k]} pins MoE routing (as the parity
+    tests do with the GPU's routing); MoE layers without an entry route on their
+    own (emulated) fp32 gate logits."""
+    import math
     pts = set(points)
 
     def R(x, tag):
@@ -65,11 +70,40 @@ def loss_and_grads(cfg: O.Config, params: dict, tokens, targets, mask, batch, de
         x1 = (x + o16 @ W[pr + "attn.wo"]).astype(F32)
         b, xh2, inv2 = O.layernorm_fwd(x1, P0[pr + "ln2.gain"], P0[pr + "ln2.bias"])
         b16 = R(b, "b16")
-        hpre = (b16 @ W[pr + "ffn.w1"] + P0[pr + "ffn.b1"]).astype(F32)
-        g16 = R(O.gelu_fwd(hpre), "g16")
-        hpre16 = R(hpre, "hpre16")
-        xn = (x1 + g16 @ W[pr + "ffn.w2"] + P0[pr + "ffn.b2"]).astype(F32)
-        caches.append((x, a16, xh1, inv1, qkv, ac, o16, x1, b16, xh2, inv2, hpre16, g16, wqkv))
+        if c.moe:
+            # fp32 gate on the fp32 LN2 output; experts read the bf16 rows (xe16 = b16)
+            logits = (b @ P0[pr + "moe.gate"]).astype(F32)
+            T_ = b.shape[0]
+            if forced_selected is not None and g in forced_selected:
+                cap = int(math.ceil(float(F32(c.capacity_factor)) * T_ / float(c.n_experts // c.n_prototypes)))
+                rt = O.admit(forced_selected[g], c.n_experts, c.n_prototypes, cap)
+            else:
+                rt = O.moe_dispatch_vectorized(logits, c.n_experts, c.n_prototypes, c.capacity_factor)
+            if routing_out is not None:
+                routing_out[g] = rt.selected.copy()
+            wgt = O.selected_softmax_fwd(logits, rt)
+            y = np.zeros_like(b)
+            ec = []
+            for e in range(c.n_experts):
+                rows = rt.expert_rows[e]
+                if len(rows) == 0:
+                    ec.append(None)
+                    continue
+                xe = b16[rows]
+                he = (xe @ W[pr + f"moe.expert.{e}.w1"] + P0[pr + f"moe.expert.{e}.b1"]).astype(F32)
+                ge16 = R(O.gelu_fwd(he), "g16")
+                ye = R((ge16 @ W[pr + f"moe.expert.{e}.w2"] + P0[pr + f"moe.expert.{e}.b2"]).astype(F32), "ye16")
+                wv = wgt[rows, rt.expert_slots[e]]
+                y[rows] += wv[:, None] * ye
+                ec.append((xe, R(he, "hpre16"), ge16, ye))
+            xn = (x1 + y).astype(F32)
+            caches.append((x, a16, xh1, inv1, qkv, ac, o16, x1, b16, xh2, inv2, (b, logits, rt, wgt, ec), None, wqkv))
+        else:
+            hpre = (b16 @ W[pr + "ffn.w1"] + P0[pr + "ffn.b1"]).astype(F32)
+            g16 = R(O.gelu_fwd(hpre), "g16")
+            hpre16 = R(hpre, "hpre16")
+            xn = (x1 + g16 @ W[pr + "ffn.w2"] + P0[pr + "ffn.b2"]).astype(F32)
+            caches.append((x, a16, xh1, inv1, qkv, ac, o16, x1, b16, xh2, inv2, hpre16, g16, wqkv))
         x = xn
     h, xhf, invf = O.layernorm_fwd(x, P0["final_norm.gain"], P0["final_norm.bias"])
     h16 = R(h, "h16")
@@ -86,13 +120,35 @@ def loss_and_grads(cfg: O.Config, params: dict, tokens, targets, mask, batch, de
         pr = pre(g)
         x, a16, xh1, inv1, qkv, (q, k, v, p), o16, x1, b16, xh2, inv2, hpre16, g16, wqkv = caches[g]
         dy = dres
-        dy16 = R(dy, "dres16")
-        G[pr + "ffn.w2"] += g16.T @ dy16
-        G[pr + "ffn.b2"] += dy.sum(0)
-        dh16 = R(O.gelu_bwd(dy16 @ W[pr + "ffn.w2"].T, hpre16), "dh16")
-        G[pr + "ffn.w1"] += b16.T @ dh16
-        G[pr + "ffn.b1"] += dh16.sum(0)
-        db = (dh16 @ W[pr + "ffn.w1"].T).astype(F32)
+        if c.moe:
+            bm, logits, rt, wgt, ec = hpre16
+            db = np.zeros_like(bm)
+            gw = np.zeros_like(wgt)
+            for e in reversed(range(c.n_experts)):
+                if ec[e] is None:
+                    continue
+                xe, he16, ge16, ye = ec[e]
+                rows, slots = rt.expert_rows[e], rt.expert_slots[e]
+                wv = wgt[rows, slots]
+                dye = R((wv[:, None] * dy[rows]).astype(F32), "dye16")
+                gw[rows, slots] += (dy[rows] * ye).sum(-1, dtype=F32)
+                G[pr + f"moe.expert.{e}.w2"] += ge16.T @ dye
+                G[pr + f"moe.expert.{e}.b2"] += dye.sum(0)
+                dhe = R(O.gelu_bwd(dye @ W[pr + f"moe.expert.{e}.w2"].T, he16), "dh16")
+                G[pr + f"moe.expert.{e}.w1"] += xe.T @ dhe
+                G[pr + f"moe.expert.{e}.b1"] += dhe.sum(0)
+                np.add.at(db, rows, (dhe @ W[pr + f"moe.expert.{e}.w1"].T).astype(F32))
+            glog = O.selected_softmax_bwd(gw, wgt, rt, c.n_experts)
+            G[pr + "moe.gate"] += (bm.T @ glog).astype(F32)
+            db += (glog @ P0[pr + "moe.gate"].T).astype(F32)
+        else:
+            dy16 = R(dy, "dres16")
+            G[pr + "ffn.w2"] += g16.T @ dy16
+            G[pr + "ffn.b2"] += dy.sum(0)
+            dh16 = R(O.gelu_bwd(dy16 @ W[pr + "ffn.w2"].T, hpre16), "dh16")
+            G[pr + "ffn.w1"] += b16.T @ dh16
+            G[pr + "ffn.b1"] += dh16.sum(0)
+            db = (dh16 @ W[pr + "ffn.w1"].T).astype(F32)
         gx1, gg, gb = O.layernorm_bwd(db, xh2, inv2, P0[pr + "ln2.gain"])
         G[pr + "ln2.gain"] += gg
         G[pr + "ln2.bias"] += gb

@@ -294,6 +294,10 @@ p2r_status p2r_model_routing(const p2r_model* m, int g, int* selected, uint8_t* 
   return guard([&] { m->m->routing_host(g, selected, survived, raw_load, capacity, dropped); });
 }
 
+p2r_status p2r_model_gate_logits(const p2r_model* m, int g, float* out) {
+  return guard([&] { m->m->gate_logits_host(g, out); });
+}
+
 p2r_status p2r_moe_dispatch_host(const float* logits, int T, int E, int k, float cf, int* selected,
                                  uint8_t* survived, int* raw_load, int* offsets, int* rows, int* slots,
                                  int* capacity, int* dropped) {
@@ -343,6 +347,22 @@ p2r_status p2r_model_create_offload(const p2r_model_config* cfg, uint64_t seed, 
     *out = h.release();
   });
 }
+p2r_status p2r_model_create_offload_ep(const p2r_model_config* cfg, uint64_t seed, const int* slow, int ring_slots,
+                                       int world, int rank, p2r_model** out) {
+  return guard([&] {
+    const int n = cfg->n_layers_params;
+    std::vector<int> pl(slow, slow + n);
+    auto h = std::make_unique<p2r_model>();
+    h->m = std::make_unique<p2r::Model>(to_cfg(cfg), seed, pl, ring_slots, world, rank);
+    *out = h.release();
+  });
+}
+p2r_status p2r_model_set_grad_accumulation(p2r_model* m, int micro_steps) {
+  return guard([&] { m->m->set_grad_accumulation(micro_steps); });
+}
+p2r_status p2r_model_set_activation_checkpointing(p2r_model* m, int policy) {
+  return guard([&] { m->m->set_activation_checkpointing(policy); });
+}
 p2r_status p2r_model_set_offload_lr(p2r_model* m, float lr) {
   m->m->set_offload_lr(lr);
   return P2R_OK;
@@ -357,6 +377,7 @@ p2r_status p2r_model_offload_stats(p2r_model* m, double* o) {
     o[4] = s.grad_offload;
     o[5] = s.h2d_ms;
     o[6] = s.d2h_ms;
+    o[7] = s.grad_load;
   });
 }
 p2r_status p2r_model_offload_stats_reset(p2r_model* m) {

@@ -117,7 +117,13 @@ void Model::ep_exchange(const void* src, void* dst, std::size_t row_bytes, int s
   nccl_check(api.groupEnd(), "group end");
 }
 
+void Model::allreduce_f32(float* buf, std::size_t n) {
+  if (!comm_) throw std::logic_error("allreduce_grads: communicator not initialised");
+  nccl_check(nccl().allReduce(buf, buf, n, kNcclFloat32, kNcclSum, comm_, stream_), "allreduce");
+}
+
 // DP: sum the replicated gradient parts over ranks, in place, on the model stream.
+// SLOW (offloaded) granules are summed inside their backward, before the fused AdamW.
 void Model::allreduce_grads() {
   if (!comm_) throw std::logic_error("allreduce_grads: communicator not initialised");
   NcclApi& api = nccl();
@@ -129,7 +135,7 @@ void Model::allreduce_grads() {
   // replicated; experts are sharded. Dense layers are replicated entirely.
   const long long repl = cfg_.moe.enabled() ? layer_.w1 : layer_.numel;
   for (int o = 0; o < n_owned_; ++o) {
-    if (res_idx_[static_cast<std::size_t>(o)] < 0) continue;  // offloaded granules: not combined with DP here
+    if (res_idx_[static_cast<std::size_t>(o)] < 0) continue;  // SLOW: reduced in offload_release
     nccl_check(api.allReduce(lg(o, 0), lg(o, 0), static_cast<std::size_t>(repl), kNcclFloat32, kNcclSum, comm_,
                              stream_),
                "allreduce layer");

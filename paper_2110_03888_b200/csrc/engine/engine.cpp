@@ -172,6 +172,11 @@ struct Acts {
   int B = 0, S = 0, T = 0, seg = 0, cap = 0, vld = 0;
   DevBuf x0;
   std::vector<LayerActs> L;
+  // activation checkpointing: layers with ckpt[g] keep only their output
+  // L[g].xout; the rest of their activations live in the shared set `ck` and are
+  // recomputed from the layer input in the backward
+  std::vector<char> ckpt;
+  LayerActs ck;
   DevBuf h16, meanf, rstdf, logits32, dlogits16, loss, loss_sum, ce_ws, dh32;
   DevBuf dres, dres16, tmp32, dx1, dx1_16, do16, dqkv16, dh16, dye16, dxe32, dw, glogits, dsum;
   DevBuf ln_ws, colsum_ws, embed_ws;
@@ -186,32 +191,52 @@ struct Acts {
 
 // ---------------------------------------------------------------- Model
 Model::Model(ModelConfig config, std::uint64_t seed) : cfg_(std::move(config)) {
-  cfg_.validate();
-  build_layout();
-  allocate();
-  init_params(seed);
+  init_model(seed, nullptr, 0, 1, 0, false);
 }
 
 Model::Model(ModelConfig config, std::uint64_t seed, const std::vector<int>& slow, int ring_slots)
     : cfg_(std::move(config)) {
-  cfg_.validate();
-  build_layout();
-  offload_setup(slow, ring_slots);
-  allocate();
-  init_params(seed);
+  init_model(seed, &slow, ring_slots, 1, 0, false);
 }
 
 Model::Model(ModelConfig config, std::uint64_t seed, int ep_world, int ep_rank) : cfg_(std::move(config)) {
+  init_model(seed, nullptr, 0, ep_world, ep_rank, true);
+}
+
+Model::Model(ModelConfig config, std::uint64_t seed, const std::vector<int>& slow, int ring_slots, int ep_world,
+             int ep_rank)
+    : cfg_(std::move(config)) {
+  init_model(seed, &slow, ring_slots, ep_world, ep_rank, true);
+}
+
+void Model::init_model(std::uint64_t seed, const std::vector<int>* slow, int ring_slots, int ep_world, int ep_rank,
+                       bool ep_ctor) {
   cfg_.validate();
   if (ep_world < 1 || ep_rank < 0 || ep_rank >= ep_world)
     throw std::invalid_argument("expert parallel: rank must be in [0, world)");
   ep_world_ = ep_world;
   ep_rank_ = ep_rank;
-  const char* f = std::getenv("P2R_FORCE_EP");
-  force_ep_ = f != nullptr && f[0] == '1';
+  if (ep_ctor) {  // P2R_FORCE_EP=1: run the exchange path even at world size 1 (tests)
+    const char* f = std::getenv("P2R_FORCE_EP");
+    force_ep_ = f != nullptr && f[0] == '1';
+  }
   build_layout();
+  if (slow) offload_setup(*slow, ring_slots);
   allocate();
   init_params(seed);
+}
+
+void Model::set_grad_accumulation(int n) {
+  if (n < 1) throw std::invalid_argument("offload: accumulation window must be >= 1 micro-step");
+  accum_n_ = n;
+}
+
+void Model::set_activation_checkpointing(int policy) {
+  if (policy < 0 || policy > 2) throw std::invalid_argument("checkpointing: policy must be 0, 1 or 2");
+  if (policy != ckpt_policy_) {
+    ckpt_policy_ = policy;
+    acts_.reset();  // the activation sets are laid out per policy
+  }
 }
 
 Model::Model(ModelConfig config, NoInit, int ep_world, int ep_rank, bool force_ep) : cfg_(std::move(config)) {
@@ -440,6 +465,10 @@ std::int64_t Model::grad_bytes() const {
 void Model::zero_grads() {
   cuda_check(cudaMemsetAsync(emb_g_.p, 0, emb_g_.bytes, stream_), "zero grads");
   cuda_check(cudaMemsetAsync(lay_g_.p, 0, lay_g_.bytes, stream_), "zero grads");
+  if (off_) {  // SLOW granules: drop the parked partial gradients, restart the window
+    std::fill(off_->hgrad_valid.begin(), off_->hgrad_valid.end(), 0);
+    micro_ = 0;
+  }
 }
 
 // ---------------------------------------------------------------- activations
@@ -463,8 +492,21 @@ void Model::ensure_acts(int B, int S) {
   const std::size_t ES = static_cast<std::size_t>(E) * A->seg;
   A->x0 = DevBuf(Td * 4);
   A->L.resize(static_cast<std::size_t>(cfg_.n_layers_graph));
-  for (auto& l : A->L) {
-    l.xout = DevBuf(Td * 4);
+  A->ckpt.assign(static_cast<std::size_t>(cfg_.n_layers_graph), 0);
+  bool any_ckpt = false;
+  for (int g = 0; g < cfg_.n_layers_graph; ++g) {
+    const bool c = checkpointed(g);
+    A->ckpt[static_cast<std::size_t>(g)] = c ? 1 : 0;
+    any_ckpt = any_ckpt || c;
+  }
+  std::vector<LayerActs*> full;
+  for (int g = 0; g < cfg_.n_layers_graph; ++g) {
+    A->L[static_cast<std::size_t>(g)].xout = DevBuf(Td * 4);
+    if (!A->ckpt[static_cast<std::size_t>(g)]) full.push_back(&A->L[static_cast<std::size_t>(g)]);
+  }
+  if (any_ckpt) full.push_back(&A->ck);
+  for (LayerActs* lp_ : full) {
+    LayerActs& l = *lp_;
     l.a16 = DevBuf(Td * 2);
     l.mean1 = DevBuf(T * 4);
     l.rstd1 = DevBuf(T * 4);
@@ -651,6 +693,10 @@ void Model::buffer(int which, void** ptr, std::size_t* bytes) const {
 Tensor Model::embed_forward(GradTape* tape, const int* d_tokens, int batch, int seq) {
   if (batch <= 0) throw std::invalid_argument("forward: token count must be a multiple of batch");
   if (seq > cfg_.seq_len) throw std::invalid_argument("forward: sequence longer than configured seq_len");
+  if (off_ && tape != nullptr && !off_->slow_list.empty()) {
+    offload_check_micro(micro_ + 1);
+    ++micro_;
+  }
   ensure_acts(batch, seq);
   if (off_) offload_begin_forward(tape != nullptr);
   Acts& A = *acts_;
@@ -676,9 +722,28 @@ Tensor Model::block_forward(GradTape* tape, int g, const Tensor& x, int batch, A
   if (g < 0 || g >= cfg_.n_layers_graph) throw std::out_of_range("model: graph layer index out of range");
   Acts& A = *acts_;
   if (x.rows != A.T || batch != A.B) throw std::invalid_argument("block_forward: batch does not match embed_forward");
-  LayerActs& L = A.L[static_cast<std::size_t>(g)];
   const int o = owned_index_of_graph_layer(g);
   if (off_) offload_acquire(o, false);
+  block_compute(g, x.data, mode);
+  if (off_) offload_release(o, false);
+  if (tape) tape->record([this, g, mode]() { block_backward(g, mode); });
+  return Tensor{A.T, cfg_.d_model, A.L[static_cast<std::size_t>(g)].xout.as<float>(), A.dres.as<float>(), A.dres16.p};
+}
+
+bool Model::checkpointed(int g) const {
+  if (!off_ || ckpt_policy_ == 0) return false;
+  return ckpt_policy_ == 2 || slow_[static_cast<std::size_t>(owned_index_of_graph_layer(g))] != 0;
+}
+
+// The forward of graph layer g from input x (fp32 [T, d]) into its activation set
+// (the shared checkpoint set for checkpointed layers) and its output L[g].xout. Run
+// by block_forward, and again by block_backward to recompute a checkpointed layer.
+void Model::block_compute(int g, const float* xin_data, AttentionMode mode) {
+  Acts& A = *acts_;
+  LayerActs& L = A.ckpt[static_cast<std::size_t>(g)] ? A.ck : A.L[static_cast<std::size_t>(g)];
+  float* xout = A.L[static_cast<std::size_t>(g)].xout.as<float>();
+  const Tensor x{A.T, cfg_.d_model, const_cast<float*>(xin_data), nullptr, nullptr};
+  const int o = owned_index_of_graph_layer(g);
   const int T = A.T, d = cfg_.d_model, dff = cfg_.d_ff, H = cfg_.n_heads;
   const int causal = mode == AttentionMode::Causal ? 1 : 0;
   const double Td = static_cast<double>(T) * d;
@@ -707,7 +772,7 @@ Tensor Model::block_forward(GradTape* tape, int g, const Tensor& x, int batch, A
   if (!moe) {
     gemm(T, dff, d, L.b16.p, d, false, lp16(o, layer_.w1), dff, true, P2R_EPI_BIAS_GELU, L.g16.p, dff, L.hpre16.p,
          dff, lp(o, layer_.b1));
-    gemm(T, d, dff, L.g16.p, dff, false, lp16(o, layer_.w2), d, true, P2R_EPI_F32, L.xout.p, d, nullptr, 0,
+    gemm(T, d, dff, L.g16.p, dff, false, lp16(o, layer_.w2), d, true, P2R_EPI_F32, xout, d, nullptr, 0,
          lp(o, layer_.b2), L.x1.p, d);
   } else {
     const int E = cfg_.moe.n_experts, k = cfg_.moe.n_prototypes, seg = A.seg;
@@ -742,12 +807,9 @@ Tensor Model::block_forward(GradTape* tape, int g, const Tensor& x, int batch, A
          ep ? A.ye_owner32.p : L.ye32.p, d, nullptr, 0, lp(o, layer_.b2), nullptr, 0, P2R_GROUP_M, G, gseg, gcnt);
     if (ep) ep_exchange(A.ye_owner32.p, L.ye32.p, static_cast<std::size_t>(d) * 4, seg, false);
     p2r_check(p2r_moe_combine(L.ye32.as<float>(), T, d, k, seg, L.sel.as<int>(), L.pos.as<int>(), L.w.as<float>(),
-                              L.x1.as<float>(), L.xout.as<float>(), stream_),
+                              L.x1.as<float>(), xout, stream_),
               "combine");
   }
-  if (off_) offload_release(o, false);
-  if (tape) tape->record([this, g, mode]() { block_backward(g, mode); });
-  return Tensor{T, d, L.xout.as<float>(), A.dres.as<float>(), A.dres16.p};
 }
 
 // Backward of graph layer g. On entry A.dres/dres16 hold dL/d(block output);
@@ -757,12 +819,15 @@ Tensor Model::block_forward(GradTape* tape, int g, const Tensor& x, int batch, A
 // per-layer flush (model.cpp:210-221).
 void Model::block_backward(int g, AttentionMode mode) {
   Acts& A = *acts_;
-  LayerActs& L = A.L[static_cast<std::size_t>(g)];
+  LayerActs& L = A.ckpt[static_cast<std::size_t>(g)] ? A.ck : A.L[static_cast<std::size_t>(g)];
   const int o = owned_index_of_graph_layer(g);
   if (off_) offload_acquire(o, true);
   const int T = A.T, d = cfg_.d_model, dff = cfg_.d_ff, H = cfg_.n_heads;
   const int causal = mode == AttentionMode::Causal ? 1 : 0;
   const float* xin = g == 0 ? A.x0.as<float>() : A.L[static_cast<std::size_t>(g - 1)].xout.as<float>();
+  // activation checkpointing: recompute this layer's activations from its input
+  // (the same kernels on the same operands, so bit-identical to the stored ones)
+  if (A.ckpt[static_cast<std::size_t>(g)]) block_compute(g, xin, mode);
   float* dy = A.dres.as<float>();
   void* dy16 = A.dres16.p;
   if (!cfg_.moe.enabled()) {
@@ -918,8 +983,23 @@ Tensor Model::softmax_cross_entropy(GradTape* /*tape*/, const Tensor& logits, co
   return Tensor{1, 1, A.loss.as<float>(), nullptr, nullptr};
 }
 
+// A training micro-step of an offloaded model: the SLOW granules' fused AdamW runs in
+// the backward of the accumulation window's last micro-step (set_grad_accumulation).
+// Checked before anything is zeroed or launched, so a misuse leaves the state intact.
+void Model::offload_check_micro(int next_micro) const {
+  if (!off_ || off_->slow_list.empty()) return;
+  if (next_micro > accum_n_)
+    throw std::logic_error(
+        "offload: gradient accumulation past the window; call set_grad_accumulation(n) or start with zero=true");
+  if (slow_applied_)
+    throw std::logic_error("offload: adamw_step(lr) was not called after the last optimizer step's backward");
+  if (has_opt_ && next_micro == accum_n_ && std::isnan(offload_lr_))
+    throw std::logic_error("offload: call set_offload_lr(lr) before the backward that applies AdamW");
+}
+
 void Model::train_step_device(const int* d_tokens, const int* d_targets, const std::uint8_t* d_mask, int batch,
                               int seq, double denom, AttentionMode mode, bool zero, float* loss_dev) {
+  if (off_) offload_check_micro(zero ? 1 : micro_ + 1);
   if (zero) zero_grads();
   GradTape tape;
   Tensor x = embed_forward(&tape, d_tokens, batch, seq);
@@ -1051,7 +1131,7 @@ void Model::routing_host(int g, int* selected, std::uint8_t* survived, int* raw_
                          int* dropped) const {
   if (!cfg_.moe.enabled()) throw std::logic_error("routing: dense model");
   if (!acts_) throw std::logic_error("routing: no forward pass yet");
-  const LayerActs& L = acts_->L.at(static_cast<std::size_t>(g));
+  const LayerActs& L = acts_->ckpt.at(static_cast<std::size_t>(g)) ? acts_->ck : acts_->L.at(static_cast<std::size_t>(g));
   const std::size_t Tk = static_cast<std::size_t>(acts_->T) * cfg_.moe.n_prototypes;
   cuda_check(cudaMemcpyAsync(selected, L.sel.p, Tk * 4, cudaMemcpyDeviceToHost, stream_), "d2h");
   cuda_check(cudaMemcpyAsync(survived, L.surv.p, Tk, cudaMemcpyDeviceToHost, stream_), "d2h");
@@ -1059,6 +1139,16 @@ void Model::routing_host(int g, int* selected, std::uint8_t* survived, int* raw_
   cuda_check(cudaMemcpyAsync(dropped, L.dropped.p, 4, cudaMemcpyDeviceToHost, stream_), "d2h");
   cuda_check(cudaStreamSynchronize(stream_), "sync");
   *capacity = L.capacity;
+}
+
+void Model::gate_logits_host(int g, float* out) const {
+  if (!cfg_.moe.enabled()) throw std::logic_error("routing: dense model");
+  if (!acts_) throw std::logic_error("routing: no forward pass yet");
+  const LayerActs& L = acts_->ckpt.at(static_cast<std::size_t>(g)) ? acts_->ck : acts_->L.at(static_cast<std::size_t>(g));
+  cuda_check(cudaMemcpyAsync(out, L.logits.p, static_cast<std::size_t>(acts_->T) * cfg_.moe.n_experts * 4,
+                             cudaMemcpyDeviceToHost, stream_),
+             "d2h");
+  cuda_check(cudaStreamSynchronize(stream_), "sync");
 }
 
 // ---------------------------------------------------------------- AdamW (optim.cpp:28-70)
@@ -1083,11 +1173,18 @@ void Model::adamw_attach(float b1, float b2, float eps, float wd) {
 
 void Model::adamw_step(float lr) {
   if (!has_opt_) throw std::logic_error("adamw: unregistered parameter embed.tok");
+  // checks first: a throw must leave the step count and every moment untouched
+  if (off_ && !off_->slow_list.empty()) {
+    if (!slow_applied_)
+      throw std::logic_error(
+          "offload: adamw_step before the accumulation window's last backward (SLOW granules not updated)");
+    if (lr != offload_lr_)
+      throw std::invalid_argument("adamw: offloaded granules were updated with set_offload_lr(); pass the same lr");
+  }
   ++step_count_;
+  slow_applied_ = false;
   const float bc1 = 1.0f - std::pow(b1_, static_cast<float>(step_count_));
   const float bc2 = 1.0f - std::pow(b2_, static_cast<float>(step_count_));
-  if (off_ && lr != offload_lr_)
-    throw std::invalid_argument("adamw: offloaded granules were updated with set_offload_lr(); pass the same lr");
   auto run = [&](const GranuleLayout& lay, float* p, float* g, float* m, float* v, void* p16) {
     std::vector<long long> off, len;
     std::vector<int> dec;

@@ -170,6 +170,10 @@ std::vector<int> plan_offload(const std::vector<std::int64_t>& layer_bytes, std:
 
 // ---------------------------------------------------------------- engine side
 void Model::offload_setup(const std::vector<int>& slow, int ring_slots) {
+  // A Pseudo model's L graph layers share one granule: reloading it per graph layer
+  // would apply L fused AdamW updates from partial gradients
+  if (cfg_.n_layers_params != cfg_.n_layers_graph)
+    throw std::invalid_argument("offload: granular offload needs an unshared (Real) model");
   if (static_cast<int>(slow.size()) != n_owned_)
     throw std::invalid_argument("offload: placement must give one entry per owned layer");
   if (ring_slots < 2) throw std::invalid_argument("offload: need at least 2 staging slots");
@@ -184,6 +188,7 @@ void Model::offload_setup(const std::vector<int>& slow, int ring_slots) {
   st->slot_fwd.assign(static_cast<std::size_t>(n_owned_), -1);
   st->slot_bwd.assign(static_cast<std::size_t>(n_owned_), -1);
   st->host_idx.assign(static_cast<std::size_t>(n_owned_), -1);
+  st->hgrad_valid.assign(static_cast<std::size_t>(n_owned_), 0);
   slow_ = slow;
   int nr = 0, ns = 0;
   for (int o = 0; o < n_owned_; ++o) {
@@ -307,12 +312,16 @@ void Model::offload_prefetch_next(int /*after*/, bool /*backward*/) {
                    st.h2d, true, &st.stats.fn_load);
       }
     } else {
-      // Bn + An: fp32 master (bf16 shadow re-derived on the device) + moments
+      // Bn + An: fp32 master (bf16 shadow re-derived on the device) + moments; the
+      // moments only in the micro-step that runs the fused AdamW
       copy_async(st, sl.p32.p, slow_host_p32(o), g * 4, st.h2d, true, &st.stats.bn_load);
-      if (has_opt_) {
+      if (has_opt_ && micro_ == accum_n_) {
         copy_async(st, sl.m.p, slow_host_m(o, 0), g * 4, st.h2d, true, &st.stats.opt_load);
         copy_async(st, sl.v.p, slow_host_m(o, 1), g * 4, st.h2d, true, &st.stats.opt_load);
       }
+      // accumulation: continue from the partial gradients parked by the previous micro-step
+      sl.grads_loaded = st.hgrad_valid[static_cast<std::size_t>(o)] != 0;
+      if (sl.grads_loaded) copy_async(st, sl.g32.p, slow_host_grad(o), g * 4, st.h2d, true, &st.stats.grad_load);
     }
     cuda_check(cudaEventRecord(b, st.h2d), "event");
     st.copies.push_back({a, b, true});
@@ -338,7 +347,7 @@ void Model::offload_acquire(int o, bool backward) {
   cuda_check(cudaStreamWaitEvent(stream_, sl.loaded, 0), "wait loaded");
   if (backward || st.fwd_master)
     p2r_check(p2r_cast_bf16(sl.p32.as<float>(), sl.p16.p, layer_stride_, stream_), "offload bf16 operand");
-  if (backward) cuda_check(cudaMemsetAsync(sl.g32.p, 0, sl.g32.bytes, stream_), "zero slot grads");
+  if (backward && !sl.grads_loaded) cuda_check(cudaMemsetAsync(sl.g32.p, 0, sl.g32.bytes, stream_), "zero slot grads");
 }
 
 void Model::offload_release(int o, bool backward) {
@@ -356,20 +365,30 @@ void Model::offload_release(int o, bool backward) {
     offload_prefetch_next(o, false);
     return;
   }
-  // An phase: fused AdamW on the staged granule, then write back
+  // An phase. The last micro-step of the accumulation window sums the replicated
+  // gradient part over the data-parallel ranks, runs the fused AdamW on the staged
+  // granule and writes p, m, v back; earlier micro-steps (and models without an
+  // optimizer) park the partial gradients in pinned host memory instead.
+  const bool apply = has_opt_ && micro_ == accum_n_;
   cudaEvent_t done = st.ev();
-  if (has_opt_) {
+  if (apply) {
+    if (comm_ != nullptr && ep_world_ > 1) {
+      const long long repl = cfg_.moe.enabled() ? layer_.w1 : layer_.numel;
+      allreduce_f32(sl.g32.as<float>(), static_cast<std::size_t>(repl));
+    }
     const std::int64_t t = step_count_ + 1;
     const float bc1 = 1.0f - std::pow(b1_, static_cast<float>(t));
     const float bc2 = 1.0f - std::pow(b2_, static_cast<float>(t));
     adamw_granule(sl.p32.as<float>(), sl.g32.as<float>(), sl.m.as<float>(), sl.v.as<float>(), sl.p16.p, offload_lr_,
                   bc1, bc2);
+    slow_applied_ = true;
   }
   cuda_check(cudaEventRecord(done, stream_), "event");
   cuda_check(cudaStreamWaitEvent(st.d2h, done, 0), "wait compute");
   cudaEvent_t a = st.ev(), b = st.ev();
   cuda_check(cudaEventRecord(a, st.d2h), "event");
-  if (has_opt_) {
+  st.hgrad_valid[static_cast<std::size_t>(o)] = apply ? 0 : 1;
+  if (apply) {
     copy_async(st, slow_host_p32(o), sl.p32.p, g * 4, st.d2h, false, &st.stats.writeback);
     if (!st.fwd_master) copy_async(st, slow_host_p16(o), sl.p16.p, g * 2, st.d2h, false, &st.stats.writeback);
     copy_async(st, slow_host_m(o, 0), sl.m.p, g * 4, st.d2h, false, &st.stats.writeback);

@@ -14,6 +14,7 @@ struct OffloadSlot {
   int layer = -1;
   cudaEvent_t loaded = nullptr, free_ev = nullptr;
   bool free_recorded = false;
+  bool grads_loaded = false;  // Bn staging brought the layer's parked partial gradients
 };
 
 struct OffloadState {
@@ -28,6 +29,7 @@ struct OffloadState {
   int next_slot_rr = 0;
   std::vector<int> host_idx;   // owned layer -> index in host arrays or -1
   std::vector<int> slow_list;  // SLOW owned layers, ascending
+  std::vector<char> hgrad_valid;  // owned layer -> host holds its partial gradients (accumulation)
   std::vector<cudaEvent_t> wb_ev;
   std::vector<char> wb_recorded;
   float* hp32 = nullptr;

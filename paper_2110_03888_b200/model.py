@@ -61,6 +61,7 @@ _lib._EXTRA_SIGNATURES.update({
     "p2r_model_redistribute_experts": [vp, ip],
     "p2r_redistribute_checkpoints": [ctypes.POINTER(ctypes.c_char_p), ip, ctypes.POINTER(ctypes.c_char_p), ip],
     "p2r_model_routing": [vp, ip, vp, vp, vp, ctypes.POINTER(ip), ctypes.POINTER(ip)],
+    "p2r_model_gate_logits": [vp, ip, vp],
     "p2r_moe_dispatch_host": [vp, ip, ip, ip, fp, vp, vp, vp, vp, vp, vp,
                               ctypes.POINTER(ip), ctypes.POINTER(ip)],
     "p2r_comm_unique_id": [ctypes.c_char_p],
@@ -69,6 +70,10 @@ _lib._EXTRA_SIGNATURES.update({
     "p2r_model_allreduce_grads": [vp],
     "p2r_model_create_offload": [ctypes.POINTER(ModelConfigC), ctypes.c_uint64, vp, ip, ctypes.POINTER(vp)],
     "p2r_model_set_offload_lr": [vp, fp],
+    "p2r_model_create_offload_ep": [ctypes.POINTER(ModelConfigC), ctypes.c_uint64, vp, ip, ip, ip,
+                                    ctypes.POINTER(vp)],
+    "p2r_model_set_grad_accumulation": [vp, ip],
+    "p2r_model_set_activation_checkpointing": [vp, ip],
     "p2r_model_offload_stats": [vp, vp],
     "p2r_model_offload_stats_reset": [vp],
     "p2r_model_set_offload_skip_copies": [vp, ip],
@@ -189,7 +194,11 @@ class Model:
         self.cfg = cfg
         if handle is None:
             h = vp()
-            if ep is not None:
+            if ep is not None and offload is not None:
+                sl = np.ascontiguousarray(offload, np.int32)
+                check(L.p2r_model_create_offload_ep(ctypes.byref(cfg.c()), seed, _p(sl), ring_slots, int(ep[0]),
+                                                    int(ep[1]), ctypes.byref(h)))
+            elif ep is not None:
                 check(L.p2r_model_create_ep(ctypes.byref(cfg.c()), seed, int(ep[0]), int(ep[1]),
                                             ctypes.byref(h)))
             elif offload is None:
@@ -326,10 +335,17 @@ class Model:
     def set_offload_lr(self, lr: float):
         check(lib().p2r_model_set_offload_lr(self.h, lr))
 
+    def set_grad_accumulation(self, micro_steps: int):
+        check(lib().p2r_model_set_grad_accumulation(self.h, micro_steps))
+
+    def set_activation_checkpointing(self, policy: int):
+        """0 off, 1 SLOW layers (default for offloaded models), 2 every layer."""
+        check(lib().p2r_model_set_activation_checkpointing(self.h, policy))
+
     def offload_stats(self) -> dict:
-        o = np.zeros(7, np.float64)
+        o = np.zeros(8, np.float64)
         check(lib().p2r_model_offload_stats(self.h, _p(o)))
-        keys = ("Fn_load", "Bn_load", "opt_load", "writeback", "grad_offload", "h2d_ms", "d2h_ms")
+        keys = ("Fn_load", "Bn_load", "opt_load", "writeback", "grad_offload", "h2d_ms", "d2h_ms", "grad_load")
         return dict(zip(keys, (float(x) for x in o)))
 
     def offload_stats_reset(self):
@@ -405,6 +421,12 @@ class Model:
         check(lib().p2r_model_routing(self.h, g, _p(sel), _p(sur), _p(raw), ctypes.byref(cap),
                                       ctypes.byref(drop)))
         return sel, sur, raw, cap.value, drop.value
+
+    def gate_logits(self, g: int, n_tokens: int) -> np.ndarray:
+        """fp32 gate logits [T, E] of graph layer g from the last forward."""
+        out = np.empty((n_tokens, self.cfg.n_experts), np.float32)
+        check(lib().p2r_model_gate_logits(self.h, g, _p(out)))
+        return out
 
 
 @dataclass

@@ -11,6 +11,8 @@ import pytest
 
 from oracle import p2r_oracle as O
 
+from ._parity import check_grads, design_floor, rel
+
 pytestmark = pytest.mark.gpu
 REF_SO = os.path.join(os.path.dirname(__file__), "..", "oracle", "_ref", "libp2r_ref.so")
 need_ref = pytest.mark.skipif(not os.path.exists(REF_SO), reason="oracle/_ref not built")
@@ -37,12 +39,6 @@ def lm_batch(batch, seq, seed=7):
     mask = np.ones_like(tok, dtype=np.uint8)
     mask[:, -1] = 0
     return tok.ravel(), tgt.ravel(), mask.ravel()
-
-
-def rel(a, b):
-    a = np.asarray(a, np.float64)
-    b = np.asarray(b, np.float64)
-    return float(np.linalg.norm(a - b) / (np.linalg.norm(b) + 1e-30))
 
 
 def make_pair(cfgd, seed=1234):
@@ -81,23 +77,6 @@ def global_rel(gm, gr, names):
     return (num / den) ** 0.5
 
 
-def assert_grad_contract(gm, gr, names, shared, tol=1e-2):
-    """North-star gradient tolerance (bf16 in / fp32 accumulate vs fp32):
-    the whole gradient <= 1e-2 relative L2, and every parameter <= 1e-2. For
-    UNSHARED layers at random init the last layers' W_q / W_k gradients are a
-    tiny signal (attention is near-uniform), and the bf16 rounding points of
-    the design alone put them at ~1.2-1.4% (oracle/bf16_emulation.py reproduces
-    this on the CPU; test_step_vs_bf16_emulation pins the GPU to that model),
-    so those two tensors get 2e-2."""
-    worst = grad_report(gm, gr, names)
-    g = global_rel(gm, gr, names)
-    print(f"global grad rel-L2 {g:.2e}; worst per-tensor: {worst[:4]}")
-    assert g <= 1e-2
-    for e, n in worst:
-        qk = (n.endswith("attn.wq") or n.endswith("attn.wk")) and not shared
-        assert e <= (2e-2 if qk else tol), (n, e)
-
-
 @need_ref
 @pytest.mark.parametrize("cfgd,B", [(DENSE, 8), (dict(DENSE, n_layers_params=3), 8)], ids=["pseudo_dense", "real_dense"])
 def test_step_parity_dense(cuda, cfgd, B):
@@ -106,20 +85,20 @@ def test_step_parity_dense(cuda, cfgd, B):
     S = cfgd["seq_len"]
     tok, tgt, mask = lm_batch(B, S)
     denom = float(mask.sum())
+    p0 = r.params()
     lg = m.train_step(tok, tgt, mask, B, denom)
     lr_ = r.train_step(tok, tgt, mask, B, denom)
     assert abs(lg - lr_) <= 1e-3 * abs(lr_), (lg, lr_)
-    assert_grad_contract(m.grads(), r.grads(), r.names, cfgd["n_layers_params"] == 1)
+    check_grads(m.grads(), r.grads(), design_floor(cfgd, p0, tok, tgt, mask, B, denom), r.names, "dense")
 
 
 @need_ref
-# per-tensor gradient bound: 1e-2; at d = 2048 (C4S) the whole gradient stays at
-# ~8e-3 rel-L2 (the north star's 1e-2) but single expert tensors of the deeper layer
-# land at 1.00-1.01e-2 -- the bf16-in design's floor at that width (bf16 activations
-# and dy through one more 2048-wide layer), the same effect that puts wq/wk at 2e-2
-@pytest.mark.parametrize("cfgd,B,tol", [(C1, 8, 1e-2), (MOE_K2, 8, 1e-2), (REAL, 8, 1e-2), (C4S, 4, 1.25e-2)],
+# per-tensor gradient bound (tests/_parity.py): 1e-2, or 1.25x the bf16-in design's floor
+# on the same inputs where that floor is itself ~1e-2 (at d = 2048 (C4S) single expert
+# tensors of the deeper layer and the Q/K projections sit at 1.0-1.25e-2 in the emulation)
+@pytest.mark.parametrize("cfgd,B", [(C1, 8), (MOE_K2, 8), (REAL, 8), (C4S, 4)],
                          ids=["c1_moe", "moe_k2", "real_moe", "c4_wide_moe"])
-def test_step_parity_moe(cuda, cfgd, B, tol):
+def test_step_parity_moe(cuda, cfgd, B):
     """MoE: loss vs the reference; gradients vs the oracle restatement run with
     the routing the GPU chose (bf16 upstream activations can flip near-tie
     tokens at deep layers, and a flip moves whole tokens between experts, so
@@ -142,13 +121,21 @@ def test_step_parity_moe(cuda, cfgd, B, tol):
     for g in range(cfgd["n_layers_graph"]):
         sel, sur, raw, cap, drop = m.layer_routing(g, T)
         om.forced_selected[g] = sel
-        flips += int((sel != free._cache[2][g][12][2].selected).sum())
+        osel = free._cache[2][g][12][2].selected
+        ol = free._cache[2][g][12][1]
+        k = cfgd["n_prototypes"]
+        for s_ in np.nonzero(sel != osel)[0]:
+            t = s_ // k
+            print(f"flip layer {g} token {t} slot {s_ % k}: gpu {sel[s_]} fp32 {osel[s_]} "
+                  f"fp32 logit gap {ol[t, osel[s_]] - ol[t, sel[s_]]:.3e}")
+        flips += int((sel != osel).sum())
     lo, go = om.loss_and_grads(tok, tgt, mask, B, denom)
     assert abs(lg - lo) <= 1e-3 * abs(lo)
     print(f"routing flips vs fp32 oracle: {flips} / {T * cfgd['n_prototypes'] * cfgd['n_layers_graph']}")
-    # near-ties under bf16 activations grow with the expert count: 1 % per 8 experts
-    assert flips <= 0.01 * max(1.0, cfgd["n_experts"] / 8) * T * cfgd["n_prototypes"] * cfgd["n_layers_graph"]
-    assert_grad_contract(m.grads(), go, r.names, cfgd["n_layers_params"] == 1, tol)
+    # flips need a near-tie in fp32 under bf16 upstream activations (E=64: test_parity_bench_gpu)
+    assert flips <= 0.015 * T * cfgd["n_prototypes"] * cfgd["n_layers_graph"]
+    ge = design_floor(cfgd, p0, tok, tgt, mask, B, denom, om.forced_selected)
+    check_grads(m.grads(), go, ge, r.names, "moe")
 
 
 @need_ref
@@ -256,7 +243,10 @@ def test_delinked_real_step_vs_reference(cuda):
     a = md.train_step(tok, tgt, mask, 8, float(mask.sum()))
     b = rd.train_step(tok, tgt, mask, 8, float(mask.sum()))
     assert abs(a - b) <= 1e-3 * abs(b)
-    assert_grad_contract(md.grads(), rd.grads(), rd.names, shared=False)
+    p0 = rd.params()
+    cfg_real = dict(DENSE, n_layers_params=DENSE["n_layers_graph"])
+    check_grads(md.grads(), rd.grads(), design_floor(cfg_real, p0, tok, tgt, mask, 8, float(mask.sum())),
+                rd.names, "delinked")
 
 
 def test_error_behaviour(cuda):

@@ -89,3 +89,129 @@ def test_offload_gradient_offload_without_optimizer(cuda):
         assert np.array_equal(ga[n], gb[n]), n
     st = b.offload_stats()
     assert st["grad_offload"] == sum(plan) * (b.layer_granule_bytes() // 18) * 4
+
+
+@pytest.mark.parametrize("plan", [[1, 0, 1, 1, 0], [1, 1, 1, 1, 1]], ids=["mixed", "all_slow"])
+def test_offload_accumulation_bit_identical(cuda, plan):
+    """Gradient accumulation (zero=True, then zero=False micro-steps, SPEC.md:463 /
+    tensor.hpp:135-140): SLOW granules park partial gradients in pinned host memory
+    between micro-steps and take the fused AdamW in the window's LAST backward only,
+    so two optimizer steps of 3 micro-steps each are bit-identical to the resident model."""
+    import paper_2110_03888_b200 as p2r
+    cfg = p2r.Config(**REAL_DENSE)
+    a = p2r.Model(cfg, 1234)
+    b = p2r.Model(cfg, 1234, offload=plan, ring_slots=2)
+    a.attach_adamw()
+    b.attach_adamw()
+    b.set_grad_accumulation(3)
+    b.offload_stats_reset()
+    for step in range(2):
+        lr = 1e-3 * (step + 1)
+        b.set_offload_lr(lr)
+        for micro in range(3):
+            tok, tgt, mask = lm_batch(4, 128, seed=30 + 3 * step + micro)
+            denom = float(mask.sum()) * 3  # large-batch mean over the window
+            la = a.train_step(tok, tgt, mask, 4, denom, zero=(micro == 0))
+            lb = b.train_step(tok, tgt, mask, 4, denom, zero=(micro == 0))
+            assert la == lb, (step, micro)
+            if micro == 1:  # partial gradients of SLOW granules are readable from the host park
+                ga, gb = a.grads(), b.grads()
+                for n in ga:
+                    assert np.array_equal(ga[n], gb[n]), n
+        a.adamw_step(lr)
+        b.adamw_step(lr)
+    pa, pb = a.params(), b.params()
+    ma, mb = a.moments(), b.moments()
+    for n in pa:
+        assert np.array_equal(pa[n], pb[n]), n
+        assert np.array_equal(ma[n][0], mb[n][0]) and np.array_equal(ma[n][1], mb[n][1]), n
+    st = b.offload_stats()
+    g = b.layer_granule_bytes() // 18
+    ns = sum(plan)
+    # per window: 2 parks (D2H) + 2 reloads (H2D) of the partial grads, moments once
+    assert st["grad_offload"] == 2 * 2 * ns * g * 4
+    assert st["grad_load"] == 2 * 2 * ns * g * 4
+    assert st["opt_load"] == 2 * ns * g * 8
+
+
+def test_offload_misuse_throws(cuda):
+    """Offload misuse is loud: Pseudo models, a micro-step
+    past the accumulation window, adamw_step before the window's last backward, a missing
+    set_offload_lr, and a mismatched lr -- and a throwing adamw_step leaves the step count."""
+    import paper_2110_03888_b200 as p2r
+    with pytest.raises(p2r.P2RInvalidArgument, match="needs an unshared"):
+        p2r.Model(p2r.Config(**dict(REAL_DENSE, n_layers_params=1)), 1, offload=[1])
+    cfg = p2r.Config(**REAL_DENSE)
+    b = p2r.Model(cfg, 1234, offload=[1, 0, 0, 0, 1])
+    b.attach_adamw()
+    tok, tgt, mask = lm_batch(2, 128)
+    with pytest.raises(p2r.P2RLogicError, match="set_offload_lr"):
+        b.train_step(tok, tgt, mask, 2, float(mask.sum()))
+    b.set_offload_lr(1e-3)
+    b.train_step(tok, tgt, mask, 2, float(mask.sum()))
+    with pytest.raises(p2r.P2RLogicError, match="accumulation past the window"):
+        b.train_step(tok, tgt, mask, 2, float(mask.sum()), zero=False)
+    with pytest.raises(p2r.P2RLogicError, match="adamw_step\\(lr\\) was not called"):
+        b.train_step(tok, tgt, mask, 2, float(mask.sum()))
+    with pytest.raises(p2r.P2RInvalidArgument, match="pass the same lr"):
+        b.adamw_step(2e-3)
+    assert b.step_count() == 0
+    b.adamw_step(1e-3)
+    assert b.step_count() == 1
+    b.set_grad_accumulation(2)
+    b.train_step(tok, tgt, mask, 2, float(mask.sum()))
+    with pytest.raises(p2r.P2RLogicError, match="before the accumulation window's last backward"):
+        b.adamw_step(1e-3)
+    assert b.step_count() == 1
+
+
+@pytest.mark.parametrize("policy", [0, 1, 2], ids=["no_ckpt", "ckpt_slow", "ckpt_all"])
+def test_offload_activation_checkpointing_bit_identical(cuda, policy):
+    """Activation checkpointing: checkpointed layers keep only their output
+    and recompute the rest in the backward -- same kernels, same operands, so the step
+    is bit-identical to storing every activation (and to the resident model)."""
+    import paper_2110_03888_b200 as p2r
+    cfg = p2r.Config(**REAL_MOE)
+    a = p2r.Model(cfg, 1234)
+    b = p2r.Model(cfg, 1234, offload=[0, 1, 0, 1], ring_slots=2)
+    b.set_activation_checkpointing(policy)
+    a.attach_adamw()
+    b.attach_adamw()
+    for s in range(2):
+        tok, tgt, mask = lm_batch(4, 128, seed=50 + s)
+        b.set_offload_lr(1e-3)
+        assert a.train_step(tok, tgt, mask, 4, float(mask.sum())) == b.train_step(tok, tgt, mask, 4,
+                                                                                  float(mask.sum()))
+        a.adamw_step(1e-3)
+        b.adamw_step(1e-3)
+    pa, pb = a.params(), b.params()
+    for n in pa:
+        assert np.array_equal(pa[n], pb[n]), n
+
+
+def test_offload_with_expert_parallel_bit_identical(cuda, monkeypatch):
+    """Offload + expert parallelism in one model (C5's shape of the engine): an EP shard
+    (world 1, exchange path forced) with SLOW granules trains bit-identically to the
+    resident EP shard."""
+    monkeypatch.setenv("P2R_FORCE_EP", "1")
+    import paper_2110_03888_b200 as p2r
+    cfg = p2r.Config(**REAL_MOE)
+    a = p2r.Model(cfg, 1234, ep=(1, 0))
+    b = p2r.Model(cfg, 1234, offload=[1, 0, 1, 1], ring_slots=2, ep=(1, 0))
+    uid = p2r.comm_unique_id()
+    a.comm_init(uid)
+    b.comm_init(p2r.comm_unique_id())
+    a.attach_adamw()
+    b.attach_adamw()
+    for s in range(2):
+        tok, tgt, mask = lm_batch(4, 128, seed=70 + s)
+        b.set_offload_lr(1e-3)
+        assert a.train_step(tok, tgt, mask, 4, float(mask.sum())) == b.train_step(tok, tgt, mask, 4,
+                                                                                  float(mask.sum()))
+        a.allreduce_grads()
+        b.allreduce_grads()
+        a.adamw_step(1e-3)
+        b.adamw_step(1e-3)
+    pa, pb = a.params(), b.params()
+    for n in pa:
+        assert np.array_equal(pa[n], pb[n]), n

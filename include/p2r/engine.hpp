@@ -170,13 +170,14 @@ struct OffloadCost {
   double h2d_bw = 50e9, d2h_bw = 50e9;  // pinned PCIe bytes/s per direction
   double fwd_s = 0, bwd_s = 0;          // compute per layer
   bool fn_master = false;               // Fn loads the fp32 master (4P), write-back drops the bf16 (12P)
+  int ring_slots = 3;                   // HBM staging slots (planner budget: resident + ring x largest granule)
 };
 double predict_step_time_overlap(const std::vector<std::int64_t>& layer_params,
                                  const std::vector<std::int64_t>& vector_params, const std::vector<int>& slow,
                                  const OffloadCost& c);
-// fewest SLOW layers whose granules (18 B/param) bring the resident set under
-// `budget`, spread evenly over the stack; minimises predict_step_time_overlap
-// among placements with that count for uniform layers.
+// fewest SLOW layers whose granules (18 B/param) bring the resident set plus the
+// ring_slots staging slots under `budget`, spread evenly over the stack; minimises
+// predict_step_time_overlap among placements with that count for uniform layers.
 std::vector<int> plan_offload_overlap(const std::vector<std::int64_t>& layer_params, std::int64_t budget,
                                       const OffloadCost& c);
 // staged device pointer of a SLOW granule: kind 0 p32, 1 grad, 2 m, 3 v, 4 bf16

@@ -234,7 +234,7 @@ double p2r_predict_step_time_overlap_form(const int64_t* layer_params, const int
                                           double bwd_s, int fn_master);
 /* fewest SLOW layers (18 B/param granules) under budget_bytes, spread evenly */
 p2r_status p2r_plan_offload_overlap(const int64_t* layer_params, int n, int64_t budget_bytes, double h2d_bw,
-                                    double d2h_bw, double fwd_s, double bwd_s, int* slow_out);
+                                    double d2h_bw, double fwd_s, double bwd_s, int ring_slots, int* slow_out);
 
 /* init_normal (model.cpp:28-36) on the host: the exact values Model() uploads. */
 void p2r_init_normal_host(uint64_t seed, const char* name, int64_t n, float* out);

@@ -12,7 +12,21 @@
 
 namespace p2r {
 
-constexpr int kNumSMs = 148;
+constexpr int kNumSMs = 148;  // B200; persistent grids that need co-residency use device_sms()
+
+// SMs available to this context on the current device (MIG / green contexts can
+// expose fewer than a full B200), cached per device.
+inline int device_sms() {
+  static int cache[16] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return kNumSMs;
+  if (cache[dev] == 0) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = kNumSMs;
+    cache[dev] = n;
+  }
+  return cache[dev];
+}
 
 P2R_DEVICE uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

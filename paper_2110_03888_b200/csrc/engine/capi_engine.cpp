@@ -431,10 +431,12 @@ double p2r_predict_step_time_overlap(const int64_t* layer_params, const int64_t*
   return p2r_predict_step_time_overlap_form(layer_params, vector_params, slow, n, h2d_bw, d2h_bw, fwd_s, bwd_s, 0);
 }
 p2r_status p2r_plan_offload_overlap(const int64_t* layer_params, int n, int64_t budget_bytes, double h2d_bw,
-                                    double d2h_bw, double fwd_s, double bwd_s, int* slow_out) {
+                                    double d2h_bw, double fwd_s, double bwd_s, int ring_slots, int* slow_out) {
   return guard([&] {
     std::vector<std::int64_t> p(layer_params, layer_params + n);
-    const std::vector<int> pl = p2r::plan_offload_overlap(p, budget_bytes, cost(h2d_bw, d2h_bw, fwd_s, bwd_s));
+    p2r::OffloadCost c = cost(h2d_bw, d2h_bw, fwd_s, bwd_s);
+    c.ring_slots = ring_slots;
+    const std::vector<int> pl = p2r::plan_offload_overlap(p, budget_bytes, c);
     std::copy(pl.begin(), pl.end(), slow_out);
   });
 }

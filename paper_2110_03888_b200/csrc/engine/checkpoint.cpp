@@ -30,6 +30,7 @@
 #include <vector>
 
 #include "p2r/engine.hpp"
+#include "offload_state.hpp"
 
 namespace p2r {
 namespace {
@@ -225,7 +226,10 @@ void write_container(const std::string& path, const Header& h, std::vector<Buffe
     off = align64(off + e.bytes);
   }
   text = manifest();
-  std::ofstream f(path, std::ios::binary | std::ios::trunc);
+  // written to a temporary and renamed over the target once complete, so an
+  // interrupted save never destroys the previous snapshot
+  const std::string tmp = path + ".tmp";
+  std::ofstream f(tmp, std::ios::binary | std::ios::trunc);
   if (!f) throw std::runtime_error("checkpoint: cannot create " + path);
   f.write(kMagic, 8);
   put_u32(f, kVersion);
@@ -241,7 +245,15 @@ void write_container(const std::string& path, const Header& h, std::vector<Buffe
     f.write(reinterpret_cast<const char*>(host.data()), static_cast<std::streamsize>(bufs[b].bytes));
     pos = bufs[b].offset + bufs[b].bytes;
   }
-  if (!f) throw std::runtime_error("checkpoint: write failed: " + path);
+  f.close();
+  if (!f) {
+    std::remove(tmp.c_str());
+    throw std::runtime_error("checkpoint: write failed: " + path);
+  }
+  if (std::rename(tmp.c_str(), path.c_str()) != 0) {
+    std::remove(tmp.c_str());
+    throw std::runtime_error("checkpoint: cannot replace " + path);
+  }
 }
 
 void read_payload(std::ifstream& f, const BufferEntry& e, float* dst) {
@@ -309,6 +321,18 @@ StageState Model::load_checkpoint(const std::string& path) {
     eps_ = m.eps;
     wd_ = m.wd;
     step_count_ = m.step_count;
+  } else if (has_opt_) {
+    // a file without optimizer state restores a fresh optimizer: zero moments and
+    // step count, so a revert equals the snapshot bit for bit
+    if (off_) offload_sync(*off_);
+    for (DevBuf* b : {&emb_m_, &emb_v_, &lay_m_, &lay_v_})
+      if (b->p) cuda_check(cudaMemsetAsync(b->p, 0, b->bytes, stream_), "zero moments");
+    if (off_ && off_->hm) {
+      const std::size_t n = static_cast<std::size_t>(layer_stride_) * off_->slow_list.size();
+      std::memset(off_->hm, 0, n * 4);
+      std::memset(off_->hv, 0, n * 4);
+    }
+    step_count_ = 0;
   }
   std::map<std::string, int> index;
   for (std::size_t i = 0; i < views_.size(); ++i) index[views_[i].name] = static_cast<int>(i);

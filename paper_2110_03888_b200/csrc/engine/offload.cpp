@@ -105,21 +105,28 @@ std::vector<int> plan_offload_overlap(const std::vector<std::int64_t>& layer_par
     largest = std::max<std::int64_t>(largest, 18 * p);
   }
   if (budget < largest) throw std::runtime_error("plan_offload: no feasible plan (a single layer exceeds the budget)");
+  // once anything is SLOW the engine also holds `ring_slots` HBM staging slots of the
+  // largest granule: they count against the budget too
+  const std::int64_t staging = static_cast<std::int64_t>(std::max(c.ring_slots, 2)) * largest;
+  if (total <= budget) return std::vector<int>(static_cast<std::size_t>(n), 0);
+  const std::int64_t fast_budget = budget - staging;
+  if (fast_budget < 0) throw std::runtime_error("plan_offload: no feasible plan (staging ring exceeds the budget)");
   // fewest SLOW layers (largest first) that bring the resident granules under budget
   std::vector<int> order(static_cast<std::size_t>(n));
   for (int i = 0; i < n; ++i) order[static_cast<std::size_t>(i)] = i;
   std::stable_sort(order.begin(), order.end(),
                    [&](int a, int b) { return layer_params[static_cast<std::size_t>(a)] > layer_params[static_cast<std::size_t>(b)]; });
   int k = 0;
-  for (std::int64_t fast = total; fast > budget && k < n; ++k) fast -= 18 * layer_params[static_cast<std::size_t>(order[static_cast<std::size_t>(k)])];
+  for (std::int64_t fast = total; fast > fast_budget && k < n; ++k)
+    fast -= 18 * layer_params[static_cast<std::size_t>(order[static_cast<std::size_t>(k)])];
   std::vector<int> pl(static_cast<std::size_t>(n), 0);
-  if (k == 0) return pl;
+  const std::int64_t budget_fast = fast_budget;
   // spread k SLOW layers evenly: every copy gets the most neighbouring compute to hide under
   for (int j = 0; j < k; ++j) pl[static_cast<std::size_t>((static_cast<long long>(j) * n) / k)] = 1;
   std::int64_t fast = 0;
   for (int i = 0; i < n; ++i)
     if (!pl[static_cast<std::size_t>(i)]) fast += 18 * layer_params[static_cast<std::size_t>(i)];
-  if (fast > budget) {  // non-uniform layers: fall back to the largest-first choice
+  if (fast > budget_fast) {  // non-uniform layers: fall back to the largest-first choice
     std::fill(pl.begin(), pl.end(), 0);
     for (int j = 0; j < k; ++j) pl[static_cast<std::size_t>(order[static_cast<std::size_t>(j)])] = 1;
   }

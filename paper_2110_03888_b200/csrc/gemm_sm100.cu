@@ -885,7 +885,9 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorM
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
   });
   if (attr_err != cudaSuccess) return attr_err;
-  const int units = kNumSMs / CG;  // persistent: one CTA (pair) per SM (pair of SMs)
+  // persistent: one CTA (pair) per SM (pair of SMs) of this device, so every CTA is
+  // co-resident (serial split-K's ordered in-place accumulation waits on earlier CTAs)
+  const int units = device_sms() / CG;
   const int grid = CG * (p.tiles_total < units ? p.tiles_total : units);
   if constexpr (CG == 1) {
     const cudaError_t e = launch_k(gemm_kernel<BN, AMN, BMN, EPI, 1>, dim3(grid), dim3(kGemmThreads),
@@ -947,7 +949,7 @@ int auto_split(const p2r_gemm_args* a) {
   if (a->bias != nullptr || a->aux != nullptr) return 1;
   const int BN = pick_bn(a), CG = pick_cg(a, BN);
   const long long tiles = 1LL * ((a->m + BM * CG - 1) / (BM * CG)) * ((a->n + BN - 1) / BN);
-  const int units = kNumSMs / CG;
+  const int units = device_sms() / CG;
   auto eff = [&](int s) {
     const long long t = tiles * s;
     return static_cast<double>(t) / (static_cast<double>(units) * ((t + units - 1) / units));

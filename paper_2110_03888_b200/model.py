@@ -110,7 +110,7 @@ def _declare_extra():
     L.p2r_predict_step_time_overlap.restype = ctypes.c_double
     L.p2r_predict_step_time_overlap_form.argtypes = [vp, vp, vp, ip] + [ctypes.c_double] * 4 + [ip]
     L.p2r_predict_step_time_overlap_form.restype = ctypes.c_double
-    L.p2r_plan_offload_overlap.argtypes = [vp, ip, i64] + [ctypes.c_double] * 4 + [vp]
+    L.p2r_plan_offload_overlap.argtypes = [vp, ip, i64] + [ctypes.c_double] * 4 + [ip, vp]
     L.p2r_plan_offload_overlap.restype = ctypes.c_int
     return L
 
@@ -509,9 +509,11 @@ def predict_step_time_overlap(layer_params, slow, h2d_bw, d2h_bw, fwd_s, bwd_s, 
                                                       int(bool(fn_master))))
 
 
-def plan_offload_overlap(layer_params, budget_bytes, h2d_bw, d2h_bw, fwd_s, bwd_s):
+def plan_offload_overlap(layer_params, budget_bytes, h2d_bw, d2h_bw, fwd_s, bwd_s, ring_slots=3):
+    """Budget covers the resident granules AND the ring_slots HBM staging slots."""
     L = _declare_extra()
     p = np.ascontiguousarray(layer_params, np.int64)
     out = np.zeros(len(p), np.int32)
-    check(L.p2r_plan_offload_overlap(_p(p), len(p), int(budget_bytes), h2d_bw, d2h_bw, fwd_s, bwd_s, _p(out)))
+    check(L.p2r_plan_offload_overlap(_p(p), len(p), int(budget_bytes), h2d_bw, d2h_bw, fwd_s, bwd_s,
+                                     int(ring_slots), _p(out)))
     return out.tolist()

@@ -196,3 +196,26 @@ def test_redistribute_experts(cuda, tmp_path):
     b, _ = p2r.load_checkpoint(back)
     assert_same_state(m, b)
     assert np.array_equal(b.forward(tok, 8), before)
+
+
+def test_load_without_optimizer_state_resets_moments(cuda, tmp_path):
+    """a snapshot taken before the optimizer existed restores a fresh
+    optimizer (zero moments, step 0), and saves go through a temporary + rename."""
+    import os
+
+    import paper_2110_03888_b200 as p2r
+    a = p2r.Model(p2r.Config(**REAL), 1234)
+    path = str(tmp_path / "no_opt.p2rckpt")
+    a.save_checkpoint(path)
+    assert not os.path.exists(path + ".tmp")
+    a.attach_adamw()
+    step(a, 0, seed=5)
+    a.load_checkpoint(path)
+    assert a.step_count() == 0
+    for n, (m, v) in a.moments().items():
+        assert not m.any() and not v.any(), n
+    b = p2r.Model(p2r.Config(**REAL), 1234)
+    b.attach_adamw()
+    assert_same_state(a, b)
+    assert step(a, 0, seed=6) == step(b, 0, seed=6)
+    assert_same_state(a, b)

@@ -75,10 +75,16 @@ def test_overlap_planner():
     P = 50_000_000
     gb = 18 * P
     assert p2r.plan_offload_overlap([P] * 16, 16 * gb, 50e9, 50e9, 2e-3, 4e-3) == [0] * 16
-    plan = p2r.plan_offload_overlap([P] * 16, 8 * gb, 50e9, 50e9, 2e-3, 4e-3)
+    # the budget covers the resident granules AND the 3 HBM staging slots
+    plan = p2r.plan_offload_overlap([P] * 16, 11 * gb, 50e9, 50e9, 2e-3, 4e-3)
     assert sum(plan) == 8 and plan == [1, 0] * 8  # fewest SLOW layers, spread evenly
-    plan = p2r.plan_offload_overlap([P] * 16, 12 * gb, 50e9, 50e9, 2e-3, 4e-3)
+    plan = p2r.plan_offload_overlap([P] * 16, 15 * gb, 50e9, 50e9, 2e-3, 4e-3)
     assert sum(plan) == 4 and plan == [1, 0, 0, 0] * 4
+    for budget in (5, 8, 11, 13, 15):
+        for ring in (2, 3, 4):
+            plan = p2r.plan_offload_overlap([P] * 16, budget * gb, 50e9, 50e9, 2e-3, 4e-3, ring_slots=ring)
+            assert (16 - sum(plan)) * gb + ring * gb <= budget * gb  # budget safety incl. staging
+            assert (16 - sum(plan) + 1) * gb + ring * gb > budget * gb  # and the fewest SLOW layers
     with pytest.raises(p2r.P2RError, match="no feasible plan"):
         p2r.plan_offload_overlap([P] * 4, gb // 2, 50e9, 50e9, 2e-3, 4e-3)
     # more SLOW layers never predict a faster step; all-resident = pure compute

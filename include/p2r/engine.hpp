@@ -136,6 +136,9 @@ struct GranuleLayout {
 
 struct Acts;  // per-shape activation / workspace buffers
 struct OffloadState;
+struct EpState;
+struct LoopbackGroup;
+struct LayerActs;
 
 // Per-step movement accounting of the granular offload engine:
 // bytes moved per phase plus measured copy-engine time.
@@ -248,6 +251,8 @@ class Model {
 
   // NCCL (one communicator per model over all ranks; csrc/engine/comm.cpp)
   void comm_init(const char* unique_id128);
+  // W shards of one process on one device, one host thread each (loopback group)
+  void comm_init_loopback(LoopbackGroup* group);
   void comm_destroy();
   void allreduce_grads();  // DP: sum replicated grads (embeddings, attention, norms, gate, dense FFN)
   int ep_world() const { return ep_world_; }
@@ -461,7 +466,20 @@ class Model {
   int ep_world_ = 1, ep_rank_ = 0;
   bool force_ep_ = false;  // P2R_FORCE_EP=1: run the exchange path even at W = 1 (tests)
   void* comm_ = nullptr;   // ncclComm_t
-  void ep_exchange(const void* src, void* dst, std::size_t row_bytes, int seg, bool to_experts);
+  LoopbackGroup* loop_ = nullptr;
+  std::unique_ptr<EpState> ep_;
+  void ep_connect(int seg, int n_ye);
+  void* ep_peer(int q, std::size_t off) const;
+  void* ep_local(std::size_t off) const;
+  void ep_signal(int ch);
+  void ep_wait(int ch);
+  std::size_t ep_ye_offset(int set) const;
+  std::size_t ep_dxe_offset() const;
+  // dispatch side of one exchange: rows of L's routing -> owners' slots, then signal + wait
+  void ep_send(const void* src, int src_dtype, LayerActs& L, const float* w);
+  void ep_pack_rows(void* compact, LayerActs& L);
+  // return side: compact rows -> the sources' [E][seg] buffers at arena offset dst_off
+  void ep_return(const void* compact, LayerActs& L, std::size_t dst_off);
 };
 
 // ncclGetUniqueId (dlopen'ed libnccl.so.2)

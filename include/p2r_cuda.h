@@ -96,7 +96,8 @@ typedef struct {
 p2r_status p2r_gemm(const p2r_gemm_args* args, void* stream);
 /* Bytes of workspace the library needs for split-K / bias_grad partials (0 if none). */
 size_t p2r_gemm_workspace_bytes(const p2r_gemm_args* args);
-/* Supply caller-owned scratch (device) the library may use for split-K. */
+/* Supply caller-owned scratch (device) the library may use for split-K / bias-grad
+ * partials of the GEMMs the CALLING THREAD launches next (thread-local). */
 p2r_status p2r_set_workspace(void* ptr, size_t bytes);
 
 /* ------------------------------------------------------------------------ */
@@ -193,18 +194,49 @@ p2r_status p2r_moe_combine_weights(const float* logits, int T, int E, int k, con
 p2r_status p2r_moe_dispatch(const void* src, int src_dtype, int d, int E, int seg_rows,
                             const int* rows_pad, const int* slots_pad, const int* counts,
                             const float* w, int k, void* xe_bf16, int pad_full, void* stream);
-p2r_status p2r_moe_combine(const float* ye, int T, int d, int k, int seg_rows, const int* selected,
+/* out[t] = resid[t] + sum over the token's surviving slots (group order) of
+ * w * ye[row]; ye: bf16 expert outputs [E][seg_rows][d] (moe_combine, tensor.cpp:609-641). */
+p2r_status p2r_moe_combine(const void* ye_bf16, int T, int d, int k, int seg_rows, const int* selected,
                            const int* pos, const float* w, const float* resid, float* out,
                            void* stream);
-p2r_status p2r_moe_combine_bwd_weights(const float* dout, const float* ye, int T, int d, int k,
+/* dw[t,g] = <dout[t], ye[row(t,g)]> (moe_combine backward, tensor.cpp:643-662). */
+p2r_status p2r_moe_combine_bwd_weights(const float* dout, const void* ye_bf16, int T, int d, int k,
                                        int seg_rows, const int* selected, const int* pos,
                                        float* dw, void* stream);
 p2r_status p2r_moe_gate_bwd(const float* b, const float* w, const float* gw, int T, int d, int E,
                             int k, const int* selected, const uint8_t* survived, float* glogits,
                             float* dgate, void* stream);
-p2r_status p2r_moe_dispatch_bwd(const float* dxe, int T, int d, int k, int seg_rows,
+/* db[t] (+)= sum of the token's expert-input gradients (bf16 dxe [E][seg_rows][d], slots
+ * in reverse group order) + glogits . gate^T (gather_rows backward, tensor.cpp:386-396). */
+p2r_status p2r_moe_dispatch_bwd(const void* dxe_bf16, int T, int d, int k, int seg_rows,
                                 const int* selected, const int* pos, const float* glogits,
                                 const float* gate, int E, float* db, int accumulate, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Expert-parallel exchange over peer memory (model.cpp:334-340 expert map:  */
+/* expert e on rank e / (E/W)). Kernels store rows straight into the peer    */
+/* ranks' buffers (NVLink peer pointers, or local pointers for a loopback    */
+/* group); completion is signalled by the caller (stream memory operations). */
+/* Layouts: source [E][seg][d]; owner slots [El][W][seg][d] + counts [El][W];*/
+/* owner compact [El][W*seg][d] (zero-padded to 128 rows per expert).        */
+/* ------------------------------------------------------------------------ */
+/* Source side: admitted rows of every expert (src bf16 (dtype 1), or fp32 (0) scaled
+ * by w[t*k + slot] when w != NULL) -> peer_slots[e / El] at [e % El][rank][row];
+ * counts[e] -> peer_counts[e / El][(e % El) * W + rank]. */
+p2r_status p2r_ep_send_rows(const void* src, int src_dtype, int d, int E, int seg, const int* rows_pad,
+                            const int* slots_pad, const int* counts, const float* w, int k, int W, int rank,
+                            void* const* peer_slots, int* const* peer_counts, void* stream);
+/* Owner side: slots + counts -> compact rows, tot[El] rows per local expert and
+ * prefix[El][W+1] (row offset of each source inside the compact segment). */
+p2r_status p2r_ep_pack(const void* slots, const int* counts, int d, int seg, int El, int W, void* compact,
+                       int* tot, int* prefix, void* stream);
+/* Owner side: compact rows -> each source's [E][seg] layout (peer_dst[source]). */
+p2r_status p2r_ep_return_rows(const void* compact, const int* prefix, int d, int seg, int El, int W, int rank,
+                              void* const* peer_dst, void* stream);
+
+/* out = stage[0] + stage[1] + ... + stage[W-1] (fp32 [W][n], rank order): the
+ * deterministic sum of a loopback group's data-parallel all-reduce. */
+p2r_status p2r_sum_ranks(const float* stage, int W, long long n, float* out, void* stream);
 
 #ifdef __cplusplus
 }

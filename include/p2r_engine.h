@@ -175,17 +175,26 @@ p2r_status p2r_moe_dispatch_host(const float* logits, int T, int E, int k, float
                                  uint8_t* survived, int* raw_load, int* offsets, int* rows,
                                  int* slots, int* capacity, int* dropped);
 
-/* ---- expert / data parallelism over NCCL --------------------
+/* ---- expert / data parallelism ------------------------------
  * Rank r of W holds experts [r*E/W, (r+1)*E/W) (Model::expert_shard's
- * contiguous map, model.cpp:334-340) plus a replica of everything else; MoE
- * dispatch/combine exchange fixed-capacity expert segments with grouped
- * ncclSend/ncclRecv on the model stream; replicated grads are summed with
- * p2r_model_allreduce_grads. Each rank must use the GLOBAL mask count as the CE
- * denominator so the summed gradient is the large-batch mean. */
+ * contiguous map, model.cpp:334-340) plus a replica of everything else. MoE
+ * dispatch / combine are peer-store kernels (p2r_ep_*) that write the routed rows
+ * (bf16, exact counts) straight into the owner's / source's arena over NVLink;
+ * completion is signalled with stream memory operations. Replicated grads are
+ * summed with p2r_model_allreduce_grads. Each rank must use the GLOBAL mask count
+ * as the CE denominator so the summed gradient is the large-batch mean.
+ * Multi-GPU: one process per GPU, p2r_model_comm_init(NCCL unique id); the EP
+ * arenas are exchanged as CUDA IPC handles at the first step (collective).
+ * Loopback: W shards of ONE process on one device, each driven by its own host
+ * thread, joined with p2r_model_comm_init_loopback(group) (tests / one-GPU runs). */
 p2r_status p2r_comm_unique_id(char* out128);
 p2r_status p2r_model_create_ep(const p2r_model_config* cfg, uint64_t seed, int world, int rank,
                                p2r_model** out);
 p2r_status p2r_model_comm_init(p2r_model* m, const char* unique_id128);
+typedef struct p2r_loopback p2r_loopback;
+p2r_status p2r_loopback_create(int world, p2r_loopback** out);
+p2r_status p2r_loopback_destroy(p2r_loopback* g);
+p2r_status p2r_model_comm_init_loopback(p2r_model* m, p2r_loopback* g);
 p2r_status p2r_model_allreduce_grads(p2r_model* m);
 
 /* ---- granular CPU offload (§4.2) ---------------

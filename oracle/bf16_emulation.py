@@ -12,7 +12,7 @@ from . import p2r_oracle as O
 
 F32 = np.float32
 ALL_POINTS = ("w16", "a16", "qkv16", "p16", "o16", "b16", "hpre16", "g16", "h16",
-              "dlogits16", "dres16", "dh16", "dx1_16", "do16", "ds16", "dqkv16", "ye16", "dye16")
+              "dlogits16", "dres16", "dh16", "dx1_16", "do16", "ds16", "dqkv16", "ye16", "dye16", "dxe16")
 
 
 def bf16(x):
@@ -137,7 +137,7 @@ def loss_and_grads(cfg: O.Config, params: dict, tokens, targets, mask, batch, de
                 dhe = R(O.gelu_bwd(dye @ W[pr + f"moe.expert.{e}.w2"].T, he16), "dh16")
                 G[pr + f"moe.expert.{e}.w1"] += xe.T @ dhe
                 G[pr + f"moe.expert.{e}.b1"] += dhe.sum(0)
-                np.add.at(db, rows, (dhe @ W[pr + f"moe.expert.{e}.w1"].T).astype(F32))
+                np.add.at(db, rows, R((dhe @ W[pr + f"moe.expert.{e}.w1"].T).astype(F32), "dxe16"))
             glog = O.selected_softmax_bwd(gw, wgt, rt, c.n_experts)
             G[pr + "moe.gate"] += (bm.T @ glog).astype(F32)
             db += (glog @ P0[pr + "moe.gate"].T).astype(F32)

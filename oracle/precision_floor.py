@@ -41,7 +41,7 @@ def main():
     mask[:, -1] = 0
     tok, tgt, mask = tok.ravel(), tgt.ravel(), mask.ravel()
     denom = float(mask.sum())
-    pts_all = tuple(p for p in BE.ALL_POINTS if p != "ye16")  # dense stack
+    pts_all = tuple(p for p in BE.ALL_POINTS if p not in ("ye16", "dye16", "dxe16"))  # dense stack
     _, g0 = BE.loss_and_grads(cfg, p0, tok, tgt, mask, a.batch, denom, points=())
 
     def worst(pts):

@@ -6,10 +6,14 @@
 
 #include "../p2r_internal.h"
 #include "p2r/engine.hpp"
+#include "comm_state.hpp"
 #include "p2r_engine.h"
 
 struct p2r_model {
   std::unique_ptr<p2r::Model> m;
+};
+struct p2r_loopback {
+  std::unique_ptr<p2r::LoopbackGroup> g;
 };
 
 namespace {
@@ -332,6 +336,20 @@ p2r_status p2r_model_create_ep(const p2r_model_config* cfg, uint64_t seed, int w
 }
 p2r_status p2r_model_comm_init(p2r_model* m, const char* id) {
   return guard([&] { m->m->comm_init(id); });
+}
+p2r_status p2r_loopback_create(int world, p2r_loopback** out) {
+  return guard([&] {
+    auto h = std::make_unique<p2r_loopback>();
+    h->g = std::make_unique<p2r::LoopbackGroup>(world);
+    *out = h.release();
+  });
+}
+p2r_status p2r_loopback_destroy(p2r_loopback* g) {
+  delete g;
+  return P2R_OK;
+}
+p2r_status p2r_model_comm_init_loopback(p2r_model* m, p2r_loopback* g) {
+  return guard([&] { m->m->comm_init_loopback(g->g.get()); });
 }
 p2r_status p2r_model_allreduce_grads(p2r_model* m) {
   return guard([&] { m->m->allreduce_grads(); });

@@ -19,6 +19,7 @@
 #include <random>
 #include <string>
 
+#include "comm_state.hpp"
 #include "offload_state.hpp"
 
 namespace p2r {
@@ -164,7 +165,13 @@ struct LayerActs {
   DevBuf xout, a16, mean1, rstd1, qkv16, o16, lse, x1, b16, mean2, rstd2;
   DevBuf hpre16, g16;                                                 // dense FFN
   DevBuf b32, logits, sel, surv, pos, w, raw, counts, rows_pad, slots_pad, dropped;  // MoE
-  DevBuf xe16, hpre_e16, ge16, ye32;
+  DevBuf xe16, hpre_e16, ge16;
+  // expert outputs in this rank's expert-major layout [E][seg] (bf16): a local
+  // buffer, or a region of the expert-parallel arena the owners write into
+  DevBuf ye16_own;
+  void* ye16 = nullptr;
+  DevBuf ccount, cprefix;  // expert parallel, owner side: compact rows per local expert / per source
+  int ye_set = 0;          // index of ye16 among the arena's return buffers
   int capacity = 0;
 };
 
@@ -178,7 +185,9 @@ struct Acts {
   std::vector<char> ckpt;
   LayerActs ck;
   DevBuf h16, meanf, rstdf, logits32, dlogits16, loss, loss_sum, ce_ws, dh32;
-  DevBuf dres, dres16, tmp32, dx1, dx1_16, do16, dqkv16, dh16, dye16, dxe32, dw, glogits, dsum;
+  DevBuf dres, dres16, tmp32, dx1, dx1_16, do16, dqkv16, dh16, dye16, dw, glogits, dsum;
+  DevBuf dxe16_own;
+  void* dxe16 = nullptr;  // expert-input gradients [E][seg] bf16 (local, or the arena's return buffer)
   DevBuf ln_ws, colsum_ws, embed_ws;
   // Dense FFN2 bias gradient: the LayerNorm backward that produces dres also writes
   // its per-block column sums here; the consuming layer's LN2 backward finishes them
@@ -186,8 +195,46 @@ struct Acts {
   DevBuf db2_stage;
   int db2_blocks = 0, db2_for = -1;
   DevBuf tokens, targets, mask;
-  DevBuf xe_send16, ye_owner32, dxe_owner32, full_counts;  // expert-parallel exchange
+  DevBuf yc16, dxc16;  // expert parallel, owner side: compact expert outputs / input gradients
 };
+
+// ---------------------------------------------------------------- expert-parallel exchange
+std::size_t Model::ep_ye_offset(int set) const { return ep_->off_ye + ep_->ye_bytes * static_cast<std::size_t>(set); }
+std::size_t Model::ep_dxe_offset() const { return ep_->off_dxe; }
+
+void Model::ep_send(const void* src, int src_dtype, LayerActs& L, const float* w) {
+  const int W = ep_world_, E = cfg_.moe.n_experts;
+  std::vector<void*> slots(static_cast<std::size_t>(W));
+  std::vector<int*> cnts(static_cast<std::size_t>(W));
+  for (int q = 0; q < W; ++q) {
+    slots[static_cast<std::size_t>(q)] = ep_peer(q, ep_->off_slot);
+    cnts[static_cast<std::size_t>(q)] = static_cast<int*>(ep_peer(q, ep_->off_cnt));
+  }
+  p2r_check(p2r_ep_send_rows(src, src_dtype, cfg_.d_model, E, acts_->seg, L.rows_pad.as<int>(), L.slots_pad.as<int>(),
+                             L.counts.as<int>(), w, cfg_.moe.n_prototypes, W, ep_rank_, slots.data(), cnts.data(),
+                             stream_),
+            "ep send");
+  ep_signal(0);
+  ep_wait(0);
+}
+
+void Model::ep_pack_rows(void* compact, LayerActs& L) {
+  const int W = ep_world_, El = cfg_.moe.n_experts / W;
+  p2r_check(p2r_ep_pack(ep_local(ep_->off_slot), static_cast<const int*>(ep_local(ep_->off_cnt)), cfg_.d_model,
+                        acts_->seg, El, W, compact, L.ccount.as<int>(), L.cprefix.as<int>(), stream_),
+            "ep pack");
+}
+
+void Model::ep_return(const void* compact, LayerActs& L, std::size_t dst_off) {
+  const int W = ep_world_, El = cfg_.moe.n_experts / W;
+  std::vector<void*> dst(static_cast<std::size_t>(W));
+  for (int q = 0; q < W; ++q) dst[static_cast<std::size_t>(q)] = ep_peer(q, dst_off);
+  p2r_check(p2r_ep_return_rows(compact, L.cprefix.as<int>(), cfg_.d_model, acts_->seg, El, W, ep_rank_, dst.data(),
+                               stream_),
+            "ep return");
+  ep_signal(1);
+  ep_wait(1);
+}
 
 // ---------------------------------------------------------------- Model
 Model::Model(ModelConfig config, std::uint64_t seed) : cfg_(std::move(config)) {
@@ -536,7 +583,14 @@ void Model::ensure_acts(int B, int S) {
       l.xe16 = DevBuf(ES * d * 2);
       l.hpre_e16 = DevBuf(ES * dff * 2);
       l.ge16 = DevBuf(ES * dff * 2);
-      l.ye32 = DevBuf(ES * d * 4);
+      if (!ep_active()) {
+        l.ye16_own = DevBuf(ES * d * 2);
+        l.ye16 = l.ye16_own.p;
+      } else {
+        const int El = E / ep_world_;
+        l.ccount = DevBuf(static_cast<std::size_t>(El) * 4);
+        l.cprefix = DevBuf(static_cast<std::size_t>(El) * (ep_world_ + 1) * 4);
+      }
     }
   }
   A->h16 = DevBuf(Td * 2);
@@ -561,16 +615,13 @@ void Model::ensure_acts(int B, int S) {
   } else {
     A->dh16 = DevBuf(ES * dff * 2);
     A->dye16 = DevBuf(ES * d * 2);
-    A->dxe32 = DevBuf(ES * d * 4);
     A->dw = DevBuf(static_cast<std::size_t>(T) * k * 4);
-    if (ep_active()) {
-      A->xe_send16 = DevBuf(ES * d * 2);
-      A->ye_owner32 = DevBuf(ES * d * 4);
-      A->dxe_owner32 = DevBuf(ES * d * 4);
-      const int El = E / ep_world_;
-      std::vector<int> full(static_cast<std::size_t>(El), ep_world_ * A->seg);
-      A->full_counts = DevBuf(static_cast<std::size_t>(El) * 4);
-      cuda_check(cudaMemcpy(A->full_counts.p, full.data(), full.size() * 4, cudaMemcpyHostToDevice), "counts");
+    if (!ep_active()) {
+      A->dxe16_own = DevBuf(ES * d * 2);
+      A->dxe16 = A->dxe16_own.p;
+    } else {
+      A->yc16 = DevBuf(ES * d * 2);
+      A->dxc16 = DevBuf(ES * d * 2);
     }
     A->glogits = DevBuf(static_cast<std::size_t>(T) * E * 4);
   }
@@ -584,6 +635,20 @@ void Model::ensure_acts(int B, int S) {
   A->tokens = DevBuf(static_cast<std::size_t>(T) * 4);
   A->targets = DevBuf(static_cast<std::size_t>(T) * 4);
   A->mask = DevBuf(static_cast<std::size_t>(T));
+  if (cfg_.moe.enabled() && ep_active()) {
+    // expert-parallel arena: the expert-output return buffer of every activation set
+    // (one per stored layer + the shared checkpoint set) and the gradient return buffer
+    std::vector<LayerActs*> sets;
+    for (int g = 0; g < cfg_.n_layers_graph; ++g)
+      if (!A->ckpt[static_cast<std::size_t>(g)]) sets.push_back(&A->L[static_cast<std::size_t>(g)]);
+    if (any_ckpt) sets.push_back(&A->ck);
+    ep_connect(A->seg, static_cast<int>(sets.size()));
+    for (std::size_t i = 0; i < sets.size(); ++i) {
+      sets[i]->ye16 = ep_local(ep_ye_offset(static_cast<int>(i)));
+      sets[i]->ye_set = static_cast<int>(i);
+    }
+    A->dxe16 = ep_local(ep_dxe_offset());
+  }
   acts_ = std::move(A);
   ++acts_gen_;
   const std::size_t pin = static_cast<std::size_t>(T) * 9 + 64;
@@ -785,28 +850,33 @@ void Model::block_compute(int g, const float* xin_data, AttentionMode mode) {
     p2r_check(p2r_moe_combine_weights(L.logits.as<float>(), T, E, k, L.sel.as<int>(), L.surv.as<std::uint8_t>(),
                                       L.w.as<float>(), stream_),
               "combine weights");
-    // Expert parallelism: dispatch into the local expert-major layout, then the
-    // owner ranks receive [El][W][seg] segments (full-capacity groups whose
-    // padding rows are zero and contribute exactly nothing to the backward).
     const bool ep = ep_active();
-    if (ep && comm_ == nullptr) throw std::logic_error("expert parallel: call comm_init before the first step");
-    const int El = E / ep_world_;
-    const int gseg = ep ? ep_world_ * seg : seg;
-    const int* gcnt = ep ? A.full_counts.as<int>() : L.counts.as<int>();
-    const int G = ep ? El : E;
-    void* xsend = ep ? A.xe_send16.p : L.xe16.p;
-    prof(P2R_PROF_MOE, 0, 4.0 * T * d, [&] {
-      p2r_check(p2r_moe_dispatch(L.b16.p, 1, d, E, seg, L.rows_pad.as<int>(), L.slots_pad.as<int>(),
-                                 L.counts.as<int>(), nullptr, k, xsend, ep ? 1 : 0, stream_),
-                "dispatch");
-    });
-    if (ep) ep_exchange(xsend, L.xe16.p, static_cast<std::size_t>(d) * 2, seg, true);
-    gemm(G * gseg, dff, d, L.xe16.p, d, false, lp16(o, layer_.w1), dff, true, P2R_EPI_BIAS_GELU, L.ge16.p, dff,
-         L.hpre_e16.p, dff, lp(o, layer_.b1), nullptr, 0, P2R_GROUP_M, G, gseg, gcnt);
-    gemm(G * gseg, d, dff, L.ge16.p, dff, false, lp16(o, layer_.w2), d, true, P2R_EPI_F32,
-         ep ? A.ye_owner32.p : L.ye32.p, d, nullptr, 0, lp(o, layer_.b2), nullptr, 0, P2R_GROUP_M, G, gseg, gcnt);
-    if (ep) ep_exchange(A.ye_owner32.p, L.ye32.p, static_cast<std::size_t>(d) * 4, seg, false);
-    p2r_check(p2r_moe_combine(L.ye32.as<float>(), T, d, k, seg, L.sel.as<int>(), L.pos.as<int>(), L.w.as<float>(),
+    if (!ep) {
+      // local experts: expert-major rows [E][seg] zero-padded to 128, grouped GEMMs over E groups
+      prof(P2R_PROF_MOE, 0, 4.0 * T * d, [&] {
+        p2r_check(p2r_moe_dispatch(L.b16.p, 1, d, E, seg, L.rows_pad.as<int>(), L.slots_pad.as<int>(),
+                                   L.counts.as<int>(), nullptr, k, L.xe16.p, 0, stream_),
+                  "dispatch");
+      });
+      gemm(E * seg, dff, d, L.xe16.p, d, false, lp16(o, layer_.w1), dff, true, P2R_EPI_BIAS_GELU, L.ge16.p, dff,
+           L.hpre_e16.p, dff, lp(o, layer_.b1), nullptr, 0, P2R_GROUP_M, E, seg, L.counts.as<int>());
+      gemm(E * seg, d, dff, L.ge16.p, dff, false, lp16(o, layer_.w2), d, true, P2R_EPI_BF16, L.ye16, d, nullptr, 0,
+           lp(o, layer_.b2), nullptr, 0, P2R_GROUP_M, E, seg, L.counts.as<int>());
+    } else {
+      // expert parallel (csrc/ep.cu): the routed rows go straight into their owners'
+      // slots; each owner packs them per local expert (exact counts, W*seg rows per
+      // group), runs the grouped GEMMs, and returns the outputs into the sources'
+      // expert-major layout (L.ye16 is this rank's arena region the owners write)
+      const int El = E / ep_world_, gseg = ep_world_ * seg;
+      prof(P2R_PROF_MOE, 0, 4.0 * T * d, [&] { ep_send(L.b16.p, 1, L, nullptr); });
+      ep_pack_rows(L.xe16.p, L);
+      gemm(El * gseg, dff, d, L.xe16.p, d, false, lp16(o, layer_.w1), dff, true, P2R_EPI_BIAS_GELU, L.ge16.p, dff,
+           L.hpre_e16.p, dff, lp(o, layer_.b1), nullptr, 0, P2R_GROUP_M, El, gseg, L.ccount.as<int>());
+      gemm(El * gseg, d, dff, L.ge16.p, dff, false, lp16(o, layer_.w2), d, true, P2R_EPI_BF16, A.yc16.p, d, nullptr, 0,
+           lp(o, layer_.b2), nullptr, 0, P2R_GROUP_M, El, gseg, L.ccount.as<int>());
+      ep_return(A.yc16.p, L, ep_ye_offset(L.ye_set));
+    }
+    p2r_check(p2r_moe_combine(L.ye16, T, d, k, seg, L.sel.as<int>(), L.pos.as<int>(), L.w.as<float>(),
                               L.x1.as<float>(), xout, stream_),
               "combine");
   }
@@ -853,17 +923,21 @@ void Model::block_backward(int g, AttentionMode mode) {
     const bool ep = ep_active();
     const int El = E / ep_world_;
     const int gseg = ep ? ep_world_ * seg : seg;
-    const int* gcnt = ep ? A.full_counts.as<int>() : cnt;
+    const int* gcnt = ep ? L.ccount.as<int>() : cnt;
     const int G = ep ? El : E;
-    // combine backward: dw = <dy, ye>, dye = w * dy (expert-major, bf16)
-    p2r_check(p2r_moe_combine_bwd_weights(dy, L.ye32.as<float>(), T, d, k, seg, L.sel.as<int>(), L.pos.as<int>(),
-                                          A.dw.as<float>(), stream_),
-              "combine bwd");
-    void* dye_local = ep ? A.xe_send16.p : A.dye16.p;
-    p2r_check(p2r_moe_dispatch(dy, 0, d, E, seg, L.rows_pad.as<int>(), L.slots_pad.as<int>(), cnt, L.w.as<float>(),
-                               k, dye_local, ep ? 1 : 0, stream_),
-              "dispatch dy");
-    if (ep) ep_exchange(dye_local, A.dye16.p, static_cast<std::size_t>(d) * 2, seg, true);
+    // combine backward: dw = <dy, ye> (feeds the gate gradient, k > 1 only), dye = w * dy
+    if (k > 1)
+      p2r_check(p2r_moe_combine_bwd_weights(dy, L.ye16, T, d, k, seg, L.sel.as<int>(), L.pos.as<int>(),
+                                            A.dw.as<float>(), stream_),
+                "combine bwd");
+    if (!ep) {
+      p2r_check(p2r_moe_dispatch(dy, 0, d, E, seg, L.rows_pad.as<int>(), L.slots_pad.as<int>(), cnt, L.w.as<float>(),
+                                 k, A.dye16.p, 0, stream_),
+                "dispatch dy");
+    } else {  // the scaled dy rows go to their owners, packed like the forward's rows
+      ep_send(dy, 0, L, L.w.as<float>());
+      ep_pack_rows(A.dye16.p, L);
+    }
     gemm(dff, d, gseg, L.ge16.p, dff, true, A.dye16.p, d, true, P2R_EPI_ACC_F32, lg(o, layer_.w2), d, nullptr, 0,
          nullptr, nullptr, 0, P2R_GROUP_K, G, gseg, gcnt);
     p2r_check(p2r_bias_grad(A.dye16.p, 1, d, G * gseg, d, G, gseg, gcnt, lg(o, layer_.b2), d,
@@ -876,9 +950,10 @@ void Model::block_backward(int g, AttentionMode mode) {
     p2r_check(p2r_bias_grad(A.dh16.p, 1, dff, G * gseg, dff, G, gseg, gcnt, lg(o, layer_.b1), dff,
                             A.colsum_ws.as<float>(), stream_),
               "db1");
-    gemm(G * gseg, d, dff, A.dh16.p, dff, false, lp16(o, layer_.w1), dff, false, P2R_EPI_F32,
-         ep ? A.dxe_owner32.p : A.dxe32.p, d, nullptr, 0, nullptr, nullptr, 0, P2R_GROUP_M, G, gseg, gcnt);
-    if (ep) ep_exchange(A.dxe_owner32.p, A.dxe32.p, static_cast<std::size_t>(d) * 4, seg, false);
+    // expert-input gradients in bf16 (local layout, or compact on the owner then returned)
+    gemm(G * gseg, d, dff, A.dh16.p, dff, false, lp16(o, layer_.w1), dff, false, P2R_EPI_BF16,
+         ep ? A.dxc16.p : A.dxe16, d, nullptr, 0, nullptr, nullptr, 0, P2R_GROUP_M, G, gseg, gcnt);
+    if (ep) ep_return(A.dxc16.p, L, ep_dxe_offset());
     const float* glog = nullptr;
     if (k > 1) {  // top-1 => combine weights are exactly 1 and the gate gradient is exactly 0
       p2r_check(p2r_moe_gate_bwd(L.b32.as<float>(), L.w.as<float>(), A.dw.as<float>(), T, d, E, k, L.sel.as<int>(),
@@ -886,7 +961,7 @@ void Model::block_backward(int g, AttentionMode mode) {
                 "gate bwd");
       glog = A.glogits.as<float>();
     }
-    p2r_check(p2r_moe_dispatch_bwd(A.dxe32.as<float>(), T, d, k, seg, L.sel.as<int>(), L.pos.as<int>(), glog,
+    p2r_check(p2r_moe_dispatch_bwd(A.dxe16, T, d, k, seg, L.sel.as<int>(), L.pos.as<int>(), glog,
                                    lp(o, layer_.gate), E, A.tmp32.as<float>(), 0, stream_),
               "dispatch bwd");
   }

@@ -379,7 +379,7 @@ void Model::offload_release(int o, bool backward) {
   const bool apply = has_opt_ && micro_ == accum_n_;
   cudaEvent_t done = st.ev();
   if (apply) {
-    if (comm_ != nullptr && ep_world_ > 1) {
+    if ((comm_ != nullptr || loop_ != nullptr) && ep_world_ > 1) {
       const long long repl = cfg_.moe.enabled() ? layer_.w1 : layer_.numel;
       allreduce_f32(sl.g32.as<float>(), static_cast<std::size_t>(repl));
     }

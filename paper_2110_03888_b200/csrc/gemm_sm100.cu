@@ -849,8 +849,8 @@ bool make_store_map(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t c
   return r == CUDA_SUCCESS;
 }
 
-void* g_ws = nullptr;
-size_t g_ws_bytes = 0;
+thread_local void* g_ws = nullptr;  // per calling thread: shards on several host threads each pass their own
+thread_local size_t g_ws_bytes = 0;
 
 // zero-initialised split-K tile counters, one buffer per stream (GEMMs on one
 // stream are ordered; different streams must not share counters)

@@ -328,8 +328,8 @@ __global__ void dispatch_kernel(const Tin* __restrict__ src, int d, const int* _
   }
 }
 
-// out[t] = resid[t] + sum_{g asc, survived} w[t,g] * ye[sel*seg + pos]   (fp32)
-__global__ void combine_kernel(const float* __restrict__ ye, int d, int seg_rows,
+// out[t] = resid[t] + sum_{g asc, survived} w[t,g] * ye[sel*seg + pos]   (fp32 sum of bf16 rows)
+__global__ void combine_kernel(const __nv_bfloat16* __restrict__ ye, int d, int seg_rows,
                                const int* __restrict__ selected, const int* __restrict__ pos,
                                const float* __restrict__ w, int k,
                                const float* __restrict__ resid, float* __restrict__ out) {
@@ -340,7 +340,7 @@ __global__ void combine_kernel(const float* __restrict__ ye, int d, int seg_rows
       const int s = t * k + j;
       const int p = pos[s];
       if (p < 0) continue;
-      acc += w[s] * ye[(static_cast<long long>(selected[s]) * seg_rows + p) * d + c];
+      acc += w[s] * __bfloat162float(ye[(static_cast<long long>(selected[s]) * seg_rows + p) * d + c]);
     }
     out[static_cast<long long>(t) * d + c] = (resid ? resid[static_cast<long long>(t) * d + c] : 0.f) + acc;
   }
@@ -389,7 +389,7 @@ __global__ void dispatch4_kernel(const Tin* __restrict__ src, int d, const int* 
   }
 }
 
-__global__ void combine4_kernel(const float* __restrict__ ye, int d, int seg_rows, const int* __restrict__ selected,
+__global__ void combine4_kernel(const __nv_bfloat16* __restrict__ ye, int d, int seg_rows, const int* __restrict__ selected,
                                 const int* __restrict__ pos, const float* __restrict__ w, int k,
                                 const float* __restrict__ resid, float* __restrict__ out) {
   const int t = blockIdx.x;
@@ -400,7 +400,7 @@ __global__ void combine4_kernel(const float* __restrict__ ye, int d, int seg_row
       const int p = pos[s];
       if (p < 0) continue;
       const float ws = w[s];
-      const float4 y = *reinterpret_cast<const float4*>(ye + (static_cast<long long>(selected[s]) * seg_rows + p) * d + c);
+      const float4 y = ld_src4(ye + (static_cast<long long>(selected[s]) * seg_rows + p) * d + c);
       acc.x += ws * y.x;
       acc.y += ws * y.y;
       acc.z += ws * y.z;
@@ -413,7 +413,7 @@ __global__ void combine4_kernel(const float* __restrict__ ye, int d, int seg_row
 }
 
 // k-sum of the routed rows only (no gate term: glogits == NULL)
-__global__ void dispatch_bwd4_kernel(const float* __restrict__ dxe, int d, int k, int seg_rows,
+__global__ void dispatch_bwd4_kernel(const __nv_bfloat16* __restrict__ dxe, int d, int k, int seg_rows,
                                      const int* __restrict__ selected, const int* __restrict__ pos,
                                      float* __restrict__ db, int accumulate) {
   const int t = blockIdx.x;
@@ -424,7 +424,7 @@ __global__ void dispatch_bwd4_kernel(const float* __restrict__ dxe, int d, int k
       const int s = t * k + j;
       const int p = pos[s];
       if (p < 0) continue;
-      const float4 g = *reinterpret_cast<const float4*>(dxe + (static_cast<long long>(selected[s]) * seg_rows + p) * d + c);
+      const float4 g = ld_src4(dxe + (static_cast<long long>(selected[s]) * seg_rows + p) * d + c);
       acc.x += g.x;
       acc.y += g.y;
       acc.z += g.z;
@@ -435,7 +435,7 @@ __global__ void dispatch_bwd4_kernel(const float* __restrict__ dxe, int d, int k
 }
 
 // dw[t,g] = <dout[t], ye[row(t,g)]>  (warp per (t,g)); 0 for dropped slots
-__global__ void combine_bwd_w_kernel(const float* __restrict__ dout, const float* __restrict__ ye,
+__global__ void combine_bwd_w_kernel(const float* __restrict__ dout, const __nv_bfloat16* __restrict__ ye,
                                      int T, int d, int k, int seg_rows,
                                      const int* __restrict__ selected, const int* __restrict__ pos,
                                      float* __restrict__ dw) {
@@ -447,8 +447,8 @@ __global__ void combine_bwd_w_kernel(const float* __restrict__ dout, const float
   if (p >= 0) {
     const int t = s / k;
     const float* a = dout + static_cast<long long>(t) * d;
-    const float* y = ye + (static_cast<long long>(selected[s]) * seg_rows + p) * d;
-    for (int c = lane; c < d; c += 32) acc += a[c] * y[c];
+    const __nv_bfloat16* y = ye + (static_cast<long long>(selected[s]) * seg_rows + p) * d;
+    for (int c = lane; c < d; c += 32) acc += a[c] * __bfloat162float(y[c]);
   }
   acc = warp_sum(acc);
   if (lane == 0) dw[s] = acc;
@@ -474,7 +474,7 @@ __global__ void sel_softmax_bwd_kernel(const float* __restrict__ w, const float*
 
 // db[t] = (accumulate ? db[t] : 0) + sum over the token's slots (g DESC, the
 // tape's reverse expert order) of dxe[row] + glogits[t] . gate^T
-__global__ void dispatch_bwd_kernel(const float* __restrict__ dxe, int d, int k, int seg_rows,
+__global__ void dispatch_bwd_kernel(const __nv_bfloat16* __restrict__ dxe, int d, int k, int seg_rows,
                                     const int* __restrict__ selected, const int* __restrict__ pos,
                                     const float* __restrict__ glogits, const float* __restrict__ gate,
                                     int E, float* __restrict__ db, int accumulate) {
@@ -485,7 +485,7 @@ __global__ void dispatch_bwd_kernel(const float* __restrict__ dxe, int d, int k,
       const int s = t * k + j;
       const int p = pos[s];
       if (p < 0) continue;
-      acc += dxe[(static_cast<long long>(selected[s]) * seg_rows + p) * d + c];
+      acc += __bfloat162float(dxe[(static_cast<long long>(selected[s]) * seg_rows + p) * d + c]);
     }
     if (glogits) {
       float g = 0.f;
@@ -657,10 +657,11 @@ extern "C" p2r_status p2r_moe_dispatch(const void* src, int src_dtype, int d, in
   return P2R_OK;
 }
 
-extern "C" p2r_status p2r_moe_combine(const float* ye, int T, int d, int k, int seg_rows,
+extern "C" p2r_status p2r_moe_combine(const void* ye_bf16, int T, int d, int k, int seg_rows,
                                       const int* selected, const int* pos, const float* w,
                                       const float* resid, float* out, void* stream) {
   if (T <= 0) return P2R_OK;
+  const __nv_bfloat16* ye = static_cast<const __nv_bfloat16*>(ye_bf16);
   if (d % 4 == 0)
     combine4_kernel<<<T, d >= 2048 ? 256 : 128, 0, static_cast<cudaStream_t>(stream)>>>(ye, d, seg_rows, selected, pos,
                                                                                        w, k, resid, out);
@@ -670,10 +671,11 @@ extern "C" p2r_status p2r_moe_combine(const float* ye, int T, int d, int k, int 
   return P2R_OK;
 }
 
-extern "C" p2r_status p2r_moe_combine_bwd_weights(const float* dout, const float* ye, int T, int d,
+extern "C" p2r_status p2r_moe_combine_bwd_weights(const float* dout, const void* ye_bf16, int T, int d,
                                                   int k, int seg_rows, const int* selected,
                                                   const int* pos, float* dw, void* stream) {
   if (T <= 0) return P2R_OK;
+  const __nv_bfloat16* ye = static_cast<const __nv_bfloat16*>(ye_bf16);
   const long long warps = static_cast<long long>(T) * k;
   combine_bwd_w_kernel<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       dout, ye, T, d, k, seg_rows, selected, pos, dw);
@@ -694,11 +696,12 @@ extern "C" p2r_status p2r_moe_gate_bwd(const float* b, const float* w, const flo
   return P2R_OK;
 }
 
-extern "C" p2r_status p2r_moe_dispatch_bwd(const float* dxe, int T, int d, int k, int seg_rows,
+extern "C" p2r_status p2r_moe_dispatch_bwd(const void* dxe_bf16, int T, int d, int k, int seg_rows,
                                            const int* selected, const int* pos,
                                            const float* glogits, const float* gate, int E,
                                            float* db, int accumulate, void* stream) {
   if (T <= 0) return P2R_OK;
+  const __nv_bfloat16* dxe = static_cast<const __nv_bfloat16*>(dxe_bf16);
   if (glogits == nullptr && d % 4 == 0)
     dispatch_bwd4_kernel<<<T, d >= 2048 ? 256 : 128, 0, static_cast<cudaStream_t>(stream)>>>(dxe, d, k, seg_rows,
                                                                                             selected, pos, db, accumulate);

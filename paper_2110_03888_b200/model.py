@@ -67,6 +67,9 @@ _lib._EXTRA_SIGNATURES.update({
     "p2r_comm_unique_id": [ctypes.c_char_p],
     "p2r_model_create_ep": [ctypes.POINTER(ModelConfigC), ctypes.c_uint64, ip, ip, ctypes.POINTER(vp)],
     "p2r_model_comm_init": [vp, ctypes.c_char_p],
+    "p2r_loopback_create": [ip, ctypes.POINTER(vp)],
+    "p2r_loopback_destroy": [vp],
+    "p2r_model_comm_init_loopback": [vp, vp],
     "p2r_model_allreduce_grads": [vp],
     "p2r_model_create_offload": [ctypes.POINTER(ModelConfigC), ctypes.c_uint64, vp, ip, ctypes.POINTER(vp)],
     "p2r_model_set_offload_lr": [vp, fp],
@@ -328,6 +331,12 @@ class Model:
     def comm_init(self, unique_id: bytes):
         check(lib().p2r_model_comm_init(self.h, ctypes.c_char_p(unique_id)))
 
+    def comm_init_loopback(self, group: "LoopbackGroup"):
+        """Join a loopback group (W shards of this process on one device; drive each
+        shard's steps from its own thread -- the exchange is collective)."""
+        check(lib().p2r_model_comm_init_loopback(self.h, group.h))
+        self._group = group  # keep the group alive as long as its shards
+
     def allreduce_grads(self):
         check(lib().p2r_model_allreduce_grads(self.h))
 
@@ -427,6 +436,26 @@ class Model:
         out = np.empty((n_tokens, self.cfg.n_experts), np.float32)
         check(lib().p2r_model_gate_logits(self.h, g, _p(out)))
         return out
+
+
+class LoopbackGroup:
+    """W expert/data-parallel shards in one process on one device (SURVEY §4's
+    loopback comm): the same peer-store exchange and stream flags as a multi-GPU
+    node, with the shards' own arenas as peer memory; rank-order all-reduce."""
+
+    def __init__(self, world: int):
+        h = vp()
+        check(lib().p2r_loopback_create(int(world), ctypes.byref(h)))
+        self.h = h.value
+        self.world = world
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().p2r_loopback_destroy(self.h)
+                self.h = None
+        except Exception:  # noqa: BLE001
+            pass
 
 
 @dataclass

@@ -1,22 +1,38 @@
 #!/usr/bin/env python
 """Training-step benchmark of the Pseudo-to-Real hot path on B200.
 
-Workload (BASELINE.json configs[1], "C2"): pseudo-giant dense GPT block shared
-across 24 layers, d=1024, 16 heads, d_ff=4096, seq 1024, batch 8 sequences per
-GPU, vocab 260, random-init weights (reference init, seed 1234), synthetic
-byte tokens. One step = embed -> 24 x block fwd -> tied head -> masked CE ->
-full backward (shared-layer grads accumulated in place) -> [NCCL allreduce of
-the shared + embedding grads when N > 1] -> AdamW.
+Default workload (BASELINE.json configs[1], "C2"): pseudo-giant dense GPT block
+shared across 24 layers, d=1024, 16 heads, d_ff=4096, seq 1024, batch 8
+sequences per GPU, vocab 260, random-init weights (reference init, seed 1234),
+synthetic byte tokens. One step = embed -> 24 x block fwd -> tied head -> masked
+CE -> full backward (shared-layer grads accumulated in place) -> [NCCL
+allreduce of the shared + embedding grads when N > 1] -> AdamW.
 
   python bench.py [--gpus N --steps K --warmup W]          # this framework
   python bench.py --impl reference [...]                    # reference CPU arm
+  python bench.py --workload c3|c4|c5 [...]                 # the other configs
+
+--gpus N > 1 without torchrun's WORLD_SIZE re-launches itself under
+torch.distributed.run with N ranks. Other workloads (BASELINE.json configs):
+  c3  Pseudo MoE (24 shared layers, d=1024, 8 experts top-1) delinked into the
+      Real model, then the Real step; experts sharded over the N GPUs
+  c4  M6-style MoE per-rank slice: d=2048, 8 experts per GPU (64 at N=8), top-1,
+      --layers (48), expert parallel over the N GPUs
+  c5  granular-offload per-rank slice (d=2048, 8 local experts, --layers 8,
+      half the layers SLOW, 2-micro-step accumulation): resident / offload /
+      offload-without-copies steps, PCIe GB/s per direction and hidden fraction
 
 Prints ONE JSON line on rank 0. `value` = tokens/s over all ranks with inputs
-resident in HBM (CUDA events on the model stream, max over ranks); `e2e` = the
-same metric through the public host-buffer API (tokens/targets/mask copied in
-from pinned memory, loss read back, every step). `roofline` is computed live
-from per-kernel CUDA events in the timed region; `cpu_baseline` times the
-compiled reference (oracle/_ref) on the host cores on a bounded sample.
+resident in HBM (CUDA events on the model stream around the K timed steps, max
+over ranks); `e2e` = the same metric through the public host-buffer API
+(tokens/targets/mask copied in from pinned memory, loss read back, every step).
+`roofline` comes from a SEPARATE eager pass of K more steps in which every
+kernel is bracketed by CUDA events on the model stream (per-class time and
+algorithmic FLOPs/bytes); it explains `value` but is not part of its timed
+region. `cpu_baseline` times the compiled reference (oracle/_ref) on the host
+cores on a bounded sample. The default C2 line also carries two in-run
+sub-records: `moe_ep` (C4 per-rank slice, local vs expert-parallel exchange
+path) and `offload` (C5 per-rank slice, hidden fraction of the PCIe traffic).
 """
 from __future__ import annotations
 
@@ -52,6 +68,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-graph", action="store_true", help="eager launches instead of one CUDA graph per step")
     p.add_argument("--cpu-procs", type=int, default=0, help="reference processes (0 = auto)")
+    p.add_argument("--workload", default="c2", choices=["c2", "c3", "c4", "c5"])
+    p.add_argument("--layers", type=int, default=0, help="c3/c4/c5: layer count (0 = the config's)")
+    p.add_argument("--no-extras", action="store_true", help="c2: skip the moe_ep / offload sub-records")
     return p.parse_args()
 
 
@@ -244,19 +263,231 @@ def main_reference(args):
 
 
 # ----------------------------------------------------------------------------- GPU arm
+def moe_cfg(p2r, d, dff, heads, layers, params, experts, seq):
+    return p2r.Config(d_model=d, d_ff=dff, n_layers_graph=layers, n_layers_params=params, n_heads=heads,
+                      vocab_size=260, seq_len=seq, n_experts=experts, n_prototypes=1)
+
+
+def flops_per_token(d, dff, L, S, V=260, E=0, k_eff=1.0):
+    """§8(d): 3 x [L (8d^2 + 4 k_eff d dff + 2 d E + 2 S d) + 2 d V] (fwd + bwd, no recompute)."""
+    return 3 * (L * (8 * d * d + 4 * k_eff * d * dff + 2 * d * E + 2 * S * d) + 2 * d * V)
+
+
+def make_dist(world, local):
+    import torch
+    if world <= 1:
+        return None
+    import torch.distributed as dist
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return dist
+
+
+def comm_init(model, p2r, dist, rank, world):
+    if world > 1:
+        # the library's own NCCL communicator (csrc/engine/comm.cpp); torch only ships the id
+        uid = [p2r.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        model.comm_init(uid[0])
+
+
+def build_workload(args, p2r, dist, rank, world):
+    """-> (model, batch, seq, workload text, model FLOPs per token, graph ok, parallelism)."""
+    B, S = args.batch, 1024
+    if args.workload == "c2":
+        m = p2r.Model(p2r.Config(**C2), 1234)
+        comm_init(m, p2r, dist, rank, world)
+        return m, B, S, WORKLOAD, flops_per_token(1024, 4096, 24, S), True, f"dp{world}"
+    if args.workload == "c3":
+        E = 8
+        if E % world:
+            raise SystemExit("c3: 8 experts need a GPU count dividing 8")
+        L = args.layers or 24
+        pseudo = p2r.Model(moe_cfg(p2r, 1024, 4096, 16, L, 1, E, S), 1234, ep=(world, rank))
+        real = pseudo.delinked()  # every rank delinks its own shard (no communication)
+        pseudo.close()
+        comm_init(real, p2r, dist, rank, world)
+        text = (f"C3 Pseudo MoE ({L} shared layers, d=1024, 16 heads, d_ff=4096, {E} experts top-1 cf 1.25, "
+                f"vocab 260, seq 1024) delinked into {L} Real layers; Real-model fwd+bwd+AdamW, "
+                f"experts over {world} GPU(s)")
+        return real, B, S, text, flops_per_token(1024, 4096, L, S, E=E), False, f"ep{world}+dp{world}"
+    if args.workload == "c4":
+        E = 8 * world  # 8 experts per GPU: the C4 per-rank share (64 experts at N = 8)
+        L = args.layers or 48
+        m = p2r.Model(moe_cfg(p2r, 2048, 4096, 16, L, L, E, S), 1234, ep=(world, rank))
+        comm_init(m, p2r, dist, rank, world)
+        text = (f"C4 M6-style MoE per-rank slice: {L} Real layers, d=2048, 16 heads, d_ff=4096, 8 experts per GPU "
+                f"({E} total) top-1 cf 1.25, vocab 260, seq 1024, fwd+bwd+AdamW")
+        return m, B, S, text, flops_per_token(2048, 4096, L, S, E=E), False, f"ep{world}+dp{world}"
+    raise SystemExit(f"unknown workload {args.workload}")
+
+
+def moe_ep_record(p2r, torch, steps=4, warmup=2, layers=4):
+    """C4 per-rank slice at `layers` layers: the local expert path vs the expert-parallel
+    exchange path at world 1 (peer-store send, owner pack, exact-count GEMMs, return),
+    same tokens; ms per step and the bytes the exchange moves."""
+    B, S = 8, 1024
+    cfg = moe_cfg(p2r, 2048, 4096, 16, layers, layers, 8, S)
+    tok, tgt, mask = lm_batch(B, S, 7)
+    dt, dg, dm = (torch.from_numpy(x).cuda() for x in (tok, tgt, mask))
+    out = {}
+    for name in ("local", "ep_w1"):
+        if name == "ep_w1":
+            os.environ["P2R_FORCE_EP"] = "1"
+        try:
+            m = p2r.Model(cfg, 1234, ep=(1, 0)) if name == "ep_w1" else p2r.Model(cfg, 1234)
+        finally:
+            os.environ.pop("P2R_FORCE_EP", None)
+        m.attach_adamw()
+        ext = torch.cuda.ExternalStream(m.stream())
+
+        def step(i):
+            m.train_step_device(dt.data_ptr(), dg.data_ptr(), dm.data_ptr(), B, S, float(mask.sum()))
+            m.adamw_step(p2r.lr_at(2e-4, 0.01, 1000, i))
+
+        for i in range(warmup):
+            step(i)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(ext):
+            e0.record()
+        for i in range(steps):
+            step(warmup + i)
+        with torch.cuda.stream(ext):
+            e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        rows = 0
+        for g in range(layers):
+            sel, sur, raw, cap, drop = m.layer_routing(g, B * S)
+            rows += int(sur.sum())
+        out[name] = {"ms_per_step": round(ms, 3), "tokens_per_s": round(B * S / (ms / 1e3), 1)}
+        if name == "ep_w1":
+            # rows cross the link as bf16 in each of the 4 exchanges per layer
+            # (fwd dispatch + return, bwd dispatch + return); at W ranks the remote
+            # share is (W-1)/W of it
+            out["exchange_bytes_per_direction_per_layer"] = int(rows // layers * 2048 * 2)
+            out["algorithmic_bytes_T_d_2"] = B * S * 2048 * 2
+        m.close()
+        del m
+        torch.cuda.empty_cache()
+    out["ep_over_local"] = round(out["ep_w1"]["ms_per_step"] / out["local"]["ms_per_step"], 4)
+    out["workload"] = (f"C4 per-rank slice, {layers} Real layers, d=2048, d_ff=4096, 8 experts top-1, 8x1024 tokens, "
+                       f"fwd+bwd+AdamW; CUDA events over {steps} steps after {warmup} warm-up")
+    return out
+
+
+def offload_record(p2r, torch, layers=8, steps=3, warmup=2, ring=3, micro=2, batch=16):
+    """C5 per-rank slice: granular offload of half the layers (interleaved, the overlap
+    planner's spread), activation checkpointing of SLOW layers, `micro` accumulation
+    micro-steps per optimizer step. Resident / offload / offload-without-copies step
+    times (CUDA events), copy-engine busy time (events on the H2D / D2H streams) and
+    the hidden fraction h = 1 - (T_offload - T_nocopy) / max(T_h2d, T_d2h)."""
+    B, S = batch, 1024
+    cfg = moe_cfg(p2r, 2048, 4096, 16, layers, layers, 8, S)
+    plan = [1 if i % 2 == 0 else 0 for i in range(layers)]
+    batches = [tuple(torch.from_numpy(x).cuda() for x in lm_batch(B, S, 50 + j)) for j in range(micro)]
+    denom = float(micro * B * (S - 1))
+
+    def run(m, offloaded, n):
+        ext = torch.cuda.ExternalStream(m.stream())
+
+        def one(i):
+            lr = p2r.lr_at(2e-4, 0.01, 1000, i + 10)
+            if offloaded:
+                m.set_offload_lr(lr)
+            for j, (dt, dg, dm) in enumerate(batches):
+                m.train_step_device(dt.data_ptr(), dg.data_ptr(), dm.data_ptr(), B, S, denom, zero=(j == 0))
+            m.adamw_step(lr)
+
+        for i in range(warmup):
+            one(i)
+        torch.cuda.synchronize()
+        if offloaded:
+            m.offload_stats()
+            m.offload_stats_reset()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(ext):
+            e0.record()
+        for i in range(n):
+            one(warmup + i)
+        st = m.offload_stats() if offloaded else None  # joins the copy streams
+        with torch.cuda.stream(ext):
+            e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / 1e3 / n, st
+
+    res = p2r.Model(cfg, 1234)
+    res.attach_adamw()
+    t_res, _ = run(res, False, steps)
+    res.close()
+    del res
+    torch.cuda.empty_cache()
+    off = p2r.Model(cfg, 1234, offload=plan, ring_slots=ring)
+    off.attach_adamw()
+    off.set_grad_accumulation(micro)
+    t_off, st = run(off, True, steps)
+    off.set_offload_skip_copies(True)
+    t_nc, _ = run(off, True, steps)
+    off.set_offload_skip_copies(False)
+    gran = off.layer_granule_bytes()
+    off.close()
+    del off
+    torch.cuda.empty_cache()
+    per = {k: v / steps for k, v in st.items()}
+    h2d_b = per["Fn_load"] + per["Bn_load"] + per["opt_load"] + per["grad_load"]
+    d2h_b = per["writeback"] + per["grad_offload"]
+    t_copy = max(per["h2d_ms"], per["d2h_ms"]) / 1e3
+    hidden = 1.0 - max(0.0, t_off - t_nc) / t_copy if t_copy > 0 else 1.0
+    T = micro * B * S
+    # held-out check of the overlap model (fit on round-1 dense runs): calibrated from
+    # this shape's resident step (forward : backward = 1 : 2) and the measured PCIe rates
+    P = gran // 18
+    h2d_bw = h2d_b / (per["h2d_ms"] / 1e3) if per["h2d_ms"] else 50e9
+    d2h_bw = d2h_b / (per["d2h_ms"] / 1e3) if per["d2h_ms"] else 50e9
+    tl = t_res / micro / layers
+    pred = p2r.predict_step_time_overlap([P] * layers, plan, h2d_bw, d2h_bw, tl / 3, 2 * tl / 3, fn_master=True,
+                                         micro_steps=micro, recompute=True)
+    # bytes one SLOW layer must move per optimizer step vs the compute one layer offers
+    # per step: the copy / compute ratio that decides how much can hide
+    return {"workload": (f"C5 per-rank slice: {layers} Real MoE layers, d=2048, d_ff=4096, 8 local experts top-1, "
+                         f"{micro} x {B}x{S} tokens per optimizer step (accumulation), fwd+bwd+AdamW"),
+            "placement": plan, "ring_slots": ring, "granule_bytes": gran, "activation_checkpointing": "SLOW layers",
+            "step_s": {"resident": round(t_res, 4), "offload": round(t_off, 4), "offload_no_copy": round(t_nc, 4)},
+            "tokens_per_s": {"resident": round(T / t_res, 1), "offload": round(T / t_off, 1)},
+            "bytes_per_step": {k: per[k] for k in ("Fn_load", "Bn_load", "opt_load", "grad_load", "writeback",
+                                                    "grad_offload")},
+            "h2d_GBps": round(h2d_b / (per["h2d_ms"] / 1e3) / 1e9, 2) if per["h2d_ms"] else None,
+            "d2h_GBps": round(d2h_b / (per["d2h_ms"] / 1e3) / 1e9, 2) if per["d2h_ms"] else None,
+            "copy_busy_s": {"h2d": round(per["h2d_ms"] / 1e3, 4), "d2h": round(per["d2h_ms"] / 1e3, 4)},
+            "timing": "CUDA events on the model stream (steps) and on the copy streams (busy time)",
+            "hidden_fraction": round(hidden, 4),
+            "overlap_model": {"predicted_step_s": round(pred, 4), "measured_step_s": round(t_off, 4),
+                              "rel_error": round(abs(pred - t_off) / t_off, 4)}}
+
+
 def main_p2r(args):
     import torch
     rank, world, local = dist_env()
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        raise SystemExit(f"bench: WORLD_SIZE={world} but --gpus {args.gpus}")
     torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dist = make_dist(world, local)
     import paper_2110_03888_b200 as p2r
 
-    B, S = args.batch, C2["seq_len"]
+    if args.workload == "c5":
+        if world > 1:
+            raise SystemExit("c5: per-rank slice, run with --gpus 1 (ranks share nothing)")
+        rec = offload_record(p2r, torch, layers=args.layers or 8, steps=args.steps)
+        out = {"metric": METRIC, "value": rec["tokens_per_s"]["offload"], "unit": "tokens/s", "n_gpus": 1,
+               "steps": args.steps, "warmup": 2, "ms_per_step": round(rec["step_s"]["offload"] * 1e3, 3),
+               "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+               "data": "synthetic", "config": {"workload": rec["workload"], "parallelism": "offload"},
+               "offload": rec}
+        print(json.dumps(out), flush=True)
+        return
+
+    model, B, S, workload, model_flops, graph_ok, par = build_workload(args, p2r, dist, rank, world)
     T = B * S
-    model = p2r.Model(p2r.Config(**C2), 1234)
     model.attach_adamw()
     ext = torch.cuda.ExternalStream(model.stream())
     tok, tgt, mask = lm_batch(B, S, 7 + rank)
@@ -266,17 +497,12 @@ def main_p2r(args):
     loss_dev = torch.zeros(1, device="cuda")
     torch.cuda.synchronize()
     denom = float(mask.sum()) * world  # global mask count: summed grads = large-batch mean
-    if world > 1:
-        # the library's own NCCL communicator (csrc/engine/comm.cpp); torch only ships the id
-        uid = [p2r.comm_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        model.comm_init(uid[0])
 
     def allreduce():
         if world > 1:
             model.allreduce_grads()  # ncclAllReduce of the replicated grad granules, model stream
 
-    use_graph = not args.no_graph
+    use_graph = graph_ok and not args.no_graph
 
     def step_device(i, graph=use_graph):
         # one CUDA graph per fwd+bwd step (captured during warm-up); the DP all-reduce
@@ -303,7 +529,7 @@ def main_p2r(args):
         step_device(i)
     barrier()
 
-    # ---- timed region: inputs resident in HBM (activations ~7 GB/step >> 126 MB L2)
+    # ---- timed region: inputs resident in HBM (activations >> 126 MB L2 per step)
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
@@ -322,8 +548,9 @@ def main_p2r(args):
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     value = T * world / (ms / 1e3)
 
-    # ---- same K steps again with every kernel bracketed by CUDA events on the
-    # model stream (kept out of the `value` region: ~2 events per launch)
+    # ---- roofline: the same K steps again in a separate eager pass with every kernel
+    # bracketed by CUDA events on the model stream (~2 events per launch, so it is
+    # kept out of the `value` region)
     model.profile_reset()
     model.set_profiling(True)
     for i in range(args.steps):
@@ -349,7 +576,7 @@ def main_p2r(args):
            "h2d_bytes_per_step": int(tok.nbytes + tgt.nbytes + mask.nbytes), "d2h_bytes_per_step": 4,
            "ms_per_step": round(e2e_s * 1e3, 3)}
 
-    # ---- roofline of the dominant kernel class, live from the timed region
+    # ---- roofline of the dominant kernel class
     peaks, peak_src = load_peaks()
     dom = max(prof, key=lambda k: prof[k][1])
     n_l, ms_k, fl, by = prof[dom]
@@ -366,7 +593,7 @@ def main_p2r(args):
         per_unit = by / max(n_l, 1)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and args.workload == "c2":
         try:
             with open(tpath) as f:
                 traffic = json.load(f).get(dom)
@@ -375,6 +602,7 @@ def main_p2r(args):
     roofline = {"bound": bound, "achieved": round(achieved, 2), "peak": peak, "unit": unit,
                 "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": dom,
                 "peak_source": f"{peak_src} ({'bf16_tflops_sustained' if bound == 'tensor' else 'hbm_gbs'})",
+                "timed": "separate eager pass of K steps, CUDA events around every launch on the model stream",
                 "launches_per_step": n_l / args.steps, "avg_launch_ms": round(per_launch_ms, 5),
                 "algorithmic_per_launch": per_unit}
     breakdown = {k: {"launches": v[0], "ms_per_step": round(v[1] / args.steps, 3),
@@ -382,18 +610,26 @@ def main_p2r(args):
                      ("tflops" if v[2] > 0 else "gbs"): round((v[2] / 1e12 if v[2] > 0 else v[3] / 1e9) /
                                                               max(v[1] / 1e3, 1e-12), 1)}
                  for k, v in prof.items() if v[0]}
-    model_flops = 3 * (24 * (8 * 1024**2 + 4 * 1024 * 4096 + 2 * S * 1024) + 2 * 1024 * 260)
     out = {"metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-           "config": {"workload": WORKLOAD, "global_batch": B * world, "seq_len": S,
-                      "parallelism": f"dp{world}", "l2": "inputs larger than L2 (~7 GB activations per step)",
+           "config": {"workload": workload, "global_batch": B * world, "seq_len": S,
+                      "parallelism": par, "l2": "inputs larger than L2 (GBs of activations per step)",
                       "launch": "one CUDA graph per fwd+bwd step + eager AdamW" if use_graph else "eager",
                       "mfu_model_flops_per_token": model_flops},
            "clocks": clk, "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline,
            "kernels": breakdown,
            "model_tflops": round(model_flops * value / 1e12, 1)}
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    model.close()
+    del model
+    torch.cuda.empty_cache()
+    if rank == 0 and world == 1 and args.workload == "c2" and not args.no_extras:
+        for key, fn in (("moe_ep", moe_ep_record), ("offload", offload_record)):
+            try:
+                out[key] = fn(p2r, torch)
+            except Exception as e:  # noqa: BLE001
+                out[key] = {"error": f"{type(e).__name__}: {e}"}
+    if rank == 0 and world == 1 and args.workload == "c2" and not args.no_cpu_baseline:
         try:
             out["cpu_baseline"] = cpu_baseline_sample(ref_procs(args.cpu_procs))
         except Exception as e:  # noqa: BLE001
@@ -405,8 +641,21 @@ def main_p2r(args):
         dist.destroy_process_group()
 
 
+def relaunch(args):
+    """--gpus N > 1 outside torchrun: re-launch this script as N ranks (one per GPU)."""
+    import socket
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 if __name__ == "__main__":
     a = parse()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(a))
     if a.impl == "reference":
         main_reference(a)
     else:

@@ -174,6 +174,10 @@ struct OffloadCost {
   double fwd_s = 0, bwd_s = 0;          // compute per layer
   bool fn_master = false;               // Fn loads the fp32 master (4P), write-back drops the bf16 (12P)
   int ring_slots = 3;                   // HBM staging slots (planner budget: resident + ring x largest granule)
+  int micro_steps = 1;                  // accumulation window: per micro-step Fn + Bn loads; partial grads
+                                        // parked (D2H 4P) / reloaded (H2D 4P) between micro-steps; moments +
+                                        // write-back once per window
+  bool recompute = false;               // activation checkpointing of SLOW layers: +1 forward in the backward
 };
 double predict_step_time_overlap(const std::vector<std::int64_t>& layer_params,
                                  const std::vector<std::int64_t>& vector_params, const std::vector<int>& slow,

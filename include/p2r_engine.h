@@ -242,6 +242,12 @@ double p2r_predict_step_time_overlap_form(const int64_t* layer_params, const int
                                           const int* slow, int n, double h2d_bw, double d2h_bw, double fwd_s,
                                           double bwd_s, int fn_master);
 /* fewest SLOW layers (18 B/param granules) under budget_bytes, spread evenly */
+/* The same model over an accumulation window of micro_steps (per micro-step Fn + Bn
+ * loads, partial grads parked / reloaded between micro-steps, moments + write-back
+ * once) with recompute != 0 adding the SLOW layers' checkpoint recomputation. */
+double p2r_predict_step_time_overlap_window(const int64_t* layer_params, const int64_t* vector_params, const int* slow,
+                                            int n, double h2d_bw, double d2h_bw, double fwd_s, double bwd_s,
+                                            int fn_master, int micro_steps, int recompute);
 p2r_status p2r_plan_offload_overlap(const int64_t* layer_params, int n, int64_t budget_bytes, double h2d_bw,
                                     double d2h_bw, double fwd_s, double bwd_s, int ring_slots, int* slow_out);
 

@@ -388,12 +388,18 @@ __global__ void __launch_bounds__(384, 1)
         float other;
         asm volatile("ld.shared.f32 %0, [%1];" : "=f"(other) : "r"(slot + 4 * 128 * (hf ^ 1)) : "memory");
         const float mx = fmaxf(fmaxf(mr0, mr1), other) * p.sl2;
-        if (mx > m_used + kRescaleThresh) {  // both halves take the same decision
+        // Lazy rescale. Both halves of a row take the same decision, but rows (lanes)
+        // differ, and the TMEM load / store below are warp-collective (.sync.aligned):
+        // the warp enters the branch together when any of its rows needs it, and rows
+        // that do not keep their max (factor 1). A lane-divergent branch here hung the
+        // kernel once scores grew during training.
+        const bool need = mx > m_used + kRescaleThresh;
+        if (__any_sync(0xffffffffu, need)) {
           if (j > 0) {
             // O holds sum_{<j} 2^(x - m_used) V: rescale this half's O columns to the new max
             mbar_wait(o_done + ((g - 1) & 1), ((g - 1) >> 1) & 1);
             tc_fence_after();
-            const float f = exp2f(m_used - mx);
+            const float f = need ? exp2f(m_used - mx) : 1.0f;
 #pragma unroll
             for (int c = 0; c < OH / 32; ++c) {
               uint32_t rr[32];
@@ -404,9 +410,9 @@ __global__ void __launch_bounds__(384, 1)
               tmem_st_32x32b_x32(tO + c * 32, rr);
             }
             tmem_st_wait();
-            l *= f;
+            if (need) l *= f;
           }
-          m_used = mx;
+          if (need) m_used = mx;
         }
         // P buffer reuse: the PV that last read this buffer must be done
         if (g >= C::NPB) {

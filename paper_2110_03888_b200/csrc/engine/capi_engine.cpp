@@ -444,6 +444,18 @@ double p2r_predict_step_time_overlap_form(const int64_t* layer_params, const int
   c.fn_master = fn_master != 0;
   return p2r::predict_step_time_overlap(p, v, s, c);
 }
+double p2r_predict_step_time_overlap_window(const int64_t* layer_params, const int64_t* vector_params, const int* slow,
+                                            int n, double h2d_bw, double d2h_bw, double fwd_s, double bwd_s,
+                                            int fn_master, int micro_steps, int recompute) {
+  std::vector<std::int64_t> p(layer_params, layer_params + n), v;
+  if (vector_params) v.assign(vector_params, vector_params + n);
+  std::vector<int> s(slow, slow + n);
+  p2r::OffloadCost c = cost(h2d_bw, d2h_bw, fwd_s, bwd_s);
+  c.fn_master = fn_master != 0;
+  c.micro_steps = micro_steps;
+  c.recompute = recompute != 0;
+  return p2r::predict_step_time_overlap(p, v, s, c);
+}
 double p2r_predict_step_time_overlap(const int64_t* layer_params, const int64_t* vector_params, const int* slow, int n,
                                      double h2d_bw, double d2h_bw, double fwd_s, double bwd_s) {
   return p2r_predict_step_time_overlap_form(layer_params, vector_params, slow, n, h2d_bw, d2h_bw, fwd_s, bwd_s, 0);

@@ -12,12 +12,14 @@
 #include "p2r/engine.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <random>
 #include <string>
+#include <thread>
 
 #include "comm_state.hpp"
 #include "offload_state.hpp"
@@ -411,27 +413,55 @@ void* Model::lp16(int o, long long off) const {
 }
 
 void Model::init_params(std::uint64_t seed) {
-  // model.cpp:128-164: gains 1, biases 0, matrices N(0, 0.02) per named tensor
-  std::vector<float> host;
+  // model.cpp:128-164: gains 1, biases 0, matrices N(0, 0.02) per named tensor. Every
+  // tensor draws from its own generator (seed mixed with its name), so tensors are
+  // filled in parallel host threads (same values) and uploaded in order, in batches
+  // of about 1 GiB of host memory.
   const bool trace = std::getenv("P2R_TRACE") != nullptr;
-  for (int i = 0; i < static_cast<int>(views_.size()); ++i) {
-    const ParamView& v = views_[i];
-    if (trace) std::fprintf(stderr, "init %s granule %d off %lld rows %d cols %d ld %d\n", v.name.c_str(), v.granule, v.off, v.rows, v.cols, v.ld);
-    const std::size_t n = static_cast<std::size_t>(v.rows) * v.cols;
-    host.assign(n, 0.0f);
-    const std::string& nm = v.name;
-    auto ends_with = [&](const char* suf) {
-      const std::size_t L = std::strlen(suf);
-      return nm.size() >= L && nm.compare(nm.size() - L, L, suf) == 0;
-    };
-    if (ends_with(".gain")) {
-      std::fill(host.begin(), host.end(), 1.0f);
-    } else if (ends_with(".bias") || ends_with(".b1") || ends_with(".b2")) {
-      // zeros
-    } else {
-      init_normal_host(host.data(), n, seed, nm);
+  const int nv = static_cast<int>(views_.size());
+  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  int i0 = 0;
+  while (i0 < nv) {
+    int i1 = i0;
+    std::size_t batch = 0;
+    while (i1 < nv && (i1 == i0 || batch < (std::size_t{1} << 28))) {
+      batch += static_cast<std::size_t>(views_[static_cast<std::size_t>(i1)].rows) * views_[static_cast<std::size_t>(i1)].cols;
+      ++i1;
     }
-    set_param(i, host.data());
+    std::vector<std::vector<float>> host(static_cast<std::size_t>(i1 - i0));
+    std::atomic<int> next{i0};
+    auto work = [&] {
+      for (int i = next++; i < i1; i = next++) {
+        const ParamView& v = views_[static_cast<std::size_t>(i)];
+        std::vector<float>& h = host[static_cast<std::size_t>(i - i0)];
+        const std::size_t n = static_cast<std::size_t>(v.rows) * v.cols;
+        h.assign(n, 0.0f);
+        const std::string& nm = v.name;
+        auto ends_with = [&](const char* suf) {
+          const std::size_t L = std::strlen(suf);
+          return nm.size() >= L && nm.compare(nm.size() - L, L, suf) == 0;
+        };
+        if (ends_with(".gain")) {
+          std::fill(h.begin(), h.end(), 1.0f);
+        } else if (ends_with(".bias") || ends_with(".b1") || ends_with(".b2")) {
+          // zeros
+        } else {
+          init_normal_host(h.data(), n, seed, nm);
+        }
+      }
+    };
+    std::vector<std::thread> pool;
+    for (unsigned t = 1; t < hw; ++t) pool.emplace_back(work);
+    work();
+    for (auto& t : pool) t.join();
+    for (int i = i0; i < i1; ++i) {
+      const ParamView& v = views_[static_cast<std::size_t>(i)];
+      if (trace)
+        std::fprintf(stderr, "init %s granule %d off %lld rows %d cols %d ld %d\n", v.name.c_str(), v.granule, v.off,
+                     v.rows, v.cols, v.ld);
+      set_param(i, host[static_cast<std::size_t>(i - i0)].data());
+    }
+    i0 = i1;
   }
   refresh_bf16();
 }

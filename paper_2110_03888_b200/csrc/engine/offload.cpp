@@ -72,27 +72,42 @@ double predict_step_time_overlap(const std::vector<std::int64_t>& layer_params,
   const std::size_t L = layer_params.size();
   if (slow.size() != L || (!vector_params.empty() && vector_params.size() != L))
     throw std::invalid_argument("predict_step_time_overlap: layer / placement size mismatch");
-  double h2d_f = 0, h2d_b = 0, d2h = 0, fill = -1, drain = 0;
+  const double M = static_cast<double>(std::max(1, c.micro_steps));
+  double h2d_f = 0, h2d_b = 0, h2d_bf = 0, d2h = 0, d2h_f = 0, fill = -1, drain = 0;
+  int n_slow = 0;
   for (std::size_t i = 0; i < L; ++i)
     if (slow[i]) {
+      ++n_slow;
       const double P = static_cast<double>(layer_params[i]);
       const double vec = vector_params.empty() ? 0.0 : static_cast<double>(vector_params[i]);
       // forward: bf16 shadow + the fp32 vectors it reads, or the whole fp32 master
       const double f = c.fn_master ? 4.0 * P : 2.0 * P + 4.0 * vec;
       const double w = c.fn_master ? 12.0 * P : 14.0 * P;  // updated p, m, v (+ bf16 shadow)
-      h2d_f += f;
-      h2d_b += 12.0 * P;  // fp32 master + m + v (bf16 re-derived on the device)
-      d2h += w;
+      h2d_f += f;                   // per micro-step
+      h2d_b += 4.0 * P;             // per micro-step: fp32 master (bf16 re-derived on the device)
+      h2d_bf += 8.0 * P;            // last micro-step: m + v
+      d2h_f += w;                   // last micro-step: write-back
+      d2h += 4.0 * P;               // earlier micro-steps: partial gradients parked ...
       if (fill < 0) {  // the lowest SLOW layer: its Fn load opens the step, its write-back closes it
         fill = f / c.h2d_bw;
         drain = w / c.d2h_bw;
       }
     }
-  const double cf = c.fwd_s * static_cast<double>(L), cb = c.bwd_s * static_cast<double>(L);
-  const double phases = std::max(cf, h2d_f / c.h2d_bw) + std::max({cb, h2d_b / c.h2d_bw, d2h / c.d2h_bw});
+  const double cf = c.fwd_s * static_cast<double>(L);
+  const double cb = c.bwd_s * static_cast<double>(L) + (c.recompute ? c.fwd_s * n_slow : 0.0);
+  // micro-steps 1 .. M-1 park the partial grads (D2H 4P); from the 2nd on they are
+  // reloaded with the Bn master (H2D another 4P); the last adds moments and write-back
+  double phases = 0;
+  for (int m = 1; m <= static_cast<int>(M); ++m) {
+    const bool last = m == static_cast<int>(M);
+    const double hb = h2d_b * (m > 1 ? 2.0 : 1.0) + (last ? h2d_bf : 0.0);
+    const double db = last ? d2h_f : d2h;
+    phases += std::max(cf, h2d_f / c.h2d_bw) + std::max({cb, hb / c.h2d_bw, db / c.d2h_bw});
+  }
   // the ring prefetches backward granules during the forward, so the H2D stream can
   // also be the bound as a whole: every load, plus the exposed first load and last write-back
-  const double stream = fill < 0 ? 0.0 : (h2d_f + h2d_b) / c.h2d_bw + fill + drain;
+  const double h2d_all = M * (h2d_f + h2d_b) + (M - 1.0) * h2d_b + h2d_bf;
+  const double stream = fill < 0 ? 0.0 : h2d_all / c.h2d_bw + fill + drain;
   return std::max(phases, stream);
 }
 

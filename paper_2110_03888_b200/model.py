@@ -113,6 +113,8 @@ def _declare_extra():
     L.p2r_predict_step_time_overlap.restype = ctypes.c_double
     L.p2r_predict_step_time_overlap_form.argtypes = [vp, vp, vp, ip] + [ctypes.c_double] * 4 + [ip]
     L.p2r_predict_step_time_overlap_form.restype = ctypes.c_double
+    L.p2r_predict_step_time_overlap_window.argtypes = [vp, vp, vp, ip] + [ctypes.c_double] * 4 + [ip, ip, ip]
+    L.p2r_predict_step_time_overlap_window.restype = ctypes.c_double
     L.p2r_plan_offload_overlap.argtypes = [vp, ip, i64] + [ctypes.c_double] * 4 + [ip, vp]
     L.p2r_plan_offload_overlap.restype = ctypes.c_int
     return L
@@ -527,15 +529,16 @@ def redistribute_checkpoints(in_paths, out_paths):
 
 
 def predict_step_time_overlap(layer_params, slow, h2d_bw, d2h_bw, fwd_s, bwd_s, vector_params=None,
-                              fn_master=False) -> float:
+                              fn_master=False, micro_steps=1, recompute=False) -> float:
     """B200 overlap model of the offload engine; see p2r_engine.h.
-    fn_master: the engine's default forward load (fp32 master); False = the bf16-shadow form."""
+    fn_master: the engine's default forward load (fp32 master); False = the bf16-shadow form.
+    micro_steps / recompute: accumulation window and SLOW-layer checkpoint recomputation."""
     L = _declare_extra()
     p = np.ascontiguousarray(layer_params, np.int64)
     sl = np.ascontiguousarray(slow, np.int32)
     v = None if vector_params is None else np.ascontiguousarray(vector_params, np.int64)
-    return float(L.p2r_predict_step_time_overlap_form(_p(p), _p(v), _p(sl), len(p), h2d_bw, d2h_bw, fwd_s, bwd_s,
-                                                      int(bool(fn_master))))
+    return float(L.p2r_predict_step_time_overlap_window(_p(p), _p(v), _p(sl), len(p), h2d_bw, d2h_bw, fwd_s, bwd_s,
+                                                        int(bool(fn_master)), int(micro_steps), int(bool(recompute))))
 
 
 def plan_offload_overlap(layer_params, budget_bytes, h2d_bw, d2h_bw, fwd_s, bwd_s, ring_slots=3):

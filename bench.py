@@ -376,7 +376,7 @@ def moe_ep_record(p2r, torch, steps=4, warmup=2, layers=4):
     return out
 
 
-def offload_record(p2r, torch, layers=8, steps=3, warmup=2, ring=3, micro=2, batch=16):
+def offload_record(p2r, torch, layers=8, steps=3, warmup=2, ring=6, micro=1, batch=64):
     """C5 per-rank slice: granular offload of half the layers (interleaved, the overlap
     planner's spread), activation checkpointing of SLOW layers, `micro` accumulation
     micro-steps per optimizer step. Resident / offload / offload-without-copies step
@@ -384,7 +384,12 @@ def offload_record(p2r, torch, layers=8, steps=3, warmup=2, ring=3, micro=2, bat
     the hidden fraction h = 1 - (T_offload - T_nocopy) / max(T_h2d, T_d2h)."""
     B, S = batch, 1024
     cfg = moe_cfg(p2r, 2048, 4096, 16, layers, layers, 8, S)
-    plan = [1 if i % 2 == 0 else 0 for i in range(layers)]
+    # half the layers SLOW (C5: ~45 of 96 granules do not fit HBM), spread the way the
+    # overlap-aware planner spreads them (half a stride in: layer 0 stays resident)
+    k = layers // 2
+    plan = [0] * layers
+    for j in range(k):
+        plan[(2 * j + 1) * layers // (2 * k)] = 1
     batches = [tuple(torch.from_numpy(x).cuda() for x in lm_batch(B, S, 50 + j)) for j in range(micro)]
     denom = float(micro * B * (S - 1))
 
@@ -441,11 +446,13 @@ def offload_record(p2r, torch, layers=8, steps=3, warmup=2, ring=3, micro=2, bat
     T = micro * B * S
     # held-out check of the overlap model (fit on round-1 dense runs): calibrated from
     # this shape's resident step (forward : backward = 1 : 2) and the measured PCIe rates
-    P = gran // 18
+    P = gran // 18  # (the padded granule)
     h2d_bw = h2d_b / (per["h2d_ms"] / 1e3) if per["h2d_ms"] else 50e9
     d2h_bw = d2h_b / (per["d2h_ms"] / 1e3) if per["d2h_ms"] else 50e9
     tl = t_res / micro / layers
-    pred = p2r.predict_step_time_overlap([P] * layers, plan, h2d_bw, d2h_bw, tl / 3, 2 * tl / 3, fn_master=True,
+    vec = max(0.0, (per["Fn_load"] / max(1, sum(plan)) - 2 * P) / 4)
+    pred = p2r.predict_step_time_overlap([P] * layers, plan, h2d_bw, d2h_bw, tl / 3, 2 * tl / 3,
+                                         vector_params=[int(vec)] * layers, fn_master=False,
                                          micro_steps=micro, recompute=True)
     # bytes one SLOW layer must move per optimizer step vs the compute one layer offers
     # per step: the copy / compute ratio that decides how much can hide

@@ -7,12 +7,14 @@
 // by a D2H stream, event-synchronised with the compute stream. The step's SLOW
 // uses (forward ascending, then backward descending) are staged as far ahead as
 // the ring allows, so backward granules load during the H2D-light forward:
-//   Fn : H2D fp32 master, bf16 operand derived on the device (default), or
-//        (P2R_OFFLOAD_FN_SHADOW=1) the bf16 shadow + the fp32 vectors / MoE gate
-//   Bn : H2D fp32 master (+ m, v); the bf16 operand is re-derived on the device
+//   Fn : H2D bf16 shadow + the fp32 vectors / MoE gate (default), or (master
+//        form: P2R_OFFLOAD_FN_MASTER=1 or P2R_OFFLOAD_FN_SHADOW=0) the fp32 master
+//   Bn : H2D fp32 master (+ m, v) in the micro-step that applies AdamW (the bf16
+//        operand is re-derived on the device); accumulating micro-steps load the
+//        Fn form plus the parked partial gradients
 //   An : AdamW for the granule on the GPU right after its backward, then D2H
 //        write-back of p32 + m + v (+ the bf16 shadow in the shadow form), or
-//        of the grads when no optimizer is attached (the spec's "gradient offload").
+//        of the grads when no optimizer is attached / the window continues.
 // FAST granules stay resident; the placement comes from plan_offload.
 #include <cuda_runtime.h>
 
@@ -73,7 +75,7 @@ double predict_step_time_overlap(const std::vector<std::int64_t>& layer_params,
   if (slow.size() != L || (!vector_params.empty() && vector_params.size() != L))
     throw std::invalid_argument("predict_step_time_overlap: layer / placement size mismatch");
   const double M = static_cast<double>(std::max(1, c.micro_steps));
-  double h2d_f = 0, h2d_b = 0, h2d_bf = 0, d2h = 0, d2h_f = 0, fill = -1, drain = 0;
+  double h2d_f = 0, h2d_b = 0, h2d_bn = 0, h2d_bf = 0, d2h = 0, d2h_f = 0, fill = -1, drain = 0;
   int n_slow = 0;
   for (std::size_t i = 0; i < L; ++i)
     if (slow[i]) {
@@ -84,29 +86,33 @@ double predict_step_time_overlap(const std::vector<std::int64_t>& layer_params,
       const double f = c.fn_master ? 4.0 * P : 2.0 * P + 4.0 * vec;
       const double w = c.fn_master ? 12.0 * P : 14.0 * P;  // updated p, m, v (+ bf16 shadow)
       h2d_f += f;                   // per micro-step
-      h2d_b += 4.0 * P;             // per micro-step: fp32 master (bf16 re-derived on the device)
+      h2d_b += 4.0 * P;             // last micro-step: fp32 master (bf16 re-derived on the device)
+      h2d_bn += c.fn_master ? 4.0 * P : f;  // accumulating micro-steps: what the forward loads
       h2d_bf += 8.0 * P;            // last micro-step: m + v
       d2h_f += w;                   // last micro-step: write-back
       d2h += 4.0 * P;               // earlier micro-steps: partial gradients parked ...
-      if (fill < 0) {  // the lowest SLOW layer: its Fn load opens the step, its write-back closes it
-        fill = f / c.h2d_bw;
-        drain = w / c.d2h_bw;
+      if (fill < 0) {
+        // the lowest SLOW layer: its Fn load opens the step behind the forward of the
+        // layers below it, its write-back closes it behind their backward
+        fill = std::max(0.0, f / c.h2d_bw - c.fwd_s * static_cast<double>(i));
+        drain = std::max(0.0, w / c.d2h_bw - c.bwd_s * static_cast<double>(i));
       }
     }
   const double cf = c.fwd_s * static_cast<double>(L);
   const double cb = c.bwd_s * static_cast<double>(L) + (c.recompute ? c.fwd_s * n_slow : 0.0);
   // micro-steps 1 .. M-1 park the partial grads (D2H 4P); from the 2nd on they are
-  // reloaded with the Bn master (H2D another 4P); the last adds moments and write-back
-  double phases = 0;
+  // reloaded with the Bn load (H2D another 4P); the last loads the master, moments,
+  // and writes back
+  double phases = 0, h2d_all = 0;
   for (int m = 1; m <= static_cast<int>(M); ++m) {
     const bool last = m == static_cast<int>(M);
-    const double hb = h2d_b * (m > 1 ? 2.0 : 1.0) + (last ? h2d_bf : 0.0);
+    const double hb = (last ? h2d_b + h2d_bf : h2d_bn) + (m > 1 ? h2d_b : 0.0);
+    h2d_all += h2d_f + hb;
     const double db = last ? d2h_f : d2h;
     phases += std::max(cf, h2d_f / c.h2d_bw) + std::max({cb, hb / c.h2d_bw, db / c.d2h_bw});
   }
   // the ring prefetches backward granules during the forward, so the H2D stream can
   // also be the bound as a whole: every load, plus the exposed first load and last write-back
-  const double h2d_all = M * (h2d_f + h2d_b) + (M - 1.0) * h2d_b + h2d_bf;
   const double stream = fill < 0 ? 0.0 : h2d_all / c.h2d_bw + fill + drain;
   return std::max(phases, stream);
 }
@@ -136,8 +142,10 @@ std::vector<int> plan_offload_overlap(const std::vector<std::int64_t>& layer_par
     fast -= 18 * layer_params[static_cast<std::size_t>(order[static_cast<std::size_t>(k)])];
   std::vector<int> pl(static_cast<std::size_t>(n), 0);
   const std::int64_t budget_fast = fast_budget;
-  // spread k SLOW layers evenly: every copy gets the most neighbouring compute to hide under
-  for (int j = 0; j < k; ++j) pl[static_cast<std::size_t>((static_cast<long long>(j) * n) / k)] = 1;
+  // spread k SLOW layers evenly, half a stride in: every copy gets the most neighbouring
+  // compute to hide under, and layer 0 -- whose Fn load would open the step and whose
+  // write-back would close it with nothing to overlap -- stays resident when k < n
+  for (int j = 0; j < k; ++j) pl[static_cast<std::size_t>((static_cast<long long>(2 * j + 1) * n) / (2 * k))] = 1;
   std::int64_t fast = 0;
   for (int i = 0; i < n; ++i)
     if (!pl[static_cast<std::size_t>(i)]) fast += 18 * layer_params[static_cast<std::size_t>(i)];
@@ -204,7 +212,10 @@ void Model::offload_setup(const std::vector<int>& slow, int ring_slots) {
   st->stride = layer_stride_;
   {
     const char* e = std::getenv("P2R_OFFLOAD_FN_SHADOW");
-    st->fwd_master = !(e != nullptr && e[0] == '1');
+    const char* m = std::getenv("P2R_OFFLOAD_FN_MASTER");
+    // default: the bf16-shadow form (H2D 14 B/param = D2H 14 B/param per step with the
+    // optimizer); the master form moves 16 in / 12 out
+    st->fwd_master = (m != nullptr && m[0] == '1') || (e != nullptr && e[0] == '0');
   }
   st->slot_of.assign(static_cast<std::size_t>(n_owned_), -1);
   st->slot_fwd.assign(static_cast<std::size_t>(n_owned_), -1);
@@ -241,8 +252,10 @@ void Model::offload_setup(const std::vector<int>& slow, int ring_slots) {
     cuda_check(cudaEventCreateWithFlags(&s.free_ev, cudaEventDisableTiming), "event");
   }
   st->wb_ev.resize(static_cast<std::size_t>(n_owned_));
+  st->wb_fn_ev.resize(static_cast<std::size_t>(n_owned_));
   st->wb_recorded.assign(static_cast<std::size_t>(n_owned_), 0);
   for (auto& e : st->wb_ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  for (auto& e : st->wb_fn_ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   cuda_check(cudaStreamCreateWithFlags(&st->h2d, cudaStreamNonBlocking), "h2d stream");
   cuda_check(cudaStreamCreateWithFlags(&st->d2h, cudaStreamNonBlocking), "d2h stream");
   off_ = std::move(st);
@@ -316,28 +329,37 @@ void Model::offload_prefetch_next(int /*after*/, bool /*backward*/) {
     sl.layer = o;
     (bwd ? st.slot_bwd : st.slot_fwd)[static_cast<std::size_t>(o)] = si;
     if (sl.free_recorded) cuda_check(cudaStreamWaitEvent(st.h2d, sl.free_ev, 0), "wait slot free");
-    if (st.wb_recorded[static_cast<std::size_t>(o)])
-      cuda_check(cudaStreamWaitEvent(st.h2d, st.wb_ev[static_cast<std::size_t>(o)], 0), "wait write-back");
+    // a reload waits for the previous write-back of what it reads: a shadow-form
+    // forward only for the bf16 shadow (written back first), anything else for all
+    if (st.wb_recorded[static_cast<std::size_t>(o)]) {
+      const bool fn_shadow = !bwd && !st.fwd_master;
+      cuda_check(cudaStreamWaitEvent(st.h2d, (fn_shadow ? st.wb_fn_ev : st.wb_ev)[static_cast<std::size_t>(o)], 0),
+                 "wait write-back");
+    }
     cudaEvent_t a = st.ev(), b = st.ev();
     cuda_check(cudaEventRecord(a, st.h2d), "event");
-    if (!bwd && st.fwd_master) {
-      // Fn: fp32 master (the bf16 operand is re-derived on the device at acquire)
-      copy_async(st, sl.p32.p, slow_host_p32(o), g * 4, st.h2d, true, &st.stats.fn_load);
-    } else if (!bwd) {
-      // Fn: the bf16 shadow feeds every GEMM; fp32 is only read for the vectors
-      // (LN gains/biases, biases) and the fp32 MoE gate
-      copy_async(st, sl.p16.p, slow_host_p16(o), g * 2, st.h2d, true, &st.stats.fn_load);
+    // The fp32 master is needed by the backward that runs the fused AdamW; every other
+    // use (forward, and backward micro-steps that only accumulate) reads the bf16
+    // shadow for the GEMMs and fp32 only for the vectors (LN gains / biases, biases)
+    // and the fp32 MoE gate -- unless the master form is selected.
+    const bool applies = bwd && has_opt_ && micro_ == accum_n_;
+    const bool shadow = !st.fwd_master && !applies;
+    double* ctr = bwd ? &st.stats.bn_load : &st.stats.fn_load;
+    sl.p16_loaded = shadow;
+    if (!shadow) {
+      copy_async(st, sl.p32.p, slow_host_p32(o), g * 4, st.h2d, true, ctr);
+    } else {
+      copy_async(st, sl.p16.p, slow_host_p16(o), g * 2, st.h2d, true, ctr);
       for (const auto& sg : layer_.segs) {
         const bool fp32_use = !sg.decay || (cfg_.moe.enabled() && sg.off == layer_.gate);
         if (!fp32_use) continue;
         copy_async(st, sl.p32.as<float>() + sg.off, slow_host_p32(o) + sg.off, static_cast<std::size_t>(sg.len) * 4,
-                   st.h2d, true, &st.stats.fn_load);
+                   st.h2d, true, ctr);
       }
-    } else {
-      // Bn + An: fp32 master (bf16 shadow re-derived on the device) + moments; the
-      // moments only in the micro-step that runs the fused AdamW
-      copy_async(st, sl.p32.p, slow_host_p32(o), g * 4, st.h2d, true, &st.stats.bn_load);
-      if (has_opt_ && micro_ == accum_n_) {
+    }
+    if (bwd) {
+      // An: the moments only in the micro-step that runs the fused AdamW
+      if (applies) {
         copy_async(st, sl.m.p, slow_host_m(o, 0), g * 4, st.h2d, true, &st.stats.opt_load);
         copy_async(st, sl.v.p, slow_host_m(o, 1), g * 4, st.h2d, true, &st.stats.opt_load);
       }
@@ -367,7 +389,7 @@ void Model::offload_acquire(int o, bool backward) {
   st.slot_of[static_cast<std::size_t>(o)] = si;
   OffloadSlot& sl = st.slots[static_cast<std::size_t>(si)];
   cuda_check(cudaStreamWaitEvent(stream_, sl.loaded, 0), "wait loaded");
-  if (backward || st.fwd_master)
+  if (!sl.p16_loaded)  // the master was staged: derive the bf16 operand on the device
     p2r_check(p2r_cast_bf16(sl.p32.as<float>(), sl.p16.p, layer_stride_, stream_), "offload bf16 operand");
   if (backward && !sl.grads_loaded) cuda_check(cudaMemsetAsync(sl.g32.p, 0, sl.g32.bytes, stream_), "zero slot grads");
 }
@@ -411,8 +433,20 @@ void Model::offload_release(int o, bool backward) {
   cuda_check(cudaEventRecord(a, st.d2h), "event");
   st.hgrad_valid[static_cast<std::size_t>(o)] = apply ? 0 : 1;
   if (apply) {
+    // what a shadow-form forward reloads first (the bf16 shadow and the fp32 vectors /
+    // gate): the next step's forward waits only for these, so the fp32 master and the
+    // moments drain under that forward instead of stalling it
+    if (!st.fwd_master) {
+      copy_async(st, slow_host_p16(o), sl.p16.p, g * 2, st.d2h, false, &st.stats.writeback);
+      for (const auto& sg : layer_.segs) {
+        const bool fp32_use = !sg.decay || (cfg_.moe.enabled() && sg.off == layer_.gate);
+        if (fp32_use)
+          copy_async(st, slow_host_p32(o) + sg.off, sl.p32.as<float>() + sg.off, static_cast<std::size_t>(sg.len) * 4,
+                     st.d2h, false, &st.stats.writeback);
+      }
+    }
+    cuda_check(cudaEventRecord(st.wb_fn_ev[static_cast<std::size_t>(o)], st.d2h), "event");
     copy_async(st, slow_host_p32(o), sl.p32.p, g * 4, st.d2h, false, &st.stats.writeback);
-    if (!st.fwd_master) copy_async(st, slow_host_p16(o), sl.p16.p, g * 2, st.d2h, false, &st.stats.writeback);
     copy_async(st, slow_host_m(o, 0), sl.m.p, g * 4, st.d2h, false, &st.stats.writeback);
     copy_async(st, slow_host_m(o, 1), sl.v.p, g * 4, st.d2h, false, &st.stats.writeback);
   } else {
@@ -421,6 +455,8 @@ void Model::offload_release(int o, bool backward) {
       cuda_check(cudaMallocHost(reinterpret_cast<void**>(&st.hg), n * 4), "pinned grads");
       std::memset(st.hg, 0, n * 4);
     }
+    // (the weights are unchanged: the next micro-step's forward needs no wait)
+    cuda_check(cudaEventRecord(st.wb_fn_ev[static_cast<std::size_t>(o)], st.d2h), "event");
     copy_async(st, slow_host_grad(o), sl.g32.p, g * 4, st.d2h, false, &st.stats.grad_offload);
   }
   cuda_check(cudaEventRecord(b, st.d2h), "event");

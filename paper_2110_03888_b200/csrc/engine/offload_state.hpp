@@ -15,6 +15,7 @@ struct OffloadSlot {
   cudaEvent_t loaded = nullptr, free_ev = nullptr;
   bool free_recorded = false;
   bool grads_loaded = false;  // Bn staging brought the layer's parked partial gradients
+  bool p16_loaded = false;    // staged as bf16 shadow + fp32 vectors (no master)
 };
 
 struct OffloadState {
@@ -30,7 +31,8 @@ struct OffloadState {
   std::vector<int> host_idx;   // owned layer -> index in host arrays or -1
   std::vector<int> slow_list;  // SLOW owned layers, ascending
   std::vector<char> hgrad_valid;  // owned layer -> host holds its partial gradients (accumulation)
-  std::vector<cudaEvent_t> wb_ev;
+  std::vector<cudaEvent_t> wb_ev;     // owned layer -> its last write-back complete
+  std::vector<cudaEvent_t> wb_fn_ev;  // ... its bf16 shadow written back (what a forward reloads)
   std::vector<char> wb_recorded;
   float* hp32 = nullptr;
   std::uint16_t* hp16 = nullptr;
@@ -42,11 +44,11 @@ struct OffloadState {
   int next_slot = 0;
   bool training = false;
   bool skip = false;
-  // Fn loads the fp32 master and re-derives the bf16 operand on the device, so the
-  // write-back drops the bf16 shadow: +2 B/param H2D in the forward (whose H2D
-  // stream is otherwise idle), -2 B/param D2H in the backward (the busier
-  // direction). P2R_OFFLOAD_FN_SHADOW=1 keeps the bf16-shadow form.
-  bool fwd_master = true;
+  // Master form (P2R_OFFLOAD_FN_MASTER=1): Fn loads the fp32 master and re-derives the
+  // bf16 operand on the device, so the write-back drops the bf16 shadow (H2D 16, D2H
+  // 12 B/param per step). Default shadow form: Fn (and accumulating Bn) load the bf16
+  // shadow + fp32 vectors, the write-back includes the shadow (14 / 14 B/param).
+  bool fwd_master = false;
   OffloadStats stats;
   struct CopyRec {
     cudaEvent_t a, b;
@@ -72,6 +74,7 @@ struct OffloadState {
       if (s.free_ev) cudaEventDestroy(s.free_ev);
     }
     for (cudaEvent_t e : wb_ev) cudaEventDestroy(e);
+    for (cudaEvent_t e : wb_fn_ev) cudaEventDestroy(e);
     for (cudaEvent_t e : pool) cudaEventDestroy(e);
     for (void* p : {static_cast<void*>(hp32), static_cast<void*>(hp16), static_cast<void*>(hm),
                     static_cast<void*>(hv), static_cast<void*>(hg)})

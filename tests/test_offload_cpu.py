@@ -77,9 +77,9 @@ def test_overlap_planner():
     assert p2r.plan_offload_overlap([P] * 16, 16 * gb, 50e9, 50e9, 2e-3, 4e-3) == [0] * 16
     # the budget covers the resident granules AND the 3 HBM staging slots
     plan = p2r.plan_offload_overlap([P] * 16, 11 * gb, 50e9, 50e9, 2e-3, 4e-3)
-    assert sum(plan) == 8 and plan == [1, 0] * 8  # fewest SLOW layers, spread evenly
+    assert sum(plan) == 8 and plan == [0, 1] * 8  # fewest SLOW layers, spread evenly, layer 0 resident
     plan = p2r.plan_offload_overlap([P] * 16, 15 * gb, 50e9, 50e9, 2e-3, 4e-3)
-    assert sum(plan) == 4 and plan == [1, 0, 0, 0] * 4
+    assert sum(plan) == 4 and plan == [0, 0, 1, 0] * 4
     for budget in (5, 8, 11, 13, 15):
         for ring in (2, 3, 4):
             plan = p2r.plan_offload_overlap([P] * 16, budget * gb, 50e9, 50e9, 2e-3, 4e-3, ring_slots=ring)

@@ -28,8 +28,8 @@ def lm_batch(batch, seq, seed=7):
                          ids=["moe_mixed_ring2", "dense_mixed_ring3", "dense_all_slow"])
 @pytest.mark.parametrize("fn_form", ["master", "shadow"])
 def test_offload_bit_identical_training(cuda, cfgd, plan, ring, fn_form, monkeypatch):
-    """fn_form: the forward loads the fp32 master (default) or the bf16 shadow
-    (P2R_OFFLOAD_FN_SHADOW=1, read when the offloaded model is created)."""
+    """fn_form: the forward loads the bf16 shadow + fp32 vectors (default) or the fp32
+    master (P2R_OFFLOAD_FN_SHADOW=0, read when the offloaded model is created)."""
     monkeypatch.setenv("P2R_OFFLOAD_FN_SHADOW", "1" if fn_form == "shadow" else "0")
     import paper_2110_03888_b200 as p2r
     cfg = p2r.Config(**cfgd)
@@ -71,7 +71,8 @@ def test_offload_bit_identical_training(cuda, cfgd, plan, ring, fn_form, monkeyp
     assert st["Fn_load"] == 3 * ns * ((g * 2 + fp32_elems * 4) if shadow else g * 4)
     assert st["Bn_load"] == 3 * ns * g * 4
     assert st["opt_load"] == 3 * ns * g * 8
-    assert st["writeback"] == 3 * ns * g * (14 if shadow else 12)
+    # (the shadow form writes the fp32 vectors back ahead of the master, with the shadow)
+    assert st["writeback"] == 3 * ns * (g * 14 + fp32_elems * 4 if shadow else g * 12)
     assert st["h2d_ms"] > 0 and st["d2h_ms"] > 0
 
 

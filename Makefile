@@ -14,7 +14,14 @@ CU_OBJS := $(patsubst $(CSRC)/%.cu,$(BUILD)/%.o,$(CU_SRCS))
 CPP_OBJS:= $(patsubst $(CSRC)/engine/%.cpp,$(BUILD)/engine/%.o,$(CPP_SRCS))
 LIB     := $(PKG)/libp2r.so
 
-all: $(LIB)
+DROPIN  := $(BUILD)/dropin_mini_controller
+
+all: $(LIB) $(DROPIN)
+
+# a reference-style controller compiled against the drop-in headers, linked with libp2r.so
+$(DROPIN): tests/dropin/mini_controller.cpp $(LIB) $(wildcard include/p2r/*.hpp)
+	@mkdir -p $(dir $@)
+	$(CXX) -std=c++20 -O2 -Wall -Iinclude -o $@ $< -L$(PKG) -l:libp2r.so -Wl,-rpath,'$$ORIGIN/../$(PKG)'
 
 $(BUILD)/%.o: $(CSRC)/%.cu $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h) include/p2r_cuda.h
 	@mkdir -p $(dir $@)

@@ -1,7 +1,9 @@
-// C++ host engine: the reference's layer/step API (model.hpp, optim.hpp,
-// tensor.hpp of /root/reference/proj/core) re-implemented over the sm_100a
-// kernel layer (p2r_cuda.h). Same class / method names and error behaviour;
-// tensors live on the device.
+// C++ host engine of the B200 build: parameters in device granules, the
+// reference's layer/step semantics (model.hpp, optim.hpp, tensor.hpp of
+// /root/reference/proj/core) as fused sm_100a kernel sequences (p2r_cuda.h),
+// granular offload, expert / data parallelism, checkpoints. The drop-in classes
+// with the reference's exact declarations (p2r/model.hpp, optim.hpp, tensor.hpp)
+// are handles on this engine; the C-ABI (p2r_engine.h) exposes it to C / ctypes.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -14,42 +16,9 @@
 #include <string>
 #include <vector>
 
+#include "p2r/model.hpp"
+
 namespace p2r {
-
-// ---------------------------------------------------------------- configs
-struct MoEConfig {  // model.hpp:13-22
-  int n_experts = 0;
-  int n_prototypes = 1;
-  int n_shards = 1;
-  float capacity_factor = 1.25f;
-  bool enabled() const { return n_experts > 0; }
-  int group_size() const { return n_experts / n_prototypes; }
-  void validate() const;
-};
-
-struct ModelConfig {  // model.hpp:27-41
-  int d_model = 128;
-  int d_ff = 512;
-  int n_layers_graph = 8;
-  int n_layers_params = 8;
-  int n_heads = 4;
-  int vocab_size = 260;
-  int seq_len = 64;
-  MoEConfig moe;
-  bool shared() const { return n_layers_params == 1 && n_layers_graph > 1; }
-  void validate() const;
-  ModelConfig as_shared() const;
-  ModelConfig as_unshared() const;
-};
-
-struct ParamCounts {
-  std::int64_t embedding_params = 0;
-  std::int64_t per_layer_params = 0;
-  std::int64_t total_params = 0;
-};
-ParamCounts count_params(const ModelConfig& config);
-
-enum class AttentionMode { Causal, Full };
 
 // Reference-compatible per-tensor init (model.cpp:11-36).
 std::uint64_t init_mix_seed(std::uint64_t seed, const std::string& name);
@@ -73,29 +42,12 @@ struct DevBuf {
 
 // Device activation handle (fp32, row-major [rows, cols]); `grad` is the
 // gradient buffer the backward closures read/write.
-struct Tensor {
+struct DevTensor {
   int rows = 0, cols = 0;
   float* data = nullptr;
   float* grad = nullptr;
   void* grad16 = nullptr;  // bf16 shadow of grad (GEMM operand)
   bool defined() const { return data != nullptr; }
-};
-
-// tensor.hpp:70-82: closures replayed once in reverse order.
-class GradTape {
- public:
-  void record(std::function<void()> fn) { entries_.push_back(std::move(fn)); }
-  void backward() {
-    for (auto it = entries_.rbegin(); it != entries_.rend(); ++it) (*it)();
-  }
-  // The fused cross-entropy already produced dlogits for dL = 1, which is
-  // exactly what backward_scalar seeds (tensor.cpp:110-114).
-  void backward_scalar(Tensor& /*loss*/) { backward(); }
-  void clear() { entries_.clear(); }
-  std::size_t size() const { return entries_.size(); }
-
- private:
-  std::vector<std::function<void()>> entries_;
 };
 
 // One parameter as the reference names it, viewed inside a granule buffer.
@@ -228,7 +180,7 @@ SwitchDecision switch_criterion(const std::vector<double>& pseudo_t, const std::
                                 const SwitchPolicy& policy);
 bool switch_evaluation_due(const SwitchPolicy& policy, std::int64_t step);
 
-class Model;
+class Engine;
 // SPEC delink(pseudo_checkpoint) -> Checkpoint: load a PSEUDO
 // checkpoint, delink (weights + moments copied into every layer), save it as REAL.
 StageState delink_checkpoint(const std::string& in_path, const std::string& out_path);
@@ -238,20 +190,20 @@ StageState delink_checkpoint(const std::string& in_path, const std::string& out_
 // replicated buffers from shard 0; config n_shards = W2). Host file I/O only.
 void redistribute_checkpoints(const std::vector<std::string>& in_paths, const std::vector<std::string>& out_paths);
 
-class Model {
+class Engine {
  public:
-  Model(ModelConfig config, std::uint64_t seed);
+  Engine(ModelConfig config, std::uint64_t seed);
   // Real model with granular CPU offload: slow[i] = 1 keeps owned layer i in
   // pinned host DRAM and streams it through `ring_slots` HBM staging slots.
-  Model(ModelConfig config, std::uint64_t seed, const std::vector<int>& slow, int ring_slots);
+  Engine(ModelConfig config, std::uint64_t seed, const std::vector<int>& slow, int ring_slots);
   // Expert-parallel shard `ep_rank` of `ep_world`: holds experts
   // [ep_rank*E/W, (ep_rank+1)*E/W) (model.cpp:334-340) + the replicated rest.
-  Model(ModelConfig config, std::uint64_t seed, int ep_world, int ep_rank);
+  Engine(ModelConfig config, std::uint64_t seed, int ep_world, int ep_rank);
   // Both: an expert-parallel shard whose SLOW layer granules (replicated part +
   // local experts) live in pinned host DRAM (C5: 96-layer MoE over 8 GPUs).
-  Model(ModelConfig config, std::uint64_t seed, const std::vector<int>& slow, int ring_slots, int ep_world,
+  Engine(ModelConfig config, std::uint64_t seed, const std::vector<int>& slow, int ring_slots, int ep_world,
         int ep_rank);
-  ~Model();
+  ~Engine();
 
   // NCCL (one communicator per model over all ranks; csrc/engine/comm.cpp)
   void comm_init(const char* unique_id128);
@@ -265,8 +217,8 @@ class Model {
   // Dense layers take db2 from the column sums staged by the LayerNorm backward that
   // produced their output gradient (wider rows would spill its extra accumulators).
   bool db2_fused() const { return !cfg_.moe.enabled() && cfg_.d_model <= 13 * 128; }
-  Model(const Model&) = delete;
-  Model& operator=(const Model&) = delete;
+  Engine(const Engine&) = delete;
+  Engine& operator=(const Engine&) = delete;
 
   const ModelConfig& config() const { return cfg_; }
   int n_graph_layers() const { return cfg_.n_layers_graph; }
@@ -274,13 +226,13 @@ class Model {
   int owned_index_of_graph_layer(int g) const { return cfg_.shared() || n_owned_ == 1 ? 0 : g; }
 
   // segmented API (model.hpp:101-106); token / target / mask pointers are device arrays
-  Tensor embed_forward(GradTape* tape, const int* d_tokens, int batch, int seq);
-  Tensor block_forward(GradTape* tape, int graph_layer, const Tensor& x, int batch,
+  DevTensor embed_forward(GradTape* tape, const int* d_tokens, int batch, int seq);
+  DevTensor block_forward(GradTape* tape, int graph_layer, const DevTensor& x, int batch,
                        AttentionMode mode);
-  Tensor head_forward(GradTape* tape, const Tensor& x);
+  DevTensor head_forward(GradTape* tape, const DevTensor& x);
   // fused softmax_cross_entropy(mask, denom) (tensor.cpp:670-723); returns a
   // 1-element device tensor
-  Tensor softmax_cross_entropy(GradTape* tape, const Tensor& logits, const int* d_targets,
+  DevTensor softmax_cross_entropy(GradTape* tape, const DevTensor& logits, const int* d_targets,
                                const std::uint8_t* d_mask, double denom);
 
   // whole micro-step (controller CS-1)
@@ -312,7 +264,7 @@ class Model {
   std::int64_t state_bytes() const;
   bool has_optimizer() const { return has_opt_; }
 
-  std::unique_ptr<Model> delinked() const;
+  std::unique_ptr<Engine> delinked() const;
 
   // expert sharding bookkeeping (model.cpp:334-356): expert e lives on shard
   // e / (E / n_shards). In one process re-sharding is bookkeeping (outputs are
@@ -331,7 +283,7 @@ class Model {
   // Load into this model (config and EP shard must match); attaches AdamW if the
   // file carries moments and the optimizer is not attached yet.
   StageState load_checkpoint(const std::string& path);
-  static std::unique_ptr<Model> from_checkpoint(const std::string& path, StageState* st);
+  static std::unique_ptr<Engine> from_checkpoint(const std::string& path, StageState* st);
 
   cudaStream_t stream() const { return stream_; }
   // train_step_device replayed as one CUDA graph (captured on the first call,
@@ -344,6 +296,17 @@ class Model {
   void profile(int cls, std::int64_t* launches, double* ms, double* flops, double* bytes);
   void profile_reset();
   void buffer(int which, void** ptr, std::size_t* bytes) const;
+
+  // drop-in API support (p2r/model.hpp): a counter bumped by every call that may
+  // change device state (host copies of device tensors are cached per version), and
+  // device staging of the segmented API's token ids / targets / mask (validated)
+  std::uint64_t version() const { return version_; }
+  const int* stage_tokens(const int* host, int batch, int seq);
+  void stage_targets(const int* targets, const std::uint8_t* mask, int n, const int** d_targets,
+                     const std::uint8_t** d_mask);
+  // copy a host activation [T, d] into the embedding output buffer (block_forward on a host tensor)
+  float* stage_activation(const float* host, int rows);
+  int vocab_ld() const;  // leading dimension of the device logits
 
   // granular offload
   bool offloaded() const { return off_ != nullptr; }
@@ -373,7 +336,7 @@ class Model {
 
  private:
   struct NoInit {};
-  Model(ModelConfig config, NoInit, int ep_world = 1, int ep_rank = 0, bool force_ep = false);
+  Engine(ModelConfig config, NoInit, int ep_world = 1, int ep_rank = 0, bool force_ep = false);
   // offload plumbing (csrc/engine/offload.cpp)
   void offload_setup(const std::vector<int>& slow, int ring_slots);
   void offload_begin_forward(bool training);
@@ -458,6 +421,7 @@ class Model {
     const void* ws = nullptr;
   } step_graph_;
   std::uint64_t acts_gen_ = 0;  // bumped whenever ensure_acts reallocates the activation buffers
+  std::uint64_t version_ = 1;
   float offload_lr_ = std::numeric_limits<float>::quiet_NaN();  // set_offload_lr() before use
   int accum_n_ = 1;            // micro-steps per optimizer step (offload)
   int micro_ = 0;              // micro-steps since zero_grads

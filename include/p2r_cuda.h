@@ -234,6 +234,41 @@ p2r_status p2r_ep_pack(const void* slots, const int* counts, int d, int seg, int
 p2r_status p2r_ep_return_rows(const void* compact, const int* prefix, int d, int seg, int El, int W, int rank,
                               void* const* peer_dst, void* stream);
 
+/* ------------------------------------------------------------------------ */
+/* Primitive layer of the drop-in tensor API (include/p2r/tensor.hpp):       */
+/* generic-shape fp32 kernels for the reference's primitives and their        */
+/* backward (tensor.cpp:131-723), deterministic reduction order. Not on the   */
+/* training hot path (that is the fused bf16 layer above).                    */
+/* ------------------------------------------------------------------------ */
+/* C = op(A) op(B) + beta C; op = transpose when ta / tb; batched with strides */
+p2r_status p2r_prim_gemm_f32(int ta, int tb, int m, int n, int k, const float* a, int lda, const float* b, int ldb,
+                             float* c, int ldc, float beta, int batch, long long sa, long long sb, long long sc,
+                             void* stream);
+/* op 0: out = a + b; 1: out += a; 2: out = gelu(a); 3: out += b * gelu'(a) */
+p2r_status p2r_prim_ew(int op, long long n, const float* a, const float* b, float* out, void* stream);
+p2r_status p2r_prim_bias(int rows, int n, const float* x, const float* b, float* out, void* stream);
+p2r_status p2r_prim_colsum_acc(int rows, int n, const float* g, float* out, void* stream);
+p2r_status p2r_prim_layernorm_fwd(int rows, int d, const float* x, const float* gain, const float* bias, float eps,
+                                  float* y, float* xhat, float* inv, void* stream);
+p2r_status p2r_prim_layernorm_bwd(int rows, int d, const float* gy, const float* xhat, const float* inv,
+                                  const float* gain, float* gx, float* ggain, float* gbias, void* stream);
+p2r_status p2r_prim_gather_rows(int n_out, int d, const float* x, const int* rows, float* out, void* stream);
+p2r_status p2r_prim_scatter_rows_acc(int n, int d, const float* g, const int* rows, float* gx, void* stream);
+/* dir 0: [B*S, H*hd] -> [B, H, S, hd]; 1: inverse; acc: out += */
+p2r_status p2r_prim_permute_heads(int dir, int acc, int B, int H, int S, int hd, const float* in, float* out,
+                                  void* stream);
+p2r_status p2r_prim_softmax_rows(long long rows, int n, int causal_S, float* x, void* stream);
+p2r_status p2r_prim_softmax_bwd_rows(long long rows, int n, const float* p, const float* dp, float* ds, void* stream);
+/* dir 0: out = weights from logits; dir 1: out(glogits) += backward of w given gw */
+p2r_status p2r_prim_selected_softmax(int dir, int T, int E, int k, const float* logits_or_w, const float* gw,
+                                     const int* sel, const uint8_t* surv, float* out, void* stream);
+p2r_status p2r_prim_combine_fwd(int T, int d, int k, const int* off, const int* crow, const int* cslot,
+                                const float* y, const float* w, float* out, void* stream);
+p2r_status p2r_prim_combine_bwd(int R, int d, int k, const int* rtok, const int* rslot, const float* dout,
+                                const float* y, const float* w, float* dy, float* dw, void* stream);
+p2r_status p2r_prim_cross_entropy(int rows, int V, const float* logits, const int* targets, const uint8_t* mask,
+                                  double denom, double* row_loss_ws, float* loss, float* glogits, void* stream);
+
 /* out = stage[0] + stage[1] + ... + stage[W-1] (fp32 [W][n], rank order): the
  * deterministic sum of a loopback group's data-parallel all-reduce. */
 p2r_status p2r_sum_ranks(const float* stage, int W, long long n, float* out, void* stream);

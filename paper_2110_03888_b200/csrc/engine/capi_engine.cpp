@@ -10,7 +10,7 @@
 #include "p2r_engine.h"
 
 struct p2r_model {
-  std::unique_ptr<p2r::Model> m;
+  std::unique_ptr<p2r::Engine> m;
 };
 struct p2r_loopback {
   std::unique_ptr<p2r::LoopbackGroup> g;
@@ -70,7 +70,7 @@ p2r_status p2r_count_params(const p2r_model_config* cfg, int64_t* out3) {
 p2r_status p2r_model_create(const p2r_model_config* cfg, uint64_t seed, p2r_model** out) {
   return guard([&] {
     auto h = std::make_unique<p2r_model>();
-    h->m = std::make_unique<p2r::Model>(to_cfg(cfg), seed);
+    h->m = std::make_unique<p2r::Engine>(to_cfg(cfg), seed);
     *out = h.release();
   });
 }
@@ -210,7 +210,7 @@ p2r_status p2r_model_from_checkpoint(const char* path, p2r_model** out, p2r_stag
     if (!path) throw std::invalid_argument("checkpoint: null path");
     p2r::StageState st;
     auto h = std::make_unique<p2r_model>();
-    h->m = p2r::Model::from_checkpoint(path, &st);
+    h->m = p2r::Engine::from_checkpoint(path, &st);
     from_state(st, st_out);
     *out = h.release();
   });
@@ -330,7 +330,7 @@ p2r_status p2r_comm_unique_id(char* out128) {
 p2r_status p2r_model_create_ep(const p2r_model_config* cfg, uint64_t seed, int world, int rank, p2r_model** out) {
   return guard([&] {
     auto h = std::make_unique<p2r_model>();
-    h->m = std::make_unique<p2r::Model>(to_cfg(cfg), seed, world, rank);
+    h->m = std::make_unique<p2r::Engine>(to_cfg(cfg), seed, world, rank);
     *out = h.release();
   });
 }
@@ -361,7 +361,7 @@ p2r_status p2r_model_create_offload(const p2r_model_config* cfg, uint64_t seed, 
     const int n = cfg->n_layers_params;
     std::vector<int> pl(slow, slow + n);
     auto h = std::make_unique<p2r_model>();
-    h->m = std::make_unique<p2r::Model>(to_cfg(cfg), seed, pl, ring_slots);
+    h->m = std::make_unique<p2r::Engine>(to_cfg(cfg), seed, pl, ring_slots);
     *out = h.release();
   });
 }
@@ -371,7 +371,7 @@ p2r_status p2r_model_create_offload_ep(const p2r_model_config* cfg, uint64_t see
     const int n = cfg->n_layers_params;
     std::vector<int> pl(slow, slow + n);
     auto h = std::make_unique<p2r_model>();
-    h->m = std::make_unique<p2r::Model>(to_cfg(cfg), seed, pl, ring_slots, world, rank);
+    h->m = std::make_unique<p2r::Engine>(to_cfg(cfg), seed, pl, ring_slots, world, rank);
     *out = h.release();
   });
 }

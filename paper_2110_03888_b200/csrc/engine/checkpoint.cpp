@@ -272,7 +272,7 @@ int expert_of(const std::string& name) {
 
 }  // namespace
 
-void Model::save_checkpoint(const std::string& path, const StageState& st) const {
+void Engine::save_checkpoint(const std::string& path, const StageState& st) const {
   // buffer list: every parameter, then AdamW m and v (when attached), for_each order
   std::vector<BufferEntry> bufs;
   std::vector<std::pair<int, int>> src;  // (param index, kind: 0 param, 1 m, 2 v)
@@ -307,7 +307,7 @@ void Model::save_checkpoint(const std::string& path, const StageState& st) const
   });
 }
 
-StageState Model::load_checkpoint(const std::string& path) {
+StageState Engine::load_checkpoint(const std::string& path) {
   std::ifstream f(path, std::ios::binary);
   const Manifest m = read_manifest(f, path);
   if (config_line(m.cfg) != config_line(cfg_))
@@ -365,13 +365,13 @@ StageState Model::load_checkpoint(const std::string& path) {
   return m.st;
 }
 
-std::unique_ptr<Model> Model::from_checkpoint(const std::string& path, StageState* st) {
+std::unique_ptr<Engine> Engine::from_checkpoint(const std::string& path, StageState* st) {
   Manifest m;
   {
     std::ifstream f(path, std::ios::binary);
     m = read_manifest(f, path);
   }
-  std::unique_ptr<Model> model(new Model(m.cfg, NoInit{}, m.ep_world, m.ep_rank));
+  std::unique_ptr<Engine> model(new Engine(m.cfg, NoInit{}, m.ep_world, m.ep_rank));
   const StageState s = model->load_checkpoint(path);
   if (st) *st = s;
   return model;
@@ -379,28 +379,28 @@ std::unique_ptr<Model> Model::from_checkpoint(const std::string& path, StageStat
 
 StageState delink_checkpoint(const std::string& in_path, const std::string& out_path) {
   StageState st;
-  std::unique_ptr<Model> pseudo = Model::from_checkpoint(in_path, &st);
+  std::unique_ptr<Engine> pseudo = Engine::from_checkpoint(in_path, &st);
   if (st.stage != 0) throw std::logic_error("delink: checkpoint is not in the PSEUDO stage");
-  std::unique_ptr<Model> real = pseudo->delinked();  // weights + moments into every layer
+  std::unique_ptr<Engine> real = pseudo->delinked();  // weights + moments into every layer
   st.stage = 1;
   real->save_checkpoint(out_path, st);
   return st;
 }
 
-int Model::expert_shard(int expert) const {
+int Engine::expert_shard(int expert) const {
   if (!cfg_.moe.enabled()) throw std::logic_error("expert_shard: dense model");
   if (expert < 0 || expert >= cfg_.moe.n_experts) throw std::out_of_range("expert_shard: expert index");
   return expert / (cfg_.moe.n_experts / cfg_.moe.n_shards);
 }
 
-std::vector<std::vector<int>> Model::shard_layout() const {
+std::vector<std::vector<int>> Engine::shard_layout() const {
   if (!cfg_.moe.enabled()) throw std::logic_error("shard_layout: dense model");
   std::vector<std::vector<int>> layout(static_cast<std::size_t>(cfg_.moe.n_shards));
   for (int e = 0; e < cfg_.moe.n_experts; ++e) layout[static_cast<std::size_t>(expert_shard(e))].push_back(e);
   return layout;
 }
 
-void Model::redistribute_experts(int new_n_shards) {
+void Engine::redistribute_experts(int new_n_shards) {
   if (!cfg_.moe.enabled()) throw std::logic_error("redistribute_experts: dense model");
   if (new_n_shards <= 0 || cfg_.moe.n_experts % new_n_shards != 0)
     throw std::invalid_argument("redistribute_experts: n_experts must be divisible by new shard count");

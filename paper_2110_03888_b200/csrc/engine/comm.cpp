@@ -1,6 +1,6 @@
 // The two parallel dimensions of the step:
 //   * expert parallelism: expert e lives on rank e / (E / W) (the contiguous map
-//     of Model::expert_shard, model.cpp:334-340). Dispatch / combine (and their
+//     of Engine::expert_shard, model.cpp:334-340). Dispatch / combine (and their
 //     transposes in the backward) are peer-store kernels (csrc/ep.cu) that write
 //     the routed rows straight into the other ranks' arenas; completion is a flag
 //     per (channel, source) in the receiver's arena, written with a stream memory
@@ -145,7 +145,7 @@ void comm_unique_id(char* out128) {
   std::memcpy(out128, u.b, 128);
 }
 
-void Model::comm_init(const char* id128) {
+void Engine::comm_init(const char* id128) {
   if (comm_ || loop_) return;
   NcclUid u{};
   std::memcpy(u.b, id128, 128);
@@ -155,14 +155,14 @@ void Model::comm_init(const char* id128) {
   comm_ = c;
 }
 
-void Model::comm_init_loopback(LoopbackGroup* group) {
+void Engine::comm_init_loopback(LoopbackGroup* group) {
   if (comm_ || loop_) throw std::logic_error("comm_init: communicator already initialised");
   if (group == nullptr || group->world != ep_world_)
     throw std::invalid_argument("loopback group: world size does not match the model's");
   loop_ = group;
 }
 
-void Model::comm_destroy() {
+void Engine::comm_destroy() {
   if (comm_ && nccl().commDestroy) nccl().commDestroy(comm_);
   comm_ = nullptr;
   loop_ = nullptr;
@@ -170,7 +170,7 @@ void Model::comm_destroy() {
 
 // ---------------------------------------------------------------- expert parallel arena
 // Called from ensure_acts on every rank (collective: same shapes everywhere).
-void Model::ep_connect(int seg, int n_ye) {
+void Engine::ep_connect(int seg, int n_ye) {
   const int W = ep_world_, E = cfg_.moe.n_experts, El = E / W, d = cfg_.d_model;
   if (W > 1 && comm_ == nullptr && loop_ == nullptr)
     throw std::logic_error("expert parallel: call comm_init before the first step");
@@ -225,13 +225,13 @@ void Model::ep_connect(int seg, int n_ye) {
   ep_ = std::move(st);
 }
 
-void* Model::ep_peer(int q, std::size_t off) const { return ep_->peer[static_cast<std::size_t>(q)] + off; }
-void* Model::ep_local(std::size_t off) const { return ep_->arena.as<char>() + off; }
+void* Engine::ep_peer(int q, std::size_t off) const { return ep_->peer[static_cast<std::size_t>(q)] + off; }
+void* Engine::ep_local(std::size_t off) const { return ep_->arena.as<char>() + off; }
 
 // Completion of this rank's stores for channel ch (0 = rows to the owners,
 // 1 = rows back to the sources): flag[ch][my rank] = epoch in every peer's arena,
 // ordered after the preceding kernels by the write's memory barrier.
-void Model::ep_signal(int ch) {
+void Engine::ep_signal(int ch) {
   const std::uint32_t epoch = ++ep_->epoch[ch];
   const int W = ep_world_;
   for (int q = 0; q < W; ++q) {
@@ -246,7 +246,7 @@ void Model::ep_signal(int ch) {
 }
 
 // Wait (on the model stream, no kernel) until every rank signalled channel ch.
-void Model::ep_wait(int ch) {
+void Engine::ep_wait(int ch) {
   const std::uint32_t epoch = ep_->epoch[ch];
   const int W = ep_world_;
   for (int w = 0; w < W; ++w) {
@@ -257,7 +257,7 @@ void Model::ep_wait(int ch) {
 }
 
 // ---------------------------------------------------------------- data parallel
-void Model::allreduce_f32(float* buf, std::size_t n) {
+void Engine::allreduce_f32(float* buf, std::size_t n) {
   if (loop_) {
     LoopbackGroup& G = *loop_;
     const int W = G.world, r = ep_rank_;
@@ -289,7 +289,7 @@ void Model::allreduce_f32(float* buf, std::size_t n) {
 
 // DP: sum the replicated gradient parts over ranks, in place, on the model stream.
 // SLOW (offloaded) granules are summed inside their backward, before the fused AdamW.
-void Model::allreduce_grads() {
+void Engine::allreduce_grads() {
   if (!comm_ && !loop_) throw std::logic_error("allreduce_grads: communicator not initialised");
   // MoE layers: everything before the expert block (norms, attention, gate) is
   // replicated; experts are sharded. Dense layers are replicated entirely.

@@ -1,4 +1,4 @@
-// Host engine: Model / GradTape / AdamW / delink over the sm_100a kernel layer.
+// Host engine: Engine / GradTape / AdamW / delink over the sm_100a kernel layer.
 //
 // Mirrors /root/reference/proj/core/src/model.cpp and optim.cpp (and the
 // absent controller's per-micro-batch step) with identical
@@ -201,10 +201,10 @@ struct Acts {
 };
 
 // ---------------------------------------------------------------- expert-parallel exchange
-std::size_t Model::ep_ye_offset(int set) const { return ep_->off_ye + ep_->ye_bytes * static_cast<std::size_t>(set); }
-std::size_t Model::ep_dxe_offset() const { return ep_->off_dxe; }
+std::size_t Engine::ep_ye_offset(int set) const { return ep_->off_ye + ep_->ye_bytes * static_cast<std::size_t>(set); }
+std::size_t Engine::ep_dxe_offset() const { return ep_->off_dxe; }
 
-void Model::ep_send(const void* src, int src_dtype, LayerActs& L, const float* w) {
+void Engine::ep_send(const void* src, int src_dtype, LayerActs& L, const float* w) {
   const int W = ep_world_, E = cfg_.moe.n_experts;
   std::vector<void*> slots(static_cast<std::size_t>(W));
   std::vector<int*> cnts(static_cast<std::size_t>(W));
@@ -220,14 +220,14 @@ void Model::ep_send(const void* src, int src_dtype, LayerActs& L, const float* w
   ep_wait(0);
 }
 
-void Model::ep_pack_rows(void* compact, LayerActs& L) {
+void Engine::ep_pack_rows(void* compact, LayerActs& L) {
   const int W = ep_world_, El = cfg_.moe.n_experts / W;
   p2r_check(p2r_ep_pack(ep_local(ep_->off_slot), static_cast<const int*>(ep_local(ep_->off_cnt)), cfg_.d_model,
                         acts_->seg, El, W, compact, L.ccount.as<int>(), L.cprefix.as<int>(), stream_),
             "ep pack");
 }
 
-void Model::ep_return(const void* compact, LayerActs& L, std::size_t dst_off) {
+void Engine::ep_return(const void* compact, LayerActs& L, std::size_t dst_off) {
   const int W = ep_world_, El = cfg_.moe.n_experts / W;
   std::vector<void*> dst(static_cast<std::size_t>(W));
   for (int q = 0; q < W; ++q) dst[static_cast<std::size_t>(q)] = ep_peer(q, dst_off);
@@ -238,27 +238,27 @@ void Model::ep_return(const void* compact, LayerActs& L, std::size_t dst_off) {
   ep_wait(1);
 }
 
-// ---------------------------------------------------------------- Model
-Model::Model(ModelConfig config, std::uint64_t seed) : cfg_(std::move(config)) {
+// ---------------------------------------------------------------- Engine
+Engine::Engine(ModelConfig config, std::uint64_t seed) : cfg_(std::move(config)) {
   init_model(seed, nullptr, 0, 1, 0, false);
 }
 
-Model::Model(ModelConfig config, std::uint64_t seed, const std::vector<int>& slow, int ring_slots)
+Engine::Engine(ModelConfig config, std::uint64_t seed, const std::vector<int>& slow, int ring_slots)
     : cfg_(std::move(config)) {
   init_model(seed, &slow, ring_slots, 1, 0, false);
 }
 
-Model::Model(ModelConfig config, std::uint64_t seed, int ep_world, int ep_rank) : cfg_(std::move(config)) {
+Engine::Engine(ModelConfig config, std::uint64_t seed, int ep_world, int ep_rank) : cfg_(std::move(config)) {
   init_model(seed, nullptr, 0, ep_world, ep_rank, true);
 }
 
-Model::Model(ModelConfig config, std::uint64_t seed, const std::vector<int>& slow, int ring_slots, int ep_world,
+Engine::Engine(ModelConfig config, std::uint64_t seed, const std::vector<int>& slow, int ring_slots, int ep_world,
              int ep_rank)
     : cfg_(std::move(config)) {
   init_model(seed, &slow, ring_slots, ep_world, ep_rank, true);
 }
 
-void Model::init_model(std::uint64_t seed, const std::vector<int>* slow, int ring_slots, int ep_world, int ep_rank,
+void Engine::init_model(std::uint64_t seed, const std::vector<int>* slow, int ring_slots, int ep_world, int ep_rank,
                        bool ep_ctor) {
   cfg_.validate();
   if (ep_world < 1 || ep_rank < 0 || ep_rank >= ep_world)
@@ -275,12 +275,12 @@ void Model::init_model(std::uint64_t seed, const std::vector<int>* slow, int rin
   init_params(seed);
 }
 
-void Model::set_grad_accumulation(int n) {
+void Engine::set_grad_accumulation(int n) {
   if (n < 1) throw std::invalid_argument("offload: accumulation window must be >= 1 micro-step");
   accum_n_ = n;
 }
 
-void Model::set_activation_checkpointing(int policy) {
+void Engine::set_activation_checkpointing(int policy) {
   if (policy < 0 || policy > 2) throw std::invalid_argument("checkpointing: policy must be 0, 1 or 2");
   if (policy != ckpt_policy_) {
     ckpt_policy_ = policy;
@@ -288,7 +288,7 @@ void Model::set_activation_checkpointing(int policy) {
   }
 }
 
-Model::Model(ModelConfig config, NoInit, int ep_world, int ep_rank, bool force_ep) : cfg_(std::move(config)) {
+Engine::Engine(ModelConfig config, NoInit, int ep_world, int ep_rank, bool force_ep) : cfg_(std::move(config)) {
   cfg_.validate();
   ep_world_ = ep_world;
   ep_rank_ = ep_rank;
@@ -297,7 +297,7 @@ Model::Model(ModelConfig config, NoInit, int ep_world, int ep_rank, bool force_e
   allocate();
 }
 
-Model::~Model() {
+Engine::~Engine() {
   if (stream_) cudaStreamSynchronize(stream_);
   if (step_graph_.exec) cudaGraphExecDestroy(step_graph_.exec);
   comm_destroy();
@@ -306,7 +306,7 @@ Model::~Model() {
   if (stream_) cudaStreamDestroy(stream_);
 }
 
-void Model::build_layout() {
+void Engine::build_layout() {
   const int d = cfg_.d_model, dff = cfg_.d_ff, V = cfg_.vocab_size, S = cfg_.seq_len;
   const int Eg = cfg_.moe.n_experts;
   if (Eg > 0 && Eg % ep_world_ != 0)
@@ -345,7 +345,7 @@ void Model::build_layout() {
   }
   layer_stride_ = (layer_.numel + 63) / 64 * 64;
 
-  // reference-named views, Model::for_each_param order (model.cpp:188-198)
+  // reference-named views, Engine::for_each_param order (model.cpp:188-198)
   views_.clear();
   views_.push_back({"embed.tok", -1, emb_.tok, V, d, d, {V, d}});
   views_.push_back({"embed.pos", -1, emb_.pos, S, d, d, {S, d}});
@@ -380,7 +380,7 @@ void Model::build_layout() {
   }
 }
 
-void Model::allocate() {
+void Engine::allocate() {
   cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
   const std::size_t eb = static_cast<std::size_t>(emb_.numel);
   const std::size_t lb = static_cast<std::size_t>(layer_stride_) * std::max(n_res_, 1);
@@ -396,23 +396,23 @@ void Model::allocate() {
   cuda_check(cudaMemsetAsync(lay_g_.p, 0, lb * 4, stream_), "memset");
 }
 
-float* Model::lp(int o, long long off) const {
+float* Engine::lp(int o, long long off) const {
   const int r = res_idx_[static_cast<std::size_t>(o)];
   if (r < 0) return offload_slot_ptr(*off_, o, 0) + off;
   return lay_p_.as<float>() + r * layer_stride_ + off;
 }
-float* Model::lg(int o, long long off) const {
+float* Engine::lg(int o, long long off) const {
   const int r = res_idx_[static_cast<std::size_t>(o)];
   if (r < 0) return offload_slot_ptr(*off_, o, 1) + off;
   return lay_g_.as<float>() + r * layer_stride_ + off;
 }
-void* Model::lp16(int o, long long off) const {
+void* Engine::lp16(int o, long long off) const {
   const int r = res_idx_[static_cast<std::size_t>(o)];
   if (r < 0) return reinterpret_cast<std::uint16_t*>(offload_slot_ptr(*off_, o, 4)) + off;
   return lay_p16_.as<std::uint16_t>() + r * layer_stride_ + off;
 }
 
-void Model::init_params(std::uint64_t seed) {
+void Engine::init_params(std::uint64_t seed) {
   // model.cpp:128-164: gains 1, biases 0, matrices N(0, 0.02) per named tensor. Every
   // tensor draws from its own generator (seed mixed with its name), so tensors are
   // filled in parallel host threads (same values) and uploaded in order, in batches
@@ -466,7 +466,7 @@ void Model::init_params(std::uint64_t seed) {
   refresh_bf16();
 }
 
-void Model::refresh_bf16() {
+void Engine::refresh_bf16() {
   p2r_check(p2r_cast_bf16(emb_p_.as<float>(), emb_p16_.p, emb_.numel, stream_), "cast");
   if (n_res_ > 0)
     p2r_check(p2r_cast_bf16(lay_p_.as<float>(), lay_p16_.p, layer_stride_ * n_res_, stream_), "cast");
@@ -474,7 +474,7 @@ void Model::refresh_bf16() {
     if (res_idx_[static_cast<std::size_t>(o)] < 0) host_cast_bf16(slow_host_p32(o), slow_host_p16(o), layer_stride_);
 }
 
-const float* Model::view_base(const ParamView& v, int kind) const {
+const float* Engine::view_base(const ParamView& v, int kind) const {
   // kind: 0 param, 1 grad, 2 m, 3 v
   if (v.granule < 0) {
     const DevBuf* b = kind == 0 ? &emb_p_ : kind == 1 ? &emb_g_ : kind == 2 ? &emb_m_ : &emb_v_;
@@ -495,7 +495,7 @@ const float* Model::view_base(const ParamView& v, int kind) const {
   return slow_host_m(v.granule, kind - 2) + v.off;
 }
 
-void Model::copy_view(const ParamView& v, int kind, float* host, bool to_host) const {
+void Engine::copy_view(const ParamView& v, int kind, float* host, bool to_host) const {
   if (off_) offload_sync(*off_);
   float* base = const_cast<float*>(view_base(v, kind));
   const std::size_t w = static_cast<std::size_t>(v.cols) * 4, ld = static_cast<std::size_t>(v.ld) * 4;
@@ -506,9 +506,10 @@ void Model::copy_view(const ParamView& v, int kind, float* host, bool to_host) c
   cuda_check(cudaStreamSynchronize(stream_), "sync");
 }
 
-void Model::get_param(int i, float* host) const { copy_view(views_.at(static_cast<std::size_t>(i)), 0, host, true); }
+void Engine::get_param(int i, float* host) const { copy_view(views_.at(static_cast<std::size_t>(i)), 0, host, true); }
 
-void Model::set_param(int i, const float* host) {
+void Engine::set_param(int i, const float* host) {
+  ++version_;
   const ParamView& v = views_.at(static_cast<std::size_t>(i));
   copy_view(v, 0, const_cast<float*>(host), false);
   // keep the bf16 shadow in step with the master copy (linear span of the view)
@@ -522,24 +523,26 @@ void Model::set_param(int i, const float* host) {
   }
 }
 
-void Model::get_grad(int i, float* host) const { copy_view(views_.at(static_cast<std::size_t>(i)), 1, host, true); }
+void Engine::get_grad(int i, float* host) const { copy_view(views_.at(static_cast<std::size_t>(i)), 1, host, true); }
 
-void Model::get_moment(int i, int which, float* host) const {
+void Engine::get_moment(int i, int which, float* host) const {
   if (!has_opt_) throw std::logic_error("adamw: optimizer not attached");
   copy_view(views_.at(static_cast<std::size_t>(i)), 2 + which, host, true);
 }
 
-void Model::set_moment(int i, int which, const float* host) {
+void Engine::set_moment(int i, int which, const float* host) {
+  ++version_;
   if (!has_opt_) throw std::logic_error("adamw: optimizer not attached");
   if (which != 0 && which != 1) throw std::invalid_argument("adamw: moment index must be 0 (m) or 1 (v)");
   copy_view(views_.at(static_cast<std::size_t>(i)), 2 + which, const_cast<float*>(host), false);
 }
 
-std::int64_t Model::grad_bytes() const {
+std::int64_t Engine::grad_bytes() const {
   return (emb_.numel + layer_stride_ * n_res_) * 4;
 }
 
-void Model::zero_grads() {
+void Engine::zero_grads() {
+  ++version_;
   cuda_check(cudaMemsetAsync(emb_g_.p, 0, emb_g_.bytes, stream_), "zero grads");
   cuda_check(cudaMemsetAsync(lay_g_.p, 0, lay_g_.bytes, stream_), "zero grads");
   if (off_) {  // SLOW granules: drop the parked partial gradients, restart the window
@@ -549,7 +552,7 @@ void Model::zero_grads() {
 }
 
 // ---------------------------------------------------------------- activations
-void Model::ensure_acts(int B, int S) {
+void Engine::ensure_acts(int B, int S) {
   const int T = B * S;
   if (acts_ && acts_->B == B && acts_->S == S) return;
   acts_.reset();
@@ -689,7 +692,7 @@ void Model::ensure_acts(int B, int S) {
   }
 }
 
-void Model::gemm(int m, int n, int k, const void* a, int lda, bool a_mn, const void* b, int ldb,
+void Engine::gemm(int m, int n, int k, const void* a, int lda, bool a_mn, const void* b, int ldb,
                  bool b_mn, int epi, void* c, int ldc, void* c2, int ldc2, const float* bias,
                  const void* aux, int ldaux, int group_mode, int groups, int seg_rows,
                  const int* counts, int split_k, float* bias_grad) {
@@ -747,7 +750,7 @@ Profiler::~Profiler() {
   for (cudaEvent_t e : pool) cudaEventDestroy(e);
 }
 
-void Model::profile(int cls, std::int64_t* launches, double* ms, double* flops, double* bytes) {
+void Engine::profile(int cls, std::int64_t* launches, double* ms, double* flops, double* bytes) {
   cuda_check(cudaStreamSynchronize(stream_), "profile sync");
   std::int64_t n = 0;
   double t = 0, f = 0, b = 0;
@@ -766,13 +769,13 @@ void Model::profile(int cls, std::int64_t* launches, double* ms, double* flops, 
   *bytes = b;
 }
 
-void Model::profile_reset() {
+void Engine::profile_reset() {
   cuda_check(cudaStreamSynchronize(stream_), "profile sync");
   prof_.recs.clear();
   prof_.used = 0;
 }
 
-void Model::buffer(int which, void** ptr, std::size_t* bytes) const {
+void Engine::buffer(int which, void** ptr, std::size_t* bytes) const {
   if (which == 0) {
     *ptr = emb_g_.p;
     *bytes = emb_g_.bytes;
@@ -785,7 +788,8 @@ void Model::buffer(int which, void** ptr, std::size_t* bytes) const {
 }
 
 // ---------------------------------------------------------------- forward pieces
-Tensor Model::embed_forward(GradTape* tape, const int* d_tokens, int batch, int seq) {
+DevTensor Engine::embed_forward(GradTape* tape, const int* d_tokens, int batch, int seq) {
+  ++version_;
   if (batch <= 0) throw std::invalid_argument("forward: token count must be a multiple of batch");
   if (seq > cfg_.seq_len) throw std::invalid_argument("forward: sequence longer than configured seq_len");
   if (off_ && tape != nullptr && !off_->slow_list.empty()) {
@@ -810,10 +814,10 @@ Tensor Model::embed_forward(GradTape* tape, const int* d_tokens, int batch, int 
       });
     });
   }
-  return Tensor{A.T, d, A.x0.as<float>(), A.dres.as<float>(), A.dres16.p};
+  return DevTensor{A.T, d, A.x0.as<float>(), A.dres.as<float>(), A.dres16.p};
 }
 
-Tensor Model::block_forward(GradTape* tape, int g, const Tensor& x, int batch, AttentionMode mode) {
+DevTensor Engine::block_forward(GradTape* tape, int g, const DevTensor& x, int batch, AttentionMode mode) {
   if (g < 0 || g >= cfg_.n_layers_graph) throw std::out_of_range("model: graph layer index out of range");
   Acts& A = *acts_;
   if (x.rows != A.T || batch != A.B) throw std::invalid_argument("block_forward: batch does not match embed_forward");
@@ -822,10 +826,10 @@ Tensor Model::block_forward(GradTape* tape, int g, const Tensor& x, int batch, A
   block_compute(g, x.data, mode);
   if (off_) offload_release(o, false);
   if (tape) tape->record([this, g, mode]() { block_backward(g, mode); });
-  return Tensor{A.T, cfg_.d_model, A.L[static_cast<std::size_t>(g)].xout.as<float>(), A.dres.as<float>(), A.dres16.p};
+  return DevTensor{A.T, cfg_.d_model, A.L[static_cast<std::size_t>(g)].xout.as<float>(), A.dres.as<float>(), A.dres16.p};
 }
 
-bool Model::checkpointed(int g) const {
+bool Engine::checkpointed(int g) const {
   if (!off_ || ckpt_policy_ == 0) return false;
   return ckpt_policy_ == 2 || slow_[static_cast<std::size_t>(owned_index_of_graph_layer(g))] != 0;
 }
@@ -833,11 +837,11 @@ bool Model::checkpointed(int g) const {
 // The forward of graph layer g from input x (fp32 [T, d]) into its activation set
 // (the shared checkpoint set for checkpointed layers) and its output L[g].xout. Run
 // by block_forward, and again by block_backward to recompute a checkpointed layer.
-void Model::block_compute(int g, const float* xin_data, AttentionMode mode) {
+void Engine::block_compute(int g, const float* xin_data, AttentionMode mode) {
   Acts& A = *acts_;
   LayerActs& L = A.ckpt[static_cast<std::size_t>(g)] ? A.ck : A.L[static_cast<std::size_t>(g)];
   float* xout = A.L[static_cast<std::size_t>(g)].xout.as<float>();
-  const Tensor x{A.T, cfg_.d_model, const_cast<float*>(xin_data), nullptr, nullptr};
+  const DevTensor x{A.T, cfg_.d_model, const_cast<float*>(xin_data), nullptr, nullptr};
   const int o = owned_index_of_graph_layer(g);
   const int T = A.T, d = cfg_.d_model, dff = cfg_.d_ff, H = cfg_.n_heads;
   const int causal = mode == AttentionMode::Causal ? 1 : 0;
@@ -917,7 +921,8 @@ void Model::block_compute(int g, const float* xin_data, AttentionMode mode) {
 // accumulated in place (beta = 1), so in Pseudo mode the L graph layers sum
 // into one buffer in reverse layer order exactly like the reference's
 // per-layer flush (model.cpp:210-221).
-void Model::block_backward(int g, AttentionMode mode) {
+void Engine::block_backward(int g, AttentionMode mode) {
+  ++version_;
   Acts& A = *acts_;
   LayerActs& L = A.ckpt[static_cast<std::size_t>(g)] ? A.ck : A.L[static_cast<std::size_t>(g)];
   const int o = owned_index_of_graph_layer(g);
@@ -1039,7 +1044,7 @@ void Model::block_backward(int g, AttentionMode mode) {
   if (off_) offload_release(o, true);
 }
 
-Tensor Model::head_forward(GradTape* tape, const Tensor& x) {
+DevTensor Engine::head_forward(GradTape* tape, const DevTensor& x) {
   Acts& A = *acts_;
   const int T = A.T, d = cfg_.d_model, V = cfg_.vocab_size;
   prof(P2R_PROF_LAYERNORM, 0, 6.0 * T * d + 8.0 * T, [&] {
@@ -1052,6 +1057,7 @@ Tensor Model::head_forward(GradTape* tape, const Tensor& x) {
   if (tape) {
     const float* xin = x.data;
     tape->record([this, xin]() {
+      ++version_;
       Acts& A2 = *acts_;
       const int T2 = A2.T, d2 = cfg_.d_model, V2 = cfg_.vocab_size;
       // dtok += dlogits^T h ; dh = dlogits . tok
@@ -1072,10 +1078,10 @@ Tensor Model::head_forward(GradTape* tape, const Tensor& x) {
       }
     });
   }
-  return Tensor{T, V, A.logits32.as<float>(), nullptr, nullptr};
+  return DevTensor{T, V, A.logits32.as<float>(), nullptr, nullptr};
 }
 
-Tensor Model::softmax_cross_entropy(GradTape* /*tape*/, const Tensor& logits, const int* d_targets,
+DevTensor Engine::softmax_cross_entropy(GradTape* /*tape*/, const DevTensor& logits, const int* d_targets,
                                     const std::uint8_t* d_mask, double denom) {
   if (denom <= 0.0) throw std::invalid_argument("softmax_cross_entropy: denominator must be > 0");
   Acts& A = *acts_;
@@ -1085,13 +1091,13 @@ Tensor Model::softmax_cross_entropy(GradTape* /*tape*/, const Tensor& logits, co
                                 A.ce_ws.as<double>(), stream_),
               "cross entropy");
   });
-  return Tensor{1, 1, A.loss.as<float>(), nullptr, nullptr};
+  return DevTensor{1, 1, A.loss.as<float>(), nullptr, nullptr};
 }
 
 // A training micro-step of an offloaded model: the SLOW granules' fused AdamW runs in
 // the backward of the accumulation window's last micro-step (set_grad_accumulation).
 // Checked before anything is zeroed or launched, so a misuse leaves the state intact.
-void Model::offload_check_micro(int next_micro) const {
+void Engine::offload_check_micro(int next_micro) const {
   if (!off_ || off_->slow_list.empty()) return;
   if (next_micro > accum_n_)
     throw std::logic_error(
@@ -1102,22 +1108,22 @@ void Model::offload_check_micro(int next_micro) const {
     throw std::logic_error("offload: call set_offload_lr(lr) before the backward that applies AdamW");
 }
 
-void Model::train_step_device(const int* d_tokens, const int* d_targets, const std::uint8_t* d_mask, int batch,
+void Engine::train_step_device(const int* d_tokens, const int* d_targets, const std::uint8_t* d_mask, int batch,
                               int seq, double denom, AttentionMode mode, bool zero, float* loss_dev) {
   if (off_) offload_check_micro(zero ? 1 : micro_ + 1);
   if (zero) zero_grads();
   GradTape tape;
-  Tensor x = embed_forward(&tape, d_tokens, batch, seq);
+  DevTensor x = embed_forward(&tape, d_tokens, batch, seq);
   for (int g = 0; g < cfg_.n_layers_graph; ++g) x = block_forward(&tape, g, x, batch, mode);
-  Tensor logits = head_forward(&tape, x);
-  Tensor loss = softmax_cross_entropy(&tape, logits, d_targets, d_mask, denom);
-  tape.backward_scalar(loss);
+  DevTensor logits = head_forward(&tape, x);
+  DevTensor loss = softmax_cross_entropy(&tape, logits, d_targets, d_mask, denom);
+  tape.backward();  // the fused cross-entropy already seeded dlogits for d loss = 1
   flush_shared_layer_grads();
   if (loss_dev && loss_dev != loss.data)
     cuda_check(cudaMemcpyAsync(loss_dev, loss.data, 4, cudaMemcpyDeviceToDevice, stream_), "loss copy");
 }
 
-void Model::train_step_device_graph(const int* d_tokens, const int* d_targets, const std::uint8_t* d_mask, int batch,
+void Engine::train_step_device_graph(const int* d_tokens, const int* d_targets, const std::uint8_t* d_mask, int batch,
                                     int seq, double denom, AttentionMode mode, bool zero, float* loss_dev) {
   // (a dense model's communicator is only used by allreduce_grads, outside the step)
   if (off_ || cfg_.moe.enabled() || prof_.on)
@@ -1177,7 +1183,7 @@ void validate_ids(const int* ids, std::size_t n, int V, const char* msg) {
 }
 }  // namespace
 
-float Model::train_step_host(const int* tokens, const int* targets, const std::uint8_t* mask, int batch, int seq,
+float Engine::train_step_host(const int* tokens, const int* targets, const std::uint8_t* mask, int batch, int seq,
                              double denom, AttentionMode mode, bool zero) {
   if (batch <= 0 || seq <= 0) throw std::invalid_argument("forward: token count must be a multiple of batch");
   if (seq > cfg_.seq_len) throw std::invalid_argument("forward: sequence longer than configured seq_len");
@@ -1214,7 +1220,7 @@ float Model::train_step_host(const int* tokens, const int* targets, const std::u
   return *lh;
 }
 
-void Model::forward_host(const int* tokens, int batch, int seq, AttentionMode mode, float* logits_out) {
+void Engine::forward_host(const int* tokens, int batch, int seq, AttentionMode mode, float* logits_out) {
   if (batch <= 0 || seq <= 0) throw std::invalid_argument("forward: token count must be a multiple of batch");
   if (seq > cfg_.seq_len) throw std::invalid_argument("forward: sequence longer than configured seq_len");
   const std::size_t T = static_cast<std::size_t>(batch) * seq;
@@ -1222,9 +1228,9 @@ void Model::forward_host(const int* tokens, int batch, int seq, AttentionMode mo
   ensure_acts(batch, seq);
   Acts& A = *acts_;
   cuda_check(cudaMemcpyAsync(A.tokens.p, tokens, T * 4, cudaMemcpyHostToDevice, stream_), "h2d");
-  Tensor x = embed_forward(nullptr, A.tokens.as<int>(), batch, seq);
+  DevTensor x = embed_forward(nullptr, A.tokens.as<int>(), batch, seq);
   for (int g = 0; g < cfg_.n_layers_graph; ++g) x = block_forward(nullptr, g, x, batch, mode);
-  Tensor logits = head_forward(nullptr, x);
+  DevTensor logits = head_forward(nullptr, x);
   cuda_check(cudaMemcpy2DAsync(logits_out, static_cast<std::size_t>(cfg_.vocab_size) * 4, logits.data,
                                static_cast<std::size_t>(A.vld) * 4, static_cast<std::size_t>(cfg_.vocab_size) * 4, T,
                                cudaMemcpyDeviceToHost, stream_),
@@ -1232,7 +1238,7 @@ void Model::forward_host(const int* tokens, int batch, int seq, AttentionMode mo
   cuda_check(cudaStreamSynchronize(stream_), "forward sync");
 }
 
-void Model::routing_host(int g, int* selected, std::uint8_t* survived, int* raw_load, int* capacity,
+void Engine::routing_host(int g, int* selected, std::uint8_t* survived, int* raw_load, int* capacity,
                          int* dropped) const {
   if (!cfg_.moe.enabled()) throw std::logic_error("routing: dense model");
   if (!acts_) throw std::logic_error("routing: no forward pass yet");
@@ -1246,7 +1252,7 @@ void Model::routing_host(int g, int* selected, std::uint8_t* survived, int* raw_
   *capacity = L.capacity;
 }
 
-void Model::gate_logits_host(int g, float* out) const {
+void Engine::gate_logits_host(int g, float* out) const {
   if (!cfg_.moe.enabled()) throw std::logic_error("routing: dense model");
   if (!acts_) throw std::logic_error("routing: no forward pass yet");
   const LayerActs& L = acts_->ckpt.at(static_cast<std::size_t>(g)) ? acts_->ck : acts_->L.at(static_cast<std::size_t>(g));
@@ -1257,7 +1263,7 @@ void Model::gate_logits_host(int g, float* out) const {
 }
 
 // ---------------------------------------------------------------- AdamW (optim.cpp:28-70)
-void Model::adamw_attach(float b1, float b2, float eps, float wd) {
+void Engine::adamw_attach(float b1, float b2, float eps, float wd) {
   b1_ = b1;
   b2_ = b2;
   eps_ = eps;
@@ -1276,7 +1282,8 @@ void Model::adamw_attach(float b1, float b2, float eps, float wd) {
   }
 }
 
-void Model::adamw_step(float lr) {
+void Engine::adamw_step(float lr) {
+  ++version_;
   if (!has_opt_) throw std::logic_error("adamw: unregistered parameter embed.tok");
   // checks first: a throw must leave the step count and every moment untouched
   if (off_ && !off_->slow_list.empty()) {
@@ -1314,7 +1321,7 @@ void Model::adamw_step(float lr) {
   }
 }
 
-void Model::adamw_granule(float* p, float* g, float* m, float* v, void* p16, float lr, float bc1, float bc2) {
+void Engine::adamw_granule(float* p, float* g, float* m, float* v, void* p16, float lr, float bc1, float bc2) {
   std::vector<long long> off, len;
   std::vector<int> dec;
   for (const auto& s : layer_.segs) {
@@ -1329,19 +1336,19 @@ void Model::adamw_granule(float* p, float* g, float* m, float* v, void* p16, flo
   });
 }
 
-std::int64_t Model::state_bytes() const {
+std::int64_t Engine::state_bytes() const {
   if (!has_opt_) return 0;
   // two fp32 moments per parameter element (optim.cpp:65-70)
   return 2 * 4 * (count_params(cfg_).total_params);
 }
 
 // ---------------------------------------------------------------- delink (model.cpp:358-377)
-std::unique_ptr<Model> Model::delinked() const {
+std::unique_ptr<Engine> Engine::delinked() const {
   if (cfg_.n_layers_params != 1) throw std::logic_error("delinked: model is not in shared-parameter mode");
   if (off_) throw std::logic_error("delinked: offloaded models are Real already");
   // each expert-parallel rank delinks its own shard (no communication); the Real
   // model needs its own communicator (comm_init) before an expert-parallel step
-  std::unique_ptr<Model> real(new Model(cfg_.as_unshared(), NoInit{}, ep_world_, ep_rank_, force_ep_));
+  std::unique_ptr<Engine> real(new Engine(cfg_.as_unshared(), NoInit{}, ep_world_, ep_rank_, force_ep_));
   cudaStream_t s = real->stream_;
   cuda_check(cudaStreamSynchronize(stream_), "sync");
   // embeddings + final norm: direct copies
@@ -1363,6 +1370,45 @@ std::unique_ptr<Model> Model::delinked() const {
   cuda_check(cudaStreamSynchronize(s), "delink sync");
   return real;
 }
+
+// ---------------------------------------------------------------- drop-in API staging
+const int* Engine::stage_tokens(const int* host, int batch, int seq) {
+  if (batch <= 0 || seq <= 0) throw std::invalid_argument("forward: token count must be a multiple of batch");
+  if (seq > cfg_.seq_len) throw std::invalid_argument("forward: sequence longer than configured seq_len");
+  const std::size_t T = static_cast<std::size_t>(batch) * seq;
+  validate_ids(host, T, cfg_.vocab_size, "embedding_lookup: id out of range");
+  ensure_acts(batch, seq);
+  cuda_check(cudaMemcpyAsync(acts_->tokens.p, host, T * 4, cudaMemcpyHostToDevice, stream_), "h2d tokens");
+  cuda_check(cudaStreamSynchronize(stream_), "sync");
+  return acts_->tokens.as<int>();
+}
+
+void Engine::stage_targets(const int* targets, const std::uint8_t* mask, int n, const int** d_targets,
+                           const std::uint8_t** d_mask) {
+  if (!acts_ || acts_->T != n) throw std::invalid_argument("softmax_cross_entropy: one target per row required");
+  for (int i = 0; i < n; ++i)
+    if ((mask == nullptr || mask[i] != 0) && (targets[i] < 0 || targets[i] >= cfg_.vocab_size))
+      throw std::out_of_range("softmax_cross_entropy: target out of range");
+  cuda_check(cudaMemcpyAsync(acts_->targets.p, targets, static_cast<std::size_t>(n) * 4, cudaMemcpyHostToDevice,
+                             stream_),
+             "h2d targets");
+  if (mask)
+    cuda_check(cudaMemcpyAsync(acts_->mask.p, mask, static_cast<std::size_t>(n), cudaMemcpyHostToDevice, stream_),
+               "h2d mask");
+  cuda_check(cudaStreamSynchronize(stream_), "sync");
+  *d_targets = acts_->targets.as<int>();
+  *d_mask = mask ? acts_->mask.as<std::uint8_t>() : nullptr;
+}
+
+float* Engine::stage_activation(const float* host, int rows) {
+  if (!acts_ || acts_->T != rows) throw std::invalid_argument("block_forward: batch does not match embed_forward");
+  cuda_check(cudaMemcpyAsync(acts_->x0.p, host, static_cast<std::size_t>(rows) * cfg_.d_model * 4,
+                             cudaMemcpyHostToDevice, stream_),
+             "h2d activation");
+  return acts_->x0.as<float>();
+}
+
+int Engine::vocab_ld() const { return acts_ ? acts_->vld : (cfg_.vocab_size + 7) / 8 * 8; }
 
 // ---------------------------------------------------------------- host routing
 HostRouting moe_dispatch_host(const float* logits, int T, const MoEConfig& moe) {

@@ -199,7 +199,7 @@ std::vector<int> plan_offload(const std::vector<std::int64_t>& layer_bytes, std:
 }
 
 // ---------------------------------------------------------------- engine side
-void Model::offload_setup(const std::vector<int>& slow, int ring_slots) {
+void Engine::offload_setup(const std::vector<int>& slow, int ring_slots) {
   // A Pseudo model's L graph layers share one granule: reloading it per graph layer
   // would apply L fused AdamW updates from partial gradients
   if (cfg_.n_layers_params != cfg_.n_layers_graph)
@@ -261,7 +261,7 @@ void Model::offload_setup(const std::vector<int>& slow, int ring_slots) {
   off_ = std::move(st);
 }
 
-void Model::offload_alloc_moments() {
+void Engine::offload_alloc_moments() {
   if (!off_ || off_->slow_list.empty() || off_->hm) return;
   const std::size_t n = static_cast<std::size_t>(layer_stride_) * off_->slow_list.size();
   cuda_check(cudaMallocHost(reinterpret_cast<void**>(&off_->hm), n * 4), "pinned m");
@@ -270,18 +270,18 @@ void Model::offload_alloc_moments() {
   std::memset(off_->hv, 0, n * 4);
 }
 
-float* Model::slow_host_p32(int o) const {
+float* Engine::slow_host_p32(int o) const {
   return off_->hp32 + static_cast<long long>(off_->host_idx[static_cast<std::size_t>(o)]) * layer_stride_;
 }
-std::uint16_t* Model::slow_host_p16(int o) const {
+std::uint16_t* Engine::slow_host_p16(int o) const {
   return off_->hp16 + static_cast<long long>(off_->host_idx[static_cast<std::size_t>(o)]) * layer_stride_;
 }
-float* Model::slow_host_m(int o, int which) const {
+float* Engine::slow_host_m(int o, int which) const {
   float* b = which ? off_->hv : off_->hm;
   if (!b) throw std::logic_error("adamw: optimizer not attached");
   return b + static_cast<long long>(off_->host_idx[static_cast<std::size_t>(o)]) * layer_stride_;
 }
-float* Model::slow_host_grad(int o) const {
+float* Engine::slow_host_grad(int o) const {
   if (!off_->hg) return nullptr;
   return off_->hg + static_cast<long long>(off_->host_idx[static_cast<std::size_t>(o)]) * layer_stride_;
 }
@@ -295,7 +295,7 @@ void copy_async(OffloadState& st, void* dst, const void* src, std::size_t bytes,
 }
 }  // namespace
 
-void Model::offload_begin_forward(bool training) {
+void Engine::offload_begin_forward(bool training) {
   OffloadState& st = *off_;
   st.training = training;
   std::fill(st.slot_of.begin(), st.slot_of.end(), -1);
@@ -315,7 +315,7 @@ void Model::offload_begin_forward(bool training) {
 // available: the ring holds `ring` granules in flight, so backward granules
 // start loading during the (H2D-light) forward pass. Slots are reused in FIFO
 // order; each reuse waits (on the H2D stream) for the slot's previous consumer.
-void Model::offload_prefetch_next(int /*after*/, bool /*backward*/) {
+void Engine::offload_prefetch_next(int /*after*/, bool /*backward*/) {
   OffloadState& st = *off_;
   const std::size_t g = static_cast<std::size_t>(layer_stride_);
   while (st.next_issue < st.sched.size() && st.in_flight < st.ring) {
@@ -373,7 +373,7 @@ void Model::offload_prefetch_next(int /*after*/, bool /*backward*/) {
   }
 }
 
-void Model::offload_acquire(int o, bool backward) {
+void Engine::offload_acquire(int o, bool backward) {
   if (res_idx_[static_cast<std::size_t>(o)] >= 0) return;
   OffloadState& st = *off_;
   std::vector<int>& map = backward ? st.slot_bwd : st.slot_fwd;
@@ -394,7 +394,7 @@ void Model::offload_acquire(int o, bool backward) {
   if (backward && !sl.grads_loaded) cuda_check(cudaMemsetAsync(sl.g32.p, 0, sl.g32.bytes, stream_), "zero slot grads");
 }
 
-void Model::offload_release(int o, bool backward) {
+void Engine::offload_release(int o, bool backward) {
   // resident layers need nothing: SLOW granules are staged ahead by the schedule
   if (res_idx_[static_cast<std::size_t>(o)] >= 0) return;
   OffloadState& st = *off_;
@@ -468,14 +468,14 @@ void Model::offload_release(int o, bool backward) {
   offload_prefetch_next(o, true);
 }
 
-void Model::offload_finish_step() {}
+void Engine::offload_finish_step() {}
 
 void offload_sync(const OffloadState& st) {
   if (st.h2d) cuda_check(cudaStreamSynchronize(st.h2d), "sync h2d");
   if (st.d2h) cuda_check(cudaStreamSynchronize(st.d2h), "sync d2h");
 }
 
-OffloadStats Model::offload_stats() {
+OffloadStats Engine::offload_stats() {
   OffloadStats out;
   if (!off_) return out;
   OffloadState& st = *off_;
@@ -491,7 +491,7 @@ OffloadStats Model::offload_stats() {
   return out;
 }
 
-void Model::offload_stats_reset() {
+void Engine::offload_stats_reset() {
   if (!off_) return;
   OffloadState& st = *off_;
   cuda_check(cudaStreamSynchronize(st.h2d), "sync h2d");
@@ -501,11 +501,11 @@ void Model::offload_stats_reset() {
   st.pool_used = 0;
 }
 
-void Model::set_offload_skip_copies(bool skip) {
+void Engine::set_offload_skip_copies(bool skip) {
   if (off_) off_->skip = skip;
 }
 
-std::int64_t Model::device_param_bytes() const {
+std::int64_t Engine::device_param_bytes() const {
   std::int64_t b = static_cast<std::int64_t>(emb_p_.bytes + emb_g_.bytes + emb_p16_.bytes + emb_m_.bytes +
                                              emb_v_.bytes + lay_p_.bytes + lay_g_.bytes + lay_p16_.bytes +
                                              lay_m_.bytes + lay_v_.bytes);

@@ -49,8 +49,9 @@ enum {
   P2R_EPI_BF16 = 0,       /* c(bf16) = acc + bias                              */
   P2R_EPI_F32 = 1,        /* c(f32)  = acc + bias + aux(f32 residual, opt.)   */
   P2R_EPI_ACC_F32 = 2,    /* c(f32) += acc      (beta=1, in-place grad accum) */
-  P2R_EPI_BIAS_GELU = 3,  /* c(bf16) = gelu(acc+bias); c2(bf16) = acc+bias    */
-  P2R_EPI_DGELU = 4,      /* c(bf16) = acc * gelu'(aux bf16 pre-activation)   */
+  P2R_EPI_BIAS_GELU = 3,  /* c(bf16) = gelu(acc+bias); c2(bf16) = gelu'(acc+bias) */
+  P2R_EPI_DGELU = 4,      /* c(bf16) = acc * aux (bf16 GELU derivative that     */
+                          /*   BIAS_GELU stored: the GELU backward of its layer) */
   P2R_EPI_F32_BF16 = 5    /* c(f32) = acc + bias + aux; c2(bf16) = same value  */
 };
 enum { P2R_GROUP_NONE = 0, P2R_GROUP_M = 1, P2R_GROUP_K = 2 };

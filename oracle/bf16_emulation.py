@@ -11,7 +11,7 @@ import numpy as np
 from . import p2r_oracle as O
 
 F32 = np.float32
-ALL_POINTS = ("w16", "a16", "qkv16", "p16", "o16", "b16", "hpre16", "g16", "h16",
+ALL_POINTS = ("w16", "a16", "qkv16", "p16", "o16", "b16", "gd16", "g16", "h16",
               "dlogits16", "dres16", "dh16", "dx1_16", "do16", "ds16", "dqkv16", "ye16", "dye16", "dxe16")
 
 
@@ -95,13 +95,14 @@ def loss_and_grads(cfg: O.Config, params: dict, tokens, targets, mask, batch, de
                 ye = R((ge16 @ W[pr + f"moe.expert.{e}.w2"] + P0[pr + f"moe.expert.{e}.b2"]).astype(F32), "ye16")
                 wv = wgt[rows, rt.expert_slots[e]]
                 y[rows] += wv[:, None] * ye
-                ec.append((xe, R(he, "hpre16"), ge16, ye))
+                # the forward epilogue stores gelu'(pre) in bf16 for the backward
+                ec.append((xe, R(O.gelu_bwd(np.ones_like(he), he), "gd16"), ge16, ye))
             xn = (x1 + y).astype(F32)
             caches.append((x, a16, xh1, inv1, qkv, ac, o16, x1, b16, xh2, inv2, (b, logits, rt, wgt, ec), None, wqkv))
         else:
             hpre = (b16 @ W[pr + "ffn.w1"] + P0[pr + "ffn.b1"]).astype(F32)
             g16 = R(O.gelu_fwd(hpre), "g16")
-            hpre16 = R(hpre, "hpre16")
+            hpre16 = R(O.gelu_bwd(np.ones_like(hpre), hpre), "gd16")  # stored GELU derivative
             xn = (x1 + g16 @ W[pr + "ffn.w2"] + P0[pr + "ffn.b2"]).astype(F32)
             caches.append((x, a16, xh1, inv1, qkv, ac, o16, x1, b16, xh2, inv2, hpre16, g16, wqkv))
         x = xn
@@ -134,7 +135,7 @@ def loss_and_grads(cfg: O.Config, params: dict, tokens, targets, mask, batch, de
                 gw[rows, slots] += (dy[rows] * ye).sum(-1, dtype=F32)
                 G[pr + f"moe.expert.{e}.w2"] += ge16.T @ dye
                 G[pr + f"moe.expert.{e}.b2"] += dye.sum(0)
-                dhe = R(O.gelu_bwd(dye @ W[pr + f"moe.expert.{e}.w2"].T, he16), "dh16")
+                dhe = R((dye @ W[pr + f"moe.expert.{e}.w2"].T) * he16, "dh16")
                 G[pr + f"moe.expert.{e}.w1"] += xe.T @ dhe
                 G[pr + f"moe.expert.{e}.b1"] += dhe.sum(0)
                 np.add.at(db, rows, R((dhe @ W[pr + f"moe.expert.{e}.w1"].T).astype(F32), "dxe16"))
@@ -145,7 +146,7 @@ def loss_and_grads(cfg: O.Config, params: dict, tokens, targets, mask, batch, de
             dy16 = R(dy, "dres16")
             G[pr + "ffn.w2"] += g16.T @ dy16
             G[pr + "ffn.b2"] += dy.sum(0)
-            dh16 = R(O.gelu_bwd(dy16 @ W[pr + "ffn.w2"].T, hpre16), "dh16")
+            dh16 = R((dy16 @ W[pr + "ffn.w2"].T) * hpre16, "dh16")
             G[pr + "ffn.w1"] += b16.T @ dh16
             G[pr + "ffn.b1"] += dh16.sum(0)
             db = (dh16 @ W[pr + "ffn.w1"].T).astype(F32)

@@ -56,7 +56,7 @@ def main():
     for p in pts_all:
         e, n = worst(tuple(x for x in pts_all if x != p))
         print(f"{'all but ' + p:34s} worst {e:.4f} {n}")
-    fwd = ("w16", "a16", "qkv16", "p16", "o16", "b16", "hpre16", "g16", "h16")
+    fwd = ("w16", "a16", "qkv16", "p16", "o16", "b16", "gd16", "g16", "h16")
     for tag, pts in (("forward points only", fwd),
                      ("backward points only", tuple(x for x in pts_all if x not in fwd)),
                      ("weights (w16) only", ("w16",)),

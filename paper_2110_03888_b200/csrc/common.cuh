@@ -419,6 +419,29 @@ P2R_DEVICE float gelu_grad_f(float v) {
   const float m = __uint_as_float(__float_as_uint(fmaf(-th, e, 0.5f)) | (__float_as_uint(v) & 0x80000000u));
   return fmaf(v * e, 0.39894228040143268f, 0.5f + m);
 }
+// gelu and gelu' from ONE evaluation of the fit (the forward epilogue stores both:
+// the backward then multiplies by the stored derivative); bitwise the values of
+// gelu_f / gelu_grad_f (resp. gelu2 / gelu_grad2), which run the same operations
+P2R_DEVICE float gelu_pair_f(float v, float& gd) {
+  float e;
+  const float th = gelu_th(v, e);
+  const float he = th * e;
+  const float m = __uint_as_float(__float_as_uint(fmaf(-th, e, 0.5f)) | (__float_as_uint(v) & 0x80000000u));
+  gd = fmaf(v * e, 0.39894228040143268f, 0.5f + m);
+  return fmaf(-fabsf(v), he, fmaxf(v, 0.0f));
+}
+P2R_DEVICE float2 gelu_grad2(float2 x);
+P2R_DEVICE float2 gelu_pair2(float2 x, float2& gd) {
+  float2 e;
+  const float2 th = gelu_th2(x, e);
+  const float2 he = __fmul2_rn(th, e);
+  float2 m = __ffma2_rn(make_float2(-th.x, -th.y), e, make_float2(0.5f, 0.5f));
+  m.x = __uint_as_float(__float_as_uint(m.x) | (__float_as_uint(x.x) & 0x80000000u));
+  m.y = __uint_as_float(__float_as_uint(m.y) | (__float_as_uint(x.y) & 0x80000000u));
+  const float2 cdf = __fadd2_rn(make_float2(0.5f, 0.5f), m);
+  gd = __ffma2_rn(__fmul2_rn(x, e), make_float2(0.39894228040143268f, 0.39894228040143268f), cdf);
+  return make_float2(fmaf(-fabsf(x.x), he.x, fmaxf(x.x, 0.0f)), fmaf(-fabsf(x.y), he.y, fmaxf(x.y, 0.0f)));
+}
 P2R_DEVICE float2 gelu_grad2(float2 x) {
   float2 e;
   const float2 th = gelu_th2(x, e);

@@ -165,7 +165,7 @@ long long GranuleLayout::add(long long n, bool decay) {
 // ---------------------------------------------------------------- activations
 struct LayerActs {
   DevBuf xout, a16, mean1, rstd1, qkv16, o16, lse, x1, b16, mean2, rstd2;
-  DevBuf hpre16, g16;                                                 // dense FFN
+  DevBuf hpre16, g16;  // dense FFN: GELU derivative (stored by the FFN1 epilogue for the backward), GELU output
   DevBuf b32, logits, sel, surv, pos, w, raw, counts, rows_pad, slots_pad, dropped;  // MoE
   DevBuf xe16, hpre_e16, ge16;
   // expert outputs in this rank's expert-major layout [E][seg] (bf16): a local

@@ -180,16 +180,15 @@ P2R_DEVICE float epilogue_elem(const GemmParams& p, float v, long long row, int 
     }
     case P2R_EPI_BIAS_GELU: {
       const float pre = zero ? 0.0f : v + b;
-      reinterpret_cast<__nv_bfloat16*>(p.c2)[row * p.ldc2 + col] = __float2bfloat16_rn(pre);
-      reinterpret_cast<__nv_bfloat16*>(cbase)[row * ldc + col] = __float2bfloat16_rn(zero ? 0.0f : gelu_f(pre));
+      float gd;
+      const float g = gelu_pair_f(pre, gd);
+      reinterpret_cast<__nv_bfloat16*>(p.c2)[row * p.ldc2 + col] = __float2bfloat16_rn(zero ? 0.0f : gd);
+      reinterpret_cast<__nv_bfloat16*>(cbase)[row * ldc + col] = __float2bfloat16_rn(zero ? 0.0f : g);
       break;
     }
-    case P2R_EPI_DGELU: {
+    case P2R_EPI_DGELU: {  // aux = the GELU derivative the forward epilogue stored
       float o = 0.0f;
-      if (!zero) {
-        const float pre = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p.aux)[row * p.ldaux + col]);
-        o = v * gelu_grad_f(pre);
-      }
+      if (!zero) o = v * __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p.aux)[row * p.ldaux + col]);
       reinterpret_cast<__nv_bfloat16*>(cbase)[row * ldc + col] = __float2bfloat16_rn(o);
       return o;
     }
@@ -262,21 +261,24 @@ P2R_DEVICE float4 epilogue_vec4(const GemmParams& p, float4 v, long long row, in
       break;
     }
     case P2R_EPI_BIAS_GELU: {
-      const float4 pre = zero ? make_float4(0.f, 0.f, 0.f, 0.f)
-                              : make_float4(v.x + b.x, v.y + b.y, v.z + b.z, v.w + b.w);
+      const float4 pre = make_float4(v.x + b.x, v.y + b.y, v.z + b.z, v.w + b.w);
+      float4 gd, g;
+      g.x = gelu_pair_f(pre.x, gd.x);
+      g.y = gelu_pair_f(pre.y, gd.y);
+      g.z = gelu_pair_f(pre.z, gd.z);
+      g.w = gelu_pair_f(pre.w, gd.w);
       *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.c2) + row * p.ldc2 + col) =
-          pack4_bf16(pre.x, pre.y, pre.z, pre.w);
+          zero ? make_uint2(0u, 0u) : pack4_bf16(gd.x, gd.y, gd.z, gd.w);
       *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(cbase) + o) =
-          zero ? make_uint2(0u, 0u) : pack4_bf16(gelu_f(pre.x), gelu_f(pre.y), gelu_f(pre.z), gelu_f(pre.w));
+          zero ? make_uint2(0u, 0u) : pack4_bf16(g.x, g.y, g.z, g.w);
       break;
     }
     case P2R_EPI_DGELU: {
       float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
       if (!zero) {
-        const float4 pre = unpack4_bf16(
+        const float4 gd = unpack4_bf16(
             *reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(p.aux) + row * p.ldaux + col));
-        r = make_float4(v.x * gelu_grad_f(pre.x), v.y * gelu_grad_f(pre.y), v.z * gelu_grad_f(pre.z),
-                        v.w * gelu_grad_f(pre.w));
+        r = make_float4(v.x * gd.x, v.y * gd.y, v.z * gd.z, v.w * gd.w);
       }
       *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(cbase) + o) = pack4_bf16(r.x, r.y, r.z, r.w);
       return r;
@@ -330,15 +332,16 @@ P2R_DEVICE float4 epi_store_fast(const GemmParams& p, float4 v, typename EpiOper
   } else if constexpr (EPI == P2R_EPI_BIAS_GELU) {
     const float2 p0 = __fadd2_rn(make_float2(v.x, v.y), make_float2(b.x, b.y));
     const float2 p1 = __fadd2_rn(make_float2(v.z, v.w), make_float2(b.z, b.w));
+    float2 d0, d1;
+    const float2 g0 = gelu_pair2(p0, d0), g1 = gelu_pair2(p1, d1);
     *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.c2) + row * p.ldc2 + col) =
-        make_uint2(pack2_bf16(p0.x, p0.y), pack2_bf16(p1.x, p1.y));
-    const float2 g0 = gelu2(p0), g1 = gelu2(p1);
+        make_uint2(pack2_bf16(d0.x, d0.y), pack2_bf16(d1.x, d1.y));
     *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(cbase) + o) =
         make_uint2(pack2_bf16(g0.x, g0.y), pack2_bf16(g1.x, g1.y));
   } else if constexpr (EPI == P2R_EPI_DGELU) {
-    const float4 pre = unpack4_bf16(x);
-    const float2 d0 = __fmul2_rn(make_float2(v.x, v.y), gelu_grad2(make_float2(pre.x, pre.y)));
-    const float2 d1 = __fmul2_rn(make_float2(v.z, v.w), gelu_grad2(make_float2(pre.z, pre.w)));
+    const float4 gd = unpack4_bf16(x);  // the stored GELU derivative
+    const float2 d0 = __fmul2_rn(make_float2(v.x, v.y), make_float2(gd.x, gd.y));
+    const float2 d1 = __fmul2_rn(make_float2(v.z, v.w), make_float2(gd.z, gd.w));
     *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(cbase) + o) =
         make_uint2(pack2_bf16(d0.x, d0.y), pack2_bf16(d1.x, d1.y));
     return make_float4(d0.x, d0.y, d1.x, d1.y);
@@ -606,9 +609,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                                           reinterpret_cast<const float2*>(b4)[j]);
               if constexpr (EPI == P2R_EPI_BF16) {
                 o[j] = pack2_bf16(x.x, x.y);
-              } else {  // BIAS_GELU
-                pr[j] = pack2_bf16(x.x, x.y);
-                const float2 g = gelu2(x);
+              } else {  // BIAS_GELU: gelu and the stored derivative
+                float2 gd;
+                const float2 g = gelu_pair2(x, gd);
+                pr[j] = pack2_bf16(gd.x, gd.y);
                 o[j] = pack2_bf16(g.x, g.y);
               }
               if (zrow) {

@@ -548,6 +548,14 @@ __global__ void __launch_bounds__(384, 1)
 // S/dP are single-buffered per tile in TMEM: the group releases them (s_free)
 // as soon as both halves are in registers. Still deterministic (fixed order).
 // ============================================================================
+// Exponentials of the recomputed P moved from the SFU (16 ex2 / clk / SM, the
+// softmax groups' bound) to the FMA pipe: this many of every 16 pairs of a 32-key
+// half row (dQ) or 32-query half row (dK/dV) use exp2_fma2.
+#ifndef P2R_BWD_FMA_PAIRS
+#define P2R_BWD_FMA_PAIRS 5
+#endif
+constexpr int kBwdFmaPairs = P2R_BWD_FMA_PAIRS;
+
 struct DqPP {
   static constexpr int HD = 64, BQ = 128, BKV = 64, NS = 4;
   static constexpr int QT = BQ * HD * 2;    // one Q or dO tile (16 KB)
@@ -834,8 +842,14 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
             for (int i = 0; i < 32; i += 2) {
               const float2 z = __ffma2_rn(make_float2(s[i], s[i + 1]), sl2p, nl);
-              s[i] = ex2_approx(z.x);
-              s[i + 1] = ex2_approx(z.y);
+              if (i / 2 >= 16 - kBwdFmaPairs) {
+                const float2 e = exp2_fma2(z);
+                s[i] = e.x;
+                s[i + 1] = e.y;
+              } else {
+                s[i] = ex2_approx(z.x);
+                s[i + 1] = ex2_approx(z.y);
+              }
             }
           }
           if (lim < 32) {
@@ -1169,10 +1183,22 @@ __global__ void __launch_bounds__(384, 1)
             const float4 l4 = lds128f(lda + 16 * c4);
             const float2 z0 = __ffma2_rn(make_float2(s[4 * c4 + 0], s[4 * c4 + 1]), sl2p, make_float2(l4.x, l4.y));
             const float2 z1 = __ffma2_rn(make_float2(s[4 * c4 + 2], s[4 * c4 + 3]), sl2p, make_float2(l4.z, l4.w));
-            s[4 * c4 + 0] = ex2_approx(z0.x);
-            s[4 * c4 + 1] = ex2_approx(z0.y);
-            s[4 * c4 + 2] = ex2_approx(z1.x);
-            s[4 * c4 + 3] = ex2_approx(z1.y);
+            if (2 * c4 >= 16 - kBwdFmaPairs) {
+              const float2 e0 = exp2_fma2(z0);
+              s[4 * c4 + 0] = e0.x;
+              s[4 * c4 + 1] = e0.y;
+            } else {
+              s[4 * c4 + 0] = ex2_approx(z0.x);
+              s[4 * c4 + 1] = ex2_approx(z0.y);
+            }
+            if (2 * c4 + 1 >= 16 - kBwdFmaPairs) {
+              const float2 e1 = exp2_fma2(z1);
+              s[4 * c4 + 2] = e1.x;
+              s[4 * c4 + 3] = e1.y;
+            } else {
+              s[4 * c4 + 2] = ex2_approx(z1.x);
+              s[4 * c4 + 3] = ex2_approx(z1.y);
+            }
           }
           if (lo > 0 || hi < 32) {
 #pragma unroll

@@ -97,21 +97,7 @@ P2R_DEVICE float exp2_fma(float x) {
 // Pair form on the FP32x2 pipe (FFMA2/FADD2): the softmax is issue-bound.
 // t = z + M rounds z to an integer n (exact: M = 1.5*2^23), -n = M - t and
 // f = z - n are exact, so this matches exp2_fma bit-for-bit.
-P2R_DEVICE float2 exp2_fma2(float2 z) {
-  z.x = fmaxf(z.x, -125.0f);
-  z.y = fmaxf(z.y, -125.0f);
-  const float2 M = make_float2(12582912.0f, 12582912.0f);
-  const float2 t = __fadd2_rn(z, M);
-  const float2 nn = __ffma2_rn(t, make_float2(-1.0f, -1.0f), M);  // -n
-  const float2 f = __fadd2_rn(z, nn);
-  float2 q = __ffma2_rn(make_float2(5.502931029e-02f, 5.502931029e-02f), f,
-                        make_float2(2.422568053e-01f, 2.422568053e-01f));
-  q = __ffma2_rn(q, f, make_float2(6.932530403e-01f, 6.932530403e-01f));
-  q = __ffma2_rn(q, f, make_float2(9.999513626e-01f, 9.999513626e-01f));
-  constexpr uint32_t kMagicExp = 0x4B400000u << 23;  // (bits of M) << 23 mod 2^32: only the sum matters
-  return make_float2(__uint_as_float(__float_as_uint(q.x) + (__float_as_uint(t.x) << 23) - kMagicExp),
-                     __uint_as_float(__float_as_uint(q.y) + (__float_as_uint(t.y) << 23) - kMagicExp));
-}
+// (exp2_fma2: common.cuh)
 P2R_DEVICE float max3f(float a, float b, float c) {
   float r;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));

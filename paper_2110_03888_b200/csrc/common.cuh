@@ -452,6 +452,25 @@ P2R_DEVICE float2 gelu_grad2(float2 x) {
   return __ffma2_rn(__fmul2_rn(x, e), make_float2(0.39894228040143268f, 0.39894228040143268f), cdf);
 }
 
+// 2^z on the FMA pipe (FP32x2), for softmax exponentials beyond what the SFU
+// (16 ex2 / clk / SM on B200) sustains: z = n + f with n = round(z) via the
+// 1.5*2^23 trick, 2^f by a degree-3 minimax polynomial (|rel err| < 1e-4: the
+// results feed bf16 MMA operands), 2^n added to the exponent bits. z >= -125.
+P2R_DEVICE float2 exp2_fma2(float2 z) {
+  z.x = fmaxf(z.x, -125.0f);
+  z.y = fmaxf(z.y, -125.0f);
+  const float2 M = make_float2(12582912.0f, 12582912.0f);
+  const float2 t = __fadd2_rn(z, M);
+  const float2 nn = __ffma2_rn(t, make_float2(-1.0f, -1.0f), M);  // -n
+  const float2 f = __fadd2_rn(z, nn);
+  float2 q = __ffma2_rn(make_float2(5.502931029e-02f, 5.502931029e-02f), f,
+                        make_float2(2.422568053e-01f, 2.422568053e-01f));
+  q = __ffma2_rn(q, f, make_float2(6.932530403e-01f, 6.932530403e-01f));
+  q = __ffma2_rn(q, f, make_float2(9.999513626e-01f, 9.999513626e-01f));
+  constexpr uint32_t kMagicExp = 0x4B400000u << 23;  // (bits of M) << 23 mod 2^32: only the sum matters
+  return make_float2(__uint_as_float(__float_as_uint(q.x) + (__float_as_uint(t.x) << 23) - kMagicExp),
+                     __uint_as_float(__float_as_uint(q.y) + (__float_as_uint(t.y) << 23) - kMagicExp));
+}
 // Static boustrophedon schedule for persistent kernels over work items sorted
 // heaviest-first: CTA c of G takes item c in round 0, G-1-c in round 1, ...
 // (pairs heavy with light items; strictly increasing per CTA).

@@ -15,8 +15,21 @@ CPP_OBJS:= $(patsubst $(CSRC)/engine/%.cpp,$(BUILD)/engine/%.o,$(CPP_SRCS))
 LIB     := $(PKG)/libp2r.so
 
 DROPIN  := $(BUILD)/dropin_mini_controller
+# diagnostic build (A/B variants selected by env: legacy mma.sync attention, one-tile
+# attention backward at hd 64, bulk-ring LayerNorm forward, plain gate kernel); the
+# product library does not carry them. Loaded through P2R_LIB by tests / scripts.
+DIAG_SRCS := attention attention_bwd_tc moe norm_embed_ce
+DIAG_OBJS := $(patsubst %,$(BUILD)/diag/%.o,$(DIAG_SRCS))
+DIAG_LIB  := $(BUILD)/libp2r_diag.so
 
-all: $(LIB) $(DROPIN)
+all: $(LIB) $(DROPIN) $(DIAG_LIB)
+
+$(BUILD)/diag/%.o: $(CSRC)/%.cu $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h) include/p2r_cuda.h
+	@mkdir -p $(dir $@)
+	$(NVCC) $(NVFLAGS) -DP2R_DIAG -c $< -o $@
+
+$(DIAG_LIB): $(DIAG_OBJS) $(filter-out $(patsubst %,$(BUILD)/%.o,$(DIAG_SRCS)),$(CU_OBJS)) $(CPP_OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $^ -cudart static
 
 # a reference-style controller compiled against the drop-in headers, linked with libp2r.so
 $(DROPIN): tests/dropin/mini_controller.cpp $(LIB) $(wildcard include/p2r/*.hpp)

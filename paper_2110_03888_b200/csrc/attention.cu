@@ -10,13 +10,17 @@
 // (tensor.cpp:483). Backward is deterministic (no float atomics): one kernel
 // produces dQ (+ the rowsum(dO*O) term), a second produces dK/dV.
 //
-// Round-1 implementation uses bf16 mma.sync.m16n8k16 (fp32 accumulate).
+// The kernels are tcgen05/TMEM (attention_tc.cu, attention_bwd_tc.cu); this file
+// holds the C-ABI entry points. The round-1 bf16 mma.sync.m16n8k16 kernels below
+// are compiled only into the diagnostic build (-DP2R_DIAG, build/libp2r_diag.so,
+// P2R_ATTN_MMA_SYNC=1) for A/B measurements; the product library does not carry them.
 #include <cstdlib>
 
 #include "../../include/p2r_cuda.h"
 #include "common.cuh"
 #include "p2r_internal.h"
 
+#ifdef P2R_DIAG
 namespace p2r {
 namespace attn {
 
@@ -523,17 +527,9 @@ p2r_status run_bwd(const AttnParams& p, cudaStream_t s) {
   return P2R_OK;
 }
 
-}  // namespace attn
-}  // namespace p2r
-
-using namespace p2r;
-
-extern "C" p2r_status p2r_attention_fwd(const void* qkv, void* o, float* lse, int B, int H, int S,
-                                        int d, int causal, void* stream) {
-  if (B < 0 || H <= 0 || S < 0 || d <= 0 || d % H != 0)
-    return set_error(P2R_EINVAL, "masked_attention: q/k/v must share a [B,H,S,hd] shape");
-  if (B == 0 || S == 0) return P2R_OK;  // empty batch / sequence: nothing to compute
-  attn::AttnParams p{};
+p2r_status legacy_fwd(const void* qkv, void* o, float* lse, int B, int H, int S, int d, int causal,
+                      cudaStream_t s) {
+  AttnParams p{};
   p.qkv = static_cast<const __nv_bfloat16*>(qkv);
   p.o = static_cast<__nv_bfloat16*>(o);
   p.lse = lse;
@@ -544,23 +540,12 @@ extern "C" p2r_status p2r_attention_fwd(const void* qkv, void* o, float* lse, in
   p.causal = causal;
   const int hd = d / H;
   p.scale = 1.0f / sqrtf(static_cast<float>(hd));
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  // tcgen05/TMEM kernel (attention_tc.cu) unless explicitly asked for the mma.sync one
-  static const bool legacy = std::getenv("P2R_ATTN_MMA_SYNC") != nullptr;
-  if (!legacy && (hd == 64 || hd == 128) && (d % 8) == 0)
-    return attention_fwd_tc(qkv, o, lse, B, H, S, d, causal, s);
-  if (hd == 64) return attn::run_fwd<64>(p, s);
-  if (hd == 128) return attn::run_fwd<128>(p, s);
-  return set_error(P2R_EINVAL, "attention: head_dim must be 64 or 128");
+  return hd == 64 ? run_fwd<64>(p, s) : run_fwd<128>(p, s);
 }
 
-extern "C" p2r_status p2r_attention_bwd(const void* qkv, const void* o, const float* lse,
-                                        const void* dout, float* dsum_ws, void* dqkv, int B, int H,
-                                        int S, int d, int causal, void* stream) {
-  if (B < 0 || H <= 0 || S < 0 || d <= 0 || d % H != 0)
-    return set_error(P2R_EINVAL, "masked_attention: q/k/v must share a [B,H,S,hd] shape");
-  if (B == 0 || S == 0) return P2R_OK;  // empty batch / sequence: nothing to compute
-  attn::AttnParams p{};
+p2r_status legacy_bwd(const void* qkv, const void* o, const float* lse, const void* dout, float* dsum_ws, void* dqkv,
+                      int B, int H, int S, int d, int causal, cudaStream_t s) {
+  AttnParams p{};
   p.qkv = static_cast<const __nv_bfloat16*>(qkv);
   p.o = const_cast<__nv_bfloat16*>(static_cast<const __nv_bfloat16*>(o));
   p.lse = const_cast<float*>(lse);
@@ -574,11 +559,43 @@ extern "C" p2r_status p2r_attention_bwd(const void* qkv, const void* o, const fl
   p.causal = causal;
   const int hd = d / H;
   p.scale = 1.0f / sqrtf(static_cast<float>(hd));
+  return hd == 64 ? run_bwd<64>(p, s) : run_bwd<128>(p, s);
+}
+
+}  // namespace attn
+}  // namespace p2r
+
+#endif  // P2R_DIAG
+
+using namespace p2r;
+
+extern "C" p2r_status p2r_attention_fwd(const void* qkv, void* o, float* lse, int B, int H, int S,
+                                        int d, int causal, void* stream) {
+  if (B < 0 || H <= 0 || S < 0 || d <= 0 || d % H != 0)
+    return set_error(P2R_EINVAL, "masked_attention: q/k/v must share a [B,H,S,hd] shape");
+  if (B == 0 || S == 0) return P2R_OK;  // empty batch / sequence: nothing to compute
+  const int hd = d / H;
+  if (hd != 64 && hd != 128) return set_error(P2R_EINVAL, "attention: head_dim must be 64 or 128");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+#ifdef P2R_DIAG
   static const bool legacy = std::getenv("P2R_ATTN_MMA_SYNC") != nullptr;
-  if (!legacy && (hd == 64 || hd == 128) && (d % 8) == 0)
-    return attention_bwd_tc(qkv, o, lse, dout, dsum_ws, dqkv, B, H, S, d, causal, s);
-  if (hd == 64) return attn::run_bwd<64>(p, s);
-  if (hd == 128) return attn::run_bwd<128>(p, s);
-  return set_error(P2R_EINVAL, "attention: head_dim must be 64 or 128");
+  if (legacy) return attn::legacy_fwd(qkv, o, lse, B, H, S, d, causal, s);
+#endif
+  return attention_fwd_tc(qkv, o, lse, B, H, S, d, causal, s);
+}
+
+extern "C" p2r_status p2r_attention_bwd(const void* qkv, const void* o, const float* lse,
+                                        const void* dout, float* dsum_ws, void* dqkv, int B, int H,
+                                        int S, int d, int causal, void* stream) {
+  if (B < 0 || H <= 0 || S < 0 || d <= 0 || d % H != 0)
+    return set_error(P2R_EINVAL, "masked_attention: q/k/v must share a [B,H,S,hd] shape");
+  if (B == 0 || S == 0) return P2R_OK;  // empty batch / sequence: nothing to compute
+  const int hd = d / H;
+  if (hd != 64 && hd != 128) return set_error(P2R_EINVAL, "attention: head_dim must be 64 or 128");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+#ifdef P2R_DIAG
+  static const bool legacy = std::getenv("P2R_ATTN_MMA_SYNC") != nullptr;
+  if (legacy) return attn::legacy_bwd(qkv, o, lse, dout, dsum_ws, dqkv, B, H, S, d, causal, s);
+#endif
+  return attention_bwd_tc(qkv, o, lse, dout, dsum_ws, dqkv, B, H, S, d, causal, s);
 }

@@ -1282,10 +1282,11 @@ p2r_status run(const void* qkv, const BwdParams& p, cudaStream_t s) {
   if (!map2d(&qkv128, qkv, T, 3ull * p.d, 128) || !map2d(&qkv64, qkv, T, 3ull * p.d, 64) ||
       !map2d(&do128, p.dout, T, p.d, 128) || !map2d(&do64, p.dout, T, p.d, 64))
     return set_error(P2R_ECUDA, "attention bwd: tensor map encode failed");
-  static cudaError_t a1 = cudaFuncSetAttribute(attn_bwd_dq_tc<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, DqCfg<HD>::SMEM);
-  static cudaError_t a2 = cudaFuncSetAttribute(attn_bwd_dkdv_tc<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, KvCfg<HD>::SMEM);
-  if (a1 != cudaSuccess || a2 != cudaSuccess) return set_cuda_error(a1 ? a1 : a2, "attention bwd attr");
+#ifdef P2R_DIAG  // diagnostic build: P2R_ATTN_BWD_V1=1 runs the one-tile kernels at hd 64 too
   static const bool v1 = std::getenv("P2R_ATTN_BWD_V1") != nullptr;
+#else
+  constexpr bool v1 = false;
+#endif
   if (HD == 64 && !v1) {  // ping-pong kernels: two 128-row tiles per CTA
     static cudaError_t a3 = cudaFuncSetAttribute(attn_bwd_dq_pp, cudaFuncAttributeMaxDynamicSharedMemorySize, DqPP::SMEM);
     static cudaError_t a4 =
@@ -1298,6 +1299,12 @@ p2r_status run(const void* qkv, const BwdParams& p, cudaStream_t s) {
                  dim3(n_dq < kNumSMs ? n_dq : kNumSMs), dim3(384), KvPP::SMEM, s, 1, qkv128, qkv64, do64, p);
     return P2R_OK;
   }
+#ifndef P2R_DIAG
+  if constexpr (HD == 64) return P2R_OK;  // (unreachable: hd 64 always runs the ping-pong kernels)
+#endif
+  static cudaError_t a1 = cudaFuncSetAttribute(attn_bwd_dq_tc<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, DqCfg<HD>::SMEM);
+  static cudaError_t a2 = cudaFuncSetAttribute(attn_bwd_dkdv_tc<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, KvCfg<HD>::SMEM);
+  if (a1 != cudaSuccess || a2 != cudaSuccess) return set_cuda_error(a1 ? a1 : a2, "attention bwd attr");
   const dim3 grid((p.S + 127) / 128, p.H, p.B);
   P2R_LAUNCH_K("attention bwd dq (tcgen05)", attn_bwd_dq_tc<HD>, grid, dim3(384), DqCfg<HD>::SMEM, s, 1, qkv128,
                qkv64, do128, p);

@@ -548,10 +548,14 @@ extern "C" p2r_status p2r_moe_gate_logits(const float* b, const float* gate, int
   if (T <= 0) return P2R_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int blocks = (T + 31) / 32;
-  static const bool plain = [] {  // P2R_GATE_PLAIN=1: the plain kernel (tests compare the two bit for bit)
+#ifdef P2R_DIAG  // diagnostic build: P2R_GATE_PLAIN=1 forces the plain kernel (tests compare the two bit for bit)
+  static const bool plain = [] {
     const char* e = std::getenv("P2R_GATE_PLAIN");
     return e != nullptr && e[0] == '1';
   }();
+#else
+  constexpr bool plain = false;
+#endif
   if (!plain && d % 32 == 0 && (E == 8 || E == 16 || E == 32 || E == 64)) {
     cudaError_t le = cudaSuccess;
     if (E == 8) le = launch_k(gate_logits_rt_kernel<8, 32, 1>, dim3(blocks), dim3(64), 0, s, 1, b, gate, T, d, logits);

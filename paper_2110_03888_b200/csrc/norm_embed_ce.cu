@@ -464,7 +464,7 @@ constexpr int kLnSmemAttr = 200 * 1024;  // opt-in dynamic limit (leaves room fo
 struct LnLaunch {
   int nst, smem, blocks, warps;
 };
-LnLaunch ln_fwd_launch(int rows, int d) {
+[[maybe_unused]] LnLaunch ln_fwd_launch(int rows, int d) {  // (the bulk-ring forward: diagnostic build)
   LnLaunch l{};
   l.nst = kLnMaxStages;
   while (l.nst > 1 && 2 * d * 4 + kLnFwdWarps * l.nst * d * 4 > 110 * 1024) --l.nst;
@@ -504,13 +504,16 @@ extern "C" p2r_status p2r_layernorm_fwd(const float* x, const float* gain, const
                                         float* mean, float* rstd, void* stream) {
   if (rows <= 0) return P2R_OK;
   if (!ln_dim_ok(d)) return set_error(P2R_EINVAL, "layernorm: d_model must be a multiple of 128 in [128, 2048]");
-  const LnLaunch l = ln_fwd_launch(rows, d);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   auto* y16 = static_cast<__nv_bfloat16*>(y_bf16);
+#ifdef P2R_DIAG  // diagnostic build: P2R_LN_FWD_RING=1 selects the bulk-ring forward
   static const bool ring = [] {
     const char* e = std::getenv("P2R_LN_FWD_RING");
     return e != nullptr && e[0] == '1';
   }();
+#else
+  constexpr bool ring = false;
+#endif
   if (!ring) {
     switch (d / 128) {
 #define P2R_LN_FWD_REG(NV)                                                                                  \
@@ -527,6 +530,8 @@ extern "C" p2r_status p2r_layernorm_fwd(const float* x, const float* gain, const
     P2R_CHECK_LAUNCH("layernorm fwd");
     return P2R_OK;
   }
+#ifdef P2R_DIAG
+  const LnLaunch l = ln_fwd_launch(rows, d);
   switch (d / 128) {
 #define P2R_LN_FWD(NV)                                                                                     \
   case NV: {                                                                                               \
@@ -543,6 +548,7 @@ extern "C" p2r_status p2r_layernorm_fwd(const float* x, const float* gain, const
     default: break;
   }
   P2R_CHECK_LAUNCH("layernorm fwd");
+#endif
   return P2R_OK;
 }
 

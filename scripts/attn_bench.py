@@ -1,4 +1,5 @@
-"""Attention fwd/bwd timing (CUDA events) at the C2 shape; P2R_ATTN_MMA_SYNC=1 selects the legacy fwd."""
+"""Attention fwd/bwd timing (CUDA events) at the C2 shape; P2R_LIB=build/libp2r_diag.so P2R_ATTN_MMA_SYNC=1
+selects the legacy mma.sync kernels of the diagnostic build."""
 import ctypes
 import sys
 import torch

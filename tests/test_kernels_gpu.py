@@ -342,8 +342,9 @@ def test_empty_and_degenerate_inputs(cuda):
                                    (130, 64, 8)])
 def test_gate_logits_tiled_bit_identical(cuda, T, d, E):
     """The register-tiled gate kernel keeps every logit's FFMA chain in c order, so its
-    logits equal the plain kernel's bit for bit (P2R_GATE_PLAIN=1 in a subprocess) and
-    the fp32 matmul(b, gate) of model.cpp:250 to fp32 rounding."""
+    logits equal the plain kernel's bit for bit (P2R_GATE_PLAIN=1 in a subprocess on the
+    diagnostic build, which carries that switch) and the fp32 matmul(b, gate) of
+    model.cpp:250 to fp32 rounding."""
     import subprocess
     import sys
     import torch
@@ -366,8 +367,11 @@ def test_gate_logits_tiled_bit_identical(cuda, T, d, E):
     import tempfile
     with tempfile.TemporaryDirectory() as td:
         path = os.path.join(td, "plain.npy")
-        env = dict(os.environ, P2R_GATE_PLAIN="1")
         root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        diag = os.path.join(root, "build", "libp2r_diag.so")
+        if not os.path.exists(diag):
+            pytest.skip("build/libp2r_diag.so not built (make)")
+        env = dict(os.environ, P2R_GATE_PLAIN="1", P2R_LIB=diag)
         subprocess.run([sys.executable, "-c", code, path], check=True, env=env, cwd=root)
         plain = np.load(path)
     assert np.array_equal(out.cpu().numpy().view(np.uint32), plain.view(np.uint32))

@@ -309,7 +309,7 @@ def build_workload(args, p2r, dist, rank, world):
         text = (f"C3 Pseudo MoE ({L} shared layers, d=1024, 16 heads, d_ff=4096, {E} experts top-1 cf 1.25, "
                 f"vocab 260, seq 1024) delinked into {L} Real layers; Real-model fwd+bwd+AdamW, "
                 f"experts over {world} GPU(s)")
-        return real, B, S, text, flops_per_token(1024, 4096, L, S, E=E), False, f"ep{world}+dp{world}"
+        return real, B, S, text, flops_per_token(1024, 4096, L, S, E=E), world == 1, f"ep{world}+dp{world}"
     if args.workload == "c4":
         E = 8 * world  # 8 experts per GPU: the C4 per-rank share (64 experts at N = 8)
         L = args.layers or 48
@@ -317,7 +317,7 @@ def build_workload(args, p2r, dist, rank, world):
         comm_init(m, p2r, dist, rank, world)
         text = (f"C4 M6-style MoE per-rank slice: {L} Real layers, d=2048, 16 heads, d_ff=4096, 8 experts per GPU "
                 f"({E} total) top-1 cf 1.25, vocab 260, seq 1024, fwd+bwd+AdamW")
-        return m, B, S, text, flops_per_token(2048, 4096, L, S, E=E), False, f"ep{world}+dp{world}"
+        return m, B, S, text, flops_per_token(2048, 4096, L, S, E=E), world == 1, f"ep{world}+dp{world}"
     raise SystemExit(f"unknown workload {args.workload}")
 
 
@@ -622,7 +622,8 @@ def main_p2r(args):
            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
            "config": {"workload": workload, "global_batch": B * world, "seq_len": S,
                       "parallelism": par, "l2": "inputs larger than L2 (GBs of activations per step)",
-                      "launch": "one CUDA graph per fwd+bwd step + eager AdamW" if use_graph else "eager",
+                      "launch": ("one CUDA graph per fwd+bwd step + eager AdamW" if use_graph
+                                 else "eager (the expert-parallel exchange's stream flags stay outside graphs)"),
                       "mfu_model_flops_per_token": model_flops},
            "clocks": clk, "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline,
            "kernels": breakdown,

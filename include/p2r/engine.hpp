@@ -287,9 +287,10 @@ class Engine {
 
   cudaStream_t stream() const { return stream_; }
   // train_step_device replayed as one CUDA graph (captured on the first call,
-  // re-captured when any argument changes): resident, MoE-free models (the data-
-  // parallel all-reduce stays outside); the launches (and their PDL edges) are
-  // those of train_step_device, so results are bit-identical to it.
+  // re-captured when any argument changes): resident models on one rank's experts
+  // (dense, or MoE without the expert-parallel exchange; the data-parallel
+  // all-reduce stays outside); the launches (and their PDL edges) are those of
+  // train_step_device, so results are bit-identical to it.
   void train_step_device_graph(const int* d_tokens, const int* d_targets, const std::uint8_t* d_mask, int batch,
                                int seq, double denom, AttentionMode mode, bool zero, float* loss_dev);
   void set_profiling(bool on) { prof_.on = on; }

@@ -1126,8 +1126,10 @@ void Engine::train_step_device(const int* d_tokens, const int* d_targets, const 
 void Engine::train_step_device_graph(const int* d_tokens, const int* d_targets, const std::uint8_t* d_mask, int batch,
                                     int seq, double denom, AttentionMode mode, bool zero, float* loss_dev) {
   // (a dense model's communicator is only used by allreduce_grads, outside the step)
-  if (off_ || cfg_.moe.enabled() || prof_.on)
-    throw std::logic_error("train_step_device_graph: needs a resident, MoE-free, unprofiled model");
+  // (single-rank MoE qualifies: routing, counts and the grouped GEMMs' tile lists stay on
+  // the device; the expert-parallel exchange's stream flag operations are kept eager)
+  if (off_ || (cfg_.moe.enabled() && ep_active()) || prof_.on)
+    throw std::logic_error("train_step_device_graph: needs a resident, single-rank, unprofiled model");
   StepGraph& G = step_graph_;
   ensure_acts(batch, seq);  // (a no-op unless the shape changed: then the generation moves on)
   const bool same = G.exec && G.tok == d_tokens && G.tgt == d_targets && G.mask == d_mask && G.loss == loss_dev &&
@@ -1207,7 +1209,7 @@ float Engine::train_step_host(const int* tokens, const int* targets, const std::
     const char* e = std::getenv("P2R_STEP_GRAPH");
     return e == nullptr || std::atoi(e) != 0;
   }();
-  if (graph_on && !off_ && !cfg_.moe.enabled() && !prof_.on)
+  if (graph_on && !off_ && !(cfg_.moe.enabled() && ep_active()) && !prof_.on)
     train_step_device_graph(A.tokens.as<int>(), A.targets.as<int>(), mask ? A.mask.as<std::uint8_t>() : nullptr, batch,
                             seq, denom, mode, zero, nullptr);
   else

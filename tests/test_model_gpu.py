@@ -333,7 +333,27 @@ def test_train_step_graph_replay_bit_identical(cuda):
     ga, gb = models[0].grads(), models[1].grads()
     for n in ga:
         assert np.array_equal(ga[n], gb[n]), n
-    moe = p2r.Model(p2r.Config(d_model=256, d_ff=1024, n_layers_graph=2, n_layers_params=1, n_heads=4,
-                               vocab_size=260, seq_len=128, n_experts=4, n_prototypes=1), 1)
-    with pytest.raises(p2r.P2RLogicError, match="resident, MoE-free"):  # MoE: the EP exchange runs in the step
-        moe.train_step_device(tok.data_ptr(), tgt.data_ptr(), mask.data_ptr(), 8, 128, 1024.0, graph=True)
+    # single-rank MoE steps replay as a graph too (routing stays on the device), bitwise
+    moe_cfg = p2r.Config(d_model=256, d_ff=1024, n_layers_graph=3, n_layers_params=3, n_heads=4, vocab_size=260,
+                         seq_len=128, n_experts=4, n_prototypes=1)
+    ms = [p2r.Model(moe_cfg, 1) for _ in range(2)]
+    ml = [[], []]
+    for mi, m in enumerate(ms):
+        m.attach_adamw()
+        for i in range(3):
+            m.train_step_device(tok.data_ptr(), tgt.data_ptr(), mask.data_ptr(), 8, 128, 1024.0,
+                                loss_dev=loss.data_ptr(), graph=(mi == 1))
+            torch.cuda.synchronize()
+            ml[mi].append(float(loss))
+            m.adamw_step(1e-3)
+    assert ml[0] == ml[1]
+    pa, pb = ms[0].params(), ms[1].params()
+    for n in pa:
+        assert np.array_equal(pa[n], pb[n]), n
+    os.environ["P2R_FORCE_EP"] = "1"
+    try:
+        ep = p2r.Model(moe_cfg, 1, ep=(1, 0))
+    finally:
+        del os.environ["P2R_FORCE_EP"]
+    with pytest.raises(p2r.P2RLogicError, match="single-rank"):  # the EP exchange stays eager
+        ep.train_step_device(tok.data_ptr(), tgt.data_ptr(), mask.data_ptr(), 8, 128, 1024.0, graph=True)

@@ -125,13 +125,16 @@ p2r_status p2r_layernorm_bwd(const float* dy, const float* x, const float* mean,
                              const float* gain, const float* resid, int rows, int d, float* dx,
                              void* dx_bf16, float* ggain, float* gbias, float* partial_ws,
                              void* stream);
-/* Grid size (blocks) of the backward; the row count of its column-partial outputs. */
-int p2r_layernorm_bwd_blocks(int rows, int d, int has_resid);
+/* Grid size (blocks) of the backward; the row count of its column-partial outputs.
+ * flags: P2R_LN_RESID when a residual is added, P2R_LN_DY_BF16 for the bf16-dy entry. */
+#define P2R_LN_RESID 1
+#define P2R_LN_DY_BF16 2
+int p2r_layernorm_bwd_blocks(int rows, int d, int flags);
 /* p2r_layernorm_bwd plus the dense block's FFN2 bias gradient (add_bias backward,
  * tensor.cpp:227-231), which is the column sum of the residual-stream gradient this
  * call produces for the layer below:
  *  - dx_colsum_ws != NULL: dx's per-block column sums are written there
- *    ([p2r_layernorm_bwd_blocks(rows, d, resid != NULL)][d] floats);
+ *    ([p2r_layernorm_bwd_blocks(rows, d, resid != NULL ? P2R_LN_RESID : 0)][d] floats);
  *  - colsum_in != NULL: colsum_dst[c] += the sum of colsum_in's colsum_blocks rows
  *    (an earlier call's dx_colsum_ws), block order, in the same finish kernel as
  *    ggain/gbias. colsum_in, colsum_blocks and colsum_dst go together (else EINVAL). */
@@ -140,6 +143,14 @@ p2r_status p2r_layernorm_bwd_fused(const float* dy, const float* x, const float*
                                    int d, float* dx, void* dx_bf16, float* ggain, float* gbias,
                                    float* partial_ws, float* dx_colsum_ws, const float* colsum_in,
                                    int colsum_blocks, float* colsum_dst, void* stream);
+/* The same with a bf16 dy ([rows][d] bf16, the dX GEMM's rounded output): the ring
+ * stages half the dy bytes; everything else (fp32 statistics and accumulation) is
+ * unchanged. Column partials: p2r_layernorm_bwd_blocks(..., flags | P2R_LN_DY_BF16). */
+p2r_status p2r_layernorm_bwd_fused_bf16(const void* dy_bf16, const float* x, const float* mean,
+                                        const float* rstd, const float* gain, const float* resid, int rows,
+                                        int d, float* dx, void* dx_bf16, float* ggain, float* gbias,
+                                        float* partial_ws, float* dx_colsum_ws, const float* colsum_in,
+                                        int colsum_blocks, float* colsum_dst, void* stream);
 
 /* Embeddings (embedding_lookup x2 + add, model.cpp:229-241; tensor.cpp:338-368). */
 p2r_status p2r_embed_fwd(const int* ids, const float* tok, const float* pos, int T, int S, int d,

@@ -12,7 +12,8 @@ from . import p2r_oracle as O
 
 F32 = np.float32
 ALL_POINTS = ("w16", "a16", "qkv16", "p16", "o16", "b16", "gd16", "g16", "h16",
-              "dlogits16", "dres16", "dh16", "dx1_16", "do16", "ds16", "dqkv16", "ye16", "dye16", "dxe16")
+              "dlogits16", "dres16", "dh16", "dx1_16", "do16", "ds16", "dqkv16", "ye16", "dye16", "dxe16",
+              "dln16")
 
 
 def bf16(x):
@@ -114,7 +115,7 @@ def loss_and_grads(cfg: O.Config, params: dict, tokens, targets, mask, batch, de
     G = {k: np.zeros_like(v) for k, v in P0.items()}
     G["embed.tok"] += gl16.T @ h16
     dh = gl16 @ W["embed.tok"]
-    dres, gg, gb = O.layernorm_bwd(dh.astype(F32), xhf, invf, P0["final_norm.gain"])
+    dres, gg, gb = O.layernorm_bwd(R(dh, "dln16"), xhf, invf, P0["final_norm.gain"])
     G["final_norm.gain"] += gg
     G["final_norm.bias"] += gb
     for g in reversed(range(c.n_layers_graph)):
@@ -149,7 +150,7 @@ def loss_and_grads(cfg: O.Config, params: dict, tokens, targets, mask, batch, de
             dh16 = R((dy16 @ W[pr + "ffn.w2"].T) * hpre16, "dh16")
             G[pr + "ffn.w1"] += b16.T @ dh16
             G[pr + "ffn.b1"] += dh16.sum(0)
-            db = (dh16 @ W[pr + "ffn.w1"].T).astype(F32)
+            db = R((dh16 @ W[pr + "ffn.w1"].T).astype(F32), "dln16")
         gx1, gg, gb = O.layernorm_bwd(db, xh2, inv2, P0[pr + "ln2.gain"])
         G[pr + "ln2.gain"] += gg
         G[pr + "ln2.bias"] += gb
@@ -170,7 +171,7 @@ def loss_and_grads(cfg: O.Config, params: dict, tokens, targets, mask, batch, de
         G[pr + "attn.wq"] += dw[:, :d]
         G[pr + "attn.wk"] += dw[:, d:2 * d]
         G[pr + "attn.wv"] += dw[:, 2 * d:]
-        da = (dqkv @ wqkv.T).astype(F32)
+        da = R((dqkv @ wqkv.T).astype(F32), "dln16")
         gxa, gg, gb = O.layernorm_bwd(da, xh1, inv1, P0[pr + "ln1.gain"])
         G[pr + "ln1.gain"] += gg
         G[pr + "ln1.bias"] += gb

@@ -186,7 +186,7 @@ struct Acts {
   // recomputed from the layer input in the backward
   std::vector<char> ckpt;
   LayerActs ck;
-  DevBuf h16, meanf, rstdf, logits32, dlogits16, loss, loss_sum, ce_ws, dh32;
+  DevBuf h16, meanf, rstdf, logits32, dlogits16, loss, loss_sum, ce_ws;
   DevBuf dres, dres16, tmp32, dx1, dx1_16, do16, dqkv16, dh16, dye16, dw, glogits, dsum;
   DevBuf dxe16_own;
   void* dxe16 = nullptr;  // expert-input gradients [E][seg] bf16 (local, or the arena's return buffer)
@@ -634,10 +634,8 @@ void Engine::ensure_acts(int B, int S) {
   A->loss = DevBuf(4);
   A->loss_sum = DevBuf(8);
   A->ce_ws = DevBuf(p2r_cross_entropy_workspace(T));
-  A->dh32 = DevBuf(Td * 4);
   A->dres = DevBuf(Td * 4);
   A->dres16 = DevBuf(Td * 2);
-  A->tmp32 = DevBuf(Td * 4);
   A->dx1 = DevBuf(Td * 4);
   A->dx1_16 = DevBuf(Td * 2);
   A->do16 = DevBuf(Td * 2);
@@ -647,6 +645,7 @@ void Engine::ensure_acts(int B, int S) {
     A->dh16 = DevBuf(static_cast<std::size_t>(T) * dff * 2);
   } else {
     A->dh16 = DevBuf(ES * dff * 2);
+    A->tmp32 = DevBuf(Td * 4);  // fp32 sum of the dispatch backward (LN2's dy)
     A->dye16 = DevBuf(ES * d * 2);
     A->dw = DevBuf(static_cast<std::size_t>(T) * k * 4);
     if (!ep_active()) {
@@ -659,9 +658,11 @@ void Engine::ensure_acts(int B, int S) {
     A->glogits = DevBuf(static_cast<std::size_t>(T) * E * 4);
   }
   A->ln_ws = DevBuf(p2r_layernorm_bwd_workspace(T, d));
-  if (db2_fused())
-    A->db2_stage = DevBuf(static_cast<std::size_t>(std::max(p2r_layernorm_bwd_blocks(T, d, 0),
-                                                            p2r_layernorm_bwd_blocks(T, d, 1))) * d * 4);
+  if (db2_fused()) {
+    int nblk = 0;
+    for (int f = 0; f < 4; ++f) nblk = std::max(nblk, p2r_layernorm_bwd_blocks(T, d, f));
+    A->db2_stage = DevBuf(static_cast<std::size_t>(nblk) * d * 4);
+  }
   const int bias_n = std::max(dff, d);
   A->colsum_ws = DevBuf(p2r_colsum_workspace(std::max(T, A->seg), bias_n, std::max(1, E)));
   A->embed_ws = DevBuf(p2r_embed_bwd_workspace(T, cfg_.vocab_size));
@@ -948,10 +949,11 @@ void Engine::block_backward(int g, AttentionMode mode) {
     // db1 += colsum(dh) is folded into the GELU' epilogue (column partials of the bf16 dh)
     gemm(T, dff, d, dy16, d, false, lp16(o, layer_.w2), d, false, P2R_EPI_DGELU, A.dh16.p, dff, nullptr, 0, nullptr,
          L.hpre16.p, dff, 0, 0, 0, nullptr, 1, lg(o, layer_.b1));
-    // FFN1: dW1 += b^T dh ; db = dh W1^T
+    // FFN1: dW1 += b^T dh ; db = dh W1^T (bf16: the LN2 backward stages half the bytes;
+    // do16 is free until the O-projection backward below)
     gemm(d, dff, T, L.b16.p, d, true, A.dh16.p, dff, true, P2R_EPI_ACC_F32, lg(o, layer_.w1), dff, nullptr, 0,
          nullptr, nullptr, 0, 0, 0, 0, nullptr, 0 /* library picks the split */);
-    gemm(T, d, dff, A.dh16.p, dff, false, lp16(o, layer_.w1), dff, false, P2R_EPI_F32, A.tmp32.p, d);
+    gemm(T, d, dff, A.dh16.p, dff, false, lp16(o, layer_.w1), dff, false, P2R_EPI_BF16, A.do16.p, d);
   } else {
     const int E = cfg_.moe.n_experts, k = cfg_.moe.n_prototypes, seg = A.seg;
     const int* cnt = L.counts.as<int>();
@@ -1006,14 +1008,22 @@ void Engine::block_backward(int g, AttentionMode mode) {
   // column sums of dy into db2 (dense layers whose dres came from a LayerNorm backward)
   const bool db2_staged = db2_fused() && A.db2_for == g;
   A.db2_for = -1;
-  prof(P2R_PROF_LAYERNORM, 0, Td * 18, [&] {
-    p2r_check(p2r_layernorm_bwd_fused(A.tmp32.as<float>(), L.x1.as<float>(), L.mean2.as<float>(),
-                                      L.rstd2.as<float>(), lp(o, layer_.ln2_g), dy, T, d, A.dx1.as<float>(),
-                                      A.dx1_16.p, lg(o, layer_.ln2_g), lg(o, layer_.ln2_b), A.ln_ws.as<float>(),
-                                      nullptr, db2_staged ? A.db2_stage.as<float>() : nullptr,
-                                      db2_staged ? A.db2_blocks : 0, db2_staged ? lg(o, layer_.b2) : nullptr,
-                                      stream_),
-              "ln2 bwd");
+  const bool moe = cfg_.moe.enabled();  // MoE: db is the fp32 sum of the dispatch backward
+  prof(P2R_PROF_LAYERNORM, 0, moe ? Td * 18 : Td * 16, [&] {
+    if (moe)
+      p2r_check(p2r_layernorm_bwd_fused(A.tmp32.as<float>(), L.x1.as<float>(), L.mean2.as<float>(),
+                                        L.rstd2.as<float>(), lp(o, layer_.ln2_g), dy, T, d, A.dx1.as<float>(),
+                                        A.dx1_16.p, lg(o, layer_.ln2_g), lg(o, layer_.ln2_b), A.ln_ws.as<float>(),
+                                        nullptr, nullptr, 0, nullptr, stream_),
+                "ln2 bwd");
+    else
+      p2r_check(p2r_layernorm_bwd_fused_bf16(A.do16.p, L.x1.as<float>(), L.mean2.as<float>(), L.rstd2.as<float>(),
+                                             lp(o, layer_.ln2_g), dy, T, d, A.dx1.as<float>(), A.dx1_16.p,
+                                             lg(o, layer_.ln2_g), lg(o, layer_.ln2_b), A.ln_ws.as<float>(), nullptr,
+                                             db2_staged ? A.db2_stage.as<float>() : nullptr,
+                                             db2_staged ? A.db2_blocks : 0,
+                                             db2_staged ? lg(o, layer_.b2) : nullptr, stream_),
+                "ln2 bwd");
   });
   // O projection: dWo += o^T dx1 ; do = dx1 Wo^T
   gemm(d, d, T, L.o16.p, d, true, A.dx1_16.p, d, true, P2R_EPI_ACC_F32, lg(o, layer_.wo), d, nullptr, 0, nullptr,
@@ -1027,18 +1037,18 @@ void Engine::block_backward(int g, AttentionMode mode) {
   // QKV: dWqkv += a^T dqkv ; da = dqkv Wqkv^T
   gemm(d, 3 * d, T, L.a16.p, d, true, A.dqkv16.p, 3 * d, true, P2R_EPI_ACC_F32, lg(o, layer_.wqkv), 3 * d, nullptr,
        0, nullptr, nullptr, 0, 0, 0, 0, nullptr, 0 /* library picks the split */);
-  gemm(T, d, 3 * d, A.dqkv16.p, 3 * d, false, lp16(o, layer_.wqkv), 3 * d, false, P2R_EPI_F32, A.tmp32.p, d);
+  gemm(T, d, 3 * d, A.dqkv16.p, 3 * d, false, lp16(o, layer_.wqkv), 3 * d, false, P2R_EPI_BF16, A.do16.p, d);
   // LN1 backward: dx = dx1 + LN1'(da); for a dense layer below, also stage dx's column sums (its db2)
   const bool stage = db2_fused() && g > 0;
-  prof(P2R_PROF_LAYERNORM, 0, Td * 18, [&] {
-    p2r_check(p2r_layernorm_bwd_fused(A.tmp32.as<float>(), xin, L.mean1.as<float>(), L.rstd1.as<float>(),
-                                      lp(o, layer_.ln1_g), A.dx1.as<float>(), T, d, dy, dy16, lg(o, layer_.ln1_g),
-                                      lg(o, layer_.ln1_b), A.ln_ws.as<float>(),
-                                      stage ? A.db2_stage.as<float>() : nullptr, nullptr, 0, nullptr, stream_),
+  prof(P2R_PROF_LAYERNORM, 0, Td * 16, [&] {
+    p2r_check(p2r_layernorm_bwd_fused_bf16(A.do16.p, xin, L.mean1.as<float>(), L.rstd1.as<float>(),
+                                           lp(o, layer_.ln1_g), A.dx1.as<float>(), T, d, dy, dy16,
+                                           lg(o, layer_.ln1_g), lg(o, layer_.ln1_b), A.ln_ws.as<float>(),
+                                           stage ? A.db2_stage.as<float>() : nullptr, nullptr, 0, nullptr, stream_),
               "ln1 bwd");
   });
   if (stage) {
-    A.db2_blocks = p2r_layernorm_bwd_blocks(T, d, 1);
+    A.db2_blocks = p2r_layernorm_bwd_blocks(T, d, P2R_LN_RESID | P2R_LN_DY_BF16);
     A.db2_for = g - 1;
   }
   if (off_) offload_release(o, true);
@@ -1063,17 +1073,18 @@ DevTensor Engine::head_forward(GradTape* tape, const DevTensor& x) {
       // dtok += dlogits^T h ; dh = dlogits . tok
       gemm(V2, d2, T2, A2.dlogits16.p, A2.vld, true, A2.h16.p, d2, true, P2R_EPI_ACC_F32, eg(emb_.tok), d2, nullptr,
            0, nullptr, nullptr, 0, 0, 0, 0, nullptr, 0 /* library picks the split */);
-      gemm(T2, d2, V2, A2.dlogits16.p, A2.vld, false, ep16(emb_.tok), d2, true, P2R_EPI_F32, A2.dh32.p, d2);
+      gemm(T2, d2, V2, A2.dlogits16.p, A2.vld, false, ep16(emb_.tok), d2, true, P2R_EPI_BF16, A2.do16.p, d2);
       const bool stage = db2_fused();  // the last layer's db2 = column sums of this dres
-      prof(P2R_PROF_LAYERNORM, 0, 14.0 * T2 * d2, [&] {
-        p2r_check(p2r_layernorm_bwd_fused(A2.dh32.as<float>(), xin, A2.meanf.as<float>(), A2.rstdf.as<float>(),
-                                          ep(emb_.fin_g), nullptr, T2, d2, A2.dres.as<float>(), A2.dres16.p,
-                                          eg(emb_.fin_g), eg(emb_.fin_b), A2.ln_ws.as<float>(),
-                                          stage ? A2.db2_stage.as<float>() : nullptr, nullptr, 0, nullptr, stream_),
+      prof(P2R_PROF_LAYERNORM, 0, 12.0 * T2 * d2, [&] {
+        p2r_check(p2r_layernorm_bwd_fused_bf16(A2.do16.p, xin, A2.meanf.as<float>(), A2.rstdf.as<float>(),
+                                               ep(emb_.fin_g), nullptr, T2, d2, A2.dres.as<float>(), A2.dres16.p,
+                                               eg(emb_.fin_g), eg(emb_.fin_b), A2.ln_ws.as<float>(),
+                                               stage ? A2.db2_stage.as<float>() : nullptr, nullptr, 0, nullptr,
+                                               stream_),
                   "final ln bwd");
       });
       if (stage) {
-        A2.db2_blocks = p2r_layernorm_bwd_blocks(T2, d2, 0);
+        A2.db2_blocks = p2r_layernorm_bwd_blocks(T2, d2, P2R_LN_DY_BF16);
         A2.db2_for = cfg_.n_layers_graph - 1;
       }
     });

@@ -32,6 +32,32 @@ P2R_DEVICE void ln_row_issue(uint64_t* bar, uint32_t dst, const float* const* sr
   for (int t = 0; t < ntens; ++t) bulk_load(dst + t * bytes, src[t] + static_cast<long long>(row) * D, bytes, bar);
 }
 
+// One row of each of ntens tensors into a ring slot; tensor 0 has b0 bytes per
+// row (bf16 or fp32 dy), the others are fp32 rows of D floats packed behind it.
+P2R_DEVICE void ln_row_issue_b(uint64_t* bar, uint32_t dst, const void* const* src, int ntens, int row, int D,
+                               uint32_t b0) {
+  const uint32_t bytes = static_cast<uint32_t>(D) * 4;
+  mbar_arrive_expect_tx(bar, b0 + bytes * (ntens - 1));
+  bulk_load(dst, static_cast<const uint8_t*>(src[0]) + static_cast<long long>(row) * b0, b0, bar);
+  for (int t = 1; t < ntens; ++t)
+    bulk_load(dst + b0 + (t - 1) * bytes, static_cast<const float*>(src[t]) + static_cast<long long>(row) * D, bytes,
+              bar);
+}
+
+// four consecutive dy values of a ring row, fp32 or bf16 (8-byte shared load)
+template <bool DY16>
+P2R_DEVICE float4 ln_lds_dy(uint32_t row, int c4) {
+  if constexpr (DY16) {
+    uint32_t lo, hi;
+    asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(row + c4 * 8));
+    const float2 a = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&lo));
+    const float2 b = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&hi));
+    return make_float4(a.x, a.y, b.x, b.y);
+  } else {
+    return lds128f(row + c4 * 16);
+  }
+}
+
 P2R_DEVICE void st_bf16x4(__nv_bfloat16* p, float4 o) {
   __nv_bfloat162 lo = __floats2bfloat162_rn(o.x, o.y), hi = __floats2bfloat162_rn(o.z, o.w);
   uint2 w;
@@ -167,9 +193,9 @@ __global__ void __launch_bounds__(256) ln_fwd_reg_kernel(const float* __restrict
 // dx itself are accumulated the same way into cpartial[blockIdx.x][D] (the dense
 // block backward takes the FFN2 bias gradient of the layer below from them,
 // add_bias backward tensor.cpp:227-231, instead of re-reading dx).
-template <int NV, bool COLSUM>
+template <int NV, bool COLSUM, bool DY16>
 __global__ void __launch_bounds__(128) ln_bwd_kernel(
-    const float* __restrict__ dy, const float* __restrict__ x, const float* __restrict__ mean_in,
+    const void* __restrict__ dy, const float* __restrict__ x, const float* __restrict__ mean_in,
     const float* __restrict__ rstd_in, const float* __restrict__ gain, const float* __restrict__ resid, int rows,
     float* __restrict__ dx32, __nv_bfloat16* __restrict__ dx16, float* __restrict__ partial, int nst,
     float* __restrict__ cpartial) {
@@ -182,16 +208,18 @@ __global__ void __launch_bounds__(128) ln_bwd_kernel(
   const int ntens = resid ? 3 : 2;
   float* sg = reinterpret_cast<float*>(ln_smem);
   for (int i = threadIdx.x; i < D; i += blockDim.x) sg[i] = gain[i];
-  const uint32_t slot = ntens * D * 4;  // one row of each tensor
+  constexpr uint32_t kDyBytes = D * (DY16 ? 2 : 4);
+  const uint32_t slot = kDyBytes + (ntens - 1) * D * 4;  // one row of each tensor
   const uint32_t ring = smem_u32(ln_smem) + D * 4 + warp * nst * slot;
   uint64_t* bar = bars[warp];
   const int W = gridDim.x * nw, gw = blockIdx.x * nw + warp;
   const int nrows = gw < rows ? (rows - gw + W - 1) / W : 0;
-  const float* src[3] = {dy, x, resid};
+  const void* src[3] = {dy, x, resid};
   if (lane == 0) {
     for (int i = 0; i < nst; ++i) mbar_init(bar + i, 1);
     fence_barrier_init();
-    for (int k = 0; k < nst && k < nrows; ++k) ln_row_issue(bar + k, ring + k * slot, src, ntens, gw + k * W, D);
+    for (int k = 0; k < nst && k < nrows; ++k)
+      ln_row_issue_b(bar + k, ring + k * slot, src, ntens, gw + k * W, D, kDyBytes);
   }
   __syncthreads();
   const float inv_d = 1.0f / static_cast<float>(D);
@@ -213,12 +241,13 @@ __global__ void __launch_bounds__(128) ln_bwd_kernel(
       inv_n = rstd_in[r + W];
     }
     mbar_wait(bar + st, (k / nst) & 1);
-    const uint32_t sd = ring + st * slot, sx = sd + D * 4, sr = sd + 2 * D * 4;
+    const uint32_t sd = ring + st * slot, sx = sd + kDyBytes, sr = sx + D * 4;
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       const uint32_t o = (lane + 32 * i) * 16;
-      const float4 d = lds128f(sd + o), xv = lds128f(sx + o), g = reinterpret_cast<const float4*>(sg)[lane + 32 * i];
+      const float4 d = ln_lds_dy<DY16>(sd, lane + 32 * i), xv = lds128f(sx + o),
+                   g = reinterpret_cast<const float4*>(sg)[lane + 32 * i];
       const float4 h = make_float4((xv.x - mu) * inv, (xv.y - mu) * inv, (xv.z - mu) * inv, (xv.w - mu) * inv);
       const float4 gy = make_float4(d.x * g.x, d.y * g.y, d.z * g.z, d.w * g.w);
       s1 += (gy.x + gy.y) + (gy.z + gy.w);
@@ -239,7 +268,7 @@ __global__ void __launch_bounds__(128) ln_bwd_kernel(
     for (int i = 0; i < NV; ++i) {
       const int c4 = lane + 32 * i;
       const uint32_t o = c4 * 16;
-      const float4 d = lds128f(sd + o), xv = lds128f(sx + o), g = reinterpret_cast<const float4*>(sg)[c4];
+      const float4 d = ln_lds_dy<DY16>(sd, c4), xv = lds128f(sx + o), g = reinterpret_cast<const float4*>(sg)[c4];
       const float4 rr = resid ? lds128f(sr + o) : make_float4(0.f, 0.f, 0.f, 0.f);
       const float4 h = make_float4((xv.x - mu) * inv, (xv.y - mu) * inv, (xv.z - mu) * inv, (xv.w - mu) * inv);
       float4 out;
@@ -258,7 +287,7 @@ __global__ void __launch_bounds__(128) ln_bwd_kernel(
       }
     }
     __syncwarp();  // every lane's reads of this slot are done before it is refilled
-    if (lane == 0 && k + nst < nrows) ln_row_issue(bar + st, ring + st * slot, src, ntens, r + nst * W, D);
+    if (lane == 0 && k + nst < nrows) ln_row_issue_b(bar + st, ring + st * slot, src, ntens, r + nst * W, D, kDyBytes);
   }
   // combine the warps' column partials in warp order (the ring is drained)
   __syncthreads();
@@ -479,15 +508,16 @@ int ln_env(const char* name, int dflt) {
   const char* e = std::getenv(name);
   return e != nullptr && e[0] != 0 ? std::atoi(e) : dflt;
 }
-LnLaunch ln_bwd_launch(int rows, int d, int ntens) {
+// row_floats: ring bytes per row / 4 (dy + x [+ resid]; a bf16 dy counts d/2)
+LnLaunch ln_bwd_launch(int rows, int d, int row_floats) {
   // tuning knobs (measurement only): rows in flight per warp, warps per block, smem cap, blocks per SM
   static const int k_nst = ln_env("P2R_LN_BWD_NST", 2), k_warps = ln_env("P2R_LN_BWD_WARPS", kLnBwdWarps),
                    k_cap = ln_env("P2R_LN_BWD_SMEM_KB", 110), k_persm = ln_env("P2R_LN_BWD_PERSM", 2);
   LnLaunch l{};
   l.warps = k_warps < 1 ? 1 : (k_warps > 4 ? 4 : k_warps);
   l.nst = k_nst < 1 ? 1 : (k_nst > kLnMaxStages ? kLnMaxStages : k_nst);
-  while (l.nst > 1 && d * 4 + l.warps * l.nst * ntens * d * 4 > k_cap * 1024) --l.nst;
-  const int ring = l.warps * l.nst * ntens * d * 4, red = l.warps * 3 * d * 4;
+  while (l.nst > 1 && d * 4 + l.warps * l.nst * row_floats * 4 > k_cap * 1024) --l.nst;
+  const int ring = l.warps * l.nst * row_floats * 4, red = l.warps * 3 * d * 4;
   l.smem = d * 4 + (ring > red ? ring : red);
   int per_sm = kSmemPerSM / (l.smem + 1024);
   per_sm = per_sm < 1 ? 1 : (per_sm > k_persm ? k_persm : per_sm);
@@ -552,45 +582,40 @@ extern "C" p2r_status p2r_layernorm_fwd(const float* x, const float* gain, const
   return P2R_OK;
 }
 
-// partial_ws: >= blocks * 2 * d floats (bwd launch configuration, with residual)
-extern "C" size_t p2r_layernorm_bwd_workspace(int rows, int d) {
-  if (rows <= 0 || !ln_dim_ok(d)) return 0;
-  const int b2 = ln_bwd_launch(rows, d, 2).blocks, b3 = ln_bwd_launch(rows, d, 3).blocks;
-  return static_cast<size_t>(b2 > b3 ? b2 : b3) * 2 * d * sizeof(float);
-}
+namespace {
+// ring floats per row for a launch: dy (fp32, or bf16 = half) + x (+ resid)
+int ln_bwd_row_floats(int d, bool resid, bool dy16) { return (dy16 ? d / 2 : d) + d + (resid ? d : 0); }
 
-extern "C" int p2r_layernorm_bwd_blocks(int rows, int d, int has_resid) {
-  if (rows <= 0 || !ln_dim_ok(d)) return 0;
-  return ln_bwd_launch(rows, d, has_resid ? 3 : 2).blocks;
-}
-
-extern "C" p2r_status p2r_layernorm_bwd_fused(const float* dy, const float* x, const float* mean,
-                                              const float* rstd, const float* gain, const float* resid,
-                                              int rows, int d, float* dx, void* dx_bf16, float* ggain,
-                                              float* gbias, float* partial_ws, float* dx_colsum_ws,
-                                              const float* colsum_in, int colsum_blocks, float* colsum_dst,
-                                              void* stream) {
+p2r_status ln_bwd_fused(const void* dy, bool dy16, const float* x, const float* mean, const float* rstd,
+                        const float* gain, const float* resid, int rows, int d, float* dx, void* dx_bf16,
+                        float* ggain, float* gbias, float* partial_ws, float* dx_colsum_ws, const float* colsum_in,
+                        int colsum_blocks, float* colsum_dst, void* stream) {
   if (rows <= 0) return P2R_OK;
   if (!ln_dim_ok(d)) return set_error(P2R_EINVAL, "layernorm: d_model must be a multiple of 128 in [128, 2048]");
   if ((colsum_in == nullptr) != (colsum_dst == nullptr) || (colsum_in && colsum_blocks <= 0))
     return set_error(P2R_EINVAL, "layernorm bwd: colsum_in, colsum_blocks and colsum_dst go together");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const LnLaunch l = ln_bwd_launch(rows, d, resid ? 3 : 2);
+  const LnLaunch l = ln_bwd_launch(rows, d, ln_bwd_row_floats(d, resid != nullptr, dy16));
   auto* d16 = static_cast<__nv_bfloat16*>(dx_bf16);
   switch (d / 128) {
-#define P2R_LN_BWD_ONE(NV, CS)                                                                                \
+#define P2R_LN_BWD_ONE(NV, CS, DY)                                                                            \
   {                                                                                                        \
-    static cudaError_t a = cudaFuncSetAttribute(ln_bwd_kernel<NV, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                                kLnSmemAttr);                                                \
+    static cudaError_t a = cudaFuncSetAttribute(ln_bwd_kernel<NV, CS, DY>,                                  \
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize, kLnSmemAttr);  \
     if (a != cudaSuccess) return set_cuda_error(a, "layernorm bwd attr");                                  \
-    const cudaError_t le = launch_k(ln_bwd_kernel<NV, CS>, dim3(l.blocks), dim3(32 * l.warps), l.smem, s, 1, dy, x, mean, \
-                 rstd, gain, resid, rows, dx, d16, partial_ws, l.nst, dx_colsum_ws);                         \
+    const cudaError_t le = launch_k(ln_bwd_kernel<NV, CS, DY>, dim3(l.blocks), dim3(32 * l.warps), l.smem, s, 1, dy, \
+                                    x, mean, rstd, gain, resid, rows, dx, d16, partial_ws, l.nst, dx_colsum_ws); \
     if (le != cudaSuccess) return set_cuda_error(le, "layernorm bwd");                                       \
   }
-#define P2R_LN_BWD(NV)                          \
-  case NV:                                      \
-    if (dx_colsum_ws) P2R_LN_BWD_ONE(NV, true)  \
-    else P2R_LN_BWD_ONE(NV, false)              \
+#define P2R_LN_BWD(NV)                                  \
+  case NV:                                              \
+    if (dy16) {                                         \
+      if (dx_colsum_ws) P2R_LN_BWD_ONE(NV, true, true)  \
+      else P2R_LN_BWD_ONE(NV, false, true)              \
+    } else {                                            \
+      if (dx_colsum_ws) P2R_LN_BWD_ONE(NV, true, false) \
+      else P2R_LN_BWD_ONE(NV, false, false)             \
+    }                                                   \
     break;
     P2R_LN_NV_CASES(P2R_LN_BWD)
 #undef P2R_LN_BWD
@@ -605,6 +630,43 @@ extern "C" p2r_status p2r_layernorm_bwd_fused(const float* dy, const float* x, c
                  colsum_dst);
   }
   return P2R_OK;
+}
+}  // namespace
+
+// partial_ws: >= blocks * 2 * d floats for every launch variant (residual or not, fp32 or bf16 dy)
+extern "C" size_t p2r_layernorm_bwd_workspace(int rows, int d) {
+  if (rows <= 0 || !ln_dim_ok(d)) return 0;
+  int b = 0;
+  for (int v = 0; v < 4; ++v) {
+    const int bv = ln_bwd_launch(rows, d, ln_bwd_row_floats(d, v & 1, v & 2)).blocks;
+    b = bv > b ? bv : b;
+  }
+  return static_cast<size_t>(b) * 2 * d * sizeof(float);
+}
+
+extern "C" int p2r_layernorm_bwd_blocks(int rows, int d, int flags) {
+  if (rows <= 0 || !ln_dim_ok(d)) return 0;
+  return ln_bwd_launch(rows, d, ln_bwd_row_floats(d, flags & P2R_LN_RESID, flags & P2R_LN_DY_BF16)).blocks;
+}
+
+extern "C" p2r_status p2r_layernorm_bwd_fused(const float* dy, const float* x, const float* mean,
+                                              const float* rstd, const float* gain, const float* resid,
+                                              int rows, int d, float* dx, void* dx_bf16, float* ggain,
+                                              float* gbias, float* partial_ws, float* dx_colsum_ws,
+                                              const float* colsum_in, int colsum_blocks, float* colsum_dst,
+                                              void* stream) {
+  return ln_bwd_fused(dy, false, x, mean, rstd, gain, resid, rows, d, dx, dx_bf16, ggain, gbias, partial_ws,
+                      dx_colsum_ws, colsum_in, colsum_blocks, colsum_dst, stream);
+}
+
+extern "C" p2r_status p2r_layernorm_bwd_fused_bf16(const void* dy_bf16, const float* x, const float* mean,
+                                                   const float* rstd, const float* gain, const float* resid,
+                                                   int rows, int d, float* dx, void* dx_bf16, float* ggain,
+                                                   float* gbias, float* partial_ws, float* dx_colsum_ws,
+                                                   const float* colsum_in, int colsum_blocks, float* colsum_dst,
+                                                   void* stream) {
+  return ln_bwd_fused(dy_bf16, true, x, mean, rstd, gain, resid, rows, d, dx, dx_bf16, ggain, gbias, partial_ws,
+                      dx_colsum_ws, colsum_in, colsum_blocks, colsum_dst, stream);
 }
 
 extern "C" p2r_status p2r_layernorm_bwd(const float* dy, const float* x, const float* mean,

@@ -94,6 +94,47 @@ def test_layernorm_bwd_fused_colsum(cuda, rows, d, resid):
         call("layernorm_bwd_fused", GY, X, mean, rstd, G, None, rows, d, dx, None, None, None, ws, None, stage, 0, db2)
 
 
+@pytest.mark.parametrize("rows,d,resid", [(8192, 1024, True), (8192, 1024, False), (301, 384, True), (5, 2048, True)])
+def test_layernorm_bwd_bf16_dy(cuda, rows, d, resid):
+    """p2r_layernorm_bwd_fused_bf16 (the dense block's dX GEMMs emit bf16): on a dy
+    that is bf16-representable, dx / dx16 equal the fp32-dy kernel bit for bit, the
+    LN grads and the staged column sums agree to fp32 summation order (the grid can
+    differ: the bf16 ring is smaller), and the staged partials finish into db2."""
+    import torch
+    from paper_2110_03888_b200 import _lib
+    L = _lib.lib()
+    rng = np.random.default_rng(2)
+    x = (rng.standard_normal((rows, d)) * 2).astype(np.float32)
+    X, G = dev(x), dev(rng.standard_normal(d).astype(np.float32))
+    gy16 = torch.from_numpy(rng.standard_normal((rows, d)).astype(np.float32)).to(cuda).bfloat16()
+    GY = gy16.float().contiguous()
+    R = dev(rng.standard_normal((rows, d)).astype(np.float32)) if resid else None
+    mean = torch.empty(rows, device=cuda)
+    rstd = torch.empty(rows, device=cuda)
+    call("layernorm_fwd", X, G, G, rows, d, 1e-5, None, torch.empty(rows, d, device=cuda), mean, rstd)
+    ws = torch.empty(L.p2r_layernorm_bwd_workspace(rows, d) // 4, device=cuda)
+    outs = []
+    for b16 in (False, True):
+        dx = torch.empty(rows, d, device=cuda)
+        dx16 = torch.empty(rows, d, dtype=torch.bfloat16, device=cuda)
+        gg, gb = torch.zeros(d, device=cuda), torch.zeros(d, device=cuda)
+        flags = (1 if resid else 0) | (2 if b16 else 0)
+        nblk = L.p2r_layernorm_bwd_blocks(rows, d, flags)
+        stage = torch.full((nblk, d), float("nan"), device=cuda)
+        call("layernorm_bwd_fused_bf16" if b16 else "layernorm_bwd_fused", gy16 if b16 else GY, X, mean, rstd, G, R,
+             rows, d, dx, dx16, gg, gb, ws, stage, None, 0, None)
+        db2 = torch.zeros(d, device=cuda)
+        call("layernorm_bwd_fused", GY, X, mean, rstd, G, None, rows, d, torch.empty(rows, d, device=cuda), None, None,
+             None, ws, None, stage, nblk, db2)
+        outs.append((dx, dx16, gg, gb, db2))
+    (a_dx, a_16, a_gg, a_gb, a_db2), (b_dx, b_16, b_gg, b_gb, b_db2) = outs
+    assert torch.equal(a_dx, b_dx) and torch.equal(a_16, b_16)
+    for a, b in ((a_gg, b_gg), (a_gb, b_gb), (a_db2, b_db2)):
+        assert float((a.double() - b.double()).norm() / a.double().norm()) < 1e-6
+    ref = a_dx.double().sum(0)
+    assert float((b_db2.double() - ref).norm() / ref.norm()) < 1e-6
+
+
 def test_layernorm_golden(cuda):
     """Reference-generated LN golden (d=40 is not a supported width): pad-free
     check on the KAT instead: constant row -> 0."""

@@ -88,20 +88,35 @@ def test_c3_width_real_moe_parity(cuda):
     assert abs(lg - lr_) <= 1e-3 * abs(lr_)
     free = O.Model(O.Config(**C3W), p0)
     free.forward(tok, B, keep=True)
-    forced, flips = {}, 0
+    forced, cascaded = {}, 0
     for g in range(C3W["n_layers_graph"]):
         sel, sur, raw, cap, drop = m.layer_routing(g, T)
         forced[g] = sel
         osel = free._cache[2][g][12][2].selected
         ol = free._cache[2][g][12][1]
         for t in np.nonzero(sel != osel)[0]:
-            flips += 1
-            print(f"flip layer {g} token {t}: gpu {sel[t]} oracle {osel[t]} fp32 gap {ol[t, osel[t]] - ol[t, sel[t]]:.3e}")
+            cascaded += 1
+            print(f"free-run flip layer {g} token {t}: gpu {sel[t]} oracle {osel[t]} fp32 gap "
+                  f"{ol[t, osel[t]] - ol[t, sel[t]]:.3e}")
     om = O.Model(O.Config(**C3W), p0)
     om.forced_selected = forced
     lo, go = om.loss_and_grads(tok, tgt, mask, B, denom)
     assert abs(lg - lo) <= 1e-3 * abs(lo)
+    # routing parity proper: layer g's choice against the oracle's own choice on the
+    # same earlier-layer routing (a free-running oracle also counts cascades: one early
+    # flip changes every later token's attention input). Each flip is a near-tie.
+    flips, worst = 0, 0.0
+    for g in range(C3W["n_layers_graph"]):
+        ol = om._cache[2][g][12][1]
+        own = O.moe_dispatch_vectorized(ol, C3W["n_experts"], C3W["n_prototypes"], 1.25).selected
+        for t in np.nonzero(forced[g] != own)[0]:
+            flips += 1
+            gap = float(ol[t, own[t]] - ol[t, forced[g][t]])
+            worst = max(worst, gap / float(ol.std()))
+            print(f"flip layer {g} token {t}: gpu {forced[g][t]} oracle {own[t]} fp32 gap {gap:.3e}")
+    print(f"C3-width flips {flips} (free-run incl. cascades {cascaded}), worst gap / logit std {worst:.2e}")
     assert flips <= 0.005 * T * C3W["n_layers_graph"], flips
+    assert worst <= 0.02, worst
     ge = design_floor(C3W, p0, tok, tgt, mask, B, denom, forced)
     check_grads(m.grads(), go, ge, r.names, "C3W")
 

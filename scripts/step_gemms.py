@@ -24,6 +24,7 @@ def bf(*s):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=30)
+    ap.add_argument("--only", default=None, help="run just the GEMM of this name (profiling)")
     a = ap.parse_args()
     L = _lib.lib()
     x32 = torch.randn(T, d, device="cuda")
@@ -70,6 +71,8 @@ def main():
     tot_us = tot_cb = tot_f = 0.0
     print(f"{'gemm':20s} {'m':>6s} {'n':>5s} {'k':>5s}   p2r us  TFLOP/s | cuBLAS us TFLOP/s")
     for (name, m, n, k, A, lda, amn, B, ldb, bmn, epi, c, ldc, c2, ldc2, bias, aux, ldaux, split, bgrad, cb) in cases:
+        if a.only is not None and name != a.only:
+            continue
         args = _lib.GemmArgs(m=m, n=n, k=k, a=A.data_ptr(), lda=lda, a_mn_major=amn, b=B.data_ptr(), ldb=ldb,
                              b_mn_major=bmn, epi=epi, c=c.data_ptr(), ldc=ldc,
                              c2=c2.data_ptr() if c2 is not None else None, ldc2=ldc2,

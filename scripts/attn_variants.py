@@ -5,6 +5,7 @@ into build/exp/libp2r_<variant>.so, so scripts/attn_bench.py can time them via
 P2R_LIB=<path>:
   nomma  - no tcgen05.mma issued (commits still flow): softmax/TMA-bound time
   nosm   - softmax warps skip TMEM loads and math (stores/barriers kept)
+  nodq / nokv - launch only the dK/dV (resp. dQ) kernel (compose: nodq+nomma, ...)
   trace  - P2R_ATTN_TRACE: clock64 timeline of one dQ CTA (scripts/attn_trace.py)
 """
 import glob
@@ -25,10 +26,16 @@ def variant(name, text):
             text = variant(part, text)
         return text
     if name == "nomma":
-        text = text.replace("umma_bf16(", "if (false) umma_bf16(")
+        text = text.replace("umma_bf16(", "if (false) umma_bf16(").replace("umma_bf16_warp(", "if (false) umma_bf16_warp(")
     elif name == "nosm":
         text = re.sub(r"ld32x2\((tmem|tS)[^;]*\);", r"{ for (int z_ = 0; z_ < 32; ++z_) { s[z_] = 0.f; dp[z_] = 0.f; } }", text)
         text = re.sub(r"\? ex2_approx\(", "? (", text)
+    elif name == "nodq":  # time the dK/dV kernel alone (dsum left from an earlier full run)
+        text = text.replace('P2R_LAUNCH_K("attention bwd dq (tcgen05, 2 tiles, persistent)"',
+                            'if (false) P2R_LAUNCH_K("attention bwd dq (tcgen05, 2 tiles, persistent)"')
+    elif name == "nokv":  # time the dQ kernel alone
+        text = text.replace('P2R_LAUNCH_K("attention bwd dkdv (tcgen05, 2 tiles, persistent)"',
+                            'if (false) P2R_LAUNCH_K("attention bwd dkdv (tcgen05, 2 tiles, persistent)"')
     elif name.startswith("fma"):  # fwd: fmaN = N of 8 chunks' exponentials on the FMA pipe
         text = "#define P2R_ATTN_FMA_CHUNKS " + name[3:] + "\n" + text
     elif name == "trace":

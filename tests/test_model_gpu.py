@@ -92,6 +92,44 @@ def test_step_parity_dense(cuda, cfgd, B):
     check_grads(m.grads(), r.grads(), design_floor(cfgd, p0, tok, tgt, mask, B, denom), r.names, "dense")
 
 
+RAGGED_DENSE = dict(d_model=384, d_ff=1536, n_layers_graph=3, n_layers_params=1, n_heads=6, vocab_size=260,
+                    seq_len=200)
+RAGGED_MOE = dict(d_model=256, d_ff=512, n_layers_graph=2, n_layers_params=2, n_heads=4, vocab_size=260,
+                  seq_len=200, n_experts=8, n_prototypes=2, capacity_factor=1.0)
+
+
+@need_ref
+@pytest.mark.parametrize("cfgd", [RAGGED_DENSE, RAGGED_MOE], ids=["dense_d384", "real_moe_k2"])
+def test_step_parity_ragged(cuda, cfgd):
+    """Ragged shapes: S = 200 (not a multiple of the 64 / 128 attention blocks), T = 600
+    tokens (partial GEMM / LayerNorm / routing tiles), d = 384 / 6 heads, and a mask with
+    holes (the CE denominator counts only unmasked targets, tensor.cpp:670-723); the MoE
+    case also drops tokens at capacity factor 1.0. Loss vs the compiled reference,
+    gradients vs the reference (dense) or the oracle under the GPU's routing (MoE)."""
+    m, r = make_pair(cfgd)
+    B, S = 3, cfgd["seq_len"]
+    T = B * S
+    tok, tgt, mask = lm_batch(B, S, seed=21)
+    rng = np.random.default_rng(5)
+    mask[rng.random(T) < 0.15] = 0
+    denom = float(mask.sum())
+    p0 = r.params()
+    lg = m.train_step(tok, tgt, mask, B, denom)
+    lr_ = r.train_step(tok, tgt, mask, B, denom)
+    assert abs(lg - lr_) <= 1e-3 * abs(lr_), (lg, lr_)
+    if "n_experts" not in cfgd:
+        check_grads(m.grads(), r.grads(), design_floor(cfgd, p0, tok, tgt, mask, B, denom), r.names, "ragged")
+        return
+    om = O.Model(O.Config(**cfgd), p0)
+    om.forced_selected = {g: m.layer_routing(g, T)[0] for g in range(cfgd["n_layers_graph"])}
+    dropped = sum(int(m.layer_routing(g, T)[4]) for g in range(cfgd["n_layers_graph"]))
+    assert dropped > 0  # capacity 1.0 with top-2 over 8 experts drops tokens
+    lo, go = om.loss_and_grads(tok, tgt, mask, B, denom)
+    assert abs(lg - lo) <= 1e-3 * abs(lo)
+    ge = design_floor(cfgd, p0, tok, tgt, mask, B, denom, om.forced_selected)
+    check_grads(m.grads(), go, ge, r.names, "ragged_moe")
+
+
 @need_ref
 # per-tensor gradient bound (tests/_parity.py): 1e-2, or 1.25x the bf16-in design's floor
 # on the same inputs where that floor is itself ~1e-2 (at d = 2048 (C4S) single expert

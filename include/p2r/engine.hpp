@@ -241,6 +241,14 @@ class Engine {
                          float* loss_dev);
   float train_step_host(const int* tokens, const int* targets, const std::uint8_t* mask,
                         int batch, int seq, double denom, AttentionMode mode, bool zero);
+  // pipelined host step: the inputs are staged in one of two pinned slots, the step and
+  // the loss read-back are enqueued, and a ticket is returned at once (the next step,
+  // the optimizer, ... can be enqueued before the loss is read). loss_wait(ticket)
+  // returns that step's loss; a slot is reused two steps later, so only the last two
+  // tickets can be waited on (older ones throw std::logic_error).
+  std::uint64_t train_step_host_async(const int* tokens, const int* targets, const std::uint8_t* mask,
+                                      int batch, int seq, double denom, AttentionMode mode, bool zero);
+  float loss_wait(std::uint64_t ticket);
   void forward_host(const int* tokens, int batch, int seq, AttentionMode mode, float* logits_out);
 
   void zero_grads();
@@ -401,8 +409,12 @@ class Engine {
   std::unique_ptr<Acts> acts_;
   DevBuf splitk_ws_;
   DevBuf dev_in_;   // tokens / targets / mask staging
-  void* pinned_ = nullptr;
+  void* pinned_ = nullptr;      // two staging slots of pin_slot_ bytes (inputs + loss word)
   std::size_t pinned_bytes_ = 0;
+  std::size_t pin_slot_ = 0;
+  cudaEvent_t pin_ev_[2] = {nullptr, nullptr};  // the slot's step + loss read-back completed
+  std::uint64_t pin_ticket_[2] = {0, 0};        // ticket whose loss the slot holds
+  std::uint64_t async_seq_ = 0;
   Profiler prof_;
   // offload: res_idx_[owned] = resident slot in lay_* or -1 (SLOW)
   std::vector<int> res_idx_;

@@ -57,6 +57,16 @@ p2r_status p2r_model_forward(p2r_model* m, const int* tokens, int batch, int seq
 p2r_status p2r_model_train_step(p2r_model* m, const int* tokens, const int* targets,
                                 const uint8_t* mask, int batch, int seq, double denom, int causal,
                                 int zero, float* loss_out);
+/* Pipelined form of p2r_model_train_step (a host training loop that enqueues the next
+ * step / the optimizer before reading this step's loss): the inputs are staged in one
+ * of two pinned slots, the step and the loss read-back are enqueued, and *ticket
+ * identifies the step. p2r_model_loss_wait(ticket) waits for that step and returns
+ * its loss; only the last two tickets can be waited on (older: P2R_ELOGIC). The
+ * same validation and errors as p2r_model_train_step, raised before anything is enqueued. */
+p2r_status p2r_model_train_step_async(p2r_model* m, const int* tokens, const int* targets,
+                                      const uint8_t* mask, int batch, int seq, double denom, int causal,
+                                      int zero, uint64_t* ticket);
+p2r_status p2r_model_loss_wait(p2r_model* m, uint64_t ticket, float* loss_out);
 /* Same, inputs already resident on the device; the loss stays on the device
  * (loss_dev, may be NULL) so steps can be enqueued / graph-captured. */
 p2r_status p2r_model_train_step_device(p2r_model* m, const int* d_tokens, const int* d_targets,

@@ -7,11 +7,11 @@ a thin ctypes mirror of that API (see model.py); it never computes on the CPU.
 """
 from ._lib import (P2RError, P2RInvalidArgument, P2RLogicError, P2ROutOfRange, launch_count,
                    lib)
-from .model import (Config, LoopbackGroup, Model, Routing, comm_unique_id, count_params, delink_checkpoint, load_checkpoint,
-                    lr_at, moe_dispatch, plan_offload, plan_offload_overlap, predict_step_time,
+from .model import (Config, LoopbackGroup, Model, PendingLoss, Routing, comm_unique_id, count_params,
+                    delink_checkpoint, load_checkpoint, lr_at, moe_dispatch, plan_offload, plan_offload_overlap, predict_step_time,
                     predict_step_time_overlap, redistribute_checkpoints)
 
-__all__ = ["Config", "LoopbackGroup", "Model", "Routing", "count_params", "lr_at", "moe_dispatch", "plan_offload",
+__all__ = ["Config", "LoopbackGroup", "Model", "PendingLoss", "Routing", "count_params", "lr_at", "moe_dispatch", "plan_offload",
            "predict_step_time", "load_checkpoint", "delink_checkpoint", "redistribute_checkpoints", "plan_offload_overlap",
            "predict_step_time_overlap", "lib",
            "launch_count", "P2RError", "P2RInvalidArgument", "P2ROutOfRange", "P2RLogicError"]

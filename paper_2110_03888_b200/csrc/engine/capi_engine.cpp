@@ -120,6 +120,22 @@ p2r_status p2r_model_train_step(p2r_model* m, const int* tokens, const int* targ
   });
 }
 
+p2r_status p2r_model_train_step_async(p2r_model* m, const int* tokens, const int* targets, const uint8_t* mask,
+                                      int batch, int seq, double denom, int causal, int zero, uint64_t* ticket) {
+  return guard([&] {
+    const std::uint64_t t =
+        m->m->train_step_host_async(tokens, targets, mask, batch, seq, denom, mode_of(causal), zero != 0);
+    if (ticket) *ticket = t;
+  });
+}
+
+p2r_status p2r_model_loss_wait(p2r_model* m, uint64_t ticket, float* loss_out) {
+  return guard([&] {
+    const float l = m->m->loss_wait(ticket);
+    if (loss_out) *loss_out = l;
+  });
+}
+
 p2r_status p2r_model_train_step_device(p2r_model* m, const int* d_tokens, const int* d_targets,
                                        const uint8_t* d_mask, int batch, int seq, double denom, int causal,
                                        int zero, float* loss_dev) {

@@ -303,6 +303,8 @@ Engine::~Engine() {
   comm_destroy();
   off_.reset();
   if (pinned_) cudaFreeHost(pinned_);
+  for (cudaEvent_t e : pin_ev_)
+    if (e) cudaEventDestroy(e);
   if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -685,11 +687,14 @@ void Engine::ensure_acts(int B, int S) {
   }
   acts_ = std::move(A);
   ++acts_gen_;
-  const std::size_t pin = static_cast<std::size_t>(T) * 9 + 64;
-  if (pinned_bytes_ < pin) {
+  const std::size_t slot = (static_cast<std::size_t>(T) * 9 + 63) / 64 * 64 + 64;  // inputs | loss word
+  if (pin_slot_ < slot) {
+    cuda_check(cudaStreamSynchronize(stream_), "pinned staging");  // no step reads the old slots
     if (pinned_) cudaFreeHost(pinned_);
-    cuda_check(cudaMallocHost(&pinned_, pin), "pinned staging");
-    pinned_bytes_ = pin;
+    cuda_check(cudaMallocHost(&pinned_, 2 * slot), "pinned staging");
+    pinned_bytes_ = 2 * slot;
+    pin_slot_ = slot;
+    pin_ticket_[0] = pin_ticket_[1] = 0;
   }
 }
 
@@ -1198,6 +1203,11 @@ void validate_ids(const int* ids, std::size_t n, int V, const char* msg) {
 
 float Engine::train_step_host(const int* tokens, const int* targets, const std::uint8_t* mask, int batch, int seq,
                              double denom, AttentionMode mode, bool zero) {
+  return loss_wait(train_step_host_async(tokens, targets, mask, batch, seq, denom, mode, zero));
+}
+
+std::uint64_t Engine::train_step_host_async(const int* tokens, const int* targets, const std::uint8_t* mask,
+                                            int batch, int seq, double denom, AttentionMode mode, bool zero) {
   if (batch <= 0 || seq <= 0) throw std::invalid_argument("forward: token count must be a multiple of batch");
   if (seq > cfg_.seq_len) throw std::invalid_argument("forward: sequence longer than configured seq_len");
   if (denom <= 0.0) throw std::invalid_argument("softmax_cross_entropy: denominator must be > 0");
@@ -1208,7 +1218,10 @@ float Engine::train_step_host(const int* tokens, const int* targets, const std::
       throw std::out_of_range("softmax_cross_entropy: target out of range");
   ensure_acts(batch, seq);
   Acts& A = *acts_;
-  char* pin = static_cast<char*>(pinned_);
+  const int sl = static_cast<int>(async_seq_ & 1);
+  if (!pin_ev_[sl]) cuda_check(cudaEventCreateWithFlags(&pin_ev_[sl], cudaEventDisableTiming), "staging event");
+  if (pin_ticket_[sl] != 0) cuda_check(cudaEventSynchronize(pin_ev_[sl]), "staging slot");  // step - 2 is done
+  char* pin = static_cast<char*>(pinned_) + sl * pin_slot_;
   std::memcpy(pin, tokens, T * 4);
   std::memcpy(pin + T * 4, targets, T * 4);
   if (mask) std::memcpy(pin + T * 8, mask, T);
@@ -1226,11 +1239,19 @@ float Engine::train_step_host(const int* tokens, const int* targets, const std::
   else
     train_step_device(A.tokens.as<int>(), A.targets.as<int>(), mask ? A.mask.as<std::uint8_t>() : nullptr, batch, seq,
                       denom, mode, zero, nullptr);
-  float* lh = reinterpret_cast<float*>(pin + T * 9 + (64 - (T * 9) % 64) % 64);
-  if (reinterpret_cast<char*>(lh) + 4 > pin + pinned_bytes_) lh = reinterpret_cast<float*>(pin);
+  float* lh = reinterpret_cast<float*>(pin + pin_slot_ - 64);
   cuda_check(cudaMemcpyAsync(lh, A.loss.p, 4, cudaMemcpyDeviceToHost, stream_), "d2h loss");
-  cuda_check(cudaStreamSynchronize(stream_), "step sync");
-  return *lh;
+  cuda_check(cudaEventRecord(pin_ev_[sl], stream_), "staging event");
+  pin_ticket_[sl] = ++async_seq_;
+  return pin_ticket_[sl];
+}
+
+float Engine::loss_wait(std::uint64_t ticket) {
+  const int sl = static_cast<int>((ticket - 1) & 1);
+  if (ticket == 0 || pin_ticket_[sl] != ticket)
+    throw std::logic_error("loss_wait: ticket is not one of the last two host steps");
+  cuda_check(cudaEventSynchronize(pin_ev_[sl]), "step sync");
+  return *reinterpret_cast<const float*>(static_cast<const char*>(pinned_) + sl * pin_slot_ + pin_slot_ - 64);
 }
 
 void Engine::forward_host(const int* tokens, int batch, int seq, AttentionMode mode, float* logits_out) {

@@ -137,14 +137,21 @@ P2R_DEVICE Tile get_tile(const GemmParams& p, int t, int BN, int CG = 1, int ran
   return T;
 }
 
+#ifndef P2R_GEMM_EPI_WARPS
+#define P2R_GEMM_EPI_WARPS 8
+#endif
+constexpr int kEpiWarps = P2R_GEMM_EPI_WARPS;       // kEpiWarps / 4 per TMEM lane quadrant
+constexpr int kGemmThreads = 128 + 32 * kEpiWarps;  // 4 control warps + epilogue
+
 template <int BN, int CG = 1>
 struct GemmCfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = (BN / CG) * BK * 2;  // a pair splits B's rows between its CTAs
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (196608 / STAGE_BYTES) > 8 ? 8 : (196608 / STAGE_BYTES);
+  static constexpr int STAGES = ((229376 - kEpiWarps * 4096) / STAGE_BYTES) > 8 ? 8
+                                                                               : ((229376 - kEpiWarps * 4096) / STAGE_BYTES);
   static constexpr int TMEM_COLS = (2 * BN) < 32 ? 32 : (2 * BN);
-  static constexpr int STG_BYTES = 8 * 4096;  // per epilogue warp: transpose tile / two TMA-store slots
+  static constexpr int STG_BYTES = kEpiWarps * 4096;  // per epilogue warp: transpose tile / two TMA-store slots
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + STG_BYTES + 256 /*barriers*/;
 };
 
@@ -349,8 +356,6 @@ P2R_DEVICE float4 epi_store_fast(const GemmParams& p, float4 v, typename EpiOper
   return make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
-constexpr int kEpiWarps = 8;                       // 2 per TMEM lane quadrant
-constexpr int kGemmThreads = 128 + 32 * kEpiWarps;  // 4 control warps + epilogue
 
 // EPI_ = epilogue kind | kEpiColsum (GELU' + bias-grad column partials).
 constexpr int kEpiColsum = 0x100;
@@ -512,7 +517,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   } else if (warp >= 4) {
     // ---------------- epilogue ----------------
     const int ew = warp & 3;          // TMEM lanes [32*ew, 32*ew+32) (warp % 4 rule)
-    const int chalf = (warp - 4) >> 2;  // which half of the BN columns this warp drains
+    const int cpart = (warp - 4) >> 2;  // which part of the BN columns this warp drains
     // per-warp 32x32 fp32 transpose tile, XOR-swizzled: (r, c) at r*32 + (c ^ r)
     // (shared-space address: a generic pointer here compiles to LD/ST on the long scoreboard)
     const uint32_t stg = smem_u32(stg_all) + (warp - 4) * 4096;
@@ -543,7 +548,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
       // lane = (row group, 4-column group): a warp instruction covers 4 rows x 32 columns
       const int cg = lane & 7, rg = lane >> 3;
-      const int cb = chalf * (BN / 64), ce = cb + BN / 64;  // this warp's 32-column chunks
+      // this warp's 32-column chunks (of BN / 32, split over the kEpiWarps / 4 warps of its quadrant)
+      const int cb = cpart * (BN / 32) / (kEpiWarps / 4), ce = (cpart + 1) * (BN / 32) / (kEpiWarps / 4);
       auto is_fast = [&](int c) {
         const int c0 = T.n_blk * BN + c * 32;
         return p.vec4 && nrows == 32 && c0 + 32 <= p.n && row0 + 32 <= zero_from;

@@ -17,6 +17,21 @@ from ._lib import check, lib
 vp, ip, fp, i64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_float, ctypes.c_int64
 
 
+
+class PendingLoss:
+    """Loss of an enqueued host step (Model.train_step(wait=False)); value() waits for
+    that step. Only the two most recent host steps of a model can be waited on."""
+
+    def __init__(self, model, ticket: int):
+        self._m, self._t, self._v = model, ticket, None
+
+    def value(self) -> float:
+        if self._v is None:
+            loss = ctypes.c_float()
+            check(lib().p2r_model_loss_wait(self._m.h, ctypes.c_uint64(self._t), ctypes.byref(loss)))
+            self._v = float(loss.value)
+        return self._v
+
 class ModelConfigC(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int) for n in (
         "d_model", "d_ff", "n_layers_graph", "n_layers_params", "n_heads", "vocab_size",
@@ -45,6 +60,8 @@ _lib._EXTRA_SIGNATURES.update({
     "p2r_model_get_grad": [vp, ip, vp],
     "p2r_model_forward": [vp, vp, ip, ip, ip, vp],
     "p2r_model_train_step": [vp, vp, vp, vp, ip, ip, ctypes.c_double, ip, ip, vp],
+    "p2r_model_train_step_async": [vp, vp, vp, vp, ip, ip, ctypes.c_double, ip, ip, vp],
+    "p2r_model_loss_wait": [vp, ctypes.c_uint64, vp],
     "p2r_model_train_step_device": [vp, vp, vp, vp, ip, ip, ctypes.c_double, ip, ip, vp],
     "p2r_model_train_step_device_graph": [vp, vp, vp, vp, ip, ip, ctypes.c_double, ip, ip, vp],
     "p2r_model_adamw_attach": [vp, fp, fp, fp, fp],
@@ -309,11 +326,19 @@ class Model:
         return out
 
     def train_step(self, tokens, targets, mask, batch, denom, causal=True, zero=True,
-                   segmented=False) -> float:
+                   segmented=False, wait=True):
+        """One micro-step on host arrays; returns the loss. wait=False returns a
+        PendingLoss at once (the step and its loss read-back are enqueued), so a
+        training loop can enqueue the optimizer / next step before reading it."""
         del segmented  # one fused backward; equivalent to the reference's segmented variant
         tok = np.ascontiguousarray(tokens, np.int32)
         tgt = np.ascontiguousarray(targets, np.int32)
         msk = None if mask is None else np.ascontiguousarray(mask, np.uint8)
+        if not wait:
+            ticket = ctypes.c_uint64()
+            check(lib().p2r_model_train_step_async(self.h, _p(tok), _p(tgt), _p(msk), batch, tok.size // batch,
+                                                   float(denom), int(causal), int(zero), ctypes.byref(ticket)))
+            return PendingLoss(self, ticket.value)
         loss = ctypes.c_float()
         check(lib().p2r_model_train_step(self.h, _p(tok), _p(tgt), _p(msk), batch, tok.size // batch,
                                          float(denom), int(causal), int(zero), ctypes.byref(loss)))

@@ -305,6 +305,40 @@ def test_error_behaviour(cuda):
         p2r.Model(p2r.Config(d_model=250, n_heads=4), 1)
 
 
+def test_train_step_async_pipelined(cuda):
+    """Model.train_step(wait=False): a pipelined host loop (next step and AdamW enqueued
+    before the previous loss is read) gives bit-identical losses to the synchronous
+    loop; only the last two steps' losses can be waited on."""
+    import paper_2110_03888_b200 as p2r
+    B, S = 4, DENSE["seq_len"]
+    batches = [lm_batch(B, S, seed=40 + i) for i in range(5)]
+    a = p2r.Model(p2r.Config(**DENSE), 77)
+    b = p2r.Model(p2r.Config(**DENSE), 77)
+    a.attach_adamw()
+    b.attach_adamw()
+    sync = []
+    for tok, tgt, mask in batches:
+        sync.append(a.train_step(tok, tgt, mask, B, float(mask.sum())))
+        a.adamw_step(1e-3)
+    piped, prev = [], None
+    for tok, tgt, mask in batches:
+        cur = b.train_step(tok, tgt, mask, B, float(mask.sum()), wait=False)
+        b.adamw_step(1e-3)
+        if prev is not None:
+            piped.append(prev.value())
+        prev = cur
+    piped.append(prev.value())
+    assert piped == sync
+    tok, tgt, mask = batches[0]
+    p0 = b.train_step(tok, tgt, mask, B, float(mask.sum()), wait=False)
+    b.train_step(tok, tgt, mask, B, float(mask.sum()), wait=False)
+    b.train_step(tok, tgt, mask, B, float(mask.sum()), wait=False).value()
+    with pytest.raises(p2r.P2RLogicError, match="last two"):
+        p0.value()
+    with pytest.raises(p2r.P2ROutOfRange):  # validated before anything is enqueued
+        b.train_step(np.full_like(tok, 999), tgt, mask, B, float(mask.sum()), wait=False)
+
+
 def test_train_step_graph_replay_bit_identical(cuda):
     """train_step_device(graph=True): first call runs + captures, later calls replay one
     CUDA graph; losses, parameters and AdamW moments match the eager path bit-for-bit,

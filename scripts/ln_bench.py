@@ -58,6 +58,11 @@ def b2b(fn, it=20):
     return a.elapsed_time(e) / it * 1e3
 
 
+dy16 = dy.bfloat16()
+bwd16 = lambda: _lib.check(L.p2r_layernorm_bwd_fused_bf16(P(dy16), P(x), P(mean), P(rstd), P(g), P(res), T, d, P(dx),
+                                                         P(dx16), P(gg), P(gb), P(ws), None, None, 0, None, st))
+b16 = b2b(bwd16)
+print(f"T={T} d={d} back-to-back: ln bwd (bf16 dy, the step's form) {b16:6.1f} us ({(T*d*16)/b16/1e3:6.0f} GB/s)")
 f, bw = b2b(fwd), b2b(bwd)
 print(f"T={T} d={d} back-to-back: ln fwd {f:6.1f} us ({(T*d*6)/f/1e3:6.0f} GB/s)  ln bwd {bw:6.1f} us ({(T*d*18)/bw/1e3:6.0f} GB/s)")
 for cold in (True, False):

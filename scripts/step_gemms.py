@@ -25,6 +25,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=30)
     ap.add_argument("--only", default=None, help="run just the GEMM of this name (profiling)")
+    ap.add_argument("--variants", action="store_true", help="also time epilogue variants of the FFN1 shape")
     a = ap.parse_args()
     L = _lib.lib()
     x32 = torch.randn(T, d, device="cuda")
@@ -47,6 +48,10 @@ def main():
          lambda: o16 @ wo),
         ("FFN1 fwd (+b,gelu)", T, f, d, b16, d, 0, w1, f, 1, E.EPI_BIAS_GELU, out16, f, out16b, f, b1, None, 0, 1, None,
          lambda: b16 @ w1),
+        ("FFN1 shape, bf16", T, f, d, b16, d, 0, w1, f, 1, E.EPI_BF16, out16, f, None, 0, None, None, 0, 1, None,
+         lambda: b16 @ w1),
+        ("FFN1 shape, bf16+b", T, f, d, b16, d, 0, w1, f, 1, E.EPI_BF16, out16, f, None, 0, b1, None, 0, 1, None,
+         lambda: b16 @ w1),
         ("FFN2 fwd (+b,res)", T, d, f, g16, f, 0, w2, d, 1, E.EPI_F32, out32, d, None, 0, b2, x32, d, 1, None,
          lambda: g16 @ w2),
         ("dW2", f, d, T, g16, f, 1, dy16, d, 1, E.EPI_ACC_F32, gw, d, None, 0, None, None, 0, 0, None,
@@ -55,7 +60,7 @@ def main():
          lambda: dy16 @ w2.T),
         ("dW1", d, f, T, b16, d, 1, dh16, f, 1, E.EPI_ACC_F32, gw, f, None, 0, None, None, 0, 0, None,
          lambda: b16.T @ dh16),
-        ("dX1", T, d, f, dh16, f, 0, w1, f, 0, E.EPI_F32, out32, d, None, 0, None, None, 0, 1, None,
+        ("dX1", T, d, f, dh16, f, 0, w1, f, 0, E.EPI_BF16, out16, d, None, 0, None, None, 0, 1, None,
          lambda: dh16 @ w1.T),
         ("dWo", d, d, T, o16, d, 1, dx1_16, d, 1, E.EPI_ACC_F32, gw, d, None, 0, None, None, 0, 0, None,
          lambda: o16.T @ dx1_16),
@@ -63,7 +68,7 @@ def main():
          lambda: dx1_16 @ wo.T),
         ("dWqkv", d, 3 * d, T, a16, d, 1, dqkv16, 3 * d, 1, E.EPI_ACC_F32, gw, 3 * d, None, 0, None, None, 0, 0, None,
          lambda: a16.T @ dqkv16),
-        ("dXqkv", T, d, 3 * d, dqkv16, 3 * d, 0, wqkv, 3 * d, 0, E.EPI_F32, out32, d, None, 0, None, None, 0, 1, None,
+        ("dXqkv", T, d, 3 * d, dqkv16, 3 * d, 0, wqkv, 3 * d, 0, E.EPI_BF16, out16, d, None, 0, None, None, 0, 1, None,
          lambda: dqkv16 @ wqkv.T),
     ]
     s = torch.cuda.current_stream().cuda_stream
@@ -72,6 +77,8 @@ def main():
     print(f"{'gemm':20s} {'m':>6s} {'n':>5s} {'k':>5s}   p2r us  TFLOP/s | cuBLAS us TFLOP/s")
     for (name, m, n, k, A, lda, amn, B, ldb, bmn, epi, c, ldc, c2, ldc2, bias, aux, ldaux, split, bgrad, cb) in cases:
         if a.only is not None and name != a.only:
+            continue
+        if a.only is None and "shape" in name and not a.variants:
             continue
         args = _lib.GemmArgs(m=m, n=n, k=k, a=A.data_ptr(), lda=lda, a_mn_major=amn, b=B.data_ptr(), ldb=ldb,
                              b_mn_major=bmn, epi=epi, c=c.data_ptr(), ldc=ldc,

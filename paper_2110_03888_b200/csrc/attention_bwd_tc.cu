@@ -94,6 +94,29 @@ P2R_DEVICE void ld32x2(uint32_t ta, uint32_t tb, float* a, float* b) {
   }
 }
 
+// 16 registers -> 32 lanes x 16 consecutive 32-bit TMEM columns
+P2R_DEVICE void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+// D (+)= A.B with A (M rows = TMEM lanes, K packed bf16 pairs along columns) read from TMEM
+P2R_DEVICE void umma_bf16_ta_warp(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                  uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 // ============================================================================ dQ
 template <int HD>
 struct DqCfg {
@@ -545,8 +568,11 @@ __global__ void __launch_bounds__(384, 1)
 // as two 32-column halves) each own one tile, so while one group turns S/dP
 // into P/dS the tensor core runs the other tile's MMAs and the next block's
 // S/dP — the per-block MMA <-> softmax hand-off no longer serialises the CTA.
-// S/dP are single-buffered per tile in TMEM: the group releases them (s_free)
-// as soon as both halves are in registers. Still deterministic (fixed order).
+// S/dP are single-buffered per tile in TMEM, and the group writes its bf16 dS
+// (dQ kernel) / P^T and dS^T (dK/dV kernel) back over the first 32 columns of
+// those blocks (tcgen05.st), where the dQ / dV / dK MMAs read them as their A
+// operand straight from TMEM: no smem round trip; the next block's S/dP MMA
+// waits for those MMAs. Still deterministic (fixed order).
 // ============================================================================
 // Exponentials of the recomputed P moved from the SFU (16 ex2 / clk / SM, the
 // softmax groups' bound) to the FMA pipe: this many of every 16 pairs of a 32-key
@@ -556,14 +582,16 @@ __global__ void __launch_bounds__(384, 1)
 #endif
 constexpr int kBwdFmaPairs = P2R_BWD_FMA_PAIRS;
 
+#ifndef P2R_BWD_NS
+#define P2R_BWD_NS 4
+#endif
+// (dS and P^T / dS^T live in TMEM as MMA A operands: no smem tiles for them)
 struct DqPP {
-  static constexpr int HD = 64, BQ = 128, BKV = 64, NS = 4;
+  static constexpr int HD = 64, BQ = 128, BKV = 64, NS = P2R_BWD_NS;
   static constexpr int QT = BQ * HD * 2;    // one Q or dO tile (16 KB)
   static constexpr int KT = BKV * HD * 2;   // one K or V block (8 KB)
-  static constexpr int DST = BQ * BKV * 2;  // one dS tile (16 KB)
   static constexpr int OFF_Q = 0, OFF_DO = 2 * QT, OFF_K = 4 * QT, OFF_V = OFF_K + NS * KT;
-  static constexpr int OFF_DS = OFF_V + NS * KT;   // [tile][buf]
-  static constexpr int OFF_BAR = OFF_DS + 4 * DST;
+  static constexpr int OFF_BAR = OFF_V + NS * KT;
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
   static constexpr int T_TILE = 192;  // TMEM per tile: S +0, dP +64, dQ(item parity 0) +128
   static constexpr int T_DQ1 = 384;   // dQ(item parity 1) of tile X at T_DQ1 + 64 X
@@ -593,8 +621,7 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* kv_full = bar + 2;            // [NS]
   uint64_t* kv_empty = kv_full + C::NS;   // [NS]
   uint64_t* s_full = kv_empty + C::NS;    // [tile]
-  uint64_t* s_free = s_full + 2;          // [tile]
-  uint64_t* ds_full = s_free + 2;         // [tile][buf]
+  uint64_t* ds_full = s_full + 2;         // [tile][buf]
   uint64_t* dq_done = ds_full + 4;        // [tile][buf]
   uint64_t* dq_empty = dq_done + 4;       // [tile][item parity]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_empty + 4);
@@ -632,7 +659,6 @@ __global__ void __launch_bounds__(384, 1)
     }
     for (int X = 0; X < 2; ++X) {
       mbar_init(s_full + X, 1);
-      mbar_init(s_free + X, 4);  // one arrive per warp of the group
       for (int u = 0; u < 2; ++u) {
         mbar_init(ds_full + 2 * X + u, 128);
         mbar_init(dq_done + 2 * X + u, 1);
@@ -691,8 +717,9 @@ __global__ void __launch_bounds__(384, 1)
           TRP(16 + 4 * G);
           for (int X = 0; X < 2; ++X) {
             if (j >= I.nkvt[X]) continue;
-            if (cX[X] >= 1) {
-              mbar_wait(s_free + X, (cX[X] - 1) & 1);  // the group holds S/dP of its previous block in registers
+            if (cX[X] >= 1) {  // dS(j-1) sits in this tile's S columns until the dQ MMA read it
+              const int c = cX[X] - 1;
+              mbar_wait(dq_done + 2 * X + (c & 1), (c >> 1) & 1);
               tc_fence_after();
             }
             const uint64_t a = dadd(dQ0, X * C::QT), ao = dadd(dO0, X * C::QT);
@@ -715,7 +742,6 @@ __global__ void __launch_bounds__(384, 1)
   } else if (warp == 3) {
     {  // dQ issuer (whole warp, one elected lane issues)
       constexpr uint32_t id_q = make_idesc_bf16(C::BQ, C::HD, false, true);
-      const uint64_t dS0 = make_sw128_desc(sb + C::OFF_DS, 16, 1024);
       const uint64_t dKm0 = make_sw128_desc(sb + C::OFF_K, C::BKV * 128, 1024);
       int G = 0, it = 0, cX[2] = {0, 0};
       for (int k = 0, w = blockIdx.x; w < n_items; w = snake_item(++k, blockIdx.x, gridDim.x), ++it) {
@@ -731,11 +757,12 @@ __global__ void __launch_bounds__(384, 1)
                 mbar_wait(dq_empty + 2 * X + par, ((it >> 1) & 1) ^ 1);
                 tc_fence_after();
               }
-              const uint64_t a = dadd(dS0, (2 * X + u) * C::DST), bk = dadd(dKm0, (G % C::NS) * C::KT);
+              const uint64_t bk = dadd(dKm0, (G % C::NS) * C::KT);
               const uint32_t tQ = tmem + (par ? C::T_DQ1 + 64 * X : X * C::T_TILE + 128);
+              const uint32_t tA = tmem + X * C::T_TILE;  // dS: bf16 pairs over the S block's first 32 columns
 #pragma unroll
               for (int k = 0; k < C::BKV / 16; ++k)
-                umma_bf16_warp(tQ, dadd(a, k * 32), dadd(bk, k * 2048), id_q, (j > 0 || k > 0) ? 1u : 0u);
+                umma_bf16_ta_warp(tQ, tA + k * 8, dadd(bk, k * 2048), id_q, (j > 0 || k > 0) ? 1u : 0u);
               umma_commit_warp(dq_done + 2 * X + u);
               ++cX[X];
             }
@@ -819,7 +846,6 @@ __global__ void __launch_bounds__(384, 1)
       const int nkvX = I.nkvt[X];
       for (int j = 0; j < nkvX; ++j, ++cX) {
         const int u = cX & 1;
-        const uint32_t dsb = sb + C::OFF_DS + (2 * X + u) * C::DST;
         mbar_wait(s_full + X, cX & 1);
         tc_fence_after();
         if (trw) TRP(trb + 4 * cX);
@@ -827,12 +853,7 @@ __global__ void __launch_bounds__(384, 1)
         for (int hh = 0; hh < 2; ++hh) {
           float s[32], dp[32];
           ld32x2(tS + hh * 32, tP + hh * 32, s, dp);
-          if (hh == 1) {  // S/dP(j) fully in registers: the MMA may overwrite them
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(s_free + X);
-            if (trw) TRP(trb + 4 * cX + 1);
-          }
+          if (hh == 1 && trw) TRP(trb + 4 * cX + 1);
           const int k0 = j * C::BKV + hh * 32;
           int lim = 32;
           if (q >= p.S) lim = 0;
@@ -865,11 +886,18 @@ __global__ void __launch_bounds__(384, 1)
               s[i + 1] = v.y;
             }
           }
-          if (hh == 0 && cX >= 2) mbar_wait(dq_done + 2 * X + u, ((cX - 2) >> 1) & 1);  // dS buffer reuse
-          store_row32(dsb, r, hh * 4, s);
+          // dS of these 32 keys -> bf16 pairs over columns [16 hh, 16 hh + 16) of this tile's
+          // S block (the dQ MMA's A operand; the other half's columns are not touched)
+          uint32_t wv[16];
+#pragma unroll
+          for (int i2 = 0; i2 < 16; ++i2) {
+            __nv_bfloat162 h2 = __floats2bfloat162_rn(s[2 * i2], s[2 * i2 + 1]);
+            wv[i2] = *reinterpret_cast<uint32_t*>(&h2);
+          }
+          tmem_st_32x32b_x16(tS + hh * 16, wv);
         }
         if (trw) TRP(trb + 4 * cX + 2);
-        fence_async_smem();
+        tmem_st_wait();
         tc_fence_before();
         mbar_arrive(ds_full + 2 * X + u);
         if (trw) TRP(trb + 4 * cX + 3);
@@ -898,13 +926,11 @@ __global__ void __launch_bounds__(384, 1)
 }
 
 struct KvPP {
-  static constexpr int HD = 64, BK = 128, BQ = 64, NS = 4;
+  static constexpr int HD = 64, BK = 128, BQ = 64, NS = P2R_BWD_NS;
   static constexpr int KT = BK * HD * 2;   // one K or V tile (16 KB)
   static constexpr int QT = BQ * HD * 2;   // one Q or dO block (8 KB)
-  static constexpr int PT = BK * BQ * 2;   // one P^T or dS^T tile (16 KB)
   static constexpr int OFF_K = 0, OFF_V = 2 * KT, OFF_Q = 4 * KT, OFF_DO = OFF_Q + NS * QT;
-  static constexpr int OFF_P = OFF_DO + NS * QT, OFF_DS = OFF_P + 2 * PT;
-  static constexpr int OFF_LD = OFF_DS + 2 * PT;  // [tile][slot][lse2 | D][64] floats
+  static constexpr int OFF_LD = OFF_DO + NS * QT;  // [tile][slot][lse2 | D][64] floats
   static constexpr int OFF_BAR = OFF_LD + 2 * 2 * 2 * 64 * 4;
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
   static constexpr int T_TILE = 256;  // TMEM per tile: S^T +0, dP^T +64, dV +128, dK +192
@@ -935,8 +961,7 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* q_full = bar + 2;           // [NS]
   uint64_t* q_empty = q_full + C::NS;   // [NS]
   uint64_t* s_full = q_empty + C::NS;   // [tile]
-  uint64_t* s_free = s_full + 2;        // [tile]
-  uint64_t* p_full = s_free + 2;        // [tile]
+  uint64_t* p_full = s_full + 2;        // [tile]
   uint64_t* pv_done = p_full + 2;       // [tile]
   uint64_t* acc_empty = pv_done + 2;    // [tile]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
@@ -973,7 +998,6 @@ __global__ void __launch_bounds__(384, 1)
     }
     for (int X = 0; X < 2; ++X) {
       mbar_init(s_full + X, 1);
-      mbar_init(s_free + X, 4);
       mbar_init(p_full + X, 128);
       mbar_init(pv_done + X, 1);
       mbar_init(acc_empty + X, 128);
@@ -1027,8 +1051,8 @@ __global__ void __launch_bounds__(384, 1)
           if (lane == 0 && G < 24) TRK(16 + 4 * G);
           for (int X = 0; X < 2; ++X) {
             if (i < I.i0t[X]) continue;
-            if (cX[X] >= 1) {
-              mbar_wait(s_free + X, (cX[X] - 1) & 1);
+            if (cX[X] >= 1) {  // P^T / dS^T(i-1) sit in this tile's S^T / dP^T columns until dV/dK(i-1) read them
+              mbar_wait(pv_done + X, (cX[X] - 1) & 1);
               tc_fence_after();
             }
             if (lane == 0 && G < 24) TRK(16 + 4 * G + 1 + X);
@@ -1053,7 +1077,6 @@ __global__ void __launch_bounds__(384, 1)
       constexpr uint32_t id_o = make_idesc_bf16(C::BK, C::HD, false, true);
       const uint64_t dQm0 = make_sw128_desc(sb + C::OFF_Q, C::BQ * 128, 1024);
       const uint64_t dOm0 = make_sw128_desc(sb + C::OFF_DO, C::BQ * 128, 1024);
-      const uint64_t dP0 = make_sw128_desc(sb + C::OFF_P, 16, 1024), dS0 = make_sw128_desc(sb + C::OFF_DS, 16, 1024);
       int G = 0, it = 0, cX[2] = {0, 0};
       for (int k = 0, w = blockIdx.x; w < n_items; w = snake_item(++k, blockIdx.x, gridDim.x), ++it) {
         const Item I = item(w);
@@ -1068,14 +1091,15 @@ __global__ void __launch_bounds__(384, 1)
               mbar_wait(acc_empty + X, (it & 1) ^ 1);
               tc_fence_after();
             }
-            const uint64_t ap = dadd(dP0, X * C::PT), as = dadd(dS0, X * C::PT);
             const uint64_t bo = dadd(dOm0, st * C::QT), bq = dadd(dQm0, st * C::QT);
             const uint32_t tS = tmem + X * C::T_TILE;
 #pragma unroll
             for (int k = 0; k < C::BQ / 16; ++k) {
-              // dV += P^T dO ; dK += dS^T Q   (dO / Q blocks re-read MN-major: rows = queries)
-              umma_bf16_warp(tS + 128, dadd(ap, k * 32), dadd(bo, k * 2048), id_o, (n > 0 || k > 0) ? 1u : 0u);
-              umma_bf16_warp(tS + 192, dadd(as, k * 32), dadd(bq, k * 2048), id_o, (n > 0 || k > 0) ? 1u : 0u);
+              // dV += P^T dO ; dK += dS^T Q with A = P^T / dS^T from TMEM (bf16 pairs packed over
+              // the first 32 columns of the S^T / dP^T blocks: 16 queries = 8 columns per MMA);
+              // dO / Q blocks re-read MN-major from smem (rows = queries)
+              umma_bf16_ta_warp(tS + 128, tS + k * 8, dadd(bo, k * 2048), id_o, (n > 0 || k > 0) ? 1u : 0u);
+              umma_bf16_ta_warp(tS + 192, tS + 64 + k * 8, dadd(bq, k * 2048), id_o, (n > 0 || k > 0) ? 1u : 0u);
             }
             umma_commit_warp(pv_done + X);
             if (lane == 0 && cX[X] < 48) TRK(120 + 48 * X + cX[X]);
@@ -1166,11 +1190,6 @@ __global__ void __launch_bounds__(384, 1)
         for (int hh = 0; hh < 2; ++hh) {
           float s[32], dp[32];
           ld32x2(tS + hh * 32, tP + hh * 32, s, dp);
-          if (hh == 1) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(s_free + X);
-          }
           const uint32_t lda = ldb + (slot * 128 + hh * 32) * 4;
           // visible: query q >= key (causal), q < S, key < S
           const int qb1 = q1 + hh * 32;
@@ -1216,11 +1235,20 @@ __global__ void __launch_bounds__(384, 1)
             dp[4 * c4 + 2] = v1.x;
             dp[4 * c4 + 3] = v1.y;
           }
-          if (hh == 0 && cX >= 1) mbar_wait(pv_done + X, (cX - 1) & 1);  // P^T / dS^T buffer reuse
-          store_row32(sb + C::OFF_P + X * C::PT, kr, hh * 4, s);
-          store_row32(sb + C::OFF_DS + X * C::PT, kr, hh * 4, dp);
+          // P^T / dS^T of these 32 queries -> bf16 pairs over columns [16 hh, 16 hh + 16) of the
+          // S^T / dP^T blocks (already in registers; the other half's columns are not touched)
+          uint32_t wp[16], wd[16];
+#pragma unroll
+          for (int i2 = 0; i2 < 16; ++i2) {
+            __nv_bfloat162 a2 = __floats2bfloat162_rn(s[2 * i2], s[2 * i2 + 1]);
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(dp[2 * i2], dp[2 * i2 + 1]);
+            wp[i2] = *reinterpret_cast<uint32_t*>(&a2);
+            wd[i2] = *reinterpret_cast<uint32_t*>(&b2);
+          }
+          tmem_st_32x32b_x16(tS + hh * 16, wp);
+          tmem_st_32x32b_x16(tP + hh * 16, wd);
         }
-        fence_async_smem();
+        tmem_st_wait();
         tc_fence_before();
         mbar_arrive(p_full + X);
         if (trw) TRK(240 + 128 * X + 2 * cX + 1);

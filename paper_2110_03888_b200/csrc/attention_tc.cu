@@ -30,6 +30,26 @@
 namespace p2r {
 namespace attn_tc {
 
+#ifndef P2R_FWD_NKV64
+#define P2R_FWD_NKV64 3
+#endif
+#ifndef P2R_FWD_NKV128
+#define P2R_FWD_NKV128 2
+#endif
+// O (+)= P.V with P (bf16 pairs packed along TMEM columns, rows = lanes) read from TMEM
+P2R_DEVICE void umma_bf16_ta_warp(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                  uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 constexpr int BQ = 128, BKV = 128;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThresh = 8.0f;  // log2 units: P stays <= 256 in bf16
@@ -43,17 +63,16 @@ template <int HD>
 struct Cfg {
   static constexpr int KATOMS = HD / 64;                 // 128-B K atoms per row
   static constexpr int TILE = BQ * HD * 2;               // Q / K / V tile bytes
-  static constexpr int PTILE = BQ * BKV * 2;             // P tile bytes
-  static constexpr int NPB = HD == 64 ? 2 : 1;           // P buffers
+  // P never touches smem: the softmax writes it (bf16 pairs) over its S block in TMEM,
+  // where the PV MMA reads it as the A operand
   // K/V ring depth: with 2 stages the load of block j+2 waits for PV(j) and its
   // latency lands on every block (trace: ~1.9k vs ~1.4k softmax cycles/block)
-  static constexpr int NKV = HD == 64 ? 3 : 2;
+  static constexpr int NKV = HD == 64 ? P2R_FWD_NKV64 : P2R_FWD_NKV128;
   static constexpr int NQ = HD == 64 ? 2 : 1;  // Q buffers (the next item's Q loads early)
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + NQ * TILE;
   static constexpr int OFF_V = OFF_K + NKV * TILE;
-  static constexpr int OFF_P = OFF_V + NKV * TILE;
-  static constexpr int OFF_BAR = OFF_P + NPB * PTILE;
+  static constexpr int OFF_BAR = OFF_V + NKV * TILE;
   static constexpr int XCH = (2 * 2 + 2) * 128 * 4;   // row-max exchange [2][2][128] + sums [2][128]
   static constexpr int SMEM = OFF_BAR + 256 + XCH + 1024;
   static constexpr int TMEM_S0 = 0, TMEM_S1 = 128, TMEM_O = 256;  // O buffer ob at TMEM_O + ob * HD
@@ -202,7 +221,6 @@ __global__ void __launch_bounds__(384, 1)
       // precomputed base descriptors, advanced by byte offsets (desc_add)
       const uint64_t dQ0 = make_sw128_desc(sbase + C::OFF_Q, 16, 1024);
       const uint64_t dK0 = make_sw128_desc(sbase + C::OFF_K, 16, 1024);
-      const uint64_t dP0 = make_sw128_desc(sbase + C::OFF_P, 16, 1024);
       const uint64_t dV0 = make_sw128_desc(sbase + C::OFF_V, BKV * 128, 1024);
       // PV of global block gg (block jj of item iit): O[iit & 1] (+)= P_gg . V_gg
       auto issue_pv = [&](int gg, int jj, int iit) {
@@ -215,12 +233,14 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_after();
         if (lane == 0 && gg < 22) TRF(8 + 4 * gg + 2);
         const uint32_t st = gg % C::NKV;
-        const uint64_t ap = desc_add(dP0, (gg % C::NPB) * C::PTILE), bv = desc_add(dV0, st * C::TILE);
+        const uint64_t bv = desc_add(dV0, st * C::TILE);
+        const uint32_t tp = tmem + ((gg & 1) ? C::TMEM_S1 : C::TMEM_S0);  // P_gg over S_gg's first 64 columns
 #pragma unroll
         for (int k = 0; k < BKV / 16; ++k)
-          // A = P (K-major, atom = 64 keys), B = V (MN-major: rows = keys, 64 hd per 128-B row)
-          umma_bf16_warp(tmem + C::TMEM_O + ob * HD, desc_add(ap, (k >> 2) * (BQ * 128) + (k & 3) * 32),
-                         desc_add(bv, k * 2048), idesc_o, (jj > 0 || k > 0) ? 1u : 0u);
+          // A = P from TMEM (16 keys = 8 columns per MMA), B = V (MN-major: rows = keys, 64 hd per 128-B row).
+          // S_{gg+2} reuses this TMEM block: it is issued after this PV, and the tensor pipe runs in order
+          umma_bf16_ta_warp(tmem + C::TMEM_O + ob * HD, tp + k * 8, desc_add(bv, k * 2048), idesc_o,
+                            (jj > 0 || k > 0) ? 1u : 0u);
         umma_commit_warp(kv_empty + st);
         umma_commit_warp(o_done + (gg & 1));
         if (lane == 0 && gg < 22) TRF(8 + 4 * gg + 3);
@@ -388,12 +408,11 @@ __global__ void __launch_bounds__(384, 1)
           }
           if (need) m_used = mx;
         }
-        // P buffer reuse: the PV that last read this buffer must be done
-        if (g >= C::NPB) {
-          const int gp = g - C::NPB;
-          mbar_wait(o_done + (gp & 1), (gp >> 1) & 1);
-        }
-        const uint32_t sp = smem_u32(smem) + C::OFF_P + (g % C::NPB) * C::PTILE + hf * (BQ * 128);
+        // P_g goes over S_g's TMEM block (its 64 keys -> 32 packed columns at 32 hf); both halves
+        // of the row finished reading S_g before the max exchange above, and S_g's completion
+        // implies PV_{g-2} (the previous reader of this block) completed: the pipe runs in order
+        const uint32_t tPw = tmem + lane_addr + ((g & 1) ? C::TMEM_S1 : C::TMEM_S0) + 32 * hf;
+        uint32_t pw[32];
         float2 ls = make_float2(0.0f, 0.0f);
         const float2 sl2 = make_float2(p.sl2, p.sl2), nm = make_float2(-m_used, -m_used);
 #pragma unroll
@@ -409,11 +428,13 @@ __global__ void __launch_bounds__(384, 1)
             __nv_bfloat162 hh = __floats2bfloat162_rn(e.x, e.y);
             wv[i] = *reinterpret_cast<uint32_t*>(&hh);
           }
-          sts128(sp + sw128_off(r, c16), make_uint4(wv[0], wv[1], wv[2], wv[3]));  // this half = one 64-key atom
+#pragma unroll
+          for (int i = 0; i < 4; ++i) pw[4 * c16 + i] = wv[i];
         }
+        tmem_st_32x32b_x32(tPw, pw);
         l += ls.x + ls.y;
         if (trw && g < 22) TRF(100 + 4 * g + 2);
-        fence_async_smem();
+        tmem_st_wait();
         tc_fence_before();
         mbar_arrive(p_full + (g & 1));
         if (trw && g < 22) TRF(100 + 4 * g + 3);

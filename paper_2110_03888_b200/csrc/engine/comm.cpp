@@ -160,6 +160,15 @@ void Engine::comm_init_loopback(LoopbackGroup* group) {
   if (group == nullptr || group->world != ep_world_)
     throw std::invalid_argument("loopback group: world size does not match the model's");
   loop_ = group;
+  // the all-reduce staging area is sized here, before any shard's step runs: growing it
+  // later (device sync + reallocation) could race another shard's step-graph capture
+  const std::size_t n = static_cast<std::size_t>(std::max<long long>(emb_.numel, layer_.numel));
+  std::lock_guard<std::mutex> lk(group->mu);
+  if (group->stage_floats < n) {
+    cuda_check(cudaDeviceSynchronize(), "sync");
+    group->stage = DevBuf(static_cast<std::size_t>(group->world) * n * 4);
+    group->stage_floats = n;
+  }
 }
 
 void Engine::comm_destroy() {

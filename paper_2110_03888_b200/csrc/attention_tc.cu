@@ -17,8 +17,8 @@
 //   warps 4-11 softmax: two warps per TMEM lane quadrant (query row), each
 //              owning half the keys of a block: causal mask, online softmax
 //              with CONDITIONAL rescaling of O (only when the running max grows
-//              by > 2^8), bf16 P into a SWIZZLE_128B K-major smem tile; per
-//              item, normalise O and store O / LSE.
+//              by > 2^8), bf16 P written back over the S block in TMEM (the PV
+//              MMA's A operand); per item, normalise O and store O / LSE.
 #include <cudaTypedefs.h>
 
 #include <mutex>
@@ -86,26 +86,10 @@ struct FwdParams {
   float sl2;  // softmax scale * log2(e)
 };
 
-// row-major 128-B K atom tile: element (row, k) of a [rows x 64] bf16 atom
-P2R_DEVICE uint32_t sw128_off(int row, int chunk16) {
-  return static_cast<uint32_t>(row * 128 + ((chunk16 ^ (row & 7)) << 4));
-}
-
-// 2^x on the FMA pipe (FA4-style MUFU offload): x = n + f with n = round(x) via
-// the 1.5*2^23 magic add, 2^f by a degree-3 fit on [-1/2, 1/2] (max rel. error
-// 1.4e-4, far below P's bf16 rounding), exponent added with integer ops.
-P2R_DEVICE float exp2_fma(float x) {
-  x = fmaxf(x, -125.0f);  // 2^n * p stays a normal float (masked scores -> ~2e-38)
-  const float magic = 12582912.0f;
-  const float t = x + magic;
-  const float f = x - (t - magic);
-  const float p = fmaf(fmaf(fmaf(5.502931029e-02f, f, 2.422568053e-01f), f, 6.932530403e-01f), f, 9.999513626e-01f);
-  return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - __float_as_int(magic)) << 23));
-}
-// Pair form on the FP32x2 pipe (FFMA2/FADD2): the softmax is issue-bound.
-// t = z + M rounds z to an integer n (exact: M = 1.5*2^23), -n = M - t and
-// f = z - n are exact, so this matches exp2_fma bit-for-bit.
-// (exp2_fma2: common.cuh)
+// 2^x on the FMA pipe (FA4-style MUFU offload, exp2_fma2 in common.cuh): x = n + f with
+// n = round(x) via the 1.5*2^23 magic add, 2^f by a degree-3 fit on [-1/2, 1/2] (max rel.
+// error 1.4e-4, far below P's bf16 rounding), the exponent added with integer ops; pair
+// form on the FP32x2 pipe (FFMA2/FADD2): the softmax is issue-bound.
 P2R_DEVICE float max3f(float a, float b, float c) {
   float r;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
@@ -118,7 +102,6 @@ P2R_DEVICE float ex2_approx(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-P2R_DEVICE void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 template <int HD>
 __global__ void __launch_bounds__(384, 1)

@@ -151,7 +151,8 @@ def test_layernorm_golden(cuda):
 
 
 @pytest.mark.parametrize("B,H,S,hd,causal", [(2, 4, 128, 64, 1), (1, 2, 200, 64, 1), (2, 2, 96, 64, 0),
-                                            (1, 2, 160, 128, 1), (8, 16, 1024, 64, 1)])
+                                            (1, 2, 160, 128, 1), (8, 16, 1024, 64, 1), (2, 4, 1000, 64, 1),
+                                            (1, 4, 512, 128, 0), (2, 8, 1024, 128, 1)])
 def test_attention(cuda, B, H, S, hd, causal):
     import torch
     rng = np.random.default_rng(1)

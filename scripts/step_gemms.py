@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--iters", type=int, default=30)
     ap.add_argument("--only", default=None, help="run just the GEMM of this name (profiling)")
     ap.add_argument("--variants", action="store_true", help="also time epilogue variants of the FFN1 shape")
+    ap.add_argument("--split", type=int, default=None, help="force split_k on the dW GEMMs (measurement)")
     a = ap.parse_args()
     L = _lib.lib()
     x32 = torch.randn(T, d, device="cuda")
@@ -84,7 +85,8 @@ def main():
                              b_mn_major=bmn, epi=epi, c=c.data_ptr(), ldc=ldc,
                              c2=c2.data_ptr() if c2 is not None else None, ldc2=ldc2,
                              bias=bias.data_ptr() if bias is not None else None,
-                             aux=aux.data_ptr() if aux is not None else None, ldaux=ldaux, split_k=split,
+                             aux=aux.data_ptr() if aux is not None else None, ldaux=ldaux,
+                             split_k=a.split if (a.split is not None and name.startswith("dW")) else split,
                              bias_grad=bgrad.data_ptr() if bgrad is not None else None)
         ws = torch.empty(max(1, L.p2r_gemm_workspace_bytes(ctypes.byref(args)) // 4), device="cuda")
         _lib.check(L.p2r_set_workspace(ws.data_ptr(), ws.numel() * 4))

@@ -59,6 +59,10 @@ def main():
          lambda: g16.T @ dy16),
         ("dH (gelu', db1)", T, f, d, dy16, d, 0, w2, d, 0, E.EPI_DGELU, out16, f, None, 0, None, hpre16, f, 1, db1,
          lambda: dy16 @ w2.T),
+        ("dH shape, bf16", T, f, d, dy16, d, 0, w2, d, 0, E.EPI_BF16, out16, f, None, 0, None, None, 0, 1, None,
+         lambda: dy16 @ w2.T),
+        ("dH shape, no colsum", T, f, d, dy16, d, 0, w2, d, 0, E.EPI_DGELU, out16, f, None, 0, None, hpre16, f, 1,
+         None, lambda: dy16 @ w2.T),
         ("dW1", d, f, T, b16, d, 1, dh16, f, 1, E.EPI_ACC_F32, gw, f, None, 0, None, None, 0, 0, None,
          lambda: b16.T @ dh16),
         ("dX1", T, d, f, dh16, f, 0, w1, f, 0, E.EPI_BF16, out16, d, None, 0, None, None, 0, 1, None,

@@ -190,3 +190,48 @@ def test_loopback_ep_offload_accumulation_matches_resident(cuda):
     for r in range(W):
         for n, v in runs[0][1][r].items():
             assert np.array_equal(v, runs[1][1][r][n]), (r, n)
+
+
+@pytest.mark.parametrize("cfgd", [MOE_W, dict(MOE_W, n_experts=0)], ids=["ep_moe", "dense_dp"])
+def test_loopback_pipelined_host_steps_bit_identical(cuda, cfgd):
+    """Model.train_step(wait=False) on expert-parallel / data-parallel loopback shards (the
+    exchange and the all-reduce are collective, each shard on its own host thread): the
+    next step and the all-reduce are enqueued before the previous loss is read; losses and
+    gradients are bit-identical to the synchronous loop."""
+    import paper_2110_03888_b200 as p2r
+    cfg = p2r.Config(**cfgd)
+    W, B, S, steps = 2, 2, 128, 3
+    batches = [[lm_batch(B, S, seed=60 + 10 * r + i) for i in range(steps)] for r in range(W)]
+    denom = float(sum(b[2].sum() for b in batches[0]))
+    out = {}
+    for piped in (False, True):
+        group = p2r.LoopbackGroup(W)
+        shards = [p2r.Model(cfg, 1234, ep=(W, r)) for r in range(W)]
+        for m in shards:
+            m.comm_init_loopback(group)
+
+        def run(r):
+            losses, prev = [], None
+            for i in range(steps):
+                tok, tgt, mask = batches[r][i]
+                if piped:
+                    cur = shards[r].train_step(tok, tgt, mask, B, denom, wait=False)
+                    shards[r].allreduce_grads()
+                    if prev is not None:
+                        losses.append(prev.value())
+                    prev = cur
+                else:
+                    losses.append(shards[r].train_step(tok, tgt, mask, B, denom))
+                    shards[r].allreduce_grads()
+            if piped:
+                losses.append(prev.value())
+            return losses
+
+        losses = _run_ranks([lambda r=r: run(r) for r in range(W)])
+        out[piped] = (losses, [m.grads() for m in shards])
+        for m in shards:
+            m.close()
+    assert out[True][0] == out[False][0]
+    for r in range(W):
+        for n, v in out[False][1][r].items():
+            assert np.array_equal(v, out[True][1][r][n]), (r, n)

@@ -32,8 +32,11 @@ def design_floor(cfgd, params, tok, tgt, mask, batch, denom, forced=None):
     return ge
 
 
-def check_grads(gm, gr, ge, names, tag, tol=1e-2):
-    """gm: GPU, gr: fp32 reference, ge: bf16-design emulation."""
+def check_grads(gm, gr, ge, names, tag, tol=1e-2, strict=True):
+    """gm: GPU, gr: fp32 reference, ge: bf16-design emulation. strict: every parameter
+    gradient within tol (the north-star contract); strict=False only for
+    configs where the bf16-in design's own floor on the same inputs exceeds tol (deep
+    Real dense stacks): there the bound is 1.25x that floor."""
     rows = []
     for n in names:
         if np.linalg.norm(gr[n]) == 0:
@@ -47,5 +50,5 @@ def check_grads(gm, gr, ge, names, tag, tol=1e-2):
         print(f"[{tag}]   {n:34s} gpu {e:.3e}  bf16-design floor {f:.3e}")
     assert g <= tol
     for e, f, n in rows:
-        assert e <= max(tol, 1.25 * f), (n, e, f)
+        assert e <= (tol if strict else max(tol, 1.25 * f)), (n, e, f)
     return rows

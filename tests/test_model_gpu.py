@@ -89,7 +89,10 @@ def test_step_parity_dense(cuda, cfgd, B):
     lg = m.train_step(tok, tgt, mask, B, denom)
     lr_ = r.train_step(tok, tgt, mask, B, denom)
     assert abs(lg - lr_) <= 1e-3 * abs(lr_), (lg, lr_)
-    check_grads(m.grads(), r.grads(), design_floor(cfgd, p0, tok, tgt, mask, B, denom), r.names, "dense")
+    # the three-layer Real stack's deepest Q/K projections sit at the bf16-in design floor
+    # (1.4e-2 in oracle/bf16_emulation.py on these inputs, profiles/r02_precision_floor.txt)
+    check_grads(m.grads(), r.grads(), design_floor(cfgd, p0, tok, tgt, mask, B, denom), r.names, "dense",
+                strict=cfgd["n_layers_params"] == 1)
 
 
 RAGGED_DENSE = dict(d_model=384, d_ff=1536, n_layers_graph=3, n_layers_params=1, n_heads=6, vocab_size=260,
@@ -131,9 +134,10 @@ def test_step_parity_ragged(cuda, cfgd):
 
 
 @need_ref
-# per-tensor gradient bound (tests/_parity.py): 1e-2, or 1.25x the bf16-in design's floor
-# on the same inputs where that floor is itself ~1e-2 (at d = 2048 (C4S) single expert
-# tensors of the deeper layer and the Q/K projections sit at 1.0-1.25e-2 in the emulation)
+# per-tensor gradient bound (tests/_parity.py): strict 1e-2 relative L2 on C1 (the contract's
+# config) and the top-2 case; on the deeper Real stack and the d = 2048 C4-width
+# slice the bf16-in design's own floor on the same inputs reaches 1.1-1.3e-2 for the Q/K
+# projections (oracle/bf16_emulation.py), and those are bounded by 1.25x that floor
 @pytest.mark.parametrize("cfgd,B", [(C1, 8), (MOE_K2, 8), (REAL, 8), (C4S, 4)],
                          ids=["c1_moe", "moe_k2", "real_moe", "c4_wide_moe"])
 def test_step_parity_moe(cuda, cfgd, B):
@@ -173,7 +177,7 @@ def test_step_parity_moe(cuda, cfgd, B):
     # flips need a near-tie in fp32 under bf16 upstream activations (E=64: test_parity_bench_gpu)
     assert flips <= 0.015 * T * cfgd["n_prototypes"] * cfgd["n_layers_graph"]
     ge = design_floor(cfgd, p0, tok, tgt, mask, B, denom, om.forced_selected)
-    check_grads(m.grads(), go, ge, r.names, "moe")
+    check_grads(m.grads(), go, ge, r.names, "moe", strict=cfgd in (C1, MOE_K2))
 
 
 @need_ref
@@ -284,7 +288,7 @@ def test_delinked_real_step_vs_reference(cuda):
     p0 = rd.params()
     cfg_real = dict(DENSE, n_layers_params=DENSE["n_layers_graph"])
     check_grads(md.grads(), rd.grads(), design_floor(cfg_real, p0, tok, tgt, mask, 8, float(mask.sum())),
-                rd.names, "delinked")
+                rd.names, "delinked", strict=False)  # three Real layers: Q/K at the design floor
 
 
 def test_error_behaviour(cuda):

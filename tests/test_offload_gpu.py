@@ -216,3 +216,37 @@ def test_offload_with_expert_parallel_bit_identical(cuda, monkeypatch):
     pa, pb = a.params(), b.params()
     for n in pa:
         assert np.array_equal(pa[n], pb[n]), n
+
+
+def test_offload_pipelined_host_steps_bit_identical(cuda):
+    """Model.train_step(wait=False) on an offloaded model (the SLOW granules' fused AdamW
+    runs inside the backward, the write-back on the side streams): the next step is
+    enqueued before the previous loss is read; losses, parameters and moments equal the
+    resident model's synchronous loop bit for bit."""
+    import paper_2110_03888_b200 as p2r
+    cfg = p2r.Config(**REAL_MOE)
+    a = p2r.Model(cfg, 1234)
+    b = p2r.Model(cfg, 1234, offload=[1, 0, 1, 1], ring_slots=2)
+    a.attach_adamw()
+    b.attach_adamw()
+    lr = 1e-3
+    b.set_offload_lr(lr)
+    batches = [lm_batch(4, 128, seed=30 + s) for s in range(4)]
+    sync = []
+    for tok, tgt, mask in batches:
+        sync.append(a.train_step(tok, tgt, mask, 4, float(mask.sum())))
+        a.adamw_step(lr)
+    piped, prev = [], None
+    for tok, tgt, mask in batches:
+        cur = b.train_step(tok, tgt, mask, 4, float(mask.sum()), wait=False)
+        b.adamw_step(lr)
+        if prev is not None:
+            piped.append(prev.value())
+        prev = cur
+    piped.append(prev.value())
+    assert piped == sync
+    pa, pb = a.params(), b.params()
+    ma, mb = a.moments(), b.moments()
+    for n in pa:
+        assert np.array_equal(pa[n], pb[n]), n
+        assert np.array_equal(ma[n][0], mb[n][0]) and np.array_equal(ma[n][1], mb[n][1]), n

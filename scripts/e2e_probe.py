@@ -48,3 +48,26 @@ with torch.cuda.stream(ext):
     e1.record()
 torch.cuda.synchronize()
 print(f"device step {e0.elapsed_time(e1)/10:.3f} ms")
+
+# pipelined host loop (bench's e2e): per-step device time vs the gaps between steps,
+# from events recorded on the model stream between the host calls
+evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
+prev = None
+t0 = time.perf_counter()
+for i in range(10):
+    with torch.cuda.stream(ext):
+        evs[i][0].record()
+    cur = m.train_step(tok, tgt, mask, B, denom, wait=False)
+    m.adamw_step(1e-4)
+    with torch.cuda.stream(ext):
+        evs[i][1].record()
+    if prev is not None:
+        prev.value()
+    prev = cur
+prev.value()
+tt = (time.perf_counter() - t0) / 10
+torch.cuda.synchronize()
+busy = [a.elapsed_time(b) for a, b in evs]
+gaps = [evs[i][1].elapsed_time(evs[i + 1][0]) for i in range(9)]
+print(f"pipelined e2e {tt*1e3:.3f} ms/step wall; device per step {np.mean(busy):.3f} ms "
+      f"(min {min(busy):.3f}), gap between steps {np.mean(gaps)*1e3:.1f} us (max {max(gaps)*1e3:.1f})")
